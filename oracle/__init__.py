@@ -1,0 +1,245 @@
+"""ctypes wrapper of the CPU oracle (oracle/oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs.  The product package
+(paper_1607_03936_b200) never imports this module.
+
+The oracle is built from source on first use (gcc, -O2 -fno-fast-math
+-ffp-contract=off -fopenmp) into oracle/liboracle.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+_D = C.POINTER(C.c_double)
+_I64 = C.POINTER(C.c_int64)
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so (in-tree)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-shared", "-fPIC",
+               "-o", _LIB + ".tmp", _SRC, "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = C.CDLL(_LIB)
+            L.or_create.restype = C.c_void_p
+            L.or_create.argtypes = [C.c_int, C.c_int]
+            L.or_destroy.argtypes = [C.c_void_p]
+            L.or_sizes.argtypes = [C.c_void_p, _I64]
+            L.or_tables.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, _D, C.POINTER(C.c_int)]
+            L.or_element_B.argtypes = [C.c_void_p, _D]
+            L.or_element_A_matrix.argtypes = [C.c_void_p, _D, _D]
+            L.or_dofmap.argtypes = [C.c_void_p, _I64]
+            L.or_sizes_only.argtypes = [C.c_int, C.c_int, _I64]
+            L.or_boundary_elements.argtypes = [C.c_void_p, C.POINTER(C.c_uint8)]
+            L.or_boundary_mask.argtypes = [C.c_void_p, C.POINTER(C.c_uint8)]
+            L.or_apply_A.argtypes = [C.c_void_p, _D, _D, _D, C.c_int]
+            L.or_apply_A_sampled.argtypes = [C.c_void_p, _D, _D, _I64, C.c_int64, _D]
+            L.or_apply_B.argtypes = [C.c_void_p, _D, _D, C.c_int]
+            L.or_apply_BT.argtypes = [C.c_void_p, _D, _D, C.c_int]
+            L.or_lumped.argtypes = [C.c_void_p, _D, C.c_double, C.c_double, _D, _D, _D, _D, _I64]
+            L.or_apply_K.argtypes = [C.c_void_p, _D, _D, _D, _D]
+            L.or_jacobi_diag.argtypes = [C.c_void_p, _D, _D]
+            L.or_project.argtypes = [C.c_void_p, _D]
+            L.or_pcg.argtypes = [C.c_void_p, _D, _D, _D, _D, C.c_int]
+            L.or_pcg_step.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, _D]
+            L.or_poisson.argtypes = [C.c_void_p, _D, _D, _D, _D, C.c_int]
+            L.or_wbfbt.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, _D, _D, C.c_int]
+            L.or_poisson_relres.restype = C.c_double
+            L.or_poisson_relres.argtypes = [C.c_void_p, _D, _D, _D]
+            L.or_num_threads.restype = C.c_int
+            _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_D)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def sizes_only(N: int, k: int) -> dict:
+    """Oracle's structured counts without building tables."""
+    s = np.zeros(6, dtype=np.int64)
+    lib().or_sizes_only(N, k, s.ctypes.data_as(_I64))
+    return dict(zip(("n_el", "n_nodes", "n_v", "n_p", "n_q", "n_m"), (int(v) for v in s)))
+
+
+class Oracle:
+    """One structured mesh (N^3 elements, Q_k x P_{k-1}^disc) on the unit cube."""
+
+    def __init__(self, N: int, k: int):
+        self.L = lib()
+        self.h = self.L.or_create(N, k)
+        if not self.h:
+            raise ValueError(f"oracle: bad N={N} k={k}")
+        self.N, self.k = N, k
+        s = np.zeros(6, dtype=np.int64)
+        self.L.or_sizes(self.h, s.ctypes.data_as(_I64))
+        self.n_el, self.n_nodes, self.n_v, self.n_p, self.n_q, self.n_m = (int(v) for v in s)
+        self.mu_q = None
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.L.or_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    # ---- tables / structure
+    def tables(self) -> dict:
+        n1 = self.k + 1
+        xn, xg, wg = np.zeros(n1), np.zeros(n1), np.zeros(n1)
+        phi, dphi, leg = np.zeros((n1, n1)), np.zeros((n1, n1)), np.zeros((n1, n1))
+        modes = np.zeros((self.n_m, 3), dtype=np.int32)
+        self.L.or_tables(self.h, _p(xn), _p(xg), _p(wg), _p(phi), _p(dphi), _p(leg),
+                         modes.ctypes.data_as(C.POINTER(C.c_int)))
+        return dict(xn=xn, xg=xg, wg=wg, phi=phi, dphi=dphi, leg=leg, modes=modes)
+
+    def element_B(self) -> np.ndarray:
+        B = np.zeros((self.n_m, 3 * self.n_q))
+        self.L.or_element_B(self.h, _p(B))
+        return B
+
+    def element_A_matrix(self, mue) -> np.ndarray:
+        mue = _f64(mue)
+        A = np.zeros((3 * self.n_q, 3 * self.n_q))
+        self.L.or_element_A_matrix(self.h, _p(mue), _p(A))
+        return A
+
+    def dofmap(self) -> np.ndarray:
+        m = np.zeros(self.n_el * self.n_q, dtype=np.int64)
+        self.L.or_dofmap(self.h, m.ctypes.data_as(_I64))
+        return m
+
+    def boundary_elements(self) -> np.ndarray:
+        f = np.zeros(self.n_el, dtype=np.uint8)
+        self.L.or_boundary_elements(self.h, f.ctypes.data_as(C.POINTER(C.c_uint8)))
+        return f
+
+    def boundary_mask(self) -> np.ndarray:
+        m = np.zeros(self.n_v, dtype=np.uint8)
+        self.L.or_boundary_mask(self.h, m.ctypes.data_as(C.POINTER(C.c_uint8)))
+        return m
+
+    # ---- operators
+    def apply_A(self, mu_q, u, nomask=False) -> np.ndarray:
+        mu_q, u = _f64(mu_q), _f64(u)
+        y = np.zeros(self.n_v)
+        self.L.or_apply_A(self.h, _p(mu_q), _p(u), _p(y), int(nomask))
+        return y
+
+    def apply_A_sampled(self, mu_q, u, dofs) -> np.ndarray:
+        mu_q, u = _f64(mu_q), _f64(u)
+        dofs = np.ascontiguousarray(dofs, dtype=np.int64)
+        y = np.zeros(len(dofs))
+        self.L.or_apply_A_sampled(self.h, _p(mu_q), _p(u), dofs.ctypes.data_as(_I64), len(dofs), _p(y))
+        return y
+
+    def apply_B(self, u, nomask=False) -> np.ndarray:
+        u = _f64(u)
+        p = np.zeros(self.n_p)
+        self.L.or_apply_B(self.h, _p(u), _p(p), int(nomask))
+        return p
+
+    def apply_BT(self, p, nomask=False) -> np.ndarray:
+        p = _f64(p)
+        y = np.zeros(self.n_v)
+        self.L.or_apply_BT(self.h, _p(p), _p(y), int(nomask))
+        return y
+
+    def lumped(self, mu_q, a_l=1.0, a_r=1.0) -> dict:
+        mu_q = _f64(mu_q)
+        Cw, Dw, Ci, Di = (np.zeros(self.n_nodes) for _ in range(4))
+        npos = np.zeros(2, dtype=np.int64)
+        self.L.or_lumped(self.h, _p(mu_q), float(a_l), float(a_r), _p(Cw), _p(Dw), _p(Ci), _p(Di),
+                         npos.ctypes.data_as(_I64))
+        return dict(Cw=Cw, Dw=Dw, Cinv=Ci, Dinv=Di, n_nonpos_Cw=int(npos[0]), n_nonpos_Dw=int(npos[1]))
+
+    def apply_K(self, Xinv, p) -> np.ndarray:
+        Xinv, p = _f64(Xinv), _f64(p)
+        q = np.zeros(self.n_p)
+        tv = np.zeros(self.n_v)
+        self.L.or_apply_K(self.h, _p(Xinv), _p(p), _p(q), _p(tv))
+        return q
+
+    def jacobi_diag(self, Xinv) -> np.ndarray:
+        Xinv = _f64(Xinv)
+        d = np.zeros(self.n_p)
+        self.L.or_jacobi_diag(self.h, _p(Xinv), _p(d))
+        return d
+
+    def project(self, v) -> np.ndarray:
+        v = _f64(v).copy()
+        self.L.or_project(self.h, _p(v))
+        return v
+
+    def pcg(self, Xinv, diagK, b, iters) -> np.ndarray:
+        Xinv, diagK, b = _f64(Xinv), _f64(diagK), _f64(b)
+        x = np.zeros(self.n_p)
+        self.L.or_pcg(self.h, _p(Xinv), _p(diagK), _p(b), _p(x), int(iters))
+        return x
+
+    def pcg_step(self, Xinv, diagK, x, r, p, rz):
+        """One PCG iteration from state (x, r, p, rz); returns new (x, r, p, rz)."""
+        Xinv, diagK = _f64(Xinv), _f64(diagK)
+        x, r, p = _f64(x).copy(), _f64(r).copy(), _f64(p).copy()
+        rzv = C.c_double(rz)
+        self.L.or_pcg_step(self.h, _p(Xinv), _p(diagK), _p(x), _p(r), _p(p), C.byref(rzv))
+        return x, r, p, rzv.value
+
+    def poisson(self, Xinv, diagK, b, iters) -> np.ndarray:
+        Xinv, diagK, b = _f64(Xinv), _f64(diagK), _f64(b)
+        x = np.zeros(self.n_p)
+        self.L.or_poisson(self.h, _p(Xinv), _p(diagK), _p(b), _p(x), int(iters))
+        return x
+
+    def poisson_relres(self, Xinv, b, x) -> float:
+        Xinv, b, x = _f64(Xinv), _f64(b), _f64(x)
+        return float(self.L.or_poisson_relres(self.h, _p(Xinv), _p(b), _p(x)))
+
+    # ---- composite
+    def setup(self, mu_q, a_l=1.0, a_r=1.0) -> dict:
+        """Lumped diagonals and both Jacobi diagonals (rows a3, a4)."""
+        self.mu_q = _f64(mu_q)
+        lm = self.lumped(self.mu_q, a_l, a_r)
+        lm["diagKl"] = self.jacobi_diag(lm["Cinv"])
+        lm["diagKr"] = self.jacobi_diag(lm["Dinv"])
+        self.state = lm
+        return lm
+
+    def wbfbt(self, r, iters, state=None) -> np.ndarray:
+        s = self.state if state is None else state
+        r = _f64(r)
+        z = np.zeros(self.n_p)
+        self.L.or_wbfbt(self.h, _p(self.mu_q), _p(s["Cinv"]), _p(s["Dinv"]), _p(s["diagKl"]),
+                        _p(s["diagKr"]), _p(r), _p(z), int(iters))
+        return z
+
+    @staticmethod
+    def num_threads() -> int:
+        return int(lib().or_num_threads())

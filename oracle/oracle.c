@@ -1,0 +1,598 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU oracle for the wBFBT hot path
+ * of Rudi, Stadler & Ghattas, "Weighted BFBT preconditioner for Stokes flow
+ * problems with highly heterogeneous viscosity" (arXiv 1607.03936).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_1607_03936_b200/) never links or calls it, and the
+ * two share no code, headers or tables: this file derives its 1-D tables by
+ * Newton iteration in long double; the CUDA path uses closed-form constants.
+ *
+ * Everything is IEEE binary64 (the paper fixes no precision), compiled with
+ * -O2 -fno-fast-math -ffp-contract=off.  OpenMP (if enabled) only computes
+ * element-local quantities into a buffer; every global sum (scatter-add,
+ * dot product) runs serially in a fixed order, so results are bit-identical
+ * for any thread count.
+ *
+ * Citations: PAPER.md line numbers (+ section / equation label).
+ *   eq:stokes          PAPER.md:145-162   -div[mu(grad u + grad u^T)] + grad p = f, -div u = 0, u=0 on boundary
+ *   eq:discrete-stokes PAPER.md:187-204   [A B^T; B 0]
+ *   Q_k x P_{k-1}^disc PAPER.md:205-209   continuous nodal velocity, discontinuous modal pressure
+ *   B u := -div u
+ *   eq:lumping         PAPER.md:310-323   lumping with the coefficient vector of the constant 1
+ *   eq:wbfbt           PAPER.md:438-454   C_w = M~_u(w_l), D_w = M~_u(w_r), w = sqrt(mu)
+ *   eq:bdramp          PAPER.md:2219-2251 boundary amplification a_l, a_r on elements touching the boundary
+ *   K_w (Neumann)
+ *   mu at quad points
+ * Readings of silences (R1..R14) are listed in DESIGN.md Sec. 3; the ones used
+ * here are cited inline.
+ *
+ * Parity pins: every function below is pinned by tests/test_oracle_*.py
+ * against closed forms, paper tables, invariants or brute force -- except the
+ * fixed-iteration PCG / wBFBT VALUES, whose only pins are the converged
+ * limit, scale invariance and one-step agreement: "parity unpinned" beyond
+ * those.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define OR_MAXN1 9 /* up to k = 8 */
+
+typedef struct {
+  int N, k, n1, nq, nm;
+  int64_t n_el, n_nodes, n_v, n_p;
+  double h, detJ;                  /* h = 1/N, detJ = (h/2)^3 */
+  double xn[OR_MAXN1];             /* GLL nodes (R1) */
+  double xg[OR_MAXN1], wg[OR_MAXN1]; /* Gauss-Legendre points / weights (R3) */
+  double phi[OR_MAXN1][OR_MAXN1];  /* phi[a][i]  = phi_a(xg_i)   */
+  double dphi[OR_MAXN1][OR_MAXN1]; /* dphi[a][i] = phi_a'(xg_i)  */
+  double leg[OR_MAXN1][OR_MAXN1];  /* leg[m][i]  = Lhat_m(xg_i)  */
+  int mode[200][3];                /* pressure mode exponents (R2) */
+  /* tabulated 3-D quantities on the reference element */
+  double* gphi;  /* [a][q][j] = d/dxi_j phi_a(xi_q)  (reference gradient) */
+  double* vphi;  /* [a][q]    = phi_a(xi_q) */
+  double* wq;    /* [q]       = w_qx w_qy w_qz */
+  double* Be;    /* [m][c*nq + a] element divergence matrix (constant on the uniform mesh) */
+  double* work;  /* element-local scratch for chunked parallel loops */
+  int64_t chunk;
+} or_ctx;
+
+/* ---------------------------------------------------------------- 1-D tables
+ * Legendre P_n and P_n' by the three-term recurrence, long double.           */
+static void legendre(int n, long double x, long double* P, long double* dP) {
+  long double p0 = 1.0L, p1 = x;
+  if (n == 0) { *P = 1.0L; *dP = 0.0L; return; }
+  for (int j = 2; j <= n; ++j) {
+    long double p2 = ((2.0L * j - 1.0L) * x * p1 - (j - 1.0L) * p0) / j;
+    p0 = p1; p1 = p2;
+  }
+  *P = p1;
+  /* P_n' = n (x P_n - P_{n-1}) / (x^2 - 1), valid off +-1 */
+  *dP = n * (x * p1 - p0) / (x * x - 1.0L);
+}
+
+static void sort_ld(long double* v, int n) {
+  for (int i = 1; i < n; ++i)
+    for (int j = i; j > 0 && v[j] < v[j - 1]; --j) { long double t = v[j]; v[j] = v[j - 1]; v[j - 1] = t; }
+}
+
+/* Gauss-Legendre: roots of P_n, weights 2 / ((1-x^2) P_n'(x)^2). */
+static void gauss_legendre(int n, double* x, double* w) {
+  long double r[OR_MAXN1], wl[OR_MAXN1];
+  for (int i = 0; i < n; ++i) {
+    long double z = cosl(3.14159265358979323846264338327950288L * (i + 0.75L) / (n + 0.5L));
+    for (int it = 0; it < 100; ++it) {
+      long double P, dP; legendre(n, z, &P, &dP);
+      long double dz = P / dP; z -= dz;
+      if (fabsl(dz) < 1e-30L) break;
+    }
+    r[i] = z;
+  }
+  sort_ld(r, n);
+  for (int i = 0; i < n; ++i) {
+    long double P, dP; legendre(n, r[i], &P, &dP);
+    wl[i] = 2.0L / ((1.0L - r[i] * r[i]) * dP * dP);
+    x[i] = (double)r[i]; w[i] = (double)wl[i];
+  }
+}
+
+/* GLL nodes of degree k: -1, roots of P_k', +1.  Newton on P_k' with
+ * P_k'' = (2x P_k' - k(k+1) P_k) / (1 - x^2) (Legendre ODE).                 */
+static void gll_nodes(int k, double* x) {
+  long double r[OR_MAXN1];
+  r[0] = -1.0L; r[k] = 1.0L;
+  for (int i = 1; i < k; ++i) {
+    long double z = -cosl(3.14159265358979323846264338327950288L * i / k);
+    for (int it = 0; it < 100; ++it) {
+      long double P, dP; legendre(k, z, &P, &dP);
+      long double d2P = (2.0L * z * dP - k * (k + 1.0L) * P) / (1.0L - z * z);
+      long double dz = dP / d2P; z -= dz;
+      if (fabsl(dz) < 1e-30L) break;
+    }
+    r[i] = z;
+  }
+  sort_ld(r, k + 1);
+  for (int i = 0; i <= k; ++i) x[i] = (double)r[i];
+}
+
+/* Lagrange basis on nodes xn (product formula), value and derivative at t. */
+static long double lagrange(const double* xn, int n1, int a, long double t) {
+  long double v = 1.0L;
+  for (int b = 0; b < n1; ++b) if (b != a) v *= (t - xn[b]) / ((long double)xn[a] - xn[b]);
+  return v;
+}
+static long double dlagrange(const double* xn, int n1, int a, long double t) {
+  long double s = 0.0L;
+  for (int j = 0; j < n1; ++j) {
+    if (j == a) continue;
+    long double v = 1.0L / ((long double)xn[a] - xn[j]);
+    for (int b = 0; b < n1; ++b) if (b != a && b != j) v *= (t - xn[b]) / ((long double)xn[a] - xn[b]);
+    s += v;
+  }
+  return s;
+}
+
+/* ---------------------------------------------------------------- context */
+static int or_nmodes(int k) { return k * (k + 1) * (k + 2) / 6; } /* C(k+2,3) = dim P_{k-1} in 3-D */
+
+or_ctx* or_create(int N, int k) {
+  if (N < 1 || k < 1 || k + 1 > OR_MAXN1) return NULL;
+  or_ctx* c = (or_ctx*)calloc(1, sizeof(or_ctx));
+  c->N = N; c->k = k; c->n1 = k + 1; c->nq = c->n1 * c->n1 * c->n1; c->nm = or_nmodes(k);
+  c->n_el = (int64_t)N * N * N;
+  int64_t nn1 = (int64_t)k * N + 1;
+  c->n_nodes = nn1 * nn1 * nn1; c->n_v = 3 * c->n_nodes; c->n_p = c->nm * c->n_el;
+  c->h = 1.0 / N;
+  c->detJ = (c->h / 2) * (c->h / 2) * (c->h / 2);
+  gll_nodes(k, c->xn);
+  gauss_legendre(c->n1, c->xg, c->wg);
+  for (int a = 0; a < c->n1; ++a)
+    for (int i = 0; i < c->n1; ++i) {
+      c->phi[a][i] = (double)lagrange(c->xn, c->n1, a, c->xg[i]);
+      c->dphi[a][i] = (double)dlagrange(c->xn, c->n1, a, c->xg[i]);
+    }
+  /* orthonormal Legendre Lhat_m = sqrt((2m+1)/2) P_m (R2) */
+  for (int m = 0; m < c->n1; ++m)
+    for (int i = 0; i < c->n1; ++i) {
+      long double P, dP;
+      if (m == 0) P = 1.0L; else legendre(m, c->xg[i], &P, &dP);
+      c->leg[m][i] = (double)(sqrtl((2.0L * m + 1.0L) / 2.0L) * P);
+    }
+  /* mode order (R2): for d in 0..k-1, for cz in 0..d, for cy in 0..d-cz: cx = d-cy-cz */
+  int m = 0;
+  for (int d = 0; d <= k - 1; ++d)
+    for (int cz = 0; cz <= d; ++cz)
+      for (int cy = 0; cy <= d - cz; ++cy) { c->mode[m][0] = d - cy - cz; c->mode[m][1] = cy; c->mode[m][2] = cz; ++m; }
+  const int n1 = c->n1, nq = c->nq;
+  c->gphi = (double*)malloc(sizeof(double) * nq * nq * 3);
+  c->vphi = (double*)malloc(sizeof(double) * nq * nq);
+  c->wq = (double*)malloc(sizeof(double) * nq);
+  for (int a = 0; a < nq; ++a) {
+    int ax = a % n1, ay = (a / n1) % n1, az = a / (n1 * n1);
+    for (int q = 0; q < nq; ++q) {
+      int qx = q % n1, qy = (q / n1) % n1, qz = q / (n1 * n1);
+      double px = c->phi[ax][qx], py = c->phi[ay][qy], pz = c->phi[az][qz];
+      c->vphi[a * nq + q] = px * py * pz;
+      c->gphi[(a * nq + q) * 3 + 0] = c->dphi[ax][qx] * py * pz;
+      c->gphi[(a * nq + q) * 3 + 1] = px * c->dphi[ay][qy] * pz;
+      c->gphi[(a * nq + q) * 3 + 2] = px * py * c->dphi[az][qz];
+    }
+  }
+  for (int q = 0; q < nq; ++q) {
+    int qx = q % n1, qy = (q / n1) % n1, qz = q / (n1 * n1);
+    c->wq[q] = c->wg[qx] * c->wg[qy] * c->wg[qz];
+  }
+  /* B_e[m][(c,a)] = - sum_q q_m(xi_q) d_c phi_a(xi_q) w_q detJ, d_c = (2/h) d/dxi_c
+   * (B u := -div u; B_ij = -int q_i div phi_j). */
+  c->Be = (double*)malloc(sizeof(double) * c->nm * 3 * nq);
+  for (int mm = 0; mm < c->nm; ++mm)
+    for (int cc = 0; cc < 3; ++cc)
+      for (int a = 0; a < nq; ++a) {
+        double s = 0.0;
+        for (int q = 0; q < nq; ++q) {
+          int qx = q % n1, qy = (q / n1) % n1, qz = q / (n1 * n1);
+          double qm = c->leg[c->mode[mm][0]][qx] * c->leg[c->mode[mm][1]][qy] * c->leg[c->mode[mm][2]][qz];
+          s += qm * ((2.0 / c->h) * c->gphi[(a * nq + q) * 3 + cc]) * c->wq[q] * c->detJ;
+        }
+        c->Be[(int64_t)mm * 3 * nq + cc * nq + a] = -s;
+      }
+  c->chunk = 2048;
+  c->work = (double*)malloc(sizeof(double) * c->chunk * 3 * nq);
+  return c;
+}
+
+void or_destroy(or_ctx* c) {
+  if (!c) return;
+  free(c->gphi); free(c->vphi); free(c->wq); free(c->Be); free(c->work); free(c);
+}
+
+/* Structured sizes without building tables (n_el, n_nodes, n_v, n_p, n_q, n_m). */
+void or_sizes_only(int N, int k, int64_t* out) {
+  int64_t nn1 = (int64_t)k * N + 1, n1 = k + 1;
+  out[0] = (int64_t)N * N * N; out[1] = nn1 * nn1 * nn1; out[2] = 3 * out[1];
+  out[3] = (int64_t)or_nmodes(k) * out[0]; out[4] = n1 * n1 * n1; out[5] = or_nmodes(k);
+}
+
+/* Exports for tests (tables and sizes). */
+void or_sizes(const or_ctx* c, int64_t* out) {
+  out[0] = c->n_el; out[1] = c->n_nodes; out[2] = c->n_v; out[3] = c->n_p; out[4] = c->nq; out[5] = c->nm;
+}
+void or_tables(const or_ctx* c, double* xn, double* xg, double* wg, double* phi, double* dphi, double* leg, int* modes) {
+  for (int i = 0; i < c->n1; ++i) { xn[i] = c->xn[i]; xg[i] = c->xg[i]; wg[i] = c->wg[i]; }
+  for (int a = 0; a < c->n1; ++a) for (int i = 0; i < c->n1; ++i) {
+    phi[a * c->n1 + i] = c->phi[a][i]; dphi[a * c->n1 + i] = c->dphi[a][i]; leg[a * c->n1 + i] = c->leg[a][i];
+  }
+  for (int m = 0; m < c->nm; ++m) for (int d = 0; d < 3; ++d) modes[m * 3 + d] = c->mode[m][d];
+}
+void or_element_B(const or_ctx* c, double* Be) { memcpy(Be, c->Be, sizeof(double) * c->nm * 3 * c->nq); }
+
+/* ---------------------------------------------------------------- structure
+ * a1: e = ex + N(ey + N ez); local a = ax + n1(ay + n1 az);
+ * g = (k ex + ax) + (kN+1)[(k ey + ay) + (kN+1)(k ez + az)];
+ * velocity dof (c, g) -> c*n_nodes + g (SoA); pressure (e, m) -> e*n_m + m.   */
+static int64_t or_node(const or_ctx* c, int64_t e, int a) {
+  int64_t N = c->N, k = c->k, n1 = c->n1, nn1 = k * N + 1;
+  int64_t ex = e % N, ey = (e / N) % N, ez = e / (N * N);
+  int64_t ax = a % n1, ay = (a / n1) % n1, az = a / (n1 * n1);
+  return (k * ex + ax) + nn1 * ((k * ey + ay) + nn1 * (k * ez + az));
+}
+/* boundary node iff any grid index is 0 or kN (u = 0 on the boundary) */
+static int or_node_is_boundary(const or_ctx* c, int64_t g) {
+  int64_t nn1 = (int64_t)c->k * c->N + 1;
+  int64_t gx = g % nn1, gy = (g / nn1) % nn1, gz = g / (nn1 * nn1);
+  return gx == 0 || gy == 0 || gz == 0 || gx == nn1 - 1 || gy == nn1 - 1 || gz == nn1 - 1;
+}
+/* element touches the boundary iff any index is 0 or N-1 (eq:bdramp set D) */
+static int or_elem_on_boundary(const or_ctx* c, int64_t e) {
+  int64_t N = c->N, ex = e % N, ey = (e / N) % N, ez = e / (N * N);
+  return ex == 0 || ey == 0 || ez == 0 || ex == N - 1 || ey == N - 1 || ez == N - 1;
+}
+
+void or_boundary_elements(const or_ctx* c, uint8_t* flag) {
+  for (int64_t e = 0; e < c->n_el; ++e) flag[e] = (uint8_t)or_elem_on_boundary(c, e);
+}
+void or_dofmap(const or_ctx* c, int64_t* map) {
+  for (int64_t e = 0; e < c->n_el; ++e)
+    for (int a = 0; a < c->nq; ++a) map[e * c->nq + a] = or_node(c, e, a);
+}
+void or_boundary_mask(const or_ctx* c, uint8_t* mask) { /* 1 = boundary (eliminated) dof */
+  for (int cc = 0; cc < 3; ++cc)
+    for (int64_t g = 0; g < c->n_nodes; ++g) mask[cc * c->n_nodes + g] = (uint8_t)or_node_is_boundary(c, g);
+}
+
+/* Gather element-local velocity (c, a), Dirichlet entries zeroed unless nomask. */
+static void gather_u(const or_ctx* c, int64_t e, const double* u, double* ue, int nomask) {
+  for (int cc = 0; cc < 3; ++cc)
+    for (int a = 0; a < c->nq; ++a) {
+      int64_t g = or_node(c, e, a);
+      ue[cc * c->nq + a] = (!nomask && or_node_is_boundary(c, g)) ? 0.0 : u[cc * c->n_nodes + g];
+    }
+}
+/* Scatter-add element vectors chunk [e0, e1) in element order (serial => fixed order). */
+static void scatter_chunk(const or_ctx* c, int64_t e0, int64_t e1, const double* ye, double* y) {
+  for (int64_t e = e0; e < e1; ++e)
+    for (int cc = 0; cc < 3; ++cc)
+      for (int a = 0; a < c->nq; ++a)
+        y[cc * c->n_nodes + or_node(c, e, a)] += ye[(e - e0) * 3 * c->nq + cc * c->nq + a];
+}
+static void mask_velocity(const or_ctx* c, double* y) {
+  for (int cc = 0; cc < 3; ++cc)
+    for (int64_t g = 0; g < c->n_nodes; ++g) if (or_node_is_boundary(c, g)) y[cc * c->n_nodes + g] = 0.0;
+}
+
+/* ---------------------------------------------------------------- A(mu)
+ * Element viscous-stress action by dense Gauss quadrature (R3, R4):
+ *   (A_e u_e)_{c,a} = sum_q mu_q w_q detJ sum_j d_j phi_a(x_q) (d_j u_c + d_c u_j)(x_q)
+ * i.e. int 2 mu eps(u):eps(phi_a e_c), the weak form of -div[mu(grad u + grad u^T)]
+ * (eq:stokes; A_mu = -div(2 mu grad_s u)),
+ * d_j = (2/h) d/dxi_j on the uniform mesh.                                    */
+static void element_A_apply(const or_ctx* c, const double* mue, const double* ue, double* ye) {
+  const int nq = c->nq; const double s = 2.0 / c->h;
+  for (int i = 0; i < 3 * nq; ++i) ye[i] = 0.0;
+  for (int q = 0; q < nq; ++q) {
+    double G[3][3]; /* G[cc][j] = d_j u_cc at x_q */
+    for (int cc = 0; cc < 3; ++cc) for (int j = 0; j < 3; ++j) {
+      double t = 0.0;
+      for (int a = 0; a < nq; ++a) t += ue[cc * nq + a] * (s * c->gphi[(a * nq + q) * 3 + j]);
+      G[cc][j] = t;
+    }
+    double wmu = mue[q] * c->wq[q] * c->detJ;
+    for (int cc = 0; cc < 3; ++cc)
+      for (int a = 0; a < nq; ++a) {
+        double t = 0.0;
+        for (int j = 0; j < 3; ++j) t += (s * c->gphi[(a * nq + q) * 3 + j]) * (G[cc][j] + G[j][cc]);
+        ye[cc * nq + a] += wmu * t;
+      }
+  }
+}
+
+/* Explicit element matrix (tests / dense assembly):
+ * A_e[(c,a),(d,b)] = sum_q mu_q w_q detJ [delta_cd grad phi_a . grad phi_b + d_d phi_a d_c phi_b] */
+void or_element_A_matrix(const or_ctx* c, const double* mue, double* Ae) {
+  const int nq = c->nq, n = 3 * nq; const double s = 2.0 / c->h;
+  for (int64_t i = 0; i < (int64_t)n * n; ++i) Ae[i] = 0.0;
+  for (int q = 0; q < nq; ++q) {
+    double wmu = mue[q] * c->wq[q] * c->detJ;
+    for (int cc = 0; cc < 3; ++cc) for (int a = 0; a < nq; ++a)
+      for (int d = 0; d < 3; ++d) for (int b = 0; b < nq; ++b) {
+        double v = 0.0;
+        if (cc == d) for (int j = 0; j < 3; ++j) v += (s * c->gphi[(a * nq + q) * 3 + j]) * (s * c->gphi[(b * nq + q) * 3 + j]);
+        v += (s * c->gphi[(a * nq + q) * 3 + d]) * (s * c->gphi[(b * nq + q) * 3 + cc]);
+        Ae[(int64_t)(cc * nq + a) * n + d * nq + b] += wmu * v;
+      }
+  }
+}
+
+/* y = M A(mu) M u  (nomask != 0: no Dirichlet elimination -- test pins only) */
+void or_apply_A(or_ctx* c, const double* mu_q, const double* u, double* y, int nomask) {
+  const int nq = c->nq;
+  memset(y, 0, sizeof(double) * c->n_v);
+  for (int64_t e0 = 0; e0 < c->n_el; e0 += c->chunk) {
+    int64_t e1 = e0 + c->chunk < c->n_el ? e0 + c->chunk : c->n_el;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = e0; e < e1; ++e) {
+      double ue[3 * 729];
+      gather_u(c, e, u, ue, nomask);
+      element_A_apply(c, mu_q + e * nq, ue, c->work + (e - e0) * 3 * nq);
+    }
+    scatter_chunk(c, e0, e1, c->work, y);
+  }
+  if (!nomask) mask_velocity(c, y);
+}
+
+/* A at sampled velocity dofs only: y_s = (M A M u)[dofs[s]] (full-size sampled parity). */
+void or_apply_A_sampled(or_ctx* c, const double* mu_q, const double* u, const int64_t* dofs, int64_t ns, double* ys) {
+  const int nq = c->nq, n1 = c->n1; const int64_t N = c->N, k = c->k, nn1 = k * N + 1;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t s = 0; s < ns; ++s) {
+    int64_t dof = dofs[s]; int cc = (int)(dof / c->n_nodes); int64_t g = dof % c->n_nodes;
+    double acc = 0.0;
+    if (!or_node_is_boundary(c, g)) {
+      int64_t gx = g % nn1, gy = (g / nn1) % nn1, gz = g / (nn1 * nn1);
+      /* elements containing node g, in increasing element index */
+      for (int64_t ez = 0; ez < N; ++ez) { int64_t az = gz - k * ez; if (az < 0 || az > k) continue;
+        for (int64_t ey = 0; ey < N; ++ey) { int64_t ay = gy - k * ey; if (ay < 0 || ay > k) continue;
+          for (int64_t ex = 0; ex < N; ++ex) { int64_t ax = gx - k * ex; if (ax < 0 || ax > k) continue;
+            int64_t e = ex + N * (ey + N * ez);
+            double ue[3 * 729], ye[3 * 729];
+            gather_u(c, e, u, ue, 0);
+            element_A_apply(c, mu_q + e * nq, ue, ye);
+            acc += ye[cc * nq + (int)(ax + n1 * (ay + n1 * az))];
+          } } }
+    }
+    ys[s] = acc;
+  }
+}
+
+/* ---------------------------------------------------------------- B, B^T
+ * p_e = B_e (M u)_e  (divergence, B u := -div u)                */
+void or_apply_B(or_ctx* c, const double* u, double* p, int nomask) {
+  const int nq = c->nq, nm = c->nm;
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < c->n_el; ++e) {
+    double ue[3 * 729];
+    gather_u(c, e, u, ue, nomask);
+    for (int m = 0; m < nm; ++m) {
+      double s = 0.0;
+      for (int i = 0; i < 3 * nq; ++i) s += c->Be[(int64_t)m * 3 * nq + i] * ue[i];
+      p[e * nm + m] = s;
+    }
+  }
+}
+
+/* y = M B^T p  (gradient) */
+void or_apply_BT(or_ctx* c, const double* p, double* y, int nomask) {
+  const int nq = c->nq, nm = c->nm;
+  memset(y, 0, sizeof(double) * c->n_v);
+  for (int64_t e0 = 0; e0 < c->n_el; e0 += c->chunk) {
+    int64_t e1 = e0 + c->chunk < c->n_el ? e0 + c->chunk : c->n_el;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = e0; e < e1; ++e) {
+      double* ye = c->work + (e - e0) * 3 * nq;
+      for (int i = 0; i < 3 * nq; ++i) {
+        double s = 0.0;
+        for (int m = 0; m < nm; ++m) s += c->Be[(int64_t)m * 3 * nq + i] * p[e * nm + m];
+        ye[i] = s;
+      }
+    }
+    scatter_chunk(c, e0, e1, c->work, y);
+  }
+  if (!nomask) mask_velocity(c, y);
+}
+
+/* ---------------------------------------------------------------- C_w, D_w
+ * Lumped weighted velocity mass (eq:lumping generalised as in eq:wbfbt,
+ * PAPER.md:310-323, 446-454; R7: w = sqrt(mu); eq:bdramp PAPER.md:2232-2245):
+ *   l_e[a](w) = sum_q w_{e,q} phi_a(xi_q) w_q detJ,   C[g] = sum_{e ni g} l_e[a](w_l)
+ * (row sums: the coefficient vector of the constant 1 is all-ones, R8).
+ * Cinv = M/C, Dinv = M/D on nodes; entries <= 0 at interior nodes are counted
+ * and reported, not altered (R9).                                             */
+void or_lumped(or_ctx* c, const double* mu_q, double a_l, double a_r,
+               double* Cw, double* Dw, double* Cinv, double* Dinv, int64_t* nonpos) {
+  const int nq = c->nq;
+  memset(Cw, 0, sizeof(double) * c->n_nodes);
+  memset(Dw, 0, sizeof(double) * c->n_nodes);
+  double* le = (double*)malloc(sizeof(double) * nq);
+  for (int64_t e = 0; e < c->n_el; ++e) {
+    int onb = or_elem_on_boundary(c, e);
+    double al = onb ? a_l : 1.0, ar = onb ? a_r : 1.0;
+    for (int a = 0; a < nq; ++a) {
+      double sl = 0.0, sr = 0.0;
+      for (int q = 0; q < nq; ++q) {
+        double sq = sqrt(mu_q[e * nq + q]);
+        sl += (al * sq) * c->vphi[a * nq + q] * c->wq[q] * c->detJ;
+        sr += (ar * sq) * c->vphi[a * nq + q] * c->wq[q] * c->detJ;
+      }
+      int64_t g = or_node(c, e, a);
+      Cw[g] += sl; Dw[g] += sr;
+    }
+  }
+  free(le);
+  nonpos[0] = nonpos[1] = 0;
+  for (int64_t g = 0; g < c->n_nodes; ++g) {
+    int b = or_node_is_boundary(c, g);
+    if (!b && Cw[g] <= 0.0) nonpos[0]++;
+    if (!b && Dw[g] <= 0.0) nonpos[1]++;
+    Cinv[g] = b ? 0.0 : 1.0 / Cw[g];
+    Dinv[g] = b ? 0.0 : 1.0 / Dw[g];
+  }
+}
+
+/* ---------------------------------------------------------------- K_w, diag
+ * K p = B (Xinv o (B^T p)), Xinv a nodal diagonal acting on all 3 components
+ * (PAPER.md:2453-2461).                                                       */
+void or_apply_K(or_ctx* c, const double* Xinv, const double* p, double* q, double* tmp_v /* n_v */) {
+  or_apply_BT(c, p, tmp_v, 0);
+  for (int cc = 0; cc < 3; ++cc)
+    for (int64_t g = 0; g < c->n_nodes; ++g) tmp_v[cc * c->n_nodes + g] *= Xinv[g];
+  or_apply_B(c, tmp_v, q, 0);
+}
+
+/* diag(K)_{e,m} = sum_{c,a} B_e[m,(c,a)]^2 Xinv[g(e,a)] */
+void or_jacobi_diag(or_ctx* c, const double* Xinv, double* diag) {
+  const int nq = c->nq, nm = c->nm;
+  for (int64_t e = 0; e < c->n_el; ++e)
+    for (int m = 0; m < nm; ++m) {
+      double s = 0.0;
+      for (int cc = 0; cc < 3; ++cc)
+        for (int a = 0; a < nq; ++a) {
+          double b = c->Be[(int64_t)m * 3 * nq + cc * nq + a];
+          s += b * b * Xinv[or_node(c, e, a)];
+        }
+      diag[e * nm + m] = s;
+    }
+}
+
+/* ---------------------------------------------------------------- projection
+ * P v = v - (z0.v / z0.z0) z0, z0 = coefficients of the constant pressure:
+ * 1 = 2^{3/2} Lhat_0^3, so z0 = 2^{3/2} on mode 0 of every element (R10;
+ * Neumann null space).                         */
+static double dot(const double* a, const double* b, int64_t n) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+  return s;
+}
+void or_project(const or_ctx* c, double* v) {
+  const double z = 2.0 * sqrt(2.0);
+  double zv = 0.0, zz = 0.0;
+  for (int64_t e = 0; e < c->n_el; ++e) { zv += z * v[e * c->nm]; zz += z * z; }
+  double f = zv / zz;
+  for (int64_t e = 0; e < c->n_el; ++e) v[e * c->nm] -= f * z;
+}
+
+/* ---------------------------------------------------------------- PCG
+ * Fixed-iteration Jacobi-PCG standing in for the paper's HMG V-cycle
+ * (north_star (5), reading R11):
+ *   x=0; r=b; z=Minv r; p=z; rz=<r,z>
+ *   repeat iters: if rz==0 break; q=Kp; pq=<p,q>; if pq==0 break;
+ *     a=rz/pq; x+=a p; r-=a q; z=Minv r; rz'=<r,z>; b=rz'/rz; p=z+b p; rz=rz'  */
+typedef struct { double* r; double* z; double* p; double* q; double* tv; } or_pcg_ws;
+
+static void pcg_step(or_ctx* c, const double* Xinv, const double* Minv, double* x, double* r, double* p,
+                     double* rz, double* z, double* q, double* tv, double* ab) {
+  const int64_t n = c->n_p;
+  or_apply_K(c, Xinv, p, q, tv);
+  double pq = dot(p, q, n);
+  if (pq == 0.0) { if (ab) { ab[0] = 0; ab[1] = 0; } return; }
+  double alpha = *rz / pq;
+  for (int64_t i = 0; i < n; ++i) x[i] += alpha * p[i];
+  for (int64_t i = 0; i < n; ++i) r[i] -= alpha * q[i];
+  for (int64_t i = 0; i < n; ++i) z[i] = Minv[i] * r[i];
+  double rz2 = dot(r, z, n);
+  double beta = rz2 / *rz;
+  for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+  *rz = rz2;
+  if (ab) { ab[0] = alpha; ab[1] = beta; }
+}
+
+/* x = PCG(K_side, b) with K_side = B Xinv B^T, Minv = 1/diag(K_side). */
+void or_pcg(or_ctx* c, const double* Xinv, const double* diagK, const double* b, double* x, int iters) {
+  const int64_t n = c->n_p;
+  double* r = (double*)malloc(sizeof(double) * n); double* z = (double*)malloc(sizeof(double) * n);
+  double* p = (double*)malloc(sizeof(double) * n); double* q = (double*)malloc(sizeof(double) * n);
+  double* Minv = (double*)malloc(sizeof(double) * n); double* tv = (double*)malloc(sizeof(double) * c->n_v);
+  for (int64_t i = 0; i < n; ++i) Minv[i] = 1.0 / diagK[i];
+  for (int64_t i = 0; i < n; ++i) { x[i] = 0.0; r[i] = b[i]; z[i] = Minv[i] * r[i]; p[i] = z[i]; }
+  double rz = dot(r, z, n);
+  for (int it = 0; it < iters; ++it) {
+    if (rz == 0.0) break;
+    double ab[2];
+    pcg_step(c, Xinv, Minv, x, r, p, &rz, z, q, tv, ab);
+    if (ab[0] == 0.0 && ab[1] == 0.0) break; /* pq == 0 */
+  }
+  free(r); free(z); free(p); free(q); free(Minv); free(tv);
+}
+
+/* One PCG iteration from a supplied state (x, r, p, rz) -- one-step parity. */
+void or_pcg_step(or_ctx* c, const double* Xinv, const double* diagK, double* x, double* r, double* p, double* rz) {
+  const int64_t n = c->n_p;
+  double* z = (double*)malloc(sizeof(double) * n); double* q = (double*)malloc(sizeof(double) * n);
+  double* Minv = (double*)malloc(sizeof(double) * n); double* tv = (double*)malloc(sizeof(double) * c->n_v);
+  for (int64_t i = 0; i < n; ++i) Minv[i] = 1.0 / diagK[i];
+  pcg_step(c, Xinv, Minv, x, r, p, rz, z, q, tv, NULL);
+  free(z); free(q); free(Minv); free(tv);
+}
+
+/* Projected Poisson solve: x = P PCG(K_side, P b) (R10). */
+void or_poisson(or_ctx* c, const double* Xinv, const double* diagK, const double* b, double* x, int iters) {
+  double* bb = (double*)malloc(sizeof(double) * c->n_p);
+  memcpy(bb, b, sizeof(double) * c->n_p);
+  or_project(c, bb);
+  or_pcg(c, Xinv, diagK, bb, x, iters);
+  or_project(c, x);
+  free(bb);
+}
+
+/* ---------------------------------------------------------------- wBFBT
+ * z = S~^{-1}_wBFBT r  (eq:wbfbt), applied right to left:
+ *   y = P PCG(K_r, P r); v = Dinv o (B^T y); v = A v; v = Cinv o v; s = P(B v);
+ *   z = P PCG(K_l, s)
+ * with K_l = B Cinv B^T, K_r = B Dinv B^T.              */
+void or_wbfbt(or_ctx* c, const double* mu_q, const double* Cinv, const double* Dinv,
+              const double* diagKl, const double* diagKr, const double* r, double* z, int iters) {
+  const int64_t np = c->n_p, nv = c->n_v, nn = c->n_nodes;
+  double* y = (double*)malloc(sizeof(double) * np);
+  double* s = (double*)malloc(sizeof(double) * np);
+  double* v = (double*)malloc(sizeof(double) * nv);
+  double* w = (double*)malloc(sizeof(double) * nv);
+  double* rr = (double*)malloc(sizeof(double) * np);
+  memcpy(rr, r, sizeof(double) * np);
+  or_project(c, rr);
+  or_pcg(c, Dinv, diagKr, rr, y, iters);
+  or_project(c, y);
+  free(rr);
+  or_apply_BT(c, y, v, 0);
+  for (int cc = 0; cc < 3; ++cc) for (int64_t g = 0; g < nn; ++g) v[cc * nn + g] *= Dinv[g];
+  or_apply_A(c, mu_q, v, w, 0);
+  for (int cc = 0; cc < 3; ++cc) for (int64_t g = 0; g < nn; ++g) w[cc * nn + g] *= Cinv[g];
+  or_apply_B(c, w, s, 0);
+  or_project(c, s);
+  or_pcg(c, Cinv, diagKl, s, z, iters);
+  or_project(c, z);
+  free(y); free(s); free(v); free(w);
+}
+
+/* Relative residual ||b - K x|| / ||b|| of a Poisson solve (quality check). */
+double or_poisson_relres(or_ctx* c, const double* Xinv, const double* b, const double* x) {
+  double* q = (double*)malloc(sizeof(double) * c->n_p);
+  double* tv = (double*)malloc(sizeof(double) * c->n_v);
+  or_apply_K(c, Xinv, x, q, tv);
+  double nr = 0.0, nb = 0.0;
+  for (int64_t i = 0; i < c->n_p; ++i) { double d = b[i] - q[i]; nr += d * d; nb += b[i] * b[i]; }
+  free(q); free(tv);
+  return sqrt(nr) / sqrt(nb);
+}
+
+int or_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
