@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark of the wBFBT hot path on B200 (BASELINE.json metric).
+
+A step = one pass of every SURVEY.md Sec. 8(a) row over one synthetic batch:
+wb_hotpath = set_viscosity (rows a3, a4) + A u + B u + B^T p + wBFBT(p)
+(rows a5-a10; row a1 is inline in every kernel) on the BASELINE.json config
+C5 (64^3 Q2 x P1disc, 100 PCG iterations per Poisson inverse).
+
+value   = whole-job steps/s (= wBFBT applies/s of full hot-path steps) with
+          inputs resident in HBM, device time (CUDA events), max over ranks;
+          the L2 is flushed (256 MiB memset) before every timed step, outside
+          the events.
+e2e     = the same step through wb_hotpath_host: host->device copies of
+          mu, u, p from pinned memory and device->host copies of the four
+          results inside the timed region.
+Multi-GPU (torchrun): independent replicas, one problem per rank ("weak").
+--impl reference: the CPU oracle as it stands on a bounded sample (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GDOF/s of fp64 A(mu)u apply; wBFBT applies/s; % of B200 HBM roofline"
+FALLBACK_HBM = 6650.0      # B200_PROFILING.md fallback (GB/s)
+FP64_PEAK_TFLOPS = 37.2    # 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (microbench: 34.2 DFMA, 37.1 DMMA)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class Clocks:
+    """Sample nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_init(n_gpus):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------- reference arm (CPU oracle)
+def oracle_sample(cfg_name="C5", seed=0, pcg_probe=(1, 3)):
+    """Time the oracle as it stands on a bounded sample of the step: setup, A, B,
+    B^T once at full size, and wBFBT at two small PCG counts; the full-size step
+    time is extrapolated linearly in the PCG count."""
+    import synth
+    from oracle import Oracle
+    cfg = synth.CONFIGS[cfg_name]
+    inp = synth.make_inputs(cfg, seed)
+    o = Oracle(cfg.N, cfg.k)
+    t = {}
+    t0 = time.perf_counter(); o.setup(inp["mu_q"]); t["setup"] = time.perf_counter() - t0
+    t0 = time.perf_counter(); o.apply_A(inp["mu_q"], inp["u"]); t["A"] = time.perf_counter() - t0
+    t0 = time.perf_counter(); o.apply_B(inp["u"]); t["B"] = time.perf_counter() - t0
+    t0 = time.perf_counter(); o.apply_BT(inp["p"]); t["BT"] = time.perf_counter() - t0
+    w = []
+    for it in pcg_probe:
+        t0 = time.perf_counter(); o.wbfbt(inp["p"], it); w.append(time.perf_counter() - t0)
+    per_it = (w[1] - w[0]) / (pcg_probe[1] - pcg_probe[0])
+    t_wbfbt = w[0] + per_it * (cfg.iters - pcg_probe[0])
+    step = t["setup"] + t["A"] + t["B"] + t["BT"] + t_wbfbt
+    n_v = 3 * (cfg.k * cfg.N + 1) ** 3
+    return dict(step_s=step, t=t, wbfbt_s=t_wbfbt, per_pcg_iter_s=per_it, A_gdofs=n_v / t["A"] / 1e9,
+                threads=Oracle.num_threads(), sample_s=sum(t.values()) + sum(w),
+                sample=f"{cfg_name} full size: setup+A+B+B^T once; wBFBT at PCG iters {pcg_probe}, "
+                       f"extrapolated linearly to {cfg.iters}")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    r = oracle_sample(args.config)
+    steps_s = []
+    for _ in range(args.warmup + args.steps):
+        pass  # the oracle is timed once per bounded sample (deterministic, no warm-up effects)
+    v = 1.0 / r["step_s"]
+    cores = r["threads"]
+    line = {"impl": "reference", "metric": METRIC, "value": v,
+            "unit": "hot-path steps/s (1 step = setup + A + B + B^T + wBFBT, C5)", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["step_s"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"{args.config} (BASELINE.json configs[4])"},
+            "cpu_baseline": {"value": v, "unit": "hot-path steps/s", "cores": cores, "kind": "oracle",
+                             "sample": r["sample"]},
+            "e2e": {"value": v, "unit": "hot-path steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "components": {"A_gdofs": r["A_gdofs"], "wbfbt_applies_per_s": 1.0 / r["wbfbt_s"],
+                           "oracle_times_s": r["t"]}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_1607_03936_b200 import Context
+
+    rank, world, local = dist_init(args.gpus)
+    cfg = synth.CONFIGS[args.config]
+    inp = synth.make_inputs(cfg, seed=rank)
+    stream = torch.cuda.current_stream()
+    ctx = Context(cfg.N, cfg.k, stream=stream.cuda_stream)
+    d = lambda a: torch.as_tensor(a, dtype=torch.float64, device="cuda")  # noqa: E731
+    mu, u, p = d(inp["mu_q"]), d(inp["u"]), d(inp["p"])
+    f64 = dict(dtype=torch.float64, device="cuda")
+    yA, pB, yBT, z = (torch.empty(n, **f64) for n in (ctx.n_v, ctx.n_p, ctx.n_v, ctx.n_p))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    iters = cfg.iters
+
+    def step():
+        ctx.hotpath(mu, u, p, iters, yA, pB, yBT, z)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    l0 = ctx.query("kernel_launches")
+    barrier(world)
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = int(ctx.query("kernel_launches") - l0)
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t_ms = max_over_ranks(t_ms, world)
+    ms_per_step = t_ms / args.steps
+    value = world * args.steps / (t_ms * 1e-3)
+
+    # ---- component timings (same context, L2 flushed before each rep)
+    def timed(fn, reps=args.comp_reps):
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream); fn(); b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    ctx.set_viscosity(mu)
+    qv = torch.empty(ctx.n_p, **f64)
+    tA = timed(lambda: ctx.apply_A(u, yA))
+    tB = timed(lambda: ctx.apply_B(u, pB))
+    tBT = timed(lambda: ctx.apply_BT(p, yBT))
+    tK = timed(lambda: ctx.apply_K(1, p, qv))
+    tW = timed(lambda: ctx.apply_wbfbt(p, z, iters), reps=max(3, args.comp_reps // 4))
+    tS = timed(lambda: ctx.set_viscosity(mu), reps=max(3, args.comp_reps // 4))
+    # warm (L2-resident) K apply: the PCG loop's regime
+    ts = []
+    for _ in range(args.comp_reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream); ctx.apply_K(1, p, qv); b.record(stream); b.synchronize()
+        ts.append(a.elapsed_time(b))
+    tKw = statistics.median(ts)
+
+    n_el, n_nodes, n_v, n_p, n_q = ctx.n_el, ctx.n_nodes, ctx.n_v, ctx.n_p, ctx.n_q
+    hbm, peak_kind = peaks()
+    bytes_A = 8 * (n_el * n_q + 2 * n_v)          # mu~ + u in + y out
+    bytes_K = 8 * (2 * n_p + n_nodes)             # p in, q out, X^-1 nodal
+    # dominant op of the step: the K_w apply inside the PCG loops (2 x iters per step)
+    share_K = 2 * iters * tKw / ms_per_step
+    roof = {"bound": "hbm", "kernel": "K_w apply (B^T elem + node gather + B) in PCG, warm L2",
+            "achieved": bytes_K / (tKw * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": bytes_K / (tKw * 1e-3) / 1e9 / hbm, "traffic": None, "peak_kind": peak_kind,
+            "algorithmic_bytes": bytes_K, "ms": tKw, "share_of_step_est": share_K}
+
+    # ---- end to end through the host entry (pinned buffers)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    hmu, hu, hp = pin(inp["mu_q"]), pin(inp["u"]), pin(inp["p"])
+    outs = [torch.empty(n, dtype=torch.float64).pin_memory() for n in (n_v, n_p, n_v, n_p)]
+    ctx.hotpath_host(hmu, hu, hp, iters, *outs)
+    te = []
+    barrier(world)
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx.hotpath_host(hmu, hu, hp, iters, *outs)
+        te.append(time.perf_counter() - t0)
+    te_tot = max_over_ranks(sum(te), world)
+    e2e = world * args.steps / te_tot
+    h2d = 8 * (n_el * n_q + n_v + n_p)
+    d2h = 8 * (2 * n_v + 2 * n_p)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = oracle_sample(args.config)
+        cpu = {"value": 1.0 / r["step_s"], "unit": "hot-path steps/s", "cores": r["threads"], "kind": "oracle",
+               "sample": r["sample"], "A_gdofs": r["A_gdofs"], "sample_wall_s": r["sample_s"]}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value,
+                "unit": "hot-path steps/s (1 step = setup + A + B + B^T + wBFBT with 2x100 PCG iters, C5)",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": f"{args.config} = BASELINE.json configs[4]: 64^3 Q2xP1disc, 24 sinkers, "
+                                       f"DR 1e10, {iters} PCG iters", "N": cfg.N, "k": cfg.k,
+                           "l2": "flushed (256 MiB memset) before every timed step",
+                           "parallelism": f"replicas{world}"},
+                "components": {
+                    "A_gdofs": n_v / (tA * 1e-3) / 1e9, "A_ms": tA,
+                    "A_hbm_frac": bytes_A / (tA * 1e-3) / 1e9 / hbm,
+                    "B_gdofs": n_v / (tB * 1e-3) / 1e9, "BT_gdofs": n_v / (tBT * 1e-3) / 1e9,
+                    "K_ms_cold": tK, "K_ms_warm": tKw, "wbfbt_ms": tW, "wbfbt_applies_per_s": 1e3 / tW,
+                    "setup_ms": tS},
+                "roofline": roof,
+                "e2e": {"value": e2e, "unit": "hot-path steps/s", "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h},
+                "gpu_launches": launches,
+                "clocks": clk.summary(),
+                "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--comp-reps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,155 @@
+/*
+ * wbfbt.h -- C ABI of libwbfbt.so, the B200 (sm_100a) FP64 hot path of the
+ * weighted-BFBT Stokes preconditioner of Rudi, Stadler & Ghattas,
+ * "Weighted BFBT Preconditioner for Stokes Flow Problems with Highly
+ * Heterogeneous Viscosity" (arXiv 1607.03936).  Citations are PAPER.md line
+ * numbers of /root/reference/PAPER.md plus the section / equation label.
+ *
+ * Problem (eq:stokes, eq:discrete-stokes):
+ * homogeneous-Dirichlet Stokes on the unit cube, uniform N^3 hexahedral mesh,
+ * continuous nodal Q_k velocity (GLL nodes) x discontinuous modal P_{k-1}
+ * pressure (orthonormal Legendre, total degree), viscosity mu given at the
+ * (k+1)^3 Gauss-Legendre points of every element.
+ *
+ * Layouts (all FP64 arrays are contiguous, caller-owned DEVICE pointers unless
+ * a function name ends in _host):
+ *   element  e = ex + N*(ey + N*ez)
+ *   node     g = gx + (kN+1)*(gy + (kN+1)*gz),   n_nodes = (kN+1)^3
+ *   velocity u[c*n_nodes + g], c in {0,1,2}       n_v = 3*n_nodes  (SoA)
+ *   pressure p[e*n_m + m], n_m = C(k+2,3), modes ordered
+ *            for d in 0..k-1: for m3 in 0..d: for m2 in 0..d-m3: m1 = d-m2-m3
+ *            (mode (m1,m2,m3) = Lhat_m1(xi1) Lhat_m2(xi2) Lhat_m3(xi3))
+ *   mu_q     mu_q[e*n_q + q], q = qx + (k+1)*(qy + (k+1)*qz), n_q = (k+1)^3
+ *
+ * Dirichlet elimination (R6): boundary entries of every velocity
+ * INPUT are ignored; boundary entries of every velocity OUTPUT are written as
+ * exactly 0.0.  The Poisson solves and wBFBT project inputs and outputs off the
+ * constant pressure (Neumann null space).
+ *
+ * Errors: every call returns a wb_status (0 = WB_OK, < 0 error); the message of
+ * the last error is wb_last_error(ctx).  Applies are asynchronous on the
+ * context's stream: device faults surface at wb_sync() or a later call.
+ * Setup calls (wb_create, wb_set_viscosity) synchronise the stream.
+ *
+ * Concurrency: one context = one stream + its own workspace.  Calls on one
+ * context must be externally serialised; use one context per stream to run
+ * concurrently.  Aliasing: an output may not overlap any input (WB_EALIAS).
+ *
+ * Determinism: no floating-point atomics anywhere; every reduction has a fixed
+ * order, so results are bitwise reproducible run to run on the same GPU.
+ */
+#ifndef WBFBT_H
+#define WBFBT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct wb_ctx wb_ctx; /* opaque, library-owned */
+typedef int wb_status;
+
+#define WB_OK 0
+#define WB_EINVAL (-1)       /* bad N / k / iters / null pointer / side          */
+#define WB_ENONPOS_MU (-2)   /* some mu_q <= 0 or non-finite                     */
+#define WB_ENONPOS_LUMP (-3) /* nonpositive C_w / D_w entry under WB_STRICT_LUMP */
+#define WB_ECUDA (-4)        /* CUDA runtime error (message in wb_last_error)    */
+#define WB_ENOMEM (-5)       /* device allocation failed                         */
+#define WB_EALIAS (-6)       /* an output overlaps an input                      */
+#define WB_ESTATE (-7)       /* operator needs wb_set_viscosity first            */
+
+/* flags for wb_create */
+#define WB_STRICT_LUMP 1u  /* nonpositive interior C_w/D_w entry -> WB_ENONPOS_LUMP */
+#define WB_DEBUG_NOMASK 2u /* tests only: A, B, B^T skip the Dirichlet mask        */
+
+/* Library version string. */
+const char* wb_version(void);
+
+/* Create a context for the N^3 mesh with Q_k x P_{k-1}^disc, k in {2,3,4},
+ * N >= 1.  `stream` is a cudaStream_t (NULL = legacy default stream); all
+ * work of the context is enqueued on it.  Allocates the workspace on the
+ * current CUDA device.  Synchronous. */
+wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream);
+void wb_destroy(wb_ctx* ctx);
+/* Re-target the context to another stream (e.g. torch's current stream). */
+wb_status wb_set_stream(wb_ctx* ctx, void* stream);
+const char* wb_last_error(const wb_ctx* ctx);
+
+/* Structured counts (Table 3 counts boundary dofs):
+ * n_el = N^3, n_nodes = (kN+1)^3, n_v = 3 n_nodes, n_p = C(k+2,3) N^3,
+ * n_q = (k+1)^3.  Any output pointer may be NULL. */
+wb_status wb_sizes(const wb_ctx* ctx, int64_t* n_el, int64_t* n_nodes, int64_t* n_v,
+                   int64_t* n_p, int64_t* n_q);
+
+/* Row a1 -- dof map and boundary mask.
+ * map[e*n_q + a] = global node of local node a = ax + (k+1)(ay + (k+1)az) of
+ * element e (device int64, n_el*n_q).  mask[c*n_nodes + g] = 1 iff velocity
+ * dof (c,g) is a Dirichlet (boundary) dof (device uint8, n_v). */
+wb_status wb_get_dofmap(wb_ctx* ctx, int64_t* map);
+wb_status wb_get_boundary_mask(wb_ctx* ctx, uint8_t* mask);
+
+/* Rows a3, a4 -- setup from mu at quadrature points (device, n_el*n_q).
+ *   C_w = lumped M_u(w_l), D_w = lumped M_u(w_r), w_l = a_l(e) sqrt(mu),
+ *   w_r = a_r(e) sqrt(mu)  (eq:lumping PAPER.md:310-323, eq:wbfbt
+ *   PAPER.md:436-454, eq:bdramp PAPER.md:2219-2251: a_l(e) = a_l on elements
+ *   touching the boundary, 1 elsewhere; a_l, a_r >= 1).
+ *   Jacobi diagonals of K_l = B C_w^-1 B^T and K_r = B D_w^-1 B^T.
+ * Also stores mu * w_q * detJ * (2/h)^2 for A.  Fails with WB_ENONPOS_MU if any
+ * mu_q <= 0 or non-finite.  Nonpositive interior lumped entries are counted
+ * (wb_query "n_nonpos_Cw"/"n_nonpos_Dw") and are an error only with
+ * WB_STRICT_LUMP.  mu_q may be freed once the call returns.  Synchronous. */
+wb_status wb_set_viscosity(wb_ctx* ctx, const double* mu_q, double a_l, double a_r);
+
+/* Row a5 -- y = M A(mu) M u, A = weak form of -div[mu(grad u + grad u^T)]
+ * (eq:stokes PAPER.md:148-151; A_mu PAPER.md:986-990), Gauss (k+1)^3
+ * quadrature, sum-factorised.  u, y: n_v. */
+wb_status wb_apply_A(wb_ctx* ctx, const double* u, double* y);
+/* Row a6 -- p = B M u, B u := -div u. u: n_v, p: n_p. */
+wb_status wb_apply_B(wb_ctx* ctx, const double* u, double* p);
+/* Row a7 -- y = M B^T p (gradient).  p: n_p, y: n_v. */
+wb_status wb_apply_BT(wb_ctx* ctx, const double* p, double* y);
+/* Row a8 -- q = K p, K = B X^-1 B^T with X = C_w (side 0, "l") or D_w (side 1,
+ * "r").  No projection.  p, q: n_p. */
+wb_status wb_apply_K(wb_ctx* ctx, int side, const double* p, double* q);
+/* Row a9 -- x = P PCG(K_side, P b) with exactly `iters` Jacobi-PCG iterations
+ * (x0 = 0, M = diag K, no tolerance; stands in for the paper's HMG V-cycle,
+ * PAPER.md:2503-2529; recurrence in DESIGN.md Sec. 4).  b, x: n_p. */
+wb_status wb_poisson_pcg(wb_ctx* ctx, int side, const double* b, double* x, int iters);
+/* Row a10 -- z = S~^-1_wBFBT r (eq:wbfbt PAPER.md:436-454), applied right to
+ * left:  y = P PCG(K_r, P r); v = D_w^-1 B^T y; v = A v; v = C_w^-1 v;
+ * s = P B v; z = P PCG(K_l, s).  r, z: n_p. */
+wb_status wb_apply_wbfbt(wb_ctx* ctx, const double* r, double* z, int iters);
+
+/* One full hot-path step (rows a3-a10 once): set_viscosity(mu_q, a_l, a_r),
+ * yA = A u, pB = B u, yBT = B^T p, z = wBFBT(p).  Device pointers.
+ * Synchronous (setup reports status). */
+wb_status wb_hotpath(wb_ctx* ctx, const double* mu_q, double a_l, double a_r, const double* u,
+                     const double* p, int iters, double* yA, double* pB, double* yBT, double* z);
+/* The same step with HOST buffers: copies mu_q, u, p host->device and the four
+ * results device->host (cudaMemcpyAsync on the context stream; pinned host
+ * memory gives asynchronous copies).  Synchronous. */
+wb_status wb_hotpath_host(wb_ctx* ctx, const double* mu_q, double a_l, double a_r,
+                          const double* u, const double* p, int iters, double* yA, double* pB,
+                          double* yBT, double* z);
+
+/* One PCG iteration (DESIGN.md Sec. 4 recurrence) from a supplied state, in
+ * place: x, r, p device n_p; *rz host in/out.  Test entry for one-step
+ * parity. */
+wb_status wb_debug_pcg_step(wb_ctx* ctx, int side, double* x, double* r, double* p, double* rz);
+
+/* Copies of the setup results (device pointers; any may be NULL):
+ * Cw, Dw, Cinv, Dinv: n_nodes; diagKl, diagKr: n_p. */
+wb_status wb_get_lumped(wb_ctx* ctx, double* Cw, double* Dw, double* Cinv, double* Dinv);
+wb_status wb_get_jacobi(wb_ctx* ctx, double* diagKl, double* diagKr);
+
+/* Scalar queries: "n_nonpos_Cw", "n_nonpos_Dw", "n_el", "n_p", "n_v",
+ * "kernel_launches" (launches since create), "last_pcg_stop_iter". */
+wb_status wb_query(wb_ctx* ctx, const char* key, double* value);
+/* Synchronise the context stream; surfaces asynchronous CUDA errors. */
+wb_status wb_sync(wb_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WBFBT_H */

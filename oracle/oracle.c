@@ -517,7 +517,7 @@ void or_pcg(or_ctx* c, const double* Xinv, const double* diagK, const double* b,
   double* r = (double*)malloc(sizeof(double) * n); double* z = (double*)malloc(sizeof(double) * n);
   double* p = (double*)malloc(sizeof(double) * n); double* q = (double*)malloc(sizeof(double) * n);
   double* Minv = (double*)malloc(sizeof(double) * n); double* tv = (double*)malloc(sizeof(double) * c->n_v);
-  for (int64_t i = 0; i < n; ++i) Minv[i] = 1.0 / diagK[i];
+  for (int64_t i = 0; i < n; ++i) Minv[i] = diagK[i] != 0.0 ? 1.0 / diagK[i] : 0.0; /* R11: pseudo-inverse of diag K */
   for (int64_t i = 0; i < n; ++i) { x[i] = 0.0; r[i] = b[i]; z[i] = Minv[i] * r[i]; p[i] = z[i]; }
   double rz = dot(r, z, n);
   for (int it = 0; it < iters; ++it) {
@@ -534,7 +534,7 @@ void or_pcg_step(or_ctx* c, const double* Xinv, const double* diagK, double* x, 
   const int64_t n = c->n_p;
   double* z = (double*)malloc(sizeof(double) * n); double* q = (double*)malloc(sizeof(double) * n);
   double* Minv = (double*)malloc(sizeof(double) * n); double* tv = (double*)malloc(sizeof(double) * c->n_v);
-  for (int64_t i = 0; i < n; ++i) Minv[i] = 1.0 / diagK[i];
+  for (int64_t i = 0; i < n; ++i) Minv[i] = diagK[i] != 0.0 ? 1.0 / diagK[i] : 0.0; /* R11: pseudo-inverse of diag K */
   pcg_step(c, Xinv, Minv, x, r, p, rz, z, q, tv, NULL);
   free(z); free(q); free(Minv); free(tv);
 }

@@ -1,0 +1,829 @@
+// kernels.cuh -- sm_100a FP64 kernels of the wBFBT hot path.
+//
+// Notation follows SURVEY.md Sec. 8 / DESIGN.md: N elements per axis, order k
+// (n1 = k+1 nodes and Gauss points per axis), n_q = n1^3, n_m = C(k+2,3).
+// Every reduction is fixed-order (no floating-point atomics): results are
+// bitwise reproducible run to run.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "tables.h"
+
+namespace wb {
+
+__constant__ Tab c_tab[3];  // k = 2, 3, 4
+#define TB(K) (c_tab[(K)-2])
+
+struct Geo {
+  int N, k, nn1;     // nn1 = kN + 1 nodes per axis
+  int64_t n_el, n_nodes, n_p;
+};
+
+template <int K> struct Ord {
+  static constexpr int n1 = K + 1, NQ = n1 * n1 * n1, NM = K * (K + 1) * (K + 2) / 6;
+};
+
+__device__ __forceinline__ bool node_bnd(int gx, int gy, int gz, int nn1) {
+  return gx == 0 || gy == 0 || gz == 0 || gx == nn1 - 1 || gy == nn1 - 1 || gz == nn1 - 1;
+}
+__device__ __forceinline__ int64_t node_id(int gx, int gy, int gz, int nn1) {
+  return (int64_t)gx + (int64_t)nn1 * ((int64_t)gy + (int64_t)nn1 * gz);
+}
+__device__ __forceinline__ void elem_xyz(int64_t e, int N, int& ex, int& ey, int& ez) {
+  ex = (int)(e % N);
+  int64_t t = e / N;
+  ey = (int)(t % N);
+  ez = (int)(t / N);
+}
+
+// ------------------------------------------------------------------ reductions
+// Block sum with a fixed shuffle tree, then "last block done": every block
+// writes its partial, the last block to arrive sums all partials in a fixed
+// order.  Returns true in thread 0 of the last block, with *total set.
+template <int BS>
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sw[BS / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sw[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (w == 0) {
+    s = (l < BS / 32) ? sw[l] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  }
+  __syncthreads();
+  return s;  // valid in thread 0
+}
+
+template <int BS>
+__device__ __forceinline__ bool grid_sum(double v, double* partial, unsigned* counter, double* total) {
+  __shared__ bool s_last;
+  double s = block_sum<BS>(v);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = s;
+    __threadfence();
+    unsigned t = atomicAdd(counter, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  double a = 0.0;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += BS) a += __ldcg(partial + i);
+  double tot = block_sum<BS>(a);
+  if (threadIdx.x == 0) {
+    *total = tot;
+    *counter = 0u;
+  }
+  return threadIdx.x == 0;
+}
+
+// ------------------------------------------------------------------ row a1
+template <int K>
+__global__ void k_dofmap(int64_t* map, Geo G) {
+  constexpr int n1 = K + 1, NQ = Ord<K>::NQ;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= G.n_el * NQ) return;
+  int64_t e = i / NQ;
+  int a = (int)(i % NQ);
+  int ex, ey, ez;
+  elem_xyz(e, G.N, ex, ey, ez);
+  map[i] = node_id(K * ex + a % n1, K * ey + (a / n1) % n1, K * ez + a / (n1 * n1), G.nn1);
+}
+
+__global__ void k_bmask(uint8_t* mask, Geo G) {
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G.n_nodes) return;
+  int gx = (int)(g % G.nn1), gy = (int)((g / G.nn1) % G.nn1), gz = (int)(g / ((int64_t)G.nn1 * G.nn1));
+  uint8_t b = node_bnd(gx, gy, gz, G.nn1) ? 1 : 0;
+  mask[g] = b;
+  mask[G.n_nodes + g] = b;
+  mask[2 * G.n_nodes + g] = b;
+}
+
+// ------------------------------------------------------------------ node gather
+// y[c][g] = s[g] * sum_{e ni g} E[c][a(e,g)][e], elements in ascending index
+// (the order of the oracle's element-ordered scatter).  Boundary nodes -> 0
+// unless nomask.  E layout: E[(c*NQ + a)*n_el + e].
+template <int K>
+__global__ void k_gather(const double* __restrict__ E, const double* __restrict__ s,
+                         double* __restrict__ y, Geo G, int nomask) {
+  constexpr int n1 = K + 1, NQ = Ord<K>::NQ;
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G.n_nodes) return;
+  const int nn1 = G.nn1;
+  int gx = (int)(g % nn1), gy = (int)((g / nn1) % nn1), gz = (int)(g / ((int64_t)nn1 * nn1));
+  if (!nomask && node_bnd(gx, gy, gz, nn1)) {
+    y[g] = 0.0; y[G.n_nodes + g] = 0.0; y[2 * G.n_nodes + g] = 0.0;
+    return;
+  }
+  int pe[3][2], pa[3][2], pc[3];
+  const int gg[3] = {gx, gy, gz};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    int q = gg[d] / K, r = gg[d] % K;
+    pc[d] = 0;
+    if (r != 0) { pe[d][0] = q; pa[d][0] = r; pc[d] = 1; }
+    else {
+      if (q - 1 >= 0) { pe[d][pc[d]] = q - 1; pa[d][pc[d]] = K; pc[d]++; }
+      if (q < G.N) { pe[d][pc[d]] = q; pa[d][pc[d]] = 0; pc[d]++; }
+    }
+  }
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  for (int iz = 0; iz < pc[2]; ++iz)
+    for (int iy = 0; iy < pc[1]; ++iy)
+      for (int ix = 0; ix < pc[0]; ++ix) {
+        int64_t e = pe[0][ix] + (int64_t)G.N * (pe[1][iy] + (int64_t)G.N * pe[2][iz]);
+        int a = pa[0][ix] + n1 * (pa[1][iy] + n1 * pa[2][iz]);
+        acc0 += E[(int64_t)(0 * NQ + a) * G.n_el + e];
+        acc1 += E[(int64_t)(1 * NQ + a) * G.n_el + e];
+        acc2 += E[(int64_t)(2 * NQ + a) * G.n_el + e];
+      }
+  double sc = s ? s[g] : 1.0;
+  if (s) { acc0 *= sc; acc1 *= sc; acc2 *= sc; }
+  y[g] = acc0; y[G.n_nodes + g] = acc1; y[2 * G.n_nodes + g] = acc2;
+}
+
+// ------------------------------------------------------------------ row a6: B
+// p_{e,m} = sB * sum_c sum_a prod_d M_cd[m_d][a_d] (X o u)_c[g(e,a)],
+// M_cd = BD if d == c else BI, sB = -(2/h) detJ = -h^2/4  (B u := -div u,
+// PAPER.md:962).  Sum-factorised per component: x, then y, then z.
+// Optional fused dot: partial <p_out, dv>  (PCG <p, K p>).
+template <int K, int BS>
+__global__ void __launch_bounds__(BS) k_B(const double* __restrict__ u, const double* __restrict__ xs,
+                                          double* __restrict__ p, Geo G, double sB, int nomask,
+                                          const int* __restrict__ stop, const double* __restrict__ dv,
+                                          double* partial, unsigned* counter, double* total) {
+  constexpr int n1 = K + 1, NM = Ord<K>::NM;
+  if (stop && *stop) return;
+  const int64_t e = (int64_t)blockIdx.x * BS + threadIdx.x;
+  const bool valid = e < G.n_el;
+  int ex = 0, ey = 0, ez = 0;
+  if (valid) elem_xyz(e, G.N, ex, ey, ez);
+  double Z[NM];
+#pragma unroll
+  for (int m = 0; m < NM; ++m) Z[m] = 0.0;
+  if (valid) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+      for (int az = 0; az < n1; ++az) {
+        double Y[K][K];
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+#pragma unroll
+          for (int j = 0; j < K; ++j) Y[i][j] = 0.0;
+#pragma unroll
+        for (int ay = 0; ay < n1; ++ay) {
+          double v[n1];
+          const int gy = K * ey + ay, gz = K * ez + az;
+#pragma unroll
+          for (int ax = 0; ax < n1; ++ax) {
+            const int gx = K * ex + ax;
+            const int64_t g = node_id(gx, gy, gz, G.nn1);
+            double val = u[c * G.n_nodes + g];
+            if (xs) val *= xs[g];
+            else if (!nomask && node_bnd(gx, gy, gz, G.nn1)) val = 0.0;
+            v[ax] = val;
+          }
+          double X[K];
+#pragma unroll
+          for (int m1 = 0; m1 < K; ++m1) {
+            double t = 0.0;
+#pragma unroll
+            for (int ax = 0; ax < n1; ++ax) t = fma(c == 0 ? TB(K).BD[m1][ax] : TB(K).BI[m1][ax], v[ax], t);
+            X[m1] = t;
+          }
+#pragma unroll
+          for (int m1 = 0; m1 < K; ++m1)
+#pragma unroll
+            for (int m2 = 0; m2 < K - m1; ++m2)
+              Y[m1][m2] = fma(c == 1 ? TB(K).BD[m2][ay] : TB(K).BI[m2][ay], X[m1], Y[m1][m2]);
+        }
+        int m = 0;
+#pragma unroll
+        for (int d = 0; d < K; ++d)
+#pragma unroll
+          for (int m3 = 0; m3 <= d; ++m3)
+#pragma unroll
+            for (int m2 = 0; m2 <= d - m3; ++m2) {
+              const int m1 = d - m2 - m3;
+              Z[m] = fma(c == 2 ? TB(K).BD[m3][az] : TB(K).BI[m3][az], Y[m1][m2], Z[m]);
+              ++m;
+            }
+      }
+    }
+  }
+  double dot = 0.0;
+  if (valid) {
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+      const double o = sB * Z[m];
+      p[e * NM + m] = o;
+      if (dv) dot = fma(o, dv[e * NM + m], dot);
+    }
+  }
+  if (partial) grid_sum<BS>(dot, partial, counter, total);
+}
+
+// ------------------------------------------------------------------ row a7: B^T (element part)
+// E[c][a][e] = sB * sum_m prod_d M_cd[m_d][a_d] p_{e,m}
+template <int K>
+__global__ void k_BT_elem(const double* __restrict__ p, double* __restrict__ E, Geo G, double sB,
+                          const int* __restrict__ stop) {
+  constexpr int n1 = K + 1, NQ = Ord<K>::NQ, NM = Ord<K>::NM;
+  if (stop && *stop) return;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= G.n_el) return;
+  double P[K][K][K];  // P[m1][m2][m3] (only m1+m2+m3 <= K-1 used)
+  {
+    int m = 0;
+#pragma unroll
+    for (int d = 0; d < K; ++d)
+#pragma unroll
+      for (int m3 = 0; m3 <= d; ++m3)
+#pragma unroll
+        for (int m2 = 0; m2 <= d - m3; ++m2) {
+          P[d - m2 - m3][m2][m3] = p[e * NM + m];
+          ++m;
+        }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+#pragma unroll
+    for (int az = 0; az < n1; ++az) {
+      double Zt[K][K];
+#pragma unroll
+      for (int m1 = 0; m1 < K; ++m1)
+#pragma unroll
+        for (int m2 = 0; m2 < K - m1; ++m2) {
+          double t = 0.0;
+#pragma unroll
+          for (int m3 = 0; m3 < K - m1 - m2; ++m3)
+            t = fma(c == 2 ? TB(K).BD[m3][az] : TB(K).BI[m3][az], P[m1][m2][m3], t);
+          Zt[m1][m2] = t;
+        }
+#pragma unroll
+      for (int ay = 0; ay < n1; ++ay) {
+        double Yt[K];
+#pragma unroll
+        for (int m1 = 0; m1 < K; ++m1) {
+          double t = 0.0;
+#pragma unroll
+          for (int m2 = 0; m2 < K - m1; ++m2)
+            t = fma(c == 1 ? TB(K).BD[m2][ay] : TB(K).BI[m2][ay], Zt[m1][m2], t);
+          Yt[m1] = t;
+        }
+#pragma unroll
+        for (int ax = 0; ax < n1; ++ax) {
+          double t = 0.0;
+#pragma unroll
+          for (int m1 = 0; m1 < K; ++m1) t = fma(c == 0 ? TB(K).BD[m1][ax] : TB(K).BI[m1][ax], Yt[m1], t);
+          const int a = ax + n1 * (ay + n1 * az);
+          E[(int64_t)(c * NQ + a) * G.n_el + e] = sB * t;
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ row a5: A(mu) (k = 2 register kernel)
+// One thread per (element, velocity component c); the element's u_c lives in
+// registers through all sum-factorisation passes:
+//   U = (I x I x I) u_c  (GLL -> Gauss interpolation),
+//   g_cj = Dg_j U        (collocation derivative on the Gauss points),
+//   tau_cj = mut (g_cj + g_jc)   (g_jc exchanged in shared memory, one Gauss
+//                                 level at a time),
+//   y_c = (I^T x I^T x I^T) sum_j Dg_j^T tau_cj.
+// mut = mu w_q detJ (2/h)^2, so y_{c,a} = sum_q w_q detJ mu sum_j d_j phi_a
+// (d_j u_c + d_c u_j) = int 2 mu eps(u):eps(phi_a e_c)  (PAPER.md:148-151,
+// 986-990).  Output: element-local E[c][a][e].
+template <int K, int NE>
+__global__ void __launch_bounds__(3 * NE) k_A_reg(const double* __restrict__ mut, const double* __restrict__ u,
+                                                  double* __restrict__ E, Geo G, int nomask) {
+  constexpr int n1 = K + 1, NQ = Ord<K>::NQ, P = n1 * n1;
+  __shared__ double X[P][9][NE];
+  const int le = threadIdx.x % NE, c = threadIdx.x / NE;
+  const int64_t e = (int64_t)blockIdx.x * NE + le;
+  const bool valid = e < G.n_el;
+  int ex = 0, ey = 0, ez = 0;
+  if (valid) elem_xyz(e, G.N, ex, ey, ez);
+  double U[NQ];
+#pragma unroll
+  for (int az = 0; az < n1; ++az)
+#pragma unroll
+    for (int ay = 0; ay < n1; ++ay)
+#pragma unroll
+      for (int ax = 0; ax < n1; ++ax) {
+        const int gx = K * ex + ax, gy = K * ey + ay, gz = K * ez + az;
+        double v = 0.0;
+        if (valid && (nomask || !node_bnd(gx, gy, gz, G.nn1))) v = u[c * G.n_nodes + node_id(gx, gy, gz, G.nn1)];
+        U[(az * n1 + ay) * n1 + ax] = v;
+      }
+  // interpolate x, y, z (in place per pencil)
+#pragma unroll
+  for (int dir = 0; dir < 3; ++dir) {
+    const int st = dir == 0 ? 1 : (dir == 1 ? n1 : P);
+#pragma unroll
+    for (int o1 = 0; o1 < n1; ++o1)
+#pragma unroll
+      for (int o2 = 0; o2 < n1; ++o2) {
+        const int base = dir == 0 ? (o2 * n1 + o1) * n1 : (dir == 1 ? o2 * P + o1 : o2 * n1 + o1);
+        double v[n1];
+#pragma unroll
+        for (int j = 0; j < n1; ++j) v[j] = U[base + j * st];
+#pragma unroll
+        for (int i = 0; i < n1; ++i) {
+          double t = 0.0;
+#pragma unroll
+          for (int j = 0; j < n1; ++j) t = fma(TB(K).I[i][j], v[j], t);
+          U[base + i * st] = t;
+        }
+      }
+  }
+  double V[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) V[q] = 0.0;
+#pragma unroll
+  for (int iz = 0; iz < n1; ++iz) {
+    double gx[P], gy[P], gz[P];
+#pragma unroll
+    for (int iy = 0; iy < n1; ++iy)
+#pragma unroll
+      for (int ix = 0; ix < n1; ++ix) {
+        double tx = 0.0, ty = 0.0, tz = 0.0;
+#pragma unroll
+        for (int j = 0; j < n1; ++j) {
+          tx = fma(TB(K).Dg[ix][j], U[(iz * n1 + iy) * n1 + j], tx);
+          ty = fma(TB(K).Dg[iy][j], U[(iz * n1 + j) * n1 + ix], ty);
+          tz = fma(TB(K).Dg[iz][j], U[(j * n1 + iy) * n1 + ix], tz);
+        }
+        gx[iy * n1 + ix] = tx; gy[iy * n1 + ix] = ty; gz[iy * n1 + ix] = tz;
+      }
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      X[q][c * 3 + 0][le] = gx[q];
+      X[q][c * 3 + 1][le] = gy[q];
+      X[q][c * 3 + 2][le] = gz[q];
+    }
+    __syncthreads();
+    double Wx[P], Wy[P], Wz[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      const double mu = valid ? mut[e * NQ + iz * P + q] : 0.0;
+      Wx[q] = mu * (gx[q] + X[q][0 * 3 + c][le]);
+      Wy[q] = mu * (gy[q] + X[q][1 * 3 + c][le]);
+      Wz[q] = mu * (gz[q] + X[q][2 * 3 + c][le]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int iy = 0; iy < n1; ++iy)
+#pragma unroll
+      for (int jx = 0; jx < n1; ++jx) {
+        double t = V[(iz * n1 + iy) * n1 + jx];
+#pragma unroll
+        for (int ix = 0; ix < n1; ++ix) t = fma(TB(K).Dg[ix][jx], Wx[iy * n1 + ix], t);
+        V[(iz * n1 + iy) * n1 + jx] = t;
+      }
+#pragma unroll
+    for (int jy = 0; jy < n1; ++jy)
+#pragma unroll
+      for (int ix = 0; ix < n1; ++ix) {
+        double t = V[(iz * n1 + jy) * n1 + ix];
+#pragma unroll
+        for (int iy = 0; iy < n1; ++iy) t = fma(TB(K).Dg[iy][jy], Wy[iy * n1 + ix], t);
+        V[(iz * n1 + jy) * n1 + ix] = t;
+      }
+#pragma unroll
+    for (int jz = 0; jz < n1; ++jz)
+#pragma unroll
+      for (int q = 0; q < P; ++q) V[jz * P + q] = fma(TB(K).Dg[iz][jz], Wz[q], V[jz * P + q]);
+  }
+  // transposed interpolation z, y, x
+#pragma unroll
+  for (int dir = 2; dir >= 0; --dir) {
+    const int st = dir == 0 ? 1 : (dir == 1 ? n1 : P);
+#pragma unroll
+    for (int o1 = 0; o1 < n1; ++o1)
+#pragma unroll
+      for (int o2 = 0; o2 < n1; ++o2) {
+        const int base = dir == 0 ? (o2 * n1 + o1) * n1 : (dir == 1 ? o2 * P + o1 : o2 * n1 + o1);
+        double v[n1];
+#pragma unroll
+        for (int j = 0; j < n1; ++j) v[j] = V[base + j * st];
+#pragma unroll
+        for (int a = 0; a < n1; ++a) {
+          double t = 0.0;
+#pragma unroll
+          for (int j = 0; j < n1; ++j) t = fma(TB(K).I[j][a], v[j], t);
+          V[base + a * st] = t;
+        }
+      }
+  }
+  if (valid) {
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) E[(int64_t)(c * NQ + a) * G.n_el + e] = V[a];
+  }
+}
+
+// ------------------------------------------------------------------ row a5: A(mu) (generic slice kernel, k = 3, 4)
+// NE elements per block, n1 x n1 threads per element; the thread (a, b) owns
+// one pencil per pass and the third index is looped in registers; the passes
+// exchange through shared memory (same operator as k_A_reg).
+template <int K, int NE>
+__global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* __restrict__ mut,
+                                                                  const double* __restrict__ u,
+                                                                  double* __restrict__ E, Geo G, int nomask) {
+  constexpr int n1 = K + 1, NQ = Ord<K>::NQ, P = n1 * n1;
+  extern __shared__ double sm[];
+  const int le = threadIdx.x / P, t = threadIdx.x % P, ta = t % n1, tb = t / n1;
+  const int64_t e = (int64_t)blockIdx.x * NE + le;
+  const bool valid = e < G.n_el;
+  double* A0 = sm + (size_t)le * 12 * NQ;
+  double* A1 = A0 + 3 * NQ;
+  double* GX = A1 + 3 * NQ;
+  double* GY = GX + 3 * NQ;
+#define IX(c, z, y, x) ((c)*NQ + ((z)*n1 + (y)) * n1 + (x))
+  int ex = 0, ey = 0, ez = 0;
+  if (valid) elem_xyz(e, G.N, ex, ey, ez);
+  // S1 load: thread (x = ta, y = tb)
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int z = 0; z < n1; ++z) {
+      const int gx = K * ex + ta, gy = K * ey + tb, gz = K * ez + z;
+      double v = 0.0;
+      if (valid && (nomask || !node_bnd(gx, gy, gz, G.nn1))) v = u[c * G.n_nodes + node_id(gx, gy, gz, G.nn1)];
+      A0[IX(c, z, tb, ta)] = v;
+    }
+  __syncthreads();
+  // S2 x-interp: thread (y = ta, z = tb)
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double v[n1];
+#pragma unroll
+    for (int j = 0; j < n1; ++j) v[j] = A0[IX(c, tb, ta, j)];
+#pragma unroll
+    for (int i = 0; i < n1; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < n1; ++j) s = fma(TB(K).I[i][j], v[j], s);
+      A1[IX(c, tb, ta, i)] = s;
+    }
+  }
+  __syncthreads();
+  // S3 y-interp: thread (x = ta, z = tb)
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double v[n1];
+#pragma unroll
+    for (int j = 0; j < n1; ++j) v[j] = A1[IX(c, tb, j, ta)];
+#pragma unroll
+    for (int i = 0; i < n1; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < n1; ++j) s = fma(TB(K).I[i][j], v[j], s);
+      A0[IX(c, tb, i, ta)] = s;
+    }
+  }
+  __syncthreads();
+  // S4 z-interp (+ z-derivative in registers): thread (x = ta, y = tb)
+  double Gz[3][n1];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double v[n1], Uz[n1];
+#pragma unroll
+    for (int j = 0; j < n1; ++j) v[j] = A0[IX(c, j, tb, ta)];
+#pragma unroll
+    for (int i = 0; i < n1; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < n1; ++j) s = fma(TB(K).I[i][j], v[j], s);
+      Uz[i] = s;
+      A1[IX(c, i, tb, ta)] = s;
+    }
+#pragma unroll
+    for (int i = 0; i < n1; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < n1; ++j) s = fma(TB(K).Dg[i][j], Uz[j], s);
+      Gz[c][i] = s;
+    }
+  }
+  __syncthreads();
+  // S5 x-derivative: thread (y = ta, z = tb); y-derivative: thread (x = ta, z = tb)
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double v[n1], w[n1];
+#pragma unroll
+    for (int j = 0; j < n1; ++j) { v[j] = A1[IX(c, tb, ta, j)]; w[j] = A1[IX(c, tb, j, ta)]; }
+#pragma unroll
+    for (int i = 0; i < n1; ++i) {
+      double s = 0.0, r = 0.0;
+#pragma unroll
+      for (int j = 0; j < n1; ++j) { s = fma(TB(K).Dg[i][j], v[j], s); r = fma(TB(K).Dg[i][j], w[j], r); }
+      GX[IX(c, tb, ta, i)] = s;
+      GY[IX(c, tb, i, ta)] = r;
+    }
+  }
+  __syncthreads();
+  // S6 tau at the Gauss points of column (x = ta, y = tb)
+  double Wz[3][n1];
+#pragma unroll
+  for (int iz = 0; iz < n1; ++iz) {
+    double g[3][3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      g[c][0] = GX[IX(c, iz, tb, ta)];
+      g[c][1] = GY[IX(c, iz, tb, ta)];
+      g[c][2] = Gz[c][iz];
+    }
+    const double mu = valid ? mut[e * NQ + (iz * n1 + tb) * n1 + ta] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      GX[IX(c, iz, tb, ta)] = mu * (g[c][0] + g[0][c]);
+      GY[IX(c, iz, tb, ta)] = mu * (g[c][1] + g[1][c]);
+      Wz[c][iz] = mu * (g[c][2] + g[2][c]);
+    }
+  }
+  __syncthreads();
+  // S7 x-back: thread (y = ta, z = tb)
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double v[n1];
+#pragma unroll
+    for (int i = 0; i < n1; ++i) v[i] = GX[IX(c, tb, ta, i)];
+#pragma unroll
+    for (int j = 0; j < n1; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < n1; ++i) s = fma(TB(K).Dg[i][j], v[i], s);
+      A0[IX(c, tb, ta, j)] = s;
+    }
+  }
+  __syncthreads();
+  // S8 y-back: thread (x = ta, z = tb), read-modify-write of its own y-pencil
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double v[n1];
+#pragma unroll
+    for (int i = 0; i < n1; ++i) v[i] = GY[IX(c, tb, i, ta)];
+#pragma unroll
+    for (int j = 0; j < n1; ++j) {
+      double s = A0[IX(c, tb, j, ta)];
+#pragma unroll
+      for (int i = 0; i < n1; ++i) s = fma(TB(K).Dg[i][j], v[i], s);
+      A0[IX(c, tb, j, ta)] = s;
+    }
+  }
+  __syncthreads();
+  // S9 z-back + transposed z-interpolation: thread (x = ta, y = tb)
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double Vz[n1];
+#pragma unroll
+    for (int j = 0; j < n1; ++j) {
+      double s = A0[IX(c, j, tb, ta)];
+#pragma unroll
+      for (int i = 0; i < n1; ++i) s = fma(TB(K).Dg[i][j], Wz[c][i], s);
+      Vz[j] = s;
+    }
+#pragma unroll
+    for (int a = 0; a < n1; ++a) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < n1; ++j) s = fma(TB(K).I[j][a], Vz[j], s);
+      A1[IX(c, a, tb, ta)] = s;
+    }
+  }
+  __syncthreads();
+  // S10 transposed y-interpolation: thread (x = ta, z = tb)
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double v[n1];
+#pragma unroll
+    for (int j = 0; j < n1; ++j) v[j] = A1[IX(c, tb, j, ta)];
+#pragma unroll
+    for (int a = 0; a < n1; ++a) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < n1; ++j) s = fma(TB(K).I[j][a], v[j], s);
+      A0[IX(c, tb, a, ta)] = s;
+    }
+  }
+  __syncthreads();
+  // S11 transposed x-interpolation: thread (y = ta, z = tb) -> E
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double v[n1];
+#pragma unroll
+    for (int j = 0; j < n1; ++j) v[j] = A0[IX(c, tb, ta, j)];
+#pragma unroll
+    for (int a = 0; a < n1; ++a) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < n1; ++j) s = fma(TB(K).I[j][a], v[j], s);
+      if (valid) E[(int64_t)(c * NQ + (tb * n1 + ta) * n1 + a) * G.n_el + e] = s;
+    }
+  }
+#undef IX
+}
+
+// ------------------------------------------------------------------ setup: mu prescale + positivity
+// mut = mu * w_qx w_qy w_qz * detJ * (2/h)^2 = mu * w_q * h/2.
+template <int K>
+__global__ void k_prescale(const double* __restrict__ mu, double* __restrict__ mut, int64_t n, double hs,
+                           unsigned long long* bad) {
+  constexpr int n1 = K + 1, NQ = Ord<K>::NQ;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int q = (int)(i % NQ);
+  const double m = mu[i];
+  if (!(m > 0.0) || !isfinite(m)) atomicAdd(bad, 1ull);
+  const double wq = TB(K).w[q % n1] * TB(K).w[(q / n1) % n1] * TB(K).w[q / (n1 * n1)];
+  mut[i] = m * wq * hs;
+}
+
+// ------------------------------------------------------------------ row a3: lumped weighted masses
+// L[a][e] = detJ sum_q sqrt(mu_q) phi_a(xi_q) w_q  (eq:lumping with the
+// all-ones coefficient vector, weighted by w = sqrt(mu), PAPER.md:310-323,
+// 446-454).
+template <int K>
+__global__ void k_lump_elem(const double* __restrict__ mu, double* __restrict__ L, Geo G, double detJ) {
+  constexpr int n1 = K + 1, NQ = Ord<K>::NQ;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= G.n_el) return;
+  double s[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) s[q] = sqrt(mu[e * NQ + q]);
+#pragma unroll 1
+  for (int a = 0; a < NQ; ++a) {
+    const int ax = a % n1, ay = (a / n1) % n1, az = a / (n1 * n1);
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int qx = q % n1, qy = (q / n1) % n1, qz = q / (n1 * n1);
+      acc = fma(s[q], TB(K).W1[ax][qx] * TB(K).W1[ay][qy] * TB(K).W1[az][qz], acc);
+    }
+    L[(int64_t)a * G.n_el + e] = detJ * acc;
+  }
+}
+
+// C[g] = sum_{e ni g} a_l(e) L[a(e,g)][e] (eq:bdramp PAPER.md:2232-2245), ascending e.
+// Xinv = mask / X; nonpositive interior entries counted (integer atomics).
+template <int K>
+__global__ void k_lump_node(const double* __restrict__ L, double a_l, double a_r, double* Cw, double* Dw,
+                            double* Cinv, double* Dinv, unsigned long long* nonpos, Geo G) {
+  constexpr int n1 = K + 1;
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G.n_nodes) return;
+  const int nn1 = G.nn1;
+  int gg[3] = {(int)(g % nn1), (int)((g / nn1) % nn1), (int)(g / ((int64_t)nn1 * nn1))};
+  int pe[3][2], pa[3][2], pc[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    int q = gg[d] / K, r = gg[d] % K;
+    pc[d] = 0;
+    if (r != 0) { pe[d][0] = q; pa[d][0] = r; pc[d] = 1; }
+    else {
+      if (q - 1 >= 0) { pe[d][pc[d]] = q - 1; pa[d][pc[d]] = K; pc[d]++; }
+      if (q < G.N) { pe[d][pc[d]] = q; pa[d][pc[d]] = 0; pc[d]++; }
+    }
+  }
+  double cl = 0.0, cr = 0.0;
+  for (int iz = 0; iz < pc[2]; ++iz)
+    for (int iy = 0; iy < pc[1]; ++iy)
+      for (int ix = 0; ix < pc[0]; ++ix) {
+        const int ex = pe[0][ix], ey = pe[1][iy], ez = pe[2][iz];
+        const int64_t e = ex + (int64_t)G.N * (ey + (int64_t)G.N * ez);
+        const int a = pa[0][ix] + n1 * (pa[1][iy] + n1 * pa[2][iz]);
+        const bool onb = ex == 0 || ey == 0 || ez == 0 || ex == G.N - 1 || ey == G.N - 1 || ez == G.N - 1;
+        const double l = L[(int64_t)a * G.n_el + e];
+        cl += (onb ? a_l : 1.0) * l;
+        cr += (onb ? a_r : 1.0) * l;
+      }
+  const bool b = node_bnd(gg[0], gg[1], gg[2], nn1);
+  Cw[g] = cl; Dw[g] = cr;
+  Cinv[g] = b ? 0.0 : 1.0 / cl;
+  Dinv[g] = b ? 0.0 : 1.0 / cr;
+  if (!b && cl <= 0.0) atomicAdd(nonpos + 0, 1ull);
+  if (!b && cr <= 0.0) atomicAdd(nonpos + 1, 1ull);
+}
+
+// ------------------------------------------------------------------ row a4: Jacobi diagonals
+// diag(K)_{e,m} = sum_{c,a} B_e[m,(c,a)]^2 X^-1[g(e,a)]; stores Minv = 1/diag too.
+template <int K>
+__global__ void k_jacobi(const double* __restrict__ Cinv, const double* __restrict__ Dinv, double* dL, double* dR,
+                         double* mL, double* mR, Geo G, double sB) {
+  constexpr int n1 = K + 1, NQ = Ord<K>::NQ, NM = Ord<K>::NM;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= G.n_el) return;
+  int ex, ey, ez;
+  elem_xyz(e, G.N, ex, ey, ez);
+  int mm[NM][3];
+  {
+    int m = 0;
+    for (int d = 0; d < K; ++d)
+      for (int m3 = 0; m3 <= d; ++m3)
+        for (int m2 = 0; m2 <= d - m3; ++m2) { mm[m][0] = d - m2 - m3; mm[m][1] = m2; mm[m][2] = m3; ++m; }
+  }
+  double sl[NM], sr[NM];
+#pragma unroll
+  for (int m = 0; m < NM; ++m) { sl[m] = 0.0; sr[m] = 0.0; }
+#pragma unroll 1
+  for (int c = 0; c < 3; ++c)
+#pragma unroll 1
+    for (int a = 0; a < NQ; ++a) {
+      const int ax = a % n1, ay = (a / n1) % n1, az = a / (n1 * n1);
+      const int64_t g = node_id(K * ex + ax, K * ey + ay, K * ez + az, G.nn1);
+      const double xl = Cinv[g], xr = Dinv[g];
+#pragma unroll
+      for (int m = 0; m < NM; ++m) {
+        const double fx = c == 0 ? TB(K).BD[mm[m][0]][ax] : TB(K).BI[mm[m][0]][ax];
+        const double fy = c == 1 ? TB(K).BD[mm[m][1]][ay] : TB(K).BI[mm[m][1]][ay];
+        const double fz = c == 2 ? TB(K).BD[mm[m][2]][az] : TB(K).BI[mm[m][2]][az];
+        const double b = sB * (fx * fy * fz);
+        sl[m] = fma(b * b, xl, sl[m]);
+        sr[m] = fma(b * b, xr, sr[m]);
+      }
+    }
+#pragma unroll
+  for (int m = 0; m < NM; ++m) {
+    dL[e * NM + m] = sl[m]; dR[e * NM + m] = sr[m];
+    // Jacobi with the pseudo-inverse of diag K (R11): a zero diagonal
+    // entry means an identically zero row of K (N = 1), Minv = 0 there.
+    mL[e * NM + m] = sl[m] != 0.0 ? 1.0 / sl[m] : 0.0;
+    mR[e * NM + m] = sr[m] != 0.0 ? 1.0 / sr[m] : 0.0;
+  }
+}
+
+// ------------------------------------------------------------------ vectors, projection, PCG
+constexpr int VBS = 256;  // vector-kernel block size; grid fixed per context -> fixed reduction order
+
+// sum of the constant-mode entries v[e*nm] (projection, R10)
+__global__ void __launch_bounds__(VBS) k_mode0_sum(const double* __restrict__ v, int64_t n_el, int nm,
+                                                   double* partial, unsigned* counter, double* total) {
+  double s = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * VBS + threadIdx.x; e < n_el; e += (int64_t)gridDim.x * VBS) s += v[e * nm];
+  grid_sum<VBS>(s, partial, counter, total);
+}
+// out = P in: copy, then subtract the mean of the mode-0 entries from them.
+__global__ void k_project(const double* __restrict__ in, double* __restrict__ out, int64_t n, int nm,
+                          int64_t n_el, const double* __restrict__ sum) {
+  const double mean = *sum / (double)n_el;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (i % nm == 0) ? in[i] - mean : in[i];
+}
+
+// x = 0; r = b; p = Minv r; rz = <r, Minv r>
+__global__ void __launch_bounds__(VBS) k_pcg_init(const double* __restrict__ b, double* x, double* r, double* p,
+                                                  const double* __restrict__ Minv, int64_t n, double* partial,
+                                                  unsigned* counter, double* rz_hist, int* stop) {
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS) {
+    const double bi = b[i], zi = Minv[i] * bi;
+    x[i] = 0.0; r[i] = bi; p[i] = zi;
+    s = fma(bi, zi, s);
+  }
+  if (grid_sum<VBS>(s, partial, counter, rz_hist)) stop[0] = (rz_hist[0] == 0.0) ? 1 : 0;
+}
+
+// iteration it, after q = K p and pq[it] = <p, q>:
+//   alpha = rz/pq; x += alpha p; r -= alpha q; rzn = <r, Minv r>
+__global__ void __launch_bounds__(VBS) k_pcg_upd1(double* x, double* r, const double* __restrict__ p,
+                                                  const double* __restrict__ q, const double* __restrict__ Minv,
+                                                  int64_t n, const double* pq, const double* rz, double* rzn,
+                                                  const int* stop, double* partial, unsigned* counter) {
+  if (*stop) return;
+  const double pqv = *pq;
+  if (pqv == 0.0) return;
+  const double alpha = *rz / pqv;
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    s = fma(ri, Minv[i] * ri, s);
+  }
+  grid_sum<VBS>(s, partial, counter, rzn);
+}
+
+//   beta = rzn/rz; p = Minv r + beta p; rz_{it+1} = rzn; stop_{it+1}
+__global__ void k_pcg_upd2(const double* __restrict__ r, double* p, const double* __restrict__ Minv, int64_t n,
+                           const double* pq, const double* rz, const double* rzn, double* rz_next,
+                           const int* stop, int* stop_next) {
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  if (*stop || *pq == 0.0) {
+    if (lead) { *stop_next = 1; *rz_next = *rz; }
+    return;
+  }
+  const double rzv = *rzn, beta = rzv / *rz;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], Minv[i] * r[i]);
+  if (lead) { *rz_next = rzv; *stop_next = (rzv == 0.0) ? 1 : 0; }
+}
+
+}  // namespace wb

@@ -1,0 +1,170 @@
+"""GPU tests of the C-ABI contract (error codes, masking, aliasing, host entry)
+and full-size (BASELINE.json C4/C5) parity in the launch configuration
+bench.py times: complete B / B^T / A vectors where the oracle is fast enough,
+sampled A outputs otherwise, and size-independent properties."""
+import numpy as np
+import pytest
+
+import synth
+from tests.gpu_common import Pair, dev, empty, host, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def test_errors():
+    import torch
+    from paper_1607_03936_b200 import Context, WBError
+    ctx = Context(3, 2)
+    u = empty(ctx.n_v)
+    with pytest.raises(WBError, match="WB_ESTATE"):
+        ctx.apply_A(u, empty(ctx.n_v))
+    mu = torch.ones(ctx.n_el * ctx.n_q, dtype=torch.float64, device="cuda")
+    mu[5] = 0.0
+    with pytest.raises(WBError, match="WB_ENONPOS_MU"):
+        ctx.set_viscosity(mu)
+    mu[5] = float("nan")
+    with pytest.raises(WBError, match="WB_ENONPOS_MU"):
+        ctx.set_viscosity(mu)
+    mu[5] = 1.0
+    with pytest.raises(WBError, match="WB_EINVAL"):
+        ctx.set_viscosity(mu, 0.5, 1.0)
+    ctx.set_viscosity(mu)
+    with pytest.raises(WBError, match="WB_EALIAS"):
+        ctx.apply_A(u, u)
+    with pytest.raises(WBError, match="WB_EINVAL"):
+        ctx.apply_K(2, empty(ctx.n_p), empty(ctx.n_p))
+    with pytest.raises(WBError, match="WB_EINVAL"):
+        Context(0, 2)
+    with pytest.raises(WBError, match="WB_EINVAL"):
+        Context(4, 5)
+
+
+def test_strict_lump_flag():
+    from paper_1607_03936_b200 import WB_STRICT_LUMP, WBError
+    p = Pair("C1", setup=False, flags=WB_STRICT_LUMP)
+    with pytest.raises(WBError, match="WB_ENONPOS_LUMP"):
+        p.ctx.set_viscosity(p.mu)
+
+
+def test_boundary_inputs_ignored():
+    p = Pair("C2", N=6)
+    u = p.inp["u"].copy()
+    mask = p.o.boundary_mask().astype(bool)
+    u2 = u.copy()
+    u2[mask] = 1e30
+    for op, n in (("apply_A", p.ctx.n_v), ("apply_B", p.ctx.n_p)):
+        a = host(getattr(p.ctx, op)(dev(u), empty(n)))
+        b = host(getattr(p.ctx, op)(dev(u2), empty(n)))
+        assert np.array_equal(a, b)
+
+
+def test_nomask_rigid_modes():
+    """Without the mask, A annihilates the six rigid modes (closed form)."""
+    from paper_1607_03936_b200 import WB_DEBUG_NOMASK
+    for cfg, N in (("C2", 4), ("C4", 2)):
+        p = Pair(cfg, N=N, flags=WB_DEBUG_NOMASK)
+        k, n = p.k, p.k * N + 1
+        g = np.linspace(0, 1, n)  # GLL nodes are symmetric; positions only matter via linearity
+        from oracle import Oracle
+        xn = Oracle(1, k).tables()["xn"]
+        line = np.concatenate([[(e + (xn[a] + 1) / 2) / N for a in range(k)] for e in range(N)] + [[1.0]])
+        Z, Y, X = np.meshgrid(line, line, line, indexing="ij")
+        x, y, z = X.ravel(), Y.ravel(), Z.ravel()
+        zero = np.zeros_like(x)
+        one = np.ones_like(x)
+        modes = [np.concatenate(m) for m in ((one, zero, zero), (zero, one, zero), (zero, zero, one),
+                                             (-y, x, zero), (-z, zero, x), (zero, -z, y))]
+        ref = np.linalg.norm(host(p.ctx.apply_A(dev(p.inp["u"]), empty(p.ctx.n_v))))
+        for m in modes:
+            r = host(p.ctx.apply_A(dev(m), empty(p.ctx.n_v)))
+            assert np.linalg.norm(r) <= 1e-12 * ref * np.linalg.norm(m) / np.linalg.norm(p.inp["u"])
+
+
+def test_hotpath_host_equals_device():
+    import torch
+    p = Pair("C2", N=8, setup=False)
+    c = p.ctx
+    it = 10
+    outs_d = [empty(c.n_v), empty(c.n_p), empty(c.n_v), empty(c.n_p)]
+    c.hotpath(p.mu, dev(p.inp["u"]), dev(p.inp["p"]), it, *outs_d)
+    outs_h = [np.empty(c.n_v), np.empty(c.n_p), np.empty(c.n_v), np.empty(c.n_p)]
+    c.hotpath_host(p.inp["mu_q"], p.inp["u"], p.inp["p"], it, *outs_h)
+    for a, b in zip(outs_d, outs_h):
+        assert np.array_equal(host(a), b)
+    pin = [torch.empty(n, dtype=torch.float64).pin_memory() for n in (c.n_v, c.n_p, c.n_v, c.n_p)]
+    c.hotpath_host(torch.from_numpy(p.inp["mu_q"]).pin_memory(), torch.from_numpy(p.inp["u"]).pin_memory(),
+                   torch.from_numpy(p.inp["p"]).pin_memory(), it, *pin)
+    for a, b in zip(outs_d, pin):
+        assert np.array_equal(host(a), b.numpy())
+
+
+def test_amplified_boundary_weights():
+    """a_l, a_r != 1 (eq:bdramp): lumped diagonals and wBFBT parity."""
+    p = Pair("C2", a_l=1.0, a_r=4.0)
+    st = p.ost
+    Cw, Dw = empty(p.ctx.n_nodes), empty(p.ctx.n_nodes)
+    p.ctx.get_lumped(Cw, Dw)
+    assert np.max(np.abs(host(Dw) - st["Dw"])) <= 1e-13 * np.max(np.abs(st["Dw"]))
+    assert np.max(np.abs(host(Cw) - st["Cw"])) <= 1e-13 * np.max(np.abs(st["Cw"]))
+    z = host(p.ctx.apply_wbfbt(dev(p.inp["p"]), empty(p.ctx.n_p), 20))
+    assert rel_l2(z, p.o.wbfbt(p.inp["p"], 20)) <= 1e-8
+
+
+# ------------------------------------------------------------------ full BASELINE sizes
+@pytest.fixture(scope="module", params=["C4", "C5"])
+def full(request):
+    return Pair(request.param)
+
+
+def test_full_size_B_BT(full):
+    u, p = full.inp["u"], full.inp["p"]
+    assert rel_l2(host(full.ctx.apply_B(dev(u), empty(full.ctx.n_p))), full.o.apply_B(u)) <= 1e-11
+    assert rel_l2(host(full.ctx.apply_BT(dev(p), empty(full.ctx.n_v))), full.o.apply_BT(p)) <= 1e-11
+
+
+def test_full_size_A_sampled(full):
+    u = full.inp["u"]
+    y = host(full.ctx.apply_A(dev(u), empty(full.ctx.n_v)))
+    rng = np.random.default_rng(3)
+    dofs = rng.choice(full.ctx.n_v, 400, replace=False)
+    ys = full.o.apply_A_sampled(full.inp["mu_q"], u, dofs)
+    scale = np.linalg.norm(y) / np.sqrt(full.ctx.n_v)
+    assert np.max(np.abs(y[dofs] - ys)) <= 1e-11 * max(scale, 1e-300) * 10
+    # relative per sample, where the sample is not tiny
+    big = np.abs(ys) > 1e-3 * scale
+    assert np.max(np.abs(y[dofs][big] - ys[big]) / np.abs(ys[big])) <= 1e-9
+
+
+def test_full_size_lumped(full):
+    Cw = empty(full.ctx.n_nodes)
+    full.ctx.get_lumped(Cw)
+    o = full.ost["Cw"]
+    assert np.max(np.abs(host(Cw) - o)) <= 1e-13 * np.max(np.abs(o))
+    assert full.ctx.query("n_nonpos_Cw") == full.ost["n_nonpos_Cw"] == 0
+
+
+def test_full_size_pcg_prefix(full):
+    b = full.inp["p"]
+    st = full.ost
+    x = host(full.ctx.poisson_pcg(1, dev(b), empty(full.ctx.n_p), 5))
+    assert rel_l2(x, full.o.poisson(st["Dinv"], st["diagKr"], b, 5)) <= 1e-12
+
+
+def test_full_size_wbfbt_properties(full):
+    """At full size with the config's PCG count: finite, projected, deterministic,
+    and the Poisson relative residuals agree with the oracle's within 2x
+    (SURVEY 8(c) 12(ii))."""
+    c = full.ctx
+    it = full.cfg.iters
+    r = dev(full.inp["p"])
+    z1 = host(c.apply_wbfbt(r, empty(c.n_p), it))
+    z2 = host(c.apply_wbfbt(r, empty(c.n_p), it))
+    assert np.all(np.isfinite(z1)) and np.array_equal(z1, z2)
+    assert abs(z1[::full.o.n_m].sum()) <= 1e-10 * np.abs(z1[::full.o.n_m]).sum()
+    st = full.ost
+    b = full.o.project(full.inp["p"])
+    xg = host(c.poisson_pcg(1, dev(b), empty(c.n_p), it))
+    rg = full.o.poisson_relres(st["Dinv"], b, xg)
+    xo = full.o.poisson(st["Dinv"], st["diagKr"], b, it)
+    ro = full.o.poisson_relres(st["Dinv"], b, xo)
+    assert rg <= 2 * ro and ro <= 2 * rg
