@@ -146,6 +146,11 @@ wb_status wb_get_jacobi(wb_ctx* ctx, double* diagKl, double* diagKr);
 /* Scalar queries: "n_nonpos_Cw", "n_nonpos_Dw", "n_el", "n_p", "n_v",
  * "kernel_launches" (launches since create), "last_pcg_stop_iter". */
 wb_status wb_query(wb_ctx* ctx, const char* key, double* value);
+/* Tuning knobs (results are identical up to rounding for every setting):
+ * "a_tile" (k = 2 A tile shape: 0 = 4x4x2 elements, 1 = 4x4x4),
+ * "graph" (1 = replay the Poisson / wBFBT launch sequence as a CUDA graph,
+ * default; 0 = plain launches).  WB_EINVAL for an unknown key or value. */
+wb_status wb_set_option(wb_ctx* ctx, const char* key, double value);
 /* Synchronise the context stream; surfaces asynchronous CUDA errors. */
 wb_status wb_sync(wb_ctx* ctx);
 

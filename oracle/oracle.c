@@ -511,13 +511,21 @@ static void pcg_step(or_ctx* c, const double* Xinv, const double* Minv, double* 
   if (ab) { ab[0] = alpha; ab[1] = beta; }
 }
 
-/* x = PCG(K_side, b) with K_side = B Xinv B^T, Minv = 1/diag(K_side). */
+/* Minv = pseudo-inverse of diag(K) (R11): 1/d_i, except 0 where |d_i| <= 1e-13 max|d|
+ * (a row of K that vanishes up to rounding, e.g. the constant mode when N = 1). */
+static void jacobi_minv(const double* diagK, double* Minv, int64_t n) {
+  double dmax = 0.0;
+  for (int64_t i = 0; i < n; ++i) dmax = fabs(diagK[i]) > dmax ? fabs(diagK[i]) : dmax;
+  for (int64_t i = 0; i < n; ++i) Minv[i] = fabs(diagK[i]) > 1e-13 * dmax ? 1.0 / diagK[i] : 0.0;
+}
+
+/* x = PCG(K_side, b) with K_side = B Xinv B^T, Minv = 1/diag(K_side) (R11). */
 void or_pcg(or_ctx* c, const double* Xinv, const double* diagK, const double* b, double* x, int iters) {
   const int64_t n = c->n_p;
   double* r = (double*)malloc(sizeof(double) * n); double* z = (double*)malloc(sizeof(double) * n);
   double* p = (double*)malloc(sizeof(double) * n); double* q = (double*)malloc(sizeof(double) * n);
   double* Minv = (double*)malloc(sizeof(double) * n); double* tv = (double*)malloc(sizeof(double) * c->n_v);
-  for (int64_t i = 0; i < n; ++i) Minv[i] = diagK[i] != 0.0 ? 1.0 / diagK[i] : 0.0; /* R11: pseudo-inverse of diag K */
+  jacobi_minv(diagK, Minv, n);
   for (int64_t i = 0; i < n; ++i) { x[i] = 0.0; r[i] = b[i]; z[i] = Minv[i] * r[i]; p[i] = z[i]; }
   double rz = dot(r, z, n);
   for (int it = 0; it < iters; ++it) {
@@ -534,7 +542,7 @@ void or_pcg_step(or_ctx* c, const double* Xinv, const double* diagK, double* x, 
   const int64_t n = c->n_p;
   double* z = (double*)malloc(sizeof(double) * n); double* q = (double*)malloc(sizeof(double) * n);
   double* Minv = (double*)malloc(sizeof(double) * n); double* tv = (double*)malloc(sizeof(double) * c->n_v);
-  for (int64_t i = 0; i < n; ++i) Minv[i] = diagK[i] != 0.0 ? 1.0 / diagK[i] : 0.0; /* R11: pseudo-inverse of diag K */
+  jacobi_minv(diagK, Minv, n);
   pcg_step(c, Xinv, Minv, x, r, p, rz, z, q, tv, NULL);
   free(z); free(q); free(Minv); free(tv);
 }

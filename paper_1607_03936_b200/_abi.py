@@ -47,6 +47,7 @@ SYMBOLS = [
     ("wb_get_lumped", _i, [_vp, _vp, _vp, _vp, _vp]),
     ("wb_get_jacobi", _i, [_vp, _vp, _vp]),
     ("wb_query", _i, [_vp, C.c_char_p, C.POINTER(_d)]),
+    ("wb_set_option", _i, [_vp, C.c_char_p, _d]),
     ("wb_sync", _i, [_vp]),
 ]
 
@@ -166,6 +167,9 @@ class Context:
         v = C.c_double()
         self._check(self._L.wb_query(self._h, key.encode(), C.byref(v)))
         return v.value
+
+    def set_option(self, key: str, value: float):
+        self._check(self._L.wb_set_option(self._h, key.encode(), float(value)))
 
     # -- row a1
     def get_dofmap(self, out):

@@ -81,6 +81,61 @@ __device__ __forceinline__ bool grid_sum(double v, double* partial, unsigned* co
   return threadIdx.x == 0;
 }
 
+// max |v| over the grid (same last-block pattern)
+template <int BS>
+__device__ __forceinline__ double block_max(double v) {
+  __shared__ double sw[BS / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sw[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (w == 0) {
+    s = (l < BS / 32) ? sw[l] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_down_sync(0xffffffffu, s, o));
+  }
+  __syncthreads();
+  return s;
+}
+
+template <int BS>
+__global__ void __launch_bounds__(BS) k_absmax(const double* __restrict__ v, int64_t n, double* partial,
+                                               unsigned* counter, double* total) {
+  __shared__ bool s_last;
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * BS + threadIdx.x; i < n; i += (int64_t)gridDim.x * BS) m = fmax(m, fabs(v[i]));
+  m = block_max<BS>(m);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = m;
+    __threadfence();
+    s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double a = 0.0;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += BS) a = fmax(a, __ldcg(partial + i));
+  a = block_max<BS>(a);
+  if (threadIdx.x == 0) { *total = a; *counter = 0u; }
+}
+
+// Jacobi preconditioner with the pseudo-inverse of diag K (R11):
+// entries that vanish up to rounding, |d| <= 1e-13 max|d| (a numerically zero
+// row of K, e.g. the constant mode on the N = 1 mesh), get Minv = 0.
+// d element-major (ABI layout), minv mode-major (PCG layout): minv[m*ne + e].
+__global__ void k_minv(const double* __restrict__ d, double* __restrict__ minv, int64_t ne, int nm,
+                       const double* __restrict__ dmax) {
+  const double thr = 1e-13 * *dmax;
+  const int64_t n = ne * nm;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / ne, e = i % ne;
+    const double v = d[e * nm + m];
+    minv[i] = fabs(v) > thr ? 1.0 / v : 0.0;
+  }
+}
+
 // ------------------------------------------------------------------ row a1
 template <int K>
 __global__ void k_dofmap(int64_t* map, Geo G) {
@@ -156,7 +211,9 @@ template <int K, int BS>
 __global__ void __launch_bounds__(BS) k_B(const double* __restrict__ u, const double* __restrict__ xs,
                                           double* __restrict__ p, Geo G, double sB, int nomask,
                                           const int* __restrict__ stop, const double* __restrict__ dv,
-                                          double* partial, unsigned* counter, double* total) {
+                                          double* partial, unsigned* counter, double* total, int64_t se,
+                                          int64_t sm) {
+  // output layout p[e*se + m*sm]: (NM, 1) element-major (ABI), (1, n_el) mode-major (PCG)
   constexpr int n1 = K + 1, NM = Ord<K>::NM;
   if (stop && *stop) return;
   const int64_t e = (int64_t)blockIdx.x * BS + threadIdx.x;
@@ -222,8 +279,8 @@ __global__ void __launch_bounds__(BS) k_B(const double* __restrict__ u, const do
 #pragma unroll
     for (int m = 0; m < NM; ++m) {
       const double o = sB * Z[m];
-      p[e * NM + m] = o;
-      if (dv) dot = fma(o, dv[e * NM + m], dot);
+      p[e * se + m * sm] = o;
+      if (dv) dot = fma(o, dv[e * se + m * sm], dot);
     }
   }
   if (partial) grid_sum<BS>(dot, partial, counter, total);
@@ -233,7 +290,7 @@ __global__ void __launch_bounds__(BS) k_B(const double* __restrict__ u, const do
 // E[c][a][e] = sB * sum_m prod_d M_cd[m_d][a_d] p_{e,m}
 template <int K>
 __global__ void k_BT_elem(const double* __restrict__ p, double* __restrict__ E, Geo G, double sB,
-                          const int* __restrict__ stop) {
+                          const int* __restrict__ stop, int64_t se, int64_t sm) {
   constexpr int n1 = K + 1, NQ = Ord<K>::NQ, NM = Ord<K>::NM;
   if (stop && *stop) return;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -247,7 +304,7 @@ __global__ void k_BT_elem(const double* __restrict__ p, double* __restrict__ E, 
       for (int m3 = 0; m3 <= d; ++m3)
 #pragma unroll
         for (int m2 = 0; m2 <= d - m3; ++m2) {
-          P[d - m2 - m3][m2][m3] = p[e * NM + m];
+          P[d - m2 - m3][m2][m3] = p[e * se + m * sm];
           ++m;
         }
   }
@@ -752,12 +809,9 @@ __global__ void k_jacobi(const double* __restrict__ Cinv, const double* __restri
     }
 #pragma unroll
   for (int m = 0; m < NM; ++m) {
-    dL[e * NM + m] = sl[m]; dR[e * NM + m] = sr[m];
-    // Jacobi with the pseudo-inverse of diag K (R11): a zero diagonal
-    // entry means an identically zero row of K (N = 1), Minv = 0 there.
-    mL[e * NM + m] = sl[m] != 0.0 ? 1.0 / sl[m] : 0.0;
-    mR[e * NM + m] = sr[m] != 0.0 ? 1.0 / sr[m] : 0.0;
+    dL[e * NM + m] = sl[m]; dR[e * NM + m] = sr[m];  // Minv: k_minv (pseudo-inverse, R11)
   }
+  (void)mL; (void)mR;
 }
 
 // ------------------------------------------------------------------ vectors, projection, PCG
@@ -778,29 +832,55 @@ __global__ void k_project(const double* __restrict__ in, double* __restrict__ ou
     out[i] = (i % nm == 0) ? in[i] - mean : in[i];
 }
 
-// x = 0; r = b; p = Minv r; rz = <r, Minv r>
-__global__ void __launch_bounds__(VBS) k_pcg_init(const double* __restrict__ b, double* x, double* r, double* p,
-                                                  const double* __restrict__ Minv, int64_t n, double* partial,
-                                                  unsigned* counter, double* rz_hist, int* stop) {
+// ---- PCG, vectors mode-major v[m*ne + e]; iteration i:
+//   [stop_i] p_i = Minv r_i (+ beta_i p_{i-1}, beta_i = rz_i / rz_{i-1});  q = K p_i;
+//   pq_i = <p_i, q>; [pq_i == 0 -> stop]; alpha = rz_i / pq_i; x += alpha p_i;
+//   r -= alpha q; rz_{i+1} = <r, Minv r>; stop_{i+1} = (rz_{i+1} == 0).
+// This is the oracle's recurrence (or_pcg) with the direction update moved to
+// the top of the next iteration, so that it fuses into the K kernel.
+
+// init: r = P b (element-major b -> mode-major r, constant-mode mean removed
+// using bsum = sum_e b[e*nm]); x = 0; rz_0 = <r, Minv r>.
+__global__ void __launch_bounds__(VBS) k_pcg_init(const double* __restrict__ b, const double* __restrict__ bsum,
+                                                  double* x, double* r, const double* __restrict__ Minv, int64_t ne,
+                                                  int nm, double* partial, unsigned* counter, double* rz_hist,
+                                                  int* stop) {
+  const double mean = *bsum / (double)ne;
+  const int64_t n = ne * nm;
   double s = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS) {
-    const double bi = b[i], zi = Minv[i] * bi;
-    x[i] = 0.0; r[i] = bi; p[i] = zi;
-    s = fma(bi, zi, s);
+    const int64_t m = i / ne, e = i % ne;
+    const double bi = (m == 0) ? b[e * nm] - mean : b[e * nm + m];
+    x[i] = 0.0; r[i] = bi;
+    s = fma(bi, Minv[i] * bi, s);
   }
   if (grid_sum<VBS>(s, partial, counter, rz_hist)) stop[0] = (rz_hist[0] == 0.0) ? 1 : 0;
 }
 
-// iteration it, after q = K p and pq[it] = <p, q>:
-//   alpha = rz/pq; x += alpha p; r -= alpha q; rzn = <r, Minv r>
-__global__ void __launch_bounds__(VBS) k_pcg_upd1(double* x, double* r, const double* __restrict__ p,
-                                                  const double* __restrict__ q, const double* __restrict__ Minv,
-                                                  int64_t n, const double* pq, const double* rz, double* rzn,
-                                                  const int* stop, double* partial, unsigned* counter) {
+// direction update (generic-k path; the k = 2 path fuses it into k_K2_fused).
+// mode 0: p = Minv r; 1: p = Minv r + (rz[0]/rz[-1]) pin  (pout may equal pin).
+__global__ void k_pupd(double* pout, const double* pin, const double* __restrict__ r,
+                       const double* __restrict__ Minv, int64_t n, int mode, const double* rz, const int* stop) {
   if (*stop) return;
-  const double pqv = *pq;
-  if (pqv == 0.0) return;
-  const double alpha = *rz / pqv;
+  const double beta = mode == 1 ? rz[0] / rz[-1] : 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double z = Minv[i] * r[i];
+    pout[i] = mode == 1 ? fma(beta, pin[i], z) : z;
+  }
+}
+
+// alpha = rz_i / pq_i; x += alpha p; r -= alpha q; rz_{i+1} = <r, Minv r>; stop_{i+1}.
+// rz, pq, stop point at entry i of their histories.
+__global__ void __launch_bounds__(VBS) k_pcg_upd(double* x, double* r, const double* __restrict__ p,
+                                                 const double* __restrict__ q, const double* __restrict__ Minv,
+                                                 int64_t n, const double* pq, double* rz, int* stop,
+                                                 double* partial, unsigned* counter) {
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  if (*stop || *pq == 0.0) {
+    if (lead) { stop[1] = 1; rz[1] = rz[0]; }
+    return;
+  }
+  const double alpha = rz[0] / *pq;
   double s = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS) {
     x[i] = fma(alpha, p[i], x[i]);
@@ -808,22 +888,29 @@ __global__ void __launch_bounds__(VBS) k_pcg_upd1(double* x, double* r, const do
     r[i] = ri;
     s = fma(ri, Minv[i] * ri, s);
   }
-  grid_sum<VBS>(s, partial, counter, rzn);
+  if (grid_sum<VBS>(s, partial, counter, rz + 1)) stop[1] = (rz[1] == 0.0) ? 1 : 0;
 }
 
-//   beta = rzn/rz; p = Minv r + beta p; rz_{it+1} = rzn; stop_{it+1}
-__global__ void k_pcg_upd2(const double* __restrict__ r, double* p, const double* __restrict__ Minv, int64_t n,
-                           const double* pq, const double* rz, const double* rzn, double* rz_next,
-                           const int* stop, int* stop_next) {
-  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
-  if (*stop || *pq == 0.0) {
-    if (lead) { *stop_next = 1; *rz_next = *rz; }
-    return;
+// out (element-major) = P x (mode-major), xsum = sum of the constant-mode entries.
+__global__ void k_pcg_out(const double* __restrict__ x, const double* __restrict__ xsum, double* __restrict__ out,
+                          int64_t ne, int nm) {
+  const double mean = *xsum / (double)ne;
+  const int64_t n = ne * nm;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i / nm, m = i % nm;
+    const double v = x[m * ne + e];
+    out[i] = (m == 0) ? v - mean : v;
   }
-  const double rzv = *rzn, beta = rzv / *rz;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = fma(beta, p[i], Minv[i] * r[i]);
-  if (lead) { *rz_next = rzv; *stop_next = (rzv == 0.0) ? 1 : 0; }
+}
+
+// layout conversion element-major <-> mode-major (debug one-step entry)
+__global__ void k_transpose(const double* __restrict__ in, double* __restrict__ out, int64_t ne, int nm, int to_soa) {
+  const int64_t n = ne * nm;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / ne, e = i % ne;
+    if (to_soa) out[i] = in[e * nm + m];
+    else out[e * nm + m] = in[i];
+  }
 }
 
 }  // namespace wb

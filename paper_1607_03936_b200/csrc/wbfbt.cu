@@ -13,7 +13,7 @@
 #include <new>
 
 #include "../../include/wbfbt.h"
-#include "kernels.cuh"
+#include "kernels_k2.cuh"
 
 using namespace wb;
 
@@ -34,7 +34,14 @@ struct wb_ctx {
   // work vectors
   double* E = nullptr;                 // element-local velocity values, 3*nq*n_el
   double *tv = nullptr, *tw = nullptr;  // n_v
-  double *pr = nullptr, *pp = nullptr, *pq = nullptr;  // PCG r, p, q (n_p)
+  // PCG vectors, mode-major v[m*n_el + e]: x, r, p (double buffer), q
+  double *px = nullptr, *pr = nullptr, *pp = nullptr, *pp1 = nullptr, *pq = nullptr;
+  // CUDA graphs of the PCG iteration loop, keyed by (side, iters)
+  struct GraphEntry { int side = 0, iters = 0; long long n_launch = 0; cudaGraphExec_t exec = nullptr; };
+  static constexpr int MAX_GRAPHS = 8;
+  GraphEntry graphs[MAX_GRAPHS];
+  int n_graphs = 0;
+  cudaStream_t cap_stream = nullptr;
   double *s0 = nullptr, *s1 = nullptr, *s2 = nullptr;  // n_p scratch
   // scalars
   double* partial = nullptr;  // reduction partials
@@ -45,6 +52,14 @@ struct wb_ctx {
   unsigned long long* icount = nullptr;  // [0] bad mu, [1] nonpos Cw, [2] nonpos Dw
   int red_blocks = 0, max_partials = 0;
   double* stage = nullptr;  // wb_hotpath_host staging (lazily allocated)
+  // k = 2 tile-assembled A: face partials, flags, ticket counter
+  double* F = nullptr;
+  int* tflag = nullptr;
+  unsigned long long* ticket = nullptr;
+  unsigned long long ticket_base = 0;
+  int epoch = 0, n_tiles = 0;
+  int a_tile = 0;  // k = 2 A tile shape: 0 = 4x4x2 (96 threads), 1 = 4x4x4 (192 threads)
+  int use_graph = 1;
   long long launches = 0;
   char err[512] = {0};
 };
@@ -87,25 +102,29 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 }
 
 // scalar slots
-enum { S_SUM = 0, S_PQ1 = 1, S_NSCAL = 8 };
+// S_SUM..S_SUM+1: constant-mode sums; S_DMAX, S_DMAX+1: max|diag K_l|, max|diag K_r|; S_SCR: scratch dot
+enum { S_SUM = 0, S_DMAX = 2, S_SCR = 4, S_NSCAL = 8 };
+// rz_hist[i] = rz_i (i = 0..it_cap+1), pq_hist[i] = <p_i, K p_i>, stop[i]: iteration i is skipped
 inline double* rz_hist(wb_ctx* c) { return c->scal + S_NSCAL; }
-inline double* pq_hist(wb_ctx* c) { return c->scal + S_NSCAL + (c->it_cap + 1); }
-inline double* rzn_hist(wb_ctx* c) { return c->scal + S_NSCAL + 2 * (c->it_cap + 1); }
+inline double* pq_hist(wb_ctx* c) { return c->scal + S_NSCAL + (c->it_cap + 2); }
+
+void clear_graphs(wb_ctx* c);
 
 wb_status ensure_iters(wb_ctx* c, int iters) {
-  if (iters <= c->it_cap) return WB_OK;
+  if (iters + 2 <= c->it_cap) return WB_OK;
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  clear_graphs(c);
   if (c->scal) cudaFree(c->scal);
   if (c->stop) cudaFree(c->stop);
   c->scal = nullptr; c->stop = nullptr;
-  int cap = iters < 128 ? 128 : iters;
-  if (cudaMalloc(&c->scal, sizeof(double) * (S_NSCAL + 3 * (cap + 1))) != cudaSuccess ||
-      cudaMalloc(&c->stop, sizeof(int) * (cap + 1)) != cudaSuccess) {
+  int cap = iters + 2 < 128 ? 128 : iters + 2;
+  if (cudaMalloc(&c->scal, sizeof(double) * (S_NSCAL + 2 * (cap + 2))) != cudaSuccess ||
+      cudaMalloc(&c->stop, sizeof(int) * (cap + 2)) != cudaSuccess) {
     c->it_cap = 0;
     return set_err(c, WB_ENOMEM, "scalar workspace allocation failed");
   }
-  CUDA_TRY(c, cudaMemsetAsync(c->scal, 0, sizeof(double) * (S_NSCAL + 3 * (cap + 1)), c->stream));
-  CUDA_TRY(c, cudaMemsetAsync(c->stop, 0, sizeof(int) * (cap + 1), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->scal, 0, sizeof(double) * (S_NSCAL + 2 * (cap + 2)), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->stop, 0, sizeof(int) * (cap + 2), c->stream));
   c->it_cap = cap;
   return WB_OK;
 }
@@ -118,12 +137,7 @@ wb_status launch_A_t(wb_ctx* c, const double* u, double* out_E, int nomask) {
     k_A_reg<2, NE><<<nblk(c->n_el, NE), 3 * NE, 0, c->stream>>>(c->mut, u, out_E, c->G, nomask);
   } else {
     constexpr int NE = (K == 3) ? 8 : 5;
-    const size_t smem = (size_t)NE * 12 * Ord<K>::NQ * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      CUDA_TRY(c, cudaFuncSetAttribute(k_A_slice<K, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
+    const size_t smem = (size_t)NE * 12 * Ord<K>::NQ * sizeof(double);  // attribute set in configure_kernels
     k_A_slice<K, NE><<<nblk(c->n_el, NE), NE * (K + 1) * (K + 1), smem, c->stream>>>(c->mut, u, out_E, c->G, nomask);
   }
   LAUNCH_CHECK(c);
@@ -138,19 +152,53 @@ wb_status launch_gather_t(wb_ctx* c, const double* s, double* y, int nomask) {
 }
 
 template <int K>
-wb_status launch_BT_t(wb_ctx* c, const double* p, const int* stop) {
-  k_BT_elem<K><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(p, c->E, c->G, c->sB, stop);
+wb_status launch_BT_t(wb_ctx* c, const double* p, const int* stop, int64_t se, int64_t sm) {
+  k_BT_elem<K><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(p, c->E, c->G, c->sB, stop, se, sm);
   LAUNCH_CHECK(c);
   return WB_OK;
 }
 
 template <int K>
 wb_status launch_B_t(wb_ctx* c, const double* u, const double* xs, double* p, int nomask, const int* stop,
-                     const double* dv, double* total) {
+                     const double* dv, double* total, int64_t se, int64_t sm) {
   constexpr int BS = 128;
   k_B<K, BS><<<nblk(c->n_el, BS), BS, 0, c->stream>>>(u, xs, p, c->G, c->sB, nomask, stop, dv,
-                                                       dv ? c->partial : nullptr, c->counter, total);
+                                                       dv ? c->partial : nullptr, c->counter, total, se, sm);
   LAUNCH_CHECK(c);
+  return WB_OK;
+}
+
+// fused k = 2 Poisson operator (+ PCG direction update), see k2_fused.cuh
+template <int TX, int TY, int TZ, int MINB>
+wb_status launch_k2f_t(wb_ctx* c, const double* pold, double* pnew, const double* r, const double* Minv,
+                       const double* X, double* q, int mode, const double* rz, const int* stop, double* pq) {
+  const int N = c->N;
+  const int nt = ((N + TX - 1) / TX) * ((N + TY - 1) / TY) * ((N + TZ - 1) / TZ);
+  k_K2_fused<TX, TY, TZ, MINB><<<nt, TX * TY * TZ, FK2<TX, TY, TZ>::SMEM, c->stream>>>(
+      pold, pnew, r, Minv, X, q, c->G, c->sB, mode, rz, stop, c->partial, c->counter, pq);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+wb_status run_k2f(wb_ctx* c, const double* pold, double* pnew, const double* r, const double* Minv, const double* X,
+                  double* q, int mode, const double* rz, const int* stop, double* pq) {
+  if (c->n_el >= 148 * 256 * 2)
+    return launch_k2f_t<8, 8, 4, 2>(c, pold, pnew, r, Minv, X, q, mode, rz, stop, pq);
+  return launch_k2f_t<4, 4, 4, 6>(c, pold, pnew, r, Minv, X, q, mode, rz, stop, pq);
+}
+
+wb_status configure_kernels(wb_ctx* c) {
+  CUDA_TRY(c, cudaFuncSetAttribute(k_A_tile<4, 4, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)Tile2<4, 4, 4>::SMEM));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_A_tile<4, 4, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)Tile2<4, 4, 2>::SMEM));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_K2_fused<8, 8, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)FK2<8, 8, 4>::SMEM));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_K2_fused<4, 4, 4, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)FK2<4, 4, 4>::SMEM));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_A_slice<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(8 * 12 * Ord<3>::NQ * sizeof(double))));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_A_slice<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(5 * 12 * Ord<4>::NQ * sizeof(double))));
   return WB_OK;
 }
 
@@ -159,68 +207,150 @@ wb_status launch_B_t(wb_ctx* c, const double* u, const double* xs, double* p, in
                : ((c)->k == 3 ? fn<3>(c, __VA_ARGS__) : fn<4>(c, __VA_ARGS__)))
 
 wb_status run_A(wb_ctx* c, const double* u, double* y, int nomask) {
+  if (c->k == 2) {
+    ++c->epoch;
+    const int N = c->N;
+    int nt;
+    if (c->a_tile == 1) {
+      nt = ((N + 3) / 4) * ((N + 3) / 4) * ((N + 3) / 4);
+      k_A_tile<4, 4, 4, 2><<<nt, 192, Tile2<4, 4, 4>::SMEM, c->stream>>>(c->mut, u, y, c->F, c->tflag, c->ticket,
+                                                                         c->ticket_base, c->epoch, c->G, nomask);
+    } else {
+      nt = ((N + 3) / 4) * ((N + 3) / 4) * ((N + 1) / 2);
+      k_A_tile<4, 4, 2, 4><<<nt, 96, Tile2<4, 4, 2>::SMEM, c->stream>>>(c->mut, u, y, c->F, c->tflag, c->ticket,
+                                                                        c->ticket_base, c->epoch, c->G, nomask);
+    }
+    c->ticket_base += (unsigned long long)nt;
+    LAUNCH_CHECK(c);
+    return WB_OK;
+  }
   wb_status s = DISPATCH_K(c, launch_A_t, u, c->E, nomask);
   if (s) return s;
   return DISPATCH_K(c, launch_gather_t, (const double*)nullptr, y, nomask);
 }
-wb_status run_BT(wb_ctx* c, const double* p, const double* xs, double* y, int nomask, const int* stop) {
-  wb_status s = DISPATCH_K(c, launch_BT_t, p, stop);
-  if (s) return s;
-  if (stop) {
-    // the gather of a stopped PCG iteration is harmless (its result is unused)
+// y = M B^T p (X o ... if xs), p[e*se + m*sm]
+wb_status run_BT(wb_ctx* c, const double* p, const double* xs, double* y, int nomask, const int* stop,
+                 int64_t se, int64_t sm) {
+  if (c->k == 2) {
+    dim3 grid(nblk(c->N + 1, 64), nblk(c->G.nn1, 4), 2 * c->G.nn1);
+    k_BT_node2<<<grid, dim3(64, 4), 0, c->stream>>>(p, xs, y, c->G, c->sB, nomask, stop, se, sm);
+    LAUNCH_CHECK(c);
+    return WB_OK;
   }
+  wb_status s = DISPATCH_K(c, launch_BT_t, p, stop, se, sm);
+  if (s) return s;
   return DISPATCH_K(c, launch_gather_t, xs, y, nomask);
 }
 wb_status run_B(wb_ctx* c, const double* u, const double* xs, double* p, int nomask, const int* stop,
-                const double* dv, double* total) {
-  return DISPATCH_K(c, launch_B_t, u, xs, p, nomask, stop, dv, total);
+                const double* dv, double* total, int64_t se, int64_t sm) {
+  return DISPATCH_K(c, launch_B_t, u, xs, p, nomask, stop, dv, total, se, sm);
 }
 
-// q = K_side p  (+ <p, q> into *total when dot)
-wb_status run_K(wb_ctx* c, int side, const double* p, double* q, const int* stop, bool dot, double* total) {
-  wb_status s = run_BT(c, p, nullptr, c->tv, 0, stop);
-  if (s) return s;
-  const double* X = side == 0 ? c->Cinv : c->Dinv;
-  return run_B(c, c->tv, X, q, 0, stop, dot ? p : nullptr, total);
-}
-
-// out = P in (out may equal in)
-wb_status run_project(wb_ctx* c, const double* in, double* out) {
-  k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(in, c->n_el, c->nm, c->partial, c->counter, c->scal + S_SUM);
-  LAUNCH_CHECK(c);
-  k_project<<<c->red_blocks, VBS, 0, c->stream>>>(in, out, c->n_p, c->nm, c->n_el, c->scal + S_SUM);
-  LAUNCH_CHECK(c);
-  return WB_OK;
-}
-
-// x = PCG(K_side, b), exactly `iters` iterations (break rules of DESIGN.md Sec. 4)
-wb_status run_pcg(wb_ctx* c, int side, const double* b, double* x, int iters) {
-  wb_status s = ensure_iters(c, iters);
-  if (s) return s;
+// Mode-major K_side p_cur -> q (pq_out = <p_cur, q>), p_cur produced from
+// (pold, r) by the direction-update `mode` (0: Minv r, 1: Minv r + beta pold,
+// 2: pold as is).  Returns the buffer that holds p_cur.
+wb_status run_K_pcg(wb_ctx* c, int side, int mode, const double* pold, double* pnew, const double* r, double* q,
+                    const double* rz, const int* stop, double* pq_out, const double** pcur) {
   const double* Minv = side == 0 ? c->MinvL : c->MinvR;
-  k_pcg_init<<<c->red_blocks, VBS, 0, c->stream>>>(b, x, c->pr, c->pp, Minv, c->n_p, c->partial, c->counter,
-                                                   rz_hist(c), c->stop);
-  LAUNCH_CHECK(c);
-  for (int it = 0; it < iters; ++it) {
-    const int* st = c->stop + it;
-    s = run_K(c, side, c->pp, c->pq, st, true, pq_hist(c) + it);
-    if (s) return s;
-    k_pcg_upd1<<<c->red_blocks, VBS, 0, c->stream>>>(x, c->pr, c->pp, c->pq, Minv, c->n_p, pq_hist(c) + it,
-                                                     rz_hist(c) + it, rzn_hist(c) + it, st, c->partial, c->counter);
+  const double* X = side == 0 ? c->Cinv : c->Dinv;
+  if (c->k == 2) {
+    *pcur = pnew;
+    return run_k2f(c, pold, pnew, r, Minv, X, q, mode, rz, stop, pq_out);
+  }
+  // generic k: direction update pold -> pnew, then B^T (element + gather) and B (+ dot)
+  const double* p = pold;
+  if (mode != 2) {
+    k_pupd<<<c->red_blocks, VBS, 0, c->stream>>>(pnew, pold, r, Minv, c->n_p, mode, rz, stop);
     LAUNCH_CHECK(c);
-    k_pcg_upd2<<<c->red_blocks, VBS, 0, c->stream>>>(c->pr, c->pp, Minv, c->n_p, pq_hist(c) + it, rz_hist(c) + it,
-                                                     rzn_hist(c) + it, rz_hist(c) + it + 1, st, c->stop + it + 1);
+    p = pnew;
+  }
+  *pcur = p;
+  wb_status s = run_BT(c, p, nullptr, c->tv, 0, stop, 1, c->n_el);
+  if (s) return s;
+  return run_B(c, c->tv, X, q, 0, stop, p, pq_out, 1, c->n_el);
+}
+
+// the PCG iterations proper (no init / output), on c->stream
+wb_status pcg_loop_direct(wb_ctx* c, int side, int iters) {
+  const double* Minv = side == 0 ? c->MinvL : c->MinvR;
+  double* PB[2] = {c->pp, c->pp1};
+  for (int it = 0; it < iters; ++it) {
+    const double* pcur = nullptr;
+    wb_status s = run_K_pcg(c, side, it == 0 ? 0 : 1, PB[(it + 1) & 1], PB[it & 1], c->pr, c->pq, rz_hist(c) + it,
+                            c->stop + it, pq_hist(c) + it, &pcur);
+    if (s) return s;
+    k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->n_p, pq_hist(c) + it,
+                                                    rz_hist(c) + it, c->stop + it, c->partial, c->counter);
     LAUNCH_CHECK(c);
   }
   return WB_OK;
 }
 
+void clear_graphs(wb_ctx* c) {
+  for (int i = 0; i < c->n_graphs; ++i)
+    if (c->graphs[i].exec) cudaGraphExecDestroy(c->graphs[i].exec);
+  c->n_graphs = 0;
+}
+
+// replay of the iteration loop as one CUDA graph (captured on a private stream)
+wb_status pcg_loop(wb_ctx* c, int side, int iters) {
+  if (!c->use_graph || iters == 0 || !c->cap_stream) return pcg_loop_direct(c, side, iters);
+  wb_ctx::GraphEntry* g = nullptr;
+  for (int i = 0; i < c->n_graphs; ++i)
+    if (c->graphs[i].side == side && c->graphs[i].iters == iters) g = &c->graphs[i];
+  if (!g) {
+    if (c->n_graphs == wb_ctx::MAX_GRAPHS) clear_graphs(c);
+    g = &c->graphs[c->n_graphs];
+    cudaStream_t saved = c->stream;
+    const long long l0 = c->launches;
+    CUDA_TRY(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+    c->stream = c->cap_stream;
+    wb_status s = pcg_loop_direct(c, side, iters);
+    c->stream = saved;
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(c->cap_stream, &graph);
+    if (s) { if (graph) cudaGraphDestroy(graph); return s; }
+    if (e != cudaSuccess) return set_err(c, WB_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&g->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return set_err(c, WB_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    g->side = side; g->iters = iters; g->n_launch = c->launches - l0;
+    c->launches = l0;
+    ++c->n_graphs;
+  }
+  CUDA_TRY(c, cudaGraphLaunch(g->exec, c->stream));
+  c->launches += g->n_launch;
+  return WB_OK;
+}
+
+// x = P PCG(K_side, P b), exactly `iters` iterations (b, x element-major)
 wb_status run_poisson(wb_ctx* c, int side, const double* b, double* x, int iters) {
-  wb_status s = run_project(c, b, c->s0);
+  wb_status s = ensure_iters(c, iters);
   if (s) return s;
-  s = run_pcg(c, side, c->s0, c->s1, iters);
+  const double* Minv = side == 0 ? c->MinvL : c->MinvR;
+  k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->n_el, c->nm, c->partial, c->counter, c->scal + S_SUM);
+  LAUNCH_CHECK(c);
+  k_pcg_init<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->scal + S_SUM, c->px, c->pr, Minv, c->n_el, c->nm,
+                                                   c->partial, c->counter, rz_hist(c), c->stop);
+  LAUNCH_CHECK(c);
+  if ((s = pcg_loop(c, side, iters))) return s;
+  k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->n_el, 1, c->partial, c->counter, c->scal + S_SUM + 1);
+  LAUNCH_CHECK(c);
+  k_pcg_out<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->scal + S_SUM + 1, x, c->n_el, c->nm);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+
+// q = K_side p, element-major in and out (through the PCG kernels, mode "p as is")
+wb_status run_K(wb_ctx* c, int side, const double* p, double* q) {
+  k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(p, c->pp, c->n_el, c->nm, 1);
+  LAUNCH_CHECK(c);
+  const double* pcur = nullptr;
+  wb_status s = run_K_pcg(c, side, 2, c->pp, c->pp1, nullptr, c->pq, nullptr, nullptr, c->scal + S_SCR, &pcur);
   if (s) return s;
-  return run_project(c, c->s1, x);
+  k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(c->pq, q, c->n_el, c->nm, 0);
+  LAUNCH_CHECK(c);
+  return WB_OK;
 }
 
 wb_status run_wbfbt(wb_ctx* c, const double* r, double* z, int iters) {
@@ -228,13 +358,13 @@ wb_status run_wbfbt(wb_ctx* c, const double* r, double* z, int iters) {
   wb_status s = run_poisson(c, 1, r, c->s2, iters);
   if (s) return s;
   // v = Dinv o (B^T y)
-  s = run_BT(c, c->s2, c->Dinv, c->tw, 0, nullptr);
+  s = run_BT(c, c->s2, c->Dinv, c->tw, 0, nullptr, c->nm, 1);
   if (s) return s;
   // w = A v
   s = run_A(c, c->tw, c->tv, 0);
   if (s) return s;
   // s = P B (Cinv o w)
-  s = run_B(c, c->tv, c->Cinv, c->s2, 0, nullptr, nullptr, nullptr);
+  s = run_B(c, c->tv, c->Cinv, c->s2, 0, nullptr, nullptr, nullptr, c->nm, 1);
   if (s) return s;
   // z = P PCG(K_l, s)   (run_poisson projects its input first)
   return run_poisson(c, 0, c->s2, z, iters);
@@ -248,11 +378,16 @@ wb_status check_ctx(wb_ctx* c, bool need_visc) {
 
 void free_all(wb_ctx* c) {
   double** bufs[] = {&c->mut, &c->Cw, &c->Dw, &c->Cinv, &c->Dinv, &c->dKl, &c->dKr, &c->MinvL, &c->MinvR,
-                     &c->E, &c->tv, &c->tw, &c->pr, &c->pp, &c->pq, &c->s0, &c->s1, &c->s2, &c->partial, &c->scal,
-                     &c->stage};
+                     &c->E, &c->tv, &c->tw, &c->px, &c->pr, &c->pp, &c->pp1, &c->pq, &c->s0, &c->s1, &c->s2,
+                     &c->partial, &c->scal, &c->stage, &c->F};
+  clear_graphs(c);
+  if (c->cap_stream) { cudaStreamDestroy(c->cap_stream); c->cap_stream = nullptr; }
   for (double** b : bufs)
     if (*b) { cudaFree(*b); *b = nullptr; }
   if (c->counter) cudaFree(c->counter);
+  if (c->tflag) cudaFree(c->tflag);
+  if (c->ticket) cudaFree(c->ticket);
+  c->tflag = nullptr; c->ticket = nullptr;
   if (c->stop) cudaFree(c->stop);
   if (c->icount) cudaFree(c->icount);
   c->counter = nullptr; c->stop = nullptr; c->icount = nullptr;
@@ -290,6 +425,21 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
       delete c;
       return WB_ECUDA;
     }
+    // k = 2 dense gradient table (without sB): prod_d (d == c ? BD : BI)[m_d][a_d]
+    double bt2[3][27][4];
+    const int md[4][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}};  // mode order of wbfbt.h
+    for (int cc = 0; cc < 3; ++cc)
+      for (int a = 0; a < 27; ++a)
+        for (int m = 0; m < 4; ++m) {
+          const int ad[3] = {a % 3, (a / 3) % 3, a / 9};
+          long double v = 1.0L;
+          for (int d = 0; d < 3; ++d) v *= (d == cc ? t[0].BD[md[m][d]][ad[d]] : t[0].BI[md[m][d]][ad[d]]);
+          bt2[cc][a][m] = (double)v;
+        }
+    if (cudaMemcpyToSymbol(c_Bt2, bt2, sizeof(bt2)) != cudaSuccess) {
+      delete c;
+      return WB_ECUDA;
+    }
     g_tabs_ready = true;
   }
   int dev = 0, nsm = 148;
@@ -304,11 +454,24 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
   alloc(&c->mut, c->n_el * c->nq);
   alloc(&c->Cw, c->n_nodes); alloc(&c->Dw, c->n_nodes); alloc(&c->Cinv, c->n_nodes); alloc(&c->Dinv, c->n_nodes);
   alloc(&c->dKl, c->n_p); alloc(&c->dKr, c->n_p); alloc(&c->MinvL, c->n_p); alloc(&c->MinvR, c->n_p);
-  alloc(&c->E, 3 * c->nq * c->n_el);
+  alloc(&c->E, (k == 2 ? 1 : 3) * c->nq * c->n_el);  // k = 2: setup only (lumped element values)
   alloc(&c->tv, c->n_v); alloc(&c->tw, c->n_v);
-  alloc(&c->pr, c->n_p); alloc(&c->pp, c->n_p); alloc(&c->pq, c->n_p);
+  alloc(&c->px, c->n_p); alloc(&c->pr, c->n_p); alloc(&c->pp, c->n_p); alloc(&c->pp1, c->n_p);
+  alloc(&c->pq, c->n_p);
   alloc(&c->s0, c->n_p); alloc(&c->s1, c->n_p); alloc(&c->s2, c->n_p);
   alloc(&c->partial, c->max_partials);
+  if (k == 2) {
+    // sized for the largest tile count / shell of the two A tile shapes (4x4x2, 4x4x4)
+    const int64_t t442 = (int64_t)((N + 3) / 4) * ((N + 3) / 4) * ((N + 1) / 2);
+    const int64_t t444 = (int64_t)((N + 3) / 4) * ((N + 3) / 4) * ((N + 3) / 4);
+    c->n_tiles = (int)t442;
+    alloc(&c->F, std::max(t442 * 3 * Tile2<4, 4, 2>::SHELL, t444 * 3 * Tile2<4, 4, 4>::SHELL));
+    if (ok && cudaMalloc(&c->tflag, sizeof(int) * c->n_tiles) != cudaSuccess) ok = false;
+    if (ok && cudaMalloc(&c->ticket, sizeof(unsigned long long)) != cudaSuccess) ok = false;
+    if (ok && (cudaMemsetAsync(c->tflag, 0, sizeof(int) * c->n_tiles, c->stream) != cudaSuccess ||
+               cudaMemsetAsync(c->ticket, 0, sizeof(unsigned long long), c->stream) != cudaSuccess))
+      ok = false;
+  }
   if (ok && cudaMalloc(&c->counter, sizeof(unsigned) * 4) != cudaSuccess) ok = false;
   if (ok && cudaMalloc(&c->icount, sizeof(unsigned long long) * 4) != cudaSuccess) ok = false;
   if (!ok) {
@@ -318,7 +481,9 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
     return WB_ENOMEM;
   }
   if (cudaMemsetAsync(c->counter, 0, sizeof(unsigned) * 4, c->stream) != cudaSuccess ||
-      ensure_iters(c, 128) != WB_OK || cudaStreamSynchronize(c->stream) != cudaSuccess) {
+      ensure_iters(c, 126) != WB_OK || configure_kernels(c) != WB_OK ||
+      cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess) {
     free_all(c);
     delete c;
     return WB_ECUDA;
@@ -395,6 +560,14 @@ static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
   k_jacobi<K><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(c->Cinv, c->Dinv, c->dKl, c->dKr, c->MinvL, c->MinvR,
                                                          c->G, c->sB);
   LAUNCH_CHECK(c);
+  for (int side = 0; side < 2; ++side) {
+    const double* d = side == 0 ? c->dKl : c->dKr;
+    double* dmax = c->scal + S_DMAX + side;
+    k_absmax<VBS><<<c->red_blocks, VBS, 0, c->stream>>>(d, c->n_p, c->partial, c->counter, dmax);
+    LAUNCH_CHECK(c);
+    k_minv<<<c->red_blocks, VBS, 0, c->stream>>>(d, side == 0 ? c->MinvL : c->MinvR, c->n_el, c->nm, dmax);
+    LAUNCH_CHECK(c);
+  }
   unsigned long long np[2] = {0, 0};
   CUDA_TRY(c, cudaMemcpyAsync(np, c->icount + 1, sizeof(np), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -432,7 +605,7 @@ wb_status wb_apply_B(wb_ctx* c, const double* u, double* p) {
   if (s) return s;
   if (!u || !p) return set_err(c, WB_EINVAL, "null pointer");
   if (overlaps(u, 8 * c->n_v, p, 8 * c->n_p)) return set_err(c, WB_EALIAS, "u and p overlap");
-  return run_B(c, u, nullptr, p, (c->flags & WB_DEBUG_NOMASK) ? 1 : 0, nullptr, nullptr, nullptr);
+  return run_B(c, u, nullptr, p, (c->flags & WB_DEBUG_NOMASK) ? 1 : 0, nullptr, nullptr, nullptr, c->nm, 1);
 }
 
 wb_status wb_apply_BT(wb_ctx* c, const double* p, double* y) {
@@ -440,7 +613,7 @@ wb_status wb_apply_BT(wb_ctx* c, const double* p, double* y) {
   if (s) return s;
   if (!p || !y) return set_err(c, WB_EINVAL, "null pointer");
   if (overlaps(p, 8 * c->n_p, y, 8 * c->n_v)) return set_err(c, WB_EALIAS, "p and y overlap");
-  return run_BT(c, p, nullptr, y, (c->flags & WB_DEBUG_NOMASK) ? 1 : 0, nullptr);
+  return run_BT(c, p, nullptr, y, (c->flags & WB_DEBUG_NOMASK) ? 1 : 0, nullptr, c->nm, 1);
 }
 
 wb_status wb_apply_K(wb_ctx* c, int side, const double* p, double* q) {
@@ -448,7 +621,7 @@ wb_status wb_apply_K(wb_ctx* c, int side, const double* p, double* q) {
   if (s) return s;
   if (!p || !q || (side != 0 && side != 1)) return set_err(c, WB_EINVAL, "bad argument");
   if (overlaps(p, 8 * c->n_p, q, 8 * c->n_p)) return set_err(c, WB_EALIAS, "p and q overlap");
-  return run_K(c, side, p, q, nullptr, false, nullptr);
+  return run_K(c, side, p, q);
 }
 
 wb_status wb_poisson_pcg(wb_ctx* c, int side, const double* b, double* x, int iters) {
@@ -482,21 +655,23 @@ wb_status wb_hotpath(wb_ctx* c, const double* mu_q, double a_l, double a_r, cons
 wb_status wb_hotpath_host(wb_ctx* c, const double* mu_q, double a_l, double a_r, const double* u, const double* p,
                           int iters, double* yA, double* pB, double* yBT, double* z) {
   if (!c || !mu_q || !u || !p || !yA || !pB || !yBT || !z) return WB_EINVAL;
-  const int64_t nmu = c->n_el * c->nq;
+  // sub-buffers rounded to 32 doubles (256-byte aligned)
+  auto rnd = [](int64_t n) { return (n + 31) & ~(int64_t)31; };
+  const int64_t nmu = c->n_el * c->nq, rmu = rnd(nmu), rv = rnd(c->n_v), rp = rnd(c->n_p);
   if (!c->stage) {
-    if (cudaMalloc(&c->stage, sizeof(double) * (size_t)(nmu + 3 * c->n_v + 3 * c->n_p)) != cudaSuccess) {
+    if (cudaMalloc(&c->stage, sizeof(double) * (size_t)(rmu + 3 * rv + 3 * rp)) != cudaSuccess) {
       c->stage = nullptr;
       cudaGetLastError();
       return set_err(c, WB_ENOMEM, "staging allocation failed");
     }
   }
   double* dmu = c->stage;
-  double* du = dmu + nmu;
-  double* dyA = du + c->n_v;
-  double* dyBT = dyA + c->n_v;
-  double* dp = dyBT + c->n_v;
-  double* dpB = dp + c->n_p;
-  double* dz = dpB + c->n_p;
+  double* du = dmu + rmu;
+  double* dyA = du + rv;
+  double* dyBT = dyA + rv;
+  double* dp = dyBT + rv;
+  double* dpB = dp + rp;
+  double* dz = dpB + rp;
   const size_t bmu = sizeof(double) * nmu, bv = sizeof(double) * c->n_v, bp = sizeof(double) * c->n_p;
   CUDA_TRY(c, cudaMemcpyAsync(dmu, mu_q, bmu, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(du, u, bv, cudaMemcpyHostToDevice, c->stream));
@@ -515,18 +690,32 @@ wb_status wb_debug_pcg_step(wb_ctx* c, int side, double* x, double* r, double* p
   wb_status s = check_ctx(c, true);
   if (s) return s;
   if (!x || !r || !p || !rz || (side != 0 && side != 1)) return set_err(c, WB_EINVAL, "bad argument");
-  if ((s = ensure_iters(c, 1))) return s;
+  if ((s = ensure_iters(c, 2))) return s;
   const double* Minv = side == 0 ? c->MinvL : c->MinvR;
-  CUDA_TRY(c, cudaMemcpyAsync(rz_hist(c), rz, sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemsetAsync(c->stop, 0, sizeof(int), c->stream));
-  if ((s = run_K(c, side, p, c->pq, c->stop, true, pq_hist(c)))) return s;
-  k_pcg_upd1<<<c->red_blocks, VBS, 0, c->stream>>>(x, r, p, c->pq, Minv, c->n_p, pq_hist(c), rz_hist(c),
-                                                   rzn_hist(c), c->stop, c->partial, c->counter);
+  // state in (element-major -> mode-major), rz as rz_1, iteration index 1
+  for (int i = 0; i < 3; ++i) {
+    k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(i == 0 ? x : (i == 1 ? r : p), i == 0 ? c->px : (i == 1 ? c->pr : c->pp),
+                                                      c->n_el, c->nm, 1);
+    LAUNCH_CHECK(c);
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(rz_hist(c) + 1, rz, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->stop, 0, 3 * sizeof(int), c->stream));
+  const double* pcur = nullptr;
+  if ((s = run_K_pcg(c, side, 2, c->pp, c->pp1, c->pr, c->pq, rz_hist(c) + 1, c->stop + 1, pq_hist(c) + 1, &pcur)))
+    return s;
+  k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->n_p, pq_hist(c) + 1,
+                                                  rz_hist(c) + 1, c->stop + 1, c->partial, c->counter);
   LAUNCH_CHECK(c);
-  k_pcg_upd2<<<c->red_blocks, VBS, 0, c->stream>>>(r, p, Minv, c->n_p, pq_hist(c), rz_hist(c), rzn_hist(c),
-                                                   rz_hist(c) + 1, c->stop, c->stop + 1);
+  // p = Minv r + (rz_2 / rz_1) p   (stop flag 0: the step always ends with the direction update)
+  double* pc = const_cast<double*>(pcur);
+  k_pupd<<<c->red_blocks, VBS, 0, c->stream>>>(pc, pc, c->pr, Minv, c->n_p, 1, rz_hist(c) + 2, c->stop);
   LAUNCH_CHECK(c);
-  CUDA_TRY(c, cudaMemcpyAsync(rz, rz_hist(c) + 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  for (int i = 0; i < 3; ++i) {
+    k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(i == 0 ? c->px : (i == 1 ? c->pr : pc), i == 0 ? x : (i == 1 ? r : p),
+                                                      c->n_el, c->nm, 0);
+    LAUNCH_CHECK(c);
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(rz, rz_hist(c) + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return WB_OK;
 }
@@ -570,6 +759,19 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
     *value = first;
   } else
     return set_err(c, WB_EINVAL, "unknown query key '%s'", key);
+  return WB_OK;
+}
+
+wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
+  if (!c || !key) return WB_EINVAL;
+  if (!strcmp(key, "a_tile")) {
+    if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "a_tile must be 0 or 1");
+    c->a_tile = (int)value;
+  } else if (!strcmp(key, "graph")) {
+    if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "graph must be 0 or 1");
+    c->use_graph = (int)value;
+  } else
+    return set_err(c, WB_EINVAL, "unknown option '%s'", key);
   return WB_OK;
 }
 

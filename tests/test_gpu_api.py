@@ -98,6 +98,30 @@ def test_hotpath_host_equals_device():
         assert np.array_equal(host(a), b.numpy())
 
 
+def test_unaligned_pointers():
+    """Caller tensors need only 8-byte alignment (torch views at odd offsets)."""
+    import torch
+    for cfg, N in (("C2", 5), ("C4", 2)):
+        p = Pair(cfg, N=N)
+        c = p.ctx
+        outs = {}
+        for off in (0, 1):
+            u = torch.zeros(c.n_v + 1, dtype=torch.float64, device="cuda")
+            q = torch.zeros(c.n_p + 1, dtype=torch.float64, device="cuda")
+            u[off:off + c.n_v] = dev(p.inp["u"])
+            q[off:off + c.n_p] = dev(p.inp["p"])
+            yA, yBT = empty(c.n_v + 1), empty(c.n_v + 1)
+            pB, z = empty(c.n_p + 1), empty(c.n_p + 1)
+            uu, qq = u[off:off + c.n_v], q[off:off + c.n_p]
+            c.apply_A(uu, yA[off:off + c.n_v])
+            c.apply_B(uu, pB[off:off + c.n_p])
+            c.apply_BT(qq, yBT[off:off + c.n_v])
+            c.apply_wbfbt(qq, z[off:off + c.n_p], 5)
+            outs[off] = [host(t[off:off + n]) for t, n in ((yA, c.n_v), (pB, c.n_p), (yBT, c.n_v), (z, c.n_p))]
+        for a, b in zip(outs[0], outs[1]):
+            assert np.array_equal(a, b)
+
+
 def test_amplified_boundary_weights():
     """a_l, a_r != 1 (eq:bdramp): lumped diagonals and wBFBT parity."""
     p = Pair("C2", a_l=1.0, a_r=4.0)

@@ -142,7 +142,8 @@ def test_pcg_one_step(pair):
         if (st["n_nonpos_Cw"] if side == 0 else st["n_nonpos_Dw"]):
             continue
         x, r, p = (o.project(rng.uniform(-1, 1, o.n_p)) for _ in range(3))
-        minv = np.where(dk != 0.0, 1.0 / np.where(dk != 0.0, dk, 1.0), 0.0)  # DESIGN.md R11
+        keep = np.abs(dk) > 1e-13 * np.abs(dk).max()  # DESIGN.md R11 (pseudo-inverse of diag K)
+        minv = np.where(keep, 1.0 / np.where(keep, dk, 1.0), 0.0)
         rz = float(r @ (minv * r))
         xg, rg, pg = dev(x), dev(r), dev(p)
         rzg = ctx.debug_pcg_step(side, xg, rg, pg, rz)
