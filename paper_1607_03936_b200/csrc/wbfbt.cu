@@ -60,6 +60,11 @@ struct wb_ctx {
   int epoch = 0, n_tiles = 0;
   int a_tile = 0;  // k = 2 A tile shape: 0 = 4x4x2 (96 threads), 1 = 4x4x4 (192 threads)
   int use_graph = 1;
+  // profiling: CUDA-event pairs around every Poisson-operator launch (direct launches)
+  int profile = 0;
+  static constexpr int PROF_MAX = 4096;
+  cudaEvent_t prof_ev[2 * PROF_MAX] = {};
+  int prof_n = 0;
   long long launches = 0;
   char err[512] = {0};
 };
@@ -276,9 +281,16 @@ wb_status pcg_loop_direct(wb_ctx* c, int side, int iters) {
   double* PB[2] = {c->pp, c->pp1};
   for (int it = 0; it < iters; ++it) {
     const double* pcur = nullptr;
+    const bool prof = c->profile && c->prof_n < wb_ctx::PROF_MAX;
+    if (prof) {
+      cudaEvent_t* ev = c->prof_ev + 2 * c->prof_n;
+      if (!ev[0]) { cudaEventCreate(&ev[0]); cudaEventCreate(&ev[1]); }
+      CUDA_TRY(c, cudaEventRecord(ev[0], c->stream));
+    }
     wb_status s = run_K_pcg(c, side, it == 0 ? 0 : 1, PB[(it + 1) & 1], PB[it & 1], c->pr, c->pq, rz_hist(c) + it,
                             c->stop + it, pq_hist(c) + it, &pcur);
     if (s) return s;
+    if (prof) CUDA_TRY(c, cudaEventRecord(c->prof_ev[2 * c->prof_n++ + 1], c->stream));
     k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->n_p, pq_hist(c) + it,
                                                     rz_hist(c) + it, c->stop + it, c->partial, c->counter);
     LAUNCH_CHECK(c);
@@ -294,7 +306,7 @@ void clear_graphs(wb_ctx* c) {
 
 // replay of the iteration loop as one CUDA graph (captured on a private stream)
 wb_status pcg_loop(wb_ctx* c, int side, int iters) {
-  if (!c->use_graph || iters == 0 || !c->cap_stream) return pcg_loop_direct(c, side, iters);
+  if (!c->use_graph || c->profile || iters == 0 || !c->cap_stream) return pcg_loop_direct(c, side, iters);
   wb_ctx::GraphEntry* g = nullptr;
   for (int i = 0; i < c->n_graphs; ++i)
     if (c->graphs[i].side == side && c->graphs[i].iters == iters) g = &c->graphs[i];
@@ -382,6 +394,8 @@ void free_all(wb_ctx* c) {
                      &c->partial, &c->scal, &c->stage, &c->F};
   clear_graphs(c);
   if (c->cap_stream) { cudaStreamDestroy(c->cap_stream); c->cap_stream = nullptr; }
+  for (int i = 0; i < 2 * wb_ctx::PROF_MAX; ++i)
+    if (c->prof_ev[i]) { cudaEventDestroy(c->prof_ev[i]); c->prof_ev[i] = nullptr; }
   for (double** b : bufs)
     if (*b) { cudaFree(*b); *b = nullptr; }
   if (c->counter) cudaFree(c->counter);
@@ -748,6 +762,17 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
   else if (!strcmp(key, "n_p")) *value = (double)c->n_p;
   else if (!strcmp(key, "n_v")) *value = (double)c->n_v;
   else if (!strcmp(key, "kernel_launches")) *value = (double)c->launches;
+  else if (!strcmp(key, "prof_k_count")) *value = (double)c->prof_n;
+  else if (!strcmp(key, "prof_k_ms")) {
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    double t = 0.0;
+    for (int i = 0; i < c->prof_n; ++i) {
+      float ms = 0.f;
+      CUDA_TRY(c, cudaEventElapsedTime(&ms, c->prof_ev[2 * i], c->prof_ev[2 * i + 1]));
+      t += ms;
+    }
+    *value = t;
+  }
   else if (!strcmp(key, "last_pcg_stop_iter")) {
     int st[1024];
     int n = c->it_cap + 1 < 1024 ? c->it_cap + 1 : 1024;
@@ -770,6 +795,10 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
   } else if (!strcmp(key, "graph")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "graph must be 0 or 1");
     c->use_graph = (int)value;
+  } else if (!strcmp(key, "profile")) {
+    if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "profile must be 0 or 1");
+    c->profile = (int)value;
+    c->prof_n = 0;  // (re)start the record
   } else
     return set_err(c, WB_EINVAL, "unknown option '%s'", key);
   return WB_OK;
