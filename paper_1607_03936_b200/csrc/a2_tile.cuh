@@ -116,8 +116,11 @@ __device__ __forceinline__ void a2_elem(const double* __restrict__ Mu, const dou
     for (int x = 0; x < 3; ++x) k2_interp(k, U3(0, y, x), U3(1, y, x), U3(2, y, x));
 #pragma unroll
   for (int q = 0; q < 27; ++q) V[q] = 0.0;
-  // mut of this element, staged in shared memory by cp.async (Mu[q*NE + le])
+  // mut of this element, staged in shared memory by cp.async (Mu[q*NE + le]) by
+  // all threads of the CTA: wait for this thread's copies, then a barrier makes
+  // every thread's copies visible
   cp_async_wait_all();
+  __syncthreads();
 #pragma unroll
   for (int iz = 0; iz < 3; ++iz) {
     double mu[9];

@@ -81,6 +81,28 @@ __device__ __forceinline__ bool grid_sum(double v, double* partial, unsigned* co
   return threadIdx.x == 0;
 }
 
+// Deferred reductions: a kernel stores one partial per block (no fence, no
+// atomics) and every block of the NEXT kernel sums all of them in the same
+// fixed order (strided per thread, then the fixed shuffle tree), so all blocks
+// agree bitwise and no kernel ends with a grid-wide tail.
+template <int BS>
+__device__ __forceinline__ double sum_partials(const double* __restrict__ part, int n) {
+  __shared__ double s_tot;
+  double a = 0.0;
+  for (int i = threadIdx.x; i < n; i += BS) a += part[i];
+  a = block_sum<BS>(a);
+  if (threadIdx.x == 0) s_tot = a;
+  __syncthreads();
+  const double t = s_tot;
+  __syncthreads();
+  return t;
+}
+template <int BS>
+__device__ __forceinline__ void store_partial(double v, double* part) {
+  v = block_sum<BS>(v);
+  if (threadIdx.x == 0) part[blockIdx.x] = v;
+}
+
 // max |v| over the grid (same last-block pattern)
 template <int BS>
 __device__ __forceinline__ double block_max(double v) {
@@ -283,7 +305,8 @@ __global__ void __launch_bounds__(BS) k_B(const double* __restrict__ u, const do
       if (dv) dot = fma(o, dv[e * se + m * sm], dot);
     }
   }
-  if (partial) grid_sum<BS>(dot, partial, counter, total);
+  if (partial) store_partial<BS>(dot, partial);  // deferred: summed by k_pcg_upd
+  (void)counter; (void)total;
 }
 
 // ------------------------------------------------------------------ row a7: B^T (element part)
@@ -839,12 +862,26 @@ __global__ void k_project(const double* __restrict__ in, double* __restrict__ ou
 // This is the oracle's recurrence (or_pcg) with the direction update moved to
 // the top of the next iteration, so that it fuses into the K kernel.
 
+// PCG control at the top of iteration i (first kernel of the iteration):
+//   rz_i = sum of the previous kernel's <r, Minv r> partials (rzp, nrz),
+//   stop_i = stop_{i-1} || pq_{i-1} == 0 || rz_i == 0   (stop_0 = rz_0 == 0),
+//   beta_i = rz_i / rz_{i-1}; block 0 records rz_hist[i] and stop[i].
+// Returns stop_i (uniform over the grid).
+template <int BS>
+__device__ __forceinline__ bool pcg_control(int i, const double* __restrict__ rzp, int nrz, double* rz_hist,
+                                            const double* pq_hist, int* stop, double* beta) {
+  const double rzi = sum_partials<BS>(rzp, nrz);
+  const bool st = (i == 0) ? (rzi == 0.0) : (stop[i - 1] != 0 || pq_hist[i - 1] == 0.0 || rzi == 0.0);
+  *beta = (i == 0 || st) ? 0.0 : rzi / rz_hist[i - 1];
+  if (blockIdx.x == 0 && threadIdx.x == 0) { rz_hist[i] = rzi; stop[i] = st ? 1 : 0; }
+  return st;
+}
+
 // init: r = P b (element-major b -> mode-major r, constant-mode mean removed
-// using bsum = sum_e b[e*nm]); x = 0; rz_0 = <r, Minv r>.
+// using bsum = sum_e b[e*nm]); x = 0; partials of rz_0 = <r, Minv r> -> rzp.
 __global__ void __launch_bounds__(VBS) k_pcg_init(const double* __restrict__ b, const double* __restrict__ bsum,
                                                   double* x, double* r, const double* __restrict__ Minv, int64_t ne,
-                                                  int nm, double* partial, unsigned* counter, double* rz_hist,
-                                                  int* stop) {
+                                                  int nm, double* rzp) {
   const double mean = *bsum / (double)ne;
   const int64_t n = ne * nm;
   double s = 0.0;
@@ -854,41 +891,50 @@ __global__ void __launch_bounds__(VBS) k_pcg_init(const double* __restrict__ b, 
     x[i] = 0.0; r[i] = bi;
     s = fma(bi, Minv[i] * bi, s);
   }
-  if (grid_sum<VBS>(s, partial, counter, rz_hist)) stop[0] = (rz_hist[0] == 0.0) ? 1 : 0;
+  store_partial<VBS>(s, rzp);
 }
 
 // direction update (generic-k path; the k = 2 path fuses it into k_K2_fused).
-// mode 0: p = Minv r; 1: p = Minv r + (rz[0]/rz[-1]) pin  (pout may equal pin).
-__global__ void k_pupd(double* pout, const double* pin, const double* __restrict__ r,
-                       const double* __restrict__ Minv, int64_t n, int mode, const double* rz, const int* stop) {
-  if (*stop) return;
-  const double beta = mode == 1 ? rz[0] / rz[-1] : 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double z = Minv[i] * r[i];
-    pout[i] = mode == 1 ? fma(beta, pin[i], z) : z;
+// ctl: run pcg_control for iteration i (beta from the histories); otherwise
+// mode 1 uses beta = rz_hist[i] / rz_hist[i-1] as recorded.
+// mode 0: p = Minv r; 1: p = Minv r + beta pin  (pout may equal pin).
+__global__ void __launch_bounds__(VBS) k_pupd(double* pout, const double* pin, const double* __restrict__ r,
+                                              const double* __restrict__ Minv, int64_t n, int mode, int i, int ctl,
+                                              const double* __restrict__ rzp, int nrz, double* rz_hist,
+                                              const double* pq_hist, int* stop) {
+  double beta = 0.0;
+  if (ctl) {
+    if (pcg_control<VBS>(i, rzp, nrz, rz_hist, pq_hist, stop, &beta)) return;
+  } else if (mode == 1) {
+    beta = rz_hist[i] / rz_hist[i - 1];
+  }
+  for (int64_t j = (int64_t)blockIdx.x * VBS + threadIdx.x; j < n; j += (int64_t)gridDim.x * VBS) {
+    const double z = Minv[j] * r[j];
+    pout[j] = mode == 1 ? fma(beta, pin[j], z) : z;
   }
 }
 
-// alpha = rz_i / pq_i; x += alpha p; r -= alpha q; rz_{i+1} = <r, Minv r>; stop_{i+1}.
-// rz, pq, stop point at entry i of their histories.
+// iteration i: pq_i = sum of the K kernel's <p_i, q> partials (pqp, npq);
+// alpha = rz_i / pq_i; x += alpha p; r -= alpha q; partials of
+// rz_{i+1} = <r, Minv r> -> rzp.  Block 0 records pq_hist[i].
 __global__ void __launch_bounds__(VBS) k_pcg_upd(double* x, double* r, const double* __restrict__ p,
                                                  const double* __restrict__ q, const double* __restrict__ Minv,
-                                                 int64_t n, const double* pq, double* rz, int* stop,
-                                                 double* partial, unsigned* counter) {
-  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
-  if (*stop || *pq == 0.0) {
-    if (lead) { stop[1] = 1; rz[1] = rz[0]; }
-    return;
-  }
-  const double alpha = rz[0] / *pq;
+                                                 int64_t n, int i, const double* __restrict__ pqp, int npq,
+                                                 const double* rz_hist, double* pq_hist, const int* stop,
+                                                 double* rzp) {
+  if (stop[i]) return;
+  const double pq = sum_partials<VBS>(pqp, npq);
+  if (blockIdx.x == 0 && threadIdx.x == 0) pq_hist[i] = pq;
+  if (pq == 0.0) return;
+  const double alpha = rz_hist[i] / pq;
   double s = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS) {
-    x[i] = fma(alpha, p[i], x[i]);
-    const double ri = fma(-alpha, q[i], r[i]);
-    r[i] = ri;
-    s = fma(ri, Minv[i] * ri, s);
+  for (int64_t j = (int64_t)blockIdx.x * VBS + threadIdx.x; j < n; j += (int64_t)gridDim.x * VBS) {
+    x[j] = fma(alpha, p[j], x[j]);
+    const double rj = fma(-alpha, q[j], r[j]);
+    r[j] = rj;
+    s = fma(rj, Minv[j] * rj, s);
   }
-  if (grid_sum<VBS>(s, partial, counter, rz + 1)) stop[1] = (rz[1] == 0.0) ? 1 : 0;
+  store_partial<VBS>(s, rzp);
 }
 
 // out (element-major) = P x (mode-major), xsum = sum of the constant-mode entries.

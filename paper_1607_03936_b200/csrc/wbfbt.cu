@@ -45,12 +45,13 @@ struct wb_ctx {
   double *s0 = nullptr, *s1 = nullptr, *s2 = nullptr;  // n_p scratch
   // scalars
   double* partial = nullptr;  // reduction partials
+  double *pqp = nullptr, *rzp = nullptr;  // PCG deferred-reduction partials (<p,Kp> per K block, <r,Mr> per vector block)
   unsigned* counter = nullptr;
   double* scal = nullptr;  // [0..7] misc totals, then rz_hist, pq_hist, rzn_hist
   int* stop = nullptr;
   int it_cap = 0;
   unsigned long long* icount = nullptr;  // [0] bad mu, [1] nonpos Cw, [2] nonpos Dw
-  int red_blocks = 0, max_partials = 0;
+  int red_blocks = 0, max_partials = 0, nsm = 148;
   double* stage = nullptr;  // wb_hotpath_host staging (lazily allocated)
   // k = 2 tile-assembled A: face partials, flags, ticket counter
   double* F = nullptr;
@@ -60,6 +61,8 @@ struct wb_ctx {
   int epoch = 0, n_tiles = 0;
   int a_tile = 0;  // k = 2 A tile shape: 0 = 4x4x2 (96 threads), 1 = 4x4x4 (192 threads)
   int use_graph = 1;
+  int k_var = 1;  // k = 2 fused K variant: 0 = 2 CTAs/SM (register-capped), 1 = 1 CTA/SM (faster: L1 left free)
+  int k_dbg = 0;  // timing probe bits for the fused K kernel (results invalid when nonzero)
   // profiling: CUDA-event pairs around every Poisson-operator launch (direct launches)
   int profile = 0;
   static constexpr int PROF_MAX = 4096;
@@ -167,28 +170,41 @@ template <int K>
 wb_status launch_B_t(wb_ctx* c, const double* u, const double* xs, double* p, int nomask, const int* stop,
                      const double* dv, double* total, int64_t se, int64_t sm) {
   constexpr int BS = 128;
+  // dv: fused <p_out, dv> block partials into `total` (deferred reduction, PCG only)
   k_B<K, BS><<<nblk(c->n_el, BS), BS, 0, c->stream>>>(u, xs, p, c->G, c->sB, nomask, stop, dv,
-                                                       dv ? c->partial : nullptr, c->counter, total, se, sm);
+                                                       dv ? total : nullptr, c->counter, nullptr, se, sm);
   LAUNCH_CHECK(c);
   return WB_OK;
 }
 
 // fused k = 2 Poisson operator (+ PCG direction update), see k2_fused.cuh
+struct PcgArgs {  // PCG iteration context for the first kernel of an iteration
+  int it = 0, ctl = 0;
+};
+
 template <int TX, int TY, int TZ, int MINB>
 wb_status launch_k2f_t(wb_ctx* c, const double* pold, double* pnew, const double* r, const double* Minv,
-                       const double* X, double* q, int mode, const double* rz, const int* stop, double* pq) {
+                       const double* X, double* q, int mode, PcgArgs a, int* npq) {
   const int N = c->N;
   const int nt = ((N + TX - 1) / TX) * ((N + TY - 1) / TY) * ((N + TZ - 1) / TZ);
-  k_K2_fused<TX, TY, TZ, MINB><<<nt, TX * TY * TZ, FK2<TX, TY, TZ>::SMEM, c->stream>>>(
-      pold, pnew, r, Minv, X, q, c->G, c->sB, mode, rz, stop, c->partial, c->counter, pq);
+  // persistent CTAs: as many as are resident at once (fixed per context -> fixed reduction order)
+  int occ = 0;
+  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_K2_fused<TX, TY, TZ, MINB>, FK2<TX, TY, TZ>::NTH,
+                                                            FK2<TX, TY, TZ>::SMEM));
+  const int grid = std::max(1, std::min(nt, occ * c->nsm));
+  k_K2_fused<TX, TY, TZ, MINB><<<grid, FK2<TX, TY, TZ>::NTH, FK2<TX, TY, TZ>::SMEM, c->stream>>>(
+      pold, pnew, r, Minv, X, q, c->G, c->sB, mode | c->k_dbg, a.it, a.ctl, c->rzp, c->red_blocks, rz_hist(c), pq_hist(c),
+      c->stop, c->pqp);
   LAUNCH_CHECK(c);
+  *npq = grid;
   return WB_OK;
 }
 wb_status run_k2f(wb_ctx* c, const double* pold, double* pnew, const double* r, const double* Minv, const double* X,
-                  double* q, int mode, const double* rz, const int* stop, double* pq) {
+                  double* q, int mode, PcgArgs a, int* npq) {
   if (c->n_el >= 148 * 256 * 2)
-    return launch_k2f_t<8, 8, 4, 2>(c, pold, pnew, r, Minv, X, q, mode, rz, stop, pq);
-  return launch_k2f_t<4, 4, 4, 6>(c, pold, pnew, r, Minv, X, q, mode, rz, stop, pq);
+    return c->k_var == 1 ? launch_k2f_t<4, 8, 8, 1>(c, pold, pnew, r, Minv, X, q, mode, a, npq)
+                         : launch_k2f_t<4, 8, 8, 2>(c, pold, pnew, r, Minv, X, q, mode, a, npq);
+  return launch_k2f_t<4, 4, 4, 6>(c, pold, pnew, r, Minv, X, q, mode, a, npq);
 }
 
 wb_status configure_kernels(wb_ctx* c) {
@@ -196,8 +212,10 @@ wb_status configure_kernels(wb_ctx* c) {
                                    (int)Tile2<4, 4, 4>::SMEM));
   CUDA_TRY(c, cudaFuncSetAttribute(k_A_tile<4, 4, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)Tile2<4, 4, 2>::SMEM));
-  CUDA_TRY(c, cudaFuncSetAttribute(k_K2_fused<8, 8, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)FK2<8, 8, 4>::SMEM));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_K2_fused<4, 8, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)FK2<4, 8, 8>::SMEM));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_K2_fused<4, 8, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)FK2<4, 8, 8>::SMEM));
   CUDA_TRY(c, cudaFuncSetAttribute(k_K2_fused<4, 4, 4, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)FK2<4, 4, 4>::SMEM));
   CUDA_TRY(c, cudaFuncSetAttribute(k_A_slice<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -254,25 +272,33 @@ wb_status run_B(wb_ctx* c, const double* u, const double* xs, double* p, int nom
 // Mode-major K_side p_cur -> q (pq_out = <p_cur, q>), p_cur produced from
 // (pold, r) by the direction-update `mode` (0: Minv r, 1: Minv r + beta pold,
 // 2: pold as is).  Returns the buffer that holds p_cur.
+// Mode-major q = K_side p_cur, with the <p_cur, q> block partials in pqp
+// (*npq of them), p_cur produced from (pold, r) by the direction-update `mode`
+// (0: Minv r, 1: Minv r + beta pold, 2: pold as is).  a.ctl: this is the first
+// kernel of PCG iteration a.it (runs pcg_control: stop test, beta).
+// Returns the buffer that holds p_cur.
 wb_status run_K_pcg(wb_ctx* c, int side, int mode, const double* pold, double* pnew, const double* r, double* q,
-                    const double* rz, const int* stop, double* pq_out, const double** pcur) {
+                    PcgArgs a, const double** pcur, int* npq) {
   const double* Minv = side == 0 ? c->MinvL : c->MinvR;
   const double* X = side == 0 ? c->Cinv : c->Dinv;
   if (c->k == 2) {
     *pcur = pnew;
-    return run_k2f(c, pold, pnew, r, Minv, X, q, mode, rz, stop, pq_out);
+    return run_k2f(c, pold, pnew, r, Minv, X, q, mode, a, npq);
   }
-  // generic k: direction update pold -> pnew, then B^T (element + gather) and B (+ dot)
+  // generic k: direction update pold -> pnew (+ control), then B^T (element + gather) and B (+ dot)
   const double* p = pold;
+  const int* stop = a.ctl ? c->stop + a.it : nullptr;
   if (mode != 2) {
-    k_pupd<<<c->red_blocks, VBS, 0, c->stream>>>(pnew, pold, r, Minv, c->n_p, mode, rz, stop);
+    k_pupd<<<c->red_blocks, VBS, 0, c->stream>>>(pnew, pold, r, Minv, c->n_p, mode, a.it, a.ctl, c->rzp,
+                                                 c->red_blocks, rz_hist(c), pq_hist(c), c->stop);
     LAUNCH_CHECK(c);
     p = pnew;
   }
   *pcur = p;
   wb_status s = run_BT(c, p, nullptr, c->tv, 0, stop, 1, c->n_el);
   if (s) return s;
-  return run_B(c, c->tv, X, q, 0, stop, p, pq_out, 1, c->n_el);
+  *npq = (int)nblk(c->n_el, 128);
+  return run_B(c, c->tv, X, q, 0, stop, p, c->pqp, 1, c->n_el);
 }
 
 // the PCG iterations proper (no init / output), on c->stream
@@ -287,12 +313,14 @@ wb_status pcg_loop_direct(wb_ctx* c, int side, int iters) {
       if (!ev[0]) { cudaEventCreate(&ev[0]); cudaEventCreate(&ev[1]); }
       CUDA_TRY(c, cudaEventRecord(ev[0], c->stream));
     }
-    wb_status s = run_K_pcg(c, side, it == 0 ? 0 : 1, PB[(it + 1) & 1], PB[it & 1], c->pr, c->pq, rz_hist(c) + it,
-                            c->stop + it, pq_hist(c) + it, &pcur);
+    PcgArgs a;
+    a.it = it; a.ctl = 1;
+    int npq = 0;
+    wb_status s = run_K_pcg(c, side, it == 0 ? 0 : 1, PB[(it + 1) & 1], PB[it & 1], c->pr, c->pq, a, &pcur, &npq);
     if (s) return s;
     if (prof) CUDA_TRY(c, cudaEventRecord(c->prof_ev[2 * c->prof_n++ + 1], c->stream));
-    k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->n_p, pq_hist(c) + it,
-                                                    rz_hist(c) + it, c->stop + it, c->partial, c->counter);
+    k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->n_p, it, c->pqp, npq,
+                                                    rz_hist(c), pq_hist(c), c->stop, c->rzp);
     LAUNCH_CHECK(c);
   }
   return WB_OK;
@@ -342,8 +370,7 @@ wb_status run_poisson(wb_ctx* c, int side, const double* b, double* x, int iters
   const double* Minv = side == 0 ? c->MinvL : c->MinvR;
   k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->n_el, c->nm, c->partial, c->counter, c->scal + S_SUM);
   LAUNCH_CHECK(c);
-  k_pcg_init<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->scal + S_SUM, c->px, c->pr, Minv, c->n_el, c->nm,
-                                                   c->partial, c->counter, rz_hist(c), c->stop);
+  k_pcg_init<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->scal + S_SUM, c->px, c->pr, Minv, c->n_el, c->nm, c->rzp);
   LAUNCH_CHECK(c);
   if ((s = pcg_loop(c, side, iters))) return s;
   k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->n_el, 1, c->partial, c->counter, c->scal + S_SUM + 1);
@@ -358,7 +385,8 @@ wb_status run_K(wb_ctx* c, int side, const double* p, double* q) {
   k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(p, c->pp, c->n_el, c->nm, 1);
   LAUNCH_CHECK(c);
   const double* pcur = nullptr;
-  wb_status s = run_K_pcg(c, side, 2, c->pp, c->pp1, nullptr, c->pq, nullptr, nullptr, c->scal + S_SCR, &pcur);
+  int npq = 0;
+  wb_status s = run_K_pcg(c, side, 2, c->pp, c->pp1, nullptr, c->pq, PcgArgs{}, &pcur, &npq);
   if (s) return s;
   k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(c->pq, q, c->n_el, c->nm, 0);
   LAUNCH_CHECK(c);
@@ -391,7 +419,7 @@ wb_status check_ctx(wb_ctx* c, bool need_visc) {
 void free_all(wb_ctx* c) {
   double** bufs[] = {&c->mut, &c->Cw, &c->Dw, &c->Cinv, &c->Dinv, &c->dKl, &c->dKr, &c->MinvL, &c->MinvR,
                      &c->E, &c->tv, &c->tw, &c->px, &c->pr, &c->pp, &c->pp1, &c->pq, &c->s0, &c->s1, &c->s2,
-                     &c->partial, &c->scal, &c->stage, &c->F};
+                     &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->F};
   clear_graphs(c);
   if (c->cap_stream) { cudaStreamDestroy(c->cap_stream); c->cap_stream = nullptr; }
   for (int i = 0; i < 2 * wb_ctx::PROF_MAX; ++i)
@@ -460,6 +488,7 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   c->red_blocks = 2 * nsm;
+  c->nsm = nsm;
   c->max_partials = (int)std::max<int64_t>(c->red_blocks, (c->n_el + 127) / 128 + 1);
   bool ok = true;
   auto alloc = [&](double** p, int64_t n) {
@@ -474,6 +503,8 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
   alloc(&c->pq, c->n_p);
   alloc(&c->s0, c->n_p); alloc(&c->s1, c->n_p); alloc(&c->s2, c->n_p);
   alloc(&c->partial, c->max_partials);
+  alloc(&c->pqp, c->n_el / 32 + 1024);  // >= blocks of any K-apply grid (tiles >= 64 elements, k_B 128)
+  alloc(&c->rzp, c->red_blocks);
   if (k == 2) {
     // sized for the largest tile count / shell of the two A tile shapes (4x4x2, 4x4x4)
     const int64_t t442 = (int64_t)((N + 3) / 4) * ((N + 3) / 4) * ((N + 1) / 2);
@@ -715,14 +746,17 @@ wb_status wb_debug_pcg_step(wb_ctx* c, int side, double* x, double* r, double* p
   CUDA_TRY(c, cudaMemcpyAsync(rz_hist(c) + 1, rz, sizeof(double), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(c->stop, 0, 3 * sizeof(int), c->stream));
   const double* pcur = nullptr;
-  if ((s = run_K_pcg(c, side, 2, c->pp, c->pp1, c->pr, c->pq, rz_hist(c) + 1, c->stop + 1, pq_hist(c) + 1, &pcur)))
-    return s;
-  k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->n_p, pq_hist(c) + 1,
-                                                  rz_hist(c) + 1, c->stop + 1, c->partial, c->counter);
+  int npq = 0;
+  PcgArgs a;
+  a.it = 1; a.ctl = 0;  // rz_1 and stop_1 given
+  if ((s = run_K_pcg(c, side, 2, c->pp, c->pp1, c->pr, c->pq, a, &pcur, &npq))) return s;
+  k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->n_p, 1, c->pqp, npq,
+                                                  rz_hist(c), pq_hist(c), c->stop, c->rzp);
   LAUNCH_CHECK(c);
-  // p = Minv r + (rz_2 / rz_1) p   (stop flag 0: the step always ends with the direction update)
+  // p = Minv r + (rz_2 / rz_1) p with the control of iteration 2 (records rz_2)
   double* pc = const_cast<double*>(pcur);
-  k_pupd<<<c->red_blocks, VBS, 0, c->stream>>>(pc, pc, c->pr, Minv, c->n_p, 1, rz_hist(c) + 2, c->stop);
+  k_pupd<<<c->red_blocks, VBS, 0, c->stream>>>(pc, pc, c->pr, Minv, c->n_p, 1, 2, 1, c->rzp, c->red_blocks,
+                                               rz_hist(c), pq_hist(c), c->stop);
   LAUNCH_CHECK(c);
   for (int i = 0; i < 3; ++i) {
     k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(i == 0 ? c->px : (i == 1 ? c->pr : pc), i == 0 ? x : (i == 1 ? r : p),
@@ -763,6 +797,16 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
   else if (!strcmp(key, "n_v")) *value = (double)c->n_v;
   else if (!strcmp(key, "kernel_launches")) *value = (double)c->launches;
   else if (!strcmp(key, "prof_k_count")) *value = (double)c->prof_n;
+  else if (!strcmp(key, "occ_k2")) {  // resident CTAs per SM of the large-mesh fused K kernel
+    int nb = 0;
+    CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_K2_fused<4, 8, 8, 2>, FK2<4, 8, 8>::NTH,
+                                                              FK2<4, 8, 8>::SMEM));
+    *value = nb;
+  } else if (!strcmp(key, "occ_a2")) {
+    int nb = 0;
+    CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_A_tile<4, 4, 2, 4>, 96, Tile2<4, 4, 2>::SMEM));
+    *value = nb;
+  }
   else if (!strcmp(key, "prof_k_ms")) {
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     double t = 0.0;
@@ -795,6 +839,13 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
   } else if (!strcmp(key, "graph")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "graph must be 0 or 1");
     c->use_graph = (int)value;
+  } else if (!strcmp(key, "k_variant")) {
+    if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k_variant must be 0 or 1");
+    c->k_var = (int)value;
+    clear_graphs(c);
+  } else if (!strcmp(key, "k_dbg")) {  // timing probe only: 0x100 / 0x200 / 0x400 skip phases
+    c->k_dbg = ((int)value) & 0xff00;
+    clear_graphs(c);
   } else if (!strcmp(key, "profile")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "profile must be 0 or 1");
     c->profile = (int)value;

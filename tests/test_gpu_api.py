@@ -174,6 +174,19 @@ def test_full_size_pcg_prefix(full):
     assert rel_l2(x, full.o.poisson(st["Dinv"], st["diagKr"], b, 5)) <= 1e-12
 
 
+def test_full_size_repeat_bitwise(full):
+    """Race detector: repeated launches at full size are bitwise identical
+    (A's tile look-back and staged loads, the fused K kernel, the PCG loop)."""
+    c = full.ctx
+    u, r = dev(full.inp["u"]), dev(full.inp["p"])
+    ya = host(c.apply_A(u, empty(c.n_v)))
+    for _ in range(10):
+        assert np.array_equal(host(c.apply_A(u, empty(c.n_v))), ya)
+    xk = host(c.poisson_pcg(1, r, empty(c.n_p), 10))
+    for _ in range(5):
+        assert np.array_equal(host(c.poisson_pcg(1, r, empty(c.n_p), 10)), xk)
+
+
 def test_full_size_wbfbt_properties(full):
     """At full size with the config's PCG count: finite, projected, deterministic,
     and the Poisson relative residuals agree with the oracle's within 2x

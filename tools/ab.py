@@ -52,3 +52,12 @@ c.set_option("graph", 1)
 it = synth.CONFIGS[cfg].iters
 print(f"wBFBT({it}): {timed(lambda: c.apply_wbfbt(p, pv, it), reps=5, cold=False):.1f} us")
 print(f"setup: {timed(lambda: c.set_viscosity(mu), reps=5):.1f} us")
+for kv in (0, 1):
+    c.set_option("k_variant", kv)
+    t10 = timed(lambda: c.poisson_pcg(1, p, pv, 10), reps=10, cold=False)
+    t50 = timed(lambda: c.poisson_pcg(1, p, pv, 50), reps=10, cold=False)
+    c.set_option("profile", 1)
+    c.poisson_pcg(1, p, pv, 20)
+    kms = c.query("prof_k_ms") / c.query("prof_k_count")
+    c.set_option("profile", 0)
+    print(f"k_variant={kv}: per-iter {(t50 - t10) / 40:.2f} us, K kernel {kms*1e3:.2f} us")
