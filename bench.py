@@ -118,13 +118,25 @@ def barrier(world):
 
 
 def max_over_ranks(x, world):
+    """Max of a per-rank scalar (device time) over all ranks (NCCL on GPUs, gloo on CPU)."""
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def replica_seed(rank):
+    """Replicas only: rank r solves its own problem, seed r."""
+    return rank
+
+
+def job_throughput(world, steps, max_ms):
+    """Whole-job steps/s: all ranks' steps over the slowest rank's device time."""
+    return world * steps / (max_ms * 1e-3)
 
 
 # ---------------------------------------------------------------------- reference arm (CPU oracle)
@@ -189,7 +201,7 @@ def run_ours(args):
 
     rank, world, local = dist_init(args.gpus)
     cfg = synth.CONFIGS[args.config]
-    inp = synth.make_inputs(cfg, seed=rank)
+    inp = synth.make_inputs(cfg, seed=replica_seed(rank))
     stream = torch.cuda.current_stream()
     ctx = Context(cfg.N, cfg.k, stream=stream.cuda_stream)
     d = lambda a: torch.as_tensor(a, dtype=torch.float64, device="cuda")  # noqa: E731
@@ -221,7 +233,7 @@ def run_ours(args):
     t_ms = sum(a.elapsed_time(b) for a, b in ev)
     t_ms = max_over_ranks(t_ms, world)
     ms_per_step = t_ms / args.steps
-    value = world * args.steps / (t_ms * 1e-3)
+    value = job_throughput(world, args.steps, t_ms)
 
     # ---- component timings (same context, L2 flushed before each rep)
     def timed(fn, reps=args.comp_reps):
