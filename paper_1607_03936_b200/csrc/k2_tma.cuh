@@ -1,0 +1,264 @@
+// k2_tma.cuh -- the fused k = 2 Poisson operator (k2_fused.cuh) with TMA
+// staging: persistent CTAs (one per SM) walk the element tiles; the halo box of
+// p_old, r, Minv (4-D tensor maps over the mode-major PCG vectors, hardware
+// zero fill outside the mesh) and the X box (3-D tensor map over a copy of X
+// with 16-byte-aligned rows) land in shared memory by cp.async.bulk.tensor,
+// completion tracked by mbarriers.  Each buffer is refilled for the NEXT tile
+// as soon as the current tile has consumed it (r, Minv after step 0, X after
+// step 1, p after step 2), so the loads overlap the compute of steps 1 and 2.
+// Same arithmetic as k_K2_fused (identical per-node / per-element order).
+#pragma once
+#include <cuda.h>
+#include "k2_fused.cuh"
+
+namespace wb {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred P;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Layout constants of the TMA variant (tile TX x TY x TZ elements).
+// TMA tile loads of fp64 need the innermost start coordinate 16-byte aligned
+// (even): the element box starts at ex0 - 2 (ex0 is a multiple of 4) and is
+// BXW = TX + 4 wide; halo element hx (= ex0 - 1 + hx) sits at box column hx + 1.
+// Step 0 repacks the boxes into Ps (odd row stride FK2::PX, conflict-free).
+template <int TX, int TY, int TZ>
+struct FKT {
+  using F = FK2<TX, TY, TZ>;
+  static constexpr int HX = TX + 2, HY = TY + 2, HZ = TZ + 2;
+  static constexpr int BXW = TX + 4, NB = BXW * HY * HZ;  // raw box (BXW, HY, HZ, 4)
+  static constexpr int XB = (F::MX + 1) & ~1;             // X box row (16-byte multiple), start 2 ex0 (even)
+  static constexpr int NX = XB * F::MY * F::MZ;
+  static constexpr unsigned PBYTES = 4u * NB * 8u, XBYTES = (unsigned)NX * 8u;
+  // shared layout (bytes): raw p | raw r | raw Minv | Ps | X | T | barriers, each 1024-aligned
+  static constexpr size_t al(size_t b) { return (b + 1023) & ~(size_t)1023; }
+  static constexpr size_t OFF_P = 0, OFF_R = al(PBYTES), OFF_M = OFF_R + al(PBYTES), OFF_S = OFF_M + al(PBYTES),
+                          OFF_X = OFF_S + al(4u * F::NH * 8u), OFF_T = OFF_X + al(XBYTES),
+                          OFF_B = OFF_T + al(3u * F::NN * 8u);
+  static constexpr size_t SMEM = OFF_B + 64 + 1024;  // + slack for 1024-byte base alignment
+};
+
+// x-pencil as in fk2_pencil, with the TMA box layouts: Ps rows of HX, Xs rows of XB (natural x order)
+template <int TX, int TY, int TZ, int RY, int RZ>
+__device__ __forceinline__ void fkt_pencil(const double* __restrict__ Ps, double* __restrict__ T,
+                                           const double* __restrict__ Xs, int jy, int jz, double sB) {
+  using F = FK2<TX, TY, TZ>;
+  using K = FKT<TX, TY, TZ>;
+  const int ny = 2 * jy + RY, nz = 2 * jz + RZ;
+  double acc[3][F::MX];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int nx = 0; nx < F::MX; ++nx) acc[c][nx] = 0.0;
+#pragma unroll
+  for (int iz = 0; iz < (RZ ? 1 : 2); ++iz) {
+    const int qz = RZ ? jz + 1 : jz + iz;
+    const int az = RZ ? 1 : (iz == 0 ? 2 : 0);
+#pragma unroll
+    for (int iy = 0; iy < (RY ? 1 : 2); ++iy) {
+      const int qy = RY ? jy + 1 : jy + iy;
+      const int ay = RY ? 1 : (iy == 0 ? 2 : 0);
+      const double* Pr = Ps + F::PX * (qy + F::HY * qz);
+#pragma unroll
+      for (int qx = 0; qx < K::HX; ++qx) {
+        double pm[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) pm[m] = Pr[m * F::NH + qx];
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+          const int nx = 2 * qx - 2 + ax;
+          if (nx < 0 || nx >= F::MX) continue;
+          const int a = ax + 3 * (ay + 3 * az);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            if (bt2_nz(0, a, m)) acc[0][nx] = fma(c_Bt2[0][a][m], pm[m], acc[0][nx]);
+            if (bt2_nz(1, a, m)) acc[1][nx] = fma(c_Bt2[1][a][m], pm[m], acc[1][nx]);
+            if (bt2_nz(2, a, m)) acc[2][nx] = fma(c_Bt2[2][a][m], pm[m], acc[2][nx]);
+          }
+        }
+      }
+    }
+  }
+  double* Tr = T + F::RS * (ny + F::MY * nz);
+  const double* Xr = Xs + K::XB * (ny + F::MY * nz);
+#pragma unroll
+  for (int nx = 0; nx < F::MX; ++nx) {
+    const double f = sB * Xr[nx];  // zero-filled outside the mesh; X = 0 on the boundary
+#pragma unroll
+    for (int c = 0; c < 3; ++c) Tr[c * F::NN + F::col(nx)] = f * acc[c][nx];
+  }
+}
+
+// Same contract as k_K2_fused (mode, ctl, partials), tensor maps instead of pointers for the
+// loads: tm_pold / tm_r / tm_minv over [m][ez][ey][ex], tm_x over the padded nodal X.
+template <int TX, int TY, int TZ>
+__global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, 1)
+    k_K2_tma(const __grid_constant__ CUtensorMap tm_pold, const __grid_constant__ CUtensorMap tm_r,
+             const __grid_constant__ CUtensorMap tm_minv, const __grid_constant__ CUtensorMap tm_x,
+             double* __restrict__ pnew, double* __restrict__ q, Geo G, double sB, int mode, int it, int ctl,
+             const double* __restrict__ rzp, int nrz, double* rz_hist, const double* pq_hist, int* stop,
+             double* pqp) {
+  using F = FK2<TX, TY, TZ>;
+  using K = FKT<TX, TY, TZ>;
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sb = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  double* Pb = (double*)(sb + K::OFF_P);  // raw boxes (BXW x HY x HZ x 4)
+  double* Rb = (double*)(sb + K::OFF_R);
+  double* Mb = (double*)(sb + K::OFF_M);
+  double* Ps = (double*)(sb + K::OFF_S);  // p on the tile + halo, rows of F::PX
+  double* Xs = (double*)(sb + K::OFF_X);
+  double* T = (double*)(sb + K::OFF_T);
+  uint64_t* bar = (uint64_t*)(sb + K::OFF_B);  // [0] r+Minv, [1] p_old, [2] X
+  const int N = G.N;
+  const int64_t ne = G.n_el;
+  const int NTX = (N + TX - 1) / TX, NTY = (N + TY - 1) / TY, NTZ = (N + TZ - 1) / TZ;
+  const int n_tiles = NTX * NTY * NTZ;
+  double beta = 0.0;
+  if (ctl) {
+    if (pcg_control<F::NTH>(it, rzp, nrz, rz_hist, pq_hist, stop, &beta)) return;
+  } else if (mode == 1) {
+    beta = rz_hist[it] / rz_hist[it - 1];
+  }
+  auto coords = [&](int tile, int& ex0, int& ey0, int& ez0) {
+    ex0 = TX * (tile % NTX); ey0 = TY * ((tile / NTX) % NTY); ez0 = TZ * (tile / (NTX * NTY));
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); mbar_init(&bar[2], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int tile = blockIdx.x;
+  if (threadIdx.x == 0 && tile < n_tiles) {
+    int ex0, ey0, ez0;
+    coords(tile, ex0, ey0, ez0);
+    mbar_expect_tx(&bar[0], 3 * K::PBYTES);
+    tma_load_4d(Rb, &tm_r, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
+    tma_load_4d(Mb, &tm_minv, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
+    tma_load_4d(Pb, &tm_pold, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
+    mbar_expect_tx(&bar[2], K::XBYTES);
+    tma_load_3d(Xs, &tm_x, 2 * ex0, 2 * ey0, 2 * ez0, &bar[2]);
+  }
+  double dot = 0.0;
+  for (int k = 0; tile < n_tiles; ++k, tile += gridDim.x) {
+    const unsigned ph = k & 1;
+    const int next = tile + gridDim.x;
+    int ex0, ey0, ez0, nx0 = 0, ny0 = 0, nz0 = 0;
+    coords(tile, ex0, ey0, ez0);
+    if (next < n_tiles) coords(next, nx0, ny0, nz0);
+    // 0. p = Minv r (+ beta p_old) from the raw boxes into Ps; own elements -> p_new
+    mbar_wait(&bar[0], ph);
+    for (int i = threadIdx.x; i < F::NH; i += F::NTH) {
+      const int hx = i % F::PX, hy = (i / F::PX) % F::HY, hz = i / (F::PX * F::HY);
+      const int ex = ex0 + hx - 1, ey = ey0 + hy - 1, ez = ez0 + hz - 1;
+      const bool own = hx >= 1 && hy >= 1 && hz >= 1 && hx <= TX && hy <= TY && hz <= TZ && ex < N && ey < N &&
+                       ez < N;
+      const int64_t e = ex + (int64_t)N * (ey + (int64_t)N * ez);
+      const int jb = (hx + 1) + K::BXW * (hy + K::HY * hz);  // box column of halo element hx
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int j = m * K::NB + jb;
+        double v = 0.0;
+        if (hx < K::HX) {  // pad column of Ps stays 0
+          if (mode == 2) v = Pb[j];
+          else {
+            const double z = Mb[j] * Rb[j];
+            v = (mode == 1) ? fma(beta, Pb[j], z) : z;
+          }
+        }
+        Ps[m * F::NH + i] = v;
+        if (own) pnew[m * ne + e] = v;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && next < n_tiles) {  // raw p, r, Minv buffers are free
+      fence_proxy_async();
+      mbar_expect_tx(&bar[0], 3 * K::PBYTES);
+      tma_load_4d(Rb, &tm_r, nx0 - 2, ny0 - 1, nz0 - 1, 0, &bar[0]);
+      tma_load_4d(Mb, &tm_minv, nx0 - 2, ny0 - 1, nz0 - 1, 0, &bar[0]);
+      tma_load_4d(Pb, &tm_pold, nx0 - 2, ny0 - 1, nz0 - 1, 0, &bar[0]);
+    }
+    // 1. t at the tile nodes by x-pencils
+    mbar_wait(&bar[2], ph);
+    {
+      const int t = threadIdx.x;
+      if (t < F::OFF1) {
+        if (t < F::cls_n(0, 0)) fkt_pencil<TX, TY, TZ, 0, 0>(Ps, T, Xs, t % (TY + 1), t / (TY + 1), sB);
+      } else if (t < F::OFF2) {
+        const int i = t - F::OFF1;
+        if (i < F::cls_n(1, 0)) fkt_pencil<TX, TY, TZ, 1, 0>(Ps, T, Xs, i % TY, i / TY, sB);
+      } else if (t < F::OFF3) {
+        const int i = t - F::OFF2;
+        if (i < F::cls_n(0, 1)) fkt_pencil<TX, TY, TZ, 0, 1>(Ps, T, Xs, i % (TY + 1), i / (TY + 1), sB);
+      } else {
+        const int i = t - F::OFF3;
+        if (i < F::cls_n(1, 1)) fkt_pencil<TX, TY, TZ, 1, 1>(Ps, T, Xs, i % TY, i / TY, sB);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && next < n_tiles) {  // X buffer is free
+      fence_proxy_async();
+      mbar_expect_tx(&bar[2], K::XBYTES);
+      tma_load_3d(Xs, &tm_x, 2 * nx0, 2 * ny0, 2 * nz0, &bar[2]);
+    }
+    // 2. q = sB Bt^T t per element, <p, q>
+    if (threadIdx.x < F::NE) {
+      const int lx = threadIdx.x % TX, ly = (threadIdx.x / TX) % TY, lz = threadIdx.x / (TX * TY);
+      const int ex = ex0 + lx, ey = ey0 + ly, ez = ez0 + lz;
+      if (ex < N && ey < N && ez < N) {
+        double qm[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int a = 0; a < 27; ++a) {
+            const int ax = a % 3, ay = (a / 3) % 3, az = a / 9;
+            const int cx = ax == 1 ? TX + 1 + lx : lx + (ax >> 1);
+            const double tv = T[c * F::NN + F::RS * ((2 * ly + ay) + F::MY * (2 * lz + az)) + cx];
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+              if (bt2_nz(c, a, m)) qm[m] = fma(c_Bt2[c][a][m], tv, qm[m]);
+          }
+        const int64_t e = ex + (int64_t)N * (ey + (int64_t)N * ez);
+        const int h = (lx + 1) + F::PX * ((ly + 1) + F::HY * (lz + 1));
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const double o = sB * qm[m];
+          q[m * ne + e] = o;
+          dot = fma(Ps[m * F::NH + h], o, dot);
+        }
+      }
+    }
+    __syncthreads();  // Ps, T are rewritten by the next tile
+  }
+  store_partial<F::NTH>(dot, pqp);
+}
+
+}  // namespace wb

@@ -3,6 +3,7 @@
 // The context owns all workspace; every call enqueues kernels on the context
 // stream.  See DESIGN.md for the data layout and the kernel list.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -62,6 +63,13 @@ struct wb_ctx {
   int a_tile = 0;  // k = 2 A tile shape: 0 = 4x4x2 (96 threads), 1 = 4x4x4 (192 threads)
   int use_graph = 1;
   int k_var = 1;  // k = 2 fused K variant: 0 = 2 CTAs/SM (register-capped), 1 = 1 CTA/SM (faster: L1 left free)
+  // TMA variant of the fused K kernel (k = 2, even N, large meshes): tensor maps over the
+  // mode-major PCG vectors and over row-padded copies of C_w^-1 / D_w^-1
+  bool tma_ok = false;
+  int use_tma = 1;
+  double *XpL = nullptr, *XpR = nullptr;
+  int xp = 0;
+  CUtensorMap tm_pp, tm_pp1, tm_pr, tm_mL, tm_mR, tm_xL, tm_xR;
   int k_dbg = 0;  // timing probe bits for the fused K kernel (results invalid when nonzero)
   // profiling: CUDA-event pairs around every Poisson-operator launch (direct launches)
   int profile = 0;
@@ -199,12 +207,95 @@ wb_status launch_k2f_t(wb_ctx* c, const double* pold, double* pnew, const double
   *npq = grid;
   return WB_OK;
 }
+const CUtensorMap* tmap_of(wb_ctx* c, const double* p) {
+  if (p == c->pp) return &c->tm_pp;
+  if (p == c->pp1) return &c->tm_pp1;
+  if (p == c->pr) return &c->tm_pr;
+  if (p == c->MinvL) return &c->tm_mL;
+  if (p == c->MinvR) return &c->tm_mR;
+  if (p == c->Cinv) return &c->tm_xL;
+  if (p == c->Dinv) return &c->tm_xR;
+  return nullptr;
+}
+
 wb_status run_k2f(wb_ctx* c, const double* pold, double* pnew, const double* r, const double* Minv, const double* X,
                   double* q, int mode, PcgArgs a, int* npq) {
+  if (c->tma_ok && c->use_tma && c->n_el >= 148 * 256 * 2) {
+    using KT = FKT<4, 8, 8>;
+    const CUtensorMap *tp = tmap_of(c, pold), *tr = tmap_of(c, r ? r : c->pr), *tm = tmap_of(c, Minv),
+                      *tx = tmap_of(c, X);
+    if (tp && tr && tm && tx) {
+      const int N = c->N;
+      const int nt = ((N + 3) / 4) * ((N + 7) / 8) * ((N + 7) / 8);
+      const int grid = std::max(1, std::min(nt, c->nsm));  // persistent, one CTA per SM
+      k_K2_tma<4, 8, 8><<<grid, FK2<4, 8, 8>::NTH, KT::SMEM, c->stream>>>(
+          *tp, *tr, *tm, *tx, pnew, q, c->G, c->sB, mode, a.it, a.ctl, c->rzp, c->red_blocks, rz_hist(c),
+          pq_hist(c), c->stop, c->pqp);
+      LAUNCH_CHECK(c);
+      *npq = grid;
+      return WB_OK;
+    }
+  }
   if (c->n_el >= 148 * 256 * 2)
     return c->k_var == 1 ? launch_k2f_t<4, 8, 8, 1>(c, pold, pnew, r, Minv, X, q, mode, a, npq)
                          : launch_k2f_t<4, 8, 8, 2>(c, pold, pnew, r, Minv, X, q, mode, a, npq);
   return launch_k2f_t<4, 4, 4, 6>(c, pold, pnew, r, Minv, X, q, mode, a, npq);
+}
+
+// ---- TMA tensor maps (driver entry point through the runtime; no libcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+bool get_encode() {
+  if (g_encode) return true;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn) {
+    cudaGetLastError();
+    return false;
+  }
+  g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  return true;
+}
+// mode-major PCG vector [m][ez][ey][ex]: 4-D map, box = one tile + halo, all modes
+bool make_tm_vec(CUtensorMap* tm, const double* base, int N, int nm) {
+  using KT = FKT<4, 8, 8>;
+  const cuuint64_t dims[4] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)nm};
+  const cuuint64_t strides[3] = {(cuuint64_t)N * 8, (cuuint64_t)N * N * 8, (cuuint64_t)N * N * N * 8};
+  const cuuint32_t box[4] = {(cuuint32_t)KT::BXW, (cuuint32_t)KT::HY, (cuuint32_t)KT::HZ, (cuuint32_t)nm};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// nodal X with rows padded to xp: 3-D map, box = the tile's (2T+1)^3 nodes (row rounded up to even)
+bool make_tm_x(CUtensorMap* tm, const double* base, int nn1, int xp) {
+  using KT = FKT<4, 8, 8>;
+  using F = FK2<4, 8, 8>;
+  const cuuint64_t dims[3] = {(cuuint64_t)nn1, (cuuint64_t)nn1, (cuuint64_t)nn1};
+  const cuuint64_t strides[2] = {(cuuint64_t)xp * 8, (cuuint64_t)xp * nn1 * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)KT::XB, (cuuint32_t)F::MY, (cuuint32_t)F::MZ};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+bool setup_tma(wb_ctx* c) {
+  if (c->k != 2 || (c->N & 1) || !get_encode()) return false;
+  c->xp = (c->G.nn1 + 1) & ~1;
+  const size_t bx = sizeof(double) * (size_t)c->G.nn1 * c->G.nn1 * c->xp;
+  if (cudaMalloc(&c->XpL, bx) != cudaSuccess || cudaMalloc(&c->XpR, bx) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (cudaFuncSetAttribute(k_K2_tma<4, 8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)FKT<4, 8, 8>::SMEM) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return make_tm_vec(&c->tm_pp, c->pp, c->N, c->nm) && make_tm_vec(&c->tm_pp1, c->pp1, c->N, c->nm) &&
+         make_tm_vec(&c->tm_pr, c->pr, c->N, c->nm) && make_tm_vec(&c->tm_mL, c->MinvL, c->N, c->nm) &&
+         make_tm_vec(&c->tm_mR, c->MinvR, c->N, c->nm) && make_tm_x(&c->tm_xL, c->XpL, c->G.nn1, c->xp) &&
+         make_tm_x(&c->tm_xR, c->XpR, c->G.nn1, c->xp);
 }
 
 wb_status configure_kernels(wb_ctx* c) {
@@ -432,6 +523,9 @@ void free_all(wb_ctx* c) {
   c->tflag = nullptr; c->ticket = nullptr;
   if (c->stop) cudaFree(c->stop);
   if (c->icount) cudaFree(c->icount);
+  if (c->XpL) cudaFree(c->XpL);
+  if (c->XpR) cudaFree(c->XpR);
+  c->XpL = c->XpR = nullptr;
   c->counter = nullptr; c->stop = nullptr; c->icount = nullptr;
 }
 
@@ -533,6 +627,7 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
     delete c;
     return WB_ECUDA;
   }
+  c->tma_ok = setup_tma(c);  // optional fast path; the pointer kernel serves when unavailable
   *out = c;
   return WB_OK;
 }
@@ -602,6 +697,12 @@ static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
   k_lump_node<K><<<nblk(c->n_nodes, 256), 256, 0, c->stream>>>(c->E, a_l, a_r, c->Cw, c->Dw, c->Cinv, c->Dinv,
                                                                c->icount + 1, c->G);
   LAUNCH_CHECK(c);
+  if (c->tma_ok) {  // row-padded copies for the TMA tensor maps of the fused K kernel
+    k_pad_rows<<<c->red_blocks, VBS, 0, c->stream>>>(c->Cinv, c->XpL, c->G.nn1, c->xp);
+    LAUNCH_CHECK(c);
+    k_pad_rows<<<c->red_blocks, VBS, 0, c->stream>>>(c->Dinv, c->XpR, c->G.nn1, c->xp);
+    LAUNCH_CHECK(c);
+  }
   k_jacobi<K><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(c->Cinv, c->Dinv, c->dKl, c->dKr, c->MinvL, c->MinvR,
                                                          c->G, c->sB);
   LAUNCH_CHECK(c);
@@ -842,6 +943,10 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
   } else if (!strcmp(key, "k_variant")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k_variant must be 0 or 1");
     c->k_var = (int)value;
+    clear_graphs(c);
+  } else if (!strcmp(key, "tma")) {
+    if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "tma must be 0 or 1");
+    c->use_tma = (int)value;
     clear_graphs(c);
   } else if (!strcmp(key, "k_dbg")) {  // timing probe only: 0x100 / 0x200 / 0x400 skip phases
     c->k_dbg = ((int)value) & 0xff00;
