@@ -59,11 +59,26 @@ struct FKT {
   static constexpr int XB = (F::MX + 1) & ~1;             // X box row (16-byte multiple), start 2 ex0 (even)
   static constexpr int NX = XB * F::MY * F::MZ;
   static constexpr unsigned PBYTES = 4u * NB * 8u, XBYTES = (unsigned)NX * 8u;
+  // Ps[m][qx][qz][qy]: a pencil's (qy, qz) row is the fastest index, so the lanes of a
+  // pencil class (consecutive qy) read consecutive words
+  static constexpr int NHP = HX * HY * HZ;
+  __host__ __device__ static constexpr int pidx(int qx, int qy, int qz) { return qy + HY * (qz + HZ * qx); }
+  // T[c][col(nx)][row]: rows grouped by class (ny%2, nz%2), row = off[cls] + jy + CY jz;
+  // column stride TC = 4 (mod 16) makes step 2 (4 x-elements x 4 y-elements per
+  // half-warp) conflict-free, class-local rows make the pencil stores conflict-free
+  static constexpr int R00 = (TY + 1) * (TZ + 1), R10 = TY * (TZ + 1), R01 = (TY + 1) * TZ, R11 = TY * TZ;
+  static constexpr int NROW = R00 + R10 + R01 + R11;
+  static constexpr int TC = NROW + ((20 - NROW % 16) % 16);
+  static constexpr int TN = F::MX * TC;
+  __host__ __device__ static constexpr int row(int ny, int nz) {
+    return ((ny & 1) ? ((nz & 1) ? R00 + R10 + R01 : R00) : ((nz & 1) ? R00 + R10 : 0)) +
+           (ny >> 1) + ((ny & 1) ? TY : TY + 1) * (nz >> 1);
+  }
   // shared layout (bytes): raw p | raw r | raw Minv | Ps | X | T | barriers, each 1024-aligned
   static constexpr size_t al(size_t b) { return (b + 1023) & ~(size_t)1023; }
   static constexpr size_t OFF_P = 0, OFF_R = al(PBYTES), OFF_M = OFF_R + al(PBYTES), OFF_S = OFF_M + al(PBYTES),
-                          OFF_X = OFF_S + al(4u * F::NH * 8u), OFF_T = OFF_X + al(XBYTES),
-                          OFF_B = OFF_T + al(3u * F::NN * 8u);
+                          OFF_X = OFF_S + al(4u * NHP * 8u), OFF_T = OFF_X + al(XBYTES),
+                          OFF_B = OFF_T + al(3u * TN * 8u);
   static constexpr size_t SMEM = OFF_B + 64 + 1024;  // + slack for 1024-byte base alignment
 };
 
@@ -87,12 +102,11 @@ __device__ __forceinline__ void fkt_pencil(const double* __restrict__ Ps, double
     for (int iy = 0; iy < (RY ? 1 : 2); ++iy) {
       const int qy = RY ? jy + 1 : jy + iy;
       const int ay = RY ? 1 : (iy == 0 ? 2 : 0);
-      const double* Pr = Ps + F::PX * (qy + F::HY * qz);
 #pragma unroll
       for (int qx = 0; qx < K::HX; ++qx) {
         double pm[4];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) pm[m] = Pr[m * F::NH + qx];
+        for (int m = 0; m < 4; ++m) pm[m] = Ps[m * K::NHP + K::pidx(qx, qy, qz)];
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
           const int nx = 2 * qx - 2 + ax;
@@ -108,13 +122,13 @@ __device__ __forceinline__ void fkt_pencil(const double* __restrict__ Ps, double
       }
     }
   }
-  double* Tr = T + F::RS * (ny + F::MY * nz);
+  double* Tr = T + K::row(ny, nz);
   const double* Xr = Xs + K::XB * (ny + F::MY * nz);
 #pragma unroll
   for (int nx = 0; nx < F::MX; ++nx) {
     const double f = sB * Xr[nx];  // zero-filled outside the mesh; X = 0 on the boundary
 #pragma unroll
-    for (int c = 0; c < 3; ++c) Tr[c * F::NN + F::col(nx)] = f * acc[c][nx];
+    for (int c = 0; c < 3; ++c) Tr[c * K::TN + F::col(nx) * K::TC] = f * acc[c][nx];
   }
 }
 
@@ -129,8 +143,10 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, 1)
              double* pqp) {
   using F = FK2<TX, TY, TZ>;
   using K = FKT<TX, TY, TZ>;
-  extern __shared__ unsigned char smraw[];
-  unsigned char* sb = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  // offsets from the (1024-aligned) dynamic shared base itself, so that every access
+  // below stays a shared-space access (LDS/STS), not a generic one
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sb = smraw;
   double* Pb = (double*)(sb + K::OFF_P);  // raw boxes (BXW x HY x HZ x 4)
   double* Rb = (double*)(sb + K::OFF_R);
   double* Mb = (double*)(sb + K::OFF_M);
@@ -176,8 +192,8 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, 1)
     if (next < n_tiles) coords(next, nx0, ny0, nz0);
     // 0. p = Minv r (+ beta p_old) from the raw boxes into Ps; own elements -> p_new
     mbar_wait(&bar[0], ph);
-    for (int i = threadIdx.x; i < F::NH; i += F::NTH) {
-      const int hx = i % F::PX, hy = (i / F::PX) % F::HY, hz = i / (F::PX * F::HY);
+    for (int i = threadIdx.x; i < K::NHP; i += F::NTH) {
+      const int hx = i % K::HX, hy = (i / K::HX) % K::HY, hz = i / (K::HX * K::HY);
       const int ex = ex0 + hx - 1, ey = ey0 + hy - 1, ez = ez0 + hz - 1;
       const bool own = hx >= 1 && hy >= 1 && hz >= 1 && hx <= TX && hy <= TY && hz <= TZ && ex < N && ey < N &&
                        ez < N;
@@ -194,7 +210,7 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, 1)
             v = (mode == 1) ? fma(beta, Pb[j], z) : z;
           }
         }
-        Ps[m * F::NH + i] = v;
+        Ps[m * K::NHP + K::pidx(hx, hy, hz)] = v;
         if (own) pnew[m * ne + e] = v;
       }
     }
@@ -241,18 +257,18 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, 1)
           for (int a = 0; a < 27; ++a) {
             const int ax = a % 3, ay = (a / 3) % 3, az = a / 9;
             const int cx = ax == 1 ? TX + 1 + lx : lx + (ax >> 1);
-            const double tv = T[c * F::NN + F::RS * ((2 * ly + ay) + F::MY * (2 * lz + az)) + cx];
+            const double tv = T[c * K::TN + cx * K::TC + K::row(2 * ly + ay, 2 * lz + az)];
 #pragma unroll
             for (int m = 0; m < 4; ++m)
               if (bt2_nz(c, a, m)) qm[m] = fma(c_Bt2[c][a][m], tv, qm[m]);
           }
         const int64_t e = ex + (int64_t)N * (ey + (int64_t)N * ez);
-        const int h = (lx + 1) + F::PX * ((ly + 1) + F::HY * (lz + 1));
+        const int h = K::pidx(lx + 1, ly + 1, lz + 1);
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
           const double o = sB * qm[m];
           q[m * ne + e] = o;
-          dot = fma(Ps[m * F::NH + h], o, dot);
+          dot = fma(Ps[m * K::NHP + h], o, dot);
         }
       }
     }
