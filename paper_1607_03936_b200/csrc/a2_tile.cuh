@@ -79,28 +79,36 @@ __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) 
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <int NE>
-__device__ __forceinline__ void a2_elem(const double* __restrict__ Mu, const double* __restrict__ u, int64_t e,
-                                        bool valid, int ex, int ey, int ez, int c, int le, double* X,
-                                        const Geo& G, int nomask, double (&V)[27]) {
+// Staged nodal u of a TX x TY x TZ tile: Us[c][nz][ny][RSU], x split by parity
+// (even nodes, then odd) with RSU = 2 (mod 8): 4 x-consecutive elements x 4
+// y-consecutive elements (a half-warp) read 16 distinct bank pairs.
+template <int TX, int TY, int TZ>
+struct UsL {
+  static constexpr int MX = 2 * TX + 1, MY = 2 * TY + 1, MZ = 2 * TZ + 1;
+  static constexpr int RSU = MX + ((10 - MX % 8) % 8);
+  static constexpr int NN = RSU * MY * MZ;
+  __host__ __device__ static constexpr int col(int nx) { return (nx & 1) ? TX + 1 + (nx >> 1) : (nx >> 1); }
+};
+
+template <int TX, int TY, int TZ>
+__device__ __forceinline__ void a2_elem(const double* __restrict__ Mu, const double* __restrict__ Us, bool valid,
+                                        int lx, int ly, int lz, int c, int le, double* X, double (&V)[27]) {
+  constexpr int NE = TX * TY * TZ;
+  using L = UsL<TX, TY, TZ>;
   const K2Coef k = k2coef();
+  // mut and u of the tile, staged in shared memory by cp.async from all threads:
+  // wait for this thread's copies, then a barrier makes everyone's visible
+  cp_async_wait_all();
+  __syncthreads();
   double U[27];
-  {
-    const int64_t s1 = G.nn1, s2 = (int64_t)G.nn1 * G.nn1;
-    const double* ub = u + c * G.n_nodes + node_id(2 * ex, 2 * ey, 2 * ez, G.nn1);
-    // only elements touching the boundary need the per-node Dirichlet test
-    const bool eb = !nomask && (ex == 0 || ey == 0 || ez == 0 || ex == G.N - 1 || ey == G.N - 1 || ez == G.N - 1);
 #pragma unroll
-    for (int az = 0; az < 3; ++az)
+  for (int az = 0; az < 3; ++az)
 #pragma unroll
-      for (int ay = 0; ay < 3; ++ay)
+    for (int ay = 0; ay < 3; ++ay)
 #pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-          double v = valid ? __ldg(ub + ax + ay * s1 + az * s2) : 0.0;
-          if (eb && node_bnd(2 * ex + ax, 2 * ey + ay, 2 * ez + az, G.nn1)) v = 0.0;
-          U3(az, ay, ax) = v;
-        }
-  }
+      for (int ax = 0; ax < 3; ++ax)  // Dirichlet entries were staged as 0
+        U3(az, ay, ax) = Us[c * L::NN + L::RSU * ((2 * ly + ay) + L::MY * (2 * lz + az)) +
+                            (ax == 1 ? TX + 1 + lx : lx + (ax >> 1))];
   // GLL -> Gauss in x, y, z
 #pragma unroll
   for (int z = 0; z < 3; ++z)
@@ -116,11 +124,6 @@ __device__ __forceinline__ void a2_elem(const double* __restrict__ Mu, const dou
     for (int x = 0; x < 3; ++x) k2_interp(k, U3(0, y, x), U3(1, y, x), U3(2, y, x));
 #pragma unroll
   for (int q = 0; q < 27; ++q) V[q] = 0.0;
-  // mut of this element, staged in shared memory by cp.async (Mu[q*NE + le]) by
-  // all threads of the CTA: wait for this thread's copies, then a barrier makes
-  // every thread's copies visible
-  cp_async_wait_all();
-  __syncthreads();
 #pragma unroll
   for (int iz = 0; iz < 3; ++iz) {
     double mu[9];
@@ -188,7 +191,7 @@ struct Tile2 {
   static constexpr int MX = 2 * TX + 1, MY = 2 * TY + 1, MZ = 2 * TZ + 1, NN = MX * MY * MZ;
   static constexpr int SHELL = NN - (2 * TX) * (2 * TY) * (2 * TZ);
   static constexpr int XS = 81 * NE;  // exchange / slot doubles
-  static constexpr size_t SMEM = sizeof(double) * (XS + 27 * NE);  // exchange/slots, staged mut
+  static constexpr size_t SMEM = sizeof(double) * (XS + 27 * NE + 3 * UsL<TX, TY, TZ>::NN);  // exchange/slots, mut, u
   // index of an upper-shell node (nx == 2TX || ny == 2TY || nz == 2TZ)
   __device__ static __forceinline__ int shell(int nx, int ny, int nz) {
     if (nz == 2 * TZ) return ny * MX + nx;
@@ -247,17 +250,32 @@ __global__ void __launch_bounds__(3 * TX * TY * TZ, MINB)
   const int lx = le % TX, ly = (le / TX) % TY, lz = le / (TX * TY);
   const int ex = TX * tx + lx, ey = TY * ty + ly, ez = TZ * tz + lz;
   const bool valid = ex < G.N && ey < G.N && ez < G.N;
-  const int64_t e = valid ? ex + (int64_t)G.N * (ey + (int64_t)G.N * ez) : 0;
   double V[27];
-  // stage the tile's mut (27 per element, element-contiguous) into Mu[q*NE + le] asynchronously
+  // stage the tile's mut (27 per element, element-contiguous) into Mu[q*NE + le] and its
+  // nodal u (Dirichlet entries as 0, the elimination of DESIGN.md R6) into Us,
+  // asynchronously; a2_elem waits for them
   double* Mu = smem_a2 + T::XS;
+  double* Us = Mu + 27 * NE;
   for (int i = threadIdx.x; i < 27 * NE; i += NTH) {
     const int l = i / 27, q = i % 27;
     const int qx = TX * tx + l % TX, qy = TY * ty + (l / TX) % TY, qz = TZ * tz + l / (TX * TY);
     if (qx < G.N && qy < G.N && qz < G.N)
       cp_async8(Mu + q * NE + l, mut + (qx + (int64_t)G.N * (qy + (int64_t)G.N * qz)) * 27 + q);
   }
-  a2_elem<NE>(Mu, u, e, valid, ex, ey, ez, c, le, X, G, nomask, V);
+  {
+    using L = UsL<TX, TY, TZ>;
+    const int bx = 2 * TX * tx, by = 2 * TY * ty, bz = 2 * TZ * tz;
+    for (int i = threadIdx.x; i < 3 * L::MX * L::MY * L::MZ; i += NTH) {
+      const int nx = i % L::MX, ny = (i / L::MX) % L::MY, r = i / (L::MX * L::MY), nz = r % L::MZ, cc = r / L::MZ;
+      const int gx = bx + nx, gy = by + ny, gz = bz + nz;
+      double* dst = Us + cc * L::NN + L::RSU * (ny + L::MY * nz) + L::col(nx);
+      if (gx < G.nn1 && gy < G.nn1 && gz < G.nn1 && (nomask || !node_bnd(gx, gy, gz, G.nn1)))
+        cp_async8(dst, u + cc * G.n_nodes + node_id(gx, gy, gz, G.nn1));
+      else
+        *dst = 0.0;
+    }
+  }
+  a2_elem<TX, TY, TZ>(Mu, Us, valid, lx, ly, lz, c, le, X, V);
   // element slots R[c][a][le] (the exchange buffer is free after the last level's barrier)
 #pragma unroll
   for (int a = 0; a < 27; ++a) X[(c * 27 + a) * NE + le] = V[a];
@@ -278,9 +296,13 @@ __global__ void __launch_bounds__(3 * TX * TY * TZ, MINB)
         Ft[c * T::SHELL + T::shell(2 * lx + AX, 2 * ly + AY, 2 * lz + AZ)] =
             a2_node_sum<TX, TY, TZ>(X, c, lx, ly, lz, AX, AY, AZ);
       }
-  __threadfence();
+  // publish: the barrier orders every thread's F stores before thread 0's gpu-scope
+  // fence (cumulative), then the release store of the flag
   __syncthreads();
-  if (threadIdx.x == 0) asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(flag + tile), "r"(epoch) : "memory");
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(flag + tile), "r"(epoch) : "memory");
+  }
   if (threadIdx.x < 7) {
     const int o = threadIdx.x + 1;
     const int ttx = tx - (o & 1), tty = ty - ((o >> 1) & 1), ttz = tz - (o >> 2);
@@ -300,40 +322,38 @@ __global__ void __launch_bounds__(3 * TX * TY * TZ, MINB)
   const int kN = 2 * G.N;
   const int bx = 2 * TX * tx, by = 2 * TY * ty, bz = 2 * TZ * tz;
   const double* Fc = F + c * T::SHELL;
+  // Straight-line, predicated code: every neighbour partial of every owned node is
+  // loaded before any is summed (no serialised L2 round trips); absent terms are
+  // +0.0, which leaves the fixed-order sum unchanged.
 #pragma unroll
   for (int AZ = 0; AZ < 3; ++AZ)
 #pragma unroll
     for (int AY = 0; AY < 3; ++AY)
 #pragma unroll
       for (int AX = 0; AX < 3; ++AX) {
-        if ((AX == 2 && lx != TX - 1) || (AY == 2 && ly != TY - 1) || (AZ == 2 && lz != TZ - 1)) continue;
+        const bool resp = !((AX == 2 && lx != TX - 1) || (AY == 2 && ly != TY - 1) || (AZ == 2 && lz != TZ - 1));
         const int nx = 2 * lx + AX, ny = 2 * ly + AY, nz = 2 * lz + AZ;
         const int gx = bx + nx, gy = by + ny, gz = bz + nz;
-        if (gx > kN || gy > kN || gz > kN) continue;
-        if ((AX == 2 && gx != kN) || (AY == 2 && gy != kN) || (AZ == 2 && gz != kN)) continue;
-        double acc = 0.0;
-        if (nomask || !node_bnd(gx, gy, gz, G.nn1)) {
-          const bool lowx = nx == 0 && tx > 0, lowy = ny == 0 && ty > 0, lowz = nz == 0 && tz > 0;
+        const bool owned = resp && gx <= kN && gy <= kN && gz <= kN && !(AX == 2 && gx != kN) &&
+                           !(AY == 2 && gy != kN) && !(AZ == 2 && gz != kN);
+        const bool live = owned && (nomask || !node_bnd(gx, gy, gz, G.nn1));
+        const bool lowx = nx == 0 && tx > 0, lowy = ny == 0 && ty > 0, lowz = nz == 0 && tz > 0;
+        double f[7];
 #pragma unroll
-          for (int dz = -1; dz <= 0; ++dz) {
-            if (dz < 0 && !lowz) continue;
-#pragma unroll
-            for (int dy = -1; dy <= 0; ++dy) {
-              if (dy < 0 && !lowy) continue;
-#pragma unroll
-              for (int dx = -1; dx <= 0; ++dx) {
-                if (dx < 0 && !lowx) continue;
-                if (dx == 0 && dy == 0 && dz == 0) {
-                  acc += a2_node_sum<TX, TY, TZ>(X, c, lx, ly, lz, AX, AY, AZ);
-                } else {
-                  const int nt = (tx + dx) + NTX * ((ty + dy) + NTY * (tz + dz));
-                  acc += __ldcg(Fc + (size_t)nt * 3 * T::SHELL + T::shell(dx ? 2 * TX : nx, dy ? 2 * TY : ny, dz ? 2 * TZ : nz));
-                }
-              }
-            }
-          }
+        for (int o = 0; o < 7; ++o) {  // neighbour (dx, dy, dz) in {-1, 0}^3 \ {0}, ascending tile index
+          const int dz = (o < 4) ? -1 : 0, dy = ((o % 4) < 2) ? -1 : 0, dx = (o % 2 == 0) ? -1 : 0;
+          const bool need = live && (dz == 0 || lowz) && (dy == 0 || lowy) && (dx == 0 || lowx);
+          const int nt = (tx + dx) + NTX * ((ty + dy) + NTY * (tz + dz));
+          f[o] = need ? __ldcg(Fc + (size_t)nt * 3 * T::SHELL +
+                               T::shell(dx ? 2 * TX : nx, dy ? 2 * TY : ny, dz ? 2 * TZ : nz))
+                      : 0.0;
         }
-        y[c * G.n_nodes + node_id(gx, gy, gz, G.nn1)] = acc;
+        const double own = live ? a2_node_sum<TX, TY, TZ>(X, c, lx, ly, lz, AX, AY, AZ) : 0.0;
+        double acc = 0.0;
+#pragma unroll
+        for (int o = 0; o < 7; ++o) acc += f[o];
+        acc += own;
+        if (owned) y[c * G.n_nodes + node_id(gx, gy, gz, G.nn1)] = live ? acc : 0.0;
       }
 }
 

@@ -54,13 +54,15 @@ struct wb_ctx {
   unsigned long long* icount = nullptr;  // [0] bad mu, [1] nonpos Cw, [2] nonpos Dw
   int red_blocks = 0, max_partials = 0, nsm = 148;
   double* stage = nullptr;  // wb_hotpath_host staging (lazily allocated)
+  cudaStream_t copy_stream = nullptr;  // wb_hotpath_host: copies overlapped with compute
+  cudaEvent_t ev_in = nullptr, ev_ab = nullptr, ev_bt = nullptr, ev_done = nullptr;
   // k = 2 tile-assembled A: face partials, flags, ticket counter
   double* F = nullptr;
   int* tflag = nullptr;
   unsigned long long* ticket = nullptr;
   unsigned long long ticket_base = 0;
   int epoch = 0, n_tiles = 0;
-  int a_tile = 0;  // k = 2 A tile shape: 0 = 4x4x2 (96 threads), 1 = 4x4x4 (192 threads)
+  int a_tile = 1;  // k = 2 A tile shape: 0 = 4x4x2 (96 threads), 1 = 4x4x4 (192 threads, default: faster)
   int use_graph = 1;
   int k_var = 1;  // k = 2 fused K variant: 0 = 2 CTAs/SM (register-capped), 1 = 1 CTA/SM (faster: L1 left free)
   // TMA variant of the fused K kernel (k = 2, even N, large meshes): tensor maps over the
@@ -513,6 +515,9 @@ void free_all(wb_ctx* c) {
                      &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->F};
   clear_graphs(c);
   if (c->cap_stream) { cudaStreamDestroy(c->cap_stream); c->cap_stream = nullptr; }
+  if (c->copy_stream) { cudaStreamDestroy(c->copy_stream); c->copy_stream = nullptr; }
+  for (cudaEvent_t* e : {&c->ev_in, &c->ev_ab, &c->ev_bt, &c->ev_done})
+    if (*e) { cudaEventDestroy(*e); *e = nullptr; }
   for (int i = 0; i < 2 * wb_ctx::PROF_MAX; ++i)
     if (c->prof_ev[i]) { cudaEventDestroy(c->prof_ev[i]); c->prof_ev[i] = nullptr; }
   for (double** b : bufs)
@@ -819,15 +824,41 @@ wb_status wb_hotpath_host(wb_ctx* c, const double* mu_q, double a_l, double a_r,
   double* dpB = dp + rp;
   double* dz = dpB + rp;
   const size_t bmu = sizeof(double) * nmu, bv = sizeof(double) * c->n_v, bp = sizeof(double) * c->n_p;
+  // Copies overlap compute (pinned host memory makes them asynchronous): u and p
+  // travel on a copy stream during the setup; yA, pB and yBT travel back while the
+  // wBFBT PCG loops run; only mu in and z out are on the critical path.
+  if (!c->copy_stream) {
+    if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      c->copy_stream = nullptr;
+      cudaGetLastError();
+      return set_err(c, WB_ECUDA, "copy stream creation failed");
+    }
+    for (cudaEvent_t* e : {&c->ev_in, &c->ev_ab, &c->ev_bt, &c->ev_done})
+      CUDA_TRY(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  cudaStream_t cs = c->copy_stream;
+  CUDA_TRY(c, cudaEventRecord(c->ev_done, c->stream));  // previous work on the context stream
+  CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_done, 0));
   CUDA_TRY(c, cudaMemcpyAsync(dmu, mu_q, bmu, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(du, u, bv, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(dp, p, bp, cudaMemcpyHostToDevice, c->stream));
-  wb_status s = wb_hotpath(c, dmu, a_l, a_r, du, dp, iters, dyA, dpB, dyBT, dz);
+  CUDA_TRY(c, cudaMemcpyAsync(du, u, bv, cudaMemcpyHostToDevice, cs));
+  CUDA_TRY(c, cudaMemcpyAsync(dp, p, bp, cudaMemcpyHostToDevice, cs));
+  CUDA_TRY(c, cudaEventRecord(c->ev_in, cs));
+  wb_status s = wb_set_viscosity(c, dmu, a_l, a_r);  // synchronous (status)
   if (s) return s;
-  CUDA_TRY(c, cudaMemcpyAsync(yA, dyA, bv, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(pB, dpB, bp, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(yBT, dyBT, bv, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_in, 0));
+  if ((s = wb_apply_A(c, du, dyA))) return s;
+  if ((s = wb_apply_B(c, du, dpB))) return s;
+  CUDA_TRY(c, cudaEventRecord(c->ev_ab, c->stream));
+  if ((s = wb_apply_BT(c, dp, dyBT))) return s;
+  CUDA_TRY(c, cudaEventRecord(c->ev_bt, c->stream));
+  CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_ab, 0));
+  CUDA_TRY(c, cudaMemcpyAsync(yA, dyA, bv, cudaMemcpyDeviceToHost, cs));
+  CUDA_TRY(c, cudaMemcpyAsync(pB, dpB, bp, cudaMemcpyDeviceToHost, cs));
+  CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_bt, 0));
+  CUDA_TRY(c, cudaMemcpyAsync(yBT, dyBT, bv, cudaMemcpyDeviceToHost, cs));
+  if ((s = wb_apply_wbfbt(c, dp, dz, iters))) return s;
   CUDA_TRY(c, cudaMemcpyAsync(z, dz, bp, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(cs));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return WB_OK;
 }
