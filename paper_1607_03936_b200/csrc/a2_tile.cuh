@@ -14,14 +14,12 @@
 // The exchange of g_jc between the three component threads of an element goes
 // through shared memory one Gauss level at a time.
 //
-// Assembly: the TX x TY x TZ element tile sums its (2TX+1)(2TY+1)(2TZ+1)
-// nodes in shared memory in a fixed order (ascending element index); nodes on
-// the tile's upper faces go to a per-tile partial buffer F (L2-resident), and
-// every node is finalised by the tile that owns it (local index < 2T, or the
-// domain end) after a release/acquire look-back on its lower neighbours'
-// flags: partials are added in ascending tile index.  Tiles take logical
-// indices from an atomic ticket, so a tile only ever waits for tiles that have
-// already started: no deadlock, no dependence on hardware launch order.
+// Assembly (deterministic, no atomics, no inter-CTA waiting): the TX x TY x TZ
+// element tile sums its (2TX+1)(2TY+1)(2TZ+1) nodes in shared memory in a fixed
+// order (ascending element index).  Tile-interior nodes are complete and go
+// straight to y; nodes on the tile's upper shell and lower faces go to small
+// partial buffers (L2-resident), and a second kernel (k_A_skel) sums every
+// tile-skeleton node over the tiles holding it in ascending tile index.
 #pragma once
 #include "kernels.cuh"
 
@@ -189,14 +187,21 @@ template <int TX, int TY, int TZ>
 struct Tile2 {
   static constexpr int NE = TX * TY * TZ, NT = 3 * NE;
   static constexpr int MX = 2 * TX + 1, MY = 2 * TY + 1, MZ = 2 * TZ + 1, NN = MX * MY * MZ;
-  static constexpr int SHELL = NN - (2 * TX) * (2 * TY) * (2 * TZ);
+  static constexpr int SHELL = NN - (2 * TX) * (2 * TY) * (2 * TZ);                             // upper shell
+  static constexpr int LF = (2 * TX) * (2 * TY) * (2 * TZ) - (2 * TX - 1) * (2 * TY - 1) * (2 * TZ - 1);  // lower faces
   static constexpr int XS = 81 * NE;  // exchange / slot doubles
   static constexpr size_t SMEM = sizeof(double) * (XS + 27 * NE + 3 * UsL<TX, TY, TZ>::NN);  // exchange/slots, mut, u
   // index of an upper-shell node (nx == 2TX || ny == 2TY || nz == 2TZ)
-  __device__ static __forceinline__ int shell(int nx, int ny, int nz) {
+  __host__ __device__ static __forceinline__ int shell(int nx, int ny, int nz) {
     if (nz == 2 * TZ) return ny * MX + nx;
     if (ny == 2 * TY) return MX * MY + nz * MX + nx;
     return MX * MY + 2 * TZ * MX + nz * (2 * TY) + ny;
+  }
+  // index of a lower-face node (all n_d < 2T_d, some n_d == 0)
+  __host__ __device__ static __forceinline__ int lface(int nx, int ny, int nz) {
+    if (nz == 0) return ny * (2 * TX) + nx;
+    if (ny == 0) return (2 * TX) * (2 * TY) + (nz - 1) * (2 * TX) + nx;
+    return (2 * TX) * (2 * TY) + (2 * TZ - 1) * (2 * TX) + (nz - 1) * (2 * TY - 1) + (ny - 1);
   }
 };
 
@@ -231,50 +236,72 @@ __device__ __forceinline__ double a2_node_sum(const double* __restrict__ R, int 
   return acc;
 }
 
-template <int TX, int TY, int TZ, int MINB>
-__global__ void __launch_bounds__(3 * TX * TY * TZ, MINB)
-    k_A_tile(const double* __restrict__ mut, const double* __restrict__ u, double* __restrict__ y,
-             double* __restrict__ F, int* __restrict__ flag, unsigned long long* ticket,
-             unsigned long long ticket_base, int epoch, Geo G, int nomask) {
-  using T = Tile2<TX, TY, TZ>;
-  constexpr int NE = T::NE, NTH = T::NT;
-  extern __shared__ __align__(16) double smem_a2[];
-  double* X = smem_a2;  // [XS]: gradient exchange, then element slots R[c][a][le]
-  __shared__ int s_tile;
-  if (threadIdx.x == 0) s_tile = (int)(atomicAdd(ticket, 1ull) - ticket_base);
-  __syncthreads();
-  const int tile = s_tile;
-  const int NTX = (G.N + TX - 1) / TX, NTY = (G.N + TY - 1) / TY;
-  const int tx = tile % NTX, ty = (tile / NTX) % NTY, tz = tile / (NTX * NTY);
-  const int le = threadIdx.x % NE, c = threadIdx.x / NE;
-  const int lx = le % TX, ly = (le / TX) % TY, lz = le / (TX * TY);
-  const int ex = TX * tx + lx, ey = TY * ty + ly, ez = TZ * tz + lz;
-  const bool valid = ex < G.N && ey < G.N && ez < G.N;
-  double V[27];
-  // stage the tile's mut (27 per element, element-contiguous) into Mu[q*NE + le] and its
-  // nodal u (Dirichlet entries as 0, the elimination of DESIGN.md R6) into Us,
-  // asynchronously; a2_elem waits for them
-  double* Mu = smem_a2 + T::XS;
-  double* Us = Mu + 27 * NE;
-  for (int i = threadIdx.x; i < 27 * NE; i += NTH) {
-    const int l = i / 27, q = i % 27;
-    const int qx = TX * tx + l % TX, qy = TY * ty + (l / TX) % TY, qz = TZ * tz + l / (TX * TY);
-    if (qx < G.N && qy < G.N && qz < G.N)
-      cp_async8(Mu + q * NE + l, mut + (qx + (int64_t)G.N * (qy + (int64_t)G.N * qz)) * 27 + q);
-  }
-  {
-    using L = UsL<TX, TY, TZ>;
-    const int bx = 2 * TX * tx, by = 2 * TY * ty, bz = 2 * TZ * tz;
-    for (int i = threadIdx.x; i < 3 * L::MX * L::MY * L::MZ; i += NTH) {
-      const int nx = i % L::MX, ny = (i / L::MX) % L::MY, r = i / (L::MX * L::MY), nz = r % L::MZ, cc = r / L::MZ;
+__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+
+// Stage the tile's nodal u (component-major, Dirichlet entries and nodes outside
+// the mesh as 0: the elimination of DESIGN.md R6) into Us.  INNER: the tile's
+// node box lies strictly inside the mesh, no checks.
+template <int TX, int TY, int TZ, bool INNER>
+__device__ __forceinline__ void a2_stage_u(const double* __restrict__ u, double* Us, Geo G, int nomask, int bx,
+                                           int by, int bz) {
+  using L = UsL<TX, TY, TZ>;
+  constexpr int NTH = 3 * TX * TY * TZ;
+  const int nn1 = G.nn1;
+  const double* ub = u + node_id(bx, by, bz, nn1);
+  for (int i = threadIdx.x; i < 3 * L::MX * L::MY * L::MZ; i += NTH) {
+    const int nx = i % L::MX, ny = (i / L::MX) % L::MY, r = i / (L::MX * L::MY), nz = r % L::MZ, cc = r / L::MZ;
+    double* dst = Us + cc * L::NN + L::RSU * (ny + L::MY * nz) + L::col(nx);
+    const double* src = ub + cc * G.n_nodes + (int64_t)(nz * nn1 + ny) * nn1 + nx;
+    if (INNER) {
+      cp_async8(dst, src);
+    } else {
       const int gx = bx + nx, gy = by + ny, gz = bz + nz;
-      double* dst = Us + cc * L::NN + L::RSU * (ny + L::MY * nz) + L::col(nx);
-      if (gx < G.nn1 && gy < G.nn1 && gz < G.nn1 && (nomask || !node_bnd(gx, gy, gz, G.nn1)))
-        cp_async8(dst, u + cc * G.n_nodes + node_id(gx, gy, gz, G.nn1));
+      if (gx < nn1 && gy < nn1 && gz < nn1 && (nomask || !node_bnd(gx, gy, gz, nn1)))
+        cp_async8(dst, src);
       else
         *dst = 0.0;
     }
   }
+}
+
+// Kernel 1 of A: one CTA per TX x TY x TZ element tile, thread per (element,
+// component).  The tile's nodes are summed in shared memory (fixed order, a2_node_sum)
+// and leave the kernel by class:
+//   interior (0 < n_d < 2T_d in every axis): complete -> y;
+//   upper shell (some n_d == 2T_d): partial -> Fu[tile][c][shell];
+//   lower faces (else, some n_d == 0): partial -> Fl[tile][c][lface].
+// mutT is tile-blocked, mutT[tile][q][le] (zero for elements outside the mesh), so a
+// tile's viscosity is one contiguous block.  No inter-CTA communication.
+template <int TX, int TY, int TZ, int MINB>
+__global__ void __launch_bounds__(3 * TX * TY * TZ, MINB)
+    k_A_tile(const double* __restrict__ mutT, const double* __restrict__ u, double* __restrict__ y,
+             double* __restrict__ Fu, double* __restrict__ Fl, Geo G, int nomask) {
+  using T = Tile2<TX, TY, TZ>;
+  constexpr int NE = T::NE, NTH = T::NT;
+  extern __shared__ __align__(16) double smem_a2[];
+  double* X = smem_a2;  // [XS]: gradient exchange, then element slots R[c][a][le]
+  const int tile = blockIdx.x;
+  const int NTX = (G.N + TX - 1) / TX, NTY = (G.N + TY - 1) / TY;
+  const int tx = tile % NTX, ty = (tile / NTX) % NTY, tz = tile / (NTX * NTY);
+  const int le = threadIdx.x % NE, c = threadIdx.x / NE;
+  const int lx = le % TX, ly = (le / TX) % TY, lz = le / (TX * TY);
+  const bool valid = TX * tx + lx < G.N && TY * ty + ly < G.N && TZ * tz + lz < G.N;
+  const int bx = 2 * TX * tx, by = 2 * TY * ty, bz = 2 * TZ * tz;
+  double* Mu = smem_a2 + T::XS;
+  double* Us = Mu + 27 * NE;
+  {
+    const double* src = mutT + (size_t)tile * 27 * NE;
+    for (int i = threadIdx.x; i < 27 * NE / 2; i += NTH) cp_async16(Mu + 2 * i, src + 2 * i);
+  }
+  const int nn1 = G.nn1;
+  if (bx > 0 && by > 0 && bz > 0 && bx + 2 * TX < nn1 - 1 && by + 2 * TY < nn1 - 1 && bz + 2 * TZ < nn1 - 1)
+    a2_stage_u<TX, TY, TZ, true>(u, Us, G, nomask, bx, by, bz);
+  else
+    a2_stage_u<TX, TY, TZ, false>(u, Us, G, nomask, bx, by, bz);
+  double V[27];
   a2_elem<TX, TY, TZ>(Mu, Us, valid, lx, ly, lz, c, le, X, V);
   // element slots R[c][a][le] (the exchange buffer is free after the last level's barrier)
 #pragma unroll
@@ -283,78 +310,139 @@ __global__ void __launch_bounds__(3 * TX * TY * TZ, MINB)
   // Each thread is responsible for the tile nodes 2l + A, A_d in {0, 1}, plus A_d = 2
   // on the tile's upper face (l_d = T_d - 1): every tile node has exactly one
   // responsible (element, c) thread, and the node's structure is compile-time.
-  // Phase A: upper-shell nodes (some A_d = 2) -> F[tile][c][shell]
-  double* Ft = F + (size_t)tile * 3 * T::SHELL;
+  double* Fut = Fu + ((size_t)tile * 3 + c) * T::SHELL;
+  double* Flt = Fl + ((size_t)tile * 3 + c) * T::LF;
+  const int kN = 2 * G.N;
 #pragma unroll
   for (int AZ = 0; AZ < 3; ++AZ)
 #pragma unroll
     for (int AY = 0; AY < 3; ++AY)
 #pragma unroll
       for (int AX = 0; AX < 3; ++AX) {
-        if (AX < 2 && AY < 2 && AZ < 2) continue;
         if ((AX == 2 && lx != TX - 1) || (AY == 2 && ly != TY - 1) || (AZ == 2 && lz != TZ - 1)) continue;
-        Ft[c * T::SHELL + T::shell(2 * lx + AX, 2 * ly + AY, 2 * lz + AZ)] =
-            a2_node_sum<TX, TY, TZ>(X, c, lx, ly, lz, AX, AY, AZ);
+        const int nx = 2 * lx + AX, ny = 2 * ly + AY, nz = 2 * lz + AZ;
+        const double s = a2_node_sum<TX, TY, TZ>(X, c, lx, ly, lz, AX, AY, AZ);
+        if (AX == 2 || AY == 2 || AZ == 2) {
+          Fut[T::shell(nx, ny, nz)] = s;
+        } else if (nx == 0 || ny == 0 || nz == 0) {
+          Flt[T::lface(nx, ny, nz)] = s;
+        } else {
+          const int gx = bx + nx, gy = by + ny, gz = bz + nz;
+          if (gx <= kN && gy <= kN && gz <= kN)
+            y[c * G.n_nodes + node_id(gx, gy, gz, nn1)] = (nomask || !node_bnd(gx, gy, gz, nn1)) ? s : 0.0;
+        }
       }
-  // publish: the barrier orders every thread's F stores before thread 0's gpu-scope
-  // fence (cumulative), then the release store of the flag
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(flag + tile), "r"(epoch) : "memory");
+}
+
+// Kernel 2 of A: the tile-skeleton nodes (g_d a multiple of 2T_d in some axis),
+// one thread per node, all three components.  Each is summed over the tiles
+// whose closed node box holds it, in ascending tile index (per axis the lower
+// tile, whose upper shell holds the node, then the upper one), from 0.0: a fixed
+// order, so results are bitwise reproducible.  Node enumeration: x-planes, then
+// y-planes off the x-planes, then z-planes off both.
+__device__ __forceinline__ int a2_offplane(int k, int M) { return (k / (M - 1)) * M + k % (M - 1) + 1; }
+// node coordinate g on an axis of tile size S (nodes), NT tiles: the first
+// contributing tile t0, the node's local index there n0, and the count (1 or 2; the
+// second tile is t0 + 1 with local index 0)
+__device__ __forceinline__ void a2_axis(int g, int S, int NT, int& t0, int& n0, int& cnt) {
+  const int hi = g / S;
+  if (g - hi * S != 0) { t0 = hi; n0 = g - hi * S; cnt = 1; }
+  else if (hi == 0) { t0 = 0; n0 = 0; cnt = 1; }
+  else { t0 = hi - 1; n0 = S; cnt = hi < NT ? 2 : 1; }
+}
+
+template <int TX, int TY, int TZ>
+__global__ void __launch_bounds__(256) k_A_skel(const double* __restrict__ Fu, const double* __restrict__ Fl,
+                                                double* __restrict__ y, Geo G, int nomask) {
+  using T = Tile2<TX, TY, TZ>;
+  constexpr int SX = 2 * TX, SY = 2 * TY, SZ = 2 * TZ;
+  const int nn1 = G.nn1;
+  const int NTX = (G.N + TX - 1) / TX, NTY = (G.N + TY - 1) / TY, NTZ = (G.N + TZ - 1) / TZ;
+  const int PX = (nn1 - 1) / SX + 1, PY = (nn1 - 1) / SY + 1, PZ = (nn1 - 1) / SZ + 1;
+  const int QX = nn1 - PX, QY = nn1 - PY;
+  const int64_t nX = (int64_t)PX * nn1 * nn1, nY = (int64_t)QX * PY * nn1, nZ = (int64_t)QX * QY * PZ;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int gx, gy, gz;
+  if (i < nX) {
+    gx = SX * (int)(i % PX);
+    const int64_t r = i / PX;
+    gy = (int)(r % nn1); gz = (int)(r / nn1);
+  } else if ((i -= nX) < nY) {
+    gx = a2_offplane((int)(i % QX), SX);
+    const int64_t r = i / QX;
+    gy = SY * (int)(r % PY); gz = (int)(r / PY);
+  } else if ((i -= nY) < nZ) {
+    gx = a2_offplane((int)(i % QX), SX);
+    const int64_t r = i / QX;
+    gy = a2_offplane((int)(r % QY), SY); gz = SZ * (int)(r / QY);
+  } else {
+    return;
   }
-  if (threadIdx.x < 7) {
-    const int o = threadIdx.x + 1;
-    const int ttx = tx - (o & 1), tty = ty - ((o >> 1) & 1), ttz = tz - (o >> 2);
-    if (ttx >= 0 && tty >= 0 && ttz >= 0) {
-      const int* f = flag + (ttx + NTX * (tty + NTY * ttz));
-      int v;
-      while (true) {
-        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-        if (v == epoch) break;
-        __nanosleep(32);
+  const int64_t g = node_id(gx, gy, gz, nn1), nv = G.n_nodes;
+  if (!nomask && node_bnd(gx, gy, gz, nn1)) {
+    y[g] = 0.0; y[nv + g] = 0.0; y[2 * nv + g] = 0.0;
+    return;
+  }
+  // per axis: contributing tiles (ascending, t0 [, t0 + 1]) and the node's local index in each
+  int tx0, nx0, cx, ty0, ny0, cy, tz0, nz0, cz;
+  a2_axis(gx, SX, NTX, tx0, nx0, cx);
+  a2_axis(gy, SY, NTY, ty0, ny0, cy);
+  a2_axis(gz, SZ, NTZ, tz0, nz0, cz);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+  for (int iz = 0; iz < 2; ++iz) {
+    if (iz >= cz) break;
+    const int tz = tz0 + iz, nz = iz ? 0 : nz0;
+#pragma unroll
+    for (int iy = 0; iy < 2; ++iy) {
+      if (iy >= cy) break;
+      const int ty = ty0 + iy, ny = iy ? 0 : ny0;
+#pragma unroll
+      for (int ix = 0; ix < 2; ++ix) {
+        if (ix >= cx) break;
+        const int tile = (tx0 + ix) + NTX * (ty + NTY * tz);
+        const int nx = ix ? 0 : nx0;
+        const double* P;
+        int st;
+        if (nx == SX || ny == SY || nz == SZ) {
+          P = Fu + (size_t)tile * 3 * T::SHELL + T::shell(nx, ny, nz); st = T::SHELL;
+        } else {
+          P = Fl + (size_t)tile * 3 * T::LF + T::lface(nx, ny, nz); st = T::LF;
+        }
+        a0 += __ldcg(P); a1 += __ldcg(P + st); a2 += __ldcg(P + 2 * st);
       }
     }
   }
-  __syncthreads();
-  // Phase B: owned nodes (all A_d < 2, or A_d = 2 at the domain end): lower
-  // neighbours' partials in ascending tile index, then the tile's own sum.
-  const int kN = 2 * G.N;
-  const int bx = 2 * TX * tx, by = 2 * TY * ty, bz = 2 * TZ * tz;
-  const double* Fc = F + c * T::SHELL;
-  // Straight-line, predicated code: every neighbour partial of every owned node is
-  // loaded before any is summed (no serialised L2 round trips); absent terms are
-  // +0.0, which leaves the fixed-order sum unchanged.
-#pragma unroll
-  for (int AZ = 0; AZ < 3; ++AZ)
-#pragma unroll
-    for (int AY = 0; AY < 3; ++AY)
-#pragma unroll
-      for (int AX = 0; AX < 3; ++AX) {
-        const bool resp = !((AX == 2 && lx != TX - 1) || (AY == 2 && ly != TY - 1) || (AZ == 2 && lz != TZ - 1));
-        const int nx = 2 * lx + AX, ny = 2 * ly + AY, nz = 2 * lz + AZ;
-        const int gx = bx + nx, gy = by + ny, gz = bz + nz;
-        const bool owned = resp && gx <= kN && gy <= kN && gz <= kN && !(AX == 2 && gx != kN) &&
-                           !(AY == 2 && gy != kN) && !(AZ == 2 && gz != kN);
-        const bool live = owned && (nomask || !node_bnd(gx, gy, gz, G.nn1));
-        const bool lowx = nx == 0 && tx > 0, lowy = ny == 0 && ty > 0, lowz = nz == 0 && tz > 0;
-        double f[7];
-#pragma unroll
-        for (int o = 0; o < 7; ++o) {  // neighbour (dx, dy, dz) in {-1, 0}^3 \ {0}, ascending tile index
-          const int dz = (o < 4) ? -1 : 0, dy = ((o % 4) < 2) ? -1 : 0, dx = (o % 2 == 0) ? -1 : 0;
-          const bool need = live && (dz == 0 || lowz) && (dy == 0 || lowy) && (dx == 0 || lowx);
-          const int nt = (tx + dx) + NTX * ((ty + dy) + NTY * (tz + dz));
-          f[o] = need ? __ldcg(Fc + (size_t)nt * 3 * T::SHELL +
-                               T::shell(dx ? 2 * TX : nx, dy ? 2 * TY : ny, dz ? 2 * TZ : nz))
-                      : 0.0;
-        }
-        const double own = live ? a2_node_sum<TX, TY, TZ>(X, c, lx, ly, lz, AX, AY, AZ) : 0.0;
-        double acc = 0.0;
-#pragma unroll
-        for (int o = 0; o < 7; ++o) acc += f[o];
-        acc += own;
-        if (owned) y[c * G.n_nodes + node_id(gx, gy, gz, G.nn1)] = live ? acc : 0.0;
-      }
+  y[g] = a0; y[nv + g] = a1; y[2 * nv + g] = a2;
+}
+
+// number of skeleton nodes (kernel 2 threads)
+template <int TX, int TY, int TZ>
+inline int64_t a2_skel_count(int N) {
+  const int nn1 = 2 * N + 1;
+  const int PX = (nn1 - 1) / (2 * TX) + 1, PY = (nn1 - 1) / (2 * TY) + 1, PZ = (nn1 - 1) / (2 * TZ) + 1;
+  const int QX = nn1 - PX, QY = nn1 - PY;
+  return (int64_t)PX * nn1 * nn1 + (int64_t)QX * PY * nn1 + (int64_t)QX * QY * PZ;
+}
+
+// tile-blocked viscosity for k_A_tile: mutT[tile][q][le] = mu w_q h/2 (as k_prescale)
+template <int TX, int TY, int TZ>
+__global__ void k_prescale_t2(const double* __restrict__ mu, double* __restrict__ mutT, int N, double hs,
+                              unsigned long long* bad) {
+  constexpr int NE = TX * TY * TZ;
+  const int64_t n = (int64_t)N * N * N * 27;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int q = (int)(i % 27);
+  const int64_t e = i / 27;
+  const int ex = (int)(e % N), ey = (int)((e / N) % N), ez = (int)(e / ((int64_t)N * N));
+  const int NTX = (N + TX - 1) / TX, NTY = (N + TY - 1) / TY;
+  const int tile = ex / TX + NTX * (ey / TY + NTY * (ez / TZ));
+  const int le = ex % TX + TX * (ey % TY + TY * (ez % TZ));
+  const double m = mu[i];
+  if (!(m > 0.0) || !isfinite(m)) atomicAdd(bad, 1ull);
+  const double wq = TB(2).w[q % 3] * TB(2).w[(q / 3) % 3] * TB(2).w[q / 9];
+  mutT[((int64_t)tile * 27 + q) * NE + le] = m * wq * hs;
 }
 
 }  // namespace wb

@@ -61,8 +61,12 @@ struct FKT {
   static constexpr unsigned PBYTES = 4u * NB * 8u, XBYTES = (unsigned)NX * 8u;
   // Ps[m][qx][qz][qy]: a pencil's (qy, qz) row is the fastest index, so the lanes of a
   // pencil class (consecutive qy) read consecutive words
-  static constexpr int NHP = HX * HY * HZ;
-  __host__ __device__ static constexpr int pidx(int qx, int qy, int qz) { return qy + HY * (qz + HZ * qx); }
+  // qz stride QS = 9 (mod 16) and >= HY: a class-(0,0) half-warp (9 qy per qz row)
+  // then reads 16 distinct bank pairs
+  static constexpr int QS = HY + ((25 - HY % 16) % 16);
+  static constexpr int NHD = HX * HY * HZ;  // halo elements
+  static constexpr int NHP = HX * HZ * QS;  // padded Ps stride per mode
+  __host__ __device__ static constexpr int pidx(int qx, int qy, int qz) { return qy + QS * (qz + HZ * qx); }
   // T[c][col(nx)][row]: rows grouped by class (ny%2, nz%2), row = off[cls] + jy + CY jz;
   // column stride TC = 4 (mod 16) makes step 2 (4 x-elements x 4 y-elements per
   // half-warp) conflict-free, class-local rows make the pencil stores conflict-free
@@ -94,31 +98,42 @@ __device__ __forceinline__ void fkt_pencil(const double* __restrict__ Ps, double
   for (int c = 0; c < 3; ++c)
 #pragma unroll
     for (int nx = 0; nx < F::MX; ++nx) acc[c][nx] = 0.0;
+  // Factorised B^T (product structure of the element matrix): per halo x-position qx,
+  // first the (y, z) element combos of the row are folded into two x-mode weights
+  // per component, W_c[m1] (4 FMA per combo and component), then the 1-D x
+  // expansion adds W to the three nodes of element qx (6 FMA per node).
 #pragma unroll
-  for (int iz = 0; iz < (RZ ? 1 : 2); ++iz) {
-    const int qz = RZ ? jz + 1 : jz + iz;
-    const int az = RZ ? 1 : (iz == 0 ? 2 : 0);
+  for (int qx = 0; qx < K::HX; ++qx) {
+    double W[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-    for (int iy = 0; iy < (RY ? 1 : 2); ++iy) {
-      const int qy = RY ? jy + 1 : jy + iy;
-      const int ay = RY ? 1 : (iy == 0 ? 2 : 0);
+    for (int iz = 0; iz < (RZ ? 1 : 2); ++iz) {
+      const int qz = RZ ? jz + 1 : jz + iz;
+      const int az = RZ ? 1 : (iz == 0 ? 2 : 0);
 #pragma unroll
-      for (int qx = 0; qx < K::HX; ++qx) {
-        double pm[4];
+      for (int iy = 0; iy < (RY ? 1 : 2); ++iy) {
+        const int qy = RY ? jy + 1 : jy + iy;
+        const int ay = RY ? 1 : (iy == 0 ? 2 : 0);
+        const int h = K::pidx(qx, qy, qz);
+        const double p000 = Ps[h], p100 = Ps[K::NHP + h], p010 = Ps[2 * K::NHP + h], p001 = Ps[3 * K::NHP + h];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) pm[m] = Ps[m * K::NHP + K::pidx(qx, qy, qz)];
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-          const int nx = 2 * qx - 2 + ax;
-          if (nx < 0 || nx >= F::MX) continue;
-          const int a = ax + 3 * (ay + 3 * az);
-#pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            if (bt2_nz(0, a, m)) acc[0][nx] = fma(c_Bt2[0][a][m], pm[m], acc[0][nx]);
-            if (bt2_nz(1, a, m)) acc[1][nx] = fma(c_Bt2[1][a][m], pm[m], acc[1][nx]);
-            if (bt2_nz(2, a, m)) acc[2][nx] = fma(c_Bt2[2][a][m], pm[m], acc[2][nx]);
+        for (int c = 0; c < 3; ++c) {
+          if (w2_nz(c, ay, az, 0)) {
+            W[c][0] = fma(c_W2[c][ay][az][0], p000, W[c][0]);
+            W[c][1] = fma(c_W2[c][ay][az][0], p100, W[c][1]);
           }
+          if (w2_nz(c, ay, az, 1)) W[c][0] = fma(c_W2[c][ay][az][1], p010, W[c][0]);
+          if (w2_nz(c, ay, az, 2)) W[c][0] = fma(c_W2[c][ay][az][2], p001, W[c][0]);
         }
+      }
+    }
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const int nx = 2 * qx - 2 + ax;
+      if (nx < 0 || nx >= F::MX) continue;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (x2_nz(c, ax, 0)) acc[c][nx] = fma(c_X2[c][ax][0], W[c][0], acc[c][nx]);
+        if (x2_nz(c, ax, 1)) acc[c][nx] = fma(c_X2[c][ax][1], W[c][1], acc[c][nx]);
       }
     }
   }
@@ -192,7 +207,7 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, 1)
     if (next < n_tiles) coords(next, nx0, ny0, nz0);
     // 0. p = Minv r (+ beta p_old) from the raw boxes into Ps; own elements -> p_new
     mbar_wait(&bar[0], ph);
-    for (int i = threadIdx.x; i < K::NHP; i += F::NTH) {
+    for (int i = threadIdx.x; i < K::NHD; i += F::NTH) {
       const int hx = i % K::HX, hy = (i / K::HX) % K::HY, hz = i / (K::HX * K::HY);
       const int ex = ex0 + hx - 1, ey = ey0 + hy - 1, ez = ez0 + hz - 1;
       const bool own = hx >= 1 && hy >= 1 && hz >= 1 && hx <= TX && hy <= TY && hz <= TZ && ex < N && ey < N &&

@@ -13,6 +13,20 @@ namespace wb {
 // (B_e^T p)_{c,a} = sB * sum_m c_Bt2[c][a][m] p_m.
 __constant__ double c_Bt2[3][27][4];
 
+// Factorised form of the same matrix, c_Bt2[c][a][m] = X[m1][ax] * YZ[m2, m3](ay, az):
+// c_W2[c][ay][az][k] = My_c[0][ay] Mz_c[0][az] (k = 0, weight of modes (0,0,0) and
+// (1,0,0)), My_c[1][ay] Mz_c[0][az] (k = 1, mode (0,1,0)), My_c[0][ay] Mz_c[1][az]
+// (k = 2, mode (0,0,1)); c_X2[c][ax][m1] = Mx_c[m1][ax].  (M_cd = BD if d == c else BI.)
+__constant__ double c_W2[3][3][3][3];
+__constant__ double c_X2[3][3][2];
+// exact zeros: BI[1][1] = 0, BD[0][1] = 0
+__host__ __device__ constexpr bool m_nz(bool deriv, int m, int a) { return !(a == 1 && (deriv ? m == 0 : m == 1)); }
+__host__ __device__ constexpr bool w2_nz(int c, int ay, int az, int k) {
+  return k == 0 ? (m_nz(c == 1, 0, ay) && m_nz(c == 2, 0, az))
+                : (k == 1 ? (m_nz(c == 1, 1, ay) && m_nz(c == 2, 0, az)) : (m_nz(c == 1, 0, ay) && m_nz(c == 2, 1, az)));
+}
+__host__ __device__ constexpr bool x2_nz(int c, int ax, int m1) { return m_nz(c == 0, m1, ax); }
+
 // ------------------------------------------------------------------ B^T, node-centric
 // Node class (gx%2, gy%2, gz%2) is uniform across a warp, so the element
 // pairs and local indices a are compile-time constants and every coefficient

@@ -56,13 +56,10 @@ struct wb_ctx {
   double* stage = nullptr;  // wb_hotpath_host staging (lazily allocated)
   cudaStream_t copy_stream = nullptr;  // wb_hotpath_host: copies overlapped with compute
   cudaEvent_t ev_in = nullptr, ev_ab = nullptr, ev_bt = nullptr, ev_done = nullptr;
-  // k = 2 tile-assembled A: face partials, flags, ticket counter
-  double* F = nullptr;
-  int* tflag = nullptr;
-  unsigned long long* ticket = nullptr;
-  unsigned long long ticket_base = 0;
-  int epoch = 0, n_tiles = 0;
-  int a_tile = 1;  // k = 2 A tile shape: 0 = 4x4x2 (96 threads), 1 = 4x4x4 (192 threads, default: faster)
+  // k = 2 tile-assembled A (4x4x4 tiles): upper-shell and lower-face node partials
+  // (L2-resident), summed by the skeleton kernel; mut is tile-blocked for k = 2
+  double *Fu = nullptr, *Fl = nullptr;
+  int n_tiles = 0;
   int use_graph = 1;
   int k_var = 1;  // k = 2 fused K variant: 0 = 2 CTAs/SM (register-capped), 1 = 1 CTA/SM (faster: L1 left free)
   // TMA variant of the fused K kernel (k = 2, even N, large meshes): tensor maps over the
@@ -150,16 +147,15 @@ wb_status ensure_iters(wb_ctx* c, int iters) {
 // ---------------------------------------------------------------- kernel dispatch helpers
 template <int K>
 wb_status launch_A_t(wb_ctx* c, const double* u, double* out_E, int nomask) {
-  if constexpr (K == 2) {
-    constexpr int NE = 64;
-    k_A_reg<2, NE><<<nblk(c->n_el, NE), 3 * NE, 0, c->stream>>>(c->mut, u, out_E, c->G, nomask);
+  if constexpr (K == 2) {  // k = 2 goes through the tile kernels (run_A)
+    return set_err(c, WB_ESTATE, "internal: element-local A path is not used for k = 2");
   } else {
     constexpr int NE = (K == 3) ? 8 : 5;
     const size_t smem = (size_t)NE * 12 * Ord<K>::NQ * sizeof(double);  // attribute set in configure_kernels
     k_A_slice<K, NE><<<nblk(c->n_el, NE), NE * (K + 1) * (K + 1), smem, c->stream>>>(c->mut, u, out_E, c->G, nomask);
+    LAUNCH_CHECK(c);
+    return WB_OK;
   }
-  LAUNCH_CHECK(c);
-  return WB_OK;
 }
 
 template <int K>
@@ -303,8 +299,6 @@ bool setup_tma(wb_ctx* c) {
 wb_status configure_kernels(wb_ctx* c) {
   CUDA_TRY(c, cudaFuncSetAttribute(k_A_tile<4, 4, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)Tile2<4, 4, 4>::SMEM));
-  CUDA_TRY(c, cudaFuncSetAttribute(k_A_tile<4, 4, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)Tile2<4, 4, 2>::SMEM));
   CUDA_TRY(c, cudaFuncSetAttribute(k_K2_fused<4, 8, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)FK2<4, 8, 8>::SMEM));
   CUDA_TRY(c, cudaFuncSetAttribute(k_K2_fused<4, 8, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -324,19 +318,10 @@ wb_status configure_kernels(wb_ctx* c) {
 
 wb_status run_A(wb_ctx* c, const double* u, double* y, int nomask) {
   if (c->k == 2) {
-    ++c->epoch;
-    const int N = c->N;
-    int nt;
-    if (c->a_tile == 1) {
-      nt = ((N + 3) / 4) * ((N + 3) / 4) * ((N + 3) / 4);
-      k_A_tile<4, 4, 4, 2><<<nt, 192, Tile2<4, 4, 4>::SMEM, c->stream>>>(c->mut, u, y, c->F, c->tflag, c->ticket,
-                                                                         c->ticket_base, c->epoch, c->G, nomask);
-    } else {
-      nt = ((N + 3) / 4) * ((N + 3) / 4) * ((N + 1) / 2);
-      k_A_tile<4, 4, 2, 4><<<nt, 96, Tile2<4, 4, 2>::SMEM, c->stream>>>(c->mut, u, y, c->F, c->tflag, c->ticket,
-                                                                        c->ticket_base, c->epoch, c->G, nomask);
-    }
-    c->ticket_base += (unsigned long long)nt;
+    k_A_tile<4, 4, 4, 2><<<c->n_tiles, 192, Tile2<4, 4, 4>::SMEM, c->stream>>>(c->mut, u, y, c->Fu, c->Fl, c->G,
+                                                                                 nomask);
+    LAUNCH_CHECK(c);
+    k_A_skel<4, 4, 4><<<nblk(a2_skel_count<4, 4, 4>(c->N), 256), 256, 0, c->stream>>>(c->Fu, c->Fl, y, c->G, nomask);
     LAUNCH_CHECK(c);
     return WB_OK;
   }
@@ -512,7 +497,7 @@ wb_status check_ctx(wb_ctx* c, bool need_visc) {
 void free_all(wb_ctx* c) {
   double** bufs[] = {&c->mut, &c->Cw, &c->Dw, &c->Cinv, &c->Dinv, &c->dKl, &c->dKr, &c->MinvL, &c->MinvR,
                      &c->E, &c->tv, &c->tw, &c->px, &c->pr, &c->pp, &c->pp1, &c->pq, &c->s0, &c->s1, &c->s2,
-                     &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->F};
+                     &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->Fu, &c->Fl};
   clear_graphs(c);
   if (c->cap_stream) { cudaStreamDestroy(c->cap_stream); c->cap_stream = nullptr; }
   if (c->copy_stream) { cudaStreamDestroy(c->copy_stream); c->copy_stream = nullptr; }
@@ -523,9 +508,6 @@ void free_all(wb_ctx* c) {
   for (double** b : bufs)
     if (*b) { cudaFree(*b); *b = nullptr; }
   if (c->counter) cudaFree(c->counter);
-  if (c->tflag) cudaFree(c->tflag);
-  if (c->ticket) cudaFree(c->ticket);
-  c->tflag = nullptr; c->ticket = nullptr;
   if (c->stop) cudaFree(c->stop);
   if (c->icount) cudaFree(c->icount);
   if (c->XpL) cudaFree(c->XpL);
@@ -577,6 +559,24 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
           for (int d = 0; d < 3; ++d) v *= (d == cc ? t[0].BD[md[m][d]][ad[d]] : t[0].BI[md[m][d]][ad[d]]);
           bt2[cc][a][m] = (double)v;
         }
+    // factorised tables (k = 2): c_W2[c][ay][az][k], c_X2[c][ax][m1]
+    double w2[3][3][3][3], x2[3][3][2];
+    for (int cc = 0; cc < 3; ++cc) {
+      auto M = [&](int d, int m, int a) { return (long double)(d == cc ? t[0].BD[m][a] : t[0].BI[m][a]); };
+      for (int ay = 0; ay < 3; ++ay)
+        for (int az = 0; az < 3; ++az) {
+          w2[cc][ay][az][0] = (double)(M(1, 0, ay) * M(2, 0, az));
+          w2[cc][ay][az][1] = (double)(M(1, 1, ay) * M(2, 0, az));
+          w2[cc][ay][az][2] = (double)(M(1, 0, ay) * M(2, 1, az));
+        }
+      for (int ax = 0; ax < 3; ++ax)
+        for (int m1 = 0; m1 < 2; ++m1) x2[cc][ax][m1] = (double)M(0, m1, ax);
+    }
+    if (cudaMemcpyToSymbol(c_W2, w2, sizeof(w2)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_X2, x2, sizeof(x2)) != cudaSuccess) {
+      delete c;
+      return WB_ECUDA;
+    }
     if (cudaMemcpyToSymbol(c_Bt2, bt2, sizeof(bt2)) != cudaSuccess) {
       delete c;
       return WB_ECUDA;
@@ -593,7 +593,6 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
   auto alloc = [&](double** p, int64_t n) {
     if (ok && cudaMalloc(p, sizeof(double) * (size_t)(n > 0 ? n : 1)) != cudaSuccess) ok = false;
   };
-  alloc(&c->mut, c->n_el * c->nq);
   alloc(&c->Cw, c->n_nodes); alloc(&c->Dw, c->n_nodes); alloc(&c->Cinv, c->n_nodes); alloc(&c->Dinv, c->n_nodes);
   alloc(&c->dKl, c->n_p); alloc(&c->dKr, c->n_p); alloc(&c->MinvL, c->n_p); alloc(&c->MinvR, c->n_p);
   alloc(&c->E, (k == 2 ? 1 : 3) * c->nq * c->n_el);  // k = 2: setup only (lumped element values)
@@ -605,16 +604,15 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
   alloc(&c->pqp, c->n_el / 32 + 1024);  // >= blocks of any K-apply grid (tiles >= 64 elements, k_B 128)
   alloc(&c->rzp, c->red_blocks);
   if (k == 2) {
-    // sized for the largest tile count / shell of the two A tile shapes (4x4x2, 4x4x4)
-    const int64_t t442 = (int64_t)((N + 3) / 4) * ((N + 3) / 4) * ((N + 1) / 2);
-    const int64_t t444 = (int64_t)((N + 3) / 4) * ((N + 3) / 4) * ((N + 3) / 4);
-    c->n_tiles = (int)t442;
-    alloc(&c->F, std::max(t442 * 3 * Tile2<4, 4, 2>::SHELL, t444 * 3 * Tile2<4, 4, 4>::SHELL));
-    if (ok && cudaMalloc(&c->tflag, sizeof(int) * c->n_tiles) != cudaSuccess) ok = false;
-    if (ok && cudaMalloc(&c->ticket, sizeof(unsigned long long)) != cudaSuccess) ok = false;
-    if (ok && (cudaMemsetAsync(c->tflag, 0, sizeof(int) * c->n_tiles, c->stream) != cudaSuccess ||
-               cudaMemsetAsync(c->ticket, 0, sizeof(unsigned long long), c->stream) != cudaSuccess))
-      ok = false;
+    // 4x4x4 A tiles; mut tile-blocked and zero for elements outside the mesh (ragged tiles)
+    const int64_t nt = (int64_t)((N + 3) / 4) * ((N + 3) / 4) * ((N + 3) / 4);
+    c->n_tiles = (int)nt;
+    alloc(&c->mut, nt * 27 * 64);
+    if (ok && cudaMemsetAsync(c->mut, 0, sizeof(double) * (size_t)nt * 27 * 64, c->stream) != cudaSuccess) ok = false;
+    alloc(&c->Fu, nt * 3 * Tile2<4, 4, 4>::SHELL);
+    alloc(&c->Fl, nt * 3 * Tile2<4, 4, 4>::LF);
+  } else {
+    alloc(&c->mut, c->n_el * c->nq);
   }
   if (ok && cudaMalloc(&c->counter, sizeof(unsigned) * 4) != cudaSuccess) ok = false;
   if (ok && cudaMalloc(&c->icount, sizeof(unsigned long long) * 4) != cudaSuccess) ok = false;
@@ -687,7 +685,10 @@ template <int K>
 static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
   const int64_t nmu = c->n_el * c->nq;
   CUDA_TRY(c, cudaMemsetAsync(c->icount, 0, sizeof(unsigned long long) * 4, c->stream));
-  k_prescale<K><<<nblk(nmu, 256), 256, 0, c->stream>>>(mu, c->mut, nmu, c->h / 2, c->icount);
+  if constexpr (K == 2)
+    k_prescale_t2<4, 4, 4><<<nblk(nmu, 256), 256, 0, c->stream>>>(mu, c->mut, c->N, c->h / 2, c->icount);
+  else
+    k_prescale<K><<<nblk(nmu, 256), 256, 0, c->stream>>>(mu, c->mut, nmu, c->h / 2, c->icount);
   LAUNCH_CHECK(c);
   unsigned long long bad = 0;
   CUDA_TRY(c, cudaMemcpyAsync(&bad, c->icount, sizeof(bad), cudaMemcpyDeviceToHost, c->stream));
@@ -936,7 +937,7 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
     *value = nb;
   } else if (!strcmp(key, "occ_a2")) {
     int nb = 0;
-    CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_A_tile<4, 4, 2, 4>, 96, Tile2<4, 4, 2>::SMEM));
+    CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_A_tile<4, 4, 4, 2>, 192, Tile2<4, 4, 4>::SMEM));
     *value = nb;
   }
   else if (!strcmp(key, "prof_k_ms")) {
@@ -965,10 +966,7 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
 
 wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
   if (!c || !key) return WB_EINVAL;
-  if (!strcmp(key, "a_tile")) {
-    if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "a_tile must be 0 or 1");
-    c->a_tile = (int)value;
-  } else if (!strcmp(key, "graph")) {
+  if (!strcmp(key, "graph")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "graph must be 0 or 1");
     c->use_graph = (int)value;
   } else if (!strcmp(key, "k_variant")) {
