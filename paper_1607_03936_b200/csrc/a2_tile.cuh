@@ -89,15 +89,18 @@ struct UsL {
 };
 
 template <int TX, int TY, int TZ>
-__device__ __forceinline__ void a2_elem(const double* __restrict__ Mu, const double* __restrict__ Us, bool valid,
-                                        int lx, int ly, int lz, int c, int le, double* X, double (&V)[27]) {
+__device__ __forceinline__ void a2_elem(const double* __restrict__ Mu, const double* __restrict__ Us, int lx,
+                                        int ly, int lz, int c, int le, double* X, double (&V)[27]) {
   constexpr int NE = TX * TY * TZ;
   using L = UsL<TX, TY, TZ>;
   const K2Coef k = k2coef();
-  // mut and u of the tile, staged in shared memory by cp.async from all threads:
-  // wait for this thread's copies, then a barrier makes everyone's visible
-  cp_async_wait_all();
-  __syncthreads();
+  // (the caller has made the staged mut and u of the tile visible to every thread;
+  // mut is 0 for elements outside the mesh, so their V is 0)
+  // per-thread bases: every shared access below is base + compile-time offset
+  const double* __restrict__ Ub = Us + c * L::NN + L::RSU * (2 * ly + L::MY * 2 * lz) + lx;
+  const double* __restrict__ Mb = Mu + le;
+  double* Xw = X + c * 3 * NE + le;         // X[q][c][j] <- g_cj
+  const double* Xr = X + c * NE + le;       // X[q][j][c] -> g_jc
   double U[27];
 #pragma unroll
   for (int az = 0; az < 3; ++az)
@@ -105,8 +108,7 @@ __device__ __forceinline__ void a2_elem(const double* __restrict__ Mu, const dou
     for (int ay = 0; ay < 3; ++ay)
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax)  // Dirichlet entries were staged as 0
-        U3(az, ay, ax) = Us[c * L::NN + L::RSU * ((2 * ly + ay) + L::MY * (2 * lz + az)) +
-                            (ax == 1 ? TX + 1 + lx : lx + (ax >> 1))];
+        U3(az, ay, ax) = Ub[L::RSU * (ay + L::MY * az) + (ax == 1 ? TX + 1 : (ax >> 1))];
   // GLL -> Gauss in x, y, z
 #pragma unroll
   for (int z = 0; z < 3; ++z)
@@ -126,7 +128,7 @@ __device__ __forceinline__ void a2_elem(const double* __restrict__ Mu, const dou
   for (int iz = 0; iz < 3; ++iz) {
     double mu[9];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) mu[q] = valid ? Mu[(iz * 9 + q) * NE + le] : 0.0;
+    for (int q = 0; q < 9; ++q) mu[q] = Mb[(iz * 9 + q) * NE];
     double gx[9], gy[9], gz[9];
 #pragma unroll
     for (int y = 0; y < 3; ++y) k2_deriv(k, U3(iz, y, 0), U3(iz, y, 1), U3(iz, y, 2), gx[y * 3], gx[y * 3 + 1], gx[y * 3 + 2]);
@@ -142,16 +144,16 @@ __device__ __forceinline__ void a2_elem(const double* __restrict__ Mu, const dou
     // exchange: X[q][c*3 + j][le] = g_cj
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
-      X[(q * 9 + c * 3 + 0) * NE + le] = gx[q];
-      X[(q * 9 + c * 3 + 1) * NE + le] = gy[q];
-      X[(q * 9 + c * 3 + 2) * NE + le] = gz[q];
+      Xw[(q * 9 + 0) * NE] = gx[q];
+      Xw[(q * 9 + 1) * NE] = gy[q];
+      Xw[(q * 9 + 2) * NE] = gz[q];
     }
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
-      gx[q] = mu[q] * (gx[q] + X[(q * 9 + 0 * 3 + c) * NE + le]);
-      gy[q] = mu[q] * (gy[q] + X[(q * 9 + 1 * 3 + c) * NE + le]);
-      gz[q] = mu[q] * (gz[q] + X[(q * 9 + 2 * 3 + c) * NE + le]);
+      gx[q] = mu[q] * (gx[q] + Xr[(q * 9 + 0 * 3) * NE]);
+      gy[q] = mu[q] * (gy[q] + Xr[(q * 9 + 1 * 3) * NE]);
+      gz[q] = mu[q] * (gz[q] + Xr[(q * 9 + 2 * 3) * NE]);
     }
     __syncthreads();
     // back: V(iz,.,.) += Dg_x^T Wx + Dg_y^T Wy;  V(., ., .) += Dg[iz][jz] Wz
@@ -188,20 +190,14 @@ struct Tile2 {
   static constexpr int NE = TX * TY * TZ, NT = 3 * NE;
   static constexpr int MX = 2 * TX + 1, MY = 2 * TY + 1, MZ = 2 * TZ + 1, NN = MX * MY * MZ;
   static constexpr int SHELL = NN - (2 * TX) * (2 * TY) * (2 * TZ);                             // upper shell
-  static constexpr int LF = (2 * TX) * (2 * TY) * (2 * TZ) - (2 * TX - 1) * (2 * TY - 1) * (2 * TZ - 1);  // lower faces
   static constexpr int XS = 81 * NE;  // exchange / slot doubles
-  static constexpr size_t SMEM = sizeof(double) * (XS + 27 * NE + 3 * UsL<TX, TY, TZ>::NN);  // exchange/slots, mut, u
+  // exchange/slots, then two stage buffers (mut, u)
+  static constexpr size_t SMEM = sizeof(double) * (XS + 2 * (27 * NE + 3 * UsL<TX, TY, TZ>::NN));
   // index of an upper-shell node (nx == 2TX || ny == 2TY || nz == 2TZ)
   __host__ __device__ static __forceinline__ int shell(int nx, int ny, int nz) {
     if (nz == 2 * TZ) return ny * MX + nx;
     if (ny == 2 * TY) return MX * MY + nz * MX + nx;
     return MX * MY + 2 * TZ * MX + nz * (2 * TY) + ny;
-  }
-  // index of a lower-face node (all n_d < 2T_d, some n_d == 0)
-  __host__ __device__ static __forceinline__ int lface(int nx, int ny, int nz) {
-    if (nz == 0) return ny * (2 * TX) + nx;
-    if (ny == 0) return (2 * TX) * (2 * TY) + (nz - 1) * (2 * TX) + nx;
-    return (2 * TX) * (2 * TY) + (2 * TZ - 1) * (2 * TX) + (nz - 1) * (2 * TY - 1) + (ny - 1);
   }
 };
 
@@ -210,26 +206,27 @@ struct Tile2 {
 // (local 2); A = 0 -> element l-1 (local 2, if l > 0) then element l (local 0).
 // Elements in ascending index order.  A is compile-time after unrolling.
 template <int TX, int TY, int TZ>
-__device__ __forceinline__ double a2_node_sum(const double* __restrict__ R, int c, int lx, int ly, int lz, int AX,
-                                              int AY, int AZ) {
+__device__ __forceinline__ double a2_node_sum(const double* __restrict__ Rb, int lx, int ly, int lz, int AX, int AY,
+                                              int AZ) {
+  // Rb = R + c * 27 * NE + le: slot (c, a, element le + d) at Rb[a * NE + d]
   constexpr int NE = TX * TY * TZ;
   double acc = 0.0;
 #pragma unroll
   for (int kz = 0; kz < 2; ++kz) {
     if (AZ != 0 && kz == 1) continue;
-    const int qz = AZ == 0 ? lz - 1 + kz : lz, az = AZ == 0 ? (kz == 0 ? 2 : 0) : AZ;
-    if (qz < 0) continue;
+    const int dz = AZ == 0 ? kz - 1 : 0, az = AZ == 0 ? (kz == 0 ? 2 : 0) : AZ;
+    if (lz + dz < 0) continue;
 #pragma unroll
     for (int ky = 0; ky < 2; ++ky) {
       if (AY != 0 && ky == 1) continue;
-      const int qy = AY == 0 ? ly - 1 + ky : ly, ay = AY == 0 ? (ky == 0 ? 2 : 0) : AY;
-      if (qy < 0) continue;
+      const int dy = AY == 0 ? ky - 1 : 0, ay = AY == 0 ? (ky == 0 ? 2 : 0) : AY;
+      if (ly + dy < 0) continue;
 #pragma unroll
       for (int kx = 0; kx < 2; ++kx) {
         if (AX != 0 && kx == 1) continue;
-        const int qx = AX == 0 ? lx - 1 + kx : lx, ax = AX == 0 ? (kx == 0 ? 2 : 0) : AX;
-        if (qx < 0) continue;
-        acc += R[(c * 27 + ax + 3 * (ay + 3 * az)) * NE + qx + TX * (qy + TY * qz)];
+        const int dx = AX == 0 ? kx - 1 : 0, ax = AX == 0 ? (kx == 0 ? 2 : 0) : AX;
+        if (lx + dx < 0) continue;
+        acc += Rb[(ax + 3 * (ay + 3 * az)) * NE + dx + TX * (dy + TY * dz)];
       }
     }
   }
@@ -240,105 +237,165 @@ __device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc)
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Stage the tile's nodal u (component-major, Dirichlet entries and nodes outside
-// the mesh as 0: the elimination of DESIGN.md R6) into Us.  INNER: the tile's
-// node box lies strictly inside the mesh, no checks.
-template <int TX, int TY, int TZ, bool INNER>
-__device__ __forceinline__ void a2_stage_u(const double* __restrict__ u, double* Us, Geo G, int nomask, int bx,
-                                           int by, int bz) {
+// Tile geometry shared by the stage / output code
+struct A2Tile {
+  int tile, tx, ty, tz, bx, by, bz;
+  bool inner;  // the tile's node box lies strictly inside the mesh
+};
+template <int TX, int TY, int TZ>
+__device__ __forceinline__ A2Tile a2_tile_of(int tile, const Geo& G) {
+  const int NTX = (G.N + TX - 1) / TX, NTY = (G.N + TY - 1) / TY;
+  A2Tile t;
+  t.tile = tile;
+  t.tx = tile % NTX; t.ty = (tile / NTX) % NTY; t.tz = tile / (NTX * NTY);
+  t.bx = 2 * TX * t.tx; t.by = 2 * TY * t.ty; t.bz = 2 * TZ * t.tz;
+  const int e = G.nn1 - 1;
+  t.inner = t.bx > 0 && t.by > 0 && t.bz > 0 && t.bx + 2 * TX < e && t.by + 2 * TY < e && t.bz + 2 * TZ < e;
+  return t;
+}
+
+// Stage a tile by cp.async (no wait): its mut block (tile-blocked layout, one
+// contiguous block) and its nodal u, Dirichlet entries and nodes outside the mesh
+// as 0 (the elimination of DESIGN.md R6).  u rows: each warp copies RPW node rows
+// of MX per pass (lane -> (row, nx)); a thread's rows advance by RPP rows, i.e.
+// ny is fixed and (cc, nz) steps by RPP / MY, so the addresses update
+// incrementally.
+template <int TX, int TY, int TZ>
+__device__ __forceinline__ void a2_stage(const double* __restrict__ mutT, const double* __restrict__ u,
+                                         double* Mu, double* Us, const A2Tile& t, const Geo& G, int nomask) {
   using L = UsL<TX, TY, TZ>;
-  constexpr int NTH = 3 * TX * TY * TZ;
+  constexpr int NE = TX * TY * TZ, NTH = 3 * NE, NW = NTH / 32;
+  constexpr int RPW = 32 / L::MX, RPP = NW * RPW, NROWS = 3 * L::MY * L::MZ;
+  static_assert(RPP % L::MY == 0, "row stepping keeps ny fixed");
+  constexpr int DQ = RPP / L::MY;  // (cc, nz) step per pass
+  {
+    const double* src = mutT + (size_t)t.tile * 27 * NE;
+    for (int i = threadIdx.x; i < 27 * NE / 2; i += NTH) cp_async16(Mu + 2 * i, src + 2 * i);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int sub = lane / L::MX, nx = lane - sub * L::MX;
+  if (sub >= RPW) return;
+  const int r0 = w * RPW + sub;
+  const int ny = r0 % L::MY;
+  int q = r0 / L::MY;  // q = cc * MZ + nz
+  int nz = q % L::MZ, cc = q / L::MZ;
   const int nn1 = G.nn1;
-  const double* ub = u + node_id(bx, by, bz, nn1);
-  for (int i = threadIdx.x; i < 3 * L::MX * L::MY * L::MZ; i += NTH) {
-    const int nx = i % L::MX, ny = (i / L::MX) % L::MY, r = i / (L::MX * L::MY), nz = r % L::MZ, cc = r / L::MZ;
-    double* dst = Us + cc * L::NN + L::RSU * (ny + L::MY * nz) + L::col(nx);
-    const double* src = ub + cc * G.n_nodes + (int64_t)(nz * nn1 + ny) * nn1 + nx;
-    if (INNER) {
+  const int64_t nn2 = (int64_t)nn1 * nn1;
+  const double* src = u + cc * G.n_nodes + node_id(t.bx + nx, t.by + ny, t.bz + nz, nn1);
+  double* dst = Us + cc * L::NN + L::RSU * (ny + L::MY * nz) + L::col(nx);
+  const int gx = t.bx + nx, gy = t.by + ny;
+  const bool colok = gx < nn1 && gy < nn1 && (nomask || (gx != 0 && gy != 0 && gx != nn1 - 1 && gy != nn1 - 1));
+  for (int r = r0; r < NROWS; r += RPP) {
+    if (t.inner) {
       cp_async8(dst, src);
     } else {
-      const int gx = bx + nx, gy = by + ny, gz = bz + nz;
-      if (gx < nn1 && gy < nn1 && gz < nn1 && (nomask || !node_bnd(gx, gy, gz, nn1)))
+      const int gz = t.bz + nz;
+      if (colok && gz < nn1 && (nomask || (gz != 0 && gz != nn1 - 1)))
         cp_async8(dst, src);
       else
         *dst = 0.0;
     }
+    // (cc, nz) += DQ in units of nz, wrapping nz at MZ
+    nz += DQ;
+    if (nz >= L::MZ) {
+      nz -= L::MZ; ++cc;
+      src += G.n_nodes - (int64_t)(L::MZ - DQ) * nn2;
+      dst += L::NN - (L::MZ - DQ) * L::RSU * L::MY;
+    } else {
+      src += DQ * nn2;
+      dst += DQ * L::RSU * L::MY;
+    }
   }
 }
 
-// Kernel 1 of A: one CTA per TX x TY x TZ element tile, thread per (element,
-// component).  The tile's nodes are summed in shared memory (fixed order, a2_node_sum)
-// and leave the kernel by class:
-//   interior (0 < n_d < 2T_d in every axis): complete -> y;
+// Kernel 1 of A: persistent CTAs walk the TX x TY x TZ element tiles, thread per
+// (element, component); the next tile's mut and u are staged (cp.async, double
+// buffer) while the current one is computed.  The tile's nodes are summed in
+// shared memory (fixed order, a2_node_sum) and leave the kernel by class:
 //   upper shell (some n_d == 2T_d): partial -> Fu[tile][c][shell];
-//   lower faces (else, some n_d == 0): partial -> Fl[tile][c][lface].
-// mutT is tile-blocked, mutT[tile][q][le] (zero for elements outside the mesh), so a
-// tile's viscosity is one contiguous block.  No inter-CTA communication.
+//   else (all n_d < 2T_d): the tile's own sum -> y (complete for tile-interior
+//   nodes; for lower-face nodes k_A_skel adds the lower tiles' partials in front).
+// mutT is tile-blocked, mutT[tile][q][le] (zero for elements outside the mesh).
 template <int TX, int TY, int TZ, int MINB>
 __global__ void __launch_bounds__(3 * TX * TY * TZ, MINB)
     k_A_tile(const double* __restrict__ mutT, const double* __restrict__ u, double* __restrict__ y,
-             double* __restrict__ Fu, double* __restrict__ Fl, Geo G, int nomask) {
+             double* __restrict__ Fu, Geo G, int nomask) {
   using T = Tile2<TX, TY, TZ>;
-  constexpr int NE = T::NE, NTH = T::NT;
+  using L = UsL<TX, TY, TZ>;
+  constexpr int NE = T::NE;
+  constexpr int SB = 27 * NE + 3 * L::NN;  // stage buffer: Mu then Us
   extern __shared__ __align__(16) double smem_a2[];
   double* X = smem_a2;  // [XS]: gradient exchange, then element slots R[c][a][le]
-  const int tile = blockIdx.x;
-  const int NTX = (G.N + TX - 1) / TX, NTY = (G.N + TY - 1) / TY;
-  const int tx = tile % NTX, ty = (tile / NTX) % NTY, tz = tile / (NTX * NTY);
+  double* S0 = smem_a2 + T::XS;
+  const int NTX = (G.N + TX - 1) / TX, NTY = (G.N + TY - 1) / TY, NTZ = (G.N + TZ - 1) / TZ;
+  const int n_tiles = NTX * NTY * NTZ;
   const int le = threadIdx.x % NE, c = threadIdx.x / NE;
   const int lx = le % TX, ly = (le / TX) % TY, lz = le / (TX * TY);
-  const bool valid = TX * tx + lx < G.N && TY * ty + ly < G.N && TZ * tz + lz < G.N;
-  const int bx = 2 * TX * tx, by = 2 * TY * ty, bz = 2 * TZ * tz;
-  double* Mu = smem_a2 + T::XS;
-  double* Us = Mu + 27 * NE;
-  {
-    const double* src = mutT + (size_t)tile * 27 * NE;
-    for (int i = threadIdx.x; i < 27 * NE / 2; i += NTH) cp_async16(Mu + 2 * i, src + 2 * i);
-  }
-  const int nn1 = G.nn1;
-  if (bx > 0 && by > 0 && bz > 0 && bx + 2 * TX < nn1 - 1 && by + 2 * TY < nn1 - 1 && bz + 2 * TZ < nn1 - 1)
-    a2_stage_u<TX, TY, TZ, true>(u, Us, G, nomask, bx, by, bz);
-  else
-    a2_stage_u<TX, TY, TZ, false>(u, Us, G, nomask, bx, by, bz);
-  double V[27];
-  a2_elem<TX, TY, TZ>(Mu, Us, valid, lx, ly, lz, c, le, X, V);
-  // element slots R[c][a][le] (the exchange buffer is free after the last level's barrier)
+  const int nn1 = G.nn1, kN = 2 * G.N;
+  int tile = blockIdx.x;
+  if (tile >= n_tiles) return;
+  A2Tile t = a2_tile_of<TX, TY, TZ>(tile, G);
+  a2_stage<TX, TY, TZ>(mutT, u, S0, S0 + 27 * NE, t, G, nomask);
+  cp_async_commit();
+  for (int k = 0; tile < n_tiles; ++k, tile += gridDim.x) {
+    double* Mu = S0 + (k & 1) * SB;
+    double* Us = Mu + 27 * NE;
+    const int next = tile + gridDim.x;
+    if (next < n_tiles) {
+      double* Mn = S0 + ((k + 1) & 1) * SB;
+      a2_stage<TX, TY, TZ>(mutT, u, Mn, Mn + 27 * NE, a2_tile_of<TX, TY, TZ>(next, G), G, nomask);
+    }
+    cp_async_commit();
+    cp_async_wait_group<1>();  // this thread's copies of the current tile
+    __syncthreads();           // everyone's
+    double V[27];
+    a2_elem<TX, TY, TZ>(Mu, Us, lx, ly, lz, c, le, X, V);
+    // element slots R[c][a][le] (the exchange buffer is free after the last level's barrier)
+    double* Rb = X + c * 27 * NE + le;
 #pragma unroll
-  for (int a = 0; a < 27; ++a) X[(c * 27 + a) * NE + le] = V[a];
-  __syncthreads();
-  // Each thread is responsible for the tile nodes 2l + A, A_d in {0, 1}, plus A_d = 2
-  // on the tile's upper face (l_d = T_d - 1): every tile node has exactly one
-  // responsible (element, c) thread, and the node's structure is compile-time.
-  double* Fut = Fu + ((size_t)tile * 3 + c) * T::SHELL;
-  double* Flt = Fl + ((size_t)tile * 3 + c) * T::LF;
-  const int kN = 2 * G.N;
+    for (int a = 0; a < 27; ++a) Rb[a * NE] = V[a];
+    __syncthreads();
+    // Each thread is responsible for the tile nodes 2l + A, A_d in {0, 1}, plus A_d = 2
+    // on the tile's upper face (l_d = T_d - 1): every tile node has exactly one
+    // responsible (element, c) thread, and the node's structure is compile-time.
+    double* Fut = Fu + ((size_t)tile * 3 + c) * T::SHELL;
+    double* yb = y + c * G.n_nodes + node_id(t.bx, t.by, t.bz, nn1);
 #pragma unroll
-  for (int AZ = 0; AZ < 3; ++AZ)
+    for (int AZ = 0; AZ < 3; ++AZ)
 #pragma unroll
-    for (int AY = 0; AY < 3; ++AY)
+      for (int AY = 0; AY < 3; ++AY)
 #pragma unroll
-      for (int AX = 0; AX < 3; ++AX) {
-        if ((AX == 2 && lx != TX - 1) || (AY == 2 && ly != TY - 1) || (AZ == 2 && lz != TZ - 1)) continue;
-        const int nx = 2 * lx + AX, ny = 2 * ly + AY, nz = 2 * lz + AZ;
-        const double s = a2_node_sum<TX, TY, TZ>(X, c, lx, ly, lz, AX, AY, AZ);
-        if (AX == 2 || AY == 2 || AZ == 2) {
-          Fut[T::shell(nx, ny, nz)] = s;
-        } else if (nx == 0 || ny == 0 || nz == 0) {
-          Flt[T::lface(nx, ny, nz)] = s;
-        } else {
-          const int gx = bx + nx, gy = by + ny, gz = bz + nz;
-          if (gx <= kN && gy <= kN && gz <= kN)
-            y[c * G.n_nodes + node_id(gx, gy, gz, nn1)] = (nomask || !node_bnd(gx, gy, gz, nn1)) ? s : 0.0;
+        for (int AX = 0; AX < 3; ++AX) {
+          if ((AX == 2 && lx != TX - 1) || (AY == 2 && ly != TY - 1) || (AZ == 2 && lz != TZ - 1)) continue;
+          const int nx = 2 * lx + AX, ny = 2 * ly + AY, nz = 2 * lz + AZ;
+          const double s = a2_node_sum<TX, TY, TZ>(Rb, lx, ly, lz, AX, AY, AZ);
+          if (AX == 2 || AY == 2 || AZ == 2) {
+            Fut[T::shell(nx, ny, nz)] = s;
+          } else {
+            double* dst = yb + (nz * nn1 + ny) * nn1 + nx;
+            if (t.inner) {
+              *dst = s;
+            } else {
+              const int gx = t.bx + nx, gy = t.by + ny, gz = t.bz + nz;
+              if (gx <= kN && gy <= kN && gz <= kN) *dst = (nomask || !node_bnd(gx, gy, gz, nn1)) ? s : 0.0;
+            }
+          }
         }
-      }
+    __syncthreads();  // X and this stage buffer are reused
+    if (next < n_tiles) t = a2_tile_of<TX, TY, TZ>(next, G);
+  }
 }
 
 // Kernel 2 of A: the tile-skeleton nodes (g_d a multiple of 2T_d in some axis),
 // one thread per node, all three components.  Each is summed over the tiles
 // whose closed node box holds it, in ascending tile index (per axis the lower
 // tile, whose upper shell holds the node, then the upper one), from 0.0: a fixed
-// order, so results are bitwise reproducible.  Node enumeration: x-planes, then
+// order, so results are bitwise reproducible.  The last tile, when the node is
+// not on its upper shell, is the node's own tile, whose sum k_A_tile left in y.  Node enumeration: x-planes, then
 // y-planes off the x-planes, then z-planes off both.
 __device__ __forceinline__ int a2_offplane(int k, int M) { return (k / (M - 1)) * M + k % (M - 1) + 1; }
 // node coordinate g on an axis of tile size S (nodes), NT tiles: the first
@@ -352,8 +409,8 @@ __device__ __forceinline__ void a2_axis(int g, int S, int NT, int& t0, int& n0, 
 }
 
 template <int TX, int TY, int TZ>
-__global__ void __launch_bounds__(256) k_A_skel(const double* __restrict__ Fu, const double* __restrict__ Fl,
-                                                double* __restrict__ y, Geo G, int nomask) {
+__global__ void __launch_bounds__(256) k_A_skel(const double* __restrict__ Fu, double* __restrict__ y, Geo G,
+                                                int nomask) {
   using T = Tile2<TX, TY, TZ>;
   constexpr int SX = 2 * TX, SY = 2 * TY, SZ = 2 * TZ;
   const int nn1 = G.nn1;
@@ -364,9 +421,9 @@ __global__ void __launch_bounds__(256) k_A_skel(const double* __restrict__ Fu, c
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int gx, gy, gz;
   if (i < nX) {
-    gx = SX * (int)(i % PX);
-    const int64_t r = i / PX;
-    gy = (int)(r % nn1); gz = (int)(r / nn1);
+    gy = (int)(i % nn1);
+    const int64_t r = i / nn1;
+    gz = (int)(r % nn1); gx = SX * (int)(r / nn1);
   } else if ((i -= nX) < nY) {
     gx = a2_offplane((int)(i % QX), SX);
     const int64_t r = i / QX;
@@ -406,8 +463,8 @@ __global__ void __launch_bounds__(256) k_A_skel(const double* __restrict__ Fu, c
         int st;
         if (nx == SX || ny == SY || nz == SZ) {
           P = Fu + (size_t)tile * 3 * T::SHELL + T::shell(nx, ny, nz); st = T::SHELL;
-        } else {
-          P = Fl + (size_t)tile * 3 * T::LF + T::lface(nx, ny, nz); st = T::LF;
+        } else {  // the node's own tile (last in the order): its sum is already in y
+          P = y + g; st = (int)nv;
         }
         a0 += __ldcg(P); a1 += __ldcg(P + st); a2 += __ldcg(P + 2 * st);
       }

@@ -149,8 +149,8 @@ __device__ __forceinline__ void fkt_pencil(const double* __restrict__ Ps, double
 
 // Same contract as k_K2_fused (mode, ctl, partials), tensor maps instead of pointers for the
 // loads: tm_pold / tm_r / tm_minv over [m][ez][ey][ex], tm_x over the padded nodal X.
-template <int TX, int TY, int TZ>
-__global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, 1)
+template <int TX, int TY, int TZ, int MINB>
+__global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     k_K2_tma(const __grid_constant__ CUtensorMap tm_pold, const __grid_constant__ CUtensorMap tm_r,
              const __grid_constant__ CUtensorMap tm_minv, const __grid_constant__ CUtensorMap tm_x,
              double* __restrict__ pnew, double* __restrict__ q, Geo G, double sB, int mode, int it, int ctl,
@@ -173,31 +173,37 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, 1)
   const int64_t ne = G.n_el;
   const int NTX = (N + TX - 1) / TX, NTY = (N + TY - 1) / TY, NTZ = (N + TZ - 1) / TZ;
   const int n_tiles = NTX * NTY * NTZ;
-  double beta = 0.0;
-  if (ctl) {
-    if (pcg_control<F::NTH>(it, rzp, nrz, rz_hist, pq_hist, stop, &beta)) return;
-  } else if (mode == 1) {
-    beta = rz_hist[it] / rz_hist[it - 1];
-  }
   auto coords = [&](int tile, int& ex0, int& ey0, int& ez0) {
     ex0 = TX * (tile % NTX); ey0 = TY * ((tile / NTX) % NTY); ez0 = TZ * (tile / (NTX * NTY));
   };
+  // first tile's loads first: they do not depend on the control scalars, so the
+  // reduction of the previous kernel's partials below overlaps them
+  int tile = blockIdx.x;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); mbar_init(&bar[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (tile < n_tiles) {
+      int ex0, ey0, ez0;
+      coords(tile, ex0, ey0, ez0);
+      mbar_expect_tx(&bar[0], 3 * K::PBYTES);
+      tma_load_4d(Rb, &tm_r, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
+      tma_load_4d(Mb, &tm_minv, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
+      tma_load_4d(Pb, &tm_pold, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
+      mbar_expect_tx(&bar[2], K::XBYTES);
+      tma_load_3d(Xs, &tm_x, 2 * ex0, 2 * ey0, 2 * ez0, &bar[2]);
+    }
   }
-  __syncthreads();
-  int tile = blockIdx.x;
-  if (threadIdx.x == 0 && tile < n_tiles) {
-    int ex0, ey0, ez0;
-    coords(tile, ex0, ey0, ez0);
-    mbar_expect_tx(&bar[0], 3 * K::PBYTES);
-    tma_load_4d(Rb, &tm_r, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
-    tma_load_4d(Mb, &tm_minv, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
-    tma_load_4d(Pb, &tm_pold, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
-    mbar_expect_tx(&bar[2], K::XBYTES);
-    tma_load_3d(Xs, &tm_x, 2 * ex0, 2 * ey0, 2 * ez0, &bar[2]);
+  double beta = 0.0;
+  if (ctl) {
+    if (pcg_control<F::NTH>(it, rzp, nrz, rz_hist, pq_hist, stop, &beta)) {
+      // stopped: drain the bulk copies in flight before the CTA exits
+      if (threadIdx.x == 0 && tile < n_tiles) { mbar_wait(&bar[0], 0); mbar_wait(&bar[2], 0); }
+      return;
+    }
+  } else if (mode == 1) {
+    beta = rz_hist[it] / rz_hist[it - 1];
   }
+  __syncthreads();  // barrier init visible to all threads (pcg_control ends with one too)
   double dot = 0.0;
   for (int k = 0; tile < n_tiles; ++k, tile += gridDim.x) {
     const unsigned ph = k & 1;

@@ -58,7 +58,8 @@ struct wb_ctx {
   cudaEvent_t ev_in = nullptr, ev_ab = nullptr, ev_bt = nullptr, ev_done = nullptr;
   // k = 2 tile-assembled A (4x4x4 tiles): upper-shell and lower-face node partials
   // (L2-resident), summed by the skeleton kernel; mut is tile-blocked for k = 2
-  double *Fu = nullptr, *Fl = nullptr;
+  double* Fu = nullptr;
+  int a_ctas = 2;  // k = 2 A tile kernel grid: CTAs per SM (persistent), 0 = one CTA per tile
   int n_tiles = 0;
   int use_graph = 1;
   int k_var = 1;  // k = 2 fused K variant: 0 = 2 CTAs/SM (register-capped), 1 = 1 CTA/SM (faster: L1 left free)
@@ -205,6 +206,13 @@ wb_status launch_k2f_t(wb_ctx* c, const double* pold, double* pnew, const double
   *npq = grid;
   return WB_OK;
 }
+// element tile of the TMA Poisson kernel and its CTAs per SM
+#ifndef TMA_TX
+#define TMA_TX 4
+#define TMA_TY 8
+#define TMA_TZ 8
+#define TMA_MINB 1
+#endif
 const CUtensorMap* tmap_of(wb_ctx* c, const double* p) {
   if (p == c->pp) return &c->tm_pp;
   if (p == c->pp1) return &c->tm_pp1;
@@ -219,14 +227,14 @@ const CUtensorMap* tmap_of(wb_ctx* c, const double* p) {
 wb_status run_k2f(wb_ctx* c, const double* pold, double* pnew, const double* r, const double* Minv, const double* X,
                   double* q, int mode, PcgArgs a, int* npq) {
   if (c->tma_ok && c->use_tma && c->n_el >= 148 * 256 * 2) {
-    using KT = FKT<4, 8, 8>;
+    using KT = FKT<TMA_TX, TMA_TY, TMA_TZ>;
     const CUtensorMap *tp = tmap_of(c, pold), *tr = tmap_of(c, r ? r : c->pr), *tm = tmap_of(c, Minv),
                       *tx = tmap_of(c, X);
     if (tp && tr && tm && tx) {
       const int N = c->N;
-      const int nt = ((N + 3) / 4) * ((N + 7) / 8) * ((N + 7) / 8);
-      const int grid = std::max(1, std::min(nt, c->nsm));  // persistent, one CTA per SM
-      k_K2_tma<4, 8, 8><<<grid, FK2<4, 8, 8>::NTH, KT::SMEM, c->stream>>>(
+      const int nt = ((N + TMA_TX - 1) / TMA_TX) * ((N + TMA_TY - 1) / TMA_TY) * ((N + TMA_TZ - 1) / TMA_TZ);
+      const int grid = std::max(1, std::min(nt, TMA_MINB * c->nsm));  // persistent, all resident
+      k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB><<<grid, FK2<TMA_TX, TMA_TY, TMA_TZ>::NTH, KT::SMEM, c->stream>>>(
           *tp, *tr, *tm, *tx, pnew, q, c->G, c->sB, mode, a.it, a.ctl, c->rzp, c->red_blocks, rz_hist(c),
           pq_hist(c), c->stop, c->pqp);
       LAUNCH_CHECK(c);
@@ -256,7 +264,7 @@ bool get_encode() {
 }
 // mode-major PCG vector [m][ez][ey][ex]: 4-D map, box = one tile + halo, all modes
 bool make_tm_vec(CUtensorMap* tm, const double* base, int N, int nm) {
-  using KT = FKT<4, 8, 8>;
+  using KT = FKT<TMA_TX, TMA_TY, TMA_TZ>;
   const cuuint64_t dims[4] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)nm};
   const cuuint64_t strides[3] = {(cuuint64_t)N * 8, (cuuint64_t)N * N * 8, (cuuint64_t)N * N * N * 8};
   const cuuint32_t box[4] = {(cuuint32_t)KT::BXW, (cuuint32_t)KT::HY, (cuuint32_t)KT::HZ, (cuuint32_t)nm};
@@ -267,8 +275,8 @@ bool make_tm_vec(CUtensorMap* tm, const double* base, int N, int nm) {
 }
 // nodal X with rows padded to xp: 3-D map, box = the tile's (2T+1)^3 nodes (row rounded up to even)
 bool make_tm_x(CUtensorMap* tm, const double* base, int nn1, int xp) {
-  using KT = FKT<4, 8, 8>;
-  using F = FK2<4, 8, 8>;
+  using KT = FKT<TMA_TX, TMA_TY, TMA_TZ>;
+  using F = FK2<TMA_TX, TMA_TY, TMA_TZ>;
   const cuuint64_t dims[3] = {(cuuint64_t)nn1, (cuuint64_t)nn1, (cuuint64_t)nn1};
   const cuuint64_t strides[2] = {(cuuint64_t)xp * 8, (cuuint64_t)xp * nn1 * 8};
   const cuuint32_t box[3] = {(cuuint32_t)KT::XB, (cuuint32_t)F::MY, (cuuint32_t)F::MZ};
@@ -285,8 +293,8 @@ bool setup_tma(wb_ctx* c) {
     cudaGetLastError();
     return false;
   }
-  if (cudaFuncSetAttribute(k_K2_tma<4, 8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)FKT<4, 8, 8>::SMEM) != cudaSuccess) {
+  if (cudaFuncSetAttribute(k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)FKT<TMA_TX, TMA_TY, TMA_TZ>::SMEM) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
@@ -318,10 +326,10 @@ wb_status configure_kernels(wb_ctx* c) {
 
 wb_status run_A(wb_ctx* c, const double* u, double* y, int nomask) {
   if (c->k == 2) {
-    k_A_tile<4, 4, 4, 2><<<c->n_tiles, 192, Tile2<4, 4, 4>::SMEM, c->stream>>>(c->mut, u, y, c->Fu, c->Fl, c->G,
-                                                                                 nomask);
+    k_A_tile<4, 4, 4, 2><<<c->a_ctas ? std::min(c->n_tiles, c->a_ctas * c->nsm) : c->n_tiles, 192, Tile2<4, 4, 4>::SMEM, c->stream>>>(
+        c->mut, u, y, c->Fu, c->G, nomask);
     LAUNCH_CHECK(c);
-    k_A_skel<4, 4, 4><<<nblk(a2_skel_count<4, 4, 4>(c->N), 256), 256, 0, c->stream>>>(c->Fu, c->Fl, y, c->G, nomask);
+    k_A_skel<4, 4, 4><<<nblk(a2_skel_count<4, 4, 4>(c->N), 256), 256, 0, c->stream>>>(c->Fu, y, c->G, nomask);
     LAUNCH_CHECK(c);
     return WB_OK;
   }
@@ -497,7 +505,7 @@ wb_status check_ctx(wb_ctx* c, bool need_visc) {
 void free_all(wb_ctx* c) {
   double** bufs[] = {&c->mut, &c->Cw, &c->Dw, &c->Cinv, &c->Dinv, &c->dKl, &c->dKr, &c->MinvL, &c->MinvR,
                      &c->E, &c->tv, &c->tw, &c->px, &c->pr, &c->pp, &c->pp1, &c->pq, &c->s0, &c->s1, &c->s2,
-                     &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->Fu, &c->Fl};
+                     &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->Fu};
   clear_graphs(c);
   if (c->cap_stream) { cudaStreamDestroy(c->cap_stream); c->cap_stream = nullptr; }
   if (c->copy_stream) { cudaStreamDestroy(c->copy_stream); c->copy_stream = nullptr; }
@@ -610,7 +618,6 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
     alloc(&c->mut, nt * 27 * 64);
     if (ok && cudaMemsetAsync(c->mut, 0, sizeof(double) * (size_t)nt * 27 * 64, c->stream) != cudaSuccess) ok = false;
     alloc(&c->Fu, nt * 3 * Tile2<4, 4, 4>::SHELL);
-    alloc(&c->Fl, nt * 3 * Tile2<4, 4, 4>::LF);
   } else {
     alloc(&c->mut, c->n_el * c->nq);
   }
@@ -966,7 +973,10 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
 
 wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
   if (!c || !key) return WB_EINVAL;
-  if (!strcmp(key, "graph")) {
+  if (!strcmp(key, "a_ctas")) {
+    if (value < 0.0 || value > 2.0 || value != (int)value) return set_err(c, WB_EINVAL, "a_ctas must be 0, 1 or 2");
+    c->a_ctas = (int)value;
+  } else if (!strcmp(key, "graph")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "graph must be 0 or 1");
     c->use_graph = (int)value;
   } else if (!strcmp(key, "k_variant")) {
