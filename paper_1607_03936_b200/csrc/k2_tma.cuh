@@ -74,6 +74,9 @@ struct FKT {
   static constexpr int NROW = R00 + R10 + R01 + R11;
   static constexpr int TC = NROW + ((20 - NROW % 16) % 16);
   static constexpr int TN = F::MX * TC;
+  // row sums S[c][m1][lx][row] (x-contracted B per element of the row) in the T region
+  __host__ __device__ static constexpr int sidx(int c, int m1, int lx) { return ((c * 2 + m1) * TX + lx) * TC; }
+  static_assert(6 * TX <= 3 * F::MX, "S fits in the T region");
   __host__ __device__ static constexpr int row(int ny, int nz) {
     return ((ny & 1) ? ((nz & 1) ? R00 + R10 + R01 : R00) : ((nz & 1) ? R00 + R10 : 0)) +
            (ny >> 1) + ((ny & 1) ? TY : TY + 1) * (nz >> 1);
@@ -137,14 +140,28 @@ __device__ __forceinline__ void fkt_pencil(const double* __restrict__ Ps, double
       }
     }
   }
-  double* Tr = T + K::row(ny, nz);
+  // t = sB X^-1 (B^T p) at the row's nodes, then the x-contraction of B for the
+  // row's elements: S_c[m1][lx] = sum_ax Mx_c[m1][ax] t_c(2 lx + ax)
   const double* Xr = Xs + K::XB * (ny + F::MY * nz);
 #pragma unroll
   for (int nx = 0; nx < F::MX; ++nx) {
     const double f = sB * Xr[nx];  // zero-filled outside the mesh; X = 0 on the boundary
 #pragma unroll
-    for (int c = 0; c < 3; ++c) Tr[c * K::TN + F::col(nx) * K::TC] = f * acc[c][nx];
+    for (int c = 0; c < 3; ++c) acc[c][nx] *= f;
   }
+  double* Sr = T + K::row(ny, nz);
+#pragma unroll
+  for (int lx = 0; lx < TX; ++lx)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int m1 = 0; m1 < 2; ++m1) {
+        double sv = 0.0;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax)
+          if (x2_nz(c, ax, m1)) sv = fma(c_X2[c][ax][m1], acc[c][2 * lx + ax], sv);
+        Sr[K::sidx(c, m1, lx)] = sv;
+      }
 }
 
 // Same contract as k_K2_fused (mode, ctl, partials), tensor maps instead of pointers for the
@@ -271,18 +288,26 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
       const int lx = threadIdx.x % TX, ly = (threadIdx.x / TX) % TY, lz = threadIdx.x / (TX * TY);
       const int ex = ex0 + lx, ey = ey0 + ly, ez = ez0 + lz;
       if (ex < N && ey < N && ez < N) {
+        // (y, z) contraction of the row sums: q_000 += W0 S[0], q_100 += W0 S[1],
+        // q_010 += W1 S[0], q_001 += W2 S[0]  (W = c_W2[c][ay][az], exact zeros skipped)
         double qm[4] = {0.0, 0.0, 0.0, 0.0};
+        const double* Sb = T + lx * K::TC;
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
-          for (int a = 0; a < 27; ++a) {
-            const int ax = a % 3, ay = (a / 3) % 3, az = a / 9;
-            const int cx = ax == 1 ? TX + 1 + lx : lx + (ax >> 1);
-            const double tv = T[c * K::TN + cx * K::TC + K::row(2 * ly + ay, 2 * lz + az)];
+          for (int az = 0; az < 3; ++az)
 #pragma unroll
-            for (int m = 0; m < 4; ++m)
-              if (bt2_nz(c, a, m)) qm[m] = fma(c_Bt2[c][a][m], tv, qm[m]);
-          }
+            for (int ay = 0; ay < 3; ++ay) {
+              const double* Se = Sb + K::sidx(c, 0, 0) + K::row(2 * ly + ay, 2 * lz + az);
+              const double s0 = Se[0];
+              if (w2_nz(c, ay, az, 0)) {
+                const double s1 = Se[K::sidx(0, 1, 0)];
+                qm[0] = fma(c_W2[c][ay][az][0], s0, qm[0]);
+                qm[1] = fma(c_W2[c][ay][az][0], s1, qm[1]);
+              }
+              if (w2_nz(c, ay, az, 1)) qm[2] = fma(c_W2[c][ay][az][1], s0, qm[2]);
+              if (w2_nz(c, ay, az, 2)) qm[3] = fma(c_W2[c][ay][az][2], s0, qm[3]);
+            }
         const int64_t e = ex + (int64_t)N * (ey + (int64_t)N * ez);
         const int h = K::pidx(lx + 1, ly + 1, lz + 1);
 #pragma unroll

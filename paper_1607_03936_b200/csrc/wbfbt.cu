@@ -59,7 +59,7 @@ struct wb_ctx {
   // k = 2 tile-assembled A (4x4x4 tiles): upper-shell and lower-face node partials
   // (L2-resident), summed by the skeleton kernel; mut is tile-blocked for k = 2
   double* Fu = nullptr;
-  int a_ctas = 2;  // k = 2 A tile kernel grid: CTAs per SM (persistent), 0 = one CTA per tile
+  int a_ctas = 0;  // k = 2 A tile kernel grid: CTAs per SM (persistent), 0 = one CTA per tile (default: faster)
   int n_tiles = 0;
   int use_graph = 1;
   int k_var = 1;  // k = 2 fused K variant: 0 = 2 CTAs/SM (register-capped), 1 = 1 CTA/SM (faster: L1 left free)
