@@ -44,6 +44,16 @@ def peaks():
         return FALLBACK_HBM, "fallback"
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture summary
+    (profiles/ncu_traffic.json, written by tools/ncu_summary.py), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return float(json.load(f)[kernel]["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 class Clocks:
     """Sample nvidia-smi clocks / throttle reasons during the timed region."""
 
@@ -277,9 +287,12 @@ def run_ours(args):
     # fused K kernel per launch: p_old, r, Minv (mode-major n_p each), X^-1 (nodal) in;
     # p_new, q out
     bytes_K = 8 * (5 * n_p + n_nodes)
-    roof = {"bound": "hbm", "kernel": "k_K2_fused (PCG: p-update + B^T + X^-1 + B + <p,q>)",
+    kname = "k_K2_tma" if ctx.query("k_tma") else "k_K2_fused"
+    roof = {"bound": "hbm", "kernel": f"{kname} (PCG: p-update + B^T + X^-1 + B + <p,q>)",
             "achieved": bytes_K / (k_avg * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-            "frac": bytes_K / (k_avg * 1e-3) / 1e9 / hbm, "traffic": None, "peak_kind": peak_kind,
+            "frac": bytes_K / (k_avg * 1e-3) / 1e9 / hbm, "traffic": ncu_traffic(kname),
+            "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum, "
+                              "one ncu --set full capture)", "peak_kind": peak_kind,
             "algorithmic_bytes_per_launch": bytes_K, "launch_ms": k_avg, "launches_per_step": k_n / prof_steps,
             "share_of_step": k_ms / prof_steps / prof_step_ms, "profiled_step_ms": prof_step_ms}
     tKw = k_avg

@@ -144,7 +144,8 @@ wb_status wb_get_lumped(wb_ctx* ctx, double* Cw, double* Dw, double* Cinv, doubl
 wb_status wb_get_jacobi(wb_ctx* ctx, double* diagKl, double* diagKr);
 
 /* Scalar queries: "n_nonpos_Cw", "n_nonpos_Dw", "n_el", "n_p", "n_v",
- * "kernel_launches" (launches since create), "last_pcg_stop_iter". */
+ * "kernel_launches" (launches since create), "last_pcg_stop_iter", "k_tma" (1 if
+ * the k = 2 Poisson operator runs as the TMA kernel for this mesh). */
 wb_status wb_query(wb_ctx* ctx, const char* key, double* value);
 /* Tuning knobs (results are identical up to rounding for every setting):
  * "a_ctas" (k = 2 A tile kernel: persistent CTAs per SM, 1 or 2, or 0 = one

@@ -870,9 +870,12 @@ __global__ void k_project(const double* __restrict__ in, double* __restrict__ ou
 template <int BS>
 __device__ __forceinline__ bool pcg_control(int i, const double* __restrict__ rzp, int nrz, double* rz_hist,
                                             const double* pq_hist, int* stop, double* beta) {
+  // the history loads do not depend on the partial sum: issue them first
+  const int st_prev = i > 0 ? stop[i - 1] : 0;
+  const double pq_prev = i > 0 ? pq_hist[i - 1] : 1.0, rz_prev = i > 0 ? rz_hist[i - 1] : 1.0;
   const double rzi = sum_partials<BS>(rzp, nrz);
-  const bool st = (i == 0) ? (rzi == 0.0) : (stop[i - 1] != 0 || pq_hist[i - 1] == 0.0 || rzi == 0.0);
-  *beta = (i == 0 || st) ? 0.0 : rzi / rz_hist[i - 1];
+  const bool st = (i == 0) ? (rzi == 0.0) : (st_prev != 0 || pq_prev == 0.0 || rzi == 0.0);
+  *beta = (i == 0 || st) ? 0.0 : rzi / rz_prev;
   if (blockIdx.x == 0 && threadIdx.x == 0) { rz_hist[i] = rzi; stop[i] = st ? 1 : 0; }
   return st;
 }

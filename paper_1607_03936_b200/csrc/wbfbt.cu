@@ -942,6 +942,8 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
     CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_K2_fused<4, 8, 8, 2>, FK2<4, 8, 8>::NTH,
                                                               FK2<4, 8, 8>::SMEM));
     *value = nb;
+  } else if (!strcmp(key, "k_tma")) {  // 1: the Poisson operator runs as the TMA kernel (k_K2_tma)
+    *value = (c->k == 2 && c->tma_ok && c->use_tma && c->n_el >= 148 * 256 * 2) ? 1.0 : 0.0;
   } else if (!strcmp(key, "occ_a2")) {
     int nb = 0;
     CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_A_tile<4, 4, 4, 2>, 192, Tile2<4, 4, 4>::SMEM));

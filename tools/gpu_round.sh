@@ -11,10 +11,10 @@ timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_
 echo "bench rc=$rc" >> gpurun_out/${TAG}_bench.err
 if [ $rc -eq 0 ]; then
   timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/${TAG}_bench_ref.json 2> gpurun_out/${TAG}_bench_ref.err
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -c 3000 --csv \
     --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 3 --warmup 3 > gpurun_out/${TAG}_ncu_launch.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_K2_tma -s 40 -c 1 \
     -o gpurun_out/${TAG}_k2tma -f python tools/tma_check.py C5 > gpurun_out/${TAG}_ncu_full.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_A_tile -s 3 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_A_tile -s 3 -c 1 --cache-control all \
     -o gpurun_out/${TAG}_atile -f python bench.py --steps 3 --warmup 3 > gpurun_out/${TAG}_ncu_a.log 2>&1
 fi
