@@ -148,8 +148,6 @@ wb_status wb_get_jacobi(wb_ctx* ctx, double* diagKl, double* diagKr);
  * the k = 2 Poisson operator runs as the TMA kernel for this mesh). */
 wb_status wb_query(wb_ctx* ctx, const char* key, double* value);
 /* Tuning knobs (results are identical up to rounding for every setting):
- * "a_ctas" (k = 2 A tile kernel: persistent CTAs per SM, 1 or 2, or 0 = one
- * CTA per tile, the default),
  * "graph" (1 = replay the PCG iteration loop as a CUDA graph, default; 0 =
  * plain launches), "profile" (1 = plain launches with a CUDA-event pair around
  * every Poisson-operator launch; wb_query "prof_k_ms" / "prof_k_count" read

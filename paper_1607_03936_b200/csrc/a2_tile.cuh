@@ -191,8 +191,8 @@ struct Tile2 {
   static constexpr int MX = 2 * TX + 1, MY = 2 * TY + 1, MZ = 2 * TZ + 1, NN = MX * MY * MZ;
   static constexpr int SHELL = NN - (2 * TX) * (2 * TY) * (2 * TZ);                             // upper shell
   static constexpr int XS = 81 * NE;  // exchange / slot doubles
-  // exchange/slots, then two stage buffers (mut, u)
-  static constexpr size_t SMEM = sizeof(double) * (XS + 2 * (27 * NE + 3 * UsL<TX, TY, TZ>::NN));
+  // exchange/slots, then the stage buffer (mut, u)
+  static constexpr size_t SMEM = sizeof(double) * (XS + 27 * NE + 3 * UsL<TX, TY, TZ>::NN);
   // index of an upper-shell node (nx == 2TX || ny == 2TY || nz == 2TZ)
   __host__ __device__ static __forceinline__ int shell(int nx, int ny, int nz) {
     if (nz == 2 * TZ) return ny * MX + nx;
@@ -237,9 +237,6 @@ __device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc)
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // Tile geometry shared by the stage / output code
 struct A2Tile {
@@ -312,82 +309,66 @@ __device__ __forceinline__ void a2_stage(const double* __restrict__ mutT, const 
   }
 }
 
-// Kernel 1 of A: persistent CTAs walk the TX x TY x TZ element tiles, thread per
-// (element, component); the next tile's mut and u are staged (cp.async, double
-// buffer) while the current one is computed.  The tile's nodes are summed in
-// shared memory (fixed order, a2_node_sum) and leave the kernel by class:
+// Kernel 1 of A: one CTA per TX x TY x TZ element tile, thread per (element,
+// component).  The tile's nodes are summed in shared memory (fixed order,
+// a2_node_sum) and leave the kernel by class:
 //   upper shell (some n_d == 2T_d): partial -> Fu[tile][c][shell];
 //   else (all n_d < 2T_d): the tile's own sum -> y (complete for tile-interior
 //   nodes; for lower-face nodes k_A_skel adds the lower tiles' partials in front).
 // mutT is tile-blocked, mutT[tile][q][le] (zero for elements outside the mesh).
+// No inter-CTA communication; several small CTAs per SM overlap each other's
+// staging, barriers and compute.
 template <int TX, int TY, int TZ, int MINB>
 __global__ void __launch_bounds__(3 * TX * TY * TZ, MINB)
     k_A_tile(const double* __restrict__ mutT, const double* __restrict__ u, double* __restrict__ y,
              double* __restrict__ Fu, Geo G, int nomask) {
   using T = Tile2<TX, TY, TZ>;
-  using L = UsL<TX, TY, TZ>;
   constexpr int NE = T::NE;
-  constexpr int SB = 27 * NE + 3 * L::NN;  // stage buffer: Mu then Us
   extern __shared__ __align__(16) double smem_a2[];
   double* X = smem_a2;  // [XS]: gradient exchange, then element slots R[c][a][le]
-  double* S0 = smem_a2 + T::XS;
-  const int NTX = (G.N + TX - 1) / TX, NTY = (G.N + TY - 1) / TY, NTZ = (G.N + TZ - 1) / TZ;
-  const int n_tiles = NTX * NTY * NTZ;
+  double* Mu = smem_a2 + T::XS;
+  double* Us = Mu + 27 * NE;
+  const int tile = blockIdx.x;
+  const A2Tile t = a2_tile_of<TX, TY, TZ>(tile, G);
+  a2_stage<TX, TY, TZ>(mutT, u, Mu, Us, t, G, nomask);
   const int le = threadIdx.x % NE, c = threadIdx.x / NE;
   const int lx = le % TX, ly = (le / TX) % TY, lz = le / (TX * TY);
   const int nn1 = G.nn1, kN = 2 * G.N;
-  int tile = blockIdx.x;
-  if (tile >= n_tiles) return;
-  A2Tile t = a2_tile_of<TX, TY, TZ>(tile, G);
-  a2_stage<TX, TY, TZ>(mutT, u, S0, S0 + 27 * NE, t, G, nomask);
-  cp_async_commit();
-  for (int k = 0; tile < n_tiles; ++k, tile += gridDim.x) {
-    double* Mu = S0 + (k & 1) * SB;
-    double* Us = Mu + 27 * NE;
-    const int next = tile + gridDim.x;
-    if (next < n_tiles) {
-      double* Mn = S0 + ((k + 1) & 1) * SB;
-      a2_stage<TX, TY, TZ>(mutT, u, Mn, Mn + 27 * NE, a2_tile_of<TX, TY, TZ>(next, G), G, nomask);
-    }
-    cp_async_commit();
-    cp_async_wait_group<1>();  // this thread's copies of the current tile
-    __syncthreads();           // everyone's
-    double V[27];
-    a2_elem<TX, TY, TZ>(Mu, Us, lx, ly, lz, c, le, X, V);
-    // element slots R[c][a][le] (the exchange buffer is free after the last level's barrier)
-    double* Rb = X + c * 27 * NE + le;
+  cp_async_wait_all();  // this thread's copies
+  __syncthreads();      // everyone's
+  double V[27];
+  a2_elem<TX, TY, TZ>(Mu, Us, lx, ly, lz, c, le, X, V);
+  // element slots R[c][a][le] (the exchange buffer is free after the last level's barrier)
+  double* Rb = X + c * 27 * NE + le;
 #pragma unroll
-    for (int a = 0; a < 27; ++a) Rb[a * NE] = V[a];
-    __syncthreads();
-    // Each thread is responsible for the tile nodes 2l + A, A_d in {0, 1}, plus A_d = 2
-    // on the tile's upper face (l_d = T_d - 1): every tile node has exactly one
-    // responsible (element, c) thread, and the node's structure is compile-time.
-    double* Fut = Fu + ((size_t)tile * 3 + c) * T::SHELL;
-    double* yb = y + c * G.n_nodes + node_id(t.bx, t.by, t.bz, nn1);
+  for (int a = 0; a < 27; ++a) Rb[a * NE] = V[a];
+  __syncthreads();
+  // Each thread is responsible for the tile nodes 2l + A, A_d in {0, 1}, plus A_d = 2
+  // on the tile's upper face (l_d = T_d - 1): every tile node has exactly one
+  // responsible (element, c) thread, and the node's structure is compile-time.
+  double* Fut = Fu + ((size_t)tile * 3 + c) * T::SHELL;
+  double* yb = y + c * G.n_nodes + node_id(t.bx, t.by, t.bz, nn1);
 #pragma unroll
-    for (int AZ = 0; AZ < 3; ++AZ)
+  for (int AZ = 0; AZ < 3; ++AZ)
 #pragma unroll
-      for (int AY = 0; AY < 3; ++AY)
+    for (int AY = 0; AY < 3; ++AY)
 #pragma unroll
-        for (int AX = 0; AX < 3; ++AX) {
-          if ((AX == 2 && lx != TX - 1) || (AY == 2 && ly != TY - 1) || (AZ == 2 && lz != TZ - 1)) continue;
-          const int nx = 2 * lx + AX, ny = 2 * ly + AY, nz = 2 * lz + AZ;
-          const double s = a2_node_sum<TX, TY, TZ>(Rb, lx, ly, lz, AX, AY, AZ);
-          if (AX == 2 || AY == 2 || AZ == 2) {
-            Fut[T::shell(nx, ny, nz)] = s;
+      for (int AX = 0; AX < 3; ++AX) {
+        if ((AX == 2 && lx != TX - 1) || (AY == 2 && ly != TY - 1) || (AZ == 2 && lz != TZ - 1)) continue;
+        const int nx = 2 * lx + AX, ny = 2 * ly + AY, nz = 2 * lz + AZ;
+        const double s = a2_node_sum<TX, TY, TZ>(Rb, lx, ly, lz, AX, AY, AZ);
+        if (AX == 2 || AY == 2 || AZ == 2) {
+          Fut[T::shell(nx, ny, nz)] = s;
+        } else {
+          double* dst = yb + (nz * nn1 + ny) * nn1 + nx;
+          if (t.inner) {
+            *dst = s;
           } else {
-            double* dst = yb + (nz * nn1 + ny) * nn1 + nx;
-            if (t.inner) {
-              *dst = s;
-            } else {
-              const int gx = t.bx + nx, gy = t.by + ny, gz = t.bz + nz;
-              if (gx <= kN && gy <= kN && gz <= kN) *dst = (nomask || !node_bnd(gx, gy, gz, nn1)) ? s : 0.0;
-            }
+            const int gx = t.bx + nx, gy = t.by + ny, gz = t.bz + nz;
+            if (gx <= kN && gy <= kN && gz <= kN) *dst = (nomask || !node_bnd(gx, gy, gz, nn1)) ? s : 0.0;
           }
         }
-    __syncthreads();  // X and this stage buffer are reused
-    if (next < n_tiles) t = a2_tile_of<TX, TY, TZ>(next, G);
-  }
+      }
 }
 
 // Kernel 2 of A: the tile-skeleton nodes (g_d a multiple of 2T_d in some axis),

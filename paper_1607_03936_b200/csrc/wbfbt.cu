@@ -59,7 +59,6 @@ struct wb_ctx {
   // k = 2 tile-assembled A (4x4x4 tiles): upper-shell and lower-face node partials
   // (L2-resident), summed by the skeleton kernel; mut is tile-blocked for k = 2
   double* Fu = nullptr;
-  int a_ctas = 0;  // k = 2 A tile kernel grid: CTAs per SM (persistent), 0 = one CTA per tile (default: faster)
   int n_tiles = 0;
   int use_graph = 1;
   int k_var = 1;  // k = 2 fused K variant: 0 = 2 CTAs/SM (register-capped), 1 = 1 CTA/SM (faster: L1 left free)
@@ -206,6 +205,19 @@ wb_status launch_k2f_t(wb_ctx* c, const double* pold, double* pnew, const double
   *npq = grid;
   return WB_OK;
 }
+// element tile of the k = 2 A kernels and its CTAs per SM
+#ifndef A_TX
+#define A_TX 4
+#endif
+#ifndef A_TY
+#define A_TY 4
+#endif
+#ifndef A_TZ
+#define A_TZ 2
+#endif
+#ifndef A_MINB
+#define A_MINB 4
+#endif
 // element tile of the TMA Poisson kernel and its CTAs per SM
 #ifndef TMA_TX
 #define TMA_TX 4
@@ -305,8 +317,8 @@ bool setup_tma(wb_ctx* c) {
 }
 
 wb_status configure_kernels(wb_ctx* c) {
-  CUDA_TRY(c, cudaFuncSetAttribute(k_A_tile<4, 4, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)Tile2<4, 4, 4>::SMEM));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_A_tile<A_TX, A_TY, A_TZ, A_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)Tile2<A_TX, A_TY, A_TZ>::SMEM));
   CUDA_TRY(c, cudaFuncSetAttribute(k_K2_fused<4, 8, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)FK2<4, 8, 8>::SMEM));
   CUDA_TRY(c, cudaFuncSetAttribute(k_K2_fused<4, 8, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -326,10 +338,11 @@ wb_status configure_kernels(wb_ctx* c) {
 
 wb_status run_A(wb_ctx* c, const double* u, double* y, int nomask) {
   if (c->k == 2) {
-    k_A_tile<4, 4, 4, 2><<<c->a_ctas ? std::min(c->n_tiles, c->a_ctas * c->nsm) : c->n_tiles, 192, Tile2<4, 4, 4>::SMEM, c->stream>>>(
-        c->mut, u, y, c->Fu, c->G, nomask);
+    k_A_tile<A_TX, A_TY, A_TZ, A_MINB><<<c->n_tiles, 3 * A_TX * A_TY * A_TZ, Tile2<A_TX, A_TY, A_TZ>::SMEM,
+                                         c->stream>>>(c->mut, u, y, c->Fu, c->G, nomask);
     LAUNCH_CHECK(c);
-    k_A_skel<4, 4, 4><<<nblk(a2_skel_count<4, 4, 4>(c->N), 256), 256, 0, c->stream>>>(c->Fu, y, c->G, nomask);
+    k_A_skel<A_TX, A_TY, A_TZ><<<nblk(a2_skel_count<A_TX, A_TY, A_TZ>(c->N), 256), 256, 0, c->stream>>>(
+        c->Fu, y, c->G, nomask);
     LAUNCH_CHECK(c);
     return WB_OK;
   }
@@ -612,12 +625,14 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
   alloc(&c->pqp, c->n_el / 32 + 1024);  // >= blocks of any K-apply grid (tiles >= 64 elements, k_B 128)
   alloc(&c->rzp, c->red_blocks);
   if (k == 2) {
-    // 4x4x4 A tiles; mut tile-blocked and zero for elements outside the mesh (ragged tiles)
-    const int64_t nt = (int64_t)((N + 3) / 4) * ((N + 3) / 4) * ((N + 3) / 4);
+    // A tiles of A_TX x A_TY x A_TZ elements; mut tile-blocked and zero for elements
+    // outside the mesh (ragged tiles)
+    const int64_t nt = (int64_t)((N + A_TX - 1) / A_TX) * ((N + A_TY - 1) / A_TY) * ((N + A_TZ - 1) / A_TZ);
+    constexpr int64_t ne_t = A_TX * A_TY * A_TZ;
     c->n_tiles = (int)nt;
-    alloc(&c->mut, nt * 27 * 64);
-    if (ok && cudaMemsetAsync(c->mut, 0, sizeof(double) * (size_t)nt * 27 * 64, c->stream) != cudaSuccess) ok = false;
-    alloc(&c->Fu, nt * 3 * Tile2<4, 4, 4>::SHELL);
+    alloc(&c->mut, nt * 27 * ne_t);
+    if (ok && cudaMemsetAsync(c->mut, 0, sizeof(double) * (size_t)(nt * 27 * ne_t), c->stream) != cudaSuccess) ok = false;
+    alloc(&c->Fu, nt * 3 * Tile2<A_TX, A_TY, A_TZ>::SHELL);
   } else {
     alloc(&c->mut, c->n_el * c->nq);
   }
@@ -693,7 +708,7 @@ static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
   const int64_t nmu = c->n_el * c->nq;
   CUDA_TRY(c, cudaMemsetAsync(c->icount, 0, sizeof(unsigned long long) * 4, c->stream));
   if constexpr (K == 2)
-    k_prescale_t2<4, 4, 4><<<nblk(nmu, 256), 256, 0, c->stream>>>(mu, c->mut, c->N, c->h / 2, c->icount);
+    k_prescale_t2<A_TX, A_TY, A_TZ><<<nblk(nmu, 256), 256, 0, c->stream>>>(mu, c->mut, c->N, c->h / 2, c->icount);
   else
     k_prescale<K><<<nblk(nmu, 256), 256, 0, c->stream>>>(mu, c->mut, nmu, c->h / 2, c->icount);
   LAUNCH_CHECK(c);
@@ -946,7 +961,7 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
     *value = (c->k == 2 && c->tma_ok && c->use_tma && c->n_el >= 148 * 256 * 2) ? 1.0 : 0.0;
   } else if (!strcmp(key, "occ_a2")) {
     int nb = 0;
-    CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_A_tile<4, 4, 4, 2>, 192, Tile2<4, 4, 4>::SMEM));
+    CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_A_tile<A_TX, A_TY, A_TZ, A_MINB>, 3 * A_TX * A_TY * A_TZ, Tile2<A_TX, A_TY, A_TZ>::SMEM));
     *value = nb;
   }
   else if (!strcmp(key, "prof_k_ms")) {
@@ -975,10 +990,7 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
 
 wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
   if (!c || !key) return WB_EINVAL;
-  if (!strcmp(key, "a_ctas")) {
-    if (value < 0.0 || value > 2.0 || value != (int)value) return set_err(c, WB_EINVAL, "a_ctas must be 0, 1 or 2");
-    c->a_ctas = (int)value;
-  } else if (!strcmp(key, "graph")) {
+  if (!strcmp(key, "graph")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "graph must be 0 or 1");
     c->use_graph = (int)value;
   } else if (!strcmp(key, "k_variant")) {

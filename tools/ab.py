@@ -35,11 +35,8 @@ def timed(fn, reps=20, cold=True):
 
 
 n_v = c.n_v
-for g in (2, 1, 0):
-    c.set_option("a_ctas", g)
-    tA = timed(lambda: c.apply_A(u, yv))
-    print(f"A (cold L2) a_ctas={g}: {tA:.1f} us  {n_v / tA / 1e3:.1f} GDOF/s")
-c.set_option("a_ctas", 2)
+tA = timed(lambda: c.apply_A(u, yv))
+print(f"A (cold L2): {tA:.1f} us  {n_v / tA / 1e3:.1f} GDOF/s")
 print(f"B: {timed(lambda: c.apply_B(u, pv)):.1f} us")
 print(f"BT: {timed(lambda: c.apply_BT(p, yv)):.1f} us")
 print(f"K (cold): {timed(lambda: c.apply_K(1, p, pv)):.1f} us  K (warm): {timed(lambda: c.apply_K(1, p, pv), cold=False):.1f} us")
