@@ -255,34 +255,30 @@ __device__ __forceinline__ A2Tile a2_tile_of(int tile, const Geo& G) {
   return t;
 }
 
-// Stage a tile by cp.async (no wait): its mut block (tile-blocked layout, one
-// contiguous block) and its nodal u, Dirichlet entries and nodes outside the mesh
-// as 0 (the elimination of DESIGN.md R6).  u rows: each warp copies RPW node rows
-// of MX per pass (lane -> (row, nx)); a thread's rows advance by RPP rows, i.e.
-// ny is fixed and (cc, nz) steps by RPP / MY, so the addresses update
-// incrementally.
-template <int TX, int TY, int TZ>
-__device__ __forceinline__ void a2_stage(const double* __restrict__ mutT, const double* __restrict__ u,
-                                         double* Mu, double* Us, const A2Tile& t, const Geo& G, int nomask) {
+// Stage NC nodal components (component stride cs) of a tile's (2TX+1)(2TY+1)(2TZ+1)
+// node box into Us[cc][nz][ny][col] by cp.async (no wait); nodes outside the mesh,
+// and Dirichlet nodes unless nomask, as 0 (the elimination of DESIGN.md R6).  Each
+// warp copies RPW node rows of MX per pass (lane -> (row, nx)); a thread's rows
+// advance by RPP rows, i.e. ny is fixed and (cc, nz) steps by RPP / MY, so the
+// addresses update incrementally.  NTH threads take part.
+template <int TX, int TY, int TZ, int NC, int NTH>
+__device__ __forceinline__ void a2_stage_nodal(const double* __restrict__ u, int64_t cs, double* Us, const A2Tile& t,
+                                               const Geo& G, int nomask) {
   using L = UsL<TX, TY, TZ>;
-  constexpr int NE = TX * TY * TZ, NTH = 3 * NE, NW = NTH / 32;
-  constexpr int RPW = 32 / L::MX, RPP = NW * RPW, NROWS = 3 * L::MY * L::MZ;
+  constexpr int NW = NTH / 32;
+  constexpr int RPW = 32 / L::MX, RPP = NW * RPW, NROWS = NC * L::MY * L::MZ;
   static_assert(RPP % L::MY == 0, "row stepping keeps ny fixed");
   constexpr int DQ = RPP / L::MY;  // (cc, nz) step per pass
-  {
-    const double* src = mutT + (size_t)t.tile * 27 * NE;
-    for (int i = threadIdx.x; i < 27 * NE / 2; i += NTH) cp_async16(Mu + 2 * i, src + 2 * i);
-  }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int sub = lane / L::MX, nx = lane - sub * L::MX;
-  if (sub >= RPW) return;
+  if (sub >= RPW || w >= NW) return;
   const int r0 = w * RPW + sub;
   const int ny = r0 % L::MY;
   int q = r0 / L::MY;  // q = cc * MZ + nz
   int nz = q % L::MZ, cc = q / L::MZ;
   const int nn1 = G.nn1;
   const int64_t nn2 = (int64_t)nn1 * nn1;
-  const double* src = u + cc * G.n_nodes + node_id(t.bx + nx, t.by + ny, t.bz + nz, nn1);
+  const double* src = u + cc * cs + node_id(t.bx + nx, t.by + ny, t.bz + nz, nn1);
   double* dst = Us + cc * L::NN + L::RSU * (ny + L::MY * nz) + L::col(nx);
   const int gx = t.bx + nx, gy = t.by + ny;
   const bool colok = gx < nn1 && gy < nn1 && (nomask || (gx != 0 && gy != 0 && gx != nn1 - 1 && gy != nn1 - 1));
@@ -300,13 +296,26 @@ __device__ __forceinline__ void a2_stage(const double* __restrict__ mutT, const 
     nz += DQ;
     if (nz >= L::MZ) {
       nz -= L::MZ; ++cc;
-      src += G.n_nodes - (int64_t)(L::MZ - DQ) * nn2;
+      src += cs - (int64_t)(L::MZ - DQ) * nn2;
       dst += L::NN - (L::MZ - DQ) * L::RSU * L::MY;
     } else {
       src += DQ * nn2;
       dst += DQ * L::RSU * L::MY;
     }
   }
+}
+
+// Stage an A tile: its mut block (tile-blocked layout, one contiguous block) and its
+// nodal u (three components).
+template <int TX, int TY, int TZ>
+__device__ __forceinline__ void a2_stage(const double* __restrict__ mutT, const double* __restrict__ u,
+                                         double* Mu, double* Us, const A2Tile& t, const Geo& G, int nomask) {
+  constexpr int NE = TX * TY * TZ, NTH = 3 * NE;
+  {
+    const double* src = mutT + (size_t)t.tile * 27 * NE;
+    for (int i = threadIdx.x; i < 27 * NE / 2; i += NTH) cp_async16(Mu + 2 * i, src + 2 * i);
+  }
+  a2_stage_nodal<TX, TY, TZ, 3, NTH>(u, G.n_nodes, Us, t, G, nomask);
 }
 
 // Kernel 1 of A: one CTA per TX x TY x TZ element tile, thread per (element,

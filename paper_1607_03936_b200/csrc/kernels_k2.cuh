@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(256) k_BT_node2(const double* __restrict__ p, 
 #include "a2_tile.cuh"
 #include "k2_fused.cuh"
 #include "k2_tma.cuh"
+#include "k2_bbt.cuh"
 
 namespace wb {
 // nodal X -> copy with rows padded to an even length (16-byte-aligned rows for TMA)

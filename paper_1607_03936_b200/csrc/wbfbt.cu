@@ -354,8 +354,13 @@ wb_status run_A(wb_ctx* c, const double* u, double* y, int nomask) {
 wb_status run_BT(wb_ctx* c, const double* p, const double* xs, double* y, int nomask, const int* stop,
                  int64_t se, int64_t sm) {
   if (c->k == 2) {
-    dim3 grid(nblk(c->N + 1, 64), nblk(c->G.nn1, 4), 2 * c->G.nn1);
-    k_BT_node2<<<grid, dim3(64, 4), 0, c->stream>>>(p, xs, y, c->G, c->sB, nomask, stop, se, sm);
+    if (stop) {  // (generic-k PCG only; kept for completeness)
+      dim3 grid(nblk(c->N + 1, 64), nblk(c->G.nn1, 4), 2 * c->G.nn1);
+      k_BT_node2<<<grid, dim3(64, 4), 0, c->stream>>>(p, xs, y, c->G, c->sB, nomask, stop, se, sm);
+    } else {
+      const int nb = (c->G.nn1 + 7) / 8;
+      k_BT_box2<8><<<nb * nb * nb, 256, 0, c->stream>>>(p, xs, y, c->G, c->sB, nomask, se, sm);
+    }
     LAUNCH_CHECK(c);
     return WB_OK;
   }
@@ -365,6 +370,13 @@ wb_status run_BT(wb_ctx* c, const double* p, const double* xs, double* y, int no
 }
 wb_status run_B(wb_ctx* c, const double* u, const double* xs, double* p, int nomask, const int* stop,
                 const double* dv, double* total, int64_t se, int64_t sm) {
+  if (c->k == 2 && !stop && !dv) {
+    const int nt = ((c->N + 3) / 4) * ((c->N + 3) / 4) * ((c->N + 3) / 4);
+    k_B_tile2<4, 4, 4><<<nt, BTile2<4, 4, 4>::NTH, BTile2<4, 4, 4>::SMEM, c->stream>>>(u, xs, p, c->G, c->sB, nomask,
+                                                                                       se, sm);
+    LAUNCH_CHECK(c);
+    return WB_OK;
+  }
   return DISPATCH_K(c, launch_B_t, u, xs, p, nomask, stop, dv, total, se, sm);
 }
 
