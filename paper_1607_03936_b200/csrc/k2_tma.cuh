@@ -1,10 +1,10 @@
 // k2_tma.cuh -- the fused k = 2 Poisson operator (k2_fused.cuh) with TMA
 // staging: persistent CTAs (one per SM) walk the element tiles; the halo box of
-// p_old, r, Minv (4-D tensor maps over the mode-major PCG vectors, hardware
-// zero fill outside the mesh) and the X box (3-D tensor map over a copy of X
+// p_old and z = Minv r (4-D tensor maps over the mode-major PCG vectors, hardware
+// zero fill outside the mesh; z is stored by the PCG update kernel) and the X box (3-D tensor map over a copy of X
 // with 16-byte-aligned rows) land in shared memory by cp.async.bulk.tensor,
 // completion tracked by mbarriers.  Each buffer is refilled for the NEXT tile
-// as soon as the current tile has consumed it (r, Minv after step 0, X after
+// as soon as the current tile has consumed it (p, z after step 0, X after
 // step 1, p after step 2), so the loads overlap the compute of steps 1 and 2.
 // Same arithmetic as k_K2_fused (identical per-node / per-element order).
 #pragma once
@@ -12,6 +12,11 @@
 #include "k2_fused.cuh"
 
 namespace wb {
+
+// phase-timing probe (k_dbg bit 0x4000): thread 0 of every CTA adds its clock64 cycles
+// per phase: [0] prologue/control, [1] wait p/r/Minv, [2] step 0 (+ barrier),
+// [3] wait X, [4] step 1 (+ barrier), [5] step 2 (+ barrier), [6] tiles
+__device__ unsigned long long g_kprof[8];
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -81,7 +86,7 @@ struct FKT {
     return ((ny & 1) ? ((nz & 1) ? R00 + R10 + R01 : R00) : ((nz & 1) ? R00 + R10 : 0)) +
            (ny >> 1) + ((ny & 1) ? TY : TY + 1) * (nz >> 1);
   }
-  // shared layout (bytes): raw p | raw r | raw Minv | Ps | X | T | barriers, each 1024-aligned
+  // shared layout (bytes): raw p | raw r or z | raw Minv | Ps | X | T | barriers, each 1024-aligned
   static constexpr size_t al(size_t b) { return (b + 1023) & ~(size_t)1023; }
   static constexpr size_t OFF_P = 0, OFF_R = al(PBYTES), OFF_M = OFF_R + al(PBYTES), OFF_S = OFF_M + al(PBYTES),
                           OFF_X = OFF_S + al(4u * NHP * 8u), OFF_T = OFF_X + al(XBYTES),
@@ -166,9 +171,11 @@ __device__ __forceinline__ void fkt_pencil(const double* __restrict__ Ps, double
 
 // Same contract as k_K2_fused (mode, ctl, partials), tensor maps instead of pointers for the
 // loads: tm_pold / tm_r / tm_minv over [m][ez][ey][ex], tm_x over the padded nodal X.
-template <int TX, int TY, int TZ, int MINB>
+// ZB: the PCG update kernels store z = Minv r and the kernel loads a z box; else it
+// loads r and Minv boxes and forms Minv r itself (same product either way).
+template <int TX, int TY, int TZ, int MINB, bool ZB>
 __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
-    k_K2_tma(const __grid_constant__ CUtensorMap tm_pold, const __grid_constant__ CUtensorMap tm_r,
+    k_K2_tma(const __grid_constant__ CUtensorMap tm_pold, const __grid_constant__ CUtensorMap tm_z,
              const __grid_constant__ CUtensorMap tm_minv, const __grid_constant__ CUtensorMap tm_x,
              double* __restrict__ pnew, double* __restrict__ q, Geo G, double sB, int mode, int it, int ctl,
              const double* __restrict__ rzp, int nrz, double* rz_hist, const double* pq_hist, int* stop,
@@ -180,8 +187,9 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sb = smraw;
   double* Pb = (double*)(sb + K::OFF_P);  // raw boxes (BXW x HY x HZ x 4)
-  double* Rb = (double*)(sb + K::OFF_R);
-  double* Mb = (double*)(sb + K::OFF_M);
+  double* Zb = (double*)(sb + K::OFF_R);  // z = Minv r (ZB), else r
+  double* Mb = (double*)(sb + K::OFF_M);  // Minv (!ZB)
+  constexpr unsigned RAWB = (ZB ? 2u : 3u) * K::PBYTES;
   double* Ps = (double*)(sb + K::OFF_S);  // p on the tile + halo, rows of F::PX
   double* Xs = (double*)(sb + K::OFF_X);
   double* T = (double*)(sb + K::OFF_T);
@@ -202,17 +210,22 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     if (tile < n_tiles) {
       int ex0, ey0, ez0;
       coords(tile, ex0, ey0, ez0);
-      mbar_expect_tx(&bar[0], 3 * K::PBYTES);
-      tma_load_4d(Rb, &tm_r, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
-      tma_load_4d(Mb, &tm_minv, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
+      mbar_expect_tx(&bar[0], RAWB);
+      tma_load_4d(Zb, &tm_z, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
+      if (!ZB) tma_load_4d(Mb, &tm_minv, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
       tma_load_4d(Pb, &tm_pold, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
       mbar_expect_tx(&bar[2], K::XBYTES);
       tma_load_3d(Xs, &tm_x, 2 * ex0, 2 * ey0, 2 * ez0, &bar[2]);
     }
   }
+  // timing probe bits (option k_dbg; results invalid): 0x100 skip step 1, 0x200 skip
+  // step 2, 0x400 skip step 0's arithmetic and stores, 0x800 skip the q stores, 0x1000
+  // skip the p_new stores, 0x2000 never stop
+  const int dbg = mode & 0xff00;
+  mode &= 0xff;
   double beta = 0.0;
   if (ctl) {
-    if (pcg_control<F::NTH>(it, rzp, nrz, rz_hist, pq_hist, stop, &beta)) {
+    if (pcg_control<F::NTH>(it, rzp, nrz, rz_hist, pq_hist, stop, &beta) && !(dbg & 0x2000)) {
       // stopped: drain the bulk copies in flight before the CTA exits
       if (threadIdx.x == 0 && tile < n_tiles) { mbar_wait(&bar[0], 0); mbar_wait(&bar[2], 0); }
       return;
@@ -221,6 +234,19 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     beta = rz_hist[it] / rz_hist[it - 1];
   }
   __syncthreads();  // barrier init visible to all threads (pcg_control ends with one too)
+#ifdef WB_KPROF  // phase timers (tools/kphase.py builds with -DWB_KPROF)
+  const bool prof = (dbg & 0x4000) && threadIdx.x == 0;
+  unsigned long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // [7]: TMA issue after step 0
+  long long tc = clock64();
+  auto lap = [&](int k) {
+    if (prof) { const long long n = clock64(); pt[k] += (unsigned long long)(n - tc); tc = n; }
+  };
+#else
+  constexpr bool prof = false;
+  unsigned long long pt[8];
+  auto lap = [](int) {};
+#endif
+  lap(0);
   double dot = 0.0;
   for (int k = 0; tile < n_tiles; ++k, tile += gridDim.x) {
     const unsigned ph = k & 1;
@@ -230,7 +256,8 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     if (next < n_tiles) coords(next, nx0, ny0, nz0);
     // 0. p = Minv r (+ beta p_old) from the raw boxes into Ps; own elements -> p_new
     mbar_wait(&bar[0], ph);
-    for (int i = threadIdx.x; i < K::NHD; i += F::NTH) {
+    lap(1);
+    for (int i = threadIdx.x; i < ((dbg & 0x400) ? 0 : K::NHD); i += F::NTH) {
       const int hx = i % K::HX, hy = (i / K::HX) % K::HY, hz = i / (K::HX * K::HY);
       const int ex = ex0 + hx - 1, ey = ey0 + hy - 1, ez = ez0 + hz - 1;
       const bool own = hx >= 1 && hy >= 1 && hz >= 1 && hx <= TX && hy <= TY && hz <= TZ && ex < N && ey < N &&
@@ -244,25 +271,28 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
         if (hx < K::HX) {  // pad column of Ps stays 0
           if (mode == 2) v = Pb[j];
           else {
-            const double z = Mb[j] * Rb[j];
+            const double z = ZB ? Zb[j] : Mb[j] * Zb[j];
             v = (mode == 1) ? fma(beta, Pb[j], z) : z;
           }
         }
         Ps[m * K::NHP + K::pidx(hx, hy, hz)] = v;
-        if (own) pnew[m * ne + e] = v;
+        if (own && !(dbg & 0x1000)) pnew[m * ne + e] = v;
       }
     }
     __syncthreads();
+    lap(2);
     if (threadIdx.x == 0 && next < n_tiles) {  // raw p, r, Minv buffers are free
       fence_proxy_async();
-      mbar_expect_tx(&bar[0], 3 * K::PBYTES);
-      tma_load_4d(Rb, &tm_r, nx0 - 2, ny0 - 1, nz0 - 1, 0, &bar[0]);
-      tma_load_4d(Mb, &tm_minv, nx0 - 2, ny0 - 1, nz0 - 1, 0, &bar[0]);
+      mbar_expect_tx(&bar[0], RAWB);
+      tma_load_4d(Zb, &tm_z, nx0 - 2, ny0 - 1, nz0 - 1, 0, &bar[0]);
+      if (!ZB) tma_load_4d(Mb, &tm_minv, nx0 - 2, ny0 - 1, nz0 - 1, 0, &bar[0]);
       tma_load_4d(Pb, &tm_pold, nx0 - 2, ny0 - 1, nz0 - 1, 0, &bar[0]);
     }
+    lap(7);
     // 1. t at the tile nodes by x-pencils
     mbar_wait(&bar[2], ph);
-    {
+    lap(3);
+    if (!(dbg & 0x100)) {
       const int t = threadIdx.x;
       if (t < F::OFF1) {
         if (t < F::cls_n(0, 0)) fkt_pencil<TX, TY, TZ, 0, 0>(Ps, T, Xs, t % (TY + 1), t / (TY + 1), sB);
@@ -278,13 +308,14 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
       }
     }
     __syncthreads();
+    lap(4);
     if (threadIdx.x == 0 && next < n_tiles) {  // X buffer is free
       fence_proxy_async();
       mbar_expect_tx(&bar[2], K::XBYTES);
       tma_load_3d(Xs, &tm_x, 2 * nx0, 2 * ny0, 2 * nz0, &bar[2]);
     }
     // 2. q = sB Bt^T t per element, <p, q>
-    if (threadIdx.x < F::NE) {
+    if (threadIdx.x < F::NE && !(dbg & 0x200)) {
       const int lx = threadIdx.x % TX, ly = (threadIdx.x / TX) % TY, lz = threadIdx.x / (TX * TY);
       const int ex = ex0 + lx, ey = ey0 + ly, ez = ez0 + lz;
       if (ex < N && ey < N && ez < N) {
@@ -313,13 +344,17 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
           const double o = sB * qm[m];
-          q[m * ne + e] = o;
+          if (!(dbg & 0x800)) q[m * ne + e] = o;
           dot = fma(Ps[m * K::NHP + h], o, dot);
         }
       }
     }
     __syncthreads();  // Ps, T are rewritten by the next tile
+    lap(5);
+    if (prof) ++pt[6];
   }
+  if (prof)
+    for (int k = 0; k < 8; ++k) atomicAdd(&g_kprof[k], pt[k]);
   store_partial<F::NTH>(dot, pqp);
 }
 

@@ -881,10 +881,11 @@ __device__ __forceinline__ bool pcg_control(int i, const double* __restrict__ rz
 }
 
 // init: r = P b (element-major b -> mode-major r, constant-mode mean removed
-// using bsum = sum_e b[e*nm]); x = 0; partials of rz_0 = <r, Minv r> -> rzp.
+// using bsum = sum_e b[e*nm]); x = 0; partials of rz_0 = <r, Minv r> -> rzp;
+// z = Minv r stored when z != NULL (the TMA Poisson kernel reads it).
 __global__ void __launch_bounds__(VBS) k_pcg_init(const double* __restrict__ b, const double* __restrict__ bsum,
                                                   double* x, double* r, const double* __restrict__ Minv, int64_t ne,
-                                                  int nm, double* rzp) {
+                                                  int nm, double* rzp, double* z) {
   const double mean = *bsum / (double)ne;
   const int64_t n = ne * nm;
   double s = 0.0;
@@ -892,7 +893,9 @@ __global__ void __launch_bounds__(VBS) k_pcg_init(const double* __restrict__ b, 
     const int64_t m = i / ne, e = i % ne;
     const double bi = (m == 0) ? b[e * nm] - mean : b[e * nm + m];
     x[i] = 0.0; r[i] = bi;
-    s = fma(bi, Minv[i] * bi, s);
+    const double zi = Minv[i] * bi;
+    if (z) z[i] = zi;
+    s = fma(bi, zi, s);
   }
   store_partial<VBS>(s, rzp);
 }
@@ -919,23 +922,62 @@ __global__ void __launch_bounds__(VBS) k_pupd(double* pout, const double* pin, c
 
 // iteration i: pq_i = sum of the K kernel's <p_i, q> partials (pqp, npq);
 // alpha = rz_i / pq_i; x += alpha p; r -= alpha q; partials of
-// rz_{i+1} = <r, Minv r> -> rzp.  Block 0 records pq_hist[i].
+// rz_{i+1} = <r, Minv r> -> rzp; z = Minv r stored when z != NULL.  Block 0
+// records pq_hist[i].
+// Streaming: the vectors are 16-byte aligned (cudaMalloc, n even), so each thread
+// moves pairs (double2) and keeps U pairs of all five inputs in flight before any
+// arithmetic; the first batch is issued before the pq reduction, which only the
+// arithmetic needs.  The rz partial of a thread sums its entries in index order.
+template <int U>
+__device__ __forceinline__ void pcg_upd_batch(int64_t j0, int64_t stride, int64_t n2, const double2* x,
+                                              const double2* r, const double2* p, const double2* q,
+                                              const double2* M, double2 (&X)[U], double2 (&R)[U],
+                                              double2 (&P)[U], double2 (&Q)[U], double2 (&Mv)[U]) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t j = j0 + u * stride;
+    if (j < n2) { X[u] = x[j]; R[u] = r[j]; P[u] = p[j]; Q[u] = __ldcg(q + j); Mv[u] = M[j]; }
+  }
+}
 __global__ void __launch_bounds__(VBS) k_pcg_upd(double* x, double* r, const double* __restrict__ p,
                                                  const double* __restrict__ q, const double* __restrict__ Minv,
                                                  int64_t n, int i, const double* __restrict__ pqp, int npq,
                                                  const double* rz_hist, double* pq_hist, const int* stop,
-                                                 double* rzp) {
+                                                 double* rzp, double* z) {
+  constexpr int U = 2;
   if (stop[i]) return;
+  const int64_t n2 = n / 2;  // n = 4 n_el is even
+  const int64_t stride = (int64_t)gridDim.x * VBS;
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  double2* z2 = reinterpret_cast<double2*>(z);
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  const double2* q2 = reinterpret_cast<const double2*>(q);
+  const double2* M2 = reinterpret_cast<const double2*>(Minv);
+  double2 X[U], R[U], P[U], Q[U], Mv[U];
+  int64_t j0 = (int64_t)blockIdx.x * VBS + threadIdx.x;
+  pcg_upd_batch<U>(j0, stride, n2, x2, r2, p2, q2, M2, X, R, P, Q, Mv);
   const double pq = sum_partials<VBS>(pqp, npq);
   if (blockIdx.x == 0 && threadIdx.x == 0) pq_hist[i] = pq;
   if (pq == 0.0) return;
   const double alpha = rz_hist[i] / pq;
   double s = 0.0;
-  for (int64_t j = (int64_t)blockIdx.x * VBS + threadIdx.x; j < n; j += (int64_t)gridDim.x * VBS) {
-    x[j] = fma(alpha, p[j], x[j]);
-    const double rj = fma(-alpha, q[j], r[j]);
-    r[j] = rj;
-    s = fma(rj, Minv[j] * rj, s);
+  for (; j0 < n2; j0 += U * stride) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + u * stride;
+      if (j < n2) {
+        double2 xo, ro, zo;
+        xo.x = fma(alpha, P[u].x, X[u].x); xo.y = fma(alpha, P[u].y, X[u].y);
+        ro.x = fma(-alpha, Q[u].x, R[u].x); ro.y = fma(-alpha, Q[u].y, R[u].y);
+        zo.x = Mv[u].x * ro.x; zo.y = Mv[u].y * ro.y;
+        x2[j] = xo; r2[j] = ro;
+        if (z) z2[j] = zo;
+        s = fma(ro.x, zo.x, s);
+        s = fma(ro.y, zo.y, s);
+      }
+    }
+    pcg_upd_batch<U>(j0 + U * stride, stride, n2, x2, r2, p2, q2, M2, X, R, P, Q, Mv);
   }
   store_partial<VBS>(s, rzp);
 }

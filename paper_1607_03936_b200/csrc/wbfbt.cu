@@ -37,6 +37,7 @@ struct wb_ctx {
   double *tv = nullptr, *tw = nullptr;  // n_v
   // PCG vectors, mode-major v[m*n_el + e]: x, r, p (double buffer), q
   double *px = nullptr, *pr = nullptr, *pp = nullptr, *pp1 = nullptr, *pq = nullptr;
+  double* pz = nullptr;  // z = Minv r, stored by the PCG init/update kernels for the TMA Poisson kernel
   // CUDA graphs of the PCG iteration loop, keyed by (side, iters)
   struct GraphEntry { int side = 0, iters = 0; long long n_launch = 0; cudaGraphExec_t exec = nullptr; };
   static constexpr int MAX_GRAPHS = 8;
@@ -67,8 +68,13 @@ struct wb_ctx {
   bool tma_ok = false;
   int use_tma = 1;
   double *XpL = nullptr, *XpR = nullptr;
+  // k = 2, even N: MinvL | XpL | x r p p' q z | MinvR | XpR carved from one slab (each
+  // side's PCG working set contiguous; a persisting L2 access-policy window over it was
+  // measured and gave no gain)
+  double* slab = nullptr;
   int xp = 0;
-  CUtensorMap tm_pp, tm_pp1, tm_pr, tm_mL, tm_mR, tm_xL, tm_xR;
+  CUtensorMap tm_pp, tm_pp1, tm_pz, tm_pr, tm_mL, tm_mR, tm_xL, tm_xR;
+  int kz = 1;  // TMA Poisson kernel: 1 = z = Minv r stored by the PCG update and loaded as one box (default)
   int k_dbg = 0;  // timing probe bits for the fused K kernel (results invalid when nonzero)
   // profiling: CUDA-event pairs around every Poisson-operator launch (direct launches)
   int profile = 0;
@@ -228,6 +234,7 @@ wb_status launch_k2f_t(wb_ctx* c, const double* pold, double* pnew, const double
 const CUtensorMap* tmap_of(wb_ctx* c, const double* p) {
   if (p == c->pp) return &c->tm_pp;
   if (p == c->pp1) return &c->tm_pp1;
+  if (p == c->pz) return &c->tm_pz;
   if (p == c->pr) return &c->tm_pr;
   if (p == c->MinvL) return &c->tm_mL;
   if (p == c->MinvR) return &c->tm_mR;
@@ -236,18 +243,24 @@ const CUtensorMap* tmap_of(wb_ctx* c, const double* p) {
   return nullptr;
 }
 
+// the k = 2 Poisson operator runs as the TMA kernel (k_K2_tma); the PCG init/update
+// kernels then also store z = Minv r, which it reads instead of r and Minv
+bool tma_active(const wb_ctx* c) { return c->k == 2 && c->tma_ok && c->use_tma && c->n_el >= 148 * 256 * 2; }
+double* z_out(const wb_ctx* c) { return tma_active(c) && c->kz ? c->pz : nullptr; }
+
 wb_status run_k2f(wb_ctx* c, const double* pold, double* pnew, const double* r, const double* Minv, const double* X,
                   double* q, int mode, PcgArgs a, int* npq) {
-  if (c->tma_ok && c->use_tma && c->n_el >= 148 * 256 * 2) {
+  if (tma_active(c)) {
     using KT = FKT<TMA_TX, TMA_TY, TMA_TZ>;
-    const CUtensorMap *tp = tmap_of(c, pold), *tr = tmap_of(c, r ? r : c->pr), *tm = tmap_of(c, Minv),
+    const CUtensorMap *tp = tmap_of(c, pold), *tz = tmap_of(c, c->kz ? c->pz : c->pr), *tm = tmap_of(c, Minv),
                       *tx = tmap_of(c, X);
-    if (tp && tr && tm && tx) {
+    if (tp && tz && tm && tx && (mode == 2 || r == c->pr)) {
       const int N = c->N;
       const int nt = ((N + TMA_TX - 1) / TMA_TX) * ((N + TMA_TY - 1) / TMA_TY) * ((N + TMA_TZ - 1) / TMA_TZ);
       const int grid = std::max(1, std::min(nt, TMA_MINB * c->nsm));  // persistent, all resident
-      k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB><<<grid, FK2<TMA_TX, TMA_TY, TMA_TZ>::NTH, KT::SMEM, c->stream>>>(
-          *tp, *tr, *tm, *tx, pnew, q, c->G, c->sB, mode, a.it, a.ctl, c->rzp, c->red_blocks, rz_hist(c),
+      auto kern = c->kz ? k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, true> : k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, false>;
+      kern<<<grid, FK2<TMA_TX, TMA_TY, TMA_TZ>::NTH, KT::SMEM, c->stream>>>(
+          *tp, *tz, *tm, *tx, pnew, q, c->G, c->sB, mode | c->k_dbg, a.it, a.ctl, c->rzp, c->red_blocks, rz_hist(c),
           pq_hist(c), c->stop, c->pqp);
       LAUNCH_CHECK(c);
       *npq = grid;
@@ -301,18 +314,21 @@ bool setup_tma(wb_ctx* c) {
   if (c->k != 2 || (c->N & 1) || !get_encode()) return false;
   c->xp = (c->G.nn1 + 1) & ~1;
   const size_t bx = sizeof(double) * (size_t)c->G.nn1 * c->G.nn1 * c->xp;
-  if (cudaMalloc(&c->XpL, bx) != cudaSuccess || cudaMalloc(&c->XpR, bx) != cudaSuccess) {
+  if (!c->slab && (cudaMalloc(&c->XpL, bx) != cudaSuccess || cudaMalloc(&c->XpR, bx) != cudaSuccess)) {
     cudaGetLastError();
     return false;
   }
-  if (cudaFuncSetAttribute(k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)FKT<TMA_TX, TMA_TY, TMA_TZ>::SMEM) != cudaSuccess) {
+  if (cudaFuncSetAttribute(k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FKT<TMA_TX, TMA_TY, TMA_TZ>::SMEM) != cudaSuccess ||
+      cudaFuncSetAttribute(k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FKT<TMA_TX, TMA_TY, TMA_TZ>::SMEM) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
   return make_tm_vec(&c->tm_pp, c->pp, c->N, c->nm) && make_tm_vec(&c->tm_pp1, c->pp1, c->N, c->nm) &&
-         make_tm_vec(&c->tm_pr, c->pr, c->N, c->nm) && make_tm_vec(&c->tm_mL, c->MinvL, c->N, c->nm) &&
-         make_tm_vec(&c->tm_mR, c->MinvR, c->N, c->nm) && make_tm_x(&c->tm_xL, c->XpL, c->G.nn1, c->xp) &&
+         make_tm_vec(&c->tm_pz, c->pz, c->N, c->nm) && make_tm_vec(&c->tm_pr, c->pr, c->N, c->nm) &&
+         make_tm_vec(&c->tm_mL, c->MinvL, c->N, c->nm) && make_tm_vec(&c->tm_mR, c->MinvR, c->N, c->nm) &&
+         make_tm_x(&c->tm_xL, c->XpL, c->G.nn1, c->xp) &&
          make_tm_x(&c->tm_xR, c->XpR, c->G.nn1, c->xp);
 }
 
@@ -431,7 +447,8 @@ wb_status pcg_loop_direct(wb_ctx* c, int side, int iters) {
     if (s) return s;
     if (prof) CUDA_TRY(c, cudaEventRecord(c->prof_ev[2 * c->prof_n++ + 1], c->stream));
     k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->n_p, it, c->pqp, npq,
-                                                    rz_hist(c), pq_hist(c), c->stop, c->rzp);
+                                                    rz_hist(c), pq_hist(c), c->stop, c->rzp,
+                                                    z_out(c));
     LAUNCH_CHECK(c);
   }
   return WB_OK;
@@ -481,7 +498,8 @@ wb_status run_poisson(wb_ctx* c, int side, const double* b, double* x, int iters
   const double* Minv = side == 0 ? c->MinvL : c->MinvR;
   k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->n_el, c->nm, c->partial, c->counter, c->scal + S_SUM);
   LAUNCH_CHECK(c);
-  k_pcg_init<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->scal + S_SUM, c->px, c->pr, Minv, c->n_el, c->nm, c->rzp);
+  k_pcg_init<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->scal + S_SUM, c->px, c->pr, Minv, c->n_el, c->nm, c->rzp,
+                                                   z_out(c));
   LAUNCH_CHECK(c);
   if ((s = pcg_loop(c, side, iters))) return s;
   k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->n_el, 1, c->partial, c->counter, c->scal + S_SUM + 1);
@@ -529,7 +547,7 @@ wb_status check_ctx(wb_ctx* c, bool need_visc) {
 
 void free_all(wb_ctx* c) {
   double** bufs[] = {&c->mut, &c->Cw, &c->Dw, &c->Cinv, &c->Dinv, &c->dKl, &c->dKr, &c->MinvL, &c->MinvR,
-                     &c->E, &c->tv, &c->tw, &c->px, &c->pr, &c->pp, &c->pp1, &c->pq, &c->s0, &c->s1, &c->s2,
+                     &c->E, &c->tv, &c->tw, &c->px, &c->pr, &c->pp, &c->pp1, &c->pq, &c->pz, &c->s0, &c->s1, &c->s2,
                      &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->Fu};
   clear_graphs(c);
   if (c->cap_stream) { cudaStreamDestroy(c->cap_stream); c->cap_stream = nullptr; }
@@ -538,6 +556,11 @@ void free_all(wb_ctx* c) {
     if (*e) { cudaEventDestroy(*e); *e = nullptr; }
   for (int i = 0; i < 2 * wb_ctx::PROF_MAX; ++i)
     if (c->prof_ev[i]) { cudaEventDestroy(c->prof_ev[i]); c->prof_ev[i] = nullptr; }
+  if (c->slab) {  // carved arrays: one free, before the per-buffer frees below
+    c->MinvL = c->MinvR = c->XpL = c->XpR = c->px = c->pr = c->pp = c->pp1 = c->pq = c->pz = nullptr;
+    cudaFree(c->slab);
+    c->slab = nullptr;
+  }
   for (double** b : bufs)
     if (*b) { cudaFree(*b); *b = nullptr; }
   if (c->counter) cudaFree(c->counter);
@@ -547,6 +570,7 @@ void free_all(wb_ctx* c) {
   if (c->XpR) cudaFree(c->XpR);
   c->XpL = c->XpR = nullptr;
   c->counter = nullptr; c->stop = nullptr; c->icount = nullptr;
+  cudaGetLastError();  // teardown must not leave an error for the next context's launch checks
 }
 
 }  // namespace
@@ -627,11 +651,27 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
     if (ok && cudaMalloc(p, sizeof(double) * (size_t)(n > 0 ? n : 1)) != cudaSuccess) ok = false;
   };
   alloc(&c->Cw, c->n_nodes); alloc(&c->Dw, c->n_nodes); alloc(&c->Cinv, c->n_nodes); alloc(&c->Dinv, c->n_nodes);
-  alloc(&c->dKl, c->n_p); alloc(&c->dKr, c->n_p); alloc(&c->MinvL, c->n_p); alloc(&c->MinvR, c->n_p);
+  if (k == 2 && !(N & 1)) {
+    const int64_t nn1 = 2 * (int64_t)N + 1, xp = (nn1 + 1) & ~1;
+    auto up = [](int64_t n) { return (n + 31) & ~(int64_t)31; };  // 256-byte sub-arrays
+    const int64_t np = up(c->n_p), nx = up(nn1 * nn1 * xp);
+    if (ok && cudaMalloc(&c->slab, sizeof(double) * (size_t)(8 * np + 2 * nx)) != cudaSuccess) ok = false;
+    if (ok) {
+      double* q = c->slab;
+      c->MinvL = q; q += np; c->XpL = q; q += nx;
+      c->px = q; q += np; c->pr = q; q += np; c->pp = q; q += np; c->pp1 = q; q += np; c->pq = q; q += np;
+      c->pz = q; q += np;
+      c->MinvR = q; q += np; c->XpR = q;
+    }
+  }
+  alloc(&c->dKl, c->n_p); alloc(&c->dKr, c->n_p);
+  if (!c->slab) { alloc(&c->MinvL, c->n_p); alloc(&c->MinvR, c->n_p); }
   alloc(&c->E, (k == 2 ? 1 : 3) * c->nq * c->n_el);  // k = 2: setup only (lumped element values)
   alloc(&c->tv, c->n_v); alloc(&c->tw, c->n_v);
-  alloc(&c->px, c->n_p); alloc(&c->pr, c->n_p); alloc(&c->pp, c->n_p); alloc(&c->pp1, c->n_p);
-  alloc(&c->pq, c->n_p);
+  if (!c->slab) {
+    alloc(&c->px, c->n_p); alloc(&c->pr, c->n_p); alloc(&c->pp, c->n_p); alloc(&c->pp1, c->n_p);
+    alloc(&c->pq, c->n_p); alloc(&c->pz, c->n_p);
+  }
   alloc(&c->s0, c->n_p); alloc(&c->s1, c->n_p); alloc(&c->s2, c->n_p);
   alloc(&c->partial, c->max_partials);
   alloc(&c->pqp, c->n_el / 32 + 1024);  // >= blocks of any K-apply grid (tiles >= 64 elements, k_B 128)
@@ -918,7 +958,7 @@ wb_status wb_debug_pcg_step(wb_ctx* c, int side, double* x, double* r, double* p
   a.it = 1; a.ctl = 0;  // rz_1 and stop_1 given
   if ((s = run_K_pcg(c, side, 2, c->pp, c->pp1, c->pr, c->pq, a, &pcur, &npq))) return s;
   k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->n_p, 1, c->pqp, npq,
-                                                  rz_hist(c), pq_hist(c), c->stop, c->rzp);
+                                                  rz_hist(c), pq_hist(c), c->stop, c->rzp, nullptr);
   LAUNCH_CHECK(c);
   // p = Minv r + (rz_2 / rz_1) p with the control of iteration 2 (records rz_2)
   double* pc = const_cast<double*>(pcur);
@@ -969,8 +1009,19 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
     CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_K2_fused<4, 8, 8, 2>, FK2<4, 8, 8>::NTH,
                                                               FK2<4, 8, 8>::SMEM));
     *value = nb;
+  } else if (!strncmp(key, "kprof", 5) && key[5] >= '0' && key[5] <= '7' && !key[6]) {
+    // phase-timing probe of the TMA Poisson kernel (k_dbg 0x4000): accumulated cycles;
+    // reading "kprof7" (the last) clears the counters
+    unsigned long long h[8];
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    CUDA_TRY(c, cudaMemcpyFromSymbol(h, g_kprof, sizeof(h)));
+    *value = (double)h[key[5] - '0'];
+    if (key[5] == '7') {
+      memset(h, 0, sizeof(h));
+      CUDA_TRY(c, cudaMemcpyToSymbol(g_kprof, h, sizeof(h)));
+    }
   } else if (!strcmp(key, "k_tma")) {  // 1: the Poisson operator runs as the TMA kernel (k_K2_tma)
-    *value = (c->k == 2 && c->tma_ok && c->use_tma && c->n_el >= 148 * 256 * 2) ? 1.0 : 0.0;
+    *value = tma_active(c) ? 1.0 : 0.0;
   } else if (!strcmp(key, "occ_a2")) {
     int nb = 0;
     CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_A_tile<A_TX, A_TY, A_TZ, A_MINB>, 3 * A_TX * A_TY * A_TZ, Tile2<A_TX, A_TY, A_TZ>::SMEM));
@@ -1008,6 +1059,10 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
   } else if (!strcmp(key, "k_variant")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k_variant must be 0 or 1");
     c->k_var = (int)value;
+    clear_graphs(c);
+  } else if (!strcmp(key, "kz")) {
+    if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "kz must be 0 or 1");
+    c->kz = (int)value;
     clear_graphs(c);
   } else if (!strcmp(key, "tma")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "tma must be 0 or 1");

@@ -1,5 +1,5 @@
-"""Phase timing probe of the fused K kernel (option k_dbg; results invalid):
-per-iteration time of the graph-replayed PCG loop, (t(50) - t(10)) / 40."""
+"""Per PCG iteration time (graph replay, (t(50) - t(10)) / 40) at C5 over option settings.
+usage: python tools/opt_ab.py C5 "kz=0,l2win=0" "kz=1,l2win=1" ...   (each argument one setting)"""
 import os
 import statistics
 import sys
@@ -10,17 +10,17 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 from paper_1607_03936_b200 import Context  # noqa: E402
 
-cfg = sys.argv[1] if len(sys.argv) > 1 else "C5"
-inp = synth.make_inputs(cfg, 0)
+inp = synth.make_inputs(sys.argv[1], 0)
 c = Context(inp["N"], inp["k"])
 d = lambda a: torch.as_tensor(a, dtype=torch.float64, device="cuda")  # noqa: E731
 mu, p = d(inp["mu_q"]), d(inp["p"])
 pv = torch.empty(c.n_p, dtype=torch.float64, device="cuda")
 c.set_viscosity(mu)
 st = torch.cuda.current_stream()
+reps = int(os.environ.get("AB_REPS", "7"))
 
 
-def t_us(it, reps=7):
+def t_us(it):
     c.poisson_pcg(1, p, pv, it)
     ts = []
     for _ in range(reps):
@@ -30,12 +30,12 @@ def t_us(it, reps=7):
     return statistics.median(ts) * 1e3
 
 
-probes = [("full", 0), ("no step0", 0x400), ("no step1 (pencils)", 0x100), ("no step2 (elements)", 0x200),
-          ("no step1+2", 0x300), ("loads+control only", 0x700), ("no q stores", 0x800),
-          ("no pnew stores", 0x1000), ("no q, pnew stores", 0x1800)]
-for name, dbg in probes:
-    c.set_option("k_dbg", dbg | 0x2000)  # 0x2000: never stop (probe)
+ref = None
+for setting in sys.argv[2:]:
+    for kv in setting.split(","):
+        k, v = kv.split("=")
+        c.set_option(k, float(v))
     per = (t_us(50) - t_us(10)) / 40
-    print(f"k_tma={int(c.query('k_tma'))} {name:24s}: per PCG iteration {per:7.2f} us")
-c.set_option("k_dbg", 0)
-print("occupancy CTAs/SM: K2", c.query("occ_k2"), "A", c.query("occ_a2"))
+    out = pv.clone()
+    ref = out if ref is None else ref
+    print(f"{setting:30s}: per PCG iteration {per:7.2f} us  (max rel diff vs first {float((out - ref).abs().max() / ref.abs().max()):.1e})")
