@@ -206,9 +206,10 @@ struct Tile2 {
 // (local 2); A = 0 -> element l-1 (local 2, if l > 0) then element l (local 0).
 // Elements in ascending index order.  A is compile-time after unrolling.
 template <int TX, int TY, int TZ>
-__device__ __forceinline__ double a2_node_sum(const double* __restrict__ Rb, int lx, int ly, int lz, int AX, int AY,
-                                              int AZ) {
-  // Rb = R + c * 27 * NE + le: slot (c, a, element le + d) at Rb[a * NE + d]
+__device__ __forceinline__ double a2_node_sum(const double* __restrict__ Rb, const double (&V)[27], int lx, int ly,
+                                              int lz, int AX, int AY, int AZ) {
+  // Rb = R + c * 27 * NE + le: slot (c, a, element le + d) at Rb[a * NE + d].  The own
+  // element's term (always the last one) comes from its registers V.
   constexpr int NE = TX * TY * TZ;
   double acc = 0.0;
 #pragma unroll
@@ -226,12 +227,17 @@ __device__ __forceinline__ double a2_node_sum(const double* __restrict__ Rb, int
         if (AX != 0 && kx == 1) continue;
         const int dx = AX == 0 ? kx - 1 : 0, ax = AX == 0 ? (kx == 0 ? 2 : 0) : AX;
         if (lx + dx < 0) continue;
-        acc += Rb[(ax + 3 * (ay + 3 * az)) * NE + dx + TX * (dy + TY * dz)];
+        const int a = ax + 3 * (ay + 3 * az);
+        acc += (dx == 0 && dy == 0 && dz == 0) ? V[a] : Rb[a * NE + dx + TX * (dy + TY * dz)];
       }
     }
   }
   return acc;
 }
+
+// slots read by other threads: local index 2 in some axis (the node belongs to the
+// next element or the upper shell)
+__host__ __device__ constexpr bool a2_slot_shared(int a) { return a % 3 == 2 || (a / 3) % 3 == 2 || a / 9 == 2; }
 
 __device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -350,7 +356,8 @@ __global__ void __launch_bounds__(3 * TX * TY * TZ, MINB)
   // element slots R[c][a][le] (the exchange buffer is free after the last level's barrier)
   double* Rb = X + c * 27 * NE + le;
 #pragma unroll
-  for (int a = 0; a < 27; ++a) Rb[a * NE] = V[a];
+  for (int a = 0; a < 27; ++a)
+    if (a2_slot_shared(a)) Rb[a * NE] = V[a];
   __syncthreads();
   // Each thread is responsible for the tile nodes 2l + A, A_d in {0, 1}, plus A_d = 2
   // on the tile's upper face (l_d = T_d - 1): every tile node has exactly one
@@ -365,7 +372,7 @@ __global__ void __launch_bounds__(3 * TX * TY * TZ, MINB)
       for (int AX = 0; AX < 3; ++AX) {
         if ((AX == 2 && lx != TX - 1) || (AY == 2 && ly != TY - 1) || (AZ == 2 && lz != TZ - 1)) continue;
         const int nx = 2 * lx + AX, ny = 2 * ly + AY, nz = 2 * lz + AZ;
-        const double s = a2_node_sum<TX, TY, TZ>(Rb, lx, ly, lz, AX, AY, AZ);
+        const double s = a2_node_sum<TX, TY, TZ>(Rb, V, lx, ly, lz, AX, AY, AZ);
         if (AX == 2 || AY == 2 || AZ == 2) {
           Fut[T::shell(nx, ny, nz)] = s;
         } else {

@@ -79,6 +79,9 @@ struct FKT {
   static constexpr int NROW = R00 + R10 + R01 + R11;
   static constexpr int TC = NROW + ((20 - NROW % 16) % 16);
   static constexpr int TN = F::MX * TC;
+  // the thread that issues the per-tile TMA loads: lane 0 of the last warp (light
+  // class-(1,1) pencils, no element in step 2), off the heavy warps' critical path
+  static constexpr int TMA_T = F::NTH - 32;
   // row sums S[c][m1][lx][row] (x-contracted B per element of the row) in the T region
   __host__ __device__ static constexpr int sidx(int c, int m1, int lx) { return ((c * 2 + m1) * TX + lx) * TC; }
   static_assert(6 * TX <= 3 * F::MX, "S fits in the T region");
@@ -254,15 +257,12 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     int ex0, ey0, ez0, nx0 = 0, ny0 = 0, nz0 = 0;
     coords(tile, ex0, ey0, ez0);
     if (next < n_tiles) coords(next, nx0, ny0, nz0);
-    // 0. p = Minv r (+ beta p_old) from the raw boxes into Ps; own elements -> p_new
+    // 0. p = Minv r (+ beta p_old) from the raw boxes into Ps (the element step stores the
+    // tile's own p_new)
     mbar_wait(&bar[0], ph);
     lap(1);
     for (int i = threadIdx.x; i < ((dbg & 0x400) ? 0 : K::NHD); i += F::NTH) {
       const int hx = i % K::HX, hy = (i / K::HX) % K::HY, hz = i / (K::HX * K::HY);
-      const int ex = ex0 + hx - 1, ey = ey0 + hy - 1, ez = ez0 + hz - 1;
-      const bool own = hx >= 1 && hy >= 1 && hz >= 1 && hx <= TX && hy <= TY && hz <= TZ && ex < N && ey < N &&
-                       ez < N;
-      const int64_t e = ex + (int64_t)N * (ey + (int64_t)N * ez);
       const int jb = (hx + 1) + K::BXW * (hy + K::HY * hz);  // box column of halo element hx
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
@@ -276,12 +276,11 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
           }
         }
         Ps[m * K::NHP + K::pidx(hx, hy, hz)] = v;
-        if (own && !(dbg & 0x1000)) pnew[m * ne + e] = v;
       }
     }
     __syncthreads();
     lap(2);
-    if (threadIdx.x == 0 && next < n_tiles) {  // raw p, r, Minv buffers are free
+    if (threadIdx.x == K::TMA_T && next < n_tiles) {  // raw p, r, Minv buffers are free
       fence_proxy_async();
       mbar_expect_tx(&bar[0], RAWB);
       tma_load_4d(Zb, &tm_z, nx0 - 2, ny0 - 1, nz0 - 1, 0, &bar[0]);
@@ -309,7 +308,7 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     }
     __syncthreads();
     lap(4);
-    if (threadIdx.x == 0 && next < n_tiles) {  // X buffer is free
+    if (threadIdx.x == K::TMA_T && next < n_tiles) {  // X buffer is free
       fence_proxy_async();
       mbar_expect_tx(&bar[2], K::XBYTES);
       tma_load_3d(Xs, &tm_x, 2 * nx0, 2 * ny0, 2 * nz0, &bar[2]);
@@ -344,8 +343,10 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
           const double o = sB * qm[m];
+          const double pv = Ps[m * K::NHP + h];
           if (!(dbg & 0x800)) q[m * ne + e] = o;
-          dot = fma(Ps[m * K::NHP + h], o, dot);
+          if (!(dbg & 0x1000)) pnew[m * ne + e] = pv;
+          dot = fma(pv, o, dot);
         }
       }
     }
