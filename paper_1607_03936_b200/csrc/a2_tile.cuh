@@ -25,6 +25,24 @@
 
 namespace wb {
 
+#ifdef WB_KPROF
+// phase-timing probe (build -DWB_KPROF): thread 0 of every A tile CTA adds its clock64
+// cycles per phase: [0] staging issue, [1] staging wait + barrier, [2] U load + interpolation,
+// [3] Gauss levels, [4] transposed interpolation, [5] slots + barrier, [6] node sums /
+// outputs, [7] CTAs
+__device__ unsigned long long g_aprof[8];
+#define A_LAP(k)                                                              \
+  do {                                                                        \
+    if (threadIdx.x == 0) {                                                   \
+      const long long n_ = clock64();                                         \
+      atomicAdd(&g_aprof[k], (unsigned long long)(n_ - a_tc));                \
+      a_tc = n_;                                                              \
+    }                                                                         \
+  } while (0)
+#else
+#define A_LAP(k) do { } while (0)
+#endif
+
 struct K2Coef {
   double i00, i01, i02;   // I row 0 (row 2 reversed, row 1 = e_1)
   double a, b, c, d;      // Dg row 0 = (a, b, c), Dg row 1 = (d, 0, -d), Dg row 2 = (-c, -b, -a)
@@ -109,6 +127,9 @@ __device__ __forceinline__ void a2_elem(const double* __restrict__ Mu, const dou
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax)  // Dirichlet entries were staged as 0
         U3(az, ay, ax) = Ub[L::RSU * (ay + L::MY * az) + (ax == 1 ? TX + 1 : (ax >> 1))];
+#ifdef WB_KPROF
+  long long a_tc = clock64();
+#endif
   // GLL -> Gauss in x, y, z
 #pragma unroll
   for (int z = 0; z < 3; ++z)
@@ -122,6 +143,7 @@ __device__ __forceinline__ void a2_elem(const double* __restrict__ Mu, const dou
   for (int y = 0; y < 3; ++y)
 #pragma unroll
     for (int x = 0; x < 3; ++x) k2_interp(k, U3(0, y, x), U3(1, y, x), U3(2, y, x));
+  A_LAP(2);
 #pragma unroll
   for (int q = 0; q < 27; ++q) V[q] = 0.0;
 #pragma unroll
@@ -168,6 +190,7 @@ __device__ __forceinline__ void a2_elem(const double* __restrict__ Mu, const dou
       else { V[q] = fma(-k.c, gz[q], V[q]); V[9 + q] = fma(-k.b, gz[q], V[9 + q]); V[18 + q] = fma(-k.a, gz[q], V[18 + q]); }
     }
   }
+  A_LAP(3);
   // Gauss -> GLL transposed, z, y, x
 #pragma unroll
   for (int y = 0; y < 3; ++y)
@@ -181,6 +204,7 @@ __device__ __forceinline__ void a2_elem(const double* __restrict__ Mu, const dou
   for (int z = 0; z < 3; ++z)
 #pragma unroll
     for (int y = 0; y < 3; ++y) k2_interpT(k, V3(z, y, 0), V3(z, y, 1), V3(z, y, 2));
+  A_LAP(4);
 }
 #undef U3
 #undef V3
@@ -209,30 +233,38 @@ template <int TX, int TY, int TZ>
 __device__ __forceinline__ double a2_node_sum(const double* __restrict__ Rb, const double (&V)[27], int lx, int ly,
                                               int lz, int AX, int AY, int AZ) {
   // Rb = R + c * 27 * NE + le: slot (c, a, element le + d) at Rb[a * NE + d].  The own
-  // element's term (always the last one) comes from its registers V.
+  // element's term comes from its registers V.  Terms t(kz, ky, kx), k_d = 0 the lower
+  // element (absent at the tile's lower face: +0.0) and 1 the own one along axes with
+  // A_d = 0, are summed as a fixed pairwise tree: x pairs, then y, then z.
   constexpr int NE = TX * TY * TZ;
-  double acc = 0.0;
+  double t[2][2][2];
 #pragma unroll
-  for (int kz = 0; kz < 2; ++kz) {
-    if (AZ != 0 && kz == 1) continue;
-    const int dz = AZ == 0 ? kz - 1 : 0, az = AZ == 0 ? (kz == 0 ? 2 : 0) : AZ;
-    if (lz + dz < 0) continue;
+  for (int kz = 0; kz < 2; ++kz)
 #pragma unroll
-    for (int ky = 0; ky < 2; ++ky) {
-      if (AY != 0 && ky == 1) continue;
-      const int dy = AY == 0 ? ky - 1 : 0, ay = AY == 0 ? (ky == 0 ? 2 : 0) : AY;
-      if (ly + dy < 0) continue;
+    for (int ky = 0; ky < 2; ++ky)
 #pragma unroll
       for (int kx = 0; kx < 2; ++kx) {
-        if (AX != 0 && kx == 1) continue;
+        t[kz][ky][kx] = 0.0;
+        if ((AZ != 0 && kz == 1) || (AY != 0 && ky == 1) || (AX != 0 && kx == 1)) continue;
+        const int dz = AZ == 0 ? kz - 1 : 0, az = AZ == 0 ? (kz == 0 ? 2 : 0) : AZ;
+        const int dy = AY == 0 ? ky - 1 : 0, ay = AY == 0 ? (ky == 0 ? 2 : 0) : AY;
         const int dx = AX == 0 ? kx - 1 : 0, ax = AX == 0 ? (kx == 0 ? 2 : 0) : AX;
-        if (lx + dx < 0) continue;
         const int a = ax + 3 * (ay + 3 * az);
-        acc += (dx == 0 && dy == 0 && dz == 0) ? V[a] : Rb[a * NE + dx + TX * (dy + TY * dz)];
+        if (dx == 0 && dy == 0 && dz == 0) {
+          t[kz][ky][kx] = V[a];
+        } else if (lx + dx >= 0 && ly + dy >= 0 && lz + dz >= 0) {
+          t[kz][ky][kx] = Rb[a * NE + dx + TX * (dy + TY * dz)];
+        }
       }
-    }
-  }
-  return acc;
+  double sy[2][2];
+#pragma unroll
+  for (int kz = 0; kz < 2; ++kz)
+#pragma unroll
+    for (int ky = 0; ky < 2; ++ky) sy[kz][ky] = AX == 0 ? t[kz][ky][0] + t[kz][ky][1] : t[kz][ky][0];
+  double sz[2];
+#pragma unroll
+  for (int kz = 0; kz < 2; ++kz) sz[kz] = AY == 0 ? sy[kz][0] + sy[kz][1] : sy[kz][0];
+  return AZ == 0 ? sz[0] + sz[1] : sz[0];
 }
 
 // slots read by other threads: local index 2 in some axis (the node belongs to the
@@ -344,21 +376,30 @@ __global__ void __launch_bounds__(3 * TX * TY * TZ, MINB)
   double* Mu = smem_a2 + T::XS;
   double* Us = Mu + 27 * NE;
   const int tile = blockIdx.x;
+#ifdef WB_KPROF
+  long long a_tc = clock64();
+#endif
   const A2Tile t = a2_tile_of<TX, TY, TZ>(tile, G);
   a2_stage<TX, TY, TZ>(mutT, u, Mu, Us, t, G, nomask);
+  A_LAP(0);
   const int le = threadIdx.x % NE, c = threadIdx.x / NE;
   const int lx = le % TX, ly = (le / TX) % TY, lz = le / (TX * TY);
   const int nn1 = G.nn1, kN = 2 * G.N;
   cp_async_wait_all();  // this thread's copies
   __syncthreads();      // everyone's
+  A_LAP(1);
   double V[27];
   a2_elem<TX, TY, TZ>(Mu, Us, lx, ly, lz, c, le, X, V);
+#ifdef WB_KPROF
+  a_tc = clock64();  // a2_elem timed its own phases
+#endif
   // element slots R[c][a][le] (the exchange buffer is free after the last level's barrier)
   double* Rb = X + c * 27 * NE + le;
 #pragma unroll
   for (int a = 0; a < 27; ++a)
     if (a2_slot_shared(a)) Rb[a * NE] = V[a];
   __syncthreads();
+  A_LAP(5);
   // Each thread is responsible for the tile nodes 2l + A, A_d in {0, 1}, plus A_d = 2
   // on the tile's upper face (l_d = T_d - 1): every tile node has exactly one
   // responsible (element, c) thread, and the node's structure is compile-time.
@@ -374,7 +415,12 @@ __global__ void __launch_bounds__(3 * TX * TY * TZ, MINB)
         const int nx = 2 * lx + AX, ny = 2 * ly + AY, nz = 2 * lz + AZ;
         const double s = a2_node_sum<TX, TY, TZ>(Rb, V, lx, ly, lz, AX, AY, AZ);
         if (AX == 2 || AY == 2 || AZ == 2) {
-          Fut[T::shell(nx, ny, nz)] = s;
+          // (responsibility implies n_d == 2T_d exactly where A_d == 2: T::shell's branches
+          // resolve at compile time)
+          const int si = AZ == 2 ? ny * T::MX + nx
+                                 : (AY == 2 ? T::MX * T::MY + nz * T::MX + nx
+                                            : T::MX * T::MY + 2 * TZ * T::MX + nz * (2 * TY) + ny);
+          Fut[si] = s;
         } else {
           double* dst = yb + (nz * nn1 + ny) * nn1 + nx;
           if (t.inner) {
@@ -385,6 +431,10 @@ __global__ void __launch_bounds__(3 * TX * TY * TZ, MINB)
           }
         }
       }
+  A_LAP(6);
+#ifdef WB_KPROF
+  if (threadIdx.x == 0) atomicAdd(&g_aprof[7], 1ull);
+#endif
 }
 
 // Kernel 2 of A: the tile-skeleton nodes (g_d a multiple of 2T_d in some axis),

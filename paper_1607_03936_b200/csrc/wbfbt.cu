@@ -1009,6 +1009,18 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
     CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_K2_fused<4, 8, 8, 2>, FK2<4, 8, 8>::NTH,
                                                               FK2<4, 8, 8>::SMEM));
     *value = nb;
+#ifdef WB_KPROF
+  } else if (!strncmp(key, "aprof", 5) && key[5] >= '0' && key[5] <= '7' && !key[6]) {
+    // phase-timing probe of the A tile kernel; reading "aprof7" clears the counters
+    unsigned long long h[8];
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    CUDA_TRY(c, cudaMemcpyFromSymbol(h, g_aprof, sizeof(h)));
+    *value = (double)h[key[5] - '0'];
+    if (key[5] == '7') {
+      memset(h, 0, sizeof(h));
+      CUDA_TRY(c, cudaMemcpyToSymbol(g_aprof, h, sizeof(h)));
+    }
+#endif
   } else if (!strncmp(key, "kprof", 5) && key[5] >= '0' && key[5] <= '7' && !key[6]) {
     // phase-timing probe of the TMA Poisson kernel (k_dbg 0x4000): accumulated cycles;
     // reading "kprof7" (the last) clears the counters
