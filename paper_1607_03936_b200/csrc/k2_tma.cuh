@@ -43,6 +43,13 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, in
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
 }
+// 1-D bulk copy global -> shared (16-byte aligned, size a multiple of 16), mbarrier completion
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
@@ -61,9 +68,7 @@ struct FKT {
   using F = FK2<TX, TY, TZ>;
   static constexpr int HX = TX + 2, HY = TY + 2, HZ = TZ + 2;
   static constexpr int BXW = TX + 4, NB = BXW * HY * HZ;  // raw box (BXW, HY, HZ, 4)
-  static constexpr int XB = (F::MX + 1) & ~1;             // X box row (16-byte multiple), start 2 ex0 (even)
-  static constexpr int NX = XB * F::MY * F::MZ;
-  static constexpr unsigned PBYTES = 4u * NB * 8u, XBYTES = (unsigned)NX * 8u;
+  static constexpr unsigned PBYTES = 4u * NB * 8u;
   // Ps[m][qx][qz][qy]: a pencil's (qy, qz) row is the fastest index, so the lanes of a
   // pencil class (consecutive qy) read consecutive words
   // qz stride QS = 9 (mod 16) and >= HY: a class-(0,0) half-warp (9 qy per qz row)
@@ -79,6 +84,11 @@ struct FKT {
   static constexpr int NROW = R00 + R10 + R01 + R11;
   static constexpr int TC = NROW + ((20 - NROW % 16) % 16);
   static constexpr int TN = F::MX * TC;
+  // X in pencil layout: per tile one contiguous block XT[nx][row] (row as above, no
+  // padding), built at setup (k_x_tiles); a lane-consecutive pencil class reads
+  // consecutive words.  Block length rounded to 16 bytes for the bulk copy.
+  static constexpr int XTB = (F::MX * NROW + 1) & ~1;
+  static constexpr unsigned XBYTES = (unsigned)XTB * 8u;
   // the thread that issues the per-tile TMA loads: lane 0 of the last warp (light
   // class-(1,1) pencils, no element in step 2), off the heavy warps' critical path
   static constexpr int TMA_T = F::NTH - 32;
@@ -97,7 +107,7 @@ struct FKT {
   static constexpr size_t SMEM = OFF_B + 64 + 1024;  // + slack for 1024-byte base alignment
 };
 
-// x-pencil as in fk2_pencil, with the TMA box layouts: Ps rows of HX, Xs rows of XB (natural x order)
+// x-pencil as in fk2_pencil, with the staged layouts: Ps (padded qy-fastest rows), Xs (XT block)
 template <int TX, int TY, int TZ, int RY, int RZ>
 __device__ __forceinline__ void fkt_pencil(const double* __restrict__ Ps, double* __restrict__ T,
                                            const double* __restrict__ Xs, int jy, int jz, double sB) {
@@ -150,10 +160,10 @@ __device__ __forceinline__ void fkt_pencil(const double* __restrict__ Ps, double
   }
   // t = sB X^-1 (B^T p) at the row's nodes, then the x-contraction of B for the
   // row's elements: S_c[m1][lx] = sum_ax Mx_c[m1][ax] t_c(2 lx + ax)
-  const double* Xr = Xs + K::XB * (ny + F::MY * nz);
+  const double* Xr = Xs + K::row(ny, nz);
 #pragma unroll
   for (int nx = 0; nx < F::MX; ++nx) {
-    const double f = sB * Xr[nx];  // zero-filled outside the mesh; X = 0 on the boundary
+    const double f = sB * Xr[nx * K::NROW];  // 0 outside the mesh; X = 0 on the boundary
 #pragma unroll
     for (int c = 0; c < 3; ++c) acc[c][nx] *= f;
   }
@@ -173,13 +183,13 @@ __device__ __forceinline__ void fkt_pencil(const double* __restrict__ Ps, double
 }
 
 // Same contract as k_K2_fused (mode, ctl, partials), tensor maps instead of pointers for the
-// loads: tm_pold / tm_r / tm_minv over [m][ez][ey][ex], tm_x over the padded nodal X.
+// loads: tm_pold / tm_r / tm_minv over [m][ez][ey][ex]; X from its tile-blocked pencil layout XT.
 // ZB: the PCG update kernels store z = Minv r and the kernel loads a z box; else it
 // loads r and Minv boxes and forms Minv r itself (same product either way).
 template <int TX, int TY, int TZ, int MINB, bool ZB>
 __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     k_K2_tma(const __grid_constant__ CUtensorMap tm_pold, const __grid_constant__ CUtensorMap tm_z,
-             const __grid_constant__ CUtensorMap tm_minv, const __grid_constant__ CUtensorMap tm_x,
+             const __grid_constant__ CUtensorMap tm_minv, const double* __restrict__ XT,
              double* __restrict__ pnew, double* __restrict__ q, Geo G, double sB, int mode, int it, int ctl,
              const double* __restrict__ rzp, int nrz, double* rz_hist, const double* pq_hist, int* stop,
              double* pqp) {
@@ -218,7 +228,7 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
       if (!ZB) tma_load_4d(Mb, &tm_minv, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
       tma_load_4d(Pb, &tm_pold, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
       mbar_expect_tx(&bar[2], K::XBYTES);
-      tma_load_3d(Xs, &tm_x, 2 * ex0, 2 * ey0, 2 * ez0, &bar[2]);
+      bulk_load(Xs, XT + (size_t)tile * K::XTB, K::XBYTES, &bar[2]);
     }
   }
   // timing probe bits (option k_dbg; results invalid): 0x100 skip step 1, 0x200 skip
@@ -261,19 +271,21 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     // tile's own p_new)
     mbar_wait(&bar[0], ph);
     lap(1);
-    for (int i = threadIdx.x; i < ((dbg & 0x400) ? 0 : K::NHD); i += F::NTH) {
-      const int hx = i % K::HX, hy = (i / K::HX) % K::HY, hz = i / (K::HX * K::HY);
-      const int jb = (hx + 1) + K::BXW * (hy + K::HY * hz);  // box column of halo element hx
+    // walk the raw box in its own order (lane-consecutive reads); box column b holds halo
+    // element b - 1, columns 0 and BXW - 1 are padding.  With BXW = 8 a half-warp covers
+    // two box rows, and its Ps stores (stride QS * HZ per column) hit 16 distinct bank pairs.
+    for (int i = threadIdx.x; i < ((dbg & 0x400) ? 0 : K::NB); i += F::NTH) {
+      const int b = i % K::BXW, r = i / K::BXW, hy = r % K::HY, hz = r / K::HY;
+      if (b < 1 || b > K::HX) continue;
+      const int hx = b - 1;
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
-        const int j = m * K::NB + jb;
-        double v = 0.0;
-        if (hx < K::HX) {  // pad column of Ps stays 0
-          if (mode == 2) v = Pb[j];
-          else {
-            const double z = ZB ? Zb[j] : Mb[j] * Zb[j];
-            v = (mode == 1) ? fma(beta, Pb[j], z) : z;
-          }
+        const int j = m * K::NB + i;
+        double v;
+        if (mode == 2) v = Pb[j];
+        else {
+          const double z = ZB ? Zb[j] : Mb[j] * Zb[j];
+          v = (mode == 1) ? fma(beta, Pb[j], z) : z;
         }
         Ps[m * K::NHP + K::pidx(hx, hy, hz)] = v;
       }
@@ -311,7 +323,7 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     if (threadIdx.x == K::TMA_T && next < n_tiles) {  // X buffer is free
       fence_proxy_async();
       mbar_expect_tx(&bar[2], K::XBYTES);
-      tma_load_3d(Xs, &tm_x, 2 * nx0, 2 * ny0, 2 * nz0, &bar[2]);
+      bulk_load(Xs, XT + (size_t)next * K::XTB, K::XBYTES, &bar[2]);
     }
     // 2. q = sB Bt^T t per element, <p, q>
     if (threadIdx.x < F::NE && !(dbg & 0x200)) {
@@ -357,6 +369,27 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
   if (prof)
     for (int k = 0; k < 8; ++k) atomicAdd(&g_kprof[k], pt[k]);
   store_partial<F::NTH>(dot, pqp);
+}
+
+// XT[tile][nx][row(ny, nz)] = X(2 ex0 + nx, 2 ey0 + ny, 2 ez0 + nz), 0 outside the mesh
+// (the pencil layout of the TMA kernel's X block); one thread per (tile, row, nx).
+template <int TX, int TY, int TZ>
+__global__ void k_x_tiles(const double* __restrict__ X, double* __restrict__ XT, int N) {
+  using F = FK2<TX, TY, TZ>;
+  using K = FKT<TX, TY, TZ>;
+  const int nn1 = 2 * N + 1;
+  const int NTX = (N + TX - 1) / TX, NTY = (N + TY - 1) / TY, NTZ = (N + TZ - 1) / TZ;
+  const int64_t n = (int64_t)NTX * NTY * NTZ * F::MY * F::MZ * F::MX;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int nx = (int)(i % F::MX);
+    const int64_t r = i / F::MX;
+    const int ny = (int)(r % F::MY), nz = (int)((r / F::MY) % F::MZ);
+    const int tile = (int)(r / ((int64_t)F::MY * F::MZ));
+    const int tx = tile % NTX, ty = (tile / NTX) % NTY, tz = tile / (NTX * NTY);
+    const int gx = 2 * TX * tx + nx, gy = 2 * TY * ty + ny, gz = 2 * TZ * tz + nz;
+    const double v = (gx < nn1 && gy < nn1 && gz < nn1) ? X[gx + (int64_t)nn1 * (gy + (int64_t)nn1 * gz)] : 0.0;
+    XT[(int64_t)tile * K::XTB + nx * K::NROW + K::row(ny, nz)] = v;
+  }
 }
 
 }  // namespace wb

@@ -108,15 +108,3 @@ __global__ void __launch_bounds__(256) k_BT_node2(const double* __restrict__ p, 
 #include "k2_fused.cuh"
 #include "k2_tma.cuh"
 #include "k2_bbt.cuh"
-
-namespace wb {
-// nodal X -> copy with rows padded to an even length (16-byte-aligned rows for TMA)
-__global__ void k_pad_rows(const double* __restrict__ X, double* __restrict__ Xp, int nn1, int xp) {
-  const int64_t n = (int64_t)nn1 * nn1 * xp;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / xp;
-    const int gx = (int)(i % xp);
-    Xp[i] = gx < nn1 ? X[row * nn1 + gx] : 0.0;
-  }
-}
-}  // namespace wb

@@ -67,13 +67,12 @@ struct wb_ctx {
   // mode-major PCG vectors and over row-padded copies of C_w^-1 / D_w^-1
   bool tma_ok = false;
   int use_tma = 1;
-  double *XpL = nullptr, *XpR = nullptr;
+  double *XpL = nullptr, *XpR = nullptr;  // C_w^-1, D_w^-1 in the TMA kernel's X-block layout (k_x_tiles)
   // k = 2, even N: MinvL | XpL | x r p p' q z | MinvR | XpR carved from one slab (each
   // side's PCG working set contiguous; a persisting L2 access-policy window over it was
   // measured and gave no gain)
   double* slab = nullptr;
-  int xp = 0;
-  CUtensorMap tm_pp, tm_pp1, tm_pz, tm_pr, tm_mL, tm_mR, tm_xL, tm_xR;
+  CUtensorMap tm_pp, tm_pp1, tm_pz, tm_pr, tm_mL, tm_mR;
   int kz = 1;  // TMA Poisson kernel: 1 = z = Minv r stored by the PCG update and loaded as one box (default)
   int k_dbg = 0;  // timing probe bits for the fused K kernel (results invalid when nonzero)
   // profiling: CUDA-event pairs around every Poisson-operator launch (direct launches)
@@ -231,6 +230,11 @@ wb_status launch_k2f_t(wb_ctx* c, const double* pold, double* pnew, const double
 #define TMA_TZ 8
 #define TMA_MINB 1
 #endif
+// length (doubles) of one side's X in the TMA kernel's tile-blocked pencil layout
+int64_t xt_len(int N) {
+  const int64_t nt = (int64_t)((N + TMA_TX - 1) / TMA_TX) * ((N + TMA_TY - 1) / TMA_TY) * ((N + TMA_TZ - 1) / TMA_TZ);
+  return nt * FKT<TMA_TX, TMA_TY, TMA_TZ>::XTB;
+}
 const CUtensorMap* tmap_of(wb_ctx* c, const double* p) {
   if (p == c->pp) return &c->tm_pp;
   if (p == c->pp1) return &c->tm_pp1;
@@ -238,8 +242,6 @@ const CUtensorMap* tmap_of(wb_ctx* c, const double* p) {
   if (p == c->pr) return &c->tm_pr;
   if (p == c->MinvL) return &c->tm_mL;
   if (p == c->MinvR) return &c->tm_mR;
-  if (p == c->Cinv) return &c->tm_xL;
-  if (p == c->Dinv) return &c->tm_xR;
   return nullptr;
 }
 
@@ -252,15 +254,15 @@ wb_status run_k2f(wb_ctx* c, const double* pold, double* pnew, const double* r, 
                   double* q, int mode, PcgArgs a, int* npq) {
   if (tma_active(c)) {
     using KT = FKT<TMA_TX, TMA_TY, TMA_TZ>;
-    const CUtensorMap *tp = tmap_of(c, pold), *tz = tmap_of(c, c->kz ? c->pz : c->pr), *tm = tmap_of(c, Minv),
-                      *tx = tmap_of(c, X);
-    if (tp && tz && tm && tx && (mode == 2 || r == c->pr)) {
+    const CUtensorMap *tp = tmap_of(c, pold), *tz = tmap_of(c, c->kz ? c->pz : c->pr), *tm = tmap_of(c, Minv);
+    const double* xt = X == c->Cinv ? c->XpL : (X == c->Dinv ? c->XpR : nullptr);  // X in pencil layout
+    if (tp && tz && tm && xt && (mode == 2 || r == c->pr)) {
       const int N = c->N;
       const int nt = ((N + TMA_TX - 1) / TMA_TX) * ((N + TMA_TY - 1) / TMA_TY) * ((N + TMA_TZ - 1) / TMA_TZ);
       const int grid = std::max(1, std::min(nt, TMA_MINB * c->nsm));  // persistent, all resident
       auto kern = c->kz ? k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, true> : k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, false>;
       kern<<<grid, FK2<TMA_TX, TMA_TY, TMA_TZ>::NTH, KT::SMEM, c->stream>>>(
-          *tp, *tz, *tm, *tx, pnew, q, c->G, c->sB, mode | c->k_dbg, a.it, a.ctl, c->rzp, c->red_blocks, rz_hist(c),
+          *tp, *tz, *tm, xt, pnew, q, c->G, c->sB, mode | c->k_dbg, a.it, a.ctl, c->rzp, c->red_blocks, rz_hist(c),
           pq_hist(c), c->stop, c->pqp);
       LAUNCH_CHECK(c);
       *npq = grid;
@@ -298,22 +300,9 @@ bool make_tm_vec(CUtensorMap* tm, const double* base, int N, int nm) {
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-// nodal X with rows padded to xp: 3-D map, box = the tile's (2T+1)^3 nodes (row rounded up to even)
-bool make_tm_x(CUtensorMap* tm, const double* base, int nn1, int xp) {
-  using KT = FKT<TMA_TX, TMA_TY, TMA_TZ>;
-  using F = FK2<TMA_TX, TMA_TY, TMA_TZ>;
-  const cuuint64_t dims[3] = {(cuuint64_t)nn1, (cuuint64_t)nn1, (cuuint64_t)nn1};
-  const cuuint64_t strides[2] = {(cuuint64_t)xp * 8, (cuuint64_t)xp * nn1 * 8};
-  const cuuint32_t box[3] = {(cuuint32_t)KT::XB, (cuuint32_t)F::MY, (cuuint32_t)F::MZ};
-  const cuuint32_t es[3] = {1, 1, 1};
-  return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 bool setup_tma(wb_ctx* c) {
   if (c->k != 2 || (c->N & 1) || !get_encode()) return false;
-  c->xp = (c->G.nn1 + 1) & ~1;
-  const size_t bx = sizeof(double) * (size_t)c->G.nn1 * c->G.nn1 * c->xp;
+  const size_t bx = sizeof(double) * (size_t)xt_len(c->N);
   if (!c->slab && (cudaMalloc(&c->XpL, bx) != cudaSuccess || cudaMalloc(&c->XpR, bx) != cudaSuccess)) {
     cudaGetLastError();
     return false;
@@ -327,9 +316,7 @@ bool setup_tma(wb_ctx* c) {
   }
   return make_tm_vec(&c->tm_pp, c->pp, c->N, c->nm) && make_tm_vec(&c->tm_pp1, c->pp1, c->N, c->nm) &&
          make_tm_vec(&c->tm_pz, c->pz, c->N, c->nm) && make_tm_vec(&c->tm_pr, c->pr, c->N, c->nm) &&
-         make_tm_vec(&c->tm_mL, c->MinvL, c->N, c->nm) && make_tm_vec(&c->tm_mR, c->MinvR, c->N, c->nm) &&
-         make_tm_x(&c->tm_xL, c->XpL, c->G.nn1, c->xp) &&
-         make_tm_x(&c->tm_xR, c->XpR, c->G.nn1, c->xp);
+         make_tm_vec(&c->tm_mL, c->MinvL, c->N, c->nm) && make_tm_vec(&c->tm_mR, c->MinvR, c->N, c->nm);
 }
 
 wb_status configure_kernels(wb_ctx* c) {
@@ -652,9 +639,8 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
   };
   alloc(&c->Cw, c->n_nodes); alloc(&c->Dw, c->n_nodes); alloc(&c->Cinv, c->n_nodes); alloc(&c->Dinv, c->n_nodes);
   if (k == 2 && !(N & 1)) {
-    const int64_t nn1 = 2 * (int64_t)N + 1, xp = (nn1 + 1) & ~1;
     auto up = [](int64_t n) { return (n + 31) & ~(int64_t)31; };  // 256-byte sub-arrays
-    const int64_t np = up(c->n_p), nx = up(nn1 * nn1 * xp);
+    const int64_t np = up(c->n_p), nx = up(xt_len(N));
     if (ok && cudaMalloc(&c->slab, sizeof(double) * (size_t)(8 * np + 2 * nx)) != cudaSuccess) ok = false;
     if (ok) {
       double* q = c->slab;
@@ -777,10 +763,10 @@ static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
   k_lump_node<K><<<nblk(c->n_nodes, 256), 256, 0, c->stream>>>(c->E, a_l, a_r, c->Cw, c->Dw, c->Cinv, c->Dinv,
                                                                c->icount + 1, c->G);
   LAUNCH_CHECK(c);
-  if (c->tma_ok) {  // row-padded copies for the TMA tensor maps of the fused K kernel
-    k_pad_rows<<<c->red_blocks, VBS, 0, c->stream>>>(c->Cinv, c->XpL, c->G.nn1, c->xp);
+  if (c->tma_ok) {  // X = C_w^-1, D_w^-1 in the tile-blocked pencil layout of the TMA kernel
+    k_x_tiles<TMA_TX, TMA_TY, TMA_TZ><<<c->red_blocks, VBS, 0, c->stream>>>(c->Cinv, c->XpL, c->N);
     LAUNCH_CHECK(c);
-    k_pad_rows<<<c->red_blocks, VBS, 0, c->stream>>>(c->Dinv, c->XpR, c->G.nn1, c->xp);
+    k_x_tiles<TMA_TX, TMA_TY, TMA_TZ><<<c->red_blocks, VBS, 0, c->stream>>>(c->Dinv, c->XpR, c->N);
     LAUNCH_CHECK(c);
   }
   k_jacobi<K><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(c->Cinv, c->Dinv, c->dKl, c->dKr, c->MinvL, c->MinvR,
