@@ -372,23 +372,28 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
 }
 
 // XT[tile][nx][row(ny, nz)] = X(2 ex0 + nx, 2 ey0 + ny, 2 ez0 + nz), 0 outside the mesh
-// (the pencil layout of the TMA kernel's X block); one thread per (tile, row, nx).
+// (the pencil layout of the TMA kernel's X block), both sides (L: C_w^-1, R: D_w^-1).
+// One CTA per tile, one thread per node row (ny, nz): 2 x MX contiguous reads.
 template <int TX, int TY, int TZ>
-__global__ void k_x_tiles(const double* __restrict__ X, double* __restrict__ XT, int N) {
+__global__ void __launch_bounds__(FK2<TX, TY, TZ>::MY * FK2<TX, TY, TZ>::MZ)
+    k_x_tiles(const double* __restrict__ XL, const double* __restrict__ XR, double* __restrict__ XTL,
+              double* __restrict__ XTR, int N) {
   using F = FK2<TX, TY, TZ>;
   using K = FKT<TX, TY, TZ>;
   const int nn1 = 2 * N + 1;
-  const int NTX = (N + TX - 1) / TX, NTY = (N + TY - 1) / TY, NTZ = (N + TZ - 1) / TZ;
-  const int64_t n = (int64_t)NTX * NTY * NTZ * F::MY * F::MZ * F::MX;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int nx = (int)(i % F::MX);
-    const int64_t r = i / F::MX;
-    const int ny = (int)(r % F::MY), nz = (int)((r / F::MY) % F::MZ);
-    const int tile = (int)(r / ((int64_t)F::MY * F::MZ));
-    const int tx = tile % NTX, ty = (tile / NTX) % NTY, tz = tile / (NTX * NTY);
-    const int gx = 2 * TX * tx + nx, gy = 2 * TY * ty + ny, gz = 2 * TZ * tz + nz;
-    const double v = (gx < nn1 && gy < nn1 && gz < nn1) ? X[gx + (int64_t)nn1 * (gy + (int64_t)nn1 * gz)] : 0.0;
-    XT[(int64_t)tile * K::XTB + nx * K::NROW + K::row(ny, nz)] = v;
+  const int NTX = (N + TX - 1) / TX, NTY = (N + TY - 1) / TY;
+  const int tile = blockIdx.x;
+  const int tx = tile % NTX, ty = (tile / NTX) % NTY, tz = tile / (NTX * NTY);
+  const int ny = threadIdx.x % F::MY, nz = threadIdx.x / F::MY;
+  const int gx0 = 2 * TX * tx, gy = 2 * TY * ty + ny, gz = 2 * TZ * tz + nz;
+  const bool rowok = gy < nn1 && gz < nn1;
+  const int64_t src = gx0 + (int64_t)nn1 * (gy + (int64_t)nn1 * gz);
+  const int64_t dst = (int64_t)tile * K::XTB + K::row(ny, nz);
+#pragma unroll
+  for (int nx = 0; nx < F::MX; ++nx) {
+    const bool ok = rowok && gx0 + nx < nn1;
+    XTL[dst + nx * K::NROW] = ok ? XL[src + nx] : 0.0;
+    XTR[dst + nx * K::NROW] = ok ? XR[src + nx] : 0.0;
   }
 }
 

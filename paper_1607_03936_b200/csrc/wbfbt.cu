@@ -32,6 +32,7 @@ struct wb_ctx {
   double *dKl = nullptr, *dKr = nullptr, *MinvL = nullptr, *MinvR = nullptr;
   bool have_visc = false;
   long long n_nonpos[2] = {0, 0};
+  bool nonpos_pending = false;  // icount[1..2] not yet copied to n_nonpos
   // work vectors
   double* E = nullptr;                 // element-local velocity values, 3*nq*n_el
   double *tv = nullptr, *tw = nullptr;  // n_v
@@ -621,7 +622,15 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
       delete c;
       return WB_ECUDA;
     }
-    if (cudaMemcpyToSymbol(c_Bt2, bt2, sizeof(bt2)) != cudaSuccess) {
+    double j2[27][4];  // Jacobi weights: sum_c bt2[c][a][m]^2
+    for (int a = 0; a < 27; ++a)
+      for (int m = 0; m < 4; ++m) {
+        long double v = 0.0L;
+        for (int cc = 0; cc < 3; ++cc) v += (long double)bt2[cc][a][m] * (long double)bt2[cc][a][m];
+        j2[a][m] = (double)v;
+      }
+    if (cudaMemcpyToSymbol(c_Bt2, bt2, sizeof(bt2)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_J2, j2, sizeof(j2)) != cudaSuccess) {
       delete c;
       return WB_ECUDA;
     }
@@ -741,12 +750,25 @@ wb_status wb_get_boundary_mask(wb_ctx* c, uint8_t* mask) {
 
 }  // extern "C"
 
+// copy the nonpositive-lumped-entry counts of the last setup (synchronises the stream)
+static wb_status read_nonpos(wb_ctx* c) {
+  if (!c->nonpos_pending) return WB_OK;
+  unsigned long long np[2] = {0, 0};
+  CUDA_TRY(c, cudaMemcpyAsync(np, c->icount + 1, sizeof(np), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->n_nonpos[0] = (long long)np[0];
+  c->n_nonpos[1] = (long long)np[1];
+  c->nonpos_pending = false;
+  return WB_OK;
+}
+
 template <int K>
 static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
   const int64_t nmu = c->n_el * c->nq;
   CUDA_TRY(c, cudaMemsetAsync(c->icount, 0, sizeof(unsigned long long) * 4, c->stream));
-  if constexpr (K == 2)
-    k_prescale_t2<A_TX, A_TY, A_TZ><<<nblk(nmu, 256), 256, 0, c->stream>>>(mu, c->mut, c->N, c->h / 2, c->icount);
+  if constexpr (K == 2)  // mut and the element lumping values in one pass over mu
+    k_setup_mu2<A_TX, A_TY, A_TZ><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(mu, c->mut, c->E, c->N, c->h / 2,
+                                                                            c->detJ, c->icount);
   else
     k_prescale<K><<<nblk(nmu, 256), 256, 0, c->stream>>>(mu, c->mut, nmu, c->h / 2, c->icount);
   LAUNCH_CHECK(c);
@@ -757,20 +779,29 @@ static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
     c->have_visc = false;
     return set_err(c, WB_ENONPOS_MU, "%llu viscosity samples are <= 0 or non-finite", bad);
   }
-  // lumped masses: element part into E (1 component), node gather
-  k_lump_elem<K><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(mu, c->E, c->G, c->detJ);
-  LAUNCH_CHECK(c);
-  k_lump_node<K><<<nblk(c->n_nodes, 256), 256, 0, c->stream>>>(c->E, a_l, a_r, c->Cw, c->Dw, c->Cinv, c->Dinv,
-                                                               c->icount + 1, c->G);
+  // lumped masses: element part into E (1 component; k = 2: by k_setup_mu2), node gather
+  if constexpr (K == 2) {
+    dim3 grid(nblk(c->N + 1, 64), nblk(c->G.nn1, 4), 2 * c->G.nn1);
+    k_lump_node2<<<grid, dim3(64, 4), 0, c->stream>>>(c->E, a_l, a_r, c->Cw, c->Dw, c->Cinv, c->Dinv,
+                                                     c->icount + 1, c->G);
+  } else {
+    k_lump_elem<K><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(mu, c->E, c->G, c->detJ);
+    LAUNCH_CHECK(c);
+    k_lump_node<K><<<nblk(c->n_nodes, 256), 256, 0, c->stream>>>(c->E, a_l, a_r, c->Cw, c->Dw, c->Cinv, c->Dinv,
+                                                                 c->icount + 1, c->G);
+  }
   LAUNCH_CHECK(c);
   if (c->tma_ok) {  // X = C_w^-1, D_w^-1 in the tile-blocked pencil layout of the TMA kernel
-    k_x_tiles<TMA_TX, TMA_TY, TMA_TZ><<<c->red_blocks, VBS, 0, c->stream>>>(c->Cinv, c->XpL, c->N);
-    LAUNCH_CHECK(c);
-    k_x_tiles<TMA_TX, TMA_TY, TMA_TZ><<<c->red_blocks, VBS, 0, c->stream>>>(c->Dinv, c->XpR, c->N);
+    using F = FK2<TMA_TX, TMA_TY, TMA_TZ>;
+    const int nt = ((c->N + TMA_TX - 1) / TMA_TX) * ((c->N + TMA_TY - 1) / TMA_TY) * ((c->N + TMA_TZ - 1) / TMA_TZ);
+    k_x_tiles<TMA_TX, TMA_TY, TMA_TZ><<<nt, F::MY * F::MZ, 0, c->stream>>>(c->Cinv, c->Dinv, c->XpL, c->XpR, c->N);
     LAUNCH_CHECK(c);
   }
-  k_jacobi<K><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(c->Cinv, c->Dinv, c->dKl, c->dKr, c->MinvL, c->MinvR,
-                                                         c->G, c->sB);
+  if constexpr (K == 2)
+    k_jacobi2<<<nblk(c->n_el, 128), 128, 0, c->stream>>>(c->Cinv, c->Dinv, c->dKl, c->dKr, c->G, c->sB * c->sB);
+  else
+    k_jacobi<K><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(c->Cinv, c->Dinv, c->dKl, c->dKr, c->MinvL, c->MinvR,
+                                                           c->G, c->sB);
   LAUNCH_CHECK(c);
   for (int side = 0; side < 2; ++side) {
     const double* d = side == 0 ? c->dKl : c->dKr;
@@ -780,14 +811,15 @@ static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
     k_minv<<<c->red_blocks, VBS, 0, c->stream>>>(d, side == 0 ? c->MinvL : c->MinvR, c->n_el, c->nm, dmax);
     LAUNCH_CHECK(c);
   }
-  unsigned long long np[2] = {0, 0};
-  CUDA_TRY(c, cudaMemcpyAsync(np, c->icount + 1, sizeof(np), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  c->n_nonpos[0] = (long long)np[0];
-  c->n_nonpos[1] = (long long)np[1];
   c->have_visc = true;
-  if ((c->flags & WB_STRICT_LUMP) && (np[0] || np[1]))
-    return set_err(c, WB_ENONPOS_LUMP, "nonpositive lumped entries: C_w %llu, D_w %llu", np[0], np[1]);
+  c->nonpos_pending = true;  // counts read lazily (wb_query), or now in strict mode
+  if (c->flags & WB_STRICT_LUMP) {
+    wb_status s = read_nonpos(c);
+    if (s) return s;
+    if (c->n_nonpos[0] || c->n_nonpos[1])
+      return set_err(c, WB_ENONPOS_LUMP, "nonpositive lumped entries: C_w %lld, D_w %lld", c->n_nonpos[0],
+                     c->n_nonpos[1]);
+  }
   return WB_OK;
 }
 
@@ -983,8 +1015,11 @@ wb_status wb_get_jacobi(wb_ctx* c, double* dKl, double* dKr) {
 
 wb_status wb_query(wb_ctx* c, const char* key, double* value) {
   if (!c || !key || !value) return WB_EINVAL;
-  if (!strcmp(key, "n_nonpos_Cw")) *value = (double)c->n_nonpos[0];
-  else if (!strcmp(key, "n_nonpos_Dw")) *value = (double)c->n_nonpos[1];
+  if (!strcmp(key, "n_nonpos_Cw") || !strcmp(key, "n_nonpos_Dw")) {
+    wb_status s = read_nonpos(c);
+    if (s) return s;
+    *value = (double)c->n_nonpos[key[10] == 'C' ? 0 : 1];
+  }
   else if (!strcmp(key, "n_el")) *value = (double)c->n_el;
   else if (!strcmp(key, "n_p")) *value = (double)c->n_p;
   else if (!strcmp(key, "n_v")) *value = (double)c->n_v;
