@@ -62,6 +62,7 @@ typedef int wb_status;
 /* flags for wb_create */
 #define WB_STRICT_LUMP 1u  /* nonpositive interior C_w/D_w entry -> WB_ENONPOS_LUMP */
 #define WB_DEBUG_NOMASK 2u /* tests only: A, B, B^T skip the Dirichlet mask        */
+#define WB_DEBUG_SCALARS 4u /* wb_query may read the last PCG solve's alpha / beta */
 
 /* Library version string. */
 const char* wb_version(void);
@@ -144,7 +145,12 @@ wb_status wb_get_lumped(wb_ctx* ctx, double* Cw, double* Dw, double* Cinv, doubl
 wb_status wb_get_jacobi(wb_ctx* ctx, double* diagKl, double* diagKr);
 
 /* Scalar queries: "n_nonpos_Cw", "n_nonpos_Dw", "n_el", "n_p", "n_v",
- * "kernel_launches" (launches since create), "last_pcg_stop_iter", "k_tma" (1 if
+ * "kernel_launches" (launches since create), "last_pcg_stop_iter",
+ * with WB_DEBUG_SCALARS: "pcg_iters" (iterations of the last PCG solve, n),
+ * "alpha_<i>" = rz_i / pq_i and "beta_<i>" = rz_{i+1} / rz_i of its iteration i
+ * (0 <= i < n; 0 for iterations not run, as the oracle's O9 records them),
+ * "last_alpha_beta" = alpha_{n-1}, "last_beta" = beta_{n-1} (WB_ESTATE without the
+ * flag or before a solve, WB_EINVAL for i outside [0, n)), "k_tma" (1 if
  * the k = 2 Poisson operator runs as the TMA kernel for this mesh). */
 wb_status wb_query(wb_ctx* ctx, const char* key, double* value);
 /* Tuning knobs (results are identical up to rounding for every setting):

@@ -62,6 +62,8 @@ def lib():
             L.or_jacobi_diag.argtypes = [C.c_void_p, _D, _D]
             L.or_project.argtypes = [C.c_void_p, _D]
             L.or_pcg.argtypes = [C.c_void_p, _D, _D, _D, _D, C.c_int]
+            L.or_pcg_rec.argtypes = [C.c_void_p, _D, _D, _D, _D, C.c_int, _D, _D]
+            L.or_pcg_rec.restype = C.c_int
             L.or_pcg_step.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, _D]
             L.or_poisson.argtypes = [C.c_void_p, _D, _D, _D, _D, C.c_int]
             L.or_wbfbt.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, _D, _D, C.c_int]
@@ -203,6 +205,14 @@ class Oracle:
         x = np.zeros(self.n_p)
         self.L.or_pcg(self.h, _p(Xinv), _p(diagK), _p(b), _p(x), int(iters))
         return x
+
+    def pcg_scalars(self, Xinv, diagK, b, iters):
+        """PCG (O9) recording its scalars: (x, alpha[iters], beta[iters], iterations run);
+        alpha_i = rz_i / pq_i, beta_i = rz_{i+1} / rz_i (0 for iterations not run)."""
+        Xinv, diagK, b = _f64(Xinv), _f64(diagK), _f64(b)
+        x, a, bt = np.zeros(self.n_p), np.zeros(int(iters)), np.zeros(int(iters))
+        run = self.L.or_pcg_rec(self.h, _p(Xinv), _p(diagK), _p(b), _p(x), int(iters), _p(a), _p(bt))
+        return x, a, bt, int(run)
 
     def pcg_step(self, Xinv, diagK, x, r, p, rz):
         """One PCG iteration from state (x, r, p, rz); returns new (x, r, p, rz)."""

@@ -519,8 +519,17 @@ static void jacobi_minv(const double* diagK, double* Minv, int64_t n) {
   for (int64_t i = 0; i < n; ++i) Minv[i] = fabs(diagK[i]) > 1e-13 * dmax ? 1.0 / diagK[i] : 0.0;
 }
 
-/* x = PCG(K_side, b) with K_side = B Xinv B^T, Minv = 1/diag(K_side) (R11). */
+/* x = PCG(K_side, b) with K_side = B Xinv B^T, Minv = 1/diag(K_side) (R11).  When
+ * alpha / beta are non-NULL (length iters) they receive the scalars of O9 in iteration
+ * order: alpha_i = rz_i / pq_i and beta_i = rz_{i+1} / rz_i; iterations not run (a
+ * break of O9) are recorded as 0.  Returns the number of iterations run. */
+int or_pcg_rec(or_ctx* c, const double* Xinv, const double* diagK, const double* b, double* x, int iters,
+               double* alpha, double* beta);
 void or_pcg(or_ctx* c, const double* Xinv, const double* diagK, const double* b, double* x, int iters) {
+  (void)or_pcg_rec(c, Xinv, diagK, b, x, iters, NULL, NULL);
+}
+int or_pcg_rec(or_ctx* c, const double* Xinv, const double* diagK, const double* b, double* x, int iters,
+               double* alpha, double* beta) {
   const int64_t n = c->n_p;
   double* r = (double*)malloc(sizeof(double) * n); double* z = (double*)malloc(sizeof(double) * n);
   double* p = (double*)malloc(sizeof(double) * n); double* q = (double*)malloc(sizeof(double) * n);
@@ -528,13 +537,22 @@ void or_pcg(or_ctx* c, const double* Xinv, const double* diagK, const double* b,
   jacobi_minv(diagK, Minv, n);
   for (int64_t i = 0; i < n; ++i) { x[i] = 0.0; r[i] = b[i]; z[i] = Minv[i] * r[i]; p[i] = z[i]; }
   double rz = dot(r, z, n);
+  int run = 0;
+  for (int it = 0; it < iters; ++it) {
+    if (alpha) alpha[it] = 0.0;
+    if (beta) beta[it] = 0.0;
+  }
   for (int it = 0; it < iters; ++it) {
     if (rz == 0.0) break;
     double ab[2];
     pcg_step(c, Xinv, Minv, x, r, p, &rz, z, q, tv, ab);
     if (ab[0] == 0.0 && ab[1] == 0.0) break; /* pq == 0 */
+    if (alpha) alpha[it] = ab[0];
+    if (beta) beta[it] = ab[1];
+    run = it + 1;
   }
   free(r); free(z); free(p); free(q); free(Minv); free(tv);
+  return run;
 }
 
 /* One PCG iteration from a supplied state (x, r, p, rz) -- one-step parity. */

@@ -7,7 +7,7 @@ CUDA tensors (device memory, streams) and checks arguments.  There is no CPU
 fallback: importing without the built library raises.
 """
 from ._abi import (WBError, Context, lib, library_path, version, sizes,  # noqa: F401
-                   WB_STRICT_LUMP, WB_DEBUG_NOMASK, SYMBOLS)
+                   WB_STRICT_LUMP, WB_DEBUG_NOMASK, WB_DEBUG_SCALARS, SYMBOLS)
 
 __all__ = ["WBError", "Context", "lib", "library_path", "version", "sizes", "WB_STRICT_LUMP",
-           "WB_DEBUG_NOMASK", "SYMBOLS"]
+           "WB_DEBUG_NOMASK", "WB_DEBUG_SCALARS", "SYMBOLS"]

@@ -18,6 +18,7 @@ _LIB_PATH = os.path.join(HERE, "libwbfbt.so")
 
 WB_STRICT_LUMP = 1
 WB_DEBUG_NOMASK = 2
+WB_DEBUG_SCALARS = 4
 
 _STATUS = {0: "WB_OK", -1: "WB_EINVAL", -2: "WB_ENONPOS_MU", -3: "WB_ENONPOS_LUMP", -4: "WB_ECUDA",
            -5: "WB_ENOMEM", -6: "WB_EALIAS", -7: "WB_ESTATE"}

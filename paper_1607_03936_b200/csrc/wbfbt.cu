@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 #include <new>
 
 #include "../../include/wbfbt.h"
@@ -32,6 +33,7 @@ struct wb_ctx {
   double *dKl = nullptr, *dKr = nullptr, *MinvL = nullptr, *MinvR = nullptr;
   bool have_visc = false;
   long long n_nonpos[2] = {0, 0};
+  int last_pcg_iters = -1;  // iteration count of the last PCG solve (its histories are on the device)
   bool nonpos_pending = false;  // icount[1..2] not yet copied to n_nonpos
   // work vectors
   double* E = nullptr;                 // element-local velocity values, 3*nq*n_el
@@ -483,6 +485,7 @@ wb_status pcg_loop(wb_ctx* c, int side, int iters) {
 wb_status run_poisson(wb_ctx* c, int side, const double* b, double* x, int iters) {
   wb_status s = ensure_iters(c, iters);
   if (s) return s;
+  c->last_pcg_iters = iters;
   const double* Minv = side == 0 ? c->MinvL : c->MinvR;
   k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->n_el, c->nm, c->partial, c->counter, c->scal + S_SUM);
   LAUNCH_CHECK(c);
@@ -572,6 +575,7 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
   if (!out) return WB_EINVAL;
   *out = nullptr;
   if (N < 1 || N > 4096 || k < 2 || k > 4) return WB_EINVAL;
+  if (flags & ~(WB_STRICT_LUMP | WB_DEBUG_NOMASK | WB_DEBUG_SCALARS)) return WB_EINVAL;
   wb_ctx* c = new (std::nothrow) wb_ctx();
   if (!c) return WB_ENOMEM;
   c->N = N; c->k = k; c->n1 = k + 1; c->nq = c->n1 * c->n1 * c->n1; c->nm = k * (k + 1) * (k + 2) / 6;
@@ -1069,6 +1073,43 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
       t += ms;
     }
     *value = t;
+  }
+  else if (!strcmp(key, "pcg_iters") || !strncmp(key, "alpha_", 6) || !strncmp(key, "beta_", 5) ||
+           !strcmp(key, "last_alpha_beta") || !strcmp(key, "last_beta")) {
+    // PCG scalars of the last solve (WB_DEBUG_SCALARS), from the device histories:
+    // alpha_i = rz_i / pq_i, beta_i = rz_{i+1} / rz_i; 0 for iterations not run (O9)
+    if (!(c->flags & WB_DEBUG_SCALARS)) return set_err(c, WB_ESTATE, "create the context with WB_DEBUG_SCALARS");
+    const int n = c->last_pcg_iters;
+    if (n < 0) return set_err(c, WB_ESTATE, "no PCG solve yet");
+    if (!strcmp(key, "pcg_iters")) { *value = n; return WB_OK; }
+    int i;
+    if (!strcmp(key, "last_alpha_beta")) i = n - 1;          // alpha of the last iteration
+    else if (!strcmp(key, "last_beta")) i = n - 1;
+    else {
+      char* end = nullptr;
+      const char* num = key + (key[0] == 'a' ? 6 : 5);
+      i = (int)strtol(num, &end, 10);
+      if (end == num || *end) return set_err(c, WB_EINVAL, "bad iteration index in '%s'", key);
+    }
+    if (i < 0 || i >= n) return set_err(c, WB_EINVAL, "iteration %d outside the last solve (%d)", i, n);
+    double rz[2], pq = 0.0;
+    int st = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(rz, rz_hist(c) + i, sizeof(double) * (i + 1 < n ? 2 : 1), cudaMemcpyDeviceToHost,
+                                c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(&pq, pq_hist(c) + i, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(&st, c->stop + i, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if (i + 1 == n) {  // rz_n: the last update's partials, summed here in index order
+      std::vector<double> part(c->red_blocks);
+      CUDA_TRY(c, cudaMemcpyAsync(part.data(), c->rzp, sizeof(double) * c->red_blocks, cudaMemcpyDeviceToHost,
+                                  c->stream));
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      rz[1] = 0.0;
+      for (double v : part) rz[1] += v;
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    const bool ran = !st && pq != 0.0;
+    const bool is_alpha = key[0] == 'a' || !strcmp(key, "last_alpha_beta");
+    *value = !ran ? 0.0 : (is_alpha ? rz[0] / pq : rz[1] / rz[0]);
   }
   else if (!strcmp(key, "last_pcg_stop_iter")) {
     int st[1024];

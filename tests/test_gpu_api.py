@@ -37,6 +37,8 @@ def test_errors():
         Context(0, 2)
     with pytest.raises(WBError, match="WB_EINVAL"):
         Context(4, 5)
+    with pytest.raises(WBError, match="WB_EINVAL"):
+        Context(4, 2, flags=8)  # unknown flag bit
 
 
 def test_strict_lump_flag():
@@ -205,3 +207,36 @@ def test_full_size_wbfbt_properties(full):
     xo = full.o.poisson(st["Dinv"], st["diagKr"], b, it)
     ro = full.o.poisson_relres(st["Dinv"], b, xo)
     assert rg <= 2 * ro and ro <= 2 * rg
+
+
+@pytest.mark.parametrize("cfg,N", [("C2", 6), ("C1", None)])
+def test_pcg_scalars_match_oracle(cfg, N):
+    """WB_DEBUG_SCALARS: the last solve's alpha_i / beta_i (device histories) against the
+    oracle's recorded O9 scalars on the same projected right-hand side.  The first
+    iterations agree to rounding; later ones drift with CG's sensitivity, so they are
+    checked at a looser bound."""
+    from paper_1607_03936_b200 import WB_DEBUG_SCALARS, WBError
+    p = Pair(cfg, N=N, flags=WB_DEBUG_SCALARS)
+    iters = 12
+    b = p.inp["p"]
+    p.ctx.poisson_pcg(1, dev(b), empty(p.ctx.n_p), iters)
+    assert p.ctx.query("pcg_iters") == iters
+    _, al, be, run = p.o.pcg_scalars(p.ost["Dinv"], p.ost["diagKr"], p.o.project(b), iters)
+    assert run == iters
+    ga = np.array([p.ctx.query(f"alpha_{i}") for i in range(iters)])
+    gb = np.array([p.ctx.query(f"beta_{i}") for i in range(iters)])
+    assert p.ctx.query("last_alpha_beta") == ga[-1] and p.ctx.query("last_beta") == gb[-1]
+    # (no sign check: with row-sum lumping D_w may have nonpositive entries, K indefinite)
+    np.testing.assert_allclose(ga[:4], al[:4], rtol=1e-10)
+    np.testing.assert_allclose(gb[:4], be[:4], rtol=1e-9)
+    np.testing.assert_allclose(ga, al, rtol=1e-3)  # C1's K is indefinite: rounding grows
+    with pytest.raises(WBError, match="WB_EINVAL"):
+        p.ctx.query(f"alpha_{iters}")
+
+
+def test_pcg_scalars_need_flag():
+    from paper_1607_03936_b200 import WBError
+    p = Pair("C1")
+    p.ctx.poisson_pcg(1, dev(p.inp["p"]), empty(p.ctx.n_p), 3)
+    with pytest.raises(WBError, match="WB_ESTATE"):
+        p.ctx.query("alpha_0")

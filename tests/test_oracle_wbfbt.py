@@ -89,6 +89,38 @@ def test_pcg_step_matches_pcg():
     np.testing.assert_array_equal(x, o.pcg(st["Dinv"], st["diagKr"], b, 7))
 
 
+def test_pcg_scalars_match_dense_textbook_pcg():
+    """The recorded alpha_i, beta_i (O9) equal those of a textbook PCG written here in
+    numpy on the dense K (assembled from the dense B) with the same Jacobi Minv; the
+    solution equals o.pcg's bit-exactly (recording does not change the arithmetic)."""
+    o = Oracle(3, 2)
+    st = o.setup(_mild_mu(o, 5))
+    B = _dense_B(o)
+    K = B @ (np.tile(st["Dinv"], 3)[:, None] * B.T)
+    b = o.project(np.random.default_rng(4).uniform(-1, 1, o.n_p))
+    iters = 6
+    x, al, be, run = o.pcg_scalars(st["Dinv"], st["diagKr"], b, iters)
+    assert run == iters
+    np.testing.assert_array_equal(x, o.pcg(st["Dinv"], st["diagKr"], b, iters))
+    Minv = 1.0 / st["diagKr"]
+    r = b.copy(); z = Minv * r; p = z.copy(); rz = r @ z
+    for i in range(iters):
+        q = K @ p
+        a = rz / (p @ q)
+        r = r - a * q
+        z = Minv * r
+        rz2 = r @ z
+        bt = rz2 / rz
+        p = z + bt * p
+        rz = rz2
+        assert abs(al[i] - a) <= 1e-9 * abs(a), (i, al[i], a)
+        assert abs(be[i] - bt) <= 1e-7 * abs(bt), (i, be[i], bt)
+        assert al[i] > 0 and be[i] > 0  # SPD on the complement of the constants
+    # zero iterations: nothing recorded
+    _, al0, be0, run0 = o.pcg_scalars(st["Dinv"], st["diagKr"], b, 0)
+    assert run0 == 0 and al0.size == 0
+
+
 @pytest.mark.parametrize("a_l,a_r", [(1.0, 1.0), (1.0, 2.0), (3.0, 1.0)])
 def test_wbfbt_converged_equals_dense_formula(a_l, a_r):
     N, k = 2, 2
