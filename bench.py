@@ -44,6 +44,13 @@ def peaks():
         return FALLBACK_HBM, "fallback"
 
 
+# DFMA-pipe instructions per element of the k = 2 sum-factorised A using the exact zero
+# centre rows ("zero-row" count; FMA = 1), and the measured DFMA
+# rate of this B200 (profiles/r01_microbench_peaks.jsonl: 34.2 TFLOP/s = 17.1 T DFMA/s).
+A_DFMA_PER_ELEMENT = 2538
+DFMA_PEAK_INSTR_PER_S = 34.195e12 / 2
+
+
 def ncu_traffic(kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu capture summary
     (profiles/ncu_traffic.json, written by tools/ncu_summary.py), else None."""
@@ -246,10 +253,11 @@ def run_ours(args):
     value = job_throughput(world, args.steps, t_ms)
 
     # ---- component timings (same context, L2 flushed before each rep)
-    def timed(fn, reps=args.comp_reps):
+    def timed(fn, reps=args.comp_reps, cold=True):
         ts = []
         for _ in range(reps):
-            flush.zero_()
+            if cold:
+                flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream); fn(); b.record(stream)
             b.synchronize()
@@ -259,6 +267,7 @@ def run_ours(args):
     ctx.set_viscosity(mu)
     qv = torch.empty(ctx.n_p, **f64)
     tA = timed(lambda: ctx.apply_A(u, yA))
+    tAw = timed(lambda: ctx.apply_A(u, yA), cold=False)
     tB = timed(lambda: ctx.apply_B(u, pB))
     tBT = timed(lambda: ctx.apply_BT(p, yBT))
     tK = timed(lambda: ctx.apply_K(1, p, qv))
@@ -334,6 +343,8 @@ def run_ours(args):
                 "components": {
                     "A_gdofs": n_v / (tA * 1e-3) / 1e9, "A_ms": tA, "A_bytes": bytes_A,
                     "A_hbm_frac": bytes_A / (tA * 1e-3) / 1e9 / hbm,
+                    "A_fp64_frac": A_DFMA_PER_ELEMENT * n_el / (tA * 1e-3) / DFMA_PEAK_INSTR_PER_S,
+                    "A_ms_warm": tAw, "A_gdofs_warm": n_v / (tAw * 1e-3) / 1e9,
                     "B_gdofs": n_v / (tB * 1e-3) / 1e9, "BT_gdofs": n_v / (tBT * 1e-3) / 1e9,
                     "K_ms_cold": tK, "K_ms_warm": tKw, "wbfbt_ms": tW, "wbfbt_applies_per_s": 1e3 / tW,
                     "setup_ms": tS},
@@ -357,7 +368,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--comp-reps", type=int, default=20)
+    ap.add_argument("--comp-reps", type=int, default=30)  # median of >= 30 reps
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
