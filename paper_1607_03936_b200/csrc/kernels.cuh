@@ -370,149 +370,12 @@ __global__ void k_BT_elem(const double* __restrict__ p, double* __restrict__ E, 
   }
 }
 
-// ------------------------------------------------------------------ row a5: A(mu) (k = 2 register kernel)
-// One thread per (element, velocity component c); the element's u_c lives in
-// registers through all sum-factorisation passes:
-//   U = (I x I x I) u_c  (GLL -> Gauss interpolation),
-//   g_cj = Dg_j U        (collocation derivative on the Gauss points),
-//   tau_cj = mut (g_cj + g_jc)   (g_jc exchanged in shared memory, one Gauss
-//                                 level at a time),
-//   y_c = (I^T x I^T x I^T) sum_j Dg_j^T tau_cj.
-// mut = mu w_q detJ (2/h)^2, so y_{c,a} = sum_q w_q detJ mu sum_j d_j phi_a
-// (d_j u_c + d_c u_j) = int 2 mu eps(u):eps(phi_a e_c)  (PAPER.md:148-151,
-// 986-990).  Output: element-local E[c][a][e].
-template <int K, int NE>
-__global__ void __launch_bounds__(3 * NE) k_A_reg(const double* __restrict__ mut, const double* __restrict__ u,
-                                                  double* __restrict__ E, Geo G, int nomask) {
-  constexpr int n1 = K + 1, NQ = Ord<K>::NQ, P = n1 * n1;
-  __shared__ double X[P][9][NE];
-  const int le = threadIdx.x % NE, c = threadIdx.x / NE;
-  const int64_t e = (int64_t)blockIdx.x * NE + le;
-  const bool valid = e < G.n_el;
-  int ex = 0, ey = 0, ez = 0;
-  if (valid) elem_xyz(e, G.N, ex, ey, ez);
-  double U[NQ];
-#pragma unroll
-  for (int az = 0; az < n1; ++az)
-#pragma unroll
-    for (int ay = 0; ay < n1; ++ay)
-#pragma unroll
-      for (int ax = 0; ax < n1; ++ax) {
-        const int gx = K * ex + ax, gy = K * ey + ay, gz = K * ez + az;
-        double v = 0.0;
-        if (valid && (nomask || !node_bnd(gx, gy, gz, G.nn1))) v = u[c * G.n_nodes + node_id(gx, gy, gz, G.nn1)];
-        U[(az * n1 + ay) * n1 + ax] = v;
-      }
-  // interpolate x, y, z (in place per pencil)
-#pragma unroll
-  for (int dir = 0; dir < 3; ++dir) {
-    const int st = dir == 0 ? 1 : (dir == 1 ? n1 : P);
-#pragma unroll
-    for (int o1 = 0; o1 < n1; ++o1)
-#pragma unroll
-      for (int o2 = 0; o2 < n1; ++o2) {
-        const int base = dir == 0 ? (o2 * n1 + o1) * n1 : (dir == 1 ? o2 * P + o1 : o2 * n1 + o1);
-        double v[n1];
-#pragma unroll
-        for (int j = 0; j < n1; ++j) v[j] = U[base + j * st];
-#pragma unroll
-        for (int i = 0; i < n1; ++i) {
-          double t = 0.0;
-#pragma unroll
-          for (int j = 0; j < n1; ++j) t = fma(TB(K).I[i][j], v[j], t);
-          U[base + i * st] = t;
-        }
-      }
-  }
-  double V[NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) V[q] = 0.0;
-#pragma unroll
-  for (int iz = 0; iz < n1; ++iz) {
-    double gx[P], gy[P], gz[P];
-#pragma unroll
-    for (int iy = 0; iy < n1; ++iy)
-#pragma unroll
-      for (int ix = 0; ix < n1; ++ix) {
-        double tx = 0.0, ty = 0.0, tz = 0.0;
-#pragma unroll
-        for (int j = 0; j < n1; ++j) {
-          tx = fma(TB(K).Dg[ix][j], U[(iz * n1 + iy) * n1 + j], tx);
-          ty = fma(TB(K).Dg[iy][j], U[(iz * n1 + j) * n1 + ix], ty);
-          tz = fma(TB(K).Dg[iz][j], U[(j * n1 + iy) * n1 + ix], tz);
-        }
-        gx[iy * n1 + ix] = tx; gy[iy * n1 + ix] = ty; gz[iy * n1 + ix] = tz;
-      }
-#pragma unroll
-    for (int q = 0; q < P; ++q) {
-      X[q][c * 3 + 0][le] = gx[q];
-      X[q][c * 3 + 1][le] = gy[q];
-      X[q][c * 3 + 2][le] = gz[q];
-    }
-    __syncthreads();
-    double Wx[P], Wy[P], Wz[P];
-#pragma unroll
-    for (int q = 0; q < P; ++q) {
-      const double mu = valid ? mut[e * NQ + iz * P + q] : 0.0;
-      Wx[q] = mu * (gx[q] + X[q][0 * 3 + c][le]);
-      Wy[q] = mu * (gy[q] + X[q][1 * 3 + c][le]);
-      Wz[q] = mu * (gz[q] + X[q][2 * 3 + c][le]);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int iy = 0; iy < n1; ++iy)
-#pragma unroll
-      for (int jx = 0; jx < n1; ++jx) {
-        double t = V[(iz * n1 + iy) * n1 + jx];
-#pragma unroll
-        for (int ix = 0; ix < n1; ++ix) t = fma(TB(K).Dg[ix][jx], Wx[iy * n1 + ix], t);
-        V[(iz * n1 + iy) * n1 + jx] = t;
-      }
-#pragma unroll
-    for (int jy = 0; jy < n1; ++jy)
-#pragma unroll
-      for (int ix = 0; ix < n1; ++ix) {
-        double t = V[(iz * n1 + jy) * n1 + ix];
-#pragma unroll
-        for (int iy = 0; iy < n1; ++iy) t = fma(TB(K).Dg[iy][jy], Wy[iy * n1 + ix], t);
-        V[(iz * n1 + jy) * n1 + ix] = t;
-      }
-#pragma unroll
-    for (int jz = 0; jz < n1; ++jz)
-#pragma unroll
-      for (int q = 0; q < P; ++q) V[jz * P + q] = fma(TB(K).Dg[iz][jz], Wz[q], V[jz * P + q]);
-  }
-  // transposed interpolation z, y, x
-#pragma unroll
-  for (int dir = 2; dir >= 0; --dir) {
-    const int st = dir == 0 ? 1 : (dir == 1 ? n1 : P);
-#pragma unroll
-    for (int o1 = 0; o1 < n1; ++o1)
-#pragma unroll
-      for (int o2 = 0; o2 < n1; ++o2) {
-        const int base = dir == 0 ? (o2 * n1 + o1) * n1 : (dir == 1 ? o2 * P + o1 : o2 * n1 + o1);
-        double v[n1];
-#pragma unroll
-        for (int j = 0; j < n1; ++j) v[j] = V[base + j * st];
-#pragma unroll
-        for (int a = 0; a < n1; ++a) {
-          double t = 0.0;
-#pragma unroll
-          for (int j = 0; j < n1; ++j) t = fma(TB(K).I[j][a], v[j], t);
-          V[base + a * st] = t;
-        }
-      }
-  }
-  if (valid) {
-#pragma unroll
-    for (int a = 0; a < NQ; ++a) E[(int64_t)(c * NQ + a) * G.n_el + e] = V[a];
-  }
-}
-
 // ------------------------------------------------------------------ row a5: A(mu) (generic slice kernel, k = 3, 4)
 // NE elements per block, n1 x n1 threads per element; the thread (a, b) owns
 // one pencil per pass and the third index is looped in registers; the passes
-// exchange through shared memory (same operator as k_A_reg).
+// exchange through shared memory.  Output: element-local E[c][a][e] (gathered by
+// k_gather).  Same operator as the k = 2 tile kernel (a2_tile.cuh):
+// y_{c,a} = int 2 mu eps(u):eps(phi_a e_c).
 template <int K, int NE>
 __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* __restrict__ mut,
                                                                   const double* __restrict__ u,
