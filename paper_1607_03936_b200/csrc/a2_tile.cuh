@@ -529,24 +529,4 @@ inline int64_t a2_skel_count(int N) {
   return (int64_t)PX * nn1 * nn1 + (int64_t)QX * PY * nn1 + (int64_t)QX * QY * PZ;
 }
 
-// tile-blocked viscosity for k_A_tile: mutT[tile][q][le] = mu w_q h/2 (as k_prescale)
-template <int TX, int TY, int TZ>
-__global__ void k_prescale_t2(const double* __restrict__ mu, double* __restrict__ mutT, int N, double hs,
-                              unsigned long long* bad) {
-  constexpr int NE = TX * TY * TZ;
-  const int64_t n = (int64_t)N * N * N * 27;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int q = (int)(i % 27);
-  const int64_t e = i / 27;
-  const int ex = (int)(e % N), ey = (int)((e / N) % N), ez = (int)(e / ((int64_t)N * N));
-  const int NTX = (N + TX - 1) / TX, NTY = (N + TY - 1) / TY;
-  const int tile = ex / TX + NTX * (ey / TY + NTY * (ez / TZ));
-  const int le = ex % TX + TX * (ey % TY + TY * (ez % TZ));
-  const double m = mu[i];
-  if (!(m > 0.0) || !isfinite(m)) atomicAdd(bad, 1ull);
-  const double wq = TB(2).w[q % 3] * TB(2).w[(q / 3) % 3] * TB(2).w[q / 9];
-  mutT[((int64_t)tile * 27 + q) * NE + le] = m * wq * hs;
-}
-
 }  // namespace wb
