@@ -13,7 +13,7 @@ namespace wb {
 __constant__ double c_J2[27][4];
 
 // One thread per element, one read of its 27 mu samples:
-//   mutT[tile][q][le] = mu w_q h/2          (A's tile-blocked layout, as k_prescale_t2)
+//   mutT[tile][q][le] = mu w_q h/2          (A's tile-blocked layout, as k_prescale for k = 3, 4)
 //   L[a][e] = detJ sum_q sqrt(mu_q) phi_a(xi_q) w_q   (eq:lumping)
 // with L sum-factorised (x, y, z passes of the 1-D factor W1[a][i] = phi_a(xg_i) w_i).
 // Nonpositive or non-finite mu samples are counted in bad (the caller rejects them).
