@@ -43,3 +43,10 @@ for k, n in enumerate(names):
         continue
     print(f"  {n:18s} {v[k] / tiles:9.1f} cyc/tile  {100 * v[k] / tot:5.1f} %")
 print(f"  per launch per CTA: {tot / (launches * 148):9.0f} cyc = {tot / (launches * 148) / 1965:6.2f} us")
+# launch timeline of one PCG iteration (it = 5): %globaltimer per CTA
+c.set_option("k_dbg", 0x4000 | 0x2000 | extra)
+c.poisson_pcg(1, p, pv, iters)
+t = [c.query(f"ktl{k}") for k in range(6)]
+c.set_option("k_dbg", 0)
+print(f"launch it=5 (ns): span {t[0]:.0f}, CTA entry spread {t[1]:.0f}, mean entry->loop {t[2]:.0f}, "
+      f"mean loop {t[3]:.0f}, mean loop end->exit {t[4]:.0f}, exit spread {t[5]:.0f}")
