@@ -17,6 +17,14 @@ namespace wb {
 // per phase: [0] prologue/control, [1] wait p/r/Minv, [2] step 0 (+ barrier),
 // [3] wait X, [4] step 1 (+ barrier), [5] step 2 (+ barrier), [6] tiles
 __device__ unsigned long long g_kprof[8];
+// launch timeline probe (WB_KPROF, k_dbg 0x4000, PCG iteration 5 only): per CTA the
+// %globaltimer (ns) at entry, loop start, loop end and exit
+__device__ unsigned long long g_ktl[512][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -195,6 +203,10 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
              double* pqp) {
   using F = FK2<TX, TY, TZ>;
   using K = FKT<TX, TY, TZ>;
+#ifdef WB_KPROF
+  const bool tl = (mode & 0x4000) && it == 5 && threadIdx.x == 0 && blockIdx.x < 512;
+  if (tl) g_ktl[blockIdx.x][0] = gtimer();
+#endif
   // offsets from the (1024-aligned) dynamic shared base itself, so that every access
   // below stays a shared-space access (LDS/STS), not a generic one
   extern __shared__ __align__(1024) unsigned char smraw[];
@@ -260,6 +272,9 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
   auto lap = [](int) {};
 #endif
   lap(0);
+#ifdef WB_KPROF
+  if (tl) g_ktl[blockIdx.x][1] = gtimer();
+#endif
   double dot = 0.0;
   for (int k = 0; tile < n_tiles; ++k, tile += gridDim.x) {
     const unsigned ph = k & 1;
@@ -368,7 +383,13 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
   }
   if (prof)
     for (int k = 0; k < 8; ++k) atomicAdd(&g_kprof[k], pt[k]);
+#ifdef WB_KPROF
+  if (tl) g_ktl[blockIdx.x][2] = gtimer();
+#endif
   store_partial<F::NTH>(dot, pqp);
+#ifdef WB_KPROF
+  if (tl) g_ktl[blockIdx.x][3] = gtimer();
+#endif
 }
 
 // XT[tile][nx][row(ny, nz)] = X(2 ex0 + nx, 2 ey0 + ny, 2 ez0 + nz), 0 outside the mesh

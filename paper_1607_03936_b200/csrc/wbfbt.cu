@@ -1046,6 +1046,24 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
       CUDA_TRY(c, cudaMemcpyToSymbol(g_aprof, h, sizeof(h)));
     }
 #endif
+#ifdef WB_KPROF
+  } else if (!strncmp(key, "ktl", 3) && key[3] >= '0' && key[3] <= '5' && !key[4]) {
+    // launch timeline of PCG iteration 5 (ns): 0 span (last exit - first entry), 1 entry
+    // spread, 2 mean entry -> loop start, 3 mean loop, 4 mean loop end -> exit, 5 exit spread
+    unsigned long long h[512][4];
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    CUDA_TRY(c, cudaMemcpyFromSymbol(h, g_ktl, sizeof(h)));
+    const int n = std::min(c->nsm, 512);
+    unsigned long long e0 = ~0ull, e1 = 0, x0 = ~0ull, x1 = 0;
+    double pro = 0, loop = 0, epi = 0;
+    for (int i = 0; i < n; ++i) {
+      e0 = std::min(e0, h[i][0]); e1 = std::max(e1, h[i][0]);
+      x0 = std::min(x0, h[i][3]); x1 = std::max(x1, h[i][3]);
+      pro += (double)(h[i][1] - h[i][0]); loop += (double)(h[i][2] - h[i][1]); epi += (double)(h[i][3] - h[i][2]);
+    }
+    const double v[6] = {(double)(x1 - e0), (double)(e1 - e0), pro / n, loop / n, epi / n, (double)(x1 - x0)};
+    *value = v[key[3] - '0'];
+#endif
   } else if (!strncmp(key, "kprof", 5) && key[5] >= '0' && key[5] <= '7' && !key[6]) {
     // phase-timing probe of the TMA Poisson kernel (k_dbg 0x4000): accumulated cycles;
     // reading "kprof7" (the last) clears the counters
