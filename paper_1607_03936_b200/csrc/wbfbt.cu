@@ -59,7 +59,7 @@ struct wb_ctx {
   int red_blocks = 0, max_partials = 0, nsm = 148;
   double* stage = nullptr;  // wb_hotpath_host staging (lazily allocated)
   cudaStream_t copy_stream = nullptr;  // wb_hotpath_host: copies overlapped with compute
-  cudaEvent_t ev_in = nullptr, ev_ab = nullptr, ev_bt = nullptr, ev_done = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_ab = nullptr, ev_bt = nullptr, ev_done = nullptr, ev_p = nullptr;
   // k = 2 tile-assembled A (4x4x4 tiles): upper-shell and lower-face node partials
   // (L2-resident), summed by the skeleton kernel; mut is tile-blocked for k = 2
   double* Fu = nullptr;
@@ -543,7 +543,7 @@ void free_all(wb_ctx* c) {
   clear_graphs(c);
   if (c->cap_stream) { cudaStreamDestroy(c->cap_stream); c->cap_stream = nullptr; }
   if (c->copy_stream) { cudaStreamDestroy(c->copy_stream); c->copy_stream = nullptr; }
-  for (cudaEvent_t* e : {&c->ev_in, &c->ev_ab, &c->ev_bt, &c->ev_done})
+  for (cudaEvent_t* e : {&c->ev_in, &c->ev_ab, &c->ev_bt, &c->ev_done, &c->ev_p})
     if (*e) { cudaEventDestroy(*e); *e = nullptr; }
   for (int i = 0; i < 2 * wb_ctx::PROF_MAX; ++i)
     if (c->prof_ev[i]) { cudaEventDestroy(c->prof_ev[i]); c->prof_ev[i] = nullptr; }
@@ -921,39 +921,52 @@ wb_status wb_hotpath_host(wb_ctx* c, const double* mu_q, double a_l, double a_r,
   double* dpB = dp + rp;
   double* dz = dpB + rp;
   const size_t bmu = sizeof(double) * nmu, bv = sizeof(double) * c->n_v, bp = sizeof(double) * c->n_p;
-  // Copies overlap compute (pinned host memory makes them asynchronous): u and p
-  // travel on a copy stream during the setup; yA, pB and yBT travel back while the
-  // wBFBT PCG loops run; only mu in and z out are on the critical path.
+  // Copies overlap compute (pinned host memory makes them asynchronous).  Order of work:
+  // mu in (critical) -> setup -> wBFBT's right Poisson solve (needs only p, which
+  // arrives first on the copy stream) while u arrives -> the standalone A, B, B^T ->
+  // the middle of wBFBT -> its left Poisson solve, while yA, pB and yBT travel back;
+  // then z out.  The wBFBT kernel sequence is exactly run_wbfbt's.
   if (!c->copy_stream) {
     if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
       c->copy_stream = nullptr;
       cudaGetLastError();
       return set_err(c, WB_ECUDA, "copy stream creation failed");
     }
-    for (cudaEvent_t* e : {&c->ev_in, &c->ev_ab, &c->ev_bt, &c->ev_done})
+    for (cudaEvent_t* e : {&c->ev_in, &c->ev_ab, &c->ev_bt, &c->ev_done, &c->ev_p})
       CUDA_TRY(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   }
   cudaStream_t cs = c->copy_stream;
   CUDA_TRY(c, cudaEventRecord(c->ev_done, c->stream));  // previous work on the context stream
   CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_done, 0));
   CUDA_TRY(c, cudaMemcpyAsync(dmu, mu_q, bmu, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(du, u, bv, cudaMemcpyHostToDevice, cs));
   CUDA_TRY(c, cudaMemcpyAsync(dp, p, bp, cudaMemcpyHostToDevice, cs));
+  CUDA_TRY(c, cudaEventRecord(c->ev_p, cs));
+  CUDA_TRY(c, cudaMemcpyAsync(du, u, bv, cudaMemcpyHostToDevice, cs));
   CUDA_TRY(c, cudaEventRecord(c->ev_in, cs));
   wb_status s = wb_set_viscosity(c, dmu, a_l, a_r);  // synchronous (status)
   if (s) return s;
+  if (iters < 0) return set_err(c, WB_EINVAL, "iters must be >= 0");
+  const int nomask = (c->flags & WB_DEBUG_NOMASK) ? 1 : 0;
+  // wBFBT, right solve: y = P PCG(K_r, P p)
+  CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_p, 0));
+  if ((s = run_poisson(c, 1, dp, c->s2, iters))) return s;
+  // standalone applies
   CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_in, 0));
-  if ((s = wb_apply_A(c, du, dyA))) return s;
-  if ((s = wb_apply_B(c, du, dpB))) return s;
+  if ((s = run_A(c, du, dyA, nomask))) return s;
+  if ((s = run_B(c, du, nullptr, dpB, nomask, nullptr, nullptr, nullptr, c->nm, 1))) return s;
   CUDA_TRY(c, cudaEventRecord(c->ev_ab, c->stream));
-  if ((s = wb_apply_BT(c, dp, dyBT))) return s;
+  if ((s = run_BT(c, dp, nullptr, dyBT, nomask, nullptr, c->nm, 1))) return s;
   CUDA_TRY(c, cudaEventRecord(c->ev_bt, c->stream));
   CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_ab, 0));
   CUDA_TRY(c, cudaMemcpyAsync(yA, dyA, bv, cudaMemcpyDeviceToHost, cs));
   CUDA_TRY(c, cudaMemcpyAsync(pB, dpB, bp, cudaMemcpyDeviceToHost, cs));
   CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_bt, 0));
   CUDA_TRY(c, cudaMemcpyAsync(yBT, dyBT, bv, cudaMemcpyDeviceToHost, cs));
-  if ((s = wb_apply_wbfbt(c, dp, dz, iters))) return s;
+  // wBFBT, middle and left solve (as run_wbfbt)
+  if ((s = run_BT(c, c->s2, c->Dinv, c->tw, 0, nullptr, c->nm, 1))) return s;
+  if ((s = run_A(c, c->tw, c->tv, 0))) return s;
+  if ((s = run_B(c, c->tv, c->Cinv, c->s2, 0, nullptr, nullptr, nullptr, c->nm, 1))) return s;
+  if ((s = run_poisson(c, 0, c->s2, dz, iters))) return s;
   CUDA_TRY(c, cudaMemcpyAsync(z, dz, bp, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(cs));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
