@@ -127,9 +127,12 @@ wb_status wb_apply_wbfbt(wb_ctx* ctx, const double* r, double* z, int iters);
  * Synchronous (setup reports status). */
 wb_status wb_hotpath(wb_ctx* ctx, const double* mu_q, double a_l, double a_r, const double* u,
                      const double* p, int iters, double* yA, double* pB, double* yBT, double* z);
-/* The same step with HOST buffers: copies mu_q, u, p host->device and the four
- * results device->host (cudaMemcpyAsync on the context stream; pinned host
- * memory gives asynchronous copies).  Synchronous. */
+/* The same step with HOST buffers (pinned host memory gives asynchronous
+ * copies): mu_q is copied on the context stream, p and u on a library-owned copy
+ * stream that overlaps the setup and wBFBT's right Poisson solve; the standalone
+ * A, B, B^T run between the two wBFBT solves and yA, pB, yBT travel back during
+ * the left one; z last.  Same results as wb_hotpath.  The staging buffers
+ * (n_el n_q + 3 n_v + 3 n_p doubles) are allocated on first use.  Synchronous. */
 wb_status wb_hotpath_host(wb_ctx* ctx, const double* mu_q, double a_l, double a_r,
                           const double* u, const double* p, int iters, double* yA, double* pB,
                           double* yBT, double* z);
