@@ -293,16 +293,20 @@ def run_ours(args):
     n_el, n_nodes, n_v, n_p, n_q = ctx.n_el, ctx.n_nodes, ctx.n_v, ctx.n_p, ctx.n_q
     hbm, peak_kind = peaks()
     bytes_A = 8 * (n_el * n_q + 2 * n_v)          # mu~ + u in + y out
-    # fused K kernel per launch: p_old, r, Minv (mode-major n_p each), X^-1 (nodal) in;
-    # p_new, q out (DESIGN.md Sec. 7)
-    bytes_K = 8 * (5 * n_p + n_nodes)
+    # fused K kernel per launch: p_old and z = Minv r (stored by the PCG
+    # update; with option kz = 0: r and Minv) in, mode-major n_p each; X^-1 (nodal) in;
+    # p_new, q out
+    zbox = bool(ctx.query("kz"))
+    bytes_K = 8 * ((4 if zbox else 5) * n_p + n_nodes)
     kname = "k_K2_tma" if ctx.query("k_tma") else "k_K2_fused"
     roof = {"bound": "hbm", "kernel": f"{kname} (PCG: p-update + B^T + X^-1 + B + <p,q>)",
             "achieved": bytes_K / (k_avg * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
             "frac": bytes_K / (k_avg * 1e-3) / 1e9 / hbm, "traffic": ncu_traffic(kname),
             "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum, "
                               "one ncu --set full capture)", "peak_kind": peak_kind,
-            "algorithmic_bytes_per_launch": bytes_K, "launch_ms": k_avg, "launches_per_step": k_n / prof_steps,
+            "algorithmic_bytes_per_launch": bytes_K,
+            "algorithmic_bytes_def": ("8*(4*n_p + n_nodes): p_old, z in; p_new, q out; X in" if zbox else
+                                      "8*(5*n_p + n_nodes): p_old, r, Minv in; p_new, q out; X in"), "launch_ms": k_avg, "launches_per_step": k_n / prof_steps,
             "share_of_step": k_ms / prof_steps / prof_step_ms, "profiled_step_ms": prof_step_ms}
     tKw = k_avg
 

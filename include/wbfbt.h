@@ -153,7 +153,8 @@ wb_status wb_get_jacobi(wb_ctx* ctx, double* diagKl, double* diagKr);
  * "alpha_<i>" = rz_i / pq_i and "beta_<i>" = rz_{i+1} / rz_i of its iteration i
  * (0 <= i < n; 0 for iterations not run, as the oracle's O9 records them),
  * "last_alpha_beta" = alpha_{n-1}, "last_beta" = beta_{n-1} (WB_ESTATE without the
- * flag or before a solve, WB_EINVAL for i outside [0, n)), "k_tma" (1 if
+ * flag or before a solve, WB_EINVAL for i outside [0, n)), "kz" (1 if the PCG
+ * update stores z = Minv r for the TMA Poisson kernel), "k_tma" (1 if
  * the k = 2 Poisson operator runs as the TMA kernel for this mesh). */
 wb_status wb_query(wb_ctx* ctx, const char* key, double* value);
 /* Tuning knobs (results are identical up to rounding for every setting):

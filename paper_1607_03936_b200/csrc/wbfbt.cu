@@ -1088,6 +1088,8 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
       memset(h, 0, sizeof(h));
       CUDA_TRY(c, cudaMemcpyToSymbol(g_kprof, h, sizeof(h)));
     }
+  } else if (!strcmp(key, "kz")) {  // 1: the PCG update stores z = Minv r and the TMA kernel loads it
+    *value = (tma_active(c) && c->kz) ? 1.0 : 0.0;
   } else if (!strcmp(key, "k_tma")) {  // 1: the Poisson operator runs as the TMA kernel (k_K2_tma)
     *value = tma_active(c) ? 1.0 : 0.0;
   } else if (!strcmp(key, "occ_a2")) {
