@@ -159,7 +159,7 @@ wb_status wb_get_jacobi(wb_ctx* ctx, double* diagKl, double* diagKr);
 wb_status wb_query(wb_ctx* ctx, const char* key, double* value);
 /* Tuning knobs (results are identical up to rounding for every setting):
  * "kz" (k = 2 TMA Poisson kernel: 1 = the PCG update stores z = Minv r and the
- * kernel loads it as one box, the default; 0 = it loads r and Minv),
+ * kernel loads it as one box; 0 = it loads r and Minv, the default),
  * "graph" (1 = replay the PCG iteration loop as a CUDA graph, default; 0 =
  * plain launches), "profile" (1 = plain launches with a CUDA-event pair around
  * every Poisson-operator launch; wb_query "prof_k_ms" / "prof_k_count" read

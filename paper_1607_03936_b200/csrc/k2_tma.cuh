@@ -67,15 +67,17 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
 }
 
 // Layout constants of the TMA variant (tile TX x TY x TZ elements).
-// TMA tile loads of fp64 need the innermost start coordinate 16-byte aligned
-// (even): the element box starts at ex0 - 2 (ex0 is a multiple of 4) and is
-// BXW = TX + 4 wide; halo element hx (= ex0 - 1 + hx) sits at box column hx + 1.
-// Step 0 repacks the boxes into Ps (odd row stride FK2::PX, conflict-free).
+// The PCG vectors of these contexts are stored y fastest with a zero pad at each end
+// of every y column (PLay, off = 1), so the halo box (HY, HZ, HX, 4 modes) starts at
+// the even y index ey0 (fp64 TMA tile loads need a 16-byte-aligned innermost start:
+// an odd start faults) and lands as [m][hx][hz][hy], the pencil layout; step 0 copies
+// it into Ps with the padded qz stride (conflict-free pencil reads).
 template <int TX, int TY, int TZ>
 struct FKT {
   using F = FK2<TX, TY, TZ>;
   static constexpr int HX = TX + 2, HY = TY + 2, HZ = TZ + 2;
-  static constexpr int BXW = TX + 4, NB = BXW * HY * HZ;  // raw box (BXW, HY, HZ, 4)
+  static_assert(HY % 2 == 0 && TY % 2 == 0, "16-byte box rows, even y start");
+  static constexpr int NB = HX * HY * HZ;  // raw box (HY, HZ, HX) per mode
   static constexpr unsigned PBYTES = 4u * NB * 8u;
   // Ps[m][qx][qz][qy]: a pencil's (qy, qz) row is the fastest index, so the lanes of a
   // pencil class (consecutive qy) read consecutive words
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
              const __grid_constant__ CUtensorMap tm_minv, const double* __restrict__ XT,
              double* __restrict__ pnew, double* __restrict__ q, Geo G, double sB, int mode, int it, int ctl,
              const double* __restrict__ rzp, int nrz, double* rz_hist, const double* pq_hist, int* stop,
-             double* pqp) {
+             double* pqp, PLay L) {
   using F = FK2<TX, TY, TZ>;
   using K = FKT<TX, TY, TZ>;
 #ifdef WB_KPROF
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
   // below stays a shared-space access (LDS/STS), not a generic one
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sb = smraw;
-  double* Pb = (double*)(sb + K::OFF_P);  // raw boxes (BXW x HY x HZ x 4)
+  double* Pb = (double*)(sb + K::OFF_P);  // raw boxes [m][hx][hz][hy]
   double* Zb = (double*)(sb + K::OFF_R);  // z = Minv r (ZB), else r
   double* Mb = (double*)(sb + K::OFF_M);  // Minv (!ZB)
   constexpr unsigned RAWB = (ZB ? 2u : 3u) * K::PBYTES;
@@ -236,9 +238,9 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
       int ex0, ey0, ez0;
       coords(tile, ex0, ey0, ez0);
       mbar_expect_tx(&bar[0], RAWB);
-      tma_load_4d(Zb, &tm_z, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
-      if (!ZB) tma_load_4d(Mb, &tm_minv, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
-      tma_load_4d(Pb, &tm_pold, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
+      tma_load_4d(Zb, &tm_z, ey0, ez0 - 1, ex0 - 1, 0, &bar[0]);  // y from ey0 - 1 + pad
+      if (!ZB) tma_load_4d(Mb, &tm_minv, ey0, ez0 - 1, ex0 - 1, 0, &bar[0]);
+      tma_load_4d(Pb, &tm_pold, ey0, ez0 - 1, ex0 - 1, 0, &bar[0]);
       mbar_expect_tx(&bar[2], K::XBYTES);
       bulk_load(Xs, XT + (size_t)tile * K::XTB, K::XBYTES, &bar[2]);
     }
@@ -286,33 +288,25 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     // tile's own p_new)
     mbar_wait(&bar[0], ph);
     lap(1);
-    // walk the raw box in its own order (lane-consecutive reads); box column b holds halo
-    // element b - 1, columns 0 and BXW - 1 are padding.  With BXW = 8 a half-warp covers
-    // two box rows, and its Ps stores (stride QS * HZ per column) hit 16 distinct bank pairs.
-    for (int i = threadIdx.x; i < ((dbg & 0x400) ? 0 : K::NB); i += F::NTH) {
-      const int b = i % K::BXW, r = i / K::BXW, hy = r % K::HY, hz = r / K::HY;
-      if (b < 1 || b > K::HX) continue;
-      const int hx = b - 1;
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int j = m * K::NB + i;
-        double v;
-        if (mode == 2) v = Pb[j];
-        else {
-          const double z = ZB ? Zb[j] : Mb[j] * Zb[j];
-          v = (mode == 1) ? fma(beta, Pb[j], z) : z;
-        }
-        Ps[m * K::NHP + K::pidx(hx, hy, hz)] = v;
+    // the raw box is [m][hx][hz][hy] = Ps's order with row length HY instead of QS:
+    // a flat, lane-consecutive walk
+    for (int j = threadIdx.x; j < ((dbg & 0x400) ? 0 : 4 * K::NB); j += F::NTH) {
+      double v;
+      if (mode == 2) v = Pb[j];
+      else {
+        const double z = ZB ? Zb[j] : Mb[j] * Zb[j];
+        v = (mode == 1) ? fma(beta, Pb[j], z) : z;
       }
+      Ps[K::QS * (j / K::HY) + j % K::HY] = v;
     }
     __syncthreads();
     lap(2);
     if (threadIdx.x == K::TMA_T && next < n_tiles) {  // raw p, r, Minv buffers are free
       fence_proxy_async();
       mbar_expect_tx(&bar[0], RAWB);
-      tma_load_4d(Zb, &tm_z, nx0 - 2, ny0 - 1, nz0 - 1, 0, &bar[0]);
-      if (!ZB) tma_load_4d(Mb, &tm_minv, nx0 - 2, ny0 - 1, nz0 - 1, 0, &bar[0]);
-      tma_load_4d(Pb, &tm_pold, nx0 - 2, ny0 - 1, nz0 - 1, 0, &bar[0]);
+      tma_load_4d(Zb, &tm_z, ny0, nz0 - 1, nx0 - 1, 0, &bar[0]);
+      if (!ZB) tma_load_4d(Mb, &tm_minv, ny0, nz0 - 1, nx0 - 1, 0, &bar[0]);
+      tma_load_4d(Pb, &tm_pold, ny0, nz0 - 1, nx0 - 1, 0, &bar[0]);
     }
     lap(7);
     // 1. t at the tile nodes by x-pencils
@@ -371,8 +365,9 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
         for (int m = 0; m < 4; ++m) {
           const double o = sB * qm[m];
           const double pv = Ps[m * K::NHP + h];
-          if (!(dbg & 0x800)) q[m * ne + e] = o;
-          if (!(dbg & 0x1000)) pnew[m * ne + e] = pv;
+          const int64_t j = L.at(m, ex, ey, ez);
+          if (!(dbg & 0x800)) q[j] = o;
+          if (!(dbg & 0x1000)) pnew[j] = pv;
           dot = fma(pv, o, dot);
         }
       }

@@ -19,6 +19,24 @@ struct Geo {
   int64_t n_el, n_nodes, n_p;
 };
 
+// Storage of the mode-major PCG vectors (x, r, p, q, z, Minv): entry (m, e) of element
+// e = ex + N (ey + N ez) at  m sm + ex sx + ez sz + (ey + off) sy.  Default (off = 0):
+// sm = n_el, sx = 1, sy = N, sz = N^2, i.e. m n_el + e.  The TMA Poisson kernel's contexts
+// store y fastest with one zero pad at each end of every y column (off = 1, sy = 1,
+// sz = N + 2, sx = N (N + 2), sm = N^2 (N + 2)): its halo boxes then land in the pencil
+// layout.  n = storage length (4 sm for k = 2); pads stay 0 (every update maps 0 to 0).
+struct PLay {
+  int64_t sm, sx, sy, sz, n;
+  int off;
+  __host__ __device__ int64_t at(int m, int ex, int ey, int ez) const {
+    return m * sm + ex * sx + ez * sz + (ey + off) * sy;
+  }
+  __host__ __device__ int64_t at(int m, int64_t e, int N) const {
+    const int ex = (int)(e % N), ey = (int)((e / N) % N), ez = (int)(e / ((int64_t)N * N));
+    return at(m, ex, ey, ez);
+  }
+};
+
 template <int K> struct Ord {
   static constexpr int n1 = K + 1, NQ = n1 * n1 * n1, NM = K * (K + 1) * (K + 2) / 6;
 };
@@ -148,13 +166,13 @@ __global__ void __launch_bounds__(BS) k_absmax(const double* __restrict__ v, int
 // row of K, e.g. the constant mode on the N = 1 mesh), get Minv = 0.
 // d element-major (ABI layout), minv mode-major (PCG layout): minv[m*ne + e].
 __global__ void k_minv(const double* __restrict__ d, double* __restrict__ minv, int64_t ne, int nm,
-                       const double* __restrict__ dmax) {
+                       const double* __restrict__ dmax, PLay L, int N) {
   const double thr = 1e-13 * *dmax;
   const int64_t n = ne * nm;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = i / ne, e = i % ne;
     const double v = d[e * nm + m];
-    minv[i] = fabs(v) > thr ? 1.0 / v : 0.0;
+    minv[L.at((int)m, e, N)] = fabs(v) > thr ? 1.0 / v : 0.0;
   }
 }
 
@@ -748,16 +766,17 @@ __device__ __forceinline__ bool pcg_control(int i, const double* __restrict__ rz
 // z = Minv r stored when z != NULL (the TMA Poisson kernel reads it).
 __global__ void __launch_bounds__(VBS) k_pcg_init(const double* __restrict__ b, const double* __restrict__ bsum,
                                                   double* x, double* r, const double* __restrict__ Minv, int64_t ne,
-                                                  int nm, double* rzp, double* z) {
+                                                  int nm, double* rzp, double* z, PLay L, int N) {
   const double mean = *bsum / (double)ne;
   const int64_t n = ne * nm;
   double s = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS) {
     const int64_t m = i / ne, e = i % ne;
+    const int64_t j = L.at((int)m, e, N);
     const double bi = (m == 0) ? b[e * nm] - mean : b[e * nm + m];
-    x[i] = 0.0; r[i] = bi;
-    const double zi = Minv[i] * bi;
-    if (z) z[i] = zi;
+    x[j] = 0.0; r[j] = bi;
+    const double zi = Minv[j] * bi;
+    if (z) z[j] = zi;
     s = fma(bi, zi, s);
   }
   store_partial<VBS>(s, rzp);
@@ -847,23 +866,26 @@ __global__ void __launch_bounds__(VBS) k_pcg_upd(double* x, double* r, const dou
 
 // out (element-major) = P x (mode-major), xsum = sum of the constant-mode entries.
 __global__ void k_pcg_out(const double* __restrict__ x, const double* __restrict__ xsum, double* __restrict__ out,
-                          int64_t ne, int nm) {
+                          int64_t ne, int nm, PLay L, int N) {
   const double mean = *xsum / (double)ne;
   const int64_t n = ne * nm;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i / nm, m = i % nm;
-    const double v = x[m * ne + e];
+    const double v = x[L.at((int)m, e, N)];
     out[i] = (m == 0) ? v - mean : v;
   }
 }
 
 // layout conversion element-major <-> mode-major (debug one-step entry)
-__global__ void k_transpose(const double* __restrict__ in, double* __restrict__ out, int64_t ne, int nm, int to_soa) {
+// element-major [e*nm + m] <-> PCG storage (PLay); to_soa: element-major -> PCG
+__global__ void k_transpose(const double* __restrict__ in, double* __restrict__ out, int64_t ne, int nm, int to_soa,
+                            PLay L, int N) {
   const int64_t n = ne * nm;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = i / ne, e = i % ne;
-    if (to_soa) out[i] = in[e * nm + m];
-    else out[e * nm + m] = in[i];
+    const int64_t j = L.at((int)m, e, N);
+    if (to_soa) out[j] = in[e * nm + m];
+    else out[e * nm + m] = in[j];
   }
 }
 

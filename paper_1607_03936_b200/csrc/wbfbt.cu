@@ -41,6 +41,8 @@ struct wb_ctx {
   // PCG vectors, mode-major v[m*n_el + e]: x, r, p (double buffer), q
   double *px = nullptr, *pr = nullptr, *pp = nullptr, *pp1 = nullptr, *pq = nullptr;
   double* pz = nullptr;  // z = Minv r, stored by the PCG init/update kernels for the TMA Poisson kernel
+  PLay pl = {};        // storage of the PCG vectors (kernels.cuh)
+  bool ylay = false;   // y-fastest padded PCG storage: contexts of the TMA Poisson kernel
   // CUDA graphs of the PCG iteration loop, keyed by (side, iters)
   struct GraphEntry { int side = 0, iters = 0; long long n_launch = 0; cudaGraphExec_t exec = nullptr; };
   static constexpr int MAX_GRAPHS = 8;
@@ -76,7 +78,7 @@ struct wb_ctx {
   // measured and gave no gain)
   double* slab = nullptr;
   CUtensorMap tm_pp, tm_pp1, tm_pz, tm_pr, tm_mL, tm_mR;
-  int kz = 1;  // TMA Poisson kernel: 1 = z = Minv r stored by the PCG update and loaded as one box (default)
+  int kz = 0;  // TMA Poisson kernel: 1 = z = Minv r stored by the PCG update and loaded as one box; 0 = r + Minv boxes (default: faster with the y-fastest storage)
   int k_dbg = 0;  // timing probe bits for the fused K kernel (results invalid when nonzero)
   // profiling: CUDA-event pairs around every Poisson-operator launch (direct launches)
   int profile = 0;
@@ -266,7 +268,7 @@ wb_status run_k2f(wb_ctx* c, const double* pold, double* pnew, const double* r, 
       auto kern = c->kz ? k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, true> : k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, false>;
       kern<<<grid, FK2<TMA_TX, TMA_TY, TMA_TZ>::NTH, KT::SMEM, c->stream>>>(
           *tp, *tz, *tm, xt, pnew, q, c->G, c->sB, mode | c->k_dbg, a.it, a.ctl, c->rzp, c->red_blocks, rz_hist(c),
-          pq_hist(c), c->stop, c->pqp);
+          pq_hist(c), c->stop, c->pqp, c->pl);
       LAUNCH_CHECK(c);
       *npq = grid;
       return WB_OK;
@@ -293,18 +295,21 @@ bool get_encode() {
   return true;
 }
 // mode-major PCG vector [m][ez][ey][ex]: 4-D map, box = one tile + halo, all modes
+// PCG vector in the y-fastest padded storage (PLay, off = 1): 4-D map (y incl. pads, z, x,
+// mode), box = the tile's halo (HY, HZ, HX) for all modes
 bool make_tm_vec(CUtensorMap* tm, const double* base, int N, int nm) {
   using KT = FKT<TMA_TX, TMA_TY, TMA_TZ>;
-  const cuuint64_t dims[4] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)nm};
-  const cuuint64_t strides[3] = {(cuuint64_t)N * 8, (cuuint64_t)N * N * 8, (cuuint64_t)N * N * N * 8};
-  const cuuint32_t box[4] = {(cuuint32_t)KT::BXW, (cuuint32_t)KT::HY, (cuuint32_t)KT::HZ, (cuuint32_t)nm};
+  const cuuint64_t ny = (cuuint64_t)N + 2;
+  const cuuint64_t dims[4] = {ny, (cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)nm};
+  const cuuint64_t strides[3] = {ny * 8, ny * N * 8, ny * N * N * 8};
+  const cuuint32_t box[4] = {(cuuint32_t)KT::HY, (cuuint32_t)KT::HZ, (cuuint32_t)KT::HX, (cuuint32_t)nm};
   const cuuint32_t es[4] = {1, 1, 1, 1};
   return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 bool setup_tma(wb_ctx* c) {
-  if (c->k != 2 || (c->N & 1) || !get_encode()) return false;
+  if (!c->ylay) return false;
   const size_t bx = sizeof(double) * (size_t)xt_len(c->N);
   if (!c->slab && (cudaMalloc(&c->XpL, bx) != cudaSuccess || cudaMalloc(&c->XpR, bx) != cudaSuccess)) {
     cudaGetLastError();
@@ -406,7 +411,7 @@ wb_status run_K_pcg(wb_ctx* c, int side, int mode, const double* pold, double* p
   const double* p = pold;
   const int* stop = a.ctl ? c->stop + a.it : nullptr;
   if (mode != 2) {
-    k_pupd<<<c->red_blocks, VBS, 0, c->stream>>>(pnew, pold, r, Minv, c->n_p, mode, a.it, a.ctl, c->rzp,
+    k_pupd<<<c->red_blocks, VBS, 0, c->stream>>>(pnew, pold, r, Minv, c->pl.n, mode, a.it, a.ctl, c->rzp,
                                                  c->red_blocks, rz_hist(c), pq_hist(c), c->stop);
     LAUNCH_CHECK(c);
     p = pnew;
@@ -436,7 +441,7 @@ wb_status pcg_loop_direct(wb_ctx* c, int side, int iters) {
     wb_status s = run_K_pcg(c, side, it == 0 ? 0 : 1, PB[(it + 1) & 1], PB[it & 1], c->pr, c->pq, a, &pcur, &npq);
     if (s) return s;
     if (prof) CUDA_TRY(c, cudaEventRecord(c->prof_ev[2 * c->prof_n++ + 1], c->stream));
-    k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->n_p, it, c->pqp, npq,
+    k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->pl.n, it, c->pqp, npq,
                                                     rz_hist(c), pq_hist(c), c->stop, c->rzp,
                                                     z_out(c));
     LAUNCH_CHECK(c);
@@ -490,25 +495,25 @@ wb_status run_poisson(wb_ctx* c, int side, const double* b, double* x, int iters
   k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->n_el, c->nm, c->partial, c->counter, c->scal + S_SUM);
   LAUNCH_CHECK(c);
   k_pcg_init<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->scal + S_SUM, c->px, c->pr, Minv, c->n_el, c->nm, c->rzp,
-                                                   z_out(c));
+                                                   z_out(c), c->pl, c->N);
   LAUNCH_CHECK(c);
   if ((s = pcg_loop(c, side, iters))) return s;
-  k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->n_el, 1, c->partial, c->counter, c->scal + S_SUM + 1);
+  k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pl.sm, 1, c->partial, c->counter, c->scal + S_SUM + 1);
   LAUNCH_CHECK(c);
-  k_pcg_out<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->scal + S_SUM + 1, x, c->n_el, c->nm);
+  k_pcg_out<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->scal + S_SUM + 1, x, c->n_el, c->nm, c->pl, c->N);
   LAUNCH_CHECK(c);
   return WB_OK;
 }
 
 // q = K_side p, element-major in and out (through the PCG kernels, mode "p as is")
 wb_status run_K(wb_ctx* c, int side, const double* p, double* q) {
-  k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(p, c->pp, c->n_el, c->nm, 1);
+  k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(p, c->pp, c->n_el, c->nm, 1, c->pl, c->N);
   LAUNCH_CHECK(c);
   const double* pcur = nullptr;
   int npq = 0;
   wb_status s = run_K_pcg(c, side, 2, c->pp, c->pp1, nullptr, c->pq, PcgArgs{}, &pcur, &npq);
   if (s) return s;
-  k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(c->pq, q, c->n_el, c->nm, 0);
+  k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(c->pq, q, c->n_el, c->nm, 0, c->pl, c->N);
   LAUNCH_CHECK(c);
   return WB_OK;
 }
@@ -651,9 +656,18 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
     if (ok && cudaMalloc(p, sizeof(double) * (size_t)(n > 0 ? n : 1)) != cudaSuccess) ok = false;
   };
   alloc(&c->Cw, c->n_nodes); alloc(&c->Dw, c->n_nodes); alloc(&c->Cinv, c->n_nodes); alloc(&c->Dinv, c->n_nodes);
+  // PCG vector storage: y fastest with zero pads for the TMA Poisson kernel (k = 2, even N,
+  // large meshes, tensor-map encoder available), else mode-major m n_el + e
+  c->ylay = k == 2 && !(N & 1) && c->n_el >= 148 * 256 * 2 && get_encode();
+  if (c->ylay) {
+    const int64_t sz = N + 2, sx = (int64_t)N * sz, sm = (int64_t)N * sx;
+    c->pl = PLay{sm, sx, 1, sz, c->nm * sm, 1};
+  } else {
+    c->pl = PLay{c->n_el, 1, N, (int64_t)N * N, c->n_p, 0};
+  }
   if (k == 2 && !(N & 1)) {
     auto up = [](int64_t n) { return (n + 31) & ~(int64_t)31; };  // 256-byte sub-arrays
-    const int64_t np = up(c->n_p), nx = up(xt_len(N));
+    const int64_t np = up(c->pl.n), nx = up(xt_len(N));
     if (ok && cudaMalloc(&c->slab, sizeof(double) * (size_t)(8 * np + 2 * nx)) != cudaSuccess) ok = false;
     if (ok) {
       double* q = c->slab;
@@ -661,6 +675,8 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
       c->px = q; q += np; c->pr = q; q += np; c->pp = q; q += np; c->pp1 = q; q += np; c->pq = q; q += np;
       c->pz = q; q += np;
       c->MinvR = q; q += np; c->XpR = q;
+      // zero: the pads of the y-fastest storage stay 0 for good
+      if (cudaMemsetAsync(c->slab, 0, sizeof(double) * (size_t)(8 * np + 2 * nx), c->stream) != cudaSuccess) ok = false;
     }
   }
   alloc(&c->dKl, c->n_p); alloc(&c->dKr, c->n_p);
@@ -703,7 +719,12 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
     delete c;
     return WB_ECUDA;
   }
-  c->tma_ok = setup_tma(c);  // optional fast path; the pointer kernel serves when unavailable
+  c->tma_ok = setup_tma(c);  // the pointer kernel serves contexts without the y-fastest storage
+  if (c->ylay && !c->tma_ok) {
+    free_all(c);
+    delete c;
+    return WB_ECUDA;
+  }
   *out = c;
   return WB_OK;
 }
@@ -812,7 +833,8 @@ static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
     double* dmax = c->scal + S_DMAX + side;
     k_absmax<VBS><<<c->red_blocks, VBS, 0, c->stream>>>(d, c->n_p, c->partial, c->counter, dmax);
     LAUNCH_CHECK(c);
-    k_minv<<<c->red_blocks, VBS, 0, c->stream>>>(d, side == 0 ? c->MinvL : c->MinvR, c->n_el, c->nm, dmax);
+    k_minv<<<c->red_blocks, VBS, 0, c->stream>>>(d, side == 0 ? c->MinvL : c->MinvR, c->n_el, c->nm, dmax, c->pl,
+                                                 c->N);
     LAUNCH_CHECK(c);
   }
   c->have_visc = true;
@@ -982,7 +1004,7 @@ wb_status wb_debug_pcg_step(wb_ctx* c, int side, double* x, double* r, double* p
   // state in (element-major -> mode-major), rz as rz_1, iteration index 1
   for (int i = 0; i < 3; ++i) {
     k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(i == 0 ? x : (i == 1 ? r : p), i == 0 ? c->px : (i == 1 ? c->pr : c->pp),
-                                                      c->n_el, c->nm, 1);
+                                                      c->n_el, c->nm, 1, c->pl, c->N);
     LAUNCH_CHECK(c);
   }
   CUDA_TRY(c, cudaMemcpyAsync(rz_hist(c) + 1, rz, sizeof(double), cudaMemcpyHostToDevice, c->stream));
@@ -992,17 +1014,17 @@ wb_status wb_debug_pcg_step(wb_ctx* c, int side, double* x, double* r, double* p
   PcgArgs a;
   a.it = 1; a.ctl = 0;  // rz_1 and stop_1 given
   if ((s = run_K_pcg(c, side, 2, c->pp, c->pp1, c->pr, c->pq, a, &pcur, &npq))) return s;
-  k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->n_p, 1, c->pqp, npq,
+  k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->pl.n, 1, c->pqp, npq,
                                                   rz_hist(c), pq_hist(c), c->stop, c->rzp, nullptr);
   LAUNCH_CHECK(c);
   // p = Minv r + (rz_2 / rz_1) p with the control of iteration 2 (records rz_2)
   double* pc = const_cast<double*>(pcur);
-  k_pupd<<<c->red_blocks, VBS, 0, c->stream>>>(pc, pc, c->pr, Minv, c->n_p, 1, 2, 1, c->rzp, c->red_blocks,
+  k_pupd<<<c->red_blocks, VBS, 0, c->stream>>>(pc, pc, c->pr, Minv, c->pl.n, 1, 2, 1, c->rzp, c->red_blocks,
                                                rz_hist(c), pq_hist(c), c->stop);
   LAUNCH_CHECK(c);
   for (int i = 0; i < 3; ++i) {
     k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(i == 0 ? c->px : (i == 1 ? c->pr : pc), i == 0 ? x : (i == 1 ? r : p),
-                                                      c->n_el, c->nm, 0);
+                                                      c->n_el, c->nm, 0, c->pl, c->N);
     LAUNCH_CHECK(c);
   }
   CUDA_TRY(c, cudaMemcpyAsync(rz, rz_hist(c) + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -1173,6 +1195,8 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
     clear_graphs(c);
   } else if (!strcmp(key, "tma")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "tma must be 0 or 1");
+    if (c->ylay && value == 0.0)
+      return set_err(c, WB_EINVAL, "this context's PCG storage is the TMA kernel's (y fastest): tma must stay 1");
     c->use_tma = (int)value;
     clear_graphs(c);
   } else if (!strcmp(key, "k_dbg")) {  // timing probe only: 0x100 / 0x200 / 0x400 skip phases
