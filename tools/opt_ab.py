@@ -10,7 +10,7 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 from paper_1607_03936_b200 import Context  # noqa: E402
 
-inp = synth.make_inputs(sys.argv[1], 0)
+inp = synth.make_inputs(sys.argv[1], 0, N=int(os.environ["AB_N"]) if os.environ.get("AB_N") else None)
 c = Context(inp["N"], inp["k"])
 d = lambda a: torch.as_tensor(a, dtype=torch.float64, device="cuda")  # noqa: E731
 mu, p = d(inp["mu_q"]), d(inp["p"])
@@ -38,4 +38,5 @@ for setting in sys.argv[2:]:
     per = (t_us(50) - t_us(10)) / 40
     out = pv.clone()
     ref = out if ref is None else ref
-    print(f"{setting:30s}: per PCG iteration {per:7.2f} us  (max rel diff vs first {float((out - ref).abs().max() / ref.abs().max()):.1e})")
+    print(f"N={inp['N']} {setting:24s}: per PCG iteration {per:7.2f} us = {per * 1e3 / inp['N'] ** 3:.3f} ns/element"
+          f"  (max rel diff vs first {float((out - ref).abs().max() / ref.abs().max()):.1e})")
