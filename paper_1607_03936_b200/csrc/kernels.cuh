@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(BS) k_B(const double* __restrict__ u, const do
 template <int K>
 __global__ void k_BT_elem(const double* __restrict__ p, double* __restrict__ E, Geo G, double sB,
                           const int* __restrict__ stop, int64_t se, int64_t sm) {
-  constexpr int n1 = K + 1, NQ = Ord<K>::NQ, NM = Ord<K>::NM;
+  constexpr int n1 = K + 1, NQ = Ord<K>::NQ;
   if (stop && *stop) return;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= G.n_el) return;
