@@ -222,7 +222,6 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
   double* T = (double*)(sb + K::OFF_T);
   uint64_t* bar = (uint64_t*)(sb + K::OFF_B);  // [0] r+Minv, [1] p_old, [2] X
   const int N = G.N;
-  const int64_t ne = G.n_el;
   const int NTX = (N + TX - 1) / TX, NTY = (N + TY - 1) / TY, NTZ = (N + TZ - 1) / TZ;
   const int n_tiles = NTX * NTY * NTZ;
   auto coords = [&](int tile, int& ex0, int& ey0, int& ez0) {
@@ -359,7 +358,6 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
               if (w2_nz(c, ay, az, 1)) qm[2] = fma(c_W2[c][ay][az][1], s0, qm[2]);
               if (w2_nz(c, ay, az, 2)) qm[3] = fma(c_W2[c][ay][az][2], s0, qm[3]);
             }
-        const int64_t e = ex + (int64_t)N * (ey + (int64_t)N * ez);
         const int h = K::pidx(lx + 1, ly + 1, lz + 1);
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
