@@ -810,38 +810,81 @@ __global__ void __launch_bounds__(VBS) k_pupd(double* pout, const double* pin, c
 // moves pairs (double2) and keeps U pairs of all five inputs in flight before any
 // arithmetic; the first batch is issued before the pq reduction, which only the
 // arithmetic needs.  The rz partial of a thread sums its entries in index order.
-template <int U>
+// Solution-update forms of k_pcg_upd (all bitwise equal to updating every iteration):
+//   XU_SINGLE: x = fma(alpha_i, p_i, x)
+//   XU_DEFER:  x untouched (even iterations of a loop; the next odd one applies it)
+//   XU_PAIR:   x = fma(alpha_i, p_i, fma(alpha_{i-1}, p_{i-1}, x))  (odd iterations)
+// p_{i-1} is still in the other direction buffer, so x is read and written every other
+// iteration only.  k_pcg_xfin applies a deferred last update after the loop.
+enum { XU_SINGLE = 0, XU_DEFER = 1, XU_PAIR = 2 };
+template <int U, int XM>
 __device__ __forceinline__ void pcg_upd_batch(int64_t j0, int64_t stride, int64_t n2, const double2* x,
-                                              const double2* r, const double2* p, const double2* q,
-                                              const double2* M, double2 (&X)[U], double2 (&R)[U],
-                                              double2 (&P)[U], double2 (&Q)[U], double2 (&Mv)[U]) {
+                                              const double2* r, const double2* p, const double2* pp,
+                                              const double2* q, const double2* M, double2 (&X)[U],
+                                              double2 (&R)[U], double2 (&P)[U], double2 (&PP)[U], double2 (&Q)[U],
+                                              double2 (&Mv)[U]) {
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const int64_t j = j0 + u * stride;
-    if (j < n2) { X[u] = x[j]; R[u] = r[j]; P[u] = p[j]; Q[u] = __ldcg(q + j); Mv[u] = M[j]; }
+    if (j < n2) {
+      if (XM != XU_DEFER) { X[u] = x[j]; P[u] = p[j]; }
+      if (XM == XU_PAIR) PP[u] = pp[j];
+      R[u] = r[j]; Q[u] = __ldcg(q + j); Mv[u] = M[j];
+    }
   }
 }
+// iteration j made an update: not stopped and pq_j != 0 (pq_hist[j] is only valid then)
+__device__ __forceinline__ double pcg_alpha(int j, const double* rz_hist, const double* pq_hist, const int* stop) {
+  return (j >= 0 && stop[j] == 0 && pq_hist[j] != 0.0) ? rz_hist[j] / pq_hist[j] : 0.0;
+}
+// x = fma(alpha_j, p_j, x) if iteration j made an update (grid-stride)
+__device__ __forceinline__ void pcg_x_single(double* x, const double* p, int64_t n, double a) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    x[k] = fma(a, p[k], x[k]);
+}
+
+// iteration i: pq_i = sum of the K kernel's <p_i, q> partials (pqp, npq);
+// alpha = rz_i / pq_i; x update (XM above); r -= alpha q; partials of
+// rz_{i+1} = <r, Minv r> -> rzp; z = Minv r stored when z != NULL.  Block 0
+// records pq_hist[i].
+// Streaming: the vectors are 16-byte aligned (cudaMalloc, n even), so each thread
+// moves pairs (double2) and keeps U pairs of all inputs in flight before any
+// arithmetic; the first batch is issued before the pq reduction, which only the
+// arithmetic needs.  The rz partial of a thread sums its entries in index order.
+template <int XM>
 __global__ void __launch_bounds__(VBS) k_pcg_upd(double* x, double* r, const double* __restrict__ p,
-                                                 const double* __restrict__ q, const double* __restrict__ Minv,
-                                                 int64_t n, int i, const double* __restrict__ pqp, int npq,
-                                                 const double* rz_hist, double* pq_hist, const int* stop,
-                                                 double* rzp, double* z) {
+                                                 const double* __restrict__ pprev, const double* __restrict__ q,
+                                                 const double* __restrict__ Minv, int64_t n, int i,
+                                                 const double* __restrict__ pqp, int npq, const double* rz_hist,
+                                                 double* pq_hist, const int* stop, double* rzp, double* z) {
   constexpr int U = 2;
-  if (stop[i]) return;
-  const int64_t n2 = n / 2;  // n = 4 n_el is even
+  if (stop[i]) {
+    // a stopped odd iteration still owes the previous (even) iteration's deferred update
+    if (XM == XU_PAIR) {
+      const double ap = pcg_alpha(i - 1, rz_hist, pq_hist, stop);
+      if (ap != 0.0) pcg_x_single(x, pprev, n, ap);
+    }
+    return;
+  }
+  const int64_t n2 = n / 2;  // n is even
   const int64_t stride = (int64_t)gridDim.x * VBS;
   double2* x2 = reinterpret_cast<double2*>(x);
   double2* r2 = reinterpret_cast<double2*>(r);
   double2* z2 = reinterpret_cast<double2*>(z);
   const double2* p2 = reinterpret_cast<const double2*>(p);
+  const double2* pp2 = reinterpret_cast<const double2*>(pprev);
   const double2* q2 = reinterpret_cast<const double2*>(q);
   const double2* M2 = reinterpret_cast<const double2*>(Minv);
-  double2 X[U], R[U], P[U], Q[U], Mv[U];
+  double2 X[U], R[U], P[U], PP[U], Q[U], Mv[U];
   int64_t j0 = (int64_t)blockIdx.x * VBS + threadIdx.x;
-  pcg_upd_batch<U>(j0, stride, n2, x2, r2, p2, q2, M2, X, R, P, Q, Mv);
+  pcg_upd_batch<U, XM>(j0, stride, n2, x2, r2, p2, pp2, q2, M2, X, R, P, PP, Q, Mv);
+  const double ap = XM == XU_PAIR ? pcg_alpha(i - 1, rz_hist, pq_hist, stop) : 0.0;
   const double pq = sum_partials<VBS>(pqp, npq);
   if (blockIdx.x == 0 && threadIdx.x == 0) pq_hist[i] = pq;
-  if (pq == 0.0) return;
+  if (pq == 0.0) {
+    if (XM == XU_PAIR && ap != 0.0) pcg_x_single(x, pprev, n, ap);  // (no update of its own)
+    return;
+  }
   const double alpha = rz_hist[i] / pq;
   double s = 0.0;
   for (; j0 < n2; j0 += U * stride) {
@@ -849,19 +892,35 @@ __global__ void __launch_bounds__(VBS) k_pcg_upd(double* x, double* r, const dou
     for (int u = 0; u < U; ++u) {
       const int64_t j = j0 + u * stride;
       if (j < n2) {
-        double2 xo, ro, zo;
-        xo.x = fma(alpha, P[u].x, X[u].x); xo.y = fma(alpha, P[u].y, X[u].y);
+        double2 ro, zo;
+        if (XM == XU_SINGLE) {
+          double2 xo;
+          xo.x = fma(alpha, P[u].x, X[u].x); xo.y = fma(alpha, P[u].y, X[u].y);
+          x2[j] = xo;
+        } else if (XM == XU_PAIR) {
+          double2 xo;
+          xo.x = fma(alpha, P[u].x, fma(ap, PP[u].x, X[u].x));
+          xo.y = fma(alpha, P[u].y, fma(ap, PP[u].y, X[u].y));
+          x2[j] = xo;
+        }
         ro.x = fma(-alpha, Q[u].x, R[u].x); ro.y = fma(-alpha, Q[u].y, R[u].y);
         zo.x = Mv[u].x * ro.x; zo.y = Mv[u].y * ro.y;
-        x2[j] = xo; r2[j] = ro;
+        r2[j] = ro;
         if (z) z2[j] = zo;
         s = fma(ro.x, zo.x, s);
         s = fma(ro.y, zo.y, s);
       }
     }
-    pcg_upd_batch<U>(j0 + U * stride, stride, n2, x2, r2, p2, q2, M2, X, R, P, Q, Mv);
+    pcg_upd_batch<U, XM>(j0 + U * stride, stride, n2, x2, r2, p2, pp2, q2, M2, X, R, P, PP, Q, Mv);
   }
   store_partial<VBS>(s, rzp);
+}
+
+// after a loop whose last iteration i deferred its update: x = fma(alpha_i, p_i, x)
+__global__ void __launch_bounds__(VBS) k_pcg_xfin(double* x, const double* __restrict__ p, int64_t n, int i,
+                                                  const double* rz_hist, const double* pq_hist, const int* stop) {
+  const double a = pcg_alpha(i, rz_hist, pq_hist, stop);
+  if (a != 0.0) pcg_x_single(x, p, n, a);
 }
 
 // out (element-major) = P x (mode-major), xsum = sum of the constant-mode entries.

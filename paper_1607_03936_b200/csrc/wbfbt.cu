@@ -427,6 +427,7 @@ wb_status run_K_pcg(wb_ctx* c, int side, int mode, const double* pold, double* p
 wb_status pcg_loop_direct(wb_ctx* c, int side, int iters) {
   const double* Minv = side == 0 ? c->MinvL : c->MinvR;
   double* PB[2] = {c->pp, c->pp1};
+  const double* pprev = nullptr;  // p_{it-1}: K reads it, writes p_it into the other buffer
   for (int it = 0; it < iters; ++it) {
     const double* pcur = nullptr;
     const bool prof = c->profile && c->prof_n < wb_ctx::PROF_MAX;
@@ -441,9 +442,21 @@ wb_status pcg_loop_direct(wb_ctx* c, int side, int iters) {
     wb_status s = run_K_pcg(c, side, it == 0 ? 0 : 1, PB[(it + 1) & 1], PB[it & 1], c->pr, c->pq, a, &pcur, &npq);
     if (s) return s;
     if (prof) CUDA_TRY(c, cudaEventRecord(c->prof_ev[2 * c->prof_n++ + 1], c->stream));
-    k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->pl.n, it, c->pqp, npq,
-                                                    rz_hist(c), pq_hist(c), c->stop, c->rzp,
-                                                    z_out(c));
+    // x updates in pairs (odd iterations), bitwise equal to every iteration (kernels.cuh)
+    if (it & 1)
+      k_pcg_upd<XU_PAIR><<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, pprev, c->pq, Minv, c->pl.n, it,
+                                                               c->pqp, npq, rz_hist(c), pq_hist(c), c->stop,
+                                                               c->rzp, z_out(c));
+    else
+      k_pcg_upd<XU_DEFER><<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, pprev, c->pq, Minv, c->pl.n,
+                                                                it, c->pqp, npq, rz_hist(c), pq_hist(c), c->stop,
+                                                                c->rzp, z_out(c));
+    LAUNCH_CHECK(c);
+    pprev = pcur;
+  }
+  if (iters > 0 && !((iters - 1) & 1)) {  // the last iteration was even: its update is pending
+    k_pcg_xfin<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, pprev, c->pl.n, iters - 1, rz_hist(c),
+                                                     pq_hist(c), c->stop);
     LAUNCH_CHECK(c);
   }
   return WB_OK;
@@ -1014,7 +1027,8 @@ wb_status wb_debug_pcg_step(wb_ctx* c, int side, double* x, double* r, double* p
   PcgArgs a;
   a.it = 1; a.ctl = 0;  // rz_1 and stop_1 given
   if ((s = run_K_pcg(c, side, 2, c->pp, c->pp1, c->pr, c->pq, a, &pcur, &npq))) return s;
-  k_pcg_upd<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, c->pq, Minv, c->pl.n, 1, c->pqp, npq,
+  k_pcg_upd<XU_SINGLE><<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, nullptr, c->pq, Minv, c->pl.n, 1,
+                                                             c->pqp, npq,
                                                   rz_hist(c), pq_hist(c), c->stop, c->rzp, nullptr);
   LAUNCH_CHECK(c);
   // p = Minv r + (rz_2 / rz_1) p with the control of iteration 2 (records rz_2)
