@@ -155,11 +155,14 @@ wb_status wb_get_jacobi(wb_ctx* ctx, double* diagKl, double* diagKr);
  * "last_alpha_beta" = alpha_{n-1}, "last_beta" = beta_{n-1} (WB_ESTATE without the
  * flag or before a solve, WB_EINVAL for i outside [0, n)), "kz" (1 if the PCG
  * update stores z = Minv r for the TMA Poisson kernel), "k_tma" (1 if
- * the k = 2 Poisson operator runs as the TMA kernel for this mesh). */
+ * the k = 2 Poisson operator runs as the TMA kernel for this mesh), "k_ws" (1 if
+ * it runs as the warp-specialised TMA kernel). */
 wb_status wb_query(wb_ctx* ctx, const char* key, double* value);
 /* Tuning knobs (results are identical up to rounding for every setting):
  * "kz" (k = 2 TMA Poisson kernel: 1 = the PCG update stores z = Minv r and the
  * kernel loads it as one box; 0 = it loads r and Minv, the default),
+ * "k_ws" (k = 2 TMA Poisson kernel: 1 = warp-specialised, producer warps build
+ * the next tile's direction box while the consumer warps apply B^T X^-1 B),
  * "graph" (1 = replay the PCG iteration loop as a CUDA graph, default; 0 =
  * plain launches), "profile" (1 = plain launches with a CUDA-event pair around
  * every Poisson-operator launch; wb_query "prof_k_ms" / "prof_k_count" read

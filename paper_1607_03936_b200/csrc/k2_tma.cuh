@@ -192,6 +192,71 @@ __device__ __forceinline__ void fkt_pencil(const double* __restrict__ Ps, double
       }
 }
 
+// step 1 of the warp-specialised kernel: one pencil per consumer thread.  Not inlined, so
+// the pencils get the registers to themselves (inlined into the tile loop, the loop state
+// of step 2 is kept live across them and they spill under the 15-warp register cap).
+template <int TX, int TY, int TZ>
+__device__ __noinline__ void fkt_step1(const double* __restrict__ Pc, double* __restrict__ T,
+                                       const double* __restrict__ Xs, double sB) {
+  using F = FK2<TX, TY, TZ>;
+  const int t = threadIdx.x;
+  if (t < F::OFF1) {
+    if (t < F::cls_n(0, 0)) fkt_pencil<TX, TY, TZ, 0, 0>(Pc, T, Xs, t % (TY + 1), t / (TY + 1), sB);
+  } else if (t < F::OFF2) {
+    const int i = t - F::OFF1;
+    if (i < F::cls_n(1, 0)) fkt_pencil<TX, TY, TZ, 1, 0>(Pc, T, Xs, i % TY, i / TY, sB);
+  } else if (t < F::OFF3) {
+    const int i = t - F::OFF2;
+    if (i < F::cls_n(0, 1)) fkt_pencil<TX, TY, TZ, 0, 1>(Pc, T, Xs, i % (TY + 1), i / (TY + 1), sB);
+  } else {
+    const int i = t - F::OFF3;
+    if (i < F::cls_n(1, 1)) fkt_pencil<TX, TY, TZ, 1, 1>(Pc, T, Xs, i % TY, i / TY, sB);
+  }
+}
+
+// step 2 of the warp-specialised kernel (q = sB Bt^T t per element, p_new, <p, q>),
+// not inlined for the same reason; returns dot + this thread's terms
+template <int TX, int TY, int TZ>
+__device__ __noinline__ double fkt_step2(const double* __restrict__ Pc, const double* __restrict__ T,
+                                         double* __restrict__ q, double* __restrict__ pnew, PLay L, int ex0, int ey0,
+                                         int ez0, int N, double sB, double dot) {
+  using F = FK2<TX, TY, TZ>;
+  using K = FKT<TX, TY, TZ>;
+  if (threadIdx.x >= F::NE) return dot;
+  const int lx = threadIdx.x % TX, ly = (threadIdx.x / TX) % TY, lz = threadIdx.x / (TX * TY);
+  const int ex = ex0 + lx, ey = ey0 + ly, ez = ez0 + lz;
+  if (ex >= N || ey >= N || ez >= N) return dot;
+  double qm[4] = {0.0, 0.0, 0.0, 0.0};
+  const double* Sb = T + lx * K::TC;
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int az = 0; az < 3; ++az)
+#pragma unroll
+      for (int ay = 0; ay < 3; ++ay) {
+        const double* Se = Sb + K::sidx(c, 0, 0) + K::row(2 * ly + ay, 2 * lz + az);
+        const double s0 = Se[0];
+        if (w2_nz(c, ay, az, 0)) {
+          const double s1 = Se[K::sidx(0, 1, 0)];
+          qm[0] = fma(c_W2[c][ay][az][0], s0, qm[0]);
+          qm[1] = fma(c_W2[c][ay][az][0], s1, qm[1]);
+        }
+        if (w2_nz(c, ay, az, 1)) qm[2] = fma(c_W2[c][ay][az][1], s0, qm[2]);
+        if (w2_nz(c, ay, az, 2)) qm[3] = fma(c_W2[c][ay][az][2], s0, qm[3]);
+      }
+  const int h = K::pidx(lx + 1, ly + 1, lz + 1);
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const double o = sB * qm[m];
+    const double pv = Pc[m * K::NHP + h];
+    const int64_t j = L.at(m, ex, ey, ez);
+    q[j] = o;
+    pnew[j] = pv;
+    dot = fma(pv, o, dot);
+  }
+  return dot;
+}
+
 // Same contract as k_K2_fused (mode, ctl, partials), tensor maps instead of pointers for the
 // loads: tm_pold / tm_r / tm_minv over [m][ez][ey][ex]; X from its tile-blocked pencil layout XT.
 // ZB: the PCG update kernels store z = Minv r and the kernel loads a z box; else it
@@ -380,6 +445,197 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
   if (tl) g_ktl[blockIdx.x][2] = gtimer();
 #endif
   store_partial<F::NTH>(dot, pqp);
+#ifdef WB_KPROF
+  if (tl) g_ktl[blockIdx.x][3] = gtimer();
+#endif
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// barrier over a subset of the CTA's warps (ids 1, 2; 0 is __syncthreads)
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// Warp-specialised variant of k_K2_tma: the same three steps and arithmetic, but step 0
+// (p = Minv r + beta p_old into Ps) runs in PW producer warps one tile ahead of the
+// consumer warps, which run steps 1 and 2.  Ps is double-buffered without extra shared
+// memory: buffer 1 sits in the padding of buffer 0's rows (offset HY in each QS-row, and
+// QS >= 2 HY), so both keep the conflict-free pencil reads.  Handshake per Ps buffer:
+// full[b] (producers arrive after writing), empty[b] (consumer thread 0 arrives after
+// the tile's step 2).  The raw p / r / Minv boxes stay single-buffered: the producers
+// issue the next tile's loads as soon as they have read them, which is a whole
+// consumer tile before they are needed.  X stays with the consumers (loaded after step 1).
+#ifndef WS_PW
+#define WS_PW 4  // producer warps of k_K2_ws
+#endif
+template <int TX, int TY, int TZ>
+struct FKW {
+  using F = FK2<TX, TY, TZ>;
+  using K = FKT<TX, TY, TZ>;
+  static constexpr int PW = WS_PW, CNTH = F::NTH, PNTH = 32 * PW, NTH = CNTH + PNTH;
+  static constexpr int OFFB = K::HY;  // second Ps buffer
+  static_assert(K::QS >= 2 * K::HY, "both Ps buffers fit in one padded row");
+  static constexpr size_t SMEM = K::SMEM;  // the 6 mbarriers fit in the 64-byte barrier slot
+};
+
+template <int TX, int TY, int TZ, bool ZB>
+__global__ void __launch_bounds__(FKW<TX, TY, TZ>::NTH, 1)
+    k_K2_ws(const __grid_constant__ CUtensorMap tm_pold, const __grid_constant__ CUtensorMap tm_z,
+            const __grid_constant__ CUtensorMap tm_minv, const double* __restrict__ XT, double* __restrict__ pnew,
+            double* __restrict__ q, Geo G, double sB, int mode, int it, int ctl, const double* __restrict__ rzp,
+            int nrz, double* rz_hist, const double* pq_hist, int* stop, double* pqp, PLay L) {
+  using F = FK2<TX, TY, TZ>;
+  using K = FKT<TX, TY, TZ>;
+  using W = FKW<TX, TY, TZ>;
+  const int mode_in = mode;
+#ifdef WB_KPROF
+  const bool tl = (mode & 0x4000) && it == 5 && threadIdx.x == 0 && blockIdx.x < 512;
+  if (tl) g_ktl[blockIdx.x][0] = gtimer();
+#endif
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sb = smraw;
+  double* Pb = (double*)(sb + K::OFF_P);
+  double* Zb = (double*)(sb + K::OFF_R);
+  double* Mb = (double*)(sb + K::OFF_M);
+  constexpr unsigned RAWB = (ZB ? 2u : 3u) * K::PBYTES;
+  double* Ps = (double*)(sb + K::OFF_S);
+  double* Xs = (double*)(sb + K::OFF_X);
+  double* T = (double*)(sb + K::OFF_T);
+  uint64_t* bar = (uint64_t*)(sb + K::OFF_B);  // [0] raw boxes, [1] X, [2, 3] full, [4, 5] empty
+  const int N = G.N;
+  const int NTX = (N + TX - 1) / TX, NTY = (N + TY - 1) / TY, NTZ = (N + TZ - 1) / TZ;
+  const int n_tiles = NTX * NTY * NTZ;
+  auto coords = [&](int tile, int& ex0, int& ey0, int& ez0) {
+    ex0 = TX * (tile % NTX); ey0 = TY * ((tile / NTX) % NTY); ez0 = TZ * (tile / (NTX * NTY));
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1); mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], W::PNTH); mbar_init(&bar[3], W::PNTH);
+    mbar_init(&bar[4], 1); mbar_init(&bar[5], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int tile = blockIdx.x;
+    if (tile < n_tiles) {
+      int ex0, ey0, ez0;
+      coords(tile, ex0, ey0, ez0);
+      mbar_expect_tx(&bar[0], RAWB);
+      tma_load_4d(Zb, &tm_z, ey0, ez0 - 1, ex0 - 1, 0, &bar[0]);
+      if (!ZB) tma_load_4d(Mb, &tm_minv, ey0, ez0 - 1, ex0 - 1, 0, &bar[0]);
+      tma_load_4d(Pb, &tm_pold, ey0, ez0 - 1, ex0 - 1, 0, &bar[0]);
+      mbar_expect_tx(&bar[1], K::XBYTES);
+      bulk_load(Xs, XT + (size_t)tile * K::XTB, K::XBYTES, &bar[1]);
+    }
+  }
+  mode &= 0xff;
+  double beta = 0.0;
+  if (ctl) {
+    if (pcg_control<W::NTH>(it, rzp, nrz, rz_hist, pq_hist, stop, &beta)) {
+      if (threadIdx.x == 0 && (int)blockIdx.x < n_tiles) { mbar_wait(&bar[0], 0); mbar_wait(&bar[1], 0); }
+      return;
+    }
+  } else if (mode == 1) {
+    beta = rz_hist[it] / rz_hist[it - 1];
+  }
+  __syncthreads();
+#ifdef WB_KPROF
+  if (tl) g_ktl[blockIdx.x][1] = gtimer();
+  // role probes (k_dbg 0x4000; tools/wsphase.py), cycles into g_kprof: consumer thread 0
+  // [0] wait full, [1] wait X, [2] step 1 + barrier, [3] step 2 + barrier, [7] tiles;
+  // producer thread 0 [4] wait empty, [5] wait raw boxes, [6] step 0 + barrier
+  const bool prof = (mode_in & 0x4000) && (threadIdx.x == 0 || threadIdx.x == W::CNTH);
+  unsigned long long pt_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tc = clock64();
+  auto lap = [&](int k) {
+    if (prof) { const long long n = clock64(); pt_[k] += (unsigned long long)(n - tc); tc = n; }
+  };
+#else
+  auto lap = [](int) {};
+#endif
+  double dot = 0.0;
+  if (threadIdx.x >= W::CNTH) {
+    // ---- producers: step 0 for tile k into Ps buffer k & 1
+    const int pt = threadIdx.x - W::CNTH;
+    int k = 0;
+#pragma unroll 1
+    for (int tile = blockIdx.x; tile < n_tiles; ++k, tile += gridDim.x) {
+      const int b = k & 1;
+      lap(6);
+      if (k >= 2) mbar_wait(&bar[4 + b], ((k >> 1) - 1) & 1);
+      lap(4);
+      mbar_wait(&bar[0], k & 1);
+      lap(5);
+      double* Pd = Ps + b * W::OFFB;
+      // pairs (HY is even, so a pair never straddles a row): 16-byte loads of the raw boxes
+#pragma unroll 4
+      for (int j2 = pt; j2 < ((mode_in & 0x400) ? 0 : 2 * K::NB); j2 += W::PNTH) {
+        const double2 pp = reinterpret_cast<const double2*>(Pb)[j2];
+        double2 v;
+        if (mode == 2) v = pp;
+        else {
+          const double2 zz = reinterpret_cast<const double2*>(Zb)[j2];
+          double2 z = zz;
+          if (!ZB) {
+            const double2 mm = reinterpret_cast<const double2*>(Mb)[j2];
+            z.x = mm.x * zz.x; z.y = mm.y * zz.y;
+          }
+          v = z;
+          if (mode == 1) { v.x = fma(beta, pp.x, z.x); v.y = fma(beta, pp.y, z.y); }
+        }
+        double* d = Pd + K::QS * (j2 / (K::HY / 2)) + 2 * (j2 % (K::HY / 2));
+        d[0] = v.x; d[1] = v.y;
+      }
+      named_bar(2, W::PNTH);  // raw boxes consumed
+      const int next = tile + gridDim.x;
+      if (pt == 0 && next < n_tiles) {
+        int nx0, ny0, nz0;
+        coords(next, nx0, ny0, nz0);
+        fence_proxy_async();
+        mbar_expect_tx(&bar[0], RAWB);
+        tma_load_4d(Zb, &tm_z, ny0, nz0 - 1, nx0 - 1, 0, &bar[0]);
+        if (!ZB) tma_load_4d(Mb, &tm_minv, ny0, nz0 - 1, nx0 - 1, 0, &bar[0]);
+        tma_load_4d(Pb, &tm_pold, ny0, nz0 - 1, nx0 - 1, 0, &bar[0]);
+      }
+      mbar_arrive(&bar[2 + b]);
+    }
+  } else {
+    // ---- consumers: steps 1 and 2 for tile k from Ps buffer k & 1
+    int k = 0;
+#pragma unroll 1
+    for (int tile = blockIdx.x; tile < n_tiles; ++k, tile += gridDim.x) {
+      const int b = k & 1;
+      const double* Pc = Ps + b * W::OFFB;
+      const int next = tile + gridDim.x;
+      int ex0, ey0, ez0;
+      coords(tile, ex0, ey0, ez0);
+      lap(3);
+      mbar_wait(&bar[2 + b], (k >> 1) & 1);
+      lap(0);
+      mbar_wait(&bar[1], k & 1);
+      lap(1);
+      fkt_step1<TX, TY, TZ>(Pc, T, Xs, sB);
+      named_bar(1, W::CNTH);
+      lap(2);
+      if (threadIdx.x == K::TMA_T && next < n_tiles) {  // X buffer is free
+        fence_proxy_async();
+        mbar_expect_tx(&bar[1], K::XBYTES);
+        bulk_load(Xs, XT + (size_t)next * K::XTB, K::XBYTES, &bar[1]);
+      }
+      dot = fkt_step2<TX, TY, TZ>(Pc, T, q, pnew, L, ex0, ey0, ez0, N, sB, dot);
+      named_bar(1, W::CNTH);  // T and Ps buffer b are free
+      if (threadIdx.x == 0) mbar_arrive(&bar[4 + b]);
+#ifdef WB_KPROF
+      if (prof) ++pt_[7];
+#endif
+    }
+    lap(3);
+  }
+#ifdef WB_KPROF
+  lap(6);
+  if (prof)
+    for (int j = 0; j < 8; ++j)
+      if (pt_[j]) atomicAdd(&g_kprof[j], pt_[j]);
+  if (tl) g_ktl[blockIdx.x][2] = gtimer();
+#endif
+  store_partial<W::NTH>(dot, pqp);  // producers add 0.0: same sums as k_K2_tma's 11 warps
 #ifdef WB_KPROF
   if (tl) g_ktl[blockIdx.x][3] = gtimer();
 #endif

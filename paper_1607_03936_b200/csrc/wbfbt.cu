@@ -72,6 +72,7 @@ struct wb_ctx {
   // mode-major PCG vectors and over row-padded copies of C_w^-1 / D_w^-1
   bool tma_ok = false;
   int use_tma = 1;
+  int k_ws = 0;  // 1: the TMA Poisson operator runs warp-specialised (k_K2_ws)
   double *XpL = nullptr, *XpR = nullptr;  // C_w^-1, D_w^-1 in the TMA kernel's X-block layout (k_x_tiles)
   // k = 2, even N: MinvL | XpL | x r p p' q z | MinvR | XpR carved from one slab (each
   // side's PCG working set contiguous; a persisting L2 access-policy window over it was
@@ -265,8 +266,13 @@ wb_status run_k2f(wb_ctx* c, const double* pold, double* pnew, const double* r, 
       const int N = c->N;
       const int nt = ((N + TMA_TX - 1) / TMA_TX) * ((N + TMA_TY - 1) / TMA_TY) * ((N + TMA_TZ - 1) / TMA_TZ);
       const int grid = std::max(1, std::min(nt, TMA_MINB * c->nsm));  // persistent, all resident
-      auto kern = c->kz ? k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, true> : k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, false>;
-      kern<<<grid, FK2<TMA_TX, TMA_TY, TMA_TZ>::NTH, KT::SMEM, c->stream>>>(
+      using KW = FKW<TMA_TX, TMA_TY, TMA_TZ>;
+      auto kern = c->k_ws ? (c->kz ? k_K2_ws<TMA_TX, TMA_TY, TMA_TZ, true> : k_K2_ws<TMA_TX, TMA_TY, TMA_TZ, false>)
+                          : (c->kz ? k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, true>
+                                   : k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, false>);
+      const int nth = c->k_ws ? KW::NTH : FK2<TMA_TX, TMA_TY, TMA_TZ>::NTH;
+      const size_t smem = c->k_ws ? KW::SMEM : KT::SMEM;
+      kern<<<grid, nth, smem, c->stream>>>(
           *tp, *tz, *tm, xt, pnew, q, c->G, c->sB, mode | c->k_dbg, a.it, a.ctl, c->rzp, c->red_blocks, rz_hist(c),
           pq_hist(c), c->stop, c->pqp, c->pl);
       LAUNCH_CHECK(c);
@@ -318,7 +324,11 @@ bool setup_tma(wb_ctx* c) {
   if (cudaFuncSetAttribute(k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FKT<TMA_TX, TMA_TY, TMA_TZ>::SMEM) != cudaSuccess ||
       cudaFuncSetAttribute(k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FKT<TMA_TX, TMA_TY, TMA_TZ>::SMEM) != cudaSuccess) {
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FKT<TMA_TX, TMA_TY, TMA_TZ>::SMEM) != cudaSuccess ||
+      cudaFuncSetAttribute(k_K2_ws<TMA_TX, TMA_TY, TMA_TZ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)FKW<TMA_TX, TMA_TY, TMA_TZ>::SMEM) != cudaSuccess ||
+      cudaFuncSetAttribute(k_K2_ws<TMA_TX, TMA_TY, TMA_TZ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)FKW<TMA_TX, TMA_TY, TMA_TZ>::SMEM) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
@@ -1128,6 +1138,8 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
     *value = (tma_active(c) && c->kz) ? 1.0 : 0.0;
   } else if (!strcmp(key, "k_tma")) {  // 1: the Poisson operator runs as the TMA kernel (k_K2_tma)
     *value = tma_active(c) ? 1.0 : 0.0;
+  } else if (!strcmp(key, "k_ws")) {  // 1: ... as the warp-specialised TMA kernel (k_K2_ws)
+    *value = (tma_active(c) && c->k_ws) ? 1.0 : 0.0;
   } else if (!strcmp(key, "occ_a2")) {
     int nb = 0;
     CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_A_tile<A_TX, A_TY, A_TZ, A_MINB>, 3 * A_TX * A_TY * A_TZ, Tile2<A_TX, A_TY, A_TZ>::SMEM));
@@ -1206,6 +1218,10 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
   } else if (!strcmp(key, "kz")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "kz must be 0 or 1");
     c->kz = (int)value;
+    clear_graphs(c);
+  } else if (!strcmp(key, "k_ws")) {
+    if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k_ws must be 0 or 1");
+    c->k_ws = (int)value;
     clear_graphs(c);
   } else if (!strcmp(key, "tma")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "tma must be 0 or 1");

@@ -247,18 +247,26 @@ def test_large_poisson_paths_ragged_tiles(N):
     """The large-mesh Poisson kernels with tiles ragged in y and z (4x8x8 tiles): the TMA
     kernel (even N with >= 75,776 elements: N = 44, 46) and the pointer kernel it falls
     back to for odd N (N = 45).  apply_K on both sides and a 5-iteration PCG against the
-    oracle; for the TMA kernel its two variants (z box, r + Minv boxes) bitwise equal."""
+    oracle; for the TMA kernel its four variants (z box or r + Minv boxes, plain or
+    warp-specialised) bitwise equal."""
     p = Pair("C5", N=N)
-    assert p.ctx.query("k_tma") == (1 if N % 2 == 0 else 0)
+    tma = 1 if N % 2 == 0 else 0
+    assert p.ctx.query("k_tma") == tma
     st = p.ost
     b = p.inp["p"]
-    if st["n_nonpos_Cw"] == 0:
-        for side, X in ((0, st["Cinv"]), (1, st["Dinv"])):
-            q = host(p.ctx.apply_K(side, dev(b), empty(p.ctx.n_p)))
-            assert rel_l2(q, p.o.apply_K(X, b)) <= 1e-11
+    for ws in (0, 1):
+        p.ctx.set_option("k_ws", ws)
+        assert p.ctx.query("k_ws") == ws * tma
+        if st["n_nonpos_Cw"] == 0:
+            for side, X in ((0, st["Cinv"]), (1, st["Dinv"])):
+                q = host(p.ctx.apply_K(side, dev(b), empty(p.ctx.n_p)))
+                assert rel_l2(q, p.o.apply_K(X, b)) <= 1e-11
     xs = []
-    for kz in (1, 0):
-        p.ctx.set_option("kz", kz)
-        xs.append(host(p.ctx.poisson_pcg(1, dev(b), empty(p.ctx.n_p), 5)))
-    assert np.array_equal(xs[0], xs[1])
+    for ws in (0, 1):
+        p.ctx.set_option("k_ws", ws)
+        for kz in (1, 0):
+            p.ctx.set_option("kz", kz)
+            xs.append(host(p.ctx.poisson_pcg(1, dev(b), empty(p.ctx.n_p), 5)))
+    for x in xs[1:]:
+        assert np.array_equal(xs[0], x)
     assert rel_l2(xs[0], p.o.poisson(st["Dinv"], st["diagKr"], b, 5)) <= 1e-12

@@ -1,0 +1,9 @@
+#!/bin/bash
+# k_K2_ws producer-warp sweep at C5 (per PCG iteration, tools/opt_ab.py); rebuilds the library per setting
+set -x
+for pw in ${WS_PWS:-4 1 2 3}; do
+  python -c "
+import sys; sys.path.insert(0,'paper_1607_03936_b200'); import build; build.FLAGS += ['-DWS_PW=$pw']; build.build(force=True)" > /dev/null 2>&1
+  timeout 300 python -m pytest tests/test_gpu_api.py -q -x -k "ragged" 2>&1 | tail -2
+  timeout 300 python tools/opt_ab.py C5 "k_ws=0,kz=0" "k_ws=1,kz=0" "k_ws=1,kz=1" 2>&1 | tail -3
+done
