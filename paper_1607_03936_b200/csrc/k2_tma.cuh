@@ -105,9 +105,13 @@ struct FKT {
   // row sums S[c][m1][lx][row] (x-contracted B per element of the row) in the T region
   __host__ __device__ static constexpr int sidx(int c, int m1, int lx) { return ((c * 2 + m1) * TX + lx) * TC; }
   static_assert(6 * TX <= 3 * F::MX, "S fits in the T region");
+  // class (1,0) rows are jz-fastest (its pencils are assigned jz-fastest too): with the
+  // Ps row stride QS = 9 (mod 16), 8-wide jy rows would put two lanes of a half-warp on
+  // one bank pair; 9 jz values and the next jy's 7 hit 16 distinct ones
   __host__ __device__ static constexpr int row(int ny, int nz) {
-    return ((ny & 1) ? ((nz & 1) ? R00 + R10 + R01 : R00) : ((nz & 1) ? R00 + R10 : 0)) +
-           (ny >> 1) + ((ny & 1) ? TY : TY + 1) * (nz >> 1);
+    return ((ny & 1) && !(nz & 1)) ? R00 + (nz >> 1) + (TZ + 1) * (ny >> 1)
+                                   : ((ny & 1) ? R00 + R10 + R01 : ((nz & 1) ? R00 + R10 : 0)) + (ny >> 1) +
+                                         ((ny & 1) ? TY : TY + 1) * (nz >> 1);
   }
   // shared layout (bytes): raw p | raw r or z | raw Minv | Ps | X | T | barriers, each 1024-aligned
   static constexpr size_t al(size_t b) { return (b + 1023) & ~(size_t)1023; }
@@ -204,7 +208,7 @@ __device__ __noinline__ void fkt_step1(const double* __restrict__ Pc, double* __
     if (t < F::cls_n(0, 0)) fkt_pencil<TX, TY, TZ, 0, 0>(Pc, T, Xs, t % (TY + 1), t / (TY + 1), sB);
   } else if (t < F::OFF2) {
     const int i = t - F::OFF1;
-    if (i < F::cls_n(1, 0)) fkt_pencil<TX, TY, TZ, 1, 0>(Pc, T, Xs, i % TY, i / TY, sB);
+    if (i < F::cls_n(1, 0)) fkt_pencil<TX, TY, TZ, 1, 0>(Pc, T, Xs, i / (TZ + 1), i % (TZ + 1), sB);
   } else if (t < F::OFF3) {
     const int i = t - F::OFF2;
     if (i < F::cls_n(0, 1)) fkt_pencil<TX, TY, TZ, 0, 1>(Pc, T, Xs, i % (TY + 1), i / (TY + 1), sB);
@@ -382,7 +386,7 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
         if (t < F::cls_n(0, 0)) fkt_pencil<TX, TY, TZ, 0, 0>(Ps, T, Xs, t % (TY + 1), t / (TY + 1), sB);
       } else if (t < F::OFF2) {
         const int i = t - F::OFF1;
-        if (i < F::cls_n(1, 0)) fkt_pencil<TX, TY, TZ, 1, 0>(Ps, T, Xs, i % TY, i / TY, sB);
+        if (i < F::cls_n(1, 0)) fkt_pencil<TX, TY, TZ, 1, 0>(Ps, T, Xs, i / (TZ + 1), i % (TZ + 1), sB);
       } else if (t < F::OFF3) {
         const int i = t - F::OFF2;
         if (i < F::cls_n(0, 1)) fkt_pencil<TX, TY, TZ, 0, 1>(Ps, T, Xs, i % (TY + 1), i / (TY + 1), sB);
