@@ -121,6 +121,38 @@ struct FKT {
   static constexpr size_t SMEM = OFF_B + 64 + 1024;  // + slack for 1024-byte base alignment
 };
 
+// Step 0 copy, raw box [row][HY] -> Ps [row][QS] (row = (m, hx, hz)), in y-pairs:
+// v = Minv r + beta p_old (mode 1), Minv r (mode 0) or p (mode 2).  Pair item t of a
+// half-warp h = t / 16 takes pair column s = h % 5 of rows 16 (h / 5) + (t % 16): the
+// 16-byte loads (pair 5 row + s) of a quarter-warp hit 8 distinct 16-byte slots and the
+// two 8-byte stores (25 row + 2 s, + 1) of a half-warp 16 distinct bank pairs, since
+// 5 and 9 = 25 mod 16 are odd.  (A row-major walk makes the stores 2-way conflicted.)
+template <int TX, int TY, int TZ, bool ZB>
+__device__ __forceinline__ void fkt_copy_pair(int t, const double* __restrict__ Pb, const double* __restrict__ Zb,
+                                              const double* __restrict__ Mb, double* __restrict__ Pd, int mode,
+                                              double beta) {
+  using K = FKT<TX, TY, TZ>;
+  static_assert(K::HY == 10 && K::QS % 16 == 9 && (4 * K::HX * K::HZ) % 16 == 0, "pair walk layout");
+  const int h = t >> 4;
+  const int r = 16 * (h / 5) + (t & 15), sp = h % 5;
+  const int j2 = 5 * r + sp;
+  const double2 pp = reinterpret_cast<const double2*>(Pb)[j2];
+  double2 v;
+  if (mode == 2) v = pp;
+  else {
+    double2 z = reinterpret_cast<const double2*>(Zb)[j2];
+    if (!ZB) {
+      const double2 mm = reinterpret_cast<const double2*>(Mb)[j2];
+      z.x = mm.x * z.x; z.y = mm.y * z.y;
+    }
+    v = z;
+    if (mode == 1) { v.x = fma(beta, pp.x, z.x); v.y = fma(beta, pp.y, z.y); }
+  }
+  double* d = Pd + K::QS * r + 2 * sp;
+  d[0] = v.x;
+  d[1] = v.y;
+}
+
 // x-pencil as in fk2_pencil, with the staged layouts: Ps (padded qy-fastest rows), Xs (XT block)
 template <int TX, int TY, int TZ, int RY, int RZ>
 __device__ __forceinline__ void fkt_pencil(const double* __restrict__ Ps, double* __restrict__ T,
@@ -358,15 +390,8 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     lap(1);
     // the raw box is [m][hx][hz][hy] = Ps's order with row length HY instead of QS:
     // a flat, lane-consecutive walk
-    for (int j = threadIdx.x; j < ((dbg & 0x400) ? 0 : 4 * K::NB); j += F::NTH) {
-      double v;
-      if (mode == 2) v = Pb[j];
-      else {
-        const double z = ZB ? Zb[j] : Mb[j] * Zb[j];
-        v = (mode == 1) ? fma(beta, Pb[j], z) : z;
-      }
-      Ps[K::QS * (j / K::HY) + j % K::HY] = v;
-    }
+    for (int t = threadIdx.x; t < ((dbg & 0x400) ? 0 : 2 * K::NB); t += F::NTH)
+      fkt_copy_pair<TX, TY, TZ, ZB>(t, Pb, Zb, Mb, Ps, mode, beta);
     __syncthreads();
     lap(2);
     if (threadIdx.x == K::TMA_T && next < n_tiles) {  // raw p, r, Minv buffers are free
@@ -568,25 +593,9 @@ __global__ void __launch_bounds__(FKW<TX, TY, TZ>::NTH, 1)
       mbar_wait(&bar[0], k & 1);
       lap(5);
       double* Pd = Ps + b * W::OFFB;
-      // pairs (HY is even, so a pair never straddles a row): 16-byte loads of the raw boxes
 #pragma unroll 4
-      for (int j2 = pt; j2 < ((mode_in & 0x400) ? 0 : 2 * K::NB); j2 += W::PNTH) {
-        const double2 pp = reinterpret_cast<const double2*>(Pb)[j2];
-        double2 v;
-        if (mode == 2) v = pp;
-        else {
-          const double2 zz = reinterpret_cast<const double2*>(Zb)[j2];
-          double2 z = zz;
-          if (!ZB) {
-            const double2 mm = reinterpret_cast<const double2*>(Mb)[j2];
-            z.x = mm.x * zz.x; z.y = mm.y * zz.y;
-          }
-          v = z;
-          if (mode == 1) { v.x = fma(beta, pp.x, z.x); v.y = fma(beta, pp.y, z.y); }
-        }
-        double* d = Pd + K::QS * (j2 / (K::HY / 2)) + 2 * (j2 % (K::HY / 2));
-        d[0] = v.x; d[1] = v.y;
-      }
+      for (int t = pt; t < ((mode_in & 0x400) ? 0 : 2 * K::NB); t += W::PNTH)
+        fkt_copy_pair<TX, TY, TZ, ZB>(t, Pb, Zb, Mb, Pd, mode, beta);
       named_bar(2, W::PNTH);  // raw boxes consumed
       const int next = tile + gridDim.x;
       if (pt == 0 && next < n_tiles) {
