@@ -17,4 +17,6 @@ if [ $rc -eq 0 ]; then
     -o gpurun_out/${TAG}_k2tma -f python tools/tma_check.py C5 > gpurun_out/${TAG}_ncu_full.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_A_tile -s 3 -c 1 --cache-control all \
     -o gpurun_out/${TAG}_atile -f python bench.py --steps 3 --warmup 3 > gpurun_out/${TAG}_ncu_a.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pcg_upd -s 40 -c 2 \
+    -o gpurun_out/${TAG}_upd -f python tools/tma_check.py C5 > gpurun_out/${TAG}_ncu_upd.log 2>&1
 fi

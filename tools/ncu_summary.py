@@ -76,13 +76,17 @@ def main():
         if hc:
             si = hc.index("Warp Stall Sampling (All Samples)")
             data = []
-            for r in src_rows[src_rows.index(hc) + 1:]:
-                if len(r) == len(hc) and r[si].strip().isdigit() and int(r[si]) > 0:
-                    data.append((int(r[si]), r[0], r[1].strip()[:80]))
+            fname = ""
+            for r in src_rows:
+                if r and r[0] in ("File Path", "File Name") and len(r) > 1:
+                    fname = os.path.basename(r[1])
+                # source-line rows only (the interleaved SASS rows have no line number)
+                if len(r) == len(hc) and r[0].strip().isdigit() and r[si].strip().isdigit() and int(r[si]) > 0:
+                    data.append((int(r[si]), f"{fname}:{r[0]}", r[1].strip()[:80]))
             tot = sum(x[0] for x in data)
             lines.append("   top source lines by stall samples:")
             for n, ln, s in sorted(data, reverse=True)[:10]:
-                lines.append(f"     {100 * n / max(tot, 1):5.1f}%  L{ln:>4s}  {s}")
+                lines.append(f"     {100 * n / max(tot, 1):5.1f}%  {ln:>16s}  {s}")
     open(out, "w").write("\n".join(lines) + "\n")
     json.dump(traffic, open(tpath, "w"), indent=1)
     print(open(out).read())
