@@ -69,6 +69,12 @@ def lib():
             L.or_wbfbt.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, _D, _D, C.c_int]
             L.or_poisson_relres.restype = C.c_double
             L.or_poisson_relres.argtypes = [C.c_void_p, _D, _D, _D]
+            L.or_cheb_dense.argtypes = [C.c_int64, _D, _D, _D, _D, C.c_int, C.c_double, C.c_double]
+            L.or_poisson_cheb.argtypes = [C.c_void_p, _D, _D, _D, _D, C.c_int, C.c_double, C.c_double]
+            L.or_eigmax_dense.argtypes = [C.c_int64, _D, _D, _D, C.c_int]
+            L.or_eigmax_dense.restype = C.c_double
+            L.or_poisson_eigmax.argtypes = [C.c_void_p, _D, _D, _D, C.c_int]
+            L.or_poisson_eigmax.restype = C.c_double
             L.or_num_threads.restype = C.c_int
             _lib = L
     return _lib
@@ -81,6 +87,20 @@ def _p(a: np.ndarray):
 
 def _f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def cheb_dense(A, Minv, b, iters, lmin, lmax) -> np.ndarray:
+    """The Chebyshev recurrence of or_poisson_cheb on a dense matrix A (row-major), x0 = 0."""
+    A, Minv, b = _f64(A), _f64(Minv), _f64(b)
+    x = np.zeros(len(b))
+    lib().or_cheb_dense(len(b), _p(A), _p(Minv), _p(b), _p(x), int(iters), float(lmin), float(lmax))
+    return x
+
+
+def eigmax_dense(A, Minv, v0, iters) -> float:
+    """The power iteration of or_poisson_eigmax on a dense matrix A (row-major)."""
+    A, Minv, v0 = _f64(A), _f64(Minv), _f64(v0)
+    return float(lib().or_eigmax_dense(len(v0), _p(A), _p(Minv), _p(v0), int(iters)))
 
 
 def sizes_only(N: int, k: int) -> dict:
@@ -227,6 +247,18 @@ class Oracle:
         x = np.zeros(self.n_p)
         self.L.or_poisson(self.h, _p(Xinv), _p(diagK), _p(b), _p(x), int(iters))
         return x
+
+    def poisson_cheb(self, Xinv, diagK, b, iters, lmin, lmax) -> np.ndarray:
+        """x = P Cheb(K, P b): Chebyshev-accelerated Jacobi, interval [lmin, lmax] of Minv K (R16)."""
+        Xinv, diagK, b = _f64(Xinv), _f64(diagK), _f64(b)
+        x = np.zeros(self.n_p)
+        self.L.or_poisson_cheb(self.h, _p(Xinv), _p(diagK), _p(b), _p(x), int(iters), float(lmin), float(lmax))
+        return x
+
+    def poisson_eigmax(self, Xinv, diagK, v0, iters) -> float:
+        """Power-iteration estimate of the largest |eigenvalue| of Minv K from start vector v0."""
+        Xinv, diagK, v0 = _f64(Xinv), _f64(diagK), _f64(v0)
+        return float(self.L.or_poisson_eigmax(self.h, _p(Xinv), _p(diagK), _p(v0), int(iters)))
 
     def poisson_relres(self, Xinv, b, x) -> float:
         Xinv, b, x = _f64(Xinv), _f64(b), _f64(x)

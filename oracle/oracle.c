@@ -575,6 +575,112 @@ void or_poisson(or_ctx* c, const double* Xinv, const double* diagK, const double
   free(bb);
 }
 
+/* ---------------------------------------------------------------- Chebyshev
+ * Chebyshev-accelerated point-Jacobi (the paper's smoother, PAPER.md:2531-2546;
+ * SURVEY.md 8(f) #2) as a fixed-iteration inner solve.  The paper gives no
+ * recurrence or spectrum bounds (reading R16): Saad, "Iterative Methods
+ * for Sparse Linear Systems" (2003), Alg. 12.1 (Chebyshev acceleration) on
+ * M^-1 K with the Jacobi pseudo-inverse Minv of R11 as M^-1 and the caller's
+ * interval [lmin, lmax] of the spectrum of M^-1 K, from x0 = 0:
+ *   theta = (lmax + lmin)/2; delta = (lmax - lmin)/2; sigma1 = theta/delta; rho = 1/sigma1
+ *   r = b; d = (1/theta) Minv r
+ *   repeat iters: x += d; r -= K d; rho' = 1/(2 sigma1 - rho);
+ *                 d = rho' rho d + (2 rho'/delta) Minv r; rho = rho'
+ * The recurrence is written once (cheb_run) over an operator callback; the dense
+ * form (or_cheb_dense) is what tests/test_oracle_cheb.py pins against the closed
+ * form e_k = T_k((theta - lambda)/delta) / T_k(sigma1) e_0 of the error on a
+ * diagonal system.                                                            */
+typedef void (*or_op)(void* ctx, const double* in, double* out);
+static void cheb_run(or_op K, void* kctx, int64_t n, const double* Minv, const double* b, double* x, int iters,
+                     double lmin, double lmax) {
+  double* r = (double*)malloc(sizeof(double) * n);
+  double* d = (double*)malloc(sizeof(double) * n);
+  double* q = (double*)malloc(sizeof(double) * n);
+  const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin);
+  const double sigma1 = theta / delta;
+  double rho = 1.0 / sigma1;
+  for (int64_t i = 0; i < n; ++i) { x[i] = 0.0; r[i] = b[i]; d[i] = (1.0 / theta) * (Minv[i] * r[i]); }
+  for (int it = 0; it < iters; ++it) {
+    for (int64_t i = 0; i < n; ++i) x[i] += d[i];
+    K(kctx, d, q);
+    for (int64_t i = 0; i < n; ++i) r[i] -= q[i];
+    const double rho1 = 1.0 / (2.0 * sigma1 - rho);
+    const double c1 = rho1 * rho, c2 = 2.0 * rho1 / delta;
+    for (int64_t i = 0; i < n; ++i) d[i] = c1 * d[i] + c2 * (Minv[i] * r[i]);
+    rho = rho1;
+  }
+  free(r); free(d); free(q);
+}
+
+typedef struct { int64_t n; const double* A; } or_dense;
+static void dense_op(void* ctx, const double* in, double* out) {
+  const or_dense* D = (const or_dense*)ctx;
+  for (int64_t i = 0; i < D->n; ++i) {
+    double s = 0.0;
+    for (int64_t j = 0; j < D->n; ++j) s += D->A[i * D->n + j] * in[j];
+    out[i] = s;
+  }
+}
+/* the recurrence on a dense n x n matrix A (row-major) with Jacobi inverse Minv */
+void or_cheb_dense(int64_t n, const double* A, const double* Minv, const double* b, double* x, int iters,
+                   double lmin, double lmax) {
+  or_dense D = {n, A};
+  cheb_run(dense_op, &D, n, Minv, b, x, iters, lmin, lmax);
+}
+
+typedef struct { or_ctx* c; const double* Xinv; double* tv; } or_kop;
+static void k_op(void* ctx, const double* in, double* out) {
+  or_kop* k = (or_kop*)ctx;
+  or_apply_K(k->c, k->Xinv, in, out, k->tv);
+}
+/* Projected Chebyshev solve: x = P Cheb(K_side, P b) (R10, R16). */
+void or_poisson_cheb(or_ctx* c, const double* Xinv, const double* diagK, const double* b, double* x, int iters,
+                     double lmin, double lmax) {
+  const int64_t n = c->n_p;
+  double* bb = (double*)malloc(sizeof(double) * n);
+  double* Minv = (double*)malloc(sizeof(double) * n);
+  or_kop k = {c, Xinv, (double*)malloc(sizeof(double) * c->n_v)};
+  memcpy(bb, b, sizeof(double) * n);
+  or_project(c, bb);
+  jacobi_minv(diagK, Minv, n);
+  cheb_run(k_op, &k, n, Minv, bb, x, iters, lmin, lmax);
+  or_project(c, x);
+  free(bb); free(Minv); free(k.tv);
+}
+
+/* Power-iteration estimate of the largest-magnitude eigenvalue of Minv K (the
+ * input the caller turns into a Chebyshev interval, R16):
+ *   v = v0 / ||v0||; repeat iters: w = Minv (K v); lambda = ||w||; v = w / lambda
+ * Returns lambda of the last step (0 if an iterate vanishes). */
+static double power_run(or_op K, void* kctx, int64_t n, const double* Minv, const double* v0, int iters) {
+  double* v = (double*)malloc(sizeof(double) * n);
+  double* w = (double*)malloc(sizeof(double) * n);
+  double nv = sqrt(dot(v0, v0, n)), lam = 0.0;
+  for (int64_t i = 0; i < n; ++i) v[i] = nv > 0.0 ? v0[i] / nv : 0.0;
+  for (int it = 0; it < iters && nv > 0.0; ++it) {
+    K(kctx, v, w);
+    for (int64_t i = 0; i < n; ++i) w[i] = Minv[i] * w[i];
+    lam = sqrt(dot(w, w, n));
+    if (lam == 0.0) break;
+    for (int64_t i = 0; i < n; ++i) v[i] = w[i] / lam;
+  }
+  free(v); free(w);
+  return lam;
+}
+double or_eigmax_dense(int64_t n, const double* A, const double* Minv, const double* v0, int iters) {
+  or_dense D = {n, A};
+  return power_run(dense_op, &D, n, Minv, v0, iters);
+}
+double or_poisson_eigmax(or_ctx* c, const double* Xinv, const double* diagK, const double* v0, int iters) {
+  const int64_t n = c->n_p;
+  double* Minv = (double*)malloc(sizeof(double) * n);
+  or_kop k = {c, Xinv, (double*)malloc(sizeof(double) * c->n_v)};
+  jacobi_minv(diagK, Minv, n);
+  const double lam = power_run(k_op, &k, n, Minv, v0, iters);
+  free(Minv); free(k.tv);
+  return lam;
+}
+
 /* ---------------------------------------------------------------- wBFBT
  * z = S~^{-1}_wBFBT r  (eq:wbfbt), applied right to left:
  *   y = P PCG(K_r, P r); v = Dinv o (B^T y); v = A v; v = Cinv o v; s = P(B v);
