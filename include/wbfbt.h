@@ -117,6 +117,22 @@ wb_status wb_apply_K(wb_ctx* ctx, int side, const double* p, double* q);
  * (x0 = 0, M = diag K, no tolerance; stands in for the paper's HMG V-cycle,
  * PAPER.md:2503-2529; recurrence in DESIGN.md Sec. 4).  b, x: n_p. */
 wb_status wb_poisson_pcg(wb_ctx* ctx, int side, const double* b, double* x, int iters);
+/* x = P Cheb(K_side, P b): Chebyshev-accelerated point-Jacobi, the
+ * paper's smoother as a fixed-iteration inner solve.  Saad (2003)
+ * Alg. 12.1 on Minv K_side (Minv = the Jacobi pseudo-inverse of wb_poisson_pcg), x0 = 0,
+ * exactly `iters` steps, [lmin, lmax] the caller's interval of the spectrum of
+ * Minv K_side (reading R16).  b, x: device, element-major n_p; b is not
+ * modified.  WB_EINVAL for side not 0/1, iters < 0, null pointers or unless
+ * 0 < lmin < lmax < inf; WB_EALIAS if b and x overlap; WB_ESTATE before
+ * wb_set_viscosity.  Asynchronous on the context stream. */
+wb_status wb_poisson_cheb(wb_ctx* ctx, int side, const double* b, double* x, int iters, double lmin, double lmax);
+/* *lmax = power-iteration estimate of the largest |eigenvalue| of Minv K_side (R16):
+ * v = v0/||v0||, then `iters` times w = Minv (K_side v), lambda = ||w||, v = w/lambda;
+ * *lmax = the last lambda (0 if iters = 0 or an iterate vanishes).  v0: device,
+ * element-major n_p, not modified (the start vector is an input, so runs are
+ * reproducible).  lmax: host.  Synchronises the context stream.  WB_EINVAL for
+ * side not 0/1, iters < 0 or null pointers; WB_ESTATE before wb_set_viscosity. */
+wb_status wb_poisson_eigmax(wb_ctx* ctx, int side, const double* v0, int iters, double* lmax);
 /* Row a10 -- z = S~^-1_wBFBT r (eq:wbfbt PAPER.md:436-454), applied right to
  * left:  y = P PCG(K_r, P r); v = D_w^-1 B^T y; v = A v; v = C_w^-1 v;
  * s = P B v; z = P PCG(K_l, s).  r, z: n_p. */

@@ -41,6 +41,8 @@ SYMBOLS = [
     ("wb_apply_BT", _i, [_vp, _vp, _vp]),
     ("wb_apply_K", _i, [_vp, _i, _vp, _vp]),
     ("wb_poisson_pcg", _i, [_vp, _i, _vp, _vp, _i]),
+    ("wb_poisson_cheb", _i, [_vp, _i, _vp, _vp, _i, _d, _d]),
+    ("wb_poisson_eigmax", _i, [_vp, _i, _vp, _i, C.POINTER(_d)]),
     ("wb_apply_wbfbt", _i, [_vp, _vp, _vp, _i]),
     ("wb_hotpath", _i, [_vp, _vp, _d, _d, _vp, _vp, _i, _vp, _vp, _vp, _vp]),
     ("wb_hotpath_host", _i, [_vp, _vp, _d, _d, _vp, _vp, _i, _vp, _vp, _vp, _vp]),
@@ -213,6 +215,16 @@ class Context:
     def poisson_pcg(self, side: int, b, x, iters: int):
         self._check(self._L.wb_poisson_pcg(self._h, int(side), _ptr(b, self.n_p), _ptr(x, self.n_p), int(iters)))
         return x
+
+    def poisson_cheb(self, side: int, b, x, iters: int, lmin: float, lmax: float):
+        self._check(self._L.wb_poisson_cheb(self._h, int(side), _ptr(b, self.n_p), _ptr(x, self.n_p), int(iters),
+                                            float(lmin), float(lmax)))
+        return x
+
+    def poisson_eigmax(self, side: int, v0, iters: int) -> float:
+        lam = C.c_double(0.0)
+        self._check(self._L.wb_poisson_eigmax(self._h, int(side), _ptr(v0, self.n_p), int(iters), C.byref(lam)))
+        return lam.value
 
     def apply_wbfbt(self, r, z, iters: int):
         self._check(self._L.wb_apply_wbfbt(self._h, _ptr(r, self.n_p), _ptr(z, self.n_p), int(iters)))

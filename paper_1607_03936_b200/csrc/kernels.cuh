@@ -937,6 +937,57 @@ __global__ void k_pcg_out(const double* __restrict__ x, const double* __restrict
 
 // layout conversion element-major <-> mode-major (debug one-step entry)
 // element-major [e*nm + m] <-> PCG storage (PLay); to_soa: element-major -> PCG
+// ---------------------------------------------------------------- Chebyshev-Jacobi
+// One step of Saad's Alg. 12.1 after q = K d:  x += d; r -= q; d = c1 d + c2 (Minv r)
+// with the host-computed scalars c1 = rho' rho, c2 = 2 rho' / delta.  first: the start
+// d = c2 (Minv r) only (c2 = 1 / theta).  Pure streaming, no reduction.
+__global__ void __launch_bounds__(VBS) k_cheb(double* __restrict__ x, double* __restrict__ r, double* __restrict__ d,
+                                              const double* __restrict__ q, const double* __restrict__ Minv,
+                                              int64_t n, double c1, double c2, int first) {
+  const int64_t n2 = n / 2;  // n is even (PLay), 16-byte aligned vectors
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  double2* d2 = reinterpret_cast<double2*>(d);
+  const double2* q2 = reinterpret_cast<const double2*>(q);
+  const double2* M2 = reinterpret_cast<const double2*>(Minv);
+  for (int64_t j = (int64_t)blockIdx.x * VBS + threadIdx.x; j < n2; j += (int64_t)gridDim.x * VBS) {
+    const double2 m = M2[j];
+    double2 rv = r2[j];
+    if (first) {
+      d2[j] = make_double2(c2 * (m.x * rv.x), c2 * (m.y * rv.y));
+      continue;
+    }
+    const double2 dv = d2[j], qv = __ldcg(q2 + j);
+    double2 xv = x2[j];
+    xv.x += dv.x; xv.y += dv.y;
+    rv.x -= qv.x; rv.y -= qv.y;
+    x2[j] = xv;
+    r2[j] = rv;
+    d2[j] = make_double2(c1 * dv.x + c2 * (m.x * rv.x), c1 * dv.y + c2 * (m.y * rv.y));
+  }
+}
+
+// Power iteration (R16): partials of <w, w> with w = Minv o v (in place) when Minv != NULL,
+// else of <v, v>.  Deferred reduction as the PCG kernels (k_pow_scale sums the partials).
+__global__ void __launch_bounds__(VBS) k_pow_sumsq(double* __restrict__ v, const double* __restrict__ Minv,
+                                                   int64_t n, double* part) {
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS) {
+    double w = v[i];
+    if (Minv) { w *= Minv[i]; v[i] = w; }
+    s = fma(w, w, s);
+  }
+  store_partial<VBS>(s, part);
+}
+// out = in / ||in|| (||in|| = sqrt of the summed partials; 0 stays 0); block 0 stores ||in|| to *lam
+__global__ void __launch_bounds__(VBS) k_pow_scale(const double* in, double* out, int64_t n,
+                                                   const double* __restrict__ part, int npart, double* lam) {
+  const double nrm = sqrt(sum_partials<VBS>(part, npart));
+  if (blockIdx.x == 0 && threadIdx.x == 0) *lam = nrm;
+  for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS)
+    out[i] = nrm > 0.0 ? in[i] / nrm : 0.0;
+}
+
 __global__ void k_transpose(const double* __restrict__ in, double* __restrict__ out, int64_t ne, int nm, int to_soa,
                             PLay L, int N) {
   const int64_t n = ne * nm;

@@ -528,6 +528,70 @@ wb_status run_poisson(wb_ctx* c, int side, const double* b, double* x, int iters
   return WB_OK;
 }
 
+// x = P Cheb(K_side, P b) (R16): Saad Alg. 12.1 on Minv K, exactly iters steps.  The
+// direction d lives in c->pp (a TMA-mapped PCG buffer), K d goes through the Poisson
+// kernel in mode 2 ("p as is"; its p_new copy lands in c->pp1, unused); the scalars
+// are data-independent and computed here in the oracle's order.
+wb_status run_cheb(wb_ctx* c, int side, const double* b, double* x, int iters, double lmin, double lmax) {
+  const double* Minv = side == 0 ? c->MinvL : c->MinvR;
+  const int64_t n = c->pl.n;
+  k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->n_el, c->nm, c->partial, c->counter, c->scal + S_SUM);
+  LAUNCH_CHECK(c);
+  k_pcg_init<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->scal + S_SUM, c->px, c->pr, Minv, c->n_el, c->nm, c->rzp,
+                                                   nullptr, c->pl, c->N);
+  LAUNCH_CHECK(c);
+  const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin), sigma1 = theta / delta;
+  double rho = 1.0 / sigma1;
+  k_cheb<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, c->pp, nullptr, Minv, n, 0.0, 1.0 / theta, 1);
+  LAUNCH_CHECK(c);
+  for (int it = 0; it < iters; ++it) {
+    const double* pcur = nullptr;
+    int npq = 0;
+    wb_status s = run_K_pcg(c, side, 2, c->pp, c->pp1, nullptr, c->pq, PcgArgs{}, &pcur, &npq);
+    if (s) return s;
+    const double rho1 = 1.0 / (2.0 * sigma1 - rho);
+    k_cheb<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, c->pp, c->pq, Minv, n, rho1 * rho, 2.0 * rho1 / delta,
+                                                 0);
+    LAUNCH_CHECK(c);
+    rho = rho1;
+  }
+  k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pl.sm, 1, c->partial, c->counter, c->scal + S_SUM + 1);
+  LAUNCH_CHECK(c);
+  k_pcg_out<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->scal + S_SUM + 1, x, c->n_el, c->nm, c->pl, c->N);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+
+// *lam = power-iteration estimate of the largest |eigenvalue| of Minv K_side (R16):
+// v = v0 / ||v0||; iters x { w = Minv (K v); lam = ||w||; v = w / lam }.  v in c->pp.
+wb_status run_eigmax(wb_ctx* c, int side, const double* v0, int iters, double* lam) {
+  const double* Minv = side == 0 ? c->MinvL : c->MinvR;
+  const int64_t n = c->pl.n;
+  const int nb = c->red_blocks;
+  double* dlam = c->scal + S_SCR;
+  CUDA_TRY(c, cudaMemsetAsync(c->pp, 0, sizeof(double) * n, c->stream));  // pads stay 0
+  k_transpose<<<nb, VBS, 0, c->stream>>>(v0, c->pp, c->n_el, c->nm, 1, c->pl, c->N);
+  LAUNCH_CHECK(c);
+  k_pow_sumsq<<<nb, VBS, 0, c->stream>>>(c->pp, nullptr, n, c->rzp);
+  LAUNCH_CHECK(c);
+  k_pow_scale<<<nb, VBS, 0, c->stream>>>(c->pp, c->pp, n, c->rzp, nb, dlam);
+  LAUNCH_CHECK(c);
+  CUDA_TRY(c, cudaMemsetAsync(dlam, 0, sizeof(double), c->stream));  // lam = 0 for iters = 0 (as the oracle)
+  for (int it = 0; it < iters; ++it) {
+    const double* pcur = nullptr;
+    int npq = 0;
+    wb_status s = run_K_pcg(c, side, 2, c->pp, c->pp1, nullptr, c->pq, PcgArgs{}, &pcur, &npq);
+    if (s) return s;
+    k_pow_sumsq<<<nb, VBS, 0, c->stream>>>(c->pq, Minv, n, c->rzp);
+    LAUNCH_CHECK(c);
+    k_pow_scale<<<nb, VBS, 0, c->stream>>>(c->pq, c->pp, n, c->rzp, nb, dlam);
+    LAUNCH_CHECK(c);
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(lam, dlam, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return WB_OK;
+}
+
 // q = K_side p, element-major in and out (through the PCG kernels, mode "p as is")
 wb_status run_K(wb_ctx* c, int side, const double* p, double* q) {
   k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(p, c->pp, c->n_el, c->nm, 1, c->pl, c->N);
@@ -923,6 +987,23 @@ wb_status wb_poisson_pcg(wb_ctx* c, int side, const double* b, double* x, int it
   if (!b || !x || (side != 0 && side != 1) || iters < 0) return set_err(c, WB_EINVAL, "bad argument");
   if (overlaps(b, 8 * c->n_p, x, 8 * c->n_p)) return set_err(c, WB_EALIAS, "b and x overlap");
   return run_poisson(c, side, b, x, iters);
+}
+
+wb_status wb_poisson_cheb(wb_ctx* c, int side, const double* b, double* x, int iters, double lmin, double lmax) {
+  wb_status s = check_ctx(c, true);
+  if (s) return s;
+  if (!b || !x || (side != 0 && side != 1) || iters < 0) return set_err(c, WB_EINVAL, "bad argument");
+  if (!(lmin > 0.0) || !(lmax > lmin) || !std::isfinite(lmax))
+    return set_err(c, WB_EINVAL, "the interval must satisfy 0 < lmin < lmax < inf");
+  if (overlaps(b, 8 * c->n_p, x, 8 * c->n_p)) return set_err(c, WB_EALIAS, "b and x overlap");
+  return run_cheb(c, side, b, x, iters, lmin, lmax);
+}
+
+wb_status wb_poisson_eigmax(wb_ctx* c, int side, const double* v0, int iters, double* lmax) {
+  wb_status s = check_ctx(c, true);
+  if (s) return s;
+  if (!v0 || !lmax || (side != 0 && side != 1) || iters < 0) return set_err(c, WB_EINVAL, "bad argument");
+  return run_eigmax(c, side, v0, iters, lmax);
 }
 
 wb_status wb_apply_wbfbt(wb_ctx* c, const double* r, double* z, int iters) {
