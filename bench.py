@@ -273,6 +273,15 @@ def run_ours(args):
     tK = timed(lambda: ctx.apply_K(1, p, qv))
     tW = timed(lambda: ctx.apply_wbfbt(p, z, iters), reps=max(3, args.comp_reps // 4))
     tS = timed(lambda: ctx.set_viscosity(mu), reps=max(3, args.comp_reps // 4))
+    # ---- Chebyshev-accelerated Jacobi as the inner solve (side r), on the
+    # interval [0.1, 1.1] x a 20-step power-iteration estimate (R16); per-iteration time
+    # from graph replays, (t(50) - t(10)) / 40, warm
+    v0 = torch.as_tensor(np.random.default_rng(7).standard_normal(ctx.n_p), **f64)
+    lam = ctx.poisson_eigmax(1, v0, 20)
+    t_eig = timed(lambda: ctx.poisson_eigmax(1, v0, 20), reps=3)
+    t_cheb = {it: timed(lambda: ctx.poisson_cheb(1, p, qv, it, 0.1 * lam, 1.1 * lam), reps=5, cold=False)
+              for it in (10, 50, iters)}
+    cheb_iter_us = (t_cheb[50] - t_cheb[10]) / 40 * 1e3
     # ---- dominant kernel: the fused Poisson operator inside the PCG loops (2 x iters
     # launches per step).  Profiled pass: the same hot-path step with a CUDA-event
     # pair around every such launch (library option "profile": plain launches on
@@ -351,7 +360,11 @@ def run_ours(args):
                     "A_ms_warm": tAw, "A_gdofs_warm": n_v / (tAw * 1e-3) / 1e9,
                     "B_gdofs": n_v / (tB * 1e-3) / 1e9, "BT_gdofs": n_v / (tBT * 1e-3) / 1e9,
                     "K_ms_cold": tK, "K_ms_warm": tKw, "wbfbt_ms": tW, "wbfbt_applies_per_s": 1e3 / tW,
-                    "setup_ms": tS},
+                    "setup_ms": tS,
+                    "cheb": {"iter_us": cheb_iter_us, "solve_ms": t_cheb[iters], "iters": iters,
+                             "interval": [0.1 * lam, 1.1 * lam], "eigmax_20_ms": t_eig,
+                             "k_cheb_bytes_per_launch": 64 * n_p,
+                             "note": "SURVEY 8(f) #2 (not in the step): x = P Cheb(K_r, P b), R16"}},
                 "roofline": roof,
                 "e2e": {"value": e2e, "unit": "hot-path steps/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h},

@@ -331,15 +331,18 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
   // first tile's loads first: they do not depend on the control scalars, so the
   // reduction of the previous kernel's partials below overlaps them
   int tile = blockIdx.x;
+  // mode 2 (q = K p_old as is): only the p box is loaded and p_new is not stored
+  const bool pz = (mode & 0xff) != 2;
+  const unsigned rawb = pz ? RAWB : K::PBYTES;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); mbar_init(&bar[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (tile < n_tiles) {
       int ex0, ey0, ez0;
       coords(tile, ex0, ey0, ez0);
-      mbar_expect_tx(&bar[0], RAWB);
-      tma_load_4d(Zb, &tm_z, ey0, ez0 - 1, ex0 - 1, 0, &bar[0]);  // y from ey0 - 1 + pad
-      if (!ZB) tma_load_4d(Mb, &tm_minv, ey0, ez0 - 1, ex0 - 1, 0, &bar[0]);
+      mbar_expect_tx(&bar[0], rawb);
+      if (pz) tma_load_4d(Zb, &tm_z, ey0, ez0 - 1, ex0 - 1, 0, &bar[0]);  // y from ey0 - 1 + pad
+      if (pz && !ZB) tma_load_4d(Mb, &tm_minv, ey0, ez0 - 1, ex0 - 1, 0, &bar[0]);
       tma_load_4d(Pb, &tm_pold, ey0, ez0 - 1, ex0 - 1, 0, &bar[0]);
       mbar_expect_tx(&bar[2], K::XBYTES);
       bulk_load(Xs, XT + (size_t)tile * K::XTB, K::XBYTES, &bar[2]);
@@ -396,9 +399,9 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     lap(2);
     if (threadIdx.x == K::TMA_T && next < n_tiles) {  // raw p, r, Minv buffers are free
       fence_proxy_async();
-      mbar_expect_tx(&bar[0], RAWB);
-      tma_load_4d(Zb, &tm_z, ny0, nz0 - 1, nx0 - 1, 0, &bar[0]);
-      if (!ZB) tma_load_4d(Mb, &tm_minv, ny0, nz0 - 1, nx0 - 1, 0, &bar[0]);
+      mbar_expect_tx(&bar[0], rawb);
+      if (pz) tma_load_4d(Zb, &tm_z, ny0, nz0 - 1, nx0 - 1, 0, &bar[0]);
+      if (pz && !ZB) tma_load_4d(Mb, &tm_minv, ny0, nz0 - 1, nx0 - 1, 0, &bar[0]);
       tma_load_4d(Pb, &tm_pold, ny0, nz0 - 1, nx0 - 1, 0, &bar[0]);
     }
     lap(7);
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
           const double pv = Ps[m * K::NHP + h];
           const int64_t j = L.at(m, ex, ey, ez);
           if (!(dbg & 0x800)) q[j] = o;
-          if (!(dbg & 0x1000)) pnew[j] = pv;
+          if (pz && !(dbg & 0x1000)) pnew[j] = pv;
           dot = fma(pv, o, dot);
         }
       }

@@ -44,7 +44,13 @@ struct wb_ctx {
   PLay pl = {};        // storage of the PCG vectors (kernels.cuh)
   bool ylay = false;   // y-fastest padded PCG storage: contexts of the TMA Poisson kernel
   // CUDA graphs of the PCG iteration loop, keyed by (side, iters)
-  struct GraphEntry { int side = 0, iters = 0; long long n_launch = 0; cudaGraphExec_t exec = nullptr; };
+  // a captured loop: kind 0 = PCG iterations, 1 = Chebyshev iterations (interval lo, hi)
+  struct GraphEntry {
+    int kind = 0, side = 0, iters = 0;
+    double lo = 0.0, hi = 0.0;
+    long long n_launch = 0;
+    cudaGraphExec_t exec = nullptr;
+  };
   static constexpr int MAX_GRAPHS = 8;
   GraphEntry graphs[MAX_GRAPHS];
   int n_graphs = 0;
@@ -414,7 +420,7 @@ wb_status run_K_pcg(wb_ctx* c, int side, int mode, const double* pold, double* p
   const double* Minv = side == 0 ? c->MinvL : c->MinvR;
   const double* X = side == 0 ? c->Cinv : c->Dinv;
   if (c->k == 2) {
-    *pcur = pnew;
+    *pcur = mode == 2 ? pold : pnew;  // (mode 2 leaves p as is; the TMA kernel then skips the copy)
     return run_k2f(c, pold, pnew, r, Minv, X, q, mode, a, npq);
   }
   // generic k: direction update pold -> pnew (+ control), then B^T (element + gather) and B (+ dot)
@@ -478,12 +484,16 @@ void clear_graphs(wb_ctx* c) {
   c->n_graphs = 0;
 }
 
-// replay of the iteration loop as one CUDA graph (captured on a private stream)
-wb_status pcg_loop(wb_ctx* c, int side, int iters) {
-  if (!c->use_graph || c->profile || iters == 0 || !c->cap_stream) return pcg_loop_direct(c, side, iters);
+// replay of an iteration loop as one CUDA graph (captured on a private stream), keyed
+// by (kind, side, iters, lo, hi); `direct` issues the loop's launches on c->stream
+template <class F>
+wb_status graph_loop(wb_ctx* c, int kind, int side, int iters, double lo, double hi, F direct) {
+  if (!c->use_graph || c->profile || iters == 0 || !c->cap_stream) return direct();
   wb_ctx::GraphEntry* g = nullptr;
-  for (int i = 0; i < c->n_graphs; ++i)
-    if (c->graphs[i].side == side && c->graphs[i].iters == iters) g = &c->graphs[i];
+  for (int i = 0; i < c->n_graphs; ++i) {
+    const wb_ctx::GraphEntry& e = c->graphs[i];
+    if (e.kind == kind && e.side == side && e.iters == iters && e.lo == lo && e.hi == hi) g = &c->graphs[i];
+  }
   if (!g) {
     if (c->n_graphs == wb_ctx::MAX_GRAPHS) clear_graphs(c);
     g = &c->graphs[c->n_graphs];
@@ -491,7 +501,7 @@ wb_status pcg_loop(wb_ctx* c, int side, int iters) {
     const long long l0 = c->launches;
     CUDA_TRY(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
     c->stream = c->cap_stream;
-    wb_status s = pcg_loop_direct(c, side, iters);
+    wb_status s = direct();
     c->stream = saved;
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(c->cap_stream, &graph);
@@ -500,13 +510,18 @@ wb_status pcg_loop(wb_ctx* c, int side, int iters) {
     e = cudaGraphInstantiate(&g->exec, graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return set_err(c, WB_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
-    g->side = side; g->iters = iters; g->n_launch = c->launches - l0;
+    g->kind = kind; g->side = side; g->iters = iters; g->lo = lo; g->hi = hi;
+    g->n_launch = c->launches - l0;
     c->launches = l0;
     ++c->n_graphs;
   }
   CUDA_TRY(c, cudaGraphLaunch(g->exec, c->stream));
   c->launches += g->n_launch;
   return WB_OK;
+}
+
+wb_status pcg_loop(wb_ctx* c, int side, int iters) {
+  return graph_loop(c, 0, side, iters, 0.0, 0.0, [&] { return pcg_loop_direct(c, side, iters); });
 }
 
 // x = P PCG(K_side, P b), exactly `iters` iterations (b, x element-major)
@@ -528,6 +543,25 @@ wb_status run_poisson(wb_ctx* c, int side, const double* b, double* x, int iters
   return WB_OK;
 }
 
+// the Chebyshev iterations proper (Saad Alg. 12.1 steps after the start d), on c->stream
+wb_status cheb_loop_direct(wb_ctx* c, int side, int iters, double lmin, double lmax) {
+  const double* Minv = side == 0 ? c->MinvL : c->MinvR;
+  const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin), sigma1 = theta / delta;
+  double rho = 1.0 / sigma1;
+  for (int it = 0; it < iters; ++it) {
+    const double* pcur = nullptr;
+    int npq = 0;
+    wb_status s = run_K_pcg(c, side, 2, c->pp, c->pp1, nullptr, c->pq, PcgArgs{}, &pcur, &npq);
+    if (s) return s;
+    const double rho1 = 1.0 / (2.0 * sigma1 - rho);
+    k_cheb<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, c->pp, c->pq, Minv, c->pl.n, rho1 * rho,
+                                                 2.0 * rho1 / delta, 0);
+    LAUNCH_CHECK(c);
+    rho = rho1;
+  }
+  return WB_OK;
+}
+
 // x = P Cheb(K_side, P b) (R16): Saad Alg. 12.1 on Minv K, exactly iters steps.  The
 // direction d lives in c->pp (a TMA-mapped PCG buffer), K d goes through the Poisson
 // kernel in mode 2 ("p as is"; its p_new copy lands in c->pp1, unused); the scalars
@@ -540,21 +574,11 @@ wb_status run_cheb(wb_ctx* c, int side, const double* b, double* x, int iters, d
   k_pcg_init<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->scal + S_SUM, c->px, c->pr, Minv, c->n_el, c->nm, c->rzp,
                                                    nullptr, c->pl, c->N);
   LAUNCH_CHECK(c);
-  const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin), sigma1 = theta / delta;
-  double rho = 1.0 / sigma1;
+  const double theta = 0.5 * (lmax + lmin);
   k_cheb<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, c->pp, nullptr, Minv, n, 0.0, 1.0 / theta, 1);
   LAUNCH_CHECK(c);
-  for (int it = 0; it < iters; ++it) {
-    const double* pcur = nullptr;
-    int npq = 0;
-    wb_status s = run_K_pcg(c, side, 2, c->pp, c->pp1, nullptr, c->pq, PcgArgs{}, &pcur, &npq);
-    if (s) return s;
-    const double rho1 = 1.0 / (2.0 * sigma1 - rho);
-    k_cheb<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, c->pp, c->pq, Minv, n, rho1 * rho, 2.0 * rho1 / delta,
-                                                 0);
-    LAUNCH_CHECK(c);
-    rho = rho1;
-  }
+  wb_status s = graph_loop(c, 1, side, iters, lmin, lmax, [&] { return cheb_loop_direct(c, side, iters, lmin, lmax); });
+  if (s) return s;
   k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pl.sm, 1, c->partial, c->counter, c->scal + S_SUM + 1);
   LAUNCH_CHECK(c);
   k_pcg_out<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->scal + S_SUM + 1, x, c->n_el, c->nm, c->pl, c->N);
