@@ -69,6 +69,7 @@ def lib():
             L.or_wbfbt.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, _D, _D, C.c_int]
             L.or_poisson_relres.restype = C.c_double
             L.or_poisson_relres.argtypes = [C.c_void_p, _D, _D, _D]
+            L.or_grad_weights.argtypes = [C.c_void_p, _D, _D]
             L.or_cheb_dense.argtypes = [C.c_int64, _D, _D, _D, _D, C.c_int, C.c_double, C.c_double]
             L.or_poisson_cheb.argtypes = [C.c_void_p, _D, _D, _D, _D, C.c_int, C.c_double, C.c_double]
             L.or_eigmax_dense.argtypes = [C.c_int64, _D, _D, _D, C.c_int]
@@ -264,11 +265,22 @@ class Oracle:
         Xinv, b, x = _f64(Xinv), _f64(b), _f64(x)
         return float(self.L.or_poisson_relres(self.h, _p(Xinv), _p(b), _p(x)))
 
+    def grad_weights(self, mu_q) -> np.ndarray:
+        """mu_eff = sqrt(mu^2 + |grad mu|^2) at the Gauss points (rmk:wbfbt-visc-grad, R17):
+        lumping mu_eff (weight sqrt(mu_eff)) gives the viscosity-gradient wBFBT weights."""
+        mu_q = _f64(mu_q)
+        out = np.zeros_like(mu_q)
+        self.L.or_grad_weights(self.h, _p(mu_q), _p(out))
+        return out
+
     # ---- composite
-    def setup(self, mu_q, a_l=1.0, a_r=1.0) -> dict:
-        """Lumped diagonals and both Jacobi diagonals (rows a3, a4)."""
+    def setup(self, mu_q, a_l=1.0, a_r=1.0, weights="sqrt") -> dict:
+        """Lumped diagonals and both Jacobi diagonals (rows a3, a4).  weights: "sqrt"
+        (w = sqrt(mu), eq:wbfbt) or "grad" (w = (mu^2 + |grad mu|^2)^(1/4), rmk:wbfbt-visc-grad);
+        A always uses mu itself."""
         self.mu_q = _f64(mu_q)
-        lm = self.lumped(self.mu_q, a_l, a_r)
+        assert weights in ("sqrt", "grad")
+        lm = self.lumped(self.mu_q if weights == "sqrt" else self.grad_weights(self.mu_q), a_l, a_r)
         lm["diagKl"] = self.jacobi_diag(lm["Cinv"])
         lm["diagKr"] = self.jacobi_diag(lm["Dinv"])
         self.state = lm

@@ -444,6 +444,36 @@ void or_lumped(or_ctx* c, const double* mu_q, double a_l, double a_r,
   }
 }
 
+/* Viscosity-gradient wBFBT weights (rmk:wbfbt-visc-grad):
+ *   w_l = w_r = (mu^2 + |grad mu|^2)^{1/4}.
+ * mu is given only at the Gauss points, so grad mu is the gradient of the element's
+ * tensor-product Lagrange interpolant through its (k+1)^3 Gauss-point samples,
+ * d/dx_d = (2/h) d/dxi_d (reading R17).  Returned as mu_eff = sqrt(mu^2 + |grad mu|^2)
+ * = w^2, so that or_lumped(mu_eff) lumps with its weight sqrt(mu_eff) = w.        */
+void or_grad_weights(const or_ctx* c, const double* mu_q, double* mu_eff) {
+  const int n1 = c->n1, nq = c->nq;
+  double D[OR_MAXN1][OR_MAXN1]; /* D[i][j] = l_j'(xg_i), Lagrange basis on the Gauss points */
+  for (int i = 0; i < n1; ++i)
+    for (int j = 0; j < n1; ++j) D[i][j] = (double)dlagrange(c->xg, n1, j, c->xg[i]);
+  const double s = 2.0 / c->h;
+  for (int64_t e = 0; e < c->n_el; ++e) {
+    const double* m = mu_q + e * nq;
+    for (int qz = 0; qz < n1; ++qz)
+      for (int qy = 0; qy < n1; ++qy)
+        for (int qx = 0; qx < n1; ++qx) {
+          double gx = 0.0, gy = 0.0, gz = 0.0;
+          for (int j = 0; j < n1; ++j) {
+            gx += D[qx][j] * m[j + n1 * (qy + n1 * qz)];
+            gy += D[qy][j] * m[qx + n1 * (j + n1 * qz)];
+            gz += D[qz][j] * m[qx + n1 * (qy + n1 * j)];
+          }
+          gx *= s; gy *= s; gz *= s;
+          const double mu = m[qx + n1 * (qy + n1 * qz)];
+          mu_eff[e * nq + qx + n1 * (qy + n1 * qz)] = sqrt(mu * mu + (gx * gx + gy * gy + gz * gz));
+        }
+  }
+}
+
 /* ---------------------------------------------------------------- K_w, diag
  * K p = B (Xinv o (B^T p)), Xinv a nodal diagonal acting on all 3 components
  * (PAPER.md:2453-2461).                                                       */
