@@ -172,9 +172,14 @@ wb_status wb_get_jacobi(wb_ctx* ctx, double* diagKl, double* diagKr);
  * flag or before a solve, WB_EINVAL for i outside [0, n)), "kz" (1 if the PCG
  * update stores z = Minv r for the TMA Poisson kernel), "k_tma" (1 if
  * the k = 2 Poisson operator runs as the TMA kernel for this mesh), "k_ws" (1 if
- * it runs as the warp-specialised TMA kernel). */
+ * it runs as the warp-specialised TMA kernel), "weights" (the option below). */
 wb_status wb_query(wb_ctx* ctx, const char* key, double* value);
-/* Tuning knobs (results are identical up to rounding for every setting):
+/* Method option (changes the results): "weights", the wBFBT weights the next
+ * wb_set_viscosity lumps: 0 = w_l = w_r = sqrt(mu), eq:wbfbt, the default; 1 = the
+ * viscosity-gradient weights (mu^2 + |grad mu|^2)^(1/4) of rmk:wbfbt-visc-grad,
+ * PAPER.md:2132-2150, with grad mu that of each element's Gauss-point interpolant
+ * (reading R17); A keeps mu.
+ * Tuning knobs (results are identical up to rounding for every setting):
  * "kz" (k = 2 TMA Poisson kernel: 1 = the PCG update stores z = Minv r and the
  * kernel loads it as one box; 0 = it loads r and Minv, the default),
  * "k_ws" (k = 2 TMA Poisson kernel: 1 = warp-specialised, producer warps build

@@ -14,13 +14,14 @@ __constant__ double c_J2[27][4];
 
 // One thread per element, one read of its 27 mu samples:
 //   mutT[tile][q][le] = mu w_q h/2          (A's tile-blocked layout, as k_prescale for k = 3, 4)
-//   L[a][e] = detJ sum_q sqrt(mu_q) phi_a(xi_q) w_q   (eq:lumping)
+//   L[a][e] = detJ sum_q sqrt(mu_q) phi_a(xi_q) w_q   (eq:lumping),
+//   with mu_eff = wsrc in the square root when given (R17)
 // with L sum-factorised (x, y, z passes of the 1-D factor W1[a][i] = phi_a(xg_i) w_i).
 // Nonpositive or non-finite mu samples are counted in bad (the caller rejects them).
 template <int TX, int TY, int TZ>
 __global__ void __launch_bounds__(128) k_setup_mu2(const double* __restrict__ mu, double* __restrict__ mutT,
                                                    double* __restrict__ L, int N, double hs, double detJ,
-                                                   unsigned long long* bad) {
+                                                   unsigned long long* bad, const double* __restrict__ wsrc) {
   constexpr int NE = TX * TY * TZ;
   const int64_t ne = (int64_t)N * N * N;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -37,7 +38,7 @@ __global__ void __launch_bounds__(128) k_setup_mu2(const double* __restrict__ mu
     if (!(m > 0.0) || !isfinite(m)) ++nbad;
     const double wq = TB(2).w[q % 3] * TB(2).w[(q / 3) % 3] * TB(2).w[q / 9];
     mutT[((int64_t)tile * 27 + q) * NE + le] = m * wq * hs;
-    s[q] = sqrt(m);
+    s[q] = sqrt(wsrc ? wsrc[e * 27 + q] : m);  // wsrc: the gradient weights' mu_eff (R17)
   }
   if (nbad) atomicAdd(bad, (unsigned long long)nbad);
   // x pass: t1[qz][qy][ax] = sum_qx W1[ax][qx] s[qz][qy][qx]

@@ -633,6 +633,31 @@ __global__ void k_lump_elem(const double* __restrict__ mu, double* __restrict__ 
   }
 }
 
+// Viscosity-gradient weights (rmk:wbfbt-visc-grad; R17), one thread per
+// Gauss point: grad mu of the element's Gauss-point interpolant (collocation derivative
+// Dg along each axis, times s = 2/h) and out = sqrt(mu^2 + |grad mu|^2) = w^2, which the
+// lumping kernels turn into the weight sqrt(out) = w.
+template <int K>
+__global__ void __launch_bounds__(256) k_grad_weights(const double* __restrict__ mu, double* __restrict__ out,
+                                                      int64_t n, double s) {
+  constexpr int n1 = K + 1, NQ = Ord<K>::NQ;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int q = (int)(i % NQ);
+  const double* m = mu + (i - q);
+  const int qx = q % n1, qy = (q / n1) % n1, qz = q / (n1 * n1);
+  double gx = 0.0, gy = 0.0, gz = 0.0;
+#pragma unroll
+  for (int j = 0; j < n1; ++j) {
+    gx = fma(TB(K).Dg[qx][j], __ldg(m + j + n1 * (qy + n1 * qz)), gx);
+    gy = fma(TB(K).Dg[qy][j], __ldg(m + qx + n1 * (j + n1 * qz)), gy);
+    gz = fma(TB(K).Dg[qz][j], __ldg(m + qx + n1 * (qy + n1 * j)), gz);
+  }
+  gx *= s; gy *= s; gz *= s;
+  const double v = m[q];
+  out[i] = sqrt(fma(v, v, fma(gx, gx, fma(gy, gy, gz * gz))));
+}
+
 // C[g] = sum_{e ni g} a_l(e) L[a(e,g)][e] (eq:bdramp PAPER.md:2232-2245), ascending e.
 // Xinv = mask / X; nonpositive interior entries counted (integer atomics).
 template <int K>

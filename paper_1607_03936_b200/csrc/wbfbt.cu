@@ -71,6 +71,8 @@ struct wb_ctx {
   // k = 2 tile-assembled A (4x4x4 tiles): upper-shell and lower-face node partials
   // (L2-resident), summed by the skeleton kernel; mut is tile-blocked for k = 2
   double* Fu = nullptr;
+  double* mueff = nullptr;  // n_el * n_q: the viscosity-gradient weights' mu_eff (option "weights" 1, R17)
+  int weights = 0;
   int n_tiles = 0;
   int use_graph = 1;
   int k_var = 1;  // k = 2 fused K variant: 0 = 2 CTAs/SM (register-capped), 1 = 1 CTA/SM (faster: L1 left free)
@@ -655,7 +657,7 @@ wb_status check_ctx(wb_ctx* c, bool need_visc) {
 void free_all(wb_ctx* c) {
   double** bufs[] = {&c->mut, &c->Cw, &c->Dw, &c->Cinv, &c->Dinv, &c->dKl, &c->dKr, &c->MinvL, &c->MinvR,
                      &c->E, &c->tv, &c->tw, &c->px, &c->pr, &c->pp, &c->pp1, &c->pq, &c->pz, &c->s0, &c->s1, &c->s2,
-                     &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->Fu};
+                     &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->Fu, &c->mueff};
   clear_graphs(c);
   if (c->cap_stream) { cudaStreamDestroy(c->cap_stream); c->cap_stream = nullptr; }
   if (c->copy_stream) { cudaStreamDestroy(c->copy_stream); c->copy_stream = nullptr; }
@@ -902,9 +904,20 @@ template <int K>
 static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
   const int64_t nmu = c->n_el * c->nq;
   CUDA_TRY(c, cudaMemsetAsync(c->icount, 0, sizeof(unsigned long long) * 4, c->stream));
+  const double* wsrc = nullptr;  // lumping weight source: mu (eq:wbfbt) or mu_eff (R17)
+  if (c->weights == 1) {
+    if (!c->mueff && cudaMalloc(&c->mueff, sizeof(double) * nmu) != cudaSuccess) {
+      cudaGetLastError();
+      c->mueff = nullptr;
+      return set_err(c, WB_ENOMEM, "gradient-weight buffer allocation failed");
+    }
+    k_grad_weights<K><<<nblk(nmu, 256), 256, 0, c->stream>>>(mu, c->mueff, nmu, 2.0 / c->h);
+    LAUNCH_CHECK(c);
+    wsrc = c->mueff;
+  }
   if constexpr (K == 2)  // mut and the element lumping values in one pass over mu
     k_setup_mu2<A_TX, A_TY, A_TZ><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(mu, c->mut, c->E, c->N, c->h / 2,
-                                                                            c->detJ, c->icount);
+                                                                            c->detJ, c->icount, wsrc);
   else
     k_prescale<K><<<nblk(nmu, 256), 256, 0, c->stream>>>(mu, c->mut, nmu, c->h / 2, c->icount);
   LAUNCH_CHECK(c);
@@ -921,7 +934,7 @@ static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
     k_lump_node2<<<grid, dim3(64, 4), 0, c->stream>>>(c->E, a_l, a_r, c->Cw, c->Dw, c->Cinv, c->Dinv,
                                                      c->icount + 1, c->G);
   } else {
-    k_lump_elem<K><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(mu, c->E, c->G, c->detJ);
+    k_lump_elem<K><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(wsrc ? wsrc : mu, c->E, c->G, c->detJ);
     LAUNCH_CHECK(c);
     k_lump_node<K><<<nblk(c->n_nodes, 256), 256, 0, c->stream>>>(c->E, a_l, a_r, c->Cw, c->Dw, c->Cinv, c->Dinv,
                                                                  c->icount + 1, c->G);
@@ -1186,7 +1199,7 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
   if (!strcmp(key, "n_nonpos_Cw") || !strcmp(key, "n_nonpos_Dw")) {
     wb_status s = read_nonpos(c);
     if (s) return s;
-    *value = (double)c->n_nonpos[key[10] == 'C' ? 0 : 1];
+    *value = (double)c->n_nonpos[key[9] == 'C' ? 0 : 1];  // "n_nonpos_Cw"[9] == 'C'
   }
   else if (!strcmp(key, "n_el")) *value = (double)c->n_el;
   else if (!strcmp(key, "n_p")) *value = (double)c->n_p;
@@ -1243,6 +1256,8 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
     *value = (tma_active(c) && c->kz) ? 1.0 : 0.0;
   } else if (!strcmp(key, "k_tma")) {  // 1: the Poisson operator runs as the TMA kernel (k_K2_tma)
     *value = tma_active(c) ? 1.0 : 0.0;
+  } else if (!strcmp(key, "weights")) {
+    *value = c->weights;
   } else if (!strcmp(key, "k_ws")) {  // 1: ... as the warp-specialised TMA kernel (k_K2_ws)
     *value = (tma_active(c) && c->k_ws) ? 1.0 : 0.0;
   } else if (!strcmp(key, "occ_a2")) {
@@ -1324,6 +1339,9 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "kz must be 0 or 1");
     c->kz = (int)value;
     clear_graphs(c);
+  } else if (!strcmp(key, "weights")) {  // wBFBT weights of the next wb_set_viscosity (R17)
+    if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "weights must be 0 or 1");
+    c->weights = (int)value;
   } else if (!strcmp(key, "k_ws")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k_ws must be 0 or 1");
     c->k_ws = (int)value;

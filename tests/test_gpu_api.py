@@ -270,3 +270,17 @@ def test_large_poisson_paths_ragged_tiles(N):
     for x in xs[1:]:
         assert np.array_equal(xs[0], x)
     assert rel_l2(xs[0], p.o.poisson(st["Dinv"], st["diagKr"], b, 5)) <= 1e-12
+
+
+def test_nonpos_counts_per_side():
+    """n_nonpos_Cw / n_nonpos_Dw count their own side (a_l != a_r makes them differ):
+    each equals the number of nonpositive interior entries of the returned array."""
+    p = Pair("C3", N=12, a_l=1.0, a_r=3.0)
+    Cw, Dw = empty(p.ctx.n_nodes), empty(p.ctx.n_nodes)
+    p.ctx.get_lumped(Cw, Dw)
+    interior = p.o.boundary_mask()[:p.ctx.n_nodes] == 0
+    nc = int(np.sum((host(Cw) <= 0) & interior))
+    nd = int(np.sum((host(Dw) <= 0) & interior))
+    assert nc != nd
+    assert p.ctx.query("n_nonpos_Cw") == nc
+    assert p.ctx.query("n_nonpos_Dw") == nd
