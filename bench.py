@@ -273,6 +273,11 @@ def run_ours(args):
     tK = timed(lambda: ctx.apply_K(1, p, qv))
     tW = timed(lambda: ctx.apply_wbfbt(p, z, iters), reps=max(3, args.comp_reps // 4))
     tS = timed(lambda: ctx.set_viscosity(mu), reps=max(3, args.comp_reps // 4))
+    # ---- setup with the viscosity-gradient weights (R17)
+    ctx.set_option("weights", 1)
+    tSg = timed(lambda: ctx.set_viscosity(mu), reps=max(3, args.comp_reps // 4))
+    ctx.set_option("weights", 0)
+    ctx.set_viscosity(mu)
     # ---- Chebyshev-accelerated Jacobi as the inner solve (side r), on the
     # interval [0.1, 1.1] x a 20-step power-iteration estimate (R16); per-iteration time
     # from graph replays, (t(50) - t(10)) / 40, warm
@@ -360,7 +365,7 @@ def run_ours(args):
                     "A_ms_warm": tAw, "A_gdofs_warm": n_v / (tAw * 1e-3) / 1e9,
                     "B_gdofs": n_v / (tB * 1e-3) / 1e9, "BT_gdofs": n_v / (tBT * 1e-3) / 1e9,
                     "K_ms_cold": tK, "K_ms_warm": tKw, "wbfbt_ms": tW, "wbfbt_applies_per_s": 1e3 / tW,
-                    "setup_ms": tS,
+                    "setup_ms": tS, "setup_grad_weights_ms": tSg,
                     "cheb": {"iter_us": cheb_iter_us, "solve_ms": t_cheb[iters], "iters": iters,
                              "interval": [0.1 * lam, 1.1 * lam], "eigmax_20_ms": t_eig,
                              "k_cheb_bytes_per_launch": 64 * n_p,
