@@ -327,6 +327,91 @@ __global__ void __launch_bounds__(BS) k_B(const double* __restrict__ u, const do
   (void)counter; (void)total;
 }
 
+// Same B with EPB elements per block and one thread per (element, component c, z-node
+// az): the thread contracts its (ax, ay) plane to Y[m1][m2] and parks it in shared
+// memory; thread (element, m) then runs the z-contraction over (c, az) in the order of
+// k_B (c outer, az inner, the same fma chain), so the two kernels agree bit for bit.
+// 3(K+1) times the threads of k_B: at k = 4 (C4, 13.8k elements) k_B fills a third of
+// the SMs with one warp each.  Dot partials (dv) as k_B, one per block.
+template <int K, int EPB>
+struct BSplit {
+  static constexpr int NT = (EPB * 3 * (K + 1) + 31) / 32 * 32;  // whole warps (block_sum)
+};
+template <int K, int EPB>
+__global__ void __launch_bounds__(BSplit<K, EPB>::NT) k_B_split(const double* __restrict__ u,
+                                                              const double* __restrict__ xs, double* __restrict__ p,
+                                                              Geo G, double sB, int nomask,
+                                                              const int* __restrict__ stop,
+                                                              const double* __restrict__ dv, double* partial,
+                                                              int64_t se, int64_t sm) {
+  constexpr int n1 = K + 1, NM = Ord<K>::NM, NY = K * (K + 1) / 2, NT = BSplit<K, EPB>::NT;
+  __shared__ double Ys[EPB][3 * n1][NY];
+  if (stop && *stop) return;
+  const int el = threadIdx.x % EPB, slab = threadIdx.x / EPB;  // slab = c * n1 + az
+  const int c = slab / n1, az = slab % n1;
+  const int64_t e = (int64_t)blockIdx.x * EPB + el;
+  if (slab < 3 * n1 && e < G.n_el) {
+    int ex, ey, ez;
+    elem_xyz(e, G.N, ex, ey, ez);
+    double Y[NY];
+#pragma unroll
+    for (int i = 0; i < NY; ++i) Y[i] = 0.0;
+    const int gz = K * ez + az;
+#pragma unroll
+    for (int ay = 0; ay < n1; ++ay) {
+      const int gy = K * ey + ay;
+      double v[n1];
+#pragma unroll
+      for (int ax = 0; ax < n1; ++ax) {
+        const int gx = K * ex + ax;
+        const int64_t g = node_id(gx, gy, gz, G.nn1);
+        double val = u[c * G.n_nodes + g];
+        if (xs) val *= xs[g];
+        else if (!nomask && node_bnd(gx, gy, gz, G.nn1)) val = 0.0;
+        v[ax] = val;
+      }
+      double X[K];
+#pragma unroll
+      for (int m1 = 0; m1 < K; ++m1) {
+        double t = 0.0;
+#pragma unroll
+        for (int ax = 0; ax < n1; ++ax) t = fma(c == 0 ? TB(K).BD[m1][ax] : TB(K).BI[m1][ax], v[ax], t);
+        X[m1] = t;
+      }
+      int i = 0;
+#pragma unroll
+      for (int m1 = 0; m1 < K; ++m1)
+#pragma unroll
+        for (int m2 = 0; m2 < K - m1; ++m2, ++i)
+          Y[i] = fma(c == 1 ? TB(K).BD[m2][ay] : TB(K).BI[m2][ay], X[m1], Y[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < NY; ++i) Ys[el][slab][i] = Y[i];
+  }
+  __syncthreads();
+  double dot = 0.0;
+  for (int item = threadIdx.x; item < EPB * NM; item += NT) {
+    const int el2 = item % EPB, m = item / EPB;
+    const int64_t e2 = (int64_t)blockIdx.x * EPB + el2;
+    if (e2 >= G.n_el) continue;
+    // mode m -> (m1, m2, m3) in k_B's enumeration (degree d, then m3, then m2)
+    int d = 0, rem = m;
+    while (rem >= (d + 1) * (d + 2) / 2) { rem -= (d + 1) * (d + 2) / 2; ++d; }
+    int m3 = 0;
+    while (rem >= d - m3 + 1) { rem -= d - m3 + 1; ++m3; }
+    const int m2 = rem, m1 = d - m2 - m3;
+    const int yi = m1 * K - m1 * (m1 - 1) / 2 + m2;  // index of Y[m1][m2] in the packed order
+    double Z = 0.0;
+    for (int cc = 0; cc < 3; ++cc)
+      for (int z = 0; z < n1; ++z)
+        Z = fma(cc == 2 ? TB(K).BD[m3][z] : TB(K).BI[m3][z], Ys[el2][cc * n1 + z][yi], Z);
+    const double o = sB * Z;
+    p[e2 * se + m * sm] = o;
+    if (dv) dot = fma(o, dv[e2 * se + m * sm], dot);
+  }
+  if (partial) store_partial<NT>(dot, partial);
+}
+
 // ------------------------------------------------------------------ row a7: B^T (element part)
 // E[c][a][e] = sB * sum_m prod_d M_cd[m_d][a_d] p_{e,m}
 template <int K>
@@ -384,6 +469,63 @@ __global__ void k_BT_elem(const double* __restrict__ p, double* __restrict__ E, 
           E[(int64_t)(c * NQ + a) * G.n_el + e] = sB * t;
         }
       }
+    }
+  }
+}
+
+// Same element part of B^T with one thread per (element, component c, z-node az),
+// element fastest: the body of k_BT_elem for one (c, az), so the outputs agree bit for
+// bit; 3(K+1) times its threads (k = 3, 4).
+template <int K>
+__global__ void __launch_bounds__(256) k_BT_split(const double* __restrict__ p, double* __restrict__ E, Geo G,
+                                                  double sB, const int* __restrict__ stop, int64_t se, int64_t sm) {
+  constexpr int n1 = K + 1, NQ = Ord<K>::NQ;
+  if (stop && *stop) return;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= G.n_el * 3 * n1) return;
+  const int64_t e = idx % G.n_el;
+  const int slab = (int)(idx / G.n_el), c = slab / n1, az = slab % n1;
+  double P[K][K][K];
+  {
+    int m = 0;
+#pragma unroll
+    for (int d = 0; d < K; ++d)
+#pragma unroll
+      for (int m3 = 0; m3 <= d; ++m3)
+#pragma unroll
+        for (int m2 = 0; m2 <= d - m3; ++m2) {
+          P[d - m2 - m3][m2][m3] = __ldg(p + e * se + m * sm);
+          ++m;
+        }
+  }
+  double Zt[K][K];
+#pragma unroll
+  for (int m1 = 0; m1 < K; ++m1)
+#pragma unroll
+    for (int m2 = 0; m2 < K - m1; ++m2) {
+      double t = 0.0;
+#pragma unroll
+      for (int m3 = 0; m3 < K - m1 - m2; ++m3)
+        t = fma(c == 2 ? TB(K).BD[m3][az] : TB(K).BI[m3][az], P[m1][m2][m3], t);
+      Zt[m1][m2] = t;
+    }
+#pragma unroll
+  for (int ay = 0; ay < n1; ++ay) {
+    double Yt[K];
+#pragma unroll
+    for (int m1 = 0; m1 < K; ++m1) {
+      double t = 0.0;
+#pragma unroll
+      for (int m2 = 0; m2 < K - m1; ++m2) t = fma(c == 1 ? TB(K).BD[m2][ay] : TB(K).BI[m2][ay], Zt[m1][m2], t);
+      Yt[m1] = t;
+    }
+#pragma unroll
+    for (int ax = 0; ax < n1; ++ax) {
+      double t = 0.0;
+#pragma unroll
+      for (int m1 = 0; m1 < K; ++m1) t = fma(c == 0 ? TB(K).BD[m1][ax] : TB(K).BI[m1][ax], Yt[m1], t);
+      const int a = ax + n1 * (ay + n1 * az);
+      E[(int64_t)(c * NQ + a) * G.n_el + e] = sB * t;
     }
   }
 }

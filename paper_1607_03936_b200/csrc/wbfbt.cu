@@ -184,9 +184,15 @@ wb_status launch_gather_t(wb_ctx* c, const double* s, double* y, int nomask) {
   return WB_OK;
 }
 
+#ifndef BSPLIT_EPB
+#define BSPLIT_EPB 16  // elements per block of the generic split B kernel (k = 3, 4; >= 8, see pqp)
+#endif
 template <int K>
 wb_status launch_BT_t(wb_ctx* c, const double* p, const int* stop, int64_t se, int64_t sm) {
-  k_BT_elem<K><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(p, c->E, c->G, c->sB, stop, se, sm);
+  if constexpr (K == 2)
+    k_BT_elem<K><<<nblk(c->n_el, 128), 128, 0, c->stream>>>(p, c->E, c->G, c->sB, stop, se, sm);
+  else
+    k_BT_split<K><<<nblk(c->n_el * 3 * (K + 1), 256), 256, 0, c->stream>>>(p, c->E, c->G, c->sB, stop, se, sm);
   LAUNCH_CHECK(c);
   return WB_OK;
 }
@@ -196,11 +202,19 @@ wb_status launch_B_t(wb_ctx* c, const double* u, const double* xs, double* p, in
                      const double* dv, double* total, int64_t se, int64_t sm) {
   constexpr int BS = 128;
   // dv: fused <p_out, dv> block partials into `total` (deferred reduction, PCG only)
-  k_B<K, BS><<<nblk(c->n_el, BS), BS, 0, c->stream>>>(u, xs, p, c->G, c->sB, nomask, stop, dv,
-                                                       dv ? total : nullptr, c->counter, nullptr, se, sm);
+  if constexpr (K == 2) {
+    k_B<K, BS><<<nblk(c->n_el, BS), BS, 0, c->stream>>>(u, xs, p, c->G, c->sB, nomask, stop, dv,
+                                                         dv ? total : nullptr, c->counter, nullptr, se, sm);
+  } else {
+    constexpr int EPB = BSPLIT_EPB;
+    k_B_split<K, EPB><<<nblk(c->n_el, EPB), BSplit<K, EPB>::NT, 0, c->stream>>>(u, xs, p, c->G, c->sB, nomask, stop,
+                                                                                dv, dv ? total : nullptr, se, sm);
+  }
   LAUNCH_CHECK(c);
   return WB_OK;
 }
+// number of dot partials launch_B_t leaves (one per block)
+inline int b_blocks(const wb_ctx* c) { return (int)nblk(c->n_el, c->k == 2 ? 128 : BSPLIT_EPB); }
 
 // fused k = 2 Poisson operator (+ PCG direction update), see k2_fused.cuh
 struct PcgArgs {  // PCG iteration context for the first kernel of an iteration
@@ -437,7 +451,7 @@ wb_status run_K_pcg(wb_ctx* c, int side, int mode, const double* pold, double* p
   *pcur = p;
   wb_status s = run_BT(c, p, nullptr, c->tv, 0, stop, 1, c->n_el);
   if (s) return s;
-  *npq = (int)nblk(c->n_el, 128);
+  *npq = b_blocks(c);
   return run_B(c, c->tv, X, q, 0, stop, p, c->pqp, 1, c->n_el);
 }
 
@@ -802,7 +816,7 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
   }
   alloc(&c->s0, c->n_p); alloc(&c->s1, c->n_p); alloc(&c->s2, c->n_p);
   alloc(&c->partial, c->max_partials);
-  alloc(&c->pqp, c->n_el / 32 + 1024);  // >= blocks of any K-apply grid (tiles >= 64 elements, k_B 128)
+  alloc(&c->pqp, c->n_el / 8 + 1024);  // >= blocks of any K-apply grid (tiles >= 64 elements, k_B_split >= 8)
   alloc(&c->rzp, c->red_blocks);
   if (k == 2) {
     // A tiles of A_TX x A_TY x A_TZ elements; mut tile-blocked and zero for elements
