@@ -199,14 +199,27 @@ __global__ void k_bmask(uint8_t* mask, Geo G) {
   mask[2 * G.n_nodes + g] = b;
 }
 
+// Element-local velocity buffer E of the generic path (k = 3, 4: A, B^T element parts ->
+// k_gather).  Layout [c][a][e] (element fastest): the producers' element-consecutive
+// threads store contiguous words.  (Measured at C4: the [c][e][a] layout, WB_E_AFAST 1,
+// speeds the gather up 33.7 -> 27.6 us but slows the B^T element part 11.7 -> 34.4 us.)
+#ifndef WB_E_AFAST
+#define WB_E_AFAST 0
+#endif
+template <int K>
+__device__ __forceinline__ int64_t eix(int c, int a, int64_t e, int64_t n_el) {
+  constexpr int NQ = (K + 1) * (K + 1) * (K + 1);
+  return WB_E_AFAST ? ((int64_t)c * n_el + e) * NQ + a : (int64_t)(c * NQ + a) * n_el + e;
+}
+
 // ------------------------------------------------------------------ node gather
 // y[c][g] = s[g] * sum_{e ni g} E[c][a(e,g)][e], elements in ascending index
 // (the order of the oracle's element-ordered scatter).  Boundary nodes -> 0
-// unless nomask.  E layout: E[(c*NQ + a)*n_el + e].
+// unless nomask.  E layout: eix<K> (above).
 template <int K>
 __global__ void k_gather(const double* __restrict__ E, const double* __restrict__ s,
                          double* __restrict__ y, Geo G, int nomask) {
-  constexpr int n1 = K + 1, NQ = Ord<K>::NQ;
+  constexpr int n1 = K + 1;
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= G.n_nodes) return;
   const int nn1 = G.nn1;
@@ -227,16 +240,36 @@ __global__ void k_gather(const double* __restrict__ E, const double* __restrict_
       if (q < G.N) { pe[d][pc[d]] = q; pa[d][pc[d]] = 0; pc[d]++; }
     }
   }
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-  for (int iz = 0; iz < pc[2]; ++iz)
-    for (int iy = 0; iy < pc[1]; ++iy)
-      for (int ix = 0; ix < pc[0]; ++ix) {
-        int64_t e = pe[0][ix] + (int64_t)G.N * (pe[1][iy] + (int64_t)G.N * pe[2][iz]);
-        int a = pa[0][ix] + n1 * (pa[1][iy] + n1 * pa[2][iz]);
-        acc0 += E[(int64_t)(0 * NQ + a) * G.n_el + e];
-        acc1 += E[(int64_t)(1 * NQ + a) * G.n_el + e];
-        acc2 += E[(int64_t)(2 * NQ + a) * G.n_el + e];
+  // all (up to 8 x 3) loads issued before the sums: fixed 2 x 2 x 2 trip counts, the
+  // absent terms predicated off; summed in ascending element order as before
+  double t0[8], t1[8], t2[8];
+#pragma unroll
+  for (int iz = 0; iz < 2; ++iz)
+#pragma unroll
+    for (int iy = 0; iy < 2; ++iy)
+#pragma unroll
+      for (int ix = 0; ix < 2; ++ix) {
+        const int k = (iz * 2 + iy) * 2 + ix;
+        t0[k] = t1[k] = t2[k] = 0.0;
+        if (iz < pc[2] && iy < pc[1] && ix < pc[0]) {
+          const int64_t e = pe[0][ix] + (int64_t)G.N * (pe[1][iy] + (int64_t)G.N * pe[2][iz]);
+          const int a = pa[0][ix] + n1 * (pa[1][iy] + n1 * pa[2][iz]);
+          t0[k] = __ldg(E + eix<K>(0, a, e, G.n_el));
+          t1[k] = __ldg(E + eix<K>(1, a, e, G.n_el));
+          t2[k] = __ldg(E + eix<K>(2, a, e, G.n_el));
+        }
       }
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+#pragma unroll
+  for (int iz = 0; iz < 2; ++iz)
+#pragma unroll
+    for (int iy = 0; iy < 2; ++iy)
+#pragma unroll
+      for (int ix = 0; ix < 2; ++ix)
+        if (iz < pc[2] && iy < pc[1] && ix < pc[0]) {
+          const int k = (iz * 2 + iy) * 2 + ix;
+          acc0 += t0[k]; acc1 += t1[k]; acc2 += t2[k];
+        }
   double sc = s ? s[g] : 1.0;
   if (s) { acc0 *= sc; acc1 *= sc; acc2 *= sc; }
   y[g] = acc0; y[G.n_nodes + g] = acc1; y[2 * G.n_nodes + g] = acc2;
@@ -417,7 +450,7 @@ __global__ void __launch_bounds__(BSplit<K, EPB>::NT) k_B_split(const double* __
 template <int K>
 __global__ void k_BT_elem(const double* __restrict__ p, double* __restrict__ E, Geo G, double sB,
                           const int* __restrict__ stop, int64_t se, int64_t sm) {
-  constexpr int n1 = K + 1, NQ = Ord<K>::NQ;
+  constexpr int n1 = K + 1;
   if (stop && *stop) return;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= G.n_el) return;
@@ -466,7 +499,7 @@ __global__ void k_BT_elem(const double* __restrict__ p, double* __restrict__ E, 
 #pragma unroll
           for (int m1 = 0; m1 < K; ++m1) t = fma(c == 0 ? TB(K).BD[m1][ax] : TB(K).BI[m1][ax], Yt[m1], t);
           const int a = ax + n1 * (ay + n1 * az);
-          E[(int64_t)(c * NQ + a) * G.n_el + e] = sB * t;
+          E[eix<K>(c, a, e, G.n_el)] = sB * t;
         }
       }
     }
@@ -479,7 +512,7 @@ __global__ void k_BT_elem(const double* __restrict__ p, double* __restrict__ E, 
 template <int K>
 __global__ void __launch_bounds__(256) k_BT_split(const double* __restrict__ p, double* __restrict__ E, Geo G,
                                                   double sB, const int* __restrict__ stop, int64_t se, int64_t sm) {
-  constexpr int n1 = K + 1, NQ = Ord<K>::NQ;
+  constexpr int n1 = K + 1;
   if (stop && *stop) return;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= G.n_el * 3 * n1) return;
@@ -525,7 +558,7 @@ __global__ void __launch_bounds__(256) k_BT_split(const double* __restrict__ p, 
 #pragma unroll
       for (int m1 = 0; m1 < K; ++m1) t = fma(c == 0 ? TB(K).BD[m1][ax] : TB(K).BI[m1][ax], Yt[m1], t);
       const int a = ax + n1 * (ay + n1 * az);
-      E[(int64_t)(c * NQ + a) * G.n_el + e] = sB * t;
+      E[eix<K>(c, a, e, G.n_el)] = sB * t;
     }
   }
 }
@@ -729,7 +762,7 @@ __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* 
       double s = 0.0;
 #pragma unroll
       for (int j = 0; j < n1; ++j) s = fma(TB(K).I[j][a], v[j], s);
-      if (valid) E[(int64_t)(c * NQ + (tb * n1 + ta) * n1 + a) * G.n_el + e] = s;
+      if (valid) E[eix<K>(c, (tb * n1 + ta) * n1 + a, e, G.n_el)] = s;
     }
   }
 #undef IX
