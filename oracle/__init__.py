@@ -70,6 +70,10 @@ def lib():
             L.or_poisson_relres.restype = C.c_double
             L.or_poisson_relres.argtypes = [C.c_void_p, _D, _D, _D]
             L.or_grad_weights.argtypes = [C.c_void_p, _D, _D]
+            L.or_diag_A.argtypes = [C.c_void_p, _D, _D]
+            L.or_velocity_cheb.argtypes = [C.c_void_p, _D, _D, _D, C.c_int, C.c_double, C.c_double]
+            L.or_velocity_eigmax.argtypes = [C.c_void_p, _D, _D, C.c_int]
+            L.or_velocity_eigmax.restype = C.c_double
             L.or_cheb_dense.argtypes = [C.c_int64, _D, _D, _D, _D, C.c_int, C.c_double, C.c_double]
             L.or_poisson_cheb.argtypes = [C.c_void_p, _D, _D, _D, _D, C.c_int, C.c_double, C.c_double]
             L.or_eigmax_dense.argtypes = [C.c_int64, _D, _D, _D, C.c_int]
@@ -260,6 +264,24 @@ class Oracle:
         """Power-iteration estimate of the largest |eigenvalue| of Minv K from start vector v0."""
         Xinv, diagK, v0 = _f64(Xinv), _f64(diagK), _f64(v0)
         return float(self.L.or_poisson_eigmax(self.h, _p(Xinv), _p(diagK), _p(v0), int(iters)))
+
+    def diag_A(self, mu_q) -> np.ndarray:
+        """diag(M A M), n_v, Dirichlet dofs 0 (R18)."""
+        mu_q = _f64(mu_q)
+        d = np.zeros(self.n_v)
+        self.L.or_diag_A(self.h, _p(mu_q), _p(d))
+        return d
+
+    def velocity_cheb(self, mu_q, b, iters, lmin, lmax) -> np.ndarray:
+        """x = Cheb(M A M, M b) with the Jacobi inverse mask/diag(A), x0 = 0 (R16, R18)."""
+        mu_q, b = _f64(mu_q), _f64(b)
+        x = np.zeros(self.n_v)
+        self.L.or_velocity_cheb(self.h, _p(mu_q), _p(b), _p(x), int(iters), float(lmin), float(lmax))
+        return x
+
+    def velocity_eigmax(self, mu_q, v0, iters) -> float:
+        mu_q, v0 = _f64(mu_q), _f64(v0)
+        return float(self.L.or_velocity_eigmax(self.h, _p(mu_q), _p(v0), int(iters)))
 
     def poisson_relres(self, Xinv, b, x) -> float:
         Xinv, b, x = _f64(Xinv), _f64(b), _f64(x)

@@ -711,6 +711,65 @@ double or_poisson_eigmax(or_ctx* c, const double* Xinv, const double* diagK, con
   return lam;
 }
 
+/* ---------------------------------------------------------------- diag(A), Chebyshev on A
+ * diag(M A M)_{(c,g)} = sum_{e ni g} A_e[(c,a),(c,a)] (elements ascending), with
+ *   A_e[(c,a),(c,a)] = sum_q mu_q w_q detJ s^2 [ sum_j gphi(a,q,j)^2 + gphi(a,q,c)^2 ],
+ * the cc == d, b == a entries of or_element_A_matrix (s = 2/h); Dirichlet dofs 0 (the
+ * masked operator's diagonal).  Building block of the Jacobi/Chebyshev smoother on A
+ * that the paper's HMG uses for the viscous block (SURVEY 8(f) #1's
+ * approximate A^-1; reading R18).                                                     */
+void or_diag_A(or_ctx* c, const double* mu_q, double* diag) {
+  const int nq = c->nq; const double s = 2.0 / c->h;
+  memset(diag, 0, sizeof(double) * c->n_v);
+  for (int64_t e = 0; e < c->n_el; ++e)
+    for (int cc = 0; cc < 3; ++cc)
+      for (int a = 0; a < nq; ++a) {
+        double t = 0.0;
+        for (int q = 0; q < nq; ++q) {
+          double g2 = 0.0;
+          for (int j = 0; j < 3; ++j) { const double g = s * c->gphi[(a * nq + q) * 3 + j]; g2 += g * g; }
+          const double gc = s * c->gphi[(a * nq + q) * 3 + cc];
+          t += mu_q[e * nq + q] * c->wq[q] * c->detJ * (g2 + gc * gc);
+        }
+        diag[cc * c->n_nodes + or_node(c, e, a)] += t;
+      }
+  mask_velocity(c, diag);
+}
+
+typedef struct { or_ctx* c; const double* mu_q; } or_aop;
+static void a_op(void* ctx, const double* in, double* out) {
+  or_aop* a = (or_aop*)ctx;
+  or_apply_A(a->c, a->mu_q, in, out, 0);
+}
+static void masked_jacobi(const or_ctx* c, const double* diag, double* Minv) {
+  for (int64_t i = 0; i < c->n_v; ++i) Minv[i] = diag[i] > 0.0 ? 1.0 / diag[i] : 0.0;
+}
+/* x = Cheb(M A M, M b) (Saad Alg. 12.1 as or_poisson_cheb, R16) with the Jacobi inverse
+ * mask / diag(A) (R18): the Chebyshev-accelerated point-Jacobi smoother on A, x0 = 0. */
+void or_velocity_cheb(or_ctx* c, const double* mu_q, const double* b, double* x, int iters, double lmin,
+                      double lmax) {
+  const int64_t n = c->n_v;
+  double* bb = (double*)malloc(sizeof(double) * n);
+  double* d = (double*)malloc(sizeof(double) * n);
+  memcpy(bb, b, sizeof(double) * n);
+  mask_velocity(c, bb);
+  or_diag_A(c, mu_q, d);
+  masked_jacobi(c, d, d);
+  or_aop a = {c, mu_q};
+  cheb_run(a_op, &a, n, d, bb, x, iters, lmin, lmax);
+  free(bb); free(d);
+}
+/* power-iteration estimate of the largest |eigenvalue| of (mask/diag A) M A M (R18) */
+double or_velocity_eigmax(or_ctx* c, const double* mu_q, const double* v0, int iters) {
+  double* d = (double*)malloc(sizeof(double) * c->n_v);
+  or_diag_A(c, mu_q, d);
+  masked_jacobi(c, d, d);
+  or_aop a = {c, mu_q};
+  const double lam = power_run(a_op, &a, c->n_v, d, v0, iters);
+  free(d);
+  return lam;
+}
+
 /* ---------------------------------------------------------------- wBFBT
  * z = S~^{-1}_wBFBT r  (eq:wbfbt), applied right to left:
  *   y = P PCG(K_r, P r); v = Dinv o (B^T y); v = A v; v = Cinv o v; s = P(B v);
