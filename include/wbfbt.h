@@ -133,6 +133,21 @@ wb_status wb_poisson_cheb(wb_ctx* ctx, int side, const double* b, double* x, int
  * reproducible).  lmax: host.  Synchronises the context stream.  WB_EINVAL for
  * side not 0/1, iters < 0 or null pointers; WB_ESTATE before wb_set_viscosity. */
 wb_status wb_poisson_eigmax(wb_ctx* ctx, int side, const double* v0, int iters, double* lmax);
+/* diag(M A M) (reading R18): dA[c * n_nodes + g] = sum over the elements holding node g of
+ * the element matrix diagonal, sum_q mu w_q detJ (2/h)^2 (|grad_xi phi_a|^2 + (d_xi_c phi_a)^2);
+ * Dirichlet dofs 0.  dA: device, n_v (SoA).  WB_EINVAL for a null pointer; WB_ESTATE
+ * before wb_set_viscosity; WB_ENOMEM if the k = 2 element buffer cannot be allocated.
+ * Asynchronous on the context stream. */
+wb_status wb_get_diagA(wb_ctx* ctx, double* dA);
+/* x = Cheb(M A M, M b): the Chebyshev-accelerated point-Jacobi smoother on the viscous
+ * block (the paper's smoother; an approximate A^-1 for SURVEY 8(f) #1),
+ * Saad Alg. 12.1 as wb_poisson_cheb with the Jacobi inverse mask / diag(A), x0 = 0,
+ * exactly `iters` steps on [lmin, lmax] (R16, R18).  b, x: device, n_v; b is not modified.
+ * Errors as wb_poisson_cheb.  Asynchronous on the context stream. */
+wb_status wb_velocity_cheb(wb_ctx* ctx, const double* b, double* x, int iters, double lmin, double lmax);
+/* *lmax = power-iteration estimate of the largest |eigenvalue| of (mask / diag A) M A M from
+ * the device start vector v0 (n_v, not modified), as wb_poisson_eigmax.  Synchronises. */
+wb_status wb_velocity_eigmax(wb_ctx* ctx, const double* v0, int iters, double* lmax);
 /* Row a10 -- z = S~^-1_wBFBT r (eq:wbfbt PAPER.md:436-454), applied right to
  * left:  y = P PCG(K_r, P r); v = D_w^-1 B^T y; v = A v; v = C_w^-1 v;
  * s = P B v; z = P PCG(K_l, s).  r, z: n_p. */

@@ -43,6 +43,9 @@ SYMBOLS = [
     ("wb_poisson_pcg", _i, [_vp, _i, _vp, _vp, _i]),
     ("wb_poisson_cheb", _i, [_vp, _i, _vp, _vp, _i, _d, _d]),
     ("wb_poisson_eigmax", _i, [_vp, _i, _vp, _i, C.POINTER(_d)]),
+    ("wb_get_diagA", _i, [_vp, _vp]),
+    ("wb_velocity_cheb", _i, [_vp, _vp, _vp, _i, _d, _d]),
+    ("wb_velocity_eigmax", _i, [_vp, _vp, _i, C.POINTER(_d)]),
     ("wb_apply_wbfbt", _i, [_vp, _vp, _vp, _i]),
     ("wb_hotpath", _i, [_vp, _vp, _d, _d, _vp, _vp, _i, _vp, _vp, _vp, _vp]),
     ("wb_hotpath_host", _i, [_vp, _vp, _d, _d, _vp, _vp, _i, _vp, _vp, _vp, _vp]),
@@ -224,6 +227,20 @@ class Context:
     def poisson_eigmax(self, side: int, v0, iters: int) -> float:
         lam = C.c_double(0.0)
         self._check(self._L.wb_poisson_eigmax(self._h, int(side), _ptr(v0, self.n_p), int(iters), C.byref(lam)))
+        return lam.value
+
+    def get_diagA(self, dA):
+        self._check(self._L.wb_get_diagA(self._h, _ptr(dA, self.n_v)))
+        return dA
+
+    def velocity_cheb(self, b, x, iters: int, lmin: float, lmax: float):
+        self._check(self._L.wb_velocity_cheb(self._h, _ptr(b, self.n_v), _ptr(x, self.n_v), int(iters), float(lmin),
+                                             float(lmax)))
+        return x
+
+    def velocity_eigmax(self, v0, iters: int) -> float:
+        lam = C.c_double(0.0)
+        self._check(self._L.wb_velocity_eigmax(self._h, _ptr(v0, self.n_v), int(iters), C.byref(lam)))
         return lam.value
 
     def apply_wbfbt(self, r, z, iters: int):

@@ -1137,6 +1137,91 @@ __global__ void k_pcg_out(const double* __restrict__ x, const double* __restrict
 
 // layout conversion element-major <-> mode-major (debug one-step entry)
 // element-major [e*nm + m] <-> PCG storage (PLay); to_soa: element-major -> PCG
+// ---------------------------------------------------------------- diag(A) (R18)
+// Element part of diag(M A M): E[c][a][e] = sum_q mut_q (sum_j g_j^2 + g_c^2), g_j the
+// reference derivative d/dxi_j phi_a at Gauss point q (mut = mu w_q h/2 carries the
+// detJ (2/h)^2 factor, as in A).  g = prod_d (d == j ? D1 : I)[q_d][a_d] with I the
+// GLL -> Gauss interpolation table and D1 = Dg I its derivative (exact: the Gauss
+// interpolant of a degree-k polynomial is the polynomial).  mut layout: tile-blocked
+// mutT[tile][q][le] when TX > 0 (k = 2, A's tiles), else mut[e][q].  One thread per element.
+template <int K, int TX, int TY, int TZ>
+__global__ void __launch_bounds__(128) k_diagA_elem(const double* __restrict__ mut, double* __restrict__ E, Geo G) {
+  constexpr int n1 = K + 1, NQ = Ord<K>::NQ;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= G.n_el) return;
+  int ex, ey, ez;
+  elem_xyz(e, G.N, ex, ey, ez);
+  int64_t mbase, mstride;
+  if constexpr (TX > 0) {
+    const int NTX = (G.N + TX - 1) / TX, NTY = (G.N + TY - 1) / TY;
+    const int tile = ex / TX + NTX * (ey / TY + NTY * (ez / TZ));
+    const int le = ex % TX + TX * (ey % TY + TY * (ez % TZ));
+    constexpr int NE = TX > 0 ? TX * TY * TZ : 1;
+    mbase = (int64_t)tile * NQ * NE + le; mstride = NE;
+  } else {
+    mbase = e * NQ; mstride = 1;
+  }
+  double D1[n1][n1];  // D1[i][a] = sum_k Dg[i][k] I[k][a]
+#pragma unroll
+  for (int i = 0; i < n1; ++i)
+#pragma unroll
+    for (int a = 0; a < n1; ++a) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < n1; ++k) t = fma(TB(K).Dg[i][k], TB(K).I[k][a], t);
+      D1[i][a] = t;
+    }
+#pragma unroll 1
+  for (int a = 0; a < NQ; ++a) {
+    const int ax = a % n1, ay = (a / n1) % n1, az = a / (n1 * n1);
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < NQ; ++q) {
+      const int qx = q % n1, qy = (q / n1) % n1, qz = q / (n1 * n1);
+      const double Ix = TB(K).I[qx][ax], Iy = TB(K).I[qy][ay], Iz = TB(K).I[qz][az];
+      const double gx = D1[qx][ax] * Iy * Iz, gy = Ix * D1[qy][ay] * Iz, gz = Ix * Iy * D1[qz][az];
+      const double g2 = gx * gx + gy * gy + gz * gz;
+      const double m = __ldg(mut + mbase + (int64_t)q * mstride);
+      t0 = fma(m, g2 + gx * gx, t0);
+      t1 = fma(m, g2 + gy * gy, t1);
+      t2 = fma(m, g2 + gz * gz, t2);
+    }
+    E[eix<K>(0, a, e, G.n_el)] = t0;
+    E[eix<K>(1, a, e, G.n_el)] = t1;
+    E[eix<K>(2, a, e, G.n_el)] = t2;
+  }
+}
+// Dinv = 1 / d where d > 0, else 0 (Dirichlet dofs, whose masked diagonal is 0)
+__global__ void k_inv_pos(const double* __restrict__ d, double* __restrict__ dinv, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dinv[i] = d[i] > 0.0 ? 1.0 / d[i] : 0.0;
+}
+// out = M in (velocity SoA, Dirichlet dofs 0)
+__global__ void k_mask_v(const double* __restrict__ in, double* __restrict__ out, Geo G) {
+  const int64_t n = 3 * G.n_nodes;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = i % G.n_nodes;
+    const int gx = (int)(g % G.nn1), gy = (int)((g / G.nn1) % G.nn1), gz = (int)(g / ((int64_t)G.nn1 * G.nn1));
+    out[i] = node_bnd(gx, gy, gz, G.nn1) ? 0.0 : in[i];
+  }
+}
+// Chebyshev step (as k_cheb) for any length, scalar: x += d; r -= q; d = c1 d + c2 (Minv r);
+// first: d = c2 (Minv r) only
+__global__ void __launch_bounds__(VBS) k_cheb_s(double* __restrict__ x, double* __restrict__ r, double* __restrict__ d,
+                                                const double* __restrict__ q, const double* __restrict__ Minv,
+                                                int64_t n, double c1, double c2, int first) {
+  for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS) {
+    const double m = Minv[i];
+    double rv = r[i];
+    if (first) { d[i] = c2 * (m * rv); continue; }
+    const double dv = d[i];
+    x[i] += dv;
+    rv -= q[i];
+    r[i] = rv;
+    d[i] = c1 * dv + c2 * (m * rv);
+  }
+}
+
 // ---------------------------------------------------------------- Chebyshev-Jacobi
 // One step of Saad's Alg. 12.1 after q = K d:  x += d; r -= q; d = c1 d + c2 (Minv r)
 // with the host-computed scalars c1 = rho' rho, c2 = 2 rho' / delta.  first: the start

@@ -72,6 +72,10 @@ struct wb_ctx {
   // (L2-resident), summed by the skeleton kernel; mut is tile-blocked for k = 2
   double* Fu = nullptr;
   double* mueff = nullptr;  // n_el * n_q: the viscosity-gradient weights' mu_eff (option "weights" 1, R17)
+  // diag(A) and the velocity smoother (R18), allocated on first use: k = 2 element buffer
+  // (3 components), mask / diag(A), a third n_v scratch vector
+  double *E3 = nullptr, *dAinv = nullptr, *tq = nullptr;
+  bool dA_valid = false;
   int weights = 0;
   int n_tiles = 0;
   int use_graph = 1;
@@ -632,6 +636,91 @@ wb_status run_eigmax(wb_ctx* c, int side, const double* v0, int iters, double* l
   return WB_OK;
 }
 
+// ---- diag(A) and the Chebyshev-Jacobi smoother on A (R18)
+bool lazy_alloc(double** p, int64_t n) {
+  if (*p) return true;
+  if (cudaMalloc(p, sizeof(double) * (size_t)n) != cudaSuccess) { cudaGetLastError(); *p = nullptr; return false; }
+  return true;
+}
+// out (n_v) = diag(M A M): element diagonals, then the fixed-order node gather (masked)
+wb_status run_diagA(wb_ctx* c, double* out) {
+  double* E = c->E;
+  if (c->k == 2) {
+    if (!lazy_alloc(&c->E3, 3 * c->nq * c->n_el)) return set_err(c, WB_ENOMEM, "diag(A) buffer allocation failed");
+    E = c->E3;
+  }
+  const unsigned nb = (unsigned)nblk(c->n_el, 128);
+  switch (c->k) {
+    case 2: k_diagA_elem<2, A_TX, A_TY, A_TZ><<<nb, 128, 0, c->stream>>>(c->mut, E, c->G); break;
+    case 3: k_diagA_elem<3, 0, 0, 0><<<nb, 128, 0, c->stream>>>(c->mut, E, c->G); break;
+    default: k_diagA_elem<4, 0, 0, 0><<<nb, 128, 0, c->stream>>>(c->mut, E, c->G); break;
+  }
+  LAUNCH_CHECK(c);
+  switch (c->k) {
+    case 2: k_gather<2><<<nblk(c->n_nodes, 256), 256, 0, c->stream>>>(E, nullptr, out, c->G, 0); break;
+    case 3: k_gather<3><<<nblk(c->n_nodes, 256), 256, 0, c->stream>>>(E, nullptr, out, c->G, 0); break;
+    default: k_gather<4><<<nblk(c->n_nodes, 256), 256, 0, c->stream>>>(E, nullptr, out, c->G, 0); break;
+  }
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+wb_status ensure_dAinv(wb_ctx* c) {
+  if (c->dA_valid) return WB_OK;
+  if (!lazy_alloc(&c->dAinv, c->n_v) || !lazy_alloc(&c->tq, c->n_v))
+    return set_err(c, WB_ENOMEM, "smoother buffer allocation failed");
+  wb_status s = run_diagA(c, c->dAinv);
+  if (s) return s;
+  k_inv_pos<<<c->red_blocks, VBS, 0, c->stream>>>(c->dAinv, c->dAinv, c->n_v);
+  LAUNCH_CHECK(c);
+  c->dA_valid = true;
+  return WB_OK;
+}
+// x = Cheb(M A M, M b) with the Jacobi inverse mask / diag(A), as or_velocity_cheb
+wb_status run_vcheb(wb_ctx* c, const double* b, double* x, int iters, double lmin, double lmax) {
+  wb_status s = ensure_dAinv(c);
+  if (s) return s;
+  const int64_t n = c->n_v;
+  double *r = c->tv, *d = c->tw, *q = c->tq;
+  CUDA_TRY(c, cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream));
+  k_mask_v<<<c->red_blocks, VBS, 0, c->stream>>>(b, r, c->G);
+  LAUNCH_CHECK(c);
+  const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin), sigma1 = theta / delta;
+  double rho = 1.0 / sigma1;
+  k_cheb_s<<<c->red_blocks, VBS, 0, c->stream>>>(x, r, d, nullptr, c->dAinv, n, 0.0, 1.0 / theta, 1);
+  LAUNCH_CHECK(c);
+  for (int it = 0; it < iters; ++it) {
+    if ((s = run_A(c, d, q, 0))) return s;
+    const double rho1 = 1.0 / (2.0 * sigma1 - rho);
+    k_cheb_s<<<c->red_blocks, VBS, 0, c->stream>>>(x, r, d, q, c->dAinv, n, rho1 * rho, 2.0 * rho1 / delta, 0);
+    LAUNCH_CHECK(c);
+    rho = rho1;
+  }
+  return WB_OK;
+}
+// power-iteration estimate of the largest |eigenvalue| of (mask / diag A) M A M
+wb_status run_veigmax(wb_ctx* c, const double* v0, int iters, double* lam) {
+  wb_status s = ensure_dAinv(c);
+  if (s) return s;
+  const int64_t n = c->n_v;
+  const int nb = c->red_blocks;
+  double *v = c->tw, *q = c->tq, *dlam = c->scal + S_SCR;
+  k_pow_sumsq<<<nb, VBS, 0, c->stream>>>(const_cast<double*>(v0), nullptr, n, c->rzp);  // (no write: Minv = NULL)
+  LAUNCH_CHECK(c);
+  k_pow_scale<<<nb, VBS, 0, c->stream>>>(v0, v, n, c->rzp, nb, dlam);
+  LAUNCH_CHECK(c);
+  CUDA_TRY(c, cudaMemsetAsync(dlam, 0, sizeof(double), c->stream));
+  for (int it = 0; it < iters; ++it) {
+    if ((s = run_A(c, v, q, 0))) return s;
+    k_pow_sumsq<<<nb, VBS, 0, c->stream>>>(q, c->dAinv, n, c->rzp);
+    LAUNCH_CHECK(c);
+    k_pow_scale<<<nb, VBS, 0, c->stream>>>(q, v, n, c->rzp, nb, dlam);
+    LAUNCH_CHECK(c);
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(lam, dlam, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return WB_OK;
+}
+
 // q = K_side p, element-major in and out (through the PCG kernels, mode "p as is")
 wb_status run_K(wb_ctx* c, int side, const double* p, double* q) {
   k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(p, c->pp, c->n_el, c->nm, 1, c->pl, c->N);
@@ -671,7 +760,8 @@ wb_status check_ctx(wb_ctx* c, bool need_visc) {
 void free_all(wb_ctx* c) {
   double** bufs[] = {&c->mut, &c->Cw, &c->Dw, &c->Cinv, &c->Dinv, &c->dKl, &c->dKr, &c->MinvL, &c->MinvR,
                      &c->E, &c->tv, &c->tw, &c->px, &c->pr, &c->pp, &c->pp1, &c->pq, &c->pz, &c->s0, &c->s1, &c->s2,
-                     &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->Fu, &c->mueff};
+                     &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->Fu, &c->mueff,
+                     &c->E3, &c->dAinv, &c->tq};
   clear_graphs(c);
   if (c->cap_stream) { cudaStreamDestroy(c->cap_stream); c->cap_stream = nullptr; }
   if (c->copy_stream) { cudaStreamDestroy(c->copy_stream); c->copy_stream = nullptr; }
@@ -918,6 +1008,7 @@ template <int K>
 static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
   const int64_t nmu = c->n_el * c->nq;
   CUDA_TRY(c, cudaMemsetAsync(c->icount, 0, sizeof(unsigned long long) * 4, c->stream));
+  c->dA_valid = false;
   const double* wsrc = nullptr;  // lumping weight source: mu (eq:wbfbt) or mu_eff (R17)
   if (c->weights == 1) {
     if (!c->mueff && cudaMalloc(&c->mueff, sizeof(double) * nmu) != cudaSuccess) {
@@ -1055,6 +1146,30 @@ wb_status wb_poisson_eigmax(wb_ctx* c, int side, const double* v0, int iters, do
   if (s) return s;
   if (!v0 || !lmax || (side != 0 && side != 1) || iters < 0) return set_err(c, WB_EINVAL, "bad argument");
   return run_eigmax(c, side, v0, iters, lmax);
+}
+
+wb_status wb_get_diagA(wb_ctx* c, double* dA) {
+  wb_status s = check_ctx(c, true);
+  if (s) return s;
+  if (!dA) return set_err(c, WB_EINVAL, "bad argument");
+  return run_diagA(c, dA);
+}
+
+wb_status wb_velocity_cheb(wb_ctx* c, const double* b, double* x, int iters, double lmin, double lmax) {
+  wb_status s = check_ctx(c, true);
+  if (s) return s;
+  if (!b || !x || iters < 0) return set_err(c, WB_EINVAL, "bad argument");
+  if (!(lmin > 0.0) || !(lmax > lmin) || !std::isfinite(lmax))
+    return set_err(c, WB_EINVAL, "the interval must satisfy 0 < lmin < lmax < inf");
+  if (overlaps(b, 8 * c->n_v, x, 8 * c->n_v)) return set_err(c, WB_EALIAS, "b and x overlap");
+  return run_vcheb(c, b, x, iters, lmin, lmax);
+}
+
+wb_status wb_velocity_eigmax(wb_ctx* c, const double* v0, int iters, double* lmax) {
+  wb_status s = check_ctx(c, true);
+  if (s) return s;
+  if (!v0 || !lmax || iters < 0) return set_err(c, WB_EINVAL, "bad argument");
+  return run_veigmax(c, v0, iters, lmax);
 }
 
 wb_status wb_apply_wbfbt(wb_ctx* c, const double* r, double* z, int iters) {
