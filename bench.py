@@ -287,6 +287,14 @@ def run_ours(args):
     t_cheb = {it: timed(lambda: ctx.poisson_cheb(1, p, qv, it, 0.1 * lam, 1.1 * lam), reps=5, cold=False)
               for it in (10, 50, iters)}
     cheb_iter_us = (t_cheb[50] - t_cheb[10]) / 40 * 1e3
+    # ---- R18: diag(A) and the Chebyshev-Jacobi smoother on A (SURVEY 8(f) #1's approximate A^-1)
+    yd = torch.empty(ctx.n_v, **f64)
+    t_diagA = timed(lambda: ctx.get_diagA(yd), reps=5)
+    vv0 = torch.as_tensor(np.random.default_rng(8).standard_normal(ctx.n_v), **f64)
+    lam_a = ctx.velocity_eigmax(vv0, 10)
+    t_vs = {it: timed(lambda: ctx.velocity_cheb(u, yd, it, 0.1 * lam_a, 1.1 * lam_a), reps=3, cold=False)
+            for it in (2, 6)}
+    vsmooth_iter_us = (t_vs[6] - t_vs[2]) / 4 * 1e3
     # ---- dominant kernel: the fused Poisson operator inside the PCG loops (2 x iters
     # launches per step).  Profiled pass: the same hot-path step with a CUDA-event
     # pair around every such launch (library option "profile": plain launches on
@@ -369,7 +377,9 @@ def run_ours(args):
                     "cheb": {"iter_us": cheb_iter_us, "solve_ms": t_cheb[iters], "iters": iters,
                              "interval": [0.1 * lam, 1.1 * lam], "eigmax_20_ms": t_eig,
                              "k_cheb_bytes_per_launch": 64 * n_p,
-                             "note": "SURVEY 8(f) #2 (not in the step): x = P Cheb(K_r, P b), R16"}},
+                             "note": "SURVEY 8(f) #2 (not in the step): x = P Cheb(K_r, P b), R16"},
+                    "velocity_smoother": {"diagA_ms": t_diagA, "iter_us": vsmooth_iter_us,
+                                          "note": "R18 (not in the step): x = Cheb(M A M, M b), Jacobi mask/diag(A)"}},
                 "roofline": roof,
                 "e2e": {"value": e2e, "unit": "hot-path steps/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h},
