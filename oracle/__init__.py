@@ -71,6 +71,11 @@ def lib():
             L.or_poisson_relres.argtypes = [C.c_void_p, _D, _D, _D]
             L.or_grad_weights.argtypes = [C.c_void_p, _D, _D]
             L.or_diag_A.argtypes = [C.c_void_p, _D, _D]
+            L.or_fgmres_dense.argtypes = [C.c_int64, _D, _D, _D, _D, C.c_int, C.c_int, C.c_double, _D]
+            L.or_fgmres_dense.restype = C.c_int
+            L.or_stokes_fgmres.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, _D, _D, _D, _D, C.c_int, C.c_int,
+                                           C.c_double, C.c_int, C.c_int, C.c_double, C.c_double, _D]
+            L.or_stokes_fgmres.restype = C.c_int
             L.or_velocity_cheb.argtypes = [C.c_void_p, _D, _D, _D, C.c_int, C.c_double, C.c_double]
             L.or_velocity_eigmax.argtypes = [C.c_void_p, _D, _D, C.c_int]
             L.or_velocity_eigmax.restype = C.c_double
@@ -106,6 +111,15 @@ def eigmax_dense(A, Minv, v0, iters) -> float:
     """The power iteration of or_poisson_eigmax on a dense matrix A (row-major)."""
     A, Minv, v0 = _f64(A), _f64(Minv), _f64(v0)
     return float(lib().or_eigmax_dense(len(v0), _p(A), _p(Minv), _p(v0), int(iters)))
+
+
+def fgmres_dense(A, P, b, restart, max_iters, rtol):
+    """(x, iterations, relres) of the oracle's FGMRES core on a dense system, right preconditioner P."""
+    A, P, b = _f64(A), _f64(P), _f64(b)
+    x, rr = np.zeros(len(b)), np.zeros(1)
+    it = lib().or_fgmres_dense(len(b), _p(A), _p(P), _p(b), _p(x), int(restart), int(max_iters), float(rtol),
+                               _p(rr))
+    return x, int(it), float(rr[0])
 
 
 def sizes_only(N: int, k: int) -> dict:
@@ -282,6 +296,16 @@ class Oracle:
     def velocity_eigmax(self, mu_q, v0, iters) -> float:
         mu_q, v0 = _f64(mu_q), _f64(v0)
         return float(self.L.or_velocity_eigmax(self.h, _p(mu_q), _p(v0), int(iters)))
+
+    def stokes_fgmres(self, f, g, restart, max_iters, rtol, pcg_iters, smooth_iters, lmin, lmax, state=None):
+        """(u, p, iterations, relres): FGMRES on [A B^T; B 0] with eq:precond-stokes (R19)."""
+        st = self.state if state is None else state
+        f, g = _f64(f), _f64(g)
+        u, p, rr = np.zeros(self.n_v), np.zeros(self.n_p), np.zeros(1)
+        it = self.L.or_stokes_fgmres(self.h, _p(self.mu_q), _p(st["Cinv"]), _p(st["Dinv"]), _p(st["diagKl"]),
+                                     _p(st["diagKr"]), _p(f), _p(g), _p(u), _p(p), int(restart), int(max_iters),
+                                     float(rtol), int(pcg_iters), int(smooth_iters), float(lmin), float(lmax), _p(rr))
+        return u, p, int(it), float(rr[0])
 
     def poisson_relres(self, Xinv, b, x) -> float:
         Xinv, b, x = _f64(Xinv), _f64(b), _f64(x)

@@ -799,6 +799,138 @@ void or_wbfbt(or_ctx* c, const double* mu_q, const double* Cinv, const double* D
   free(y); free(s); free(v); free(w);
 }
 
+/* ---------------------------------------------------------------- Stokes solve
+ * SURVEY 8(f) #1, reading R19.  [A B^T; B 0] [u; p] = [f; g] with A = M A M, B^T = M B^T
+ * and B acting on M u, right-preconditioned by eq:precond-stokes:
+ *   P = [At B^T; 0 St],  P^{-1} (a; b) = (At^{-1} (a - B^T y); y),  y = St^{-1} b,
+ * St^{-1} = -(wBFBT) (the paper's S := B A^{-1} B^T is positive, so St ~ -S and the
+ * exact choices converge in two iterations), At^{-1} = the Chebyshev-Jacobi smoother on
+ * A (R18).  Flexible GMRES (Saad 1993: restarted, modified Gram-Schmidt Arnoldi, Givens
+ * rotations, x = x0 + Z y) because the fixed-iteration PCG inside wBFBT is not a linear
+ * map; with a fixed linear preconditioner it is GMRES.  x0 = 0; stops when the Givens
+ * residual estimate is <= rtol ||b|| or after max_iters iterations; the final pressure
+ * is projected (R10).  The core runs over operator / preconditioner callbacks, and the
+ * dense form or_fgmres_dense is what tests/test_oracle_stokes.py pins.                */
+typedef void (*or_vop)(void* ctx, const double* in, double* out);
+static int fgmres_run(or_vop K, or_vop Pinv, void* ctx, int64_t n, const double* b, double* x, int m, int max_iters,
+                      double rtol, double* relres) {
+  double* V = (double*)malloc(sizeof(double) * n * (m + 1));
+  double* Z = (double*)malloc(sizeof(double) * n * m);
+  double* w = (double*)malloc(sizeof(double) * n);
+  double* H = (double*)calloc((size_t)(m + 1) * m, sizeof(double)); /* H[i*m + j] */
+  double* cs = (double*)malloc(sizeof(double) * m);
+  double* sn = (double*)malloc(sizeof(double) * m);
+  double* g = (double*)malloc(sizeof(double) * (m + 1));
+  double* y = (double*)malloc(sizeof(double) * m);
+  for (int64_t i = 0; i < n; ++i) { x[i] = 0.0; w[i] = b[i]; }
+  const double bnorm = sqrt(dot(b, b, n));
+  double beta = bnorm;
+  int total = 0;
+  while (beta > rtol * bnorm && total < max_iters) {
+    for (int64_t i = 0; i < n; ++i) V[i] = w[i] / beta;
+    for (int i = 0; i <= m; ++i) g[i] = 0.0;
+    g[0] = beta;
+    int jend = -1;
+    for (int j = 0; j < m && total < max_iters; ++j) {
+      Pinv(ctx, V + (int64_t)j * n, Z + (int64_t)j * n);
+      K(ctx, Z + (int64_t)j * n, w);
+      for (int i = 0; i <= j; ++i) {
+        const double hij = dot(w, V + (int64_t)i * n, n);
+        H[i * m + j] = hij;
+        for (int64_t t = 0; t < n; ++t) w[t] -= hij * V[(int64_t)i * n + t];
+      }
+      const double hn = sqrt(dot(w, w, n));
+      for (int i = 0; i < j; ++i) { /* previous rotations on column j */
+        const double a = H[i * m + j], bb = H[(i + 1) * m + j];
+        H[i * m + j] = cs[i] * a + sn[i] * bb;
+        H[(i + 1) * m + j] = -sn[i] * a + cs[i] * bb;
+      }
+      const double a = H[j * m + j], den = sqrt(a * a + hn * hn);
+      cs[j] = den > 0.0 ? a / den : 1.0;
+      sn[j] = den > 0.0 ? hn / den : 0.0;
+      H[j * m + j] = den;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      ++total;
+      jend = j;
+      if (hn > 0.0) for (int64_t t = 0; t < n; ++t) V[(int64_t)(j + 1) * n + t] = w[t] / hn;
+      if (fabs(g[j + 1]) <= rtol * bnorm || hn == 0.0) break;
+    }
+    for (int i = jend; i >= 0; --i) { /* back substitution */
+      double t = g[i];
+      for (int k = i + 1; k <= jend; ++k) t -= H[i * m + k] * y[k];
+      y[i] = t / H[i * m + i];
+    }
+    for (int i = 0; i <= jend; ++i)
+      for (int64_t t = 0; t < n; ++t) x[t] += y[i] * Z[(int64_t)i * n + t];
+    K(ctx, x, w); /* true residual for the restart / the stop test */
+    for (int64_t t = 0; t < n; ++t) w[t] = b[t] - w[t];
+    beta = sqrt(dot(w, w, n));
+    if (jend < 0) break;
+  }
+  if (relres) *relres = bnorm > 0.0 ? beta / bnorm : 0.0;
+  free(V); free(Z); free(w); free(H); free(cs); free(sn); free(g); free(y);
+  return total;
+}
+
+typedef struct { int64_t n; const double *A, *P; } or_dense2;
+static void dense2_K(void* c, const double* in, double* out) {
+  const or_dense2* D = (const or_dense2*)c;
+  for (int64_t i = 0; i < D->n; ++i) { double s = 0.0; for (int64_t j = 0; j < D->n; ++j) s += D->A[i * D->n + j] * in[j]; out[i] = s; }
+}
+static void dense2_P(void* c, const double* in, double* out) {
+  const or_dense2* D = (const or_dense2*)c;
+  for (int64_t i = 0; i < D->n; ++i) { double s = 0.0; for (int64_t j = 0; j < D->n; ++j) s += D->P[i * D->n + j] * in[j]; out[i] = s; }
+}
+/* the FGMRES core on a dense system A x = b with the dense right preconditioner P ~ A^-1 */
+int or_fgmres_dense(int64_t n, const double* A, const double* P, const double* b, double* x, int m, int max_iters,
+                    double rtol, double* relres) {
+  or_dense2 D = {n, A, P};
+  return fgmres_run(dense2_K, dense2_P, &D, n, b, x, m, max_iters, rtol, relres);
+}
+
+typedef struct {
+  or_ctx* c; const double *mu, *Cinv, *Dinv, *dKl, *dKr;
+  int pcg, sm; double lo, hi; double *tv, *tp;
+} or_stokes;
+static void stokes_K(void* ctx, const double* in, double* out) { /* [A B^T; B 0] (u; p) */
+  or_stokes* S = (or_stokes*)ctx;
+  or_ctx* c = S->c;
+  or_apply_A(c, S->mu, in, out, 0);
+  or_apply_BT(c, in + c->n_v, S->tv, 0);
+  for (int64_t i = 0; i < c->n_v; ++i) out[i] += S->tv[i];
+  or_apply_B(c, in, out + c->n_v, 0);
+}
+static void stokes_P(void* ctx, const double* in, double* out) { /* P^{-1} (a; b) */
+  or_stokes* S = (or_stokes*)ctx;
+  or_ctx* c = S->c;
+  double* y = out + c->n_v;
+  or_wbfbt(c, S->mu, S->Cinv, S->Dinv, S->dKl, S->dKr, in + c->n_v, y, S->pcg);
+  for (int64_t i = 0; i < c->n_p; ++i) y[i] = -y[i];
+  or_apply_BT(c, y, S->tv, 0);
+  for (int64_t i = 0; i < c->n_v; ++i) S->tv[i] = in[i] - S->tv[i];
+  or_velocity_cheb(c, S->mu, S->tv, out, S->sm, S->lo, S->hi);
+}
+int or_stokes_fgmres(or_ctx* c, const double* mu_q, const double* Cinv, const double* Dinv, const double* diagKl,
+                     const double* diagKr, const double* f, const double* g, double* u, double* p, int m,
+                     int max_iters, double rtol, int pcg_iters, int smooth_iters, double lmin, double lmax,
+                     double* relres) {
+  const int64_t n = c->n_v + c->n_p;
+  double* b = (double*)malloc(sizeof(double) * n);
+  double* x = (double*)malloc(sizeof(double) * n);
+  or_stokes S = {c, mu_q, Cinv, Dinv, diagKl, diagKr, pcg_iters, smooth_iters, lmin, lmax,
+                 (double*)malloc(sizeof(double) * c->n_v), NULL};
+  memcpy(b, f, sizeof(double) * c->n_v);
+  mask_velocity(c, b);
+  memcpy(b + c->n_v, g, sizeof(double) * c->n_p);
+  const int it = fgmres_run(stokes_K, stokes_P, &S, n, b, x, m, max_iters, rtol, relres);
+  memcpy(u, x, sizeof(double) * c->n_v);
+  memcpy(p, x + c->n_v, sizeof(double) * c->n_p);
+  or_project(c, p);
+  free(b); free(x); free(S.tv);
+  return it;
+}
+
 /* Relative residual ||b - K x|| / ||b|| of a Poisson solve (quality check). */
 double or_poisson_relres(or_ctx* c, const double* Xinv, const double* b, const double* x) {
   double* q = (double*)malloc(sizeof(double) * c->n_p);
