@@ -148,6 +148,20 @@ wb_status wb_velocity_cheb(wb_ctx* ctx, const double* b, double* x, int iters, d
 /* *lmax = power-iteration estimate of the largest |eigenvalue| of (mask / diag A) M A M from
  * the device start vector v0 (n_v, not modified), as wb_poisson_eigmax.  Synchronises. */
 wb_status wb_velocity_eigmax(wb_ctx* ctx, const double* v0, int iters, double* lmax);
+/* the Stokes solve [A B^T; B 0] (u; p) = (f; g) (eq:discrete-stokes,
+ * PAPER.md:187-204; A, B^T masked, B on masked u) by flexible GMRES with the right
+ * preconditioner of eq:precond-stokes: P^-1 (a; b) = (At^-1 (a - B^T y); y),
+ * y = -wBFBT(b) with `pcg_iters` PCG iterations per inner Poisson solve, At^-1 =
+ * wb_velocity_cheb with `smooth_iters` steps on [lmin, lmax] (reading R19).  Restarted every
+ * `restart` iterations, x0 = 0, stops when the residual estimate is <= rtol ||(M f; g)|| or
+ * after max_iters iterations; p is projected off the constants (R10).  f, u: device n_v;
+ * g, p: device n_p (element-major).  *iters (host, may be NULL): iterations run; *relres (host,
+ * may be NULL): ||b - K x|| / ||b|| of the returned solution.  Memory: (2 restart + 4)(n_v + n_p)
+ * doubles, kept for later calls.  WB_EINVAL for bad arguments or interval, WB_EALIAS for
+ * overlapping outputs, WB_ESTATE before wb_set_viscosity, WB_ENOMEM.  Synchronises. */
+wb_status wb_stokes_fgmres(wb_ctx* ctx, const double* f, const double* g, double* u, double* p, int restart,
+                           int max_iters, double rtol, int pcg_iters, int smooth_iters, double lmin, double lmax,
+                           int* iters, double* relres);
 /* Row a10 -- z = S~^-1_wBFBT r (eq:wbfbt PAPER.md:436-454), applied right to
  * left:  y = P PCG(K_r, P r); v = D_w^-1 B^T y; v = A v; v = C_w^-1 v;
  * s = P B v; z = P PCG(K_l, s).  r, z: n_p. */

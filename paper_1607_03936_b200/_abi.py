@@ -46,6 +46,7 @@ SYMBOLS = [
     ("wb_get_diagA", _i, [_vp, _vp]),
     ("wb_velocity_cheb", _i, [_vp, _vp, _vp, _i, _d, _d]),
     ("wb_velocity_eigmax", _i, [_vp, _vp, _i, C.POINTER(_d)]),
+    ("wb_stokes_fgmres", _i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _d, _i, _i, _d, _d, C.POINTER(_i), C.POINTER(_d)]),
     ("wb_apply_wbfbt", _i, [_vp, _vp, _vp, _i]),
     ("wb_hotpath", _i, [_vp, _vp, _d, _d, _vp, _vp, _i, _vp, _vp, _vp, _vp]),
     ("wb_hotpath_host", _i, [_vp, _vp, _d, _d, _vp, _vp, _i, _vp, _vp, _vp, _vp]),
@@ -242,6 +243,16 @@ class Context:
         lam = C.c_double(0.0)
         self._check(self._L.wb_velocity_eigmax(self._h, _ptr(v0, self.n_v), int(iters), C.byref(lam)))
         return lam.value
+
+    def stokes_fgmres(self, f, g, u, p, restart: int, max_iters: int, rtol: float, pcg_iters: int,
+                      smooth_iters: int, lmin: float, lmax: float):
+        """Returns (u, p, iterations, relres)."""
+        it, rr = C.c_int(0), C.c_double(0.0)
+        self._check(self._L.wb_stokes_fgmres(self._h, _ptr(f, self.n_v), _ptr(g, self.n_p), _ptr(u, self.n_v),
+                                             _ptr(p, self.n_p), int(restart), int(max_iters), float(rtol),
+                                             int(pcg_iters), int(smooth_iters), float(lmin), float(lmax),
+                                             C.byref(it), C.byref(rr)))
+        return u, p, it.value, rr.value
 
     def apply_wbfbt(self, r, z, iters: int):
         self._check(self._L.wb_apply_wbfbt(self._h, _ptr(r, self.n_p), _ptr(z, self.n_p), int(iters)))

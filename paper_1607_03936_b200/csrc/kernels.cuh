@@ -1137,6 +1137,38 @@ __global__ void k_pcg_out(const double* __restrict__ x, const double* __restrict
 
 // layout conversion element-major <-> mode-major (debug one-step entry)
 // element-major [e*nm + m] <-> PCG storage (PLay); to_soa: element-major -> PCG
+// ---------------------------------------------------------------- FGMRES helpers (R19)
+// *out = <a, b> (fixed-order grid reduction: block partials summed by the last block)
+__global__ void __launch_bounds__(VBS) k_dot_dev(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                                                 double* partial, unsigned* counter, double* out) {
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS)
+    s = fma(a[i], b[i], s);
+  grid_sum<VBS>(s, partial, counter, out);
+}
+// w -= (*h) v  (the scalar stays on the device: modified Gram-Schmidt without host round trips)
+__global__ void __launch_bounds__(VBS) k_axpy_dev(double* __restrict__ w, const double* __restrict__ v, int64_t n,
+                                                  const double* __restrict__ h) {
+  const double a = *h;
+  for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS) w[i] -= a * v[i];
+}
+// out = in / sqrt(*h2)
+__global__ void __launch_bounds__(VBS) k_unit_dev(double* __restrict__ out, const double* __restrict__ in, int64_t n,
+                                                  const double* __restrict__ h2) {
+  const double nrm = sqrt(*h2);
+  for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS) out[i] = in[i] / nrm;
+}
+// y += a x  (host scalar)
+__global__ void __launch_bounds__(VBS) k_axpy(double* __restrict__ y, const double* __restrict__ x, int64_t n, double a) {
+  for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS) y[i] += a * x[i];
+}
+// y = a x + b y
+__global__ void __launch_bounds__(VBS) k_axpby(double* __restrict__ y, const double* __restrict__ x, int64_t n, double a,
+                                               double b) {
+  for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS)
+    y[i] = a * x[i] + b * y[i];
+}
+
 // ---------------------------------------------------------------- diag(A) (R18)
 // Element part of diag(M A M): E[c][a][e] = sum_q mut_q (sum_j g_j^2 + g_c^2), g_j the
 // reference derivative d/dxi_j phi_a at Gauss point q (mut = mu w_q h/2 carries the

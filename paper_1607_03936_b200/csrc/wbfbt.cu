@@ -76,6 +76,11 @@ struct wb_ctx {
   // (3 components), mask / diag(A), a third n_v scratch vector
   double *E3 = nullptr, *dAinv = nullptr, *tq = nullptr;
   bool dA_valid = false;
+  // FGMRES Stokes solve (R19): Krylov bases V (m+1 vectors) and Z (m), work vectors, an
+  // n_v scratch, device scalars; sized for the largest restart length used so far
+  double *gV = nullptr, *gZ = nullptr, *gw = nullptr, *gb = nullptr, *gx = nullptr, *gsa = nullptr,
+         *gh = nullptr;
+  int g_m = 0;
   int weights = 0;
   int n_tiles = 0;
   int use_graph = 1;
@@ -751,6 +756,136 @@ wb_status run_wbfbt(wb_ctx* c, const double* r, double* z, int iters) {
   return run_poisson(c, 0, c->s2, z, iters);
 }
 
+// ---- Stokes solve (R19): flexible GMRES on [A B^T; B 0] with P^-1 (a; b) =
+// (At^-1 (a - B^T y); y), y = -wBFBT(b), At^-1 = the smoother on A.  Vectors are [u | p],
+// p element-major.  The Gram-Schmidt scalars stay on the device (k_dot_dev / k_axpy_dev);
+// the Hessenberg column comes to the host once per iteration for the Givens rotations.
+struct StokesPar { int pcg, sm; double lo, hi; };
+wb_status stokes_K(wb_ctx* c, const double* x, double* y) {
+  wb_status s;
+  if ((s = run_A(c, x, y, 0))) return s;
+  if ((s = run_BT(c, x + c->n_v, nullptr, c->gsa, 0, nullptr, c->nm, 1))) return s;
+  k_axpy<<<c->red_blocks, VBS, 0, c->stream>>>(y, c->gsa, c->n_v, 1.0);
+  LAUNCH_CHECK(c);
+  return run_B(c, x, nullptr, y + c->n_v, 0, nullptr, nullptr, nullptr, c->nm, 1);
+}
+wb_status stokes_P(wb_ctx* c, const double* v, double* z, const StokesPar& P) {
+  wb_status s;
+  double* y = z + c->n_v;
+  if ((s = run_wbfbt(c, v + c->n_v, y, P.pcg))) return s;
+  k_axpby<<<c->red_blocks, VBS, 0, c->stream>>>(y, y, c->n_p, 0.0, -1.0);  // y = -wBFBT(b)
+  LAUNCH_CHECK(c);
+  if ((s = run_BT(c, y, nullptr, c->gsa, 0, nullptr, c->nm, 1))) return s;
+  k_axpby<<<c->red_blocks, VBS, 0, c->stream>>>(c->gsa, v, c->n_v, 1.0, -1.0);  // a - B^T y
+  LAUNCH_CHECK(c);
+  return run_vcheb(c, c->gsa, z, P.sm, P.lo, P.hi);
+}
+wb_status dev_dot(wb_ctx* c, const double* a, const double* b, int64_t n, double* out_dev) {
+  k_dot_dev<<<c->red_blocks, VBS, 0, c->stream>>>(a, b, n, c->partial, c->counter, out_dev);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+wb_status host_scalar(wb_ctx* c, const double* dev, double* h) {
+  CUDA_TRY(c, cudaMemcpyAsync(h, dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return WB_OK;
+}
+wb_status run_stokes(wb_ctx* c, const double* f, const double* g, double* u, double* p, int m, int max_iters,
+                     double rtol, const StokesPar& P, int* iters_out, double* relres_out) {
+  const int64_t n = c->n_v + c->n_p;
+  if (m > c->g_m) {
+    for (double** b : {&c->gV, &c->gZ}) { if (*b) cudaFree(*b); *b = nullptr; }
+    if (!lazy_alloc(&c->gV, n * (m + 1)) || !lazy_alloc(&c->gZ, n * m)) {
+      c->g_m = 0;
+      return set_err(c, WB_ENOMEM, "FGMRES basis allocation failed (restart %d)", m);
+    }
+    c->g_m = m;
+  }
+  if (!lazy_alloc(&c->gw, n) || !lazy_alloc(&c->gb, n) || !lazy_alloc(&c->gx, n) || !lazy_alloc(&c->gsa, c->n_v) ||
+      !lazy_alloc(&c->gh, (int64_t)m + 2))
+    return set_err(c, WB_ENOMEM, "FGMRES work allocation failed");
+  if (c->g_m < m) return set_err(c, WB_ENOMEM, "FGMRES basis too small");
+  wb_status s;
+  k_mask_v<<<c->red_blocks, VBS, 0, c->stream>>>(f, c->gb, c->G);  // b = (M f; g)
+  LAUNCH_CHECK(c);
+  CUDA_TRY(c, cudaMemcpyAsync(c->gb + c->n_v, g, sizeof(double) * c->n_p, cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->gx, 0, sizeof(double) * n, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->gw, c->gb, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  double bn2 = 0.0;
+  if ((s = dev_dot(c, c->gb, c->gb, n, c->gh)) || (s = host_scalar(c, c->gh, &bn2))) return s;
+  const double bnorm = std::sqrt(bn2);
+  double beta = bnorm;
+  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), gv(m + 1), y(m), col(m + 2);
+  int total = 0;
+  while (beta > rtol * bnorm && total < max_iters) {
+    // V_0 = w / beta, beta^2 = <w, w> still in gh[0] from the dot that gave beta
+    k_unit_dev<<<c->red_blocks, VBS, 0, c->stream>>>(c->gV, c->gw, n, c->gh);
+    LAUNCH_CHECK(c);
+    std::fill(gv.begin(), gv.end(), 0.0);
+    gv[0] = beta;
+    int jend = -1;
+    for (int j = 0; j < m && total < max_iters; ++j) {
+      double* Vj = c->gV + (int64_t)j * n;
+      double* Zj = c->gZ + (int64_t)j * n;
+      if ((s = stokes_P(c, Vj, Zj, P)) || (s = stokes_K(c, Zj, c->gw))) return s;
+      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, scalars on the device
+        if ((s = dev_dot(c, c->gw, c->gV + (int64_t)i * n, n, c->gh + i))) return s;
+        k_axpy_dev<<<c->red_blocks, VBS, 0, c->stream>>>(c->gw, c->gV + (int64_t)i * n, n, c->gh + i);
+        LAUNCH_CHECK(c);
+      }
+      if ((s = dev_dot(c, c->gw, c->gw, n, c->gh + j + 1))) return s;
+      CUDA_TRY(c, cudaMemcpyAsync(col.data(), c->gh, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      const double hn = std::sqrt(col[j + 1]);
+      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = col[i];
+      for (int i = 0; i < j; ++i) {  // previous rotations
+        const double a = H[(size_t)i * m + j], b = H[(size_t)(i + 1) * m + j];
+        H[(size_t)i * m + j] = cs[i] * a + sn[i] * b;
+        H[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * b;
+      }
+      const double a = H[(size_t)j * m + j], den = std::sqrt(a * a + hn * hn);
+      cs[j] = den > 0.0 ? a / den : 1.0;
+      sn[j] = den > 0.0 ? hn / den : 0.0;
+      H[(size_t)j * m + j] = den;
+      gv[j + 1] = -sn[j] * gv[j];
+      gv[j] = cs[j] * gv[j];
+      ++total;
+      jend = j;
+      if (hn > 0.0) {
+        k_unit_dev<<<c->red_blocks, VBS, 0, c->stream>>>(c->gV + (int64_t)(j + 1) * n, c->gw, n, c->gh + j + 1);
+        LAUNCH_CHECK(c);
+      }
+      if (std::fabs(gv[j + 1]) <= rtol * bnorm || hn == 0.0) break;
+    }
+    for (int i = jend; i >= 0; --i) {
+      double t = gv[i];
+      for (int k = i + 1; k <= jend; ++k) t -= H[(size_t)i * m + k] * y[k];
+      y[i] = t / H[(size_t)i * m + i];
+    }
+    for (int i = 0; i <= jend; ++i) {
+      k_axpy<<<c->red_blocks, VBS, 0, c->stream>>>(c->gx, c->gZ + (int64_t)i * n, n, y[i]);
+      LAUNCH_CHECK(c);
+    }
+    if ((s = stokes_K(c, c->gx, c->gw))) return s;  // true residual
+    k_axpby<<<c->red_blocks, VBS, 0, c->stream>>>(c->gw, c->gb, n, 1.0, -1.0);
+    LAUNCH_CHECK(c);
+    if ((s = dev_dot(c, c->gw, c->gw, n, c->gh)) || (s = host_scalar(c, c->gh, &bn2))) return s;
+    beta = std::sqrt(bn2);
+    if (jend < 0) break;
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(u, c->gx, sizeof(double) * c->n_v, cudaMemcpyDeviceToDevice, c->stream));
+  // p = P x_p (R10)
+  k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(c->gx + c->n_v, c->n_el, c->nm, c->partial, c->counter,
+                                                    c->scal + S_SUM);
+  LAUNCH_CHECK(c);
+  k_project<<<c->red_blocks, VBS, 0, c->stream>>>(c->gx + c->n_v, p, c->n_p, c->nm, c->n_el, c->scal + S_SUM);
+  LAUNCH_CHECK(c);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (iters_out) *iters_out = total;
+  if (relres_out) *relres_out = bnorm > 0.0 ? beta / bnorm : 0.0;
+  return WB_OK;
+}
+
 wb_status check_ctx(wb_ctx* c, bool need_visc) {
   if (!c) return WB_EINVAL;
   if (need_visc && !c->have_visc) return set_err(c, WB_ESTATE, "wb_set_viscosity has not been called");
@@ -761,7 +896,7 @@ void free_all(wb_ctx* c) {
   double** bufs[] = {&c->mut, &c->Cw, &c->Dw, &c->Cinv, &c->Dinv, &c->dKl, &c->dKr, &c->MinvL, &c->MinvR,
                      &c->E, &c->tv, &c->tw, &c->px, &c->pr, &c->pp, &c->pp1, &c->pq, &c->pz, &c->s0, &c->s1, &c->s2,
                      &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->Fu, &c->mueff,
-                     &c->E3, &c->dAinv, &c->tq};
+                     &c->E3, &c->dAinv, &c->tq, &c->gV, &c->gZ, &c->gw, &c->gb, &c->gx, &c->gsa, &c->gh};
   clear_graphs(c);
   if (c->cap_stream) { cudaStreamDestroy(c->cap_stream); c->cap_stream = nullptr; }
   if (c->copy_stream) { cudaStreamDestroy(c->copy_stream); c->copy_stream = nullptr; }
@@ -1170,6 +1305,22 @@ wb_status wb_velocity_eigmax(wb_ctx* c, const double* v0, int iters, double* lma
   if (s) return s;
   if (!v0 || !lmax || iters < 0) return set_err(c, WB_EINVAL, "bad argument");
   return run_veigmax(c, v0, iters, lmax);
+}
+
+wb_status wb_stokes_fgmres(wb_ctx* c, const double* f, const double* g, double* u, double* p, int restart,
+                           int max_iters, double rtol, int pcg_iters, int smooth_iters, double lmin, double lmax,
+                           int* iters, double* relres) {
+  wb_status s = check_ctx(c, true);
+  if (s) return s;
+  if (!f || !g || !u || !p || restart < 1 || max_iters < 0 || !(rtol >= 0.0) || pcg_iters < 0 || smooth_iters < 0)
+    return set_err(c, WB_EINVAL, "bad argument");
+  if (!(lmin > 0.0) || !(lmax > lmin) || !std::isfinite(lmax))
+    return set_err(c, WB_EINVAL, "the smoother interval must satisfy 0 < lmin < lmax < inf");
+  if (overlaps(u, 8 * c->n_v, f, 8 * c->n_v) || overlaps(p, 8 * c->n_p, g, 8 * c->n_p) ||
+      overlaps(u, 8 * c->n_v, p, 8 * c->n_p))
+    return set_err(c, WB_EALIAS, "outputs overlap inputs or each other");
+  return run_stokes(c, f, g, u, p, restart, max_iters, rtol, StokesPar{pcg_iters, smooth_iters, lmin, lmax}, iters,
+                    relres);
 }
 
 wb_status wb_apply_wbfbt(wb_ctx* c, const double* r, double* z, int iters) {
