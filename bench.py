@@ -295,6 +295,19 @@ def run_ours(args):
     t_vs = {it: timed(lambda: ctx.velocity_cheb(u, yd, it, 0.1 * lam_a, 1.1 * lam_a), reps=3, cold=False)
             for it in (2, 6)}
     vsmooth_iter_us = (t_vs[6] - t_vs[2]) / 4 * 1e3
+    # ---- R19: the FGMRES Stokes solve: per outer iteration = one wBFBT
+    # (iters PCG per inner solve) + a 6-step smoother on A + one Stokes operator apply
+    gz = torch.zeros(ctx.n_p, **f64)
+    us, ps = torch.empty(ctx.n_v, **f64), torch.empty(ctx.n_p, **f64)
+    t_st, rr_st = {}, {}
+    for it_o in (2, 6):
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_ev.record(stream)
+        _, _, _, rr_st[it_o] = ctx.stokes_fgmres(u, gz, us, ps, 10, it_o, 0.0, iters, 6, 0.1 * lam_a, 1.1 * lam_a)
+        b_ev.record(stream)
+        b_ev.synchronize()
+        t_st[it_o] = a_ev.elapsed_time(b_ev)
+    stokes_iter_ms = (t_st[6] - t_st[2]) / 4
     # ---- dominant kernel: the fused Poisson operator inside the PCG loops (2 x iters
     # launches per step).  Profiled pass: the same hot-path step with a CUDA-event
     # pair around every such launch (library option "profile": plain launches on
@@ -379,7 +392,10 @@ def run_ours(args):
                              "k_cheb_bytes_per_launch": 64 * n_p,
                              "note": "SURVEY 8(f) #2 (not in the step): x = P Cheb(K_r, P b), R16"},
                     "velocity_smoother": {"diagA_ms": t_diagA, "iter_us": vsmooth_iter_us,
-                                          "note": "R18 (not in the step): x = Cheb(M A M, M b), Jacobi mask/diag(A)"}},
+                                          "note": "R18 (not in the step): x = Cheb(M A M, M b), Jacobi mask/diag(A)"},
+                    "stokes_fgmres": {"iter_ms": stokes_iter_ms, "relres_after": {str(k): v for k, v in rr_st.items()},
+                                      "note": "R19 (not in the step): FGMRES on [A B^T; B 0], f = u, g = 0; per "
+                                              "iteration wBFBT (2 x iters PCG) + 6 smoother steps"}},
                 "roofline": roof,
                 "e2e": {"value": e2e, "unit": "hot-path steps/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h},
