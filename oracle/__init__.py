@@ -71,6 +71,8 @@ def lib():
             L.or_poisson_relres.argtypes = [C.c_void_p, _D, _D, _D]
             L.or_grad_weights.argtypes = [C.c_void_p, _D, _D]
             L.or_diag_A.argtypes = [C.c_void_p, _D, _D]
+            L.or_wbfbt_cheb.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, _D, _D, C.c_int, C.c_double, C.c_double,
+                                        C.c_double, C.c_double]
             L.or_fgmres_dense.argtypes = [C.c_int64, _D, _D, _D, _D, C.c_int, C.c_int, C.c_double, _D]
             L.or_fgmres_dense.restype = C.c_int
             L.or_stokes_fgmres.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, _D, _D, _D, _D, C.c_int, C.c_int,
@@ -338,6 +340,16 @@ class Oracle:
         z = np.zeros(self.n_p)
         self.L.or_wbfbt(self.h, _p(self.mu_q), _p(s["Cinv"]), _p(s["Dinv"]), _p(s["diagKl"]),
                         _p(s["diagKr"]), _p(r), _p(z), int(iters))
+        return z
+
+    def wbfbt_cheb(self, r, iters, lmin_l, lmax_l, lmin_r, lmax_r, state=None) -> np.ndarray:
+        """wBFBT with Chebyshev-Jacobi inner Poisson solves on the given intervals (R16)."""
+        s = self.state if state is None else state
+        r = _f64(r)
+        z = np.zeros(self.n_p)
+        self.L.or_wbfbt_cheb(self.h, _p(self.mu_q), _p(s["Cinv"]), _p(s["Dinv"]), _p(s["diagKl"]),
+                             _p(s["diagKr"]), _p(r), _p(z), int(iters), float(lmin_l), float(lmax_l),
+                             float(lmin_r), float(lmax_r))
         return z
 
     @staticmethod

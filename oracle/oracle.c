@@ -931,6 +931,27 @@ int or_stokes_fgmres(or_ctx* c, const double* mu_q, const double* Cinv, const do
   return it;
 }
 
+/* wBFBT with Chebyshev-accelerated Jacobi as the inner Poisson solves (SURVEY 8(f) #2 "as
+ * the inner Poisson solve", R16): or_wbfbt with y = P Cheb(K_r, P r) on [lmin_r, lmax_r] and
+ * z = P Cheb(K_l, s) on [lmin_l, lmax_l].  A fixed linear map of r (unlike the PCG form). */
+void or_wbfbt_cheb(or_ctx* c, const double* mu_q, const double* Cinv, const double* Dinv, const double* diagKl,
+                   const double* diagKr, const double* r, double* z, int iters, double lmin_l, double lmax_l,
+                   double lmin_r, double lmax_r) {
+  const int64_t np = c->n_p, nv = c->n_v, nn = c->n_nodes;
+  double* y = (double*)malloc(sizeof(double) * np);
+  double* s = (double*)malloc(sizeof(double) * np);
+  double* v = (double*)malloc(sizeof(double) * nv);
+  double* w = (double*)malloc(sizeof(double) * nv);
+  or_poisson_cheb(c, Dinv, diagKr, r, y, iters, lmin_r, lmax_r);
+  or_apply_BT(c, y, v, 0);
+  for (int cc = 0; cc < 3; ++cc) for (int64_t g = 0; g < nn; ++g) v[cc * nn + g] *= Dinv[g];
+  or_apply_A(c, mu_q, v, w, 0);
+  for (int cc = 0; cc < 3; ++cc) for (int64_t g = 0; g < nn; ++g) w[cc * nn + g] *= Cinv[g];
+  or_apply_B(c, w, s, 0);
+  or_poisson_cheb(c, Cinv, diagKl, s, z, iters, lmin_l, lmax_l);
+  free(y); free(s); free(v); free(w);
+}
+
 /* Relative residual ||b - K x|| / ||b|| of a Poisson solve (quality check). */
 double or_poisson_relres(or_ctx* c, const double* Xinv, const double* b, const double* x) {
   double* q = (double*)malloc(sizeof(double) * c->n_p);

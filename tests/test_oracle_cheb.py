@@ -152,3 +152,26 @@ def test_poisson_eigmax_converges_to_spectral_radius():
         ref = np.linalg.norm(np.linalg.matrix_power(MK, it) @ v0) / np.linalg.norm(
             np.linalg.matrix_power(MK, it - 1) @ v0)
         assert abs(o.poisson_eigmax(st["Dinv"], st["diagKr"], v0, it) - ref) <= 1e-11 * ref
+
+
+def test_wbfbt_cheb_equals_closed_form():
+    """wBFBT with Chebyshev inner solves (R16) = P F_l P B C^-1 A D^-1 B^T P F_r P r, with
+    F_side the closed-form Chebyshev filter of the dense K_side (assembled B and A)."""
+    from tests.test_oracle_diagA import _dense_A
+    o = Oracle(2, 2)
+    st = o.setup(_mild_mu(o, 9), 1.0, 2.0)
+    B = _dense_B(o)
+    mask = o.boundary_mask().astype(bool)
+    A = _dense_A(o, o.mu_q)
+    A[mask, :] = 0; A[:, mask] = 0
+    Ci, Di = np.tile(st["Cinv"], 3), np.tile(st["Dinv"], 3)
+    Kl, Kr = B @ (Ci[:, None] * B.T), B @ (Di[:, None] * B.T)
+    Ml, Mr = 1.0 / st["diagKl"], 1.0 / st["diagKr"]
+    it, lo_l, hi_l, lo_r, hi_r = 7, 0.2, 2.4, 0.15, 2.2
+    r = np.random.default_rng(6).uniform(-1, 1, o.n_p)
+    P = o.project
+    y = P(_closed_form(Kr, Mr, P(r), it, lo_r, hi_r))
+    s = B @ (Ci * (A @ (Di * (B.T @ y))))
+    ref = P(_closed_form(Kl, Ml, P(s), it, lo_l, hi_l))
+    got = o.wbfbt_cheb(r, it, lo_l, hi_l, lo_r, hi_r)
+    assert np.linalg.norm(got - ref) <= 1e-11 * np.linalg.norm(ref)
