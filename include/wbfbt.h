@@ -133,6 +133,13 @@ wb_status wb_poisson_cheb(wb_ctx* ctx, int side, const double* b, double* x, int
  * reproducible).  lmax: host.  Synchronises the context stream.  WB_EINVAL for
  * side not 0/1, iters < 0 or null pointers; WB_ESTATE before wb_set_viscosity. */
 wb_status wb_poisson_eigmax(wb_ctx* ctx, int side, const double* v0, int iters, double* lmax);
+/* SURVEY 8(f) #2 "as the inner Poisson solve": from now on wBFBT (wb_apply_wbfbt,
+ * wb_hotpath[_host], wb_stokes_fgmres) solves its two Poisson problems with
+ * wb_poisson_cheb on [lmin_l, lmax_l] (K_l, side 0) and [lmin_r, lmax_r] (K_r, side 1),
+ * `iters` steps each, instead of PCG; wBFBT is then a fixed linear map (R16).  All four 0:
+ * back to PCG (the default).  WB_EINVAL unless each 0 < lmin < lmax < inf.  wb_query
+ * "inner" reads the choice. */
+wb_status wb_set_inner_cheb(wb_ctx* ctx, double lmin_l, double lmax_l, double lmin_r, double lmax_r);
 /* diag(M A M) (reading R18): dA[c * n_nodes + g] = sum over the elements holding node g of
  * the element matrix diagonal, sum_q mu w_q detJ (2/h)^2 (|grad_xi phi_a|^2 + (d_xi_c phi_a)^2);
  * Dirichlet dofs 0.  dA: device, n_v (SoA).  WB_EINVAL for a null pointer; WB_ESTATE

@@ -44,6 +44,7 @@ SYMBOLS = [
     ("wb_poisson_cheb", _i, [_vp, _i, _vp, _vp, _i, _d, _d]),
     ("wb_poisson_eigmax", _i, [_vp, _i, _vp, _i, C.POINTER(_d)]),
     ("wb_get_diagA", _i, [_vp, _vp]),
+    ("wb_set_inner_cheb", _i, [_vp, _d, _d, _d, _d]),
     ("wb_velocity_cheb", _i, [_vp, _vp, _vp, _i, _d, _d]),
     ("wb_velocity_eigmax", _i, [_vp, _vp, _i, C.POINTER(_d)]),
     ("wb_stokes_fgmres", _i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _d, _i, _i, _d, _d, C.POINTER(_i), C.POINTER(_d)]),
@@ -229,6 +230,9 @@ class Context:
         lam = C.c_double(0.0)
         self._check(self._L.wb_poisson_eigmax(self._h, int(side), _ptr(v0, self.n_p), int(iters), C.byref(lam)))
         return lam.value
+
+    def set_inner_cheb(self, lmin_l=0.0, lmax_l=0.0, lmin_r=0.0, lmax_r=0.0):
+        self._check(self._L.wb_set_inner_cheb(self._h, float(lmin_l), float(lmax_l), float(lmin_r), float(lmax_r)))
 
     def get_diagA(self, dA):
         self._check(self._L.wb_get_diagA(self._h, _ptr(dA, self.n_v)))

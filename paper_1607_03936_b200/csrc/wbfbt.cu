@@ -81,6 +81,10 @@ struct wb_ctx {
   double *gV = nullptr, *gZ = nullptr, *gw = nullptr, *gb = nullptr, *gx = nullptr, *gsa = nullptr,
          *gh = nullptr;
   int g_m = 0;
+  // wBFBT inner Poisson solves: 0 = Jacobi-PCG (a9), 1 = Chebyshev-Jacobi on [cheb_lo, cheb_hi]
+  // per side (0 = l, 1 = r), set by wb_set_inner_cheb
+  int inner = 0;
+  double cheb_lo[2] = {0.0, 0.0}, cheb_hi[2] = {0.0, 0.0};
   int weights = 0;
   int n_tiles = 0;
   int use_graph = 1;
@@ -739,9 +743,15 @@ wb_status run_K(wb_ctx* c, int side, const double* p, double* q) {
   return WB_OK;
 }
 
+// wBFBT's inner Poisson solve: PCG, or Chebyshev-Jacobi when wb_set_inner_cheb chose it
+wb_status run_inner(wb_ctx* c, int side, const double* b, double* x, int iters) {
+  if (c->inner) return run_cheb(c, side, b, x, iters, c->cheb_lo[side], c->cheb_hi[side]);
+  return run_poisson(c, side, b, x, iters);
+}
+
 wb_status run_wbfbt(wb_ctx* c, const double* r, double* z, int iters) {
   // y = P PCG(K_r, P r)
-  wb_status s = run_poisson(c, 1, r, c->s2, iters);
+  wb_status s = run_inner(c, 1, r, c->s2, iters);
   if (s) return s;
   // v = Dinv o (B^T y)
   s = run_BT(c, c->s2, c->Dinv, c->tw, 0, nullptr, c->nm, 1);
@@ -753,7 +763,7 @@ wb_status run_wbfbt(wb_ctx* c, const double* r, double* z, int iters) {
   s = run_B(c, c->tv, c->Cinv, c->s2, 0, nullptr, nullptr, nullptr, c->nm, 1);
   if (s) return s;
   // z = P PCG(K_l, s)   (run_poisson projects its input first)
-  return run_poisson(c, 0, c->s2, z, iters);
+  return run_inner(c, 0, c->s2, z, iters);
 }
 
 // ---- Stokes solve (R19): flexible GMRES on [A B^T; B 0] with P^-1 (a; b) =
@@ -1323,6 +1333,21 @@ wb_status wb_stokes_fgmres(wb_ctx* c, const double* f, const double* g, double* 
                     relres);
 }
 
+wb_status wb_set_inner_cheb(wb_ctx* c, double lmin_l, double lmax_l, double lmin_r, double lmax_r) {
+  if (!c) return WB_EINVAL;
+  if (lmin_l == 0.0 && lmax_l == 0.0 && lmin_r == 0.0 && lmax_r == 0.0) {
+    c->inner = 0;
+    return WB_OK;
+  }
+  const double lo[2] = {lmin_l, lmin_r}, hi[2] = {lmax_l, lmax_r};
+  for (int i = 0; i < 2; ++i)
+    if (!(lo[i] > 0.0) || !(hi[i] > lo[i]) || !std::isfinite(hi[i]))
+      return set_err(c, WB_EINVAL, "each interval must satisfy 0 < lmin < lmax < inf (or all four 0)");
+  for (int i = 0; i < 2; ++i) { c->cheb_lo[i] = lo[i]; c->cheb_hi[i] = hi[i]; }
+  c->inner = 1;
+  return WB_OK;
+}
+
 wb_status wb_apply_wbfbt(wb_ctx* c, const double* r, double* z, int iters) {
   wb_status s = check_ctx(c, true);
   if (s) return s;
@@ -1392,7 +1417,7 @@ wb_status wb_hotpath_host(wb_ctx* c, const double* mu_q, double a_l, double a_r,
   const int nomask = (c->flags & WB_DEBUG_NOMASK) ? 1 : 0;
   // wBFBT, right solve: y = P PCG(K_r, P p)
   CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_p, 0));
-  if ((s = run_poisson(c, 1, dp, c->s2, iters))) return s;
+  if ((s = run_inner(c, 1, dp, c->s2, iters))) return s;
   // standalone applies
   CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_in, 0));
   if ((s = run_A(c, du, dyA, nomask))) return s;
@@ -1409,7 +1434,7 @@ wb_status wb_hotpath_host(wb_ctx* c, const double* mu_q, double a_l, double a_r,
   if ((s = run_BT(c, c->s2, c->Dinv, c->tw, 0, nullptr, c->nm, 1))) return s;
   if ((s = run_A(c, c->tw, c->tv, 0))) return s;
   if ((s = run_B(c, c->tv, c->Cinv, c->s2, 0, nullptr, nullptr, nullptr, c->nm, 1))) return s;
-  if ((s = run_poisson(c, 0, c->s2, dz, iters))) return s;
+  if ((s = run_inner(c, 0, c->s2, dz, iters))) return s;
   CUDA_TRY(c, cudaMemcpyAsync(z, dz, bp, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(cs));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -1538,6 +1563,8 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
     *value = tma_active(c) ? 1.0 : 0.0;
   } else if (!strcmp(key, "weights")) {
     *value = c->weights;
+  } else if (!strcmp(key, "inner")) {  // 1: wBFBT's inner solves are Chebyshev-Jacobi (wb_set_inner_cheb)
+    *value = c->inner;
   } else if (!strcmp(key, "k_ws")) {  // 1: ... as the warp-specialised TMA kernel (k_K2_ws)
     *value = (tma_active(c) && c->k_ws) ? 1.0 : 0.0;
   } else if (!strcmp(key, "occ_a2")) {

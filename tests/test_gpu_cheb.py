@@ -97,3 +97,29 @@ def test_cheb_residual_decreases_with_exact_interval():
         x = host(p.ctx.poisson_cheb(1, dev(b), empty(p.ctx.n_p), it, 0.1 * lam, 1.1 * lam))
         res.append(p.o.poisson_relres(X, b, x))
     assert res[0] > res[1] > res[2]
+
+
+@pytest.mark.parametrize("cfg,N,iters", [("C1", None, 6), ("C2", 8, 10), ("C3", 12, 10), ("C4", 4, 8), ("C5", 44, 10)])
+def test_wbfbt_with_cheb_inner_matches_oracle(cfg, N, iters):
+    """wBFBT with Chebyshev-Jacobi inner solves (wb_set_inner_cheb, R16): a linear map, so
+    parity is rounding-level (1e-10; 1e-8 where K_w is indefinite)."""
+    p = Pair(cfg, N=N)
+    lo_l, hi_l, _, _, _ = _interval(p, 0)
+    lo_r, hi_r, _, _, _ = _interval(p, 1)
+    p.ctx.set_inner_cheb(lo_l, hi_l, lo_r, hi_r)
+    assert p.ctx.query("inner") == 1
+    b = p.inp["p"]
+    ref = p.o.wbfbt_cheb(b, iters, lo_l, hi_l, lo_r, hi_r)
+    got = host(p.ctx.apply_wbfbt(dev(b), empty(p.ctx.n_p), iters))
+    definite = p.ost["n_nonpos_Cw"] == 0 and p.ost["n_nonpos_Dw"] == 0
+    assert rel_l2(got, ref) <= (1e-10 if definite else 1e-8), rel_l2(got, ref)
+    # the hot-path entry uses the same inner solves
+    yA, pB = empty(p.ctx.n_v), empty(p.ctx.n_p)
+    yBT, z = empty(p.ctx.n_v), empty(p.ctx.n_p)
+    p.ctx.hotpath(p.mu, dev(p.inp["u"]), dev(b), iters, yA, pB, yBT, z)
+    assert np.array_equal(host(z), got)
+    p.ctx.set_inner_cheb()
+    assert p.ctx.query("inner") == 0
+    from paper_1607_03936_b200 import WBError
+    with pytest.raises(WBError):
+        p.ctx.set_inner_cheb(1.0, 0.5, 0.1, 1.0)
