@@ -287,6 +287,11 @@ def run_ours(args):
     t_cheb = {it: timed(lambda: ctx.poisson_cheb(1, p, qv, it, 0.1 * lam, 1.1 * lam), reps=5, cold=False)
               for it in (10, 50, iters)}
     cheb_iter_us = (t_cheb[50] - t_cheb[10]) / 40 * 1e3
+    # wBFBT with Chebyshev-Jacobi inner solves (both sides, iters steps each)
+    lam_l = ctx.poisson_eigmax(0, v0, 20)
+    ctx.set_inner_cheb(0.1 * lam_l, 1.1 * lam_l, 0.1 * lam, 1.1 * lam)
+    tW_cheb = timed(lambda: ctx.apply_wbfbt(p, z, iters), reps=max(3, args.comp_reps // 4))
+    ctx.set_inner_cheb()
     # ---- R18: diag(A) and the Chebyshev-Jacobi smoother on A (SURVEY 8(f) #1's approximate A^-1)
     yd = torch.empty(ctx.n_v, **f64)
     t_diagA = timed(lambda: ctx.get_diagA(yd), reps=5)
@@ -388,6 +393,7 @@ def run_ours(args):
                     "K_ms_cold": tK, "K_ms_warm": tKw, "wbfbt_ms": tW, "wbfbt_applies_per_s": 1e3 / tW,
                     "setup_ms": tS, "setup_grad_weights_ms": tSg,
                     "cheb": {"iter_us": cheb_iter_us, "solve_ms": t_cheb[iters], "iters": iters,
+                             "wbfbt_cheb_inner_ms": tW_cheb, "wbfbt_cheb_inner_applies_per_s": 1e3 / tW_cheb,
                              "interval": [0.1 * lam, 1.1 * lam], "eigmax_20_ms": t_eig,
                              "k_cheb_bytes_per_launch": 64 * n_p,
                              "note": "SURVEY 8(f) #2 (not in the step): x = P Cheb(K_r, P b), R16"},
