@@ -76,7 +76,7 @@ def lib():
             L.or_fgmres_dense.argtypes = [C.c_int64, _D, _D, _D, _D, C.c_int, C.c_int, C.c_double, _D]
             L.or_fgmres_dense.restype = C.c_int
             L.or_stokes_fgmres.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, _D, _D, _D, _D, C.c_int, C.c_int,
-                                           C.c_double, C.c_int, C.c_int, C.c_double, C.c_double, _D]
+                                           C.c_double, C.c_int, C.c_int, C.c_double, C.c_double, _D, _D]
             L.or_stokes_fgmres.restype = C.c_int
             L.or_velocity_cheb.argtypes = [C.c_void_p, _D, _D, _D, C.c_int, C.c_double, C.c_double]
             L.or_velocity_eigmax.argtypes = [C.c_void_p, _D, _D, C.c_int]
@@ -299,14 +299,18 @@ class Oracle:
         mu_q, v0 = _f64(mu_q), _f64(v0)
         return float(self.L.or_velocity_eigmax(self.h, _p(mu_q), _p(v0), int(iters)))
 
-    def stokes_fgmres(self, f, g, restart, max_iters, rtol, pcg_iters, smooth_iters, lmin, lmax, state=None):
-        """(u, p, iterations, relres): FGMRES on [A B^T; B 0] with eq:precond-stokes (R19)."""
+    def stokes_fgmres(self, f, g, restart, max_iters, rtol, pcg_iters, smooth_iters, lmin, lmax, state=None,
+                      inner=None):
+        """(u, p, iterations, relres): FGMRES on [A B^T; B 0] with eq:precond-stokes (R19).
+        inner = (lmin_l, lmax_l, lmin_r, lmax_r): wBFBT with Chebyshev inner solves."""
         st = self.state if state is None else state
         f, g = _f64(f), _f64(g)
         u, p, rr = np.zeros(self.n_v), np.zeros(self.n_p), np.zeros(1)
+        inn = _f64(inner) if inner is not None else None
         it = self.L.or_stokes_fgmres(self.h, _p(self.mu_q), _p(st["Cinv"]), _p(st["Dinv"]), _p(st["diagKl"]),
                                      _p(st["diagKr"]), _p(f), _p(g), _p(u), _p(p), int(restart), int(max_iters),
-                                     float(rtol), int(pcg_iters), int(smooth_iters), float(lmin), float(lmax), _p(rr))
+                                     float(rtol), int(pcg_iters), int(smooth_iters), float(lmin), float(lmax), _p(rr),
+                                     _p(inn) if inn is not None else None)
         return u, p, int(it), float(rr[0])
 
     def poisson_relres(self, Xinv, b, x) -> float:

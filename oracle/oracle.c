@@ -811,6 +811,9 @@ void or_wbfbt(or_ctx* c, const double* mu_q, const double* Cinv, const double* D
  * residual estimate is <= rtol ||b|| or after max_iters iterations; the final pressure
  * is projected (R10).  The core runs over operator / preconditioner callbacks, and the
  * dense form or_fgmres_dense is what tests/test_oracle_stokes.py pins.                */
+void or_wbfbt_cheb(or_ctx* c, const double* mu_q, const double* Cinv, const double* Dinv, const double* diagKl,
+                   const double* diagKr, const double* r, double* z, int iters, double lmin_l, double lmax_l,
+                   double lmin_r, double lmax_r);
 typedef void (*or_vop)(void* ctx, const double* in, double* out);
 static int fgmres_run(or_vop K, or_vop Pinv, void* ctx, int64_t n, const double* b, double* x, int m, int max_iters,
                       double rtol, double* relres) {
@@ -892,6 +895,7 @@ int or_fgmres_dense(int64_t n, const double* A, const double* P, const double* b
 typedef struct {
   or_ctx* c; const double *mu, *Cinv, *Dinv, *dKl, *dKr;
   int pcg, sm; double lo, hi; double *tv, *tp;
+  double ilo_l, ihi_l, ilo_r, ihi_r; /* > 0: wBFBT's inner solves are Chebyshev (R16) */
 } or_stokes;
 static void stokes_K(void* ctx, const double* in, double* out) { /* [A B^T; B 0] (u; p) */
   or_stokes* S = (or_stokes*)ctx;
@@ -905,21 +909,27 @@ static void stokes_P(void* ctx, const double* in, double* out) { /* P^{-1} (a; b
   or_stokes* S = (or_stokes*)ctx;
   or_ctx* c = S->c;
   double* y = out + c->n_v;
-  or_wbfbt(c, S->mu, S->Cinv, S->Dinv, S->dKl, S->dKr, in + c->n_v, y, S->pcg);
+  if (S->ilo_l > 0.0)
+    or_wbfbt_cheb(c, S->mu, S->Cinv, S->Dinv, S->dKl, S->dKr, in + c->n_v, y, S->pcg, S->ilo_l, S->ihi_l, S->ilo_r,
+                  S->ihi_r);
+  else
+    or_wbfbt(c, S->mu, S->Cinv, S->Dinv, S->dKl, S->dKr, in + c->n_v, y, S->pcg);
   for (int64_t i = 0; i < c->n_p; ++i) y[i] = -y[i];
   or_apply_BT(c, y, S->tv, 0);
   for (int64_t i = 0; i < c->n_v; ++i) S->tv[i] = in[i] - S->tv[i];
   or_velocity_cheb(c, S->mu, S->tv, out, S->sm, S->lo, S->hi);
 }
+/* inner (may be NULL): {lmin_l, lmax_l, lmin_r, lmax_r} -> wBFBT with Chebyshev inner solves */
 int or_stokes_fgmres(or_ctx* c, const double* mu_q, const double* Cinv, const double* Dinv, const double* diagKl,
                      const double* diagKr, const double* f, const double* g, double* u, double* p, int m,
                      int max_iters, double rtol, int pcg_iters, int smooth_iters, double lmin, double lmax,
-                     double* relres) {
+                     double* relres, const double* inner) {
   const int64_t n = c->n_v + c->n_p;
   double* b = (double*)malloc(sizeof(double) * n);
   double* x = (double*)malloc(sizeof(double) * n);
   or_stokes S = {c, mu_q, Cinv, Dinv, diagKl, diagKr, pcg_iters, smooth_iters, lmin, lmax,
-                 (double*)malloc(sizeof(double) * c->n_v), NULL};
+                 (double*)malloc(sizeof(double) * c->n_v), NULL,
+                 inner ? inner[0] : 0.0, inner ? inner[1] : 0.0, inner ? inner[2] : 0.0, inner ? inner[3] : 0.0};
   memcpy(b, f, sizeof(double) * c->n_v);
   mask_velocity(c, b);
   memcpy(b + c->n_v, g, sizeof(double) * c->n_p);

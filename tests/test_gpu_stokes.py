@@ -62,3 +62,29 @@ def test_stokes_fgmres_converges_and_validates():
         p.ctx.stokes_fgmres(dev(f), dev(g), empty(p.ctx.n_v), empty(p.ctx.n_p), 0, 10, 1e-6, 5, 3, lo, hi)
     with pytest.raises(WBError):
         p.ctx.stokes_fgmres(dev(f), dev(g), empty(p.ctx.n_v), empty(p.ctx.n_p), 10, 10, 1e-6, 5, 3, hi, lo)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_stokes_fgmres_cheb_inner_matches_oracle(seed):
+    """With Chebyshev-Jacobi inner solves wBFBT is linear (R16), so the whole
+    preconditioned FGMRES follows the oracle to rounding (1e-9).  C2 at its N = 16, where
+    the lumped masses are positive: on the coarse indefinite meshes (C4 at N <= 5 has 68-192
+    nonpositive entries) the K_w spectrum leaves any Chebyshev interval and the filter
+    diverges, amplifying rounding without bound."""
+    p = Pair("C2", seed=seed)
+    assert p.ost["n_nonpos_Cw"] == 0 and p.ost["n_nonpos_Dw"] == 0
+    lo, hi = _interval(p)
+    ivals = []
+    for X, d in ((p.ost["Cinv"], p.ost["diagKl"]), (p.ost["Dinv"], p.ost["diagKr"])):
+        lam = p.o.poisson_eigmax(X, d, np.random.default_rng(11).standard_normal(p.o.n_p), 30)
+        ivals += [0.1 * lam, 1.1 * lam]
+    p.ctx.set_inner_cheb(*ivals)
+    f = p.inp["u"]
+    g = np.zeros(p.ctx.n_p)
+    uo, po, ito, rro = p.o.stokes_fgmres(f, g, 4, 8, 0.0, 10, 4, lo, hi, inner=ivals)
+    ug, pg, itg, rrg = p.ctx.stokes_fgmres(dev(f), dev(g), empty(p.ctx.n_v), empty(p.ctx.n_p), 4, 8, 0.0, 10, 4,
+                                           lo, hi)
+    assert itg == ito == 8
+    assert rel_l2(host(ug), uo) <= 1e-9
+    assert rel_l2(host(pg), po) <= 1e-9
+    assert abs(rrg - rro) <= 1e-9 * rro
