@@ -572,6 +572,13 @@ wb_status run_poisson(wb_ctx* c, int side, const double* b, double* x, int iters
   return WB_OK;
 }
 
+// grid of a pure streaming kernel (no reduction partials): one item per thread, up to 16
+// waves of 148 SMs (the grid-stride loop covers the rest) -- enough loads in flight to
+// approach HBM bandwidth; the reduction grid (red_blocks) leaves the SMs latency-bound here
+inline unsigned stream_blocks(int64_t items) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(nblk(items, VBS), 148 * 16));
+}
+
 // the Chebyshev iterations proper (Saad Alg. 12.1 steps after the start d), on c->stream
 wb_status cheb_loop_direct(wb_ctx* c, int side, int iters, double lmin, double lmax) {
   const double* Minv = side == 0 ? c->MinvL : c->MinvR;
@@ -583,7 +590,7 @@ wb_status cheb_loop_direct(wb_ctx* c, int side, int iters, double lmin, double l
     wb_status s = run_K_pcg(c, side, 2, c->pp, c->pp1, nullptr, c->pq, PcgArgs{}, &pcur, &npq);
     if (s) return s;
     const double rho1 = 1.0 / (2.0 * sigma1 - rho);
-    k_cheb<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, c->pp, c->pq, Minv, c->pl.n, rho1 * rho,
+    k_cheb<<<stream_blocks(c->pl.n / 2), VBS, 0, c->stream>>>(c->px, c->pr, c->pp, c->pq, Minv, c->pl.n, rho1 * rho,
                                                  2.0 * rho1 / delta, 0);
     LAUNCH_CHECK(c);
     rho = rho1;
@@ -604,7 +611,7 @@ wb_status run_cheb(wb_ctx* c, int side, const double* b, double* x, int iters, d
                                                    nullptr, c->pl, c->N);
   LAUNCH_CHECK(c);
   const double theta = 0.5 * (lmax + lmin);
-  k_cheb<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, c->pp, nullptr, Minv, n, 0.0, 1.0 / theta, 1);
+  k_cheb<<<stream_blocks(n / 2), VBS, 0, c->stream>>>(c->px, c->pr, c->pp, nullptr, Minv, n, 0.0, 1.0 / theta, 1);
   LAUNCH_CHECK(c);
   wb_status s = graph_loop(c, 1, side, iters, lmin, lmax, [&] { return cheb_loop_direct(c, side, iters, lmin, lmax); });
   if (s) return s;
@@ -695,12 +702,12 @@ wb_status run_vcheb(wb_ctx* c, const double* b, double* x, int iters, double lmi
   LAUNCH_CHECK(c);
   const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin), sigma1 = theta / delta;
   double rho = 1.0 / sigma1;
-  k_cheb_s<<<c->red_blocks, VBS, 0, c->stream>>>(x, r, d, nullptr, c->dAinv, n, 0.0, 1.0 / theta, 1);
+  k_cheb_s<<<stream_blocks(n), VBS, 0, c->stream>>>(x, r, d, nullptr, c->dAinv, n, 0.0, 1.0 / theta, 1);
   LAUNCH_CHECK(c);
   for (int it = 0; it < iters; ++it) {
     if ((s = run_A(c, d, q, 0))) return s;
     const double rho1 = 1.0 / (2.0 * sigma1 - rho);
-    k_cheb_s<<<c->red_blocks, VBS, 0, c->stream>>>(x, r, d, q, c->dAinv, n, rho1 * rho, 2.0 * rho1 / delta, 0);
+    k_cheb_s<<<stream_blocks(n), VBS, 0, c->stream>>>(x, r, d, q, c->dAinv, n, rho1 * rho, 2.0 * rho1 / delta, 0);
     LAUNCH_CHECK(c);
     rho = rho1;
   }
