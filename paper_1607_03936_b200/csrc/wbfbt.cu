@@ -197,6 +197,9 @@ wb_status launch_gather_t(wb_ctx* c, const double* s, double* y, int nomask) {
   return WB_OK;
 }
 
+#ifndef RED_MULT
+#define RED_MULT 2  // blocks per SM of the PCG vector kernels (their rz partials: red_blocks)
+#endif
 #ifndef BSPLIT_EPB
 #define BSPLIT_EPB 16  // elements per block of the generic split B kernel (k = 3, 4; >= 8, see pqp)
 #endif
@@ -1017,7 +1020,7 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  c->red_blocks = 2 * nsm;
+  c->red_blocks = RED_MULT * nsm;
   c->nsm = nsm;
   c->max_partials = (int)std::max<int64_t>(c->red_blocks, (c->n_el + 127) / 128 + 1);
   bool ok = true;
