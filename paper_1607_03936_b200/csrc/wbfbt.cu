@@ -141,6 +141,12 @@ wb_status set_err(wb_ctx* c, wb_status s, const char* fmt, ...) {
   } while (0)
 
 inline unsigned nblk(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+// grid of a pure streaming kernel (no reduction partials): one item per thread, up to 16
+// waves of 148 SMs (the grid-stride loop covers the rest) -- enough loads in flight to
+// approach HBM bandwidth; the reduction grid (red_blocks) leaves the SMs latency-bound here
+inline unsigned stream_blocks(int64_t items) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(nblk(items, VBS), 148 * 16));
+}
 
 bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
   const char* x = (const char*)a;
@@ -570,17 +576,11 @@ wb_status run_poisson(wb_ctx* c, int side, const double* b, double* x, int iters
   if ((s = pcg_loop(c, side, iters))) return s;
   k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pl.sm, 1, c->partial, c->counter, c->scal + S_SUM + 1);
   LAUNCH_CHECK(c);
-  k_pcg_out<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->scal + S_SUM + 1, x, c->n_el, c->nm, c->pl, c->N);
+  k_pcg_out<<<stream_blocks(c->n_p), VBS, 0, c->stream>>>(c->px, c->scal + S_SUM + 1, x, c->n_el, c->nm, c->pl, c->N);
   LAUNCH_CHECK(c);
   return WB_OK;
 }
 
-// grid of a pure streaming kernel (no reduction partials): one item per thread, up to 16
-// waves of 148 SMs (the grid-stride loop covers the rest) -- enough loads in flight to
-// approach HBM bandwidth; the reduction grid (red_blocks) leaves the SMs latency-bound here
-inline unsigned stream_blocks(int64_t items) {
-  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(nblk(items, VBS), 148 * 16));
-}
 
 // the Chebyshev iterations proper (Saad Alg. 12.1 steps after the start d), on c->stream
 wb_status cheb_loop_direct(wb_ctx* c, int side, int iters, double lmin, double lmax) {
@@ -620,7 +620,7 @@ wb_status run_cheb(wb_ctx* c, int side, const double* b, double* x, int iters, d
   if (s) return s;
   k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pl.sm, 1, c->partial, c->counter, c->scal + S_SUM + 1);
   LAUNCH_CHECK(c);
-  k_pcg_out<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->scal + S_SUM + 1, x, c->n_el, c->nm, c->pl, c->N);
+  k_pcg_out<<<stream_blocks(c->n_p), VBS, 0, c->stream>>>(c->px, c->scal + S_SUM + 1, x, c->n_el, c->nm, c->pl, c->N);
   LAUNCH_CHECK(c);
   return WB_OK;
 }
@@ -633,11 +633,11 @@ wb_status run_eigmax(wb_ctx* c, int side, const double* v0, int iters, double* l
   const int nb = c->red_blocks;
   double* dlam = c->scal + S_SCR;
   CUDA_TRY(c, cudaMemsetAsync(c->pp, 0, sizeof(double) * n, c->stream));  // pads stay 0
-  k_transpose<<<nb, VBS, 0, c->stream>>>(v0, c->pp, c->n_el, c->nm, 1, c->pl, c->N);
+  k_transpose<<<stream_blocks(c->n_p), VBS, 0, c->stream>>>(v0, c->pp, c->n_el, c->nm, 1, c->pl, c->N);
   LAUNCH_CHECK(c);
   k_pow_sumsq<<<nb, VBS, 0, c->stream>>>(c->pp, nullptr, n, c->rzp);
   LAUNCH_CHECK(c);
-  k_pow_scale<<<nb, VBS, 0, c->stream>>>(c->pp, c->pp, n, c->rzp, nb, dlam);
+  k_pow_scale<<<stream_blocks(n), VBS, 0, c->stream>>>(c->pp, c->pp, n, c->rzp, nb, dlam);
   LAUNCH_CHECK(c);
   CUDA_TRY(c, cudaMemsetAsync(dlam, 0, sizeof(double), c->stream));  // lam = 0 for iters = 0 (as the oracle)
   for (int it = 0; it < iters; ++it) {
@@ -647,7 +647,7 @@ wb_status run_eigmax(wb_ctx* c, int side, const double* v0, int iters, double* l
     if (s) return s;
     k_pow_sumsq<<<nb, VBS, 0, c->stream>>>(c->pq, Minv, n, c->rzp);
     LAUNCH_CHECK(c);
-    k_pow_scale<<<nb, VBS, 0, c->stream>>>(c->pq, c->pp, n, c->rzp, nb, dlam);
+    k_pow_scale<<<stream_blocks(n), VBS, 0, c->stream>>>(c->pq, c->pp, n, c->rzp, nb, dlam);
     LAUNCH_CHECK(c);
   }
   CUDA_TRY(c, cudaMemcpyAsync(lam, dlam, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -689,7 +689,7 @@ wb_status ensure_dAinv(wb_ctx* c) {
     return set_err(c, WB_ENOMEM, "smoother buffer allocation failed");
   wb_status s = run_diagA(c, c->dAinv);
   if (s) return s;
-  k_inv_pos<<<c->red_blocks, VBS, 0, c->stream>>>(c->dAinv, c->dAinv, c->n_v);
+  k_inv_pos<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->dAinv, c->dAinv, c->n_v);
   LAUNCH_CHECK(c);
   c->dA_valid = true;
   return WB_OK;
@@ -701,7 +701,7 @@ wb_status run_vcheb(wb_ctx* c, const double* b, double* x, int iters, double lmi
   const int64_t n = c->n_v;
   double *r = c->tv, *d = c->tw, *q = c->tq;
   CUDA_TRY(c, cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream));
-  k_mask_v<<<c->red_blocks, VBS, 0, c->stream>>>(b, r, c->G);
+  k_mask_v<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(b, r, c->G);
   LAUNCH_CHECK(c);
   const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin), sigma1 = theta / delta;
   double rho = 1.0 / sigma1;
@@ -725,14 +725,14 @@ wb_status run_veigmax(wb_ctx* c, const double* v0, int iters, double* lam) {
   double *v = c->tw, *q = c->tq, *dlam = c->scal + S_SCR;
   k_pow_sumsq<<<nb, VBS, 0, c->stream>>>(const_cast<double*>(v0), nullptr, n, c->rzp);  // (no write: Minv = NULL)
   LAUNCH_CHECK(c);
-  k_pow_scale<<<nb, VBS, 0, c->stream>>>(v0, v, n, c->rzp, nb, dlam);
+  k_pow_scale<<<stream_blocks(n), VBS, 0, c->stream>>>(v0, v, n, c->rzp, nb, dlam);
   LAUNCH_CHECK(c);
   CUDA_TRY(c, cudaMemsetAsync(dlam, 0, sizeof(double), c->stream));
   for (int it = 0; it < iters; ++it) {
     if ((s = run_A(c, v, q, 0))) return s;
     k_pow_sumsq<<<nb, VBS, 0, c->stream>>>(q, c->dAinv, n, c->rzp);
     LAUNCH_CHECK(c);
-    k_pow_scale<<<nb, VBS, 0, c->stream>>>(q, v, n, c->rzp, nb, dlam);
+    k_pow_scale<<<stream_blocks(n), VBS, 0, c->stream>>>(q, v, n, c->rzp, nb, dlam);
     LAUNCH_CHECK(c);
   }
   CUDA_TRY(c, cudaMemcpyAsync(lam, dlam, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -742,13 +742,13 @@ wb_status run_veigmax(wb_ctx* c, const double* v0, int iters, double* lam) {
 
 // q = K_side p, element-major in and out (through the PCG kernels, mode "p as is")
 wb_status run_K(wb_ctx* c, int side, const double* p, double* q) {
-  k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(p, c->pp, c->n_el, c->nm, 1, c->pl, c->N);
+  k_transpose<<<stream_blocks(c->n_p), VBS, 0, c->stream>>>(p, c->pp, c->n_el, c->nm, 1, c->pl, c->N);
   LAUNCH_CHECK(c);
   const double* pcur = nullptr;
   int npq = 0;
   wb_status s = run_K_pcg(c, side, 2, c->pp, c->pp1, nullptr, c->pq, PcgArgs{}, &pcur, &npq);
   if (s) return s;
-  k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(c->pq, q, c->n_el, c->nm, 0, c->pl, c->N);
+  k_transpose<<<stream_blocks(c->n_p), VBS, 0, c->stream>>>(c->pq, q, c->n_el, c->nm, 0, c->pl, c->N);
   LAUNCH_CHECK(c);
   return WB_OK;
 }
@@ -785,7 +785,7 @@ wb_status stokes_K(wb_ctx* c, const double* x, double* y) {
   wb_status s;
   if ((s = run_A(c, x, y, 0))) return s;
   if ((s = run_BT(c, x + c->n_v, nullptr, c->gsa, 0, nullptr, c->nm, 1))) return s;
-  k_axpy<<<c->red_blocks, VBS, 0, c->stream>>>(y, c->gsa, c->n_v, 1.0);
+  k_axpy<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(y, c->gsa, c->n_v, 1.0);
   LAUNCH_CHECK(c);
   return run_B(c, x, nullptr, y + c->n_v, 0, nullptr, nullptr, nullptr, c->nm, 1);
 }
@@ -793,10 +793,10 @@ wb_status stokes_P(wb_ctx* c, const double* v, double* z, const StokesPar& P) {
   wb_status s;
   double* y = z + c->n_v;
   if ((s = run_wbfbt(c, v + c->n_v, y, P.pcg))) return s;
-  k_axpby<<<c->red_blocks, VBS, 0, c->stream>>>(y, y, c->n_p, 0.0, -1.0);  // y = -wBFBT(b)
+  k_axpby<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(y, y, c->n_p, 0.0, -1.0);  // y = -wBFBT(b)
   LAUNCH_CHECK(c);
   if ((s = run_BT(c, y, nullptr, c->gsa, 0, nullptr, c->nm, 1))) return s;
-  k_axpby<<<c->red_blocks, VBS, 0, c->stream>>>(c->gsa, v, c->n_v, 1.0, -1.0);  // a - B^T y
+  k_axpby<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->gsa, v, c->n_v, 1.0, -1.0);  // a - B^T y
   LAUNCH_CHECK(c);
   return run_vcheb(c, c->gsa, z, P.sm, P.lo, P.hi);
 }
@@ -826,7 +826,7 @@ wb_status run_stokes(wb_ctx* c, const double* f, const double* g, double* u, dou
     return set_err(c, WB_ENOMEM, "FGMRES work allocation failed");
   if (c->g_m < m) return set_err(c, WB_ENOMEM, "FGMRES basis too small");
   wb_status s;
-  k_mask_v<<<c->red_blocks, VBS, 0, c->stream>>>(f, c->gb, c->G);  // b = (M f; g)
+  k_mask_v<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(f, c->gb, c->G);  // b = (M f; g)
   LAUNCH_CHECK(c);
   CUDA_TRY(c, cudaMemcpyAsync(c->gb + c->n_v, g, sizeof(double) * c->n_p, cudaMemcpyDeviceToDevice, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(c->gx, 0, sizeof(double) * n, c->stream));
@@ -839,7 +839,7 @@ wb_status run_stokes(wb_ctx* c, const double* f, const double* g, double* u, dou
   int total = 0;
   while (beta > rtol * bnorm && total < max_iters) {
     // V_0 = w / beta, beta^2 = <w, w> still in gh[0] from the dot that gave beta
-    k_unit_dev<<<c->red_blocks, VBS, 0, c->stream>>>(c->gV, c->gw, n, c->gh);
+    k_unit_dev<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->gV, c->gw, n, c->gh);
     LAUNCH_CHECK(c);
     std::fill(gv.begin(), gv.end(), 0.0);
     gv[0] = beta;
@@ -850,7 +850,7 @@ wb_status run_stokes(wb_ctx* c, const double* f, const double* g, double* u, dou
       if ((s = stokes_P(c, Vj, Zj, P)) || (s = stokes_K(c, Zj, c->gw))) return s;
       for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, scalars on the device
         if ((s = dev_dot(c, c->gw, c->gV + (int64_t)i * n, n, c->gh + i))) return s;
-        k_axpy_dev<<<c->red_blocks, VBS, 0, c->stream>>>(c->gw, c->gV + (int64_t)i * n, n, c->gh + i);
+        k_axpy_dev<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->gw, c->gV + (int64_t)i * n, n, c->gh + i);
         LAUNCH_CHECK(c);
       }
       if ((s = dev_dot(c, c->gw, c->gw, n, c->gh + j + 1))) return s;
@@ -872,7 +872,7 @@ wb_status run_stokes(wb_ctx* c, const double* f, const double* g, double* u, dou
       ++total;
       jend = j;
       if (hn > 0.0) {
-        k_unit_dev<<<c->red_blocks, VBS, 0, c->stream>>>(c->gV + (int64_t)(j + 1) * n, c->gw, n, c->gh + j + 1);
+        k_unit_dev<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->gV + (int64_t)(j + 1) * n, c->gw, n, c->gh + j + 1);
         LAUNCH_CHECK(c);
       }
       if (std::fabs(gv[j + 1]) <= rtol * bnorm || hn == 0.0) break;
@@ -883,11 +883,11 @@ wb_status run_stokes(wb_ctx* c, const double* f, const double* g, double* u, dou
       y[i] = t / H[(size_t)i * m + i];
     }
     for (int i = 0; i <= jend; ++i) {
-      k_axpy<<<c->red_blocks, VBS, 0, c->stream>>>(c->gx, c->gZ + (int64_t)i * n, n, y[i]);
+      k_axpy<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->gx, c->gZ + (int64_t)i * n, n, y[i]);
       LAUNCH_CHECK(c);
     }
     if ((s = stokes_K(c, c->gx, c->gw))) return s;  // true residual
-    k_axpby<<<c->red_blocks, VBS, 0, c->stream>>>(c->gw, c->gb, n, 1.0, -1.0);
+    k_axpby<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->gw, c->gb, n, 1.0, -1.0);
     LAUNCH_CHECK(c);
     if ((s = dev_dot(c, c->gw, c->gw, n, c->gh)) || (s = host_scalar(c, c->gh, &bn2))) return s;
     beta = std::sqrt(bn2);
@@ -1459,7 +1459,7 @@ wb_status wb_debug_pcg_step(wb_ctx* c, int side, double* x, double* r, double* p
   const double* Minv = side == 0 ? c->MinvL : c->MinvR;
   // state in (element-major -> mode-major), rz as rz_1, iteration index 1
   for (int i = 0; i < 3; ++i) {
-    k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(i == 0 ? x : (i == 1 ? r : p), i == 0 ? c->px : (i == 1 ? c->pr : c->pp),
+    k_transpose<<<stream_blocks(c->n_p), VBS, 0, c->stream>>>(i == 0 ? x : (i == 1 ? r : p), i == 0 ? c->px : (i == 1 ? c->pr : c->pp),
                                                       c->n_el, c->nm, 1, c->pl, c->N);
     LAUNCH_CHECK(c);
   }
@@ -1480,7 +1480,7 @@ wb_status wb_debug_pcg_step(wb_ctx* c, int side, double* x, double* r, double* p
                                                rz_hist(c), pq_hist(c), c->stop);
   LAUNCH_CHECK(c);
   for (int i = 0; i < 3; ++i) {
-    k_transpose<<<c->red_blocks, VBS, 0, c->stream>>>(i == 0 ? c->px : (i == 1 ? c->pr : pc), i == 0 ? x : (i == 1 ? r : p),
+    k_transpose<<<stream_blocks(c->n_p), VBS, 0, c->stream>>>(i == 0 ? c->px : (i == 1 ? c->pr : pc), i == 0 ? x : (i == 1 ? r : p),
                                                       c->n_el, c->nm, 0, c->pl, c->N);
     LAUNCH_CHECK(c);
   }
