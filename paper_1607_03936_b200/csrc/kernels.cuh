@@ -982,6 +982,85 @@ __global__ void __launch_bounds__(VBS) k_pcg_init(const double* __restrict__ b, 
   store_partial<VBS>(s, rzp);
 }
 
+// k = 2 (n_m = 4): the same init / output through a shared-memory transpose.  A tile is
+// 32 ey x 8 ex elements at one ez: element-major b rows (8 elements x 4 modes = 32
+// consecutive words per ey) are read coalesced, the PCG vectors (y fastest, PLay) written
+// coalesced along ey.  The per-thread loops above touch one 8-byte word per 32-byte sector.
+constexpr int PT_Y = 32, PT_X = 8, PT_Q = PT_X * 4;
+__device__ __forceinline__ void pt_tile(int tile, int N, int& ex0, int& ey0, int& ez) {
+  const int nx = (N + PT_X - 1) / PT_X, ny = (N + PT_Y - 1) / PT_Y;
+  ex0 = PT_X * (tile % nx); ey0 = PT_Y * ((tile / nx) % ny); ez = tile / (nx * ny);
+}
+// rz_0: one grid reduction (block partials in `partial`, summed in order by the last
+// block) into rzp[0], rzp[1 .. nrz-1] = 0, so that the consumer's sum over nrz partials
+// gives it unchanged; this lets the grid be as wide as the data, not red_blocks.
+__global__ void __launch_bounds__(VBS) k_pcg_init_t(const double* __restrict__ b, const double* __restrict__ bsum,
+                                                    double* x, double* r, const double* __restrict__ Minv, int64_t ne,
+                                                    double* rzp, int nrz, double* partial, unsigned* counter,
+                                                    double* z, PLay L, int N) {
+  __shared__ double S[PT_Y][PT_Q + 1];
+  const double mean = *bsum / (double)ne;
+  const int nt = ((N + PT_X - 1) / PT_X) * ((N + PT_Y - 1) / PT_Y) * N;
+  double s = 0.0;
+  for (int tile = blockIdx.x; tile < nt; tile += gridDim.x) {
+    int ex0, ey0, ez;
+    pt_tile(tile, N, ex0, ey0, ez);
+    for (int t = threadIdx.x; t < PT_Y * PT_Q; t += VBS) {
+      const int yl = t / PT_Q, q = t % PT_Q, xl = q / 4, m = q % 4;
+      const int ex = ex0 + xl, ey = ey0 + yl;
+      double v = 0.0;
+      if (ex < N && ey < N) {
+        const int64_t e = ex + (int64_t)N * (ey + (int64_t)N * ez);
+        v = b[e * 4 + m];
+        if (m == 0) v -= mean;
+      }
+      S[yl][q] = v;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < PT_Y * PT_Q; t += VBS) {
+      const int yl = t % PT_Y, q = t / PT_Y, xl = q / 4, m = q % 4;
+      const int ex = ex0 + xl, ey = ey0 + yl;
+      if (ex < N && ey < N) {
+        const int64_t j = L.at(m, ex, ey, ez);
+        const double bi = S[yl][q];
+        x[j] = 0.0; r[j] = bi;
+        const double zi = Minv[j] * bi;
+        if (z) z[j] = zi;
+        s = fma(bi, zi, s);
+      }
+    }
+    __syncthreads();
+  }
+  if (grid_sum<VBS>(s, partial, counter, rzp))
+    for (int i = 1; i < nrz; ++i) rzp[i] = 0.0;
+}
+__global__ void __launch_bounds__(VBS) k_pcg_out_t(const double* __restrict__ x, const double* __restrict__ xsum,
+                                                   double* __restrict__ out, int64_t ne, PLay L, int N) {
+  __shared__ double S[PT_Y][PT_Q + 1];
+  const double mean = *xsum / (double)ne;
+  const int nt = ((N + PT_X - 1) / PT_X) * ((N + PT_Y - 1) / PT_Y) * N;
+  for (int tile = blockIdx.x; tile < nt; tile += gridDim.x) {
+    int ex0, ey0, ez;
+    pt_tile(tile, N, ex0, ey0, ez);
+    for (int t = threadIdx.x; t < PT_Y * PT_Q; t += VBS) {
+      const int yl = t % PT_Y, q = t / PT_Y, xl = q / 4, m = q % 4;
+      const int ex = ex0 + xl, ey = ey0 + yl;
+      S[yl][q] = (ex < N && ey < N) ? x[L.at(m, ex, ey, ez)] : 0.0;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < PT_Y * PT_Q; t += VBS) {
+      const int yl = t / PT_Q, q = t % PT_Q, xl = q / 4, m = q % 4;
+      const int ex = ex0 + xl, ey = ey0 + yl;
+      if (ex < N && ey < N) {
+        const int64_t e = ex + (int64_t)N * (ey + (int64_t)N * ez);
+        const double v = S[yl][q];
+        out[e * 4 + m] = (m == 0) ? v - mean : v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // direction update (generic-k path; the k = 2 path fuses it into k_K2_fused).
 // ctl: run pcg_control for iteration i (beta from the histories); otherwise
 // mode 1 uses beta = rz_hist[i] / rz_hist[i-1] as recorded.

@@ -563,6 +563,31 @@ wb_status pcg_loop(wb_ctx* c, int side, int iters) {
 }
 
 // x = P PCG(K_side, P b), exactly `iters` iterations (b, x element-major)
+// PCG input / output (R10 projection and the PLay transposes): tiled for k = 2
+wb_status launch_pcg_init(wb_ctx* c, const double* b, const double* Minv, double* z) {
+  if (c->nm == 4)
+    k_pcg_init_t<<<std::min<unsigned>(stream_blocks(c->n_p / 4), (unsigned)c->max_partials), VBS, 0, c->stream>>>(
+        b, c->scal + S_SUM, c->px, c->pr, Minv, c->n_el, c->rzp, c->red_blocks, c->partial, c->counter, z, c->pl, c->N);
+  else
+    k_pcg_init<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->scal + S_SUM, c->px, c->pr, Minv, c->n_el, c->nm, c->rzp, z,
+                                                     c->pl, c->N);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+wb_status launch_pcg_out(wb_ctx* c, double* x) {
+  if (c->nm == 4)
+    k_pcg_out_t<<<stream_blocks(c->n_p / 4), VBS, 0, c->stream>>>(c->px, c->scal + S_SUM + 1, x, c->n_el, c->pl, c->N);
+  else
+    k_pcg_out<<<stream_blocks(c->n_p), VBS, 0, c->stream>>>(c->px, c->scal + S_SUM + 1, x, c->n_el, c->nm, c->pl, c->N);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+#define LAUNCH_OR_RET(call) \
+  do {                      \
+    wb_status st_ = (call); \
+    if (st_) return st_;    \
+  } while (0)
+
 wb_status run_poisson(wb_ctx* c, int side, const double* b, double* x, int iters) {
   wb_status s = ensure_iters(c, iters);
   if (s) return s;
@@ -570,14 +595,11 @@ wb_status run_poisson(wb_ctx* c, int side, const double* b, double* x, int iters
   const double* Minv = side == 0 ? c->MinvL : c->MinvR;
   k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->n_el, c->nm, c->partial, c->counter, c->scal + S_SUM);
   LAUNCH_CHECK(c);
-  k_pcg_init<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->scal + S_SUM, c->px, c->pr, Minv, c->n_el, c->nm, c->rzp,
-                                                   z_out(c), c->pl, c->N);
-  LAUNCH_CHECK(c);
+  LAUNCH_OR_RET(launch_pcg_init(c, b, Minv, z_out(c)));
   if ((s = pcg_loop(c, side, iters))) return s;
   k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pl.sm, 1, c->partial, c->counter, c->scal + S_SUM + 1);
   LAUNCH_CHECK(c);
-  k_pcg_out<<<stream_blocks(c->n_p), VBS, 0, c->stream>>>(c->px, c->scal + S_SUM + 1, x, c->n_el, c->nm, c->pl, c->N);
-  LAUNCH_CHECK(c);
+  LAUNCH_OR_RET(launch_pcg_out(c, x));
   return WB_OK;
 }
 
@@ -610,9 +632,7 @@ wb_status run_cheb(wb_ctx* c, int side, const double* b, double* x, int iters, d
   const int64_t n = c->pl.n;
   k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->n_el, c->nm, c->partial, c->counter, c->scal + S_SUM);
   LAUNCH_CHECK(c);
-  k_pcg_init<<<c->red_blocks, VBS, 0, c->stream>>>(b, c->scal + S_SUM, c->px, c->pr, Minv, c->n_el, c->nm, c->rzp,
-                                                   nullptr, c->pl, c->N);
-  LAUNCH_CHECK(c);
+  LAUNCH_OR_RET(launch_pcg_init(c, b, Minv, nullptr));
   const double theta = 0.5 * (lmax + lmin);
   k_cheb<<<stream_blocks(n / 2), VBS, 0, c->stream>>>(c->px, c->pr, c->pp, nullptr, Minv, n, 0.0, 1.0 / theta, 1);
   LAUNCH_CHECK(c);
@@ -620,8 +640,7 @@ wb_status run_cheb(wb_ctx* c, int side, const double* b, double* x, int iters, d
   if (s) return s;
   k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pl.sm, 1, c->partial, c->counter, c->scal + S_SUM + 1);
   LAUNCH_CHECK(c);
-  k_pcg_out<<<stream_blocks(c->n_p), VBS, 0, c->stream>>>(c->px, c->scal + S_SUM + 1, x, c->n_el, c->nm, c->pl, c->N);
-  LAUNCH_CHECK(c);
+  LAUNCH_OR_RET(launch_pcg_out(c, x));
   return WB_OK;
 }
 
