@@ -1061,6 +1061,34 @@ __global__ void __launch_bounds__(VBS) k_pcg_out_t(const double* __restrict__ x,
   }
 }
 
+// k = 2 Jacobi pseudo-inverse through the same tiled transpose as k_pcg_init_t
+// (element-major diag K rows in, y-fastest PCG layout out): values as k_minv.
+__global__ void __launch_bounds__(VBS) k_minv_t(const double* __restrict__ d, double* __restrict__ minv,
+                                                const double* __restrict__ dmax, PLay L, int N) {
+  __shared__ double S[PT_Y][PT_Q + 1];
+  const double thr = 1e-13 * *dmax;
+  const int nt = ((N + PT_X - 1) / PT_X) * ((N + PT_Y - 1) / PT_Y) * N;
+  for (int tile = blockIdx.x; tile < nt; tile += gridDim.x) {
+    int ex0, ey0, ez;
+    pt_tile(tile, N, ex0, ey0, ez);
+    for (int t = threadIdx.x; t < PT_Y * PT_Q; t += VBS) {
+      const int yl = t / PT_Q, q = t % PT_Q, xl = q / 4, m = q % 4;
+      const int ex = ex0 + xl, ey = ey0 + yl;
+      S[yl][q] = (ex < N && ey < N) ? d[(ex + (int64_t)N * (ey + (int64_t)N * ez)) * 4 + m] : 0.0;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < PT_Y * PT_Q; t += VBS) {
+      const int yl = t % PT_Y, q = t / PT_Y, xl = q / 4, m = q % 4;
+      const int ex = ex0 + xl, ey = ey0 + yl;
+      if (ex < N && ey < N) {
+        const double v = S[yl][q];
+        minv[L.at(m, ex, ey, ez)] = fabs(v) > thr ? 1.0 / v : 0.0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // direction update (generic-k path; the k = 2 path fuses it into k_K2_fused).
 // ctl: run pcg_control for iteration i (beta from the histories); otherwise
 // mode 1 uses beta = rz_hist[i] / rz_hist[i-1] as recorded.

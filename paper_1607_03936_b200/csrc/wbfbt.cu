@@ -1236,8 +1236,12 @@ static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
     double* dmax = c->scal + S_DMAX + side;
     k_absmax<VBS><<<c->red_blocks, VBS, 0, c->stream>>>(d, c->n_p, c->partial, c->counter, dmax);
     LAUNCH_CHECK(c);
-    k_minv<<<c->red_blocks, VBS, 0, c->stream>>>(d, side == 0 ? c->MinvL : c->MinvR, c->n_el, c->nm, dmax, c->pl,
-                                                 c->N);
+    if (c->nm == 4)
+      k_minv_t<<<stream_blocks(c->n_p / 4), VBS, 0, c->stream>>>(d, side == 0 ? c->MinvL : c->MinvR, dmax, c->pl,
+                                                                 c->N);
+    else
+      k_minv<<<c->red_blocks, VBS, 0, c->stream>>>(d, side == 0 ? c->MinvL : c->MinvR, c->n_el, c->nm, dmax, c->pl,
+                                                   c->N);
     LAUNCH_CHECK(c);
   }
   c->have_visc = true;
