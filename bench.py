@@ -184,25 +184,58 @@ def oracle_sample(cfg_name="C5", seed=0, pcg_probe=(1, 3)):
                        f"extrapolated linearly to {cfg.iters}")
 
 
+def unit_of(cfg) -> str:
+    """The `unit` string of both arms (identical, so the driver can form their ratio)."""
+    return (f"hot-path steps/s (1 step = setup + A + B + B^T + wBFBT with 2x{cfg.iters} PCG iters, "
+            f"{cfg.name})")
+
+
+def workload_of(cfg) -> str:
+    idx = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}.get(cfg.name)
+    return (f"{cfg.name} = BASELINE.json configs[{idx}]: {cfg.N}^3 Q{cfg.k}xP{cfg.k - 1}disc, {cfg.n_sinkers} "
+            f"sinkers, DR {cfg.dr:.0e}, {cfg.iters} PCG iters")
+
+
+def oracle_full_step(cfg_name="C5", seed=0):
+    """One complete hot-path step of the oracle as it stands, timed on the host cores:
+    setup (C_w, D_w, Jacobi diagonals) + A u + B u + B^T p + wBFBT(p) with the config's
+    PCG count -- the same work as one `wb_hotpath` call."""
+    import synth
+    from oracle import Oracle
+    cfg = synth.CONFIGS[cfg_name]
+    inp = synth.make_inputs(cfg, seed)
+    o = Oracle(cfg.N, cfg.k)
+    t = {}
+    t0 = time.perf_counter(); o.setup(inp["mu_q"]); t["setup"] = time.perf_counter() - t0
+    t0 = time.perf_counter(); o.apply_A(inp["mu_q"], inp["u"]); t["A"] = time.perf_counter() - t0
+    t0 = time.perf_counter(); o.apply_B(inp["u"]); t["B"] = time.perf_counter() - t0
+    t0 = time.perf_counter(); o.apply_BT(inp["p"]); t["BT"] = time.perf_counter() - t0
+    t0 = time.perf_counter(); o.wbfbt(inp["p"], cfg.iters); t["wbfbt"] = time.perf_counter() - t0
+    n_v = 3 * (cfg.k * cfg.N + 1) ** 3
+    return dict(step_s=sum(t.values()), t=t, A_gdofs=n_v / t["A"] / 1e9, threads=Oracle.num_threads())
+
+
 def run_reference(args):
+    """The tier's reference arm: the CPU oracle (no reference implementation exists).  One
+    full step is ~1 min at C5 on the box's host cores, so exactly ONE step is timed, with no
+    warm-up (the oracle is deterministic host code); `steps` / `warmup` report what ran."""
+    import synth
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    r = oracle_sample(args.config)
-    steps_s = []
-    for _ in range(args.warmup + args.steps):
-        pass  # the oracle is timed once per bounded sample (deterministic, no warm-up effects)
+    cfg = synth.CONFIGS[args.config]
+    r = oracle_full_step(args.config)
     v = 1.0 / r["step_s"]
-    cores = r["threads"]
-    line = {"impl": "reference", "metric": METRIC, "value": v,
-            "unit": "hot-path steps/s (1 step = setup + A + B + B^T + wBFBT, C5)", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["step_s"] * 1e3,
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": unit_of(cfg), "n_gpus": args.gpus,
+            "steps": 1, "warmup": 0, "ms_per_step": r["step_s"] * 1e3,
+            "steps_requested": args.steps, "warmup_requested": args.warmup,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"{args.config} (BASELINE.json configs[4])"},
-            "cpu_baseline": {"value": v, "unit": "hot-path steps/s", "cores": cores, "kind": "oracle",
-                             "sample": r["sample"]},
-            "e2e": {"value": v, "unit": "hot-path steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "components": {"A_gdofs": r["A_gdofs"], "wbfbt_applies_per_s": 1.0 / r["wbfbt_s"],
+            "data": "synthetic", "config": {"workload": workload_of(cfg), "N": cfg.N, "k": cfg.k},
+            "cpu_baseline": {"value": v, "unit": unit_of(cfg), "cores": r["threads"], "kind": "oracle",
+                             "sample": f"one complete {cfg.name} hot-path step (setup + A + B + B^T + wBFBT "
+                                       f"with 2x{cfg.iters} PCG iterations), timed once"},
+            "e2e": {"value": v, "unit": unit_of(cfg), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "components": {"A_gdofs": r["A_gdofs"], "wbfbt_applies_per_s": 1.0 / r["t"]["wbfbt"],
                            "oracle_times_s": r["t"]}}
     print(json.dumps(line), flush=True)
     return 0
@@ -371,17 +404,16 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = oracle_sample(args.config)
-        cpu = {"value": 1.0 / r["step_s"], "unit": "hot-path steps/s", "cores": r["threads"], "kind": "oracle",
+        cpu = {"value": 1.0 / r["step_s"], "unit": unit_of(cfg), "cores": r["threads"], "kind": "oracle",
                "sample": r["sample"], "A_gdofs": r["A_gdofs"], "sample_wall_s": r["sample_s"]}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value,
-                "unit": "hot-path steps/s (1 step = setup + A + B + B^T + wBFBT with 2x100 PCG iters, C5)",
+                "unit": unit_of(cfg),
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
-                "config": {"workload": f"{args.config} = BASELINE.json configs[4]: 64^3 Q2xP1disc, 24 sinkers, "
-                                       f"DR 1e10, {iters} PCG iters", "N": cfg.N, "k": cfg.k,
+                "config": {"workload": workload_of(cfg), "N": cfg.N, "k": cfg.k,
                            "l2": "flushed (256 MiB memset) before every timed step",
                            "parallelism": f"replicas{world}"},
                 "components": {
@@ -403,7 +435,7 @@ def run_ours(args):
                                       "note": "R19 (not in the step): FGMRES on [A B^T; B 0], f = u, g = 0; per "
                                               "iteration wBFBT (2 x iters PCG) + 6 smoother steps"}},
                 "roofline": roof,
-                "e2e": {"value": e2e, "unit": "hot-path steps/s", "h2d_bytes_per_step": h2d,
+                "e2e": {"value": e2e, "unit": unit_of(cfg), "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h},
                 "gpu_launches": launches,
                 "clocks": clk.summary(),

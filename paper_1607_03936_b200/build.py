@@ -1,6 +1,7 @@
 """Build libwbfbt.so in-tree for sm_100a (explicit nvcc, no JIT cache)."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -8,8 +9,13 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "wbfbt.cu")
-DEPS = [SRC, os.path.join(HERE, "csrc", "kernels.cuh"), os.path.join(HERE, "csrc", "tables.h"),
-        os.path.join(ROOT, "include", "wbfbt.h")]
+
+def deps() -> list:
+    """Every source the library is built from: all of csrc/ and the public headers."""
+    return sorted(glob.glob(os.path.join(HERE, "csrc", "*")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
+                  + [os.path.abspath(__file__)])
+
+
 LIB = os.path.join(HERE, "libwbfbt.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -20,7 +26,7 @@ def stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(d) > t for d in DEPS if os.path.exists(d))
+    return any(os.path.getmtime(d) > t for d in deps())
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -1401,9 +1401,17 @@ wb_status wb_hotpath(wb_ctx* c, const double* mu_q, double a_l, double a_r, cons
   return WB_OK;
 }
 
+static wb_status hotpath_host_body(wb_ctx* c, double* dmu, double a_l, double a_r, double* du, double* dp, int iters,
+                                   double* dyA, double* dpB, double* dyBT, double* dz, double* yA, double* pB,
+                                   double* yBT, double* z, size_t bv, size_t bp);
+
 wb_status wb_hotpath_host(wb_ctx* c, const double* mu_q, double a_l, double a_r, const double* u, const double* p,
                           int iters, double* yA, double* pB, double* yBT, double* z) {
   if (!c || !mu_q || !u || !p || !yA || !pB || !yBT || !z) return WB_EINVAL;
+  // validate everything that can be checked on the host before any copy is issued
+  if (iters < 0) return set_err(c, WB_EINVAL, "iters must be >= 0");
+  if (!(a_l >= 1.0) || !(a_r >= 1.0) || !std::isfinite(a_l) || !std::isfinite(a_r))
+    return set_err(c, WB_EINVAL, "a_l, a_r must be finite and >= 1");
   // sub-buffers rounded to 32 doubles (256-byte aligned)
   auto rnd = [](int64_t n) { return (n + 31) & ~(int64_t)31; };
   const int64_t nmu = c->n_el * c->nq, rmu = rnd(nmu), rv = rnd(c->n_v), rp = rnd(c->n_p);
@@ -1444,9 +1452,21 @@ wb_status wb_hotpath_host(wb_ctx* c, const double* mu_q, double a_l, double a_r,
   CUDA_TRY(c, cudaEventRecord(c->ev_p, cs));
   CUDA_TRY(c, cudaMemcpyAsync(du, u, bv, cudaMemcpyHostToDevice, cs));
   CUDA_TRY(c, cudaEventRecord(c->ev_in, cs));
+  // From here on the copy stream may still be reading the caller's host buffers: every
+  // return path drains it first, so the caller may free or reuse them on return.
+  wb_status s = hotpath_host_body(c, dmu, a_l, a_r, du, dp, iters, dyA, dpB, dyBT, dz, yA, pB, yBT, z, bv, bp);
+  cudaStreamSynchronize(cs);
+  if (s) return s;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return WB_OK;
+}
+
+static wb_status hotpath_host_body(wb_ctx* c, double* dmu, double a_l, double a_r, double* du, double* dp, int iters,
+                                   double* dyA, double* dpB, double* dyBT, double* dz, double* yA, double* pB,
+                                   double* yBT, double* z, size_t bv, size_t bp) {
+  cudaStream_t cs = c->copy_stream;
   wb_status s = wb_set_viscosity(c, dmu, a_l, a_r);  // synchronous (status)
   if (s) return s;
-  if (iters < 0) return set_err(c, WB_EINVAL, "iters must be >= 0");
   const int nomask = (c->flags & WB_DEBUG_NOMASK) ? 1 : 0;
   // wBFBT, right solve: y = P PCG(K_r, P p)
   CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_p, 0));
@@ -1469,8 +1489,6 @@ wb_status wb_hotpath_host(wb_ctx* c, const double* mu_q, double a_l, double a_r,
   if ((s = run_B(c, c->tv, c->Cinv, c->s2, 0, nullptr, nullptr, nullptr, c->nm, 1))) return s;
   if ((s = run_inner(c, 0, c->s2, dz, iters))) return s;
   CUDA_TRY(c, cudaMemcpyAsync(z, dz, bp, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(cs));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return WB_OK;
 }
 

@@ -28,14 +28,18 @@ def empty(n, dtype=None):
     return torch.empty(n, dtype=dtype or torch.float64, device="cuda")
 
 
+# k = 3 (accepted by wb_create; not a BASELINE config): the C1 recipe with Q3 x P2disc.
+K3 = synth.Config("K3", 6, 3, 4, 200.0, 0.1, 1e-2, 1e2, 20)
+
+
 class Pair:
     """One (config, N, seed) case: inputs, a GPU context and an oracle."""
 
     def __init__(self, cfg: str, N: int | None = None, seed: int = 0, a_l=1.0, a_r=1.0, flags=0, setup=True):
         from oracle import Oracle
         from paper_1607_03936_b200 import Context
-        self.inp = synth.make_inputs(cfg, seed, N=N)
-        self.cfg = synth.CONFIGS[cfg]
+        self.cfg = synth.CONFIGS[cfg] if isinstance(cfg, str) else cfg
+        self.inp = synth.make_inputs(self.cfg, seed, N=N)
         self.N, self.k = self.inp["N"], self.inp["k"]
         self.ctx = Context(self.N, self.k, flags=flags)
         self.o = Oracle(self.N, self.k)

@@ -148,17 +148,21 @@ def test_full_size_B_BT(full):
     assert rel_l2(host(full.ctx.apply_BT(dev(p), empty(full.ctx.n_v))), full.o.apply_BT(p)) <= 1e-11
 
 
-def test_full_size_A_sampled(full):
-    u = full.inp["u"]
+def test_full_size_A(full):
+    """The complete A(mu)u vector at the BASELINE size against the oracle (north_star: <= 1e-11),
+    plus the low-viscosity-region check (global l2 is dominated by the mu_max regions)."""
+    u, mu = full.inp["u"], full.inp["mu_q"]
     y = host(full.ctx.apply_A(dev(u), empty(full.ctx.n_v)))
-    rng = np.random.default_rng(3)
-    dofs = rng.choice(full.ctx.n_v, 400, replace=False)
-    ys = full.o.apply_A_sampled(full.inp["mu_q"], u, dofs)
-    scale = np.linalg.norm(y) / np.sqrt(full.ctx.n_v)
-    assert np.max(np.abs(y[dofs] - ys)) <= 1e-11 * max(scale, 1e-300) * 10
-    # relative per sample, where the sample is not tiny
-    big = np.abs(ys) > 1e-3 * scale
-    assert np.max(np.abs(y[dofs][big] - ys[big]) / np.abs(ys[big])) <= 1e-9
+    yo = full.o.apply_A(mu, u)
+    assert rel_l2(y, yo) <= 1e-11
+    o = full.o
+    low_el = mu.reshape(o.n_el, o.n_q).max(axis=1) < 10 * full.cfg.mu_min
+    dm = o.dofmap().reshape(o.n_el, o.n_q)
+    hi = np.zeros(o.n_nodes, bool)
+    hi[np.unique(dm[~low_el])] = True
+    sel = np.tile(~hi, 3) & ~o.boundary_mask().astype(bool)
+    assert sel.sum() > 1000
+    assert rel_l2(y[sel], yo[sel]) <= 1e-11
 
 
 def test_full_size_lumped(full):
@@ -169,11 +173,20 @@ def test_full_size_lumped(full):
     assert full.ctx.query("n_nonpos_Cw") == full.ost["n_nonpos_Cw"] == 0
 
 
-def test_full_size_pcg_prefix(full):
+@pytest.mark.parametrize("iters", [1, 5, 10, 20])
+def test_full_size_pcg_prefix(full, iters):
+    """Prefix parity of the Poisson solve at the BASELINE size (SURVEY 8(c) 12(i')): <= 1e-12."""
     b = full.inp["p"]
     st = full.ost
-    x = host(full.ctx.poisson_pcg(1, dev(b), empty(full.ctx.n_p), 5))
-    assert rel_l2(x, full.o.poisson(st["Dinv"], st["diagKr"], b, 5)) <= 1e-12
+    x = host(full.ctx.poisson_pcg(1, dev(b), empty(full.ctx.n_p), iters))
+    assert rel_l2(x, full.o.poisson(st["Dinv"], st["diagKr"], b, iters)) <= 1e-12
+
+
+def test_full_size_apply_K(full):
+    b = full.inp["p"]
+    for side, X in ((0, full.ost["Cinv"]), (1, full.ost["Dinv"])):
+        q = host(full.ctx.apply_K(side, dev(b), empty(full.ctx.n_p)))
+        assert rel_l2(q, full.o.apply_K(X, b)) <= 1e-11
 
 
 def test_full_size_repeat_bitwise(full):
@@ -189,24 +202,44 @@ def test_full_size_repeat_bitwise(full):
         assert np.array_equal(host(c.poisson_pcg(1, r, empty(c.n_p), 10)), xk)
 
 
-def test_full_size_wbfbt_properties(full):
-    """At full size with the config's PCG count: finite, projected, deterministic,
-    and the Poisson relative residuals agree with the oracle's within 2x
-    (SURVEY 8(c) 12(ii))."""
+def test_full_size_wbfbt(full):
+    """Free-running wBFBT at the BASELINE size with the config's PCG count (C4: 2 x 50,
+    C5: 2 x 100), compared element by element with the oracle:
+    rel l2 <= 1e-8, or -- only where the oracle's own 1-ulp self-discrepancy delta_self
+    exceeds 1e-9, i.e. the fixed-iteration CG itself amplifies rounding that far --
+    <= 100 delta_self, with the Poisson relative residuals agreeing within 2x.  Also
+    finite, projected and bitwise deterministic."""
+    import json
+    import os
     c = full.ctx
     it = full.cfg.iters
-    r = dev(full.inp["p"])
-    z1 = host(c.apply_wbfbt(r, empty(c.n_p), it))
-    z2 = host(c.apply_wbfbt(r, empty(c.n_p), it))
+    r = full.inp["p"]
+    z1 = host(c.apply_wbfbt(dev(r), empty(c.n_p), it))
+    z2 = host(c.apply_wbfbt(dev(r), empty(c.n_p), it))
     assert np.all(np.isfinite(z1)) and np.array_equal(z1, z2)
     assert abs(z1[::full.o.n_m].sum()) <= 1e-10 * np.abs(z1[::full.o.n_m]).sum()
-    st = full.ost
-    b = full.o.project(full.inp["p"])
-    xg = host(c.poisson_pcg(1, dev(b), empty(c.n_p), it))
-    rg = full.o.poisson_relres(st["Dinv"], b, xg)
-    xo = full.o.poisson(st["Dinv"], st["diagKr"], b, it)
-    ro = full.o.poisson_relres(st["Dinv"], b, xo)
-    assert rg <= 2 * ro and ro <= 2 * rg
+    zo = full.o.wbfbt(r, it)
+    err = rel_l2(z1, zo)
+    rec = dict(cfg=full.cfg.name, N=full.N, k=full.k, iters=it, err=err)
+    if err > 1e-8:
+        from tests.test_gpu_parity import self_discrepancy
+        ds = self_discrepancy(full.o, r, it, zo=zo)
+        rec["delta_self"] = ds
+        st = full.ost
+        b = full.o.project(r)
+        xg = host(c.poisson_pcg(1, dev(b), empty(c.n_p), it))
+        rg = full.o.poisson_relres(st["Dinv"], b, xg)
+        ro = full.o.poisson_relres(st["Dinv"], b, full.o.poisson(st["Dinv"], st["diagKr"], b, it))
+        rec.update(relres_gpu=rg, relres_oracle=ro)
+    print("full-size wBFBT parity:", json.dumps(rec))
+    out = os.environ.get("WB_PARITY_LOG")
+    if out:
+        with open(out, "a") as f:
+            f.write(json.dumps(rec) + "\n")
+    if err <= 1e-8:
+        return
+    assert rec["delta_self"] > 1e-9 and err <= 100 * rec["delta_self"], rec
+    assert rec["relres_gpu"] <= 2 * rec["relres_oracle"] and rec["relres_oracle"] <= 2 * rec["relres_gpu"], rec
 
 
 @pytest.mark.parametrize("cfg,N", [("C2", 6), ("C1", None)])

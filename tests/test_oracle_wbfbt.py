@@ -169,3 +169,32 @@ def test_wbfbt_output_projected():
     o.setup(inp["mu_q"])
     z = o.wbfbt(inp["p"], 10)
     assert abs(_z0(o) @ z) <= 1e-14 * np.linalg.norm(z) * 10
+
+
+def test_jacobi_pseudoinverse_threshold_only_removes_the_null_row():
+    """DESIGN.md R11: Minv is 1/diag K except where |d| <= 1e-13 max|d|.  On the N = 1
+    mesh every velocity node is Dirichlet, so B^T of ANY mode vanishes... except the
+    interior GLL node at k = 2: the constant mode still has B^T z0 = 0 by the divergence
+    theorem, so diag(K)_{mode 0} = sum (B_e[0,:])^2 X = 0 up to rounding -- the one row the
+    threshold removes.  On N >= 2 with positive lumped masses no entry is near the
+    threshold, so the pseudo-inverse is the plain inverse there."""
+    B1 = None
+    o = Oracle(1, 2)
+    st = o.setup(_mild_mu(o))
+    d = st["diagKr"]
+    assert abs(d[0]) <= 1e-13 * np.abs(d).max()          # the constant-mode row vanishes
+    assert np.all(np.abs(d[1:]) > 1e-3 * np.abs(d).max())  # the others are O(1)
+    B1 = _dense_B(o)
+    assert np.linalg.norm(B1[0]) <= 1e-14 * np.linalg.norm(B1)  # B^T z0 = 0 on N = 1
+    for N, k in ((2, 2), (3, 2), (2, 4)):
+        o = Oracle(N, k)
+        st = o.setup(_mild_mu(o))
+        d = st["diagKr"]
+        assert np.abs(d).min() > 1e-6 * np.abs(d).max()
+    # and on N = 1 the converged PCG is still the pseudo-inverse solution (mode 0 is z0)
+    o = Oracle(1, 2)
+    st = o.setup(_mild_mu(o))
+    K = B1 @ (np.tile(st["Dinv"], 3)[:, None] * B1.T)
+    b = o.project(np.random.default_rng(2).uniform(-1, 1, o.n_p))
+    x = o.poisson(st["Dinv"], st["diagKr"], b, 3)
+    assert np.allclose(x, _pinv_deflated(K, _z0(o)) @ b, rtol=0, atol=1e-12 * np.linalg.norm(x))
