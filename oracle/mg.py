@@ -1,0 +1,213 @@
+"""Oracle of the geometric multigrid V-cycle for the pressure Poisson operators K_w
+(second half; PAPER.md:2468-2546 Sec. "Parallel hybrid
+spectral-geometric-algebraic multigrid (HMG) for wBFBT").
+
+TEST INFRASTRUCTURE ONLY (imported by tests/ and bench.py's reference leg; the
+product package never imports it).  Plain numpy on top of the C oracle's
+operators (oracle.Oracle: K apply, Jacobi diagonal, Chebyshev smoother, PCG,
+power iteration), each step following DESIGN.md reading R20:
+
+  * levels: N_0 = N, N_{l+1} = N_l / 2 while N_l is even and > 1 (uniform
+    element bisection = the paper's geometric coarsening);
+  * operators by re-discretisation on every level:
+    K_l = B_l X_l B_l^T with the level's own B (Q2 x P1disc on the N_l mesh) and
+    X_l = mask / C_l;
+  * the coarse weights C_l: the weight DENSITY w(g) = C_{l-1}[g] / M_{l-1}[g]
+    (M = the unweighted lumped velocity mass of that level) injected at the
+    coincident node, lumped with the coarse mass: C_l[G] = M_l[G] w(iota(G));
+  * transfers: P_l = the exact embedding of the coarse P1disc space in the fine
+    one (each coarse polynomial restricted to its 8 children), evaluated here by
+    L2 projection with Gauss quadrature; restriction = P_l^T (the L2 adjoint
+    for dual vectors, "adjoint ... with respect to the L2
+    inner products");
+  * smoother: nu steps of Chebyshev-accelerated point-Jacobi (PAPER.md:2531-2546:
+    three pre- and post-smoothing steps), interval [0.1, 1.1] lambda_l, lambda_l
+    the power-iteration estimate of the largest eigenvalue of Minv_l K_l from the
+    splitmix64 start vector (the same counter-based generator on both sides);
+  * coarsest level: Jacobi-PCG (O9) with min(n_p, 256) iterations (the paper
+    uses AMG + a direct solve at 64 elements; reading R20);
+  * V(b): x = S(b); x += P V(P^T (b - K x)); x += S(b - K x);
+  * MG-PCG: the O9 recurrence with M^-1 := V, fixed iteration count, input and
+    output projected off the constant pressure (R10).
+"""
+from __future__ import annotations
+
+import numpy as np
+from numpy.polynomial import legendre as npleg
+
+from . import Oracle
+
+NU = 3            # pre- and post-smoothing steps
+EIG_ITERS = 20    # power iterations per level
+CHEB_LO, CHEB_HI = 0.1, 1.1
+COARSE_CAP = 256  # iterations of the coarsest-level PCG
+
+
+def splitmix_vector(n: int, seed: int = 0x5EED) -> np.ndarray:
+    """v_i = uniform in [-1, 1) from the i-th splitmix64 output of state `seed`: the power-iteration start
+    vector, integer arithmetic only, so both sides draw identical doubles."""
+    M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+    with np.errstate(over="ignore"):
+        # state_i = seed + (i + 1) * golden (the standard splitmix64 stream from state `seed`)
+        z = np.uint64(seed) + (np.arange(n, dtype=np.uint64) + np.uint64(1)) * np.uint64(0x9E3779B97F4A7C15) & M64
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    u = (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+    return 2.0 * u - 1.0
+
+
+def levels_of(N: int) -> list:
+    Ns = [N]
+    while Ns[-1] % 2 == 0 and Ns[-1] > 1:
+        Ns.append(Ns[-1] // 2)
+    return Ns
+
+
+def prolongation_tables(o: Oracle) -> np.ndarray:
+    """T[s][mf][mc], s = sx + 2 sy + 4 sz: fine-child coefficient of mode mf from coarse
+    mode mc, by L2 projection on the child (orthonormal modes on the reference cube):
+    T = int_{[-1,1]^3} q_mc(xi_c(xi)) q_mf(xi) dxi with xi_c = (xi + 2 s - 1) / 2."""
+    t = o.tables()
+    xg, wg, modes = t["xg"], t["wg"], t["modes"]
+    nm = o.n_m
+
+    def lhat(m, x):
+        c = np.zeros(m + 1)
+        c[m] = 1.0
+        return np.sqrt((2 * m + 1) / 2.0) * npleg.legval(x, c)
+
+    T = np.zeros((8, nm, nm))
+    for s in range(8):
+        sh = np.array([s & 1, (s >> 1) & 1, (s >> 2) & 1]) * 2 - 1
+        for mf in range(nm):
+            for mc in range(nm):
+                acc = 0.0
+                for iz in range(len(xg)):
+                    for iy in range(len(xg)):
+                        for ix in range(len(xg)):
+                            xi = np.array([xg[ix], xg[iy], xg[iz]])
+                            xc = (xi + sh) / 2.0
+                            qc = np.prod([lhat(modes[mc][d], xc[d]) for d in range(3)])
+                            qf = np.prod([lhat(modes[mf][d], xi[d]) for d in range(3)])
+                            acc += wg[ix] * wg[iy] * wg[iz] * qc * qf
+                T[s, mf, mc] = acc
+    return T
+
+
+def child_index(Nc: int):
+    """(coarse element, child position s) -> fine element, element-major e = ex + N(ey + N ez)."""
+    Nf = 2 * Nc
+    ec = np.arange(Nc ** 3)
+    cx, cy, cz = ec % Nc, (ec // Nc) % Nc, ec // (Nc * Nc)
+    out = np.zeros((Nc ** 3, 8), dtype=np.int64)
+    for s in range(8):
+        fx, fy, fz = 2 * cx + (s & 1), 2 * cy + ((s >> 1) & 1), 2 * cz + ((s >> 2) & 1)
+        out[:, s] = fx + Nf * (fy + Nf * fz)
+    return out
+
+
+def prolong(T, xc: np.ndarray, Nc: int, nm: int) -> np.ndarray:
+    """x_f = P x_c (coarse element-major -> fine element-major)."""
+    ch = child_index(Nc)
+    xf = np.zeros(8 * Nc ** 3 * nm)
+    X = xc.reshape(-1, nm)
+    for s in range(8):
+        xf.reshape(-1, nm)[ch[:, s]] = X @ T[s].T
+    return xf
+
+
+def restrict(T, rf: np.ndarray, Nc: int, nm: int) -> np.ndarray:
+    """r_c = P^T r_f; children summed in ascending s."""
+    ch = child_index(Nc)
+    R = rf.reshape(-1, nm)
+    rc = np.zeros((Nc ** 3, nm))
+    for s in range(8):
+        rc += R[ch[:, s]] @ T[s]
+    return rc.reshape(-1)
+
+
+def inject_weights(Cf: np.ndarray, Mf: np.ndarray, Mc: np.ndarray, Nc: int, k: int = 2) -> np.ndarray:
+    """C_c[G] = M_c[G] * C_f[iota(G)] / M_f[iota(G)], iota(G) = the fine node at the coarse
+    node's position (coarse GLL grid index i -> fine index 2 i per axis, k = 2)."""
+    nc, nf = k * Nc + 1, 2 * k * Nc + 1
+    g = np.arange(nc)
+    idx = (2 * g[None, None, :] + nf * (2 * g[None, :, None] + nf * 2 * g[:, None, None])).ravel()
+    return Mc * (Cf[idx] / Mf[idx])
+
+
+class MGLevel:
+    def __init__(self, N, k, C):
+        self.o = Oracle(N, k)
+        self.N, self.C = N, C
+        mask = self.o.boundary_mask()[: self.o.n_nodes].astype(bool)
+        self.X = np.where(mask, 0.0, 1.0 / np.where(C != 0.0, C, 1.0))
+        self.diagK = self.o.jacobi_diag(self.X)
+        self.n_nonpos = int(np.sum((C <= 0.0) & ~mask))
+        self.lam = self.o.poisson_eigmax(self.X, self.diagK, splitmix_vector(self.o.n_p), EIG_ITERS)
+
+    def K(self, p):
+        return self.o.apply_K(self.X, p)
+
+    def smooth(self, b):
+        return self.o.poisson_cheb(self.X, self.diagK, b, NU, CHEB_LO * self.lam, CHEB_HI * self.lam)
+
+
+class MG:
+    """The V-cycle hierarchy of one side's K_w, built from that side's lumped mass C_w."""
+
+    def __init__(self, N: int, Cw: np.ndarray, k: int = 2):
+        assert k == 2, "pressure multigrid is built for Q2 x P1disc (R20)"
+        self.Ns = levels_of(N)
+        self.levels = []
+        C = np.asarray(Cw, dtype=np.float64)
+        M_prev = None
+        for li, Nl in enumerate(self.Ns):
+            o = Oracle(Nl, k)
+            M = o.lumped(np.ones(o.n_el * o.n_q))["Cw"]  # unweighted lumped velocity mass
+            if li > 0:
+                C = inject_weights(C, M_prev, M, Nl, k)
+            self.levels.append(MGLevel(Nl, k, C))
+            M_prev = M
+        self.T = prolongation_tables(self.levels[0].o)
+        self.nm = self.levels[0].o.n_m
+
+    def coarse_iters(self) -> int:
+        return min(self.levels[-1].o.n_p, COARSE_CAP)
+
+    def vcycle(self, b: np.ndarray, l: int = 0) -> np.ndarray:
+        L = self.levels[l]
+        if l == len(self.levels) - 1:
+            return L.o.poisson(L.X, L.diagK, b, self.coarse_iters())
+        x = L.smooth(b)
+        r = b - L.K(x)
+        Nc = self.Ns[l + 1]
+        xc = self.vcycle(restrict(self.T, r, Nc, self.nm), l + 1)
+        x = x + prolong(self.T, xc, Nc, self.nm)
+        r = b - L.K(x)
+        return x + L.smooth(r)
+
+    def pcg(self, b: np.ndarray, iters: int) -> np.ndarray:
+        """MG-preconditioned CG (O9 recurrence, M^-1 = V), exactly `iters` iterations."""
+        L0 = self.levels[0]
+        o = L0.o
+        r = o.project(b)
+        x = np.zeros_like(r)
+        z = self.vcycle(r)
+        p = z.copy()
+        rz = float(r @ z)
+        for _ in range(iters):
+            if rz == 0.0:
+                break
+            q = L0.K(p)
+            pq = float(p @ q)
+            if pq == 0.0:
+                break
+            a = rz / pq
+            x = x + a * p
+            r = r - a * q
+            z = self.vcycle(r)
+            rz1 = float(r @ z)
+            p = z + (rz1 / rz) * p
+            rz = rz1
+        return o.project(x)

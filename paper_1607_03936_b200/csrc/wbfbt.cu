@@ -100,6 +100,12 @@ struct wb_ctx {
   // measured and gave no gain)
   double* slab = nullptr;
   CUtensorMap tm_pp, tm_pp1, tm_pz, tm_pr, tm_mL, tm_mR;
+  // node-owner z-march Poisson kernel (k2_zm.cuh): tensor maps with its per-layer box,
+  // X prescaled on the padded nodal grid, option "k_zm" (default on), z-chunk length
+  bool zm_ok = false;
+  int use_zm = 0, zm_zc = 4;
+  double *XzL = nullptr, *XzR = nullptr;
+  CUtensorMap tz_pp, tz_pp1, tz_pz;
   int kz = 0;  // TMA Poisson kernel: 1 = z = Minv r stored by the PCG update and loaded as one box; 0 = r + Minv boxes (default: faster with the y-fastest storage)
   int k_dbg = 0;  // timing probe bits for the fused K kernel (results invalid when nonzero)
   // profiling: CUDA-event pairs around every Poisson-operator launch (direct launches)
@@ -298,10 +304,34 @@ const CUtensorMap* tmap_of(wb_ctx* c, const double* p) {
 // the k = 2 Poisson operator runs as the TMA kernel (k_K2_tma); the PCG init/update
 // kernels then also store z = Minv r, which it reads instead of r and Minv
 bool tma_active(const wb_ctx* c) { return c->k == 2 && c->tma_ok && c->use_tma && c->n_el >= 148 * 256 * 2; }
-double* z_out(const wb_ctx* c) { return tma_active(c) && c->kz ? c->pz : nullptr; }
+// the node-owner z-march kernel (k2_zm.cuh) replaces it where set up; it always reads z
+bool zm_active(const wb_ctx* c) { return tma_active(c) && c->zm_ok && c->use_zm; }
+double* z_out(const wb_ctx* c) { return tma_active(c) && (c->kz || zm_active(c)) ? c->pz : nullptr; }
+const CUtensorMap* zmap_of(wb_ctx* c, const double* p) {
+  if (p == c->pp) return &c->tz_pp;
+  if (p == c->pp1) return &c->tz_pp1;
+  if (p == c->pz) return &c->tz_pz;
+  return nullptr;
+}
+constexpr int ZM_TY = 16, ZM_TX = 8, ZM_MINB = 2;
 
 wb_status run_k2f(wb_ctx* c, const double* pold, double* pnew, const double* r, const double* Minv, const double* X,
                   double* q, int mode, PcgArgs a, int* npq) {
+  if (zm_active(c)) {
+    const CUtensorMap *tp = zmap_of(c, pold), *tz = zmap_of(c, c->pz);
+    const double* xz = X == c->Cinv ? c->XzL : (X == c->Dinv ? c->XzR : nullptr);
+    if (tp && tz && xz && (mode == 2 || r == c->pr)) {
+      using K = ZMK<ZM_TY, ZM_TX>;
+      const int N = c->N, zc = c->zm_zc;
+      const int grid = ((N + ZM_TY - 1) / ZM_TY) * ((N + ZM_TX - 1) / ZM_TX) * ((N + zc - 1) / zc);
+      k_K2_zm<ZM_TY, ZM_TX, ZM_MINB><<<grid, K::NTH, K::SMEM, c->stream>>>(
+          *tp, *tz, xz, pnew, q, N, zc, mode | c->k_dbg, a.it, a.ctl, c->rzp, c->red_blocks, rz_hist(c), pq_hist(c),
+          c->stop, c->pqp, c->pl);
+      LAUNCH_CHECK(c);
+      *npq = grid;
+      return WB_OK;
+    }
+  }
   if (tma_active(c)) {
     using KT = FKT<TMA_TX, TMA_TY, TMA_TZ>;
     const CUtensorMap *tp = tmap_of(c, pold), *tz = tmap_of(c, c->kz ? c->pz : c->pr), *tm = tmap_of(c, Minv);
@@ -357,6 +387,31 @@ bool make_tm_vec(CUtensorMap* tm, const double* base, int N, int nm) {
   return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// the same storage, box = one layer of the z-march kernel's column tile + halo, all modes
+bool make_tm_zm(CUtensorMap* tm, const double* base, int N, int nm) {
+  using K = ZMK<ZM_TY, ZM_TX>;
+  const cuuint64_t ny = (cuuint64_t)N + 2;
+  const cuuint64_t dims[4] = {ny, (cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)nm};
+  const cuuint64_t strides[3] = {ny * 8, ny * N * 8, ny * N * N * 8};
+  const cuuint32_t box[4] = {(cuuint32_t)K::HY, 1u, (cuuint32_t)K::HX, (cuuint32_t)nm};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+bool setup_zm(wb_ctx* c) {
+  if (!c->ylay || c->nm != 4) return false;
+  const int64_t R = 2 * (int64_t)c->N + 2;
+  const size_t bx = sizeof(double) * (size_t)(R * R * R);
+  if (cudaMalloc(&c->XzL, bx) != cudaSuccess || cudaMalloc(&c->XzR, bx) != cudaSuccess ||
+      cudaFuncSetAttribute(k_K2_zm<ZM_TY, ZM_TX, ZM_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ZMK<ZM_TY, ZM_TX>::SMEM) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return make_tm_zm(&c->tz_pp, c->pp, c->N, c->nm) && make_tm_zm(&c->tz_pp1, c->pp1, c->N, c->nm) &&
+         make_tm_zm(&c->tz_pz, c->pz, c->N, c->nm);
 }
 bool setup_tma(wb_ctx* c) {
   if (!c->ylay) return false;
@@ -953,6 +1008,9 @@ void free_all(wb_ctx* c) {
   if (c->counter) cudaFree(c->counter);
   if (c->stop) cudaFree(c->stop);
   if (c->icount) cudaFree(c->icount);
+  if (c->XzL) cudaFree(c->XzL);
+  if (c->XzR) cudaFree(c->XzR);
+  c->XzL = c->XzR = nullptr;
   if (c->XpL) cudaFree(c->XpL);
   if (c->XpR) cudaFree(c->XpR);
   c->XpL = c->XpR = nullptr;
@@ -1111,6 +1169,7 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
     return WB_ECUDA;
   }
   c->tma_ok = setup_tma(c);  // the pointer kernel serves contexts without the y-fastest storage
+  c->zm_ok = c->tma_ok && setup_zm(c);
   if (c->ylay && !c->tma_ok) {
     free_all(c);
     delete c;
@@ -1223,6 +1282,13 @@ static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
     using F = FK2<TMA_TX, TMA_TY, TMA_TZ>;
     const int nt = ((c->N + TMA_TX - 1) / TMA_TX) * ((c->N + TMA_TY - 1) / TMA_TY) * ((c->N + TMA_TZ - 1) / TMA_TZ);
     k_x_tiles<TMA_TX, TMA_TY, TMA_TZ><<<nt, F::MY * F::MZ, 0, c->stream>>>(c->Cinv, c->Dinv, c->XpL, c->XpR, c->N);
+    LAUNCH_CHECK(c);
+  }
+  if (c->zm_ok) {  // X = sB^2 C_w^-1, sB^2 D_w^-1 on the padded nodal grid of the z-march kernel
+    const double s2 = c->sB * c->sB;
+    k_xz_build<<<4 * c->nsm, 256, 0, c->stream>>>(c->Cinv, c->XzL, c->N, s2);
+    LAUNCH_CHECK(c);
+    k_xz_build<<<4 * c->nsm, 256, 0, c->stream>>>(c->Dinv, c->XzR, c->N, s2);
     LAUNCH_CHECK(c);
   }
   if constexpr (K == 2)
@@ -1616,6 +1682,10 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
     *value = c->weights;
   } else if (!strcmp(key, "inner")) {  // 1: wBFBT's inner solves are Chebyshev-Jacobi (wb_set_inner_cheb)
     *value = c->inner;
+  } else if (!strcmp(key, "k_zm")) {  // 1: the Poisson operator runs as the node-owner z-march kernel
+    *value = zm_active(c) ? 1.0 : 0.0;
+  } else if (!strcmp(key, "zm_zc")) {
+    *value = (double)c->zm_zc;
   } else if (!strcmp(key, "k_ws")) {  // 1: ... as the warp-specialised TMA kernel (k_K2_ws)
     *value = (tma_active(c) && c->k_ws) ? 1.0 : 0.0;
   } else if (!strcmp(key, "occ_a2")) {
@@ -1703,6 +1773,15 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
   } else if (!strcmp(key, "k_ws")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k_ws must be 0 or 1");
     c->k_ws = (int)value;
+    clear_graphs(c);
+  } else if (!strcmp(key, "k_zm")) {  // 1: the node-owner z-march Poisson kernel where set up
+    if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k_zm must be 0 or 1");
+    c->use_zm = (int)value;
+    clear_graphs(c);
+  } else if (!strcmp(key, "zm_zc")) {  // element layers per CTA of the z-march kernel
+    if (!(value >= 1.0 && value <= 64.0) || value != (double)(int)value)
+      return set_err(c, WB_EINVAL, "zm_zc must be an integer in [1, 64]");
+    c->zm_zc = (int)value;
     clear_graphs(c);
   } else if (!strcmp(key, "tma")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "tma must be 0 or 1");

@@ -1,0 +1,169 @@
+"""Pins of the pressure-multigrid oracle (oracle/mg.py; R20).
+
+* splitmix64 start vector: the generator's published first output from state 0;
+* prolongation = exact embedding: a coarse P1disc field evaluated at points of the fine
+  children equals the prolongated fine field there; P^T P = 8 I (orthonormal reference
+  bases, child volume 1/8);
+* restriction = L2 adjoint on dual vectors: (P^T r_f)_i = int f q_i^c for r_f[j] = int f q_j^f;
+* coarse weights: constant density injects exactly (C_l = c M_l), and stay positive;
+* MG-PCG converged equals the pseudo-inverse solution K^+ b (dense, constant deflated);
+* the V-cycle is a symmetric operator (symmetric smoother, converged coarse solve);
+* mesh independence ("iteration numbers are independent of mesh
+  size"): iterations to a 1e-6 residual reduction at N = 4, 8, 16 differ by <= 2, while
+  Jacobi-PCG's grow.
+"""
+from math import sqrt
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import Oracle
+from oracle import mg as omg
+from tests.test_oracle_B import _dense_B
+
+
+def test_splitmix_published_value():
+    M64 = (1 << 64) - 1
+    # first splitmix64 output from state 0 is 0xE220A8397B1DCDAF (Steele, Lea & Flood 2014)
+    v = omg.splitmix_vector(2, seed=0)
+    assert v[0] == 2.0 * ((0xE220A8397B1DCDAF >> 11) / 2.0 ** 53) - 1.0
+    assert np.all(np.abs(omg.splitmix_vector(1000)) <= 1.0)
+    del M64
+
+
+def _eval_p1(coef, xi):
+    """P1 field of one element (orthonormal modes 1, x, y, z on the reference cube) at xi."""
+    l0 = 1 / sqrt(2)
+    l1 = lambda t: sqrt(1.5) * t  # noqa: E731
+    return l0 ** 3 * coef[0] + l1(xi[0]) * l0 ** 2 * coef[1] + l1(xi[1]) * l0 ** 2 * coef[2] + l1(xi[2]) * l0 ** 2 * coef[3]
+
+
+def test_prolongation_is_exact_embedding():
+    o = Oracle(2, 2)
+    T = omg.prolongation_tables(o)
+    rng = np.random.default_rng(0)
+    Nc = 2
+    xc = rng.uniform(-1, 1, 4 * Nc ** 3)
+    xf = omg.prolong(T, xc, Nc, 4)
+    ch = omg.child_index(Nc)
+    for ec in range(Nc ** 3):
+        for s in range(8):
+            sh = np.array([s & 1, (s >> 1) & 1, (s >> 2) & 1]) * 2 - 1
+            for xi in rng.uniform(-1, 1, (3, 3)):
+                vf = _eval_p1(xf[4 * ch[ec, s]: 4 * ch[ec, s] + 4], xi)
+                vc = _eval_p1(xc[4 * ec: 4 * ec + 4], (xi + sh) / 2)
+                assert vf == pytest.approx(vc, abs=1e-14)
+    # P^T P = 8 I
+    PtP = sum(T[s].T @ T[s] for s in range(8))
+    assert np.allclose(PtP, 8 * np.eye(4), atol=1e-14)
+
+
+def test_restriction_is_l2_adjoint():
+    """r_f[j] = int_{fine e} f q_j for f = a coarse-elementwise P1 function g: then
+    P^T r_f = int_{coarse e} g q_i^c = (h_c/2)^3 g_c (orthonormal reference modes)."""
+    o = Oracle(2, 2)
+    T = omg.prolongation_tables(o)
+    Nc = 1
+    g = np.array([0.3, -1.2, 0.7, 2.0])
+    hf = 1.0 / (2 * Nc)
+    gf = omg.prolong(T, g, Nc, 4)
+    rf = (hf / 2) ** 3 * gf  # int_{fine e} g q_j = (h_f/2)^3 g_f[j] (g is P1 on the child)
+    rc = omg.restrict(T, rf, Nc, 4)
+    assert np.allclose(rc, (2 * hf / 2) ** 3 * g, atol=1e-15)
+
+
+def test_coarse_weights_inject_density():
+    N = 8
+    o = Oracle(N, 2)
+    M = o.lumped(np.ones(o.n_el * o.n_q))["Cw"]
+    m = omg.MG(N, 3.5 * M)
+    for L in m.levels:
+        Ml = L.o.lumped(np.ones(L.o.n_el * L.o.n_q))["Cw"]
+        assert np.allclose(L.C, 3.5 * Ml, rtol=1e-14)
+    inp = synth.make_inputs("C2", 0, N=16)
+    o = Oracle(16, 2)
+    st = o.setup(inp["mu_q"])
+    m = omg.MG(16, st["Cw"])
+    assert [L.N for L in m.levels] == [16, 8, 4, 2, 1]
+    assert all(L.n_nonpos == 0 for L in m.levels)
+
+
+def _pinv_deflated(K, nm=4):
+    n = K.shape[0]
+    z = np.zeros(n)
+    z[::nm] = 1.0
+    z /= np.linalg.norm(z)
+    Pm = np.eye(n) - np.outer(z, z)
+    ev, V = np.linalg.eigh(Pm @ K @ Pm)
+    keep = np.abs(ev) > 1e-10 * np.abs(ev).max()
+    return (V[:, keep] / ev[keep]) @ V[:, keep].T
+
+
+def _mild(o, seed=0):
+    return np.random.default_rng(seed).uniform(0.5, 2.0, o.n_el * o.n_q)
+
+
+def test_mgpcg_converges_to_pseudoinverse():
+    N = 4
+    o = Oracle(N, 2)
+    st = o.setup(_mild(o))
+    m = omg.MG(N, st["Dw"])
+    B = _dense_B(o)
+    K = B @ (np.tile(m.levels[0].X, 3)[:, None] * B.T)
+    b = o.project(np.random.default_rng(1).uniform(-1, 1, o.n_p))
+    x = m.pcg(b, 25)
+    xe = _pinv_deflated(K) @ b
+    assert np.linalg.norm(x - xe) <= 1e-9 * np.linalg.norm(xe)
+
+
+def test_vcycle_symmetric():
+    N = 4
+    o = Oracle(N, 2)
+    st = o.setup(_mild(o, 3))
+    m = omg.MG(N, st["Dw"])
+    rng = np.random.default_rng(4)
+    a, b = (o.project(rng.uniform(-1, 1, o.n_p)) for _ in range(2))
+    lhs, rhs = m.vcycle(a) @ b, a @ m.vcycle(b)
+    assert abs(lhs - rhs) <= 1e-10 * abs(lhs)
+
+
+def _iters_to(o, K_apply, prec, b, tol=1e-6, cap=400):
+    x = np.zeros_like(b)
+    r = o.project(b)
+    z = prec(r)
+    p = z.copy()
+    rz = r @ z
+    r0 = np.linalg.norm(r)
+    for it in range(1, cap + 1):
+        q = K_apply(p)
+        a = rz / (p @ q)
+        x += a * p
+        r -= a * q
+        if np.linalg.norm(r) < tol * r0:
+            return it
+        z = prec(r)
+        rz1 = r @ z
+        p = z + rz1 / rz * p
+        rz = rz1
+    return cap
+
+
+def test_mesh_independent_iterations():
+    """multigrid iteration numbers are independent of the mesh size.
+    Two smooth wide sinkers (delta = 20, omega = 0.3, viscosity ratio 10), N = 4, 8, 16."""
+    its, its_j = [], []
+    cen = np.array([[0.3, 0.4, 0.5], [0.7, 0.6, 0.4]])
+    for N in (4, 8, 16):
+        o = Oracle(N, 2)
+        mu = synth.viscosity_at_quadrature(N, 2, cen, 20.0, 0.3, 1.0, 10.0)
+        st = o.setup(mu)
+        assert st["n_nonpos_Dw"] == 0
+        m = omg.MG(N, st["Dw"])
+        L0 = m.levels[0]
+        b = o.project(np.random.default_rng(5).uniform(-1, 1, o.n_p))
+        its.append(_iters_to(o, L0.K, m.vcycle, b))
+        minv = np.where(np.abs(L0.diagK) > 1e-13 * np.abs(L0.diagK).max(), 1 / L0.diagK, 0.0)
+        its_j.append(_iters_to(o, L0.K, lambda r: minv * r, b))
+    assert max(its) - min(its) <= 2, its
+    assert its_j[-1] > 2 * its[-1] and its_j[-1] > its_j[0], (its, its_j)
