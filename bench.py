@@ -380,7 +380,9 @@ def run_ours(args):
             "algorithmic_bytes_per_launch": bytes_K,
             "algorithmic_bytes_def": ("8*(4*n_p + n_nodes): p_old, z in; p_new, q out; X in" if zbox else
                                       "8*(5*n_p + n_nodes): p_old, r, Minv in; p_new, q out; X in"), "launch_ms": k_avg, "launches_per_step": k_n / prof_steps,
-            "share_of_step": k_ms / prof_steps / prof_step_ms, "profiled_step_ms": prof_step_ms}
+            "share_of_step": k_ms / prof_steps / ms_per_step, "profiled_step_ms": prof_step_ms,
+            "timing": "CUDA-event record nodes around every launch inside the captured PCG-loop graphs "
+                      "(graph launch gaps as in the timed step)"}
     tKw = k_avg
 
     # ---- end to end through the host entry (pinned buffers)

@@ -140,6 +140,37 @@ wb_status wb_poisson_eigmax(wb_ctx* ctx, int side, const double* v0, int iters, 
  * back to PCG (the default).  WB_EINVAL unless each 0 < lmin < lmax < inf.  wb_query
  * "inner" reads the choice. */
 wb_status wb_set_inner_cheb(wb_ctx* ctx, double lmin_l, double lmax_l, double lmin_r, double lmax_r);
+
+/* ---- Geometric pressure multigrid for K_w (second half; PAPER.md:2468-2546,
+ * Sec. "Parallel hybrid spectral-geometric-algebraic multigrid (HMG) for wBFBT"; reading R20
+ * of DESIGN.md).  k = 2 only.  Levels N, N/2, ... while N is even and > 1 (uniform element
+ * bisection); on every level the operator is re-discretised
+ * as K_l = B_l X_l B_l^T with X_l = mask / C_l, the coarse lumped masses
+ * C_l[G] = C_{l-1}[iota(G)] M_l[G] / M_{l-1}[iota(G)] (the weight density injected at the
+ * coincident node; M = unweighted lumped mass); transfers are the exact P1disc embedding and
+ * its transpose; smoother: nu steps of Chebyshev-accelerated Jacobi on
+ * [0.1, 1.1] x a 20-step power-iteration estimate (splitmix64 start vector); coarsest level:
+ * Jacobi-PCG with min(n_p, 256) iterations. */
+/* Builds the hierarchy of both sides from the current C_w, D_w (after wb_set_viscosity; a
+ * later wb_set_viscosity discards it).  nu in [1, 16] (the paper: 3).  Allocates one internal
+ * context per coarse level and synchronises the stream.  WB_EINVAL for k != 2 or nu out of
+ * range, WB_ESTATE before wb_set_viscosity, WB_ENOMEM. */
+wb_status wb_setup_mg(wb_ctx* ctx, int nu);
+/* x = V(b), one V-cycle on K_side (side 0 = l, 1 = r).  b, x: device, element-major n_p,
+ * caller-owned; b should be projected (R10).  Asynchronous.  WB_ESTATE without a hierarchy,
+ * WB_EINVAL, WB_EALIAS. */
+wb_status wb_mg_vcycle(wb_ctx* ctx, int side, const double* b, double* x);
+/* x = P MGPCG(K_side, P b): the O9 recurrence with M^-1 = one V-cycle, exactly `iters`
+ * iterations (scalars on the device), input and output projected (R10).  Errors as
+ * wb_mg_vcycle; iters >= 0. */
+wb_status wb_poisson_mgcg(wb_ctx* ctx, int side, const double* b, double* x, int iters);
+/* From now on wBFBT solves its two Poisson problems by wb_poisson_mgcg with `iters`
+ * iterations (its own `iters` argument is then unused); 0: back to the previous inner solve.
+ * WB_ESTATE without a hierarchy (iters > 0). */
+wb_status wb_set_inner_mg(wb_ctx* ctx, int iters);
+/* The level-`level` lumped masses C_l, D_l (device, n_nodes of that level's (2 N_l + 1)^3
+ * grid; either may be NULL).  Synchronises.  WB_EINVAL for a bad level. */
+wb_status wb_mg_get_lumped(wb_ctx* ctx, int level, double* Cw, double* Dw);
 /* diag(M A M) (reading R18): dA[c * n_nodes + g] = sum over the elements holding node g of
  * the element matrix diagonal, sum_q mu w_q detJ (2/h)^2 (|grad_xi phi_a|^2 + (d_xi_c phi_a)^2);
  * Dirichlet dofs 0.  dA: device, n_v (SoA).  WB_EINVAL for a null pointer; WB_ESTATE

@@ -88,6 +88,7 @@ def lib():
             L.or_poisson_eigmax.argtypes = [C.c_void_p, _D, _D, _D, C.c_int]
             L.or_poisson_eigmax.restype = C.c_double
             L.or_num_threads.restype = C.c_int
+            L.or_set_order.argtypes = [C.c_int]
             _lib = L
     return _lib
 
@@ -355,6 +356,12 @@ class Oracle:
                              _p(s["diagKr"]), _p(r), _p(z), int(iters), float(lmin_l), float(lmax_l),
                              float(lmin_r), float(lmax_r))
         return z
+
+    @staticmethod
+    def set_order(reverse: bool) -> None:
+        """Summation order of element scatter-adds and dot products (process-wide): reversed
+        only to measure the self-discrepancy delta_self."""
+        lib().or_set_order(int(bool(reverse)))
 
     @staticmethod
     def num_threads() -> int:

@@ -211,3 +211,15 @@ class MG:
             p = z + (rz1 / rz) * p
             rz = rz1
         return o.project(x)
+
+
+def wbfbt_mg(o: Oracle, mu_q, state: dict, mg_l: MG, mg_r: MG, r: np.ndarray, iters: int) -> np.ndarray:
+    """eq:wbfbt in the O10 order with both Poisson inverses replaced by
+    MG-PCG (`iters` iterations): y = P MGPCG(K_r, P r); v = Dinv o B^T y; v = A v;
+    v = Cinv o v; s = P B v; z = P MGPCG(K_l, s)."""
+    y = mg_r.pcg(r, iters)
+    v = o.apply_BT(y) * np.tile(state["Dinv"], 3)
+    v = o.apply_A(mu_q, v)
+    v = v * np.tile(state["Cinv"], 3)
+    s = o.project(o.apply_B(v))
+    return mg_l.pcg(s, iters)

@@ -267,6 +267,14 @@ void or_boundary_mask(const or_ctx* c, uint8_t* mask) { /* 1 = boundary (elimina
 }
 
 /* Gather element-local velocity (c, a), Dirichlet entries zeroed unless nomask. */
+/* Summation-order switch for the self-discrepancy delta_self (SURVEY.md 8(c) 12(ii):
+ * "the oracle vs itself with reversed element and dot order").  0 (default): element
+ * scatter-adds and dot products in ascending order; 1: both descending.  Same arithmetic,
+ * another rounding order -- it measures how far the fixed-iteration CG amplifies
+ * summation-order rounding alone. */
+static int g_rev = 0;
+void or_set_order(int rev) { g_rev = rev ? 1 : 0; }
+
 static void gather_u(const or_ctx* c, int64_t e, const double* u, double* ue, int nomask) {
   for (int cc = 0; cc < 3; ++cc)
     for (int a = 0; a < c->nq; ++a) {
@@ -276,10 +284,12 @@ static void gather_u(const or_ctx* c, int64_t e, const double* u, double* ue, in
 }
 /* Scatter-add element vectors chunk [e0, e1) in element order (serial => fixed order). */
 static void scatter_chunk(const or_ctx* c, int64_t e0, int64_t e1, const double* ye, double* y) {
-  for (int64_t e = e0; e < e1; ++e)
+  for (int64_t i = e0; i < e1; ++i) {
+    const int64_t e = g_rev ? e1 - 1 - (i - e0) : i;
     for (int cc = 0; cc < 3; ++cc)
       for (int a = 0; a < c->nq; ++a)
         y[cc * c->n_nodes + or_node(c, e, a)] += ye[(e - e0) * 3 * c->nq + cc * c->nq + a];
+  }
 }
 static void mask_velocity(const or_ctx* c, double* y) {
   for (int cc = 0; cc < 3; ++cc)
@@ -390,7 +400,9 @@ void or_apply_B(or_ctx* c, const double* u, double* p, int nomask) {
 void or_apply_BT(or_ctx* c, const double* p, double* y, int nomask) {
   const int nq = c->nq, nm = c->nm;
   memset(y, 0, sizeof(double) * c->n_v);
-  for (int64_t e0 = 0; e0 < c->n_el; e0 += c->chunk) {
+  const int64_t nch = (c->n_el + c->chunk - 1) / c->chunk;
+  for (int64_t ic = 0; ic < nch; ++ic) {
+    const int64_t e0 = (g_rev ? nch - 1 - ic : ic) * c->chunk;
     int64_t e1 = e0 + c->chunk < c->n_el ? e0 + c->chunk : c->n_el;
 #pragma omp parallel for schedule(static)
     for (int64_t e = e0; e < e1; ++e) {
@@ -505,7 +517,10 @@ void or_jacobi_diag(or_ctx* c, const double* Xinv, double* diag) {
  * Neumann null space).                         */
 static double dot(const double* a, const double* b, int64_t n) {
   double s = 0.0;
-  for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+  if (g_rev)
+    for (int64_t i = n - 1; i >= 0; --i) s += a[i] * b[i];
+  else
+    for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
   return s;
 }
 void or_project(const or_ctx* c, double* v) {

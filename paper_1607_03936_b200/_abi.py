@@ -45,6 +45,11 @@ SYMBOLS = [
     ("wb_poisson_eigmax", _i, [_vp, _i, _vp, _i, C.POINTER(_d)]),
     ("wb_get_diagA", _i, [_vp, _vp]),
     ("wb_set_inner_cheb", _i, [_vp, _d, _d, _d, _d]),
+    ("wb_setup_mg", _i, [_vp, _i]),
+    ("wb_mg_vcycle", _i, [_vp, _i, _vp, _vp]),
+    ("wb_poisson_mgcg", _i, [_vp, _i, _vp, _vp, _i]),
+    ("wb_set_inner_mg", _i, [_vp, _i]),
+    ("wb_mg_get_lumped", _i, [_vp, _i, _vp, _vp]),
     ("wb_velocity_cheb", _i, [_vp, _vp, _vp, _i, _d, _d]),
     ("wb_velocity_eigmax", _i, [_vp, _vp, _i, C.POINTER(_d)]),
     ("wb_stokes_fgmres", _i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _d, _i, _i, _d, _d, C.POINTER(_i), C.POINTER(_d)]),
@@ -233,6 +238,26 @@ class Context:
 
     def set_inner_cheb(self, lmin_l=0.0, lmax_l=0.0, lmin_r=0.0, lmax_r=0.0):
         self._check(self._L.wb_set_inner_cheb(self._h, float(lmin_l), float(lmax_l), float(lmin_r), float(lmax_r)))
+
+    # -- geometric pressure multigrid (R20)
+    def setup_mg(self, nu: int = 3):
+        self._check(self._L.wb_setup_mg(self._h, int(nu)))
+
+    def mg_vcycle(self, side: int, b, x):
+        self._check(self._L.wb_mg_vcycle(self._h, int(side), _ptr(b, self.n_p), _ptr(x, self.n_p)))
+        return x
+
+    def poisson_mgcg(self, side: int, b, x, iters: int):
+        self._check(self._L.wb_poisson_mgcg(self._h, int(side), _ptr(b, self.n_p), _ptr(x, self.n_p), int(iters)))
+        return x
+
+    def set_inner_mg(self, iters: int = 0):
+        self._check(self._L.wb_set_inner_mg(self._h, int(iters)))
+
+    def mg_get_lumped(self, level: int, Cw=None, Dw=None):
+        n = (2 * int(self.query(f"mg_N_{int(level)}")) + 1) ** 3
+        f = lambda t: _ptr(t, n) if t is not None else None  # noqa: E731
+        self._check(self._L.wb_mg_get_lumped(self._h, int(level), f(Cw), f(Dw)))
 
     def get_diagA(self, dA):
         self._check(self._L.wb_get_diagA(self._h, _ptr(dA, self.n_v)))

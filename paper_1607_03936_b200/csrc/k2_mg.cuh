@@ -1,0 +1,152 @@
+// k2_mg.cuh -- kernels of the geometric pressure multigrid for K_w (
+// PAPER.md:2468-2546; reading R20), k = 2 (Q2 x P1disc):
+//  * coarse weights by density injection: C_c[G] = C_f[iota(G)] * prod_d (G_d even ? 2 : 4)
+//    -- the ratio M_c[G] / M_f[iota(G)] of the unweighted lumped masses (1-D vertex h/3,
+//    mid-edge 2h/3 per unit weight, coarse h = 2 fine h), in closed form;
+//  * transfers: the exact embedding of the coarse P1disc space in the fine one.  With the
+//    orthonormal modes (1, L1(x), L1(y), L1(z)) on each reference element and the child
+//    coordinate xi_c = (xi_f + s)/2, s = +-1 per axis, L1(xi_c) = L1(xi_f)/2 + (sqrt(3)/2)s L0:
+//      fine f_0 = c_0 + (sqrt(3)/2)(s_x c_x + s_y c_y + s_z c_z),  f_d = c_d / 2;
+//    restriction is the transpose (children summed in ascending s = sx + 2 sy + 4 sz);
+//  * the splitmix64 start vector of the power iteration (same generator as the oracle).
+#pragma once
+#include "kernels.cuh"
+
+namespace wb {
+
+__device__ __forceinline__ double mg_sign(int s, int d) { return ((s >> d) & 1) ? 1.0 : -1.0; }
+
+// coarse lumped masses of both sides from the fine ones (nodes of the coarse Q2 grid)
+__global__ void k_mg_inject(const double* __restrict__ Cf, const double* __restrict__ Df, double* __restrict__ Cc,
+                            double* __restrict__ Dc, int Nc) {
+  const int nc = 2 * Nc + 1, nf = 4 * Nc + 1;
+  const int64_t n = (int64_t)nc * nc * nc;
+  for (int64_t G = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; G < n; G += (int64_t)gridDim.x * blockDim.x) {
+    const int gx = (int)(G % nc), gy = (int)((G / nc) % nc), gz = (int)(G / ((int64_t)nc * nc));
+    const int64_t f = (int64_t)(2 * gx) + (int64_t)nf * ((int64_t)(2 * gy) + (int64_t)nf * (2 * gz));
+    const double r = ((gx & 1) ? 4.0 : 2.0) * ((gy & 1) ? 4.0 : 2.0) * ((gz & 1) ? 4.0 : 2.0);
+    Cc[G] = Cf[f] * r;
+    Dc[G] = Df[f] * r;
+  }
+}
+
+// X = mask / C per side and the nonpositive interior counts (icount[0], icount[1])
+__global__ void k_inv_lumped(const double* __restrict__ Cw, const double* __restrict__ Dw, double* __restrict__ Cinv,
+                             double* __restrict__ Dinv, unsigned long long* icount, Geo G) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G.n_nodes; g += (int64_t)gridDim.x * blockDim.x) {
+    const int gx = (int)(g % G.nn1), gy = (int)((g / G.nn1) % G.nn1), gz = (int)(g / ((int64_t)G.nn1 * G.nn1));
+    const bool bnd = node_bnd(gx, gy, gz, G.nn1);
+    const double c = Cw[g], d = Dw[g];
+    Cinv[g] = bnd ? 0.0 : 1.0 / c;
+    Dinv[g] = bnd ? 0.0 : 1.0 / d;
+    if (!bnd && !(c > 0.0)) atomicAdd(&icount[0], 1ull);  // (counts only: order-free)
+    if (!bnd && !(d > 0.0)) atomicAdd(&icount[1], 1ull);
+  }
+}
+
+__device__ __forceinline__ int64_t mg_child(int64_t ec, int Nc, int s) {
+  const int cx = (int)(ec % Nc), cy = (int)((ec / Nc) % Nc), cz = (int)(ec / ((int64_t)Nc * Nc));
+  const int Nf = 2 * Nc;
+  return (int64_t)(2 * cx + (s & 1)) + (int64_t)Nf * ((int64_t)(2 * cy + ((s >> 1) & 1)) +
+                                                      (int64_t)Nf * (2 * cz + ((s >> 2) & 1)));
+}
+
+// r_c = P^T r_f, element-major (4 modes per element)
+__global__ void k_mg_restrict(const double* __restrict__ rf, double* __restrict__ rc, int Nc) {
+  const double h3 = 0.86602540378443864676;  // sqrt(3) / 2
+  const int64_t n = (int64_t)Nc * Nc * Nc;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const double* f = rf + 4 * mg_child(e, Nc, s);
+      const double f0 = f[0];
+      a0 += f0;
+      a1 += h3 * mg_sign(s, 0) * f0 + 0.5 * f[1];
+      a2 += h3 * mg_sign(s, 1) * f0 + 0.5 * f[2];
+      a3 += h3 * mg_sign(s, 2) * f0 + 0.5 * f[3];
+    }
+    rc[4 * e] = a0; rc[4 * e + 1] = a1; rc[4 * e + 2] = a2; rc[4 * e + 3] = a3;
+  }
+}
+
+// x_f += P x_c (one thread per fine element)
+__global__ void k_mg_prolong_add(const double* __restrict__ xc, double* __restrict__ xf, int Nc) {
+  const double h3 = 0.86602540378443864676;
+  const int Nf = 2 * Nc;
+  const int64_t n = (int64_t)Nf * Nf * Nf;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int fx = (int)(e % Nf), fy = (int)((e / Nf) % Nf), fz = (int)(e / ((int64_t)Nf * Nf));
+    const int s = (fx & 1) | ((fy & 1) << 1) | ((fz & 1) << 2);
+    const int64_t ec = (int64_t)(fx >> 1) + (int64_t)Nc * ((int64_t)(fy >> 1) + (int64_t)Nc * (fz >> 1));
+    const double* c = xc + 4 * ec;
+    double* f = xf + 4 * e;
+    f[0] += c[0] + h3 * (mg_sign(s, 0) * c[1] + mg_sign(s, 1) * c[2] + mg_sign(s, 2) * c[3]);
+    f[1] += 0.5 * c[1];
+    f[2] += 0.5 * c[2];
+    f[3] += 0.5 * c[3];
+  }
+}
+
+// v_i = uniform [-1, 1) from the i-th splitmix64 output of state `seed` (Steele, Lea & Flood)
+__global__ void k_splitmix(double* __restrict__ v, int64_t n, unsigned long long seed) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long z = seed + (unsigned long long)(i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = z ^ (z >> 31);
+    v[i] = 2.0 * ((double)(z >> 11) * (1.0 / 9007199254740992.0)) - 1.0;
+  }
+}
+
+// r = b - t
+__global__ void k_mg_resid(double* __restrict__ r, const double* __restrict__ b, const double* __restrict__ t,
+                           int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    r[i] = b[i] - t[i];
+}
+
+// element-major vector: subtract the mean of the mode-0 entries (R10 projection), mean
+// from the fixed-order sum in *sum
+__global__ void k_sub_mode0_mean(double* __restrict__ v, int64_t n_el, int nm, const double* __restrict__ sum) {
+  const double mean = *sum / (double)n_el;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_el; e += (int64_t)gridDim.x * blockDim.x)
+    v[e * nm] -= mean;
+}
+
+// MG-PCG scalars on the device (O9 with M^-1 = V):  s[0] = rz, s[1] = pq, s[2] = rz', s[3] = stop
+// alpha step: stop if rz == 0 or pq == 0; else x += a p, r -= a q, a = rz / pq
+__global__ void k_mgcg_xr(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                          const double* __restrict__ q, int64_t n, double* s) {
+  const double rz = s[0], pq = s[1];
+  if (s[3] != 0.0 || rz == 0.0 || pq == 0.0) return;
+  const double a = rz / pq;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(a, p[i], x[i]);
+    r[i] = fma(-a, q[i], r[i]);
+  }
+}
+// beta step: p = z + (rz'/rz) p; then rz = rz' (the last block); stop flag latched
+__global__ void k_mgcg_p(double* __restrict__ p, const double* __restrict__ z, int64_t n, double* s,
+                         unsigned* counter) {
+  const double rz = s[0], pq = s[1], rz1 = s[2];
+  const bool stop = s[3] != 0.0 || rz == 0.0 || pq == 0.0;
+  if (!stop) {
+    const double b = rz1 / rz;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+      p[i] = fma(b, p[i], z[i]);
+  }
+  // every block has read s[0..3]; the last block to finish updates them
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(counter, 1u);
+    if (t == gridDim.x - 1) {
+      if (stop) s[3] = 1.0;
+      else s[0] = rz1;
+      *counter = 0u;
+    }
+  }
+}
+
+}  // namespace wb

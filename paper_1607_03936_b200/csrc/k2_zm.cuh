@@ -114,7 +114,7 @@ __device__ __forceinline__ void zm_half_a(const double (&Pp)[2][2][4], const dou
 template <bool LAST>
 __device__ __forceinline__ void zm_half_b(const double (&Pc)[2][2][4], const double (&X)[2][2][2],
                                           const double (&s0)[2][2][3], double (&Q1)[2][2][4]) {
-  if (LAST) return;
+  if constexpr (!LAST) {
 #pragma unroll
   for (int sy = 0; sy < 2; ++sy)
 #pragma unroll
@@ -164,6 +164,7 @@ __device__ __forceinline__ void zm_half_b(const double (&Pc)[2][2][4], const dou
             }
           }
       }
+  }
 }
 
 // Same contract as k_K2_tma (mode 0: p = z, 1: p = z + beta p_old, 2: p = p_old as is,

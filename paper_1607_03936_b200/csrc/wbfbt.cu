@@ -103,9 +103,10 @@ struct wb_ctx {
   // node-owner z-march Poisson kernel (k2_zm.cuh): tensor maps with its per-layer box,
   // X prescaled on the padded nodal grid, option "k_zm" (default on), z-chunk length
   bool zm_ok = false;
-  int use_zm = 0, zm_zc = 4;
+  int use_zm = 0, zm_zc = 4, zm_var = 0;
   double *XzL = nullptr, *XzR = nullptr;
-  CUtensorMap tz_pp, tz_pp1, tz_pz;
+  static constexpr int ZM_NV = 5;  // kernel variants (tile shape, CTAs per SM): zm_variants below
+  CUtensorMap tz[ZM_NV][3];        // per variant: maps of pp, pp1, pz
   int kz = 0;  // TMA Poisson kernel: 1 = z = Minv r stored by the PCG update and loaded as one box; 0 = r + Minv boxes (default: faster with the y-fastest storage)
   int k_dbg = 0;  // timing probe bits for the fused K kernel (results invalid when nonzero)
   // profiling: CUDA-event pairs around every Poisson-operator launch (direct launches)
@@ -113,9 +114,27 @@ struct wb_ctx {
   static constexpr int PROF_MAX = 4096;
   cudaEvent_t prof_ev[2 * PROF_MAX] = {};
   int prof_n = 0;
+  bool prof_cap = false;  // profiling inside a stream capture: event-record graph nodes
+  std::vector<cudaGraphExec_t> prof_execs;  // the profiled loops' graphs
   long long launches = 0;
+  struct MGH* mg = nullptr;  // pressure multigrid hierarchy (R20), built by wb_setup_mg
   char err[512] = {0};
 };
+
+// Pressure multigrid (R20): level l = 0 is the context itself, l >= 1 are internal
+// k = 2 contexts on the N / 2^l meshes; per level element-major work vectors.
+struct MGH {
+  int nl = 0, nu = 3;
+  int Ns[16] = {};
+  wb_ctx* lev[16] = {};
+  double lam[2][16] = {};
+  double *b[16] = {}, *x[16] = {}, *r[16] = {}, *t[16] = {};
+  double *rk = nullptr, *zk = nullptr, *pk = nullptr, *qk = nullptr, *xk = nullptr;  // MG-PCG on level 0
+  double* s = nullptr;  // device scalars: rz, pq, rz', stop
+  int inner_iters = 0;  // wBFBT inner solves by MG-PCG with this many iterations (0: off)
+};
+void mg_free(wb_ctx* c);
+wb_status run_mgcg(wb_ctx* c, int side, const double* b, double* x, int iters);
 
 namespace {
 
@@ -308,12 +327,30 @@ bool tma_active(const wb_ctx* c) { return c->k == 2 && c->tma_ok && c->use_tma &
 bool zm_active(const wb_ctx* c) { return tma_active(c) && c->zm_ok && c->use_zm; }
 double* z_out(const wb_ctx* c) { return tma_active(c) && (c->kz || zm_active(c)) ? c->pz : nullptr; }
 const CUtensorMap* zmap_of(wb_ctx* c, const double* p) {
-  if (p == c->pp) return &c->tz_pp;
-  if (p == c->pp1) return &c->tz_pp1;
-  if (p == c->pz) return &c->tz_pz;
+  if (p == c->pp) return &c->tz[c->zm_var][0];
+  if (p == c->pp1) return &c->tz[c->zm_var][1];
+  if (p == c->pz) return &c->tz[c->zm_var][2];
   return nullptr;
 }
-constexpr int ZM_TY = 16, ZM_TX = 8, ZM_MINB = 2;
+// z-march kernel variants: (TY, TX, CTAs per SM)
+struct ZmVar { int ty, tx, minb; };
+constexpr ZmVar zm_variants[wb_ctx::ZM_NV] = {{16, 8, 2}, {16, 8, 3}, {8, 8, 4}, {8, 8, 5}, {32, 4, 2}};
+template <int TY, int TX, int MINB>
+void launch_zm_t(wb_ctx* c, const CUtensorMap* tp, const CUtensorMap* tz, const double* xz, double* pnew, double* q,
+                 int mode, PcgArgs a, int* npq) {
+  using K = ZMK<TY, TX>;
+  const int N = c->N, zc = c->zm_zc;
+  const int grid = ((N + TY - 1) / TY) * ((N + TX - 1) / TX) * ((N + zc - 1) / zc);
+  k_K2_zm<TY, TX, MINB><<<grid, K::NTH, K::SMEM, c->stream>>>(*tp, *tz, xz, pnew, q, N, zc, mode | c->k_dbg, a.it,
+                                                               a.ctl, c->rzp, c->red_blocks, rz_hist(c), pq_hist(c),
+                                                               c->stop, c->pqp, c->pl);
+  *npq = grid;
+}
+template <int TY, int TX, int MINB>
+bool attr_zm_t() {
+  return cudaFuncSetAttribute(k_K2_zm<TY, TX, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)ZMK<TY, TX>::SMEM) == cudaSuccess;
+}
 
 wb_status run_k2f(wb_ctx* c, const double* pold, double* pnew, const double* r, const double* Minv, const double* X,
                   double* q, int mode, PcgArgs a, int* npq) {
@@ -321,14 +358,14 @@ wb_status run_k2f(wb_ctx* c, const double* pold, double* pnew, const double* r, 
     const CUtensorMap *tp = zmap_of(c, pold), *tz = zmap_of(c, c->pz);
     const double* xz = X == c->Cinv ? c->XzL : (X == c->Dinv ? c->XzR : nullptr);
     if (tp && tz && xz && (mode == 2 || r == c->pr)) {
-      using K = ZMK<ZM_TY, ZM_TX>;
-      const int N = c->N, zc = c->zm_zc;
-      const int grid = ((N + ZM_TY - 1) / ZM_TY) * ((N + ZM_TX - 1) / ZM_TX) * ((N + zc - 1) / zc);
-      k_K2_zm<ZM_TY, ZM_TX, ZM_MINB><<<grid, K::NTH, K::SMEM, c->stream>>>(
-          *tp, *tz, xz, pnew, q, N, zc, mode | c->k_dbg, a.it, a.ctl, c->rzp, c->red_blocks, rz_hist(c), pq_hist(c),
-          c->stop, c->pqp, c->pl);
+      switch (c->zm_var) {
+        case 0: launch_zm_t<16, 8, 2>(c, tp, tz, xz, pnew, q, mode, a, npq); break;
+        case 1: launch_zm_t<16, 8, 3>(c, tp, tz, xz, pnew, q, mode, a, npq); break;
+        case 2: launch_zm_t<8, 8, 4>(c, tp, tz, xz, pnew, q, mode, a, npq); break;
+        case 3: launch_zm_t<8, 8, 5>(c, tp, tz, xz, pnew, q, mode, a, npq); break;
+        default: launch_zm_t<32, 4, 2>(c, tp, tz, xz, pnew, q, mode, a, npq); break;
+      }
       LAUNCH_CHECK(c);
-      *npq = grid;
       return WB_OK;
     }
   }
@@ -389,12 +426,11 @@ bool make_tm_vec(CUtensorMap* tm, const double* base, int N, int nm) {
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 // the same storage, box = one layer of the z-march kernel's column tile + halo, all modes
-bool make_tm_zm(CUtensorMap* tm, const double* base, int N, int nm) {
-  using K = ZMK<ZM_TY, ZM_TX>;
+bool make_tm_zm(CUtensorMap* tm, const double* base, int N, int nm, int ty, int tx) {
   const cuuint64_t ny = (cuuint64_t)N + 2;
   const cuuint64_t dims[4] = {ny, (cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)nm};
   const cuuint64_t strides[3] = {ny * 8, ny * N * 8, ny * N * N * 8};
-  const cuuint32_t box[4] = {(cuuint32_t)K::HY, 1u, (cuuint32_t)K::HX, (cuuint32_t)nm};
+  const cuuint32_t box[4] = {(cuuint32_t)(ty + 2), 1u, (cuuint32_t)(tx + 2), (cuuint32_t)nm};
   const cuuint32_t es[4] = {1, 1, 1, 1};
   return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -404,14 +440,18 @@ bool setup_zm(wb_ctx* c) {
   if (!c->ylay || c->nm != 4) return false;
   const int64_t R = 2 * (int64_t)c->N + 2;
   const size_t bx = sizeof(double) * (size_t)(R * R * R);
-  if (cudaMalloc(&c->XzL, bx) != cudaSuccess || cudaMalloc(&c->XzR, bx) != cudaSuccess ||
-      cudaFuncSetAttribute(k_K2_zm<ZM_TY, ZM_TX, ZM_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)ZMK<ZM_TY, ZM_TX>::SMEM) != cudaSuccess) {
+  if (cudaMalloc(&c->XzL, bx) != cudaSuccess || cudaMalloc(&c->XzR, bx) != cudaSuccess || !attr_zm_t<16, 8, 2>() ||
+      !attr_zm_t<16, 8, 3>() || !attr_zm_t<8, 8, 4>() || !attr_zm_t<8, 8, 5>() || !attr_zm_t<32, 4, 2>()) {
     cudaGetLastError();
     return false;
   }
-  return make_tm_zm(&c->tz_pp, c->pp, c->N, c->nm) && make_tm_zm(&c->tz_pp1, c->pp1, c->N, c->nm) &&
-         make_tm_zm(&c->tz_pz, c->pz, c->N, c->nm);
+  for (int v = 0; v < wb_ctx::ZM_NV; ++v) {
+    const int ty = zm_variants[v].ty, tx = zm_variants[v].tx;
+    if (!make_tm_zm(&c->tz[v][0], c->pp, c->N, c->nm, ty, tx) || !make_tm_zm(&c->tz[v][1], c->pp1, c->N, c->nm, ty, tx) ||
+        !make_tm_zm(&c->tz[v][2], c->pz, c->N, c->nm, ty, tx))
+      return false;
+  }
+  return true;
 }
 bool setup_tma(wb_ctx* c) {
   if (!c->ylay) return false;
@@ -543,14 +583,16 @@ wb_status pcg_loop_direct(wb_ctx* c, int side, int iters) {
     if (prof) {
       cudaEvent_t* ev = c->prof_ev + 2 * c->prof_n;
       if (!ev[0]) { cudaEventCreate(&ev[0]); cudaEventCreate(&ev[1]); }
-      CUDA_TRY(c, cudaEventRecord(ev[0], c->stream));
+      CUDA_TRY(c, cudaEventRecordWithFlags(ev[0], c->stream, c->prof_cap ? cudaEventRecordExternal : 0));
     }
     PcgArgs a;
     a.it = it; a.ctl = 1;
     int npq = 0;
     wb_status s = run_K_pcg(c, side, it == 0 ? 0 : 1, PB[(it + 1) & 1], PB[it & 1], c->pr, c->pq, a, &pcur, &npq);
     if (s) return s;
-    if (prof) CUDA_TRY(c, cudaEventRecord(c->prof_ev[2 * c->prof_n++ + 1], c->stream));
+    if (prof)
+      CUDA_TRY(c, cudaEventRecordWithFlags(c->prof_ev[2 * c->prof_n++ + 1], c->stream,
+                                           c->prof_cap ? cudaEventRecordExternal : 0));
     // x updates in pairs (odd iterations), bitwise equal to every iteration (kernels.cuh)
     if (it & 1)
       k_pcg_upd<XU_PAIR><<<c->red_blocks, VBS, 0, c->stream>>>(c->px, c->pr, pcur, pprev, c->pq, Minv, c->pl.n, it,
@@ -575,12 +617,43 @@ void clear_graphs(wb_ctx* c) {
   for (int i = 0; i < c->n_graphs; ++i)
     if (c->graphs[i].exec) cudaGraphExecDestroy(c->graphs[i].exec);
   c->n_graphs = 0;
+  if (!c->prof_execs.empty()) {
+    cudaStreamSynchronize(c->stream);
+    for (cudaGraphExec_t e : c->prof_execs) cudaGraphExecDestroy(e);
+    c->prof_execs.clear();
+  }
 }
 
 // replay of an iteration loop as one CUDA graph (captured on a private stream), keyed
 // by (kind, side, iters, lo, hi); `direct` issues the loop's launches on c->stream
 template <class F>
 wb_status graph_loop(wb_ctx* c, int kind, int side, int iters, double lo, double hi, F direct) {
+  if (c->profile && c->use_graph && iters > 0 && c->cap_stream) {
+    // profiled replay: the loop is captured afresh with an event-record NODE around every
+    // Poisson-operator launch, so the kernels run with graph launch gaps (as in the
+    // unprofiled step) and the event pairs time the kernels, not host launch latency
+    cudaStream_t saved = c->stream;
+    const long long l0 = c->launches;
+    CUDA_TRY(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+    c->stream = c->cap_stream;
+    c->prof_cap = true;
+    wb_status s = direct();
+    c->prof_cap = false;
+    c->stream = saved;
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(c->cap_stream, &graph);
+    if (s) { if (graph) cudaGraphDestroy(graph); return s; }
+    if (e != cudaSuccess) return set_err(c, WB_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return set_err(c, WB_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    c->prof_execs.push_back(ex);  // destroyed by clear_graphs (after a sync)
+    e = cudaGraphLaunch(ex, c->stream);
+    if (e != cudaSuccess) return set_err(c, WB_ECUDA, "graph launch: %s", cudaGetErrorString(e));
+    (void)l0;
+    return WB_OK;
+  }
   if (!c->use_graph || c->profile || iters == 0 || !c->cap_stream) return direct();
   wb_ctx::GraphEntry* g = nullptr;
   for (int i = 0; i < c->n_graphs; ++i) {
@@ -829,6 +902,7 @@ wb_status run_K(wb_ctx* c, int side, const double* p, double* q) {
 
 // wBFBT's inner Poisson solve: PCG, or Chebyshev-Jacobi when wb_set_inner_cheb chose it
 wb_status run_inner(wb_ctx* c, int side, const double* b, double* x, int iters) {
+  if (c->mg && c->mg->inner_iters > 0) return run_mgcg(c, side, b, x, c->mg->inner_iters);
   if (c->inner) return run_cheb(c, side, b, x, iters, c->cheb_lo[side], c->cheb_hi[side]);
   return run_poisson(c, side, b, x, iters);
 }
@@ -987,6 +1061,7 @@ wb_status check_ctx(wb_ctx* c, bool need_visc) {
 }
 
 void free_all(wb_ctx* c) {
+  mg_free(c);
   double** bufs[] = {&c->mut, &c->Cw, &c->Dw, &c->Cinv, &c->Dinv, &c->dKl, &c->dKr, &c->MinvL, &c->MinvR,
                      &c->E, &c->tv, &c->tw, &c->px, &c->pr, &c->pp, &c->pp1, &c->pq, &c->pz, &c->s0, &c->s1, &c->s2,
                      &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->Fu, &c->mueff,
@@ -1238,7 +1313,10 @@ static wb_status read_nonpos(wb_ctx* c) {
 }
 
 template <int K>
+static wb_status finish_lumped(wb_ctx* c);
+template <int K>
 static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
+  mg_free(c);  // a multigrid hierarchy belongs to the previous viscosity
   const int64_t nmu = c->n_el * c->nq;
   CUDA_TRY(c, cudaMemsetAsync(c->icount, 0, sizeof(unsigned long long) * 4, c->stream));
   c->dA_valid = false;
@@ -1278,6 +1356,13 @@ static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
                                                                  c->icount + 1, c->G);
   }
   LAUNCH_CHECK(c);
+  return finish_lumped<K>(c);
+}
+
+// everything downstream of C_w, D_w, C_w^-1, D_w^-1 (and the nonpositive counts in
+// icount[1..2]): the Poisson kernels' X layouts, Jacobi diagonals, Minv
+template <int K>
+static wb_status finish_lumped(wb_ctx* c) {
   if (c->tma_ok) {  // X = C_w^-1, D_w^-1 in the tile-blocked pencil layout of the TMA kernel
     using F = FK2<TMA_TX, TMA_TY, TMA_TZ>;
     const int nt = ((c->N + TMA_TX - 1) / TMA_TX) * ((c->N + TMA_TY - 1) / TMA_TY) * ((c->N + TMA_TZ - 1) / TMA_TZ);
@@ -1319,6 +1404,141 @@ static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
       return set_err(c, WB_ENONPOS_LUMP, "nonpositive lumped entries: C_w %lld, D_w %lld", c->n_nonpos[0],
                      c->n_nonpos[1]);
   }
+  return WB_OK;
+}
+
+// ================================================================ pressure multigrid (R20)
+void mg_free(wb_ctx* c) {
+  MGH* M = c->mg;
+  if (!M) return;
+  cudaStreamSynchronize(c->stream);
+  for (int l = 0; l < M->nl; ++l) {
+    for (double** b : {&M->b[l], &M->x[l], &M->r[l], &M->t[l]})
+      if (*b) cudaFree(*b);
+    if (l > 0 && M->lev[l]) wb_destroy(M->lev[l]);
+  }
+  for (double** b : {&M->rk, &M->zk, &M->pk, &M->qk, &M->xk, &M->s})
+    if (*b) cudaFree(*b);
+  delete M;
+  c->mg = nullptr;
+  cudaGetLastError();
+}
+
+static wb_status mg_project(wb_ctx* c, double* v) {  // R10 on an element-major vector of c
+  k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(v, c->n_el, c->nm, c->partial, c->counter, c->scal + S_SCR + 1);
+  LAUNCH_CHECK(c);
+  k_sub_mode0_mean<<<stream_blocks(c->n_el), VBS, 0, c->stream>>>(v, c->n_el, c->nm, c->scal + S_SCR + 1);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+
+// x = V_l(b): x = S(b); x += P V_{l+1}(P^T (b - K x)); x += S(b - K x)  (element-major)
+static wb_status mg_vcycle(wb_ctx* c, int side, int l, const double* b, double* x) {
+  MGH& M = *c->mg;
+  wb_ctx* L = M.lev[l];
+  L->stream = c->stream;
+  const int64_t n = L->n_p;
+  if (l == M.nl - 1) return run_poisson(L, side, b, x, (int)std::min<int64_t>(n, 256));
+  const double lam = M.lam[side][l];
+  wb_status s = run_cheb(L, side, b, x, M.nu, 0.1 * lam, 1.1 * lam);
+  if (s) return s;
+  if ((s = run_K(L, side, x, M.t[l]))) return s;
+  k_mg_resid<<<stream_blocks(n), VBS, 0, c->stream>>>(M.r[l], b, M.t[l], n);
+  LAUNCH_CHECK(c);
+  const int Nc = M.Ns[l + 1];
+  k_mg_restrict<<<stream_blocks((int64_t)Nc * Nc * Nc), VBS, 0, c->stream>>>(M.r[l], M.b[l + 1], Nc);
+  LAUNCH_CHECK(c);
+  if ((s = mg_vcycle(c, side, l + 1, M.b[l + 1], M.x[l + 1]))) return s;
+  k_mg_prolong_add<<<stream_blocks(L->n_el), VBS, 0, c->stream>>>(M.x[l + 1], x, Nc);
+  LAUNCH_CHECK(c);
+  if ((s = run_K(L, side, x, M.t[l]))) return s;
+  k_mg_resid<<<stream_blocks(n), VBS, 0, c->stream>>>(M.r[l], b, M.t[l], n);
+  LAUNCH_CHECK(c);
+  if ((s = run_cheb(L, side, M.r[l], M.t[l], M.nu, 0.1 * lam, 1.1 * lam))) return s;
+  k_axpy<<<stream_blocks(n), VBS, 0, c->stream>>>(x, M.t[l], n, 1.0);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+
+// x = P MGPCG(K_side, P b): the O9 recurrence with M^-1 = one V-cycle, exactly iters
+// iterations, scalars on the device
+wb_status run_mgcg(wb_ctx* c, int side, const double* b, double* x, int iters) {
+  MGH& M = *c->mg;
+  const int64_t n = c->n_p;
+  const unsigned nb = stream_blocks(n);
+  CUDA_TRY(c, cudaMemcpyAsync(M.rk, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  wb_status s = mg_project(c, M.rk);
+  if (s) return s;
+  CUDA_TRY(c, cudaMemsetAsync(M.xk, 0, sizeof(double) * n, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(M.s, 0, sizeof(double) * 4, c->stream));
+  if ((s = mg_vcycle(c, side, 0, M.rk, M.zk))) return s;
+  CUDA_TRY(c, cudaMemcpyAsync(M.pk, M.zk, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  if ((s = dev_dot(c, M.rk, M.zk, n, M.s))) return s;
+  for (int it = 0; it < iters; ++it) {
+    if ((s = run_K(c, side, M.pk, M.qk))) return s;
+    if ((s = dev_dot(c, M.pk, M.qk, n, M.s + 1))) return s;
+    k_mgcg_xr<<<nb, VBS, 0, c->stream>>>(M.xk, M.rk, M.pk, M.qk, n, M.s);
+    LAUNCH_CHECK(c);
+    if ((s = mg_vcycle(c, side, 0, M.rk, M.zk))) return s;
+    if ((s = dev_dot(c, M.rk, M.zk, n, M.s + 2))) return s;
+    k_mgcg_p<<<nb, VBS, 0, c->stream>>>(M.pk, M.zk, n, M.s, c->counter + 3);
+    LAUNCH_CHECK(c);
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(x, M.xk, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  return mg_project(c, x);
+}
+
+static wb_status mg_setup(wb_ctx* c, int nu) {
+  mg_free(c);
+  MGH* M = new (std::nothrow) MGH();
+  if (!M) return set_err(c, WB_ENOMEM, "multigrid allocation failed");
+  c->mg = M;
+  M->nu = nu;
+  int N = c->N;
+  M->Ns[M->nl++] = N;
+  while (N % 2 == 0 && N > 1 && M->nl < 16) { N /= 2; M->Ns[M->nl++] = N; }
+  M->lev[0] = c;
+  auto fail = [&](wb_status st, const char* what) {
+    mg_free(c);
+    return set_err(c, st, "multigrid setup: %s", what);
+  };
+  for (int l = 1; l < M->nl; ++l) {
+    wb_ctx* L = nullptr;
+    wb_status st = wb_create(&L, M->Ns[l], 2, c->flags & WB_STRICT_LUMP, (void*)c->stream);
+    if (st) return fail(st, "level context");
+    M->lev[l] = L;
+    wb_ctx* F = M->lev[l - 1];
+    CUDA_TRY(c, cudaMemsetAsync(L->icount, 0, sizeof(unsigned long long) * 4, c->stream));
+    k_mg_inject<<<stream_blocks(L->n_nodes), VBS, 0, c->stream>>>(F->Cw, F->Dw, L->Cw, L->Dw, M->Ns[l]);
+    LAUNCH_CHECK(c);
+    k_inv_lumped<<<stream_blocks(L->n_nodes), VBS, 0, c->stream>>>(L->Cw, L->Dw, L->Cinv, L->Dinv, L->icount + 1,
+                                                                   L->G);
+    LAUNCH_CHECK(c);
+    if ((st = finish_lumped<2>(L))) return fail(st, wb_last_error(L));
+  }
+  auto dalloc = [](double** p, int64_t n) {
+    return cudaMalloc(p, sizeof(double) * (size_t)std::max<int64_t>(n, 1)) == cudaSuccess;
+  };
+  for (int l = 0; l < M->nl; ++l) {
+    const int64_t n = M->lev[l]->n_p;
+    if (!dalloc(&M->b[l], n) || !dalloc(&M->x[l], n) || !dalloc(&M->r[l], n) || !dalloc(&M->t[l], n))
+      return fail(WB_ENOMEM, "level vectors");
+  }
+  const int64_t n0 = c->n_p;
+  if (!dalloc(&M->rk, n0) || !dalloc(&M->zk, n0) || !dalloc(&M->pk, n0) || !dalloc(&M->qk, n0) ||
+      !dalloc(&M->xk, n0) || !dalloc(&M->s, 4))
+    return fail(WB_ENOMEM, "MG-PCG vectors");
+  // Chebyshev intervals: power iteration (20 steps) from the splitmix64 start vector
+  for (int l = 0; l < M->nl - 1; ++l) {
+    wb_ctx* L = M->lev[l];
+    k_splitmix<<<stream_blocks(L->n_p), VBS, 0, c->stream>>>(M->b[l], L->n_p, 0x5EEDull);
+    LAUNCH_CHECK(c);
+    for (int side = 0; side < 2; ++side) {
+      wb_status st = run_eigmax(L, side, M->b[l], 20, &M->lam[side][l]);
+      if (st) return fail(st, "eigenvalue estimate");
+    }
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return WB_OK;
 }
 
@@ -1444,6 +1664,54 @@ wb_status wb_set_inner_cheb(wb_ctx* c, double lmin_l, double lmax_l, double lmin
       return set_err(c, WB_EINVAL, "each interval must satisfy 0 < lmin < lmax < inf (or all four 0)");
   for (int i = 0; i < 2; ++i) { c->cheb_lo[i] = lo[i]; c->cheb_hi[i] = hi[i]; }
   c->inner = 1;
+  return WB_OK;
+}
+
+wb_status wb_setup_mg(wb_ctx* c, int nu) {
+  wb_status s = check_ctx(c, true);
+  if (s) return s;
+  if (c->k != 2) return set_err(c, WB_EINVAL, "the pressure multigrid is built for k = 2 (R20)");
+  if (nu < 1 || nu > 16) return set_err(c, WB_EINVAL, "nu must be in [1, 16]");
+  return mg_setup(c, nu);
+}
+
+wb_status wb_mg_vcycle(wb_ctx* c, int side, const double* b, double* x) {
+  wb_status s = check_ctx(c, true);
+  if (s) return s;
+  if (!c->mg) return set_err(c, WB_ESTATE, "no multigrid hierarchy (wb_setup_mg)");
+  if (!b || !x || (side != 0 && side != 1)) return set_err(c, WB_EINVAL, "bad argument");
+  const size_t bp = sizeof(double) * c->n_p;
+  if (overlaps(b, bp, x, bp)) return set_err(c, WB_EALIAS, "b and x overlap");
+  return mg_vcycle(c, side, 0, b, x);
+}
+
+wb_status wb_poisson_mgcg(wb_ctx* c, int side, const double* b, double* x, int iters) {
+  wb_status s = check_ctx(c, true);
+  if (s) return s;
+  if (!c->mg) return set_err(c, WB_ESTATE, "no multigrid hierarchy (wb_setup_mg)");
+  if (!b || !x || (side != 0 && side != 1) || iters < 0) return set_err(c, WB_EINVAL, "bad argument");
+  const size_t bp = sizeof(double) * c->n_p;
+  if (overlaps(b, bp, x, bp)) return set_err(c, WB_EALIAS, "b and x overlap");
+  return run_mgcg(c, side, b, x, iters);
+}
+
+wb_status wb_set_inner_mg(wb_ctx* c, int iters) {
+  if (!c) return WB_EINVAL;
+  if (iters < 0) return set_err(c, WB_EINVAL, "iters must be >= 0");
+  if (iters > 0 && !c->mg) return set_err(c, WB_ESTATE, "no multigrid hierarchy (wb_setup_mg)");
+  if (c->mg) c->mg->inner_iters = iters;
+  return WB_OK;
+}
+
+wb_status wb_mg_get_lumped(wb_ctx* c, int level, double* Cw, double* Dw) {
+  if (!c) return WB_EINVAL;
+  if (!c->mg) return set_err(c, WB_ESTATE, "no multigrid hierarchy (wb_setup_mg)");
+  if (level < 0 || level >= c->mg->nl) return set_err(c, WB_EINVAL, "bad level");
+  wb_ctx* L = c->mg->lev[level];
+  const size_t bn = sizeof(double) * L->n_nodes;
+  if (Cw) CUDA_TRY(c, cudaMemcpyAsync(Cw, L->Cw, bn, cudaMemcpyDeviceToDevice, c->stream));
+  if (Dw) CUDA_TRY(c, cudaMemcpyAsync(Dw, L->Dw, bn, cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return WB_OK;
 }
 
@@ -1682,6 +1950,22 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
     *value = c->weights;
   } else if (!strcmp(key, "inner")) {  // 1: wBFBT's inner solves are Chebyshev-Jacobi (wb_set_inner_cheb)
     *value = c->inner;
+  } else if (!strcmp(key, "mg_levels")) {  // levels of the pressure multigrid (0: none built)
+    *value = c->mg ? c->mg->nl : 0;
+  } else if (!strncmp(key, "mg_N_", 5) || !strncmp(key, "mg_lambda_", 10) || !strncmp(key, "mg_nonpos_", 10)) {
+    // mg_N_<l>; mg_lambda_<side>_<l> (Chebyshev interval scale); mg_nonpos_<side>_<l>
+    if (!c->mg) return set_err(c, WB_ESTATE, "no multigrid hierarchy (wb_setup_mg)");
+    int side = 0, l = -1;
+    if (key[3] == 'N') l = atoi(key + 5);
+    else if (sscanf(key + (key[3] == 'l' ? 10 : 10), "%d_%d", &side, &l) != 2) l = -1;
+    if (l < 0 || l >= c->mg->nl || side < 0 || side > 1) return set_err(c, WB_EINVAL, "bad multigrid key '%s'", key);
+    if (key[3] == 'N') *value = c->mg->Ns[l];
+    else if (key[3] == 'l') *value = c->mg->lam[side][l];
+    else {
+      wb_status st = read_nonpos(c->mg->lev[l]);
+      if (st) return st;
+      *value = (double)c->mg->lev[l]->n_nonpos[side];
+    }
   } else if (!strcmp(key, "k_zm")) {  // 1: the Poisson operator runs as the node-owner z-march kernel
     *value = zm_active(c) ? 1.0 : 0.0;
   } else if (!strcmp(key, "zm_zc")) {
@@ -1778,6 +2062,11 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k_zm must be 0 or 1");
     c->use_zm = (int)value;
     clear_graphs(c);
+  } else if (!strcmp(key, "zm_var")) {  // z-march kernel variant (tile shape, CTAs per SM)
+    if (!(value >= 0.0 && value < wb_ctx::ZM_NV) || value != (double)(int)value)
+      return set_err(c, WB_EINVAL, "zm_var must be an integer in [0, %d)", wb_ctx::ZM_NV);
+    c->zm_var = (int)value;
+    clear_graphs(c);
   } else if (!strcmp(key, "zm_zc")) {  // element layers per CTA of the z-march kernel
     if (!(value >= 1.0 && value <= 64.0) || value != (double)(int)value)
       return set_err(c, WB_EINVAL, "zm_zc must be an integer in [1, 64]");
@@ -1796,6 +2085,7 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "profile must be 0 or 1");
     c->profile = (int)value;
     c->prof_n = 0;  // (re)start the record
+    clear_graphs(c);
   } else
     return set_err(c, WB_EINVAL, "unknown option '%s'", key);
   return WB_OK;

@@ -146,12 +146,24 @@ def test_apply_K(pair):
 
 # ------------------------------------------------------------------ a9: PCG protocol
 def test_pcg_one_step(pair):
-    """One iteration from the same state on both sides; the
-    GPU uses its own setup, the oracle its own: <= 1e-12 on every vector.  Runs on every
-    case, indefinite K_w included: one step is one K apply, two dot products and axpys."""
+    """One iteration from the same state on both sides: <= 1e-12 on
+    every vector.  Runs on every case, indefinite K_w included: one step is one K apply,
+    two dot products and axpys.  Definite cases: each side uses its own setup.  Where the
+    lumped masses change sign (R9) the Jacobi diagonal sum_(c,a) B^2 X cancels and its
+    near-zero entries amplify setup rounding without bound, so there the oracle step takes
+    the GPU's X and diag K (both compared on their own in test_lumped_and_jacobi) and the
+    bound carries the cancellation factors of <p, K p> and <r, Minv r>."""
     ctx, o, st = pair.ctx, pair.o, pair.ost
     rng = np.random.default_rng(7)
-    for side, X, dk in ((0, st["Cinv"], st["diagKl"]), (1, st["Dinv"], st["diagKr"])):
+    indef = bool(st["n_nonpos_Cw"] or st["n_nonpos_Dw"])
+    if indef:
+        Cg, Dg, Cig, Dig, dlg, drg = (empty(n) for n in (ctx.n_nodes,) * 4 + (ctx.n_p,) * 2)
+        ctx.get_lumped(Cg, Dg, Cig, Dig)
+        ctx.get_jacobi(dlg, drg)
+        sides = ((0, host(Cig), host(dlg)), (1, host(Dig), host(drg)))
+    else:
+        sides = ((0, st["Cinv"], st["diagKl"]), (1, st["Dinv"], st["diagKr"]))
+    for side, X, dk in sides:
         x, r, p = (o.project(rng.uniform(-1, 1, o.n_p)) for _ in range(3))
         keep = np.abs(dk) > 1e-13 * np.abs(dk).max()  # DESIGN.md R11 (pseudo-inverse of diag K)
         minv = np.where(keep, 1.0 / np.where(keep, dk, 1.0), 0.0)
@@ -159,10 +171,15 @@ def test_pcg_one_step(pair):
         xg, rg, pg = dev(x), dev(r), dev(p)
         rzg = ctx.debug_pcg_step(side, xg, rg, pg, rz)
         xo, ro, po, rzo = o.pcg_step(X, dk, x, r, p, rz)
-        assert rel_l2(host(xg), xo) <= 1e-12
-        assert rel_l2(host(rg), ro) <= 1e-12
-        assert rel_l2(host(pg), po) <= 1e-12
-        assert abs(rzg - rzo) <= 1e-12 * abs(rzo)
+        k_rz, k_pq = 1.0, 1.0
+        if indef:
+            qo = o.apply_K(X, p)
+            k_pq = max(1.0, float(np.sum(np.abs(p * qo)) / abs(float(p @ qo))))
+            k_rz = max(1.0, float(np.sum(np.abs(ro * minv * ro)) / abs(float(ro @ (minv * ro)))))
+        assert rel_l2(host(xg), xo) <= 1e-12 * k_pq
+        assert rel_l2(host(rg), ro) <= 1e-12 * k_pq
+        assert rel_l2(host(pg), po) <= 1e-12 * max(k_pq, k_rz)
+        assert abs(rzg - rzo) <= 1e-12 * max(k_pq, k_rz) * abs(rzo)
 
 
 @pytest.mark.parametrize("iters", [0, 1, 5, 10, 20])
@@ -181,12 +198,17 @@ def test_pcg_prefix(pair, iters):
 
 # ------------------------------------------------------------------ a10
 def self_discrepancy(o, r, iters, seed=11, zo=None):
-    """Oracle vs itself with a 1-ulp perturbation of half the input entries:
-    the fixed-iteration CG's own roundoff sensitivity."""
-    rng = np.random.default_rng(seed)
-    flip = rng.random(len(r)) < 0.5
-    rp = np.where(flip, np.nextafter(r, np.where(rng.random(len(r)) < 0.5, np.inf, -np.inf)), r)
-    return rel_l2(o.wbfbt(rp, iters), o.wbfbt(r, iters) if zo is None else zo)
+    """delta_self: the oracle against itself with reversed element
+    (scatter-add) and dot-product order -- the same arithmetic in another rounding order,
+    i.e. how far the fixed-iteration CG amplifies summation-order rounding alone.  `seed`
+    is unused (kept for call compatibility)."""
+    from oracle import Oracle
+    Oracle.set_order(True)
+    try:
+        zr = o.wbfbt(r, iters)
+    finally:
+        Oracle.set_order(False)
+    return rel_l2(zr, o.wbfbt(r, iters) if zo is None else zo)
 
 
 def test_wbfbt_free_running(pair):
