@@ -7,7 +7,7 @@ coefficient (multi-sinker viscosity, Sec. 2.1) sampled at
 the points where the library expects it, and U(-1,1) vectors.
 """
 from .multisinker import (CONFIGS, Config, sizes, gauss_points_1d, sinker_centers,
-                          chi, viscosity, viscosity_at_quadrature, make_inputs)
+                          chi, viscosity, viscosity_at_quadrature, forcing_at_quadrature, make_inputs)
 
 __all__ = ["CONFIGS", "Config", "sizes", "gauss_points_1d", "sinker_centers", "chi",
-           "viscosity", "viscosity_at_quadrature", "make_inputs"]
+           "viscosity", "viscosity_at_quadrature", "forcing_at_quadrature", "make_inputs"]

@@ -111,6 +111,27 @@ def viscosity_at_quadrature(N: int, k: int, centers: np.ndarray, delta: float, o
     return out.reshape(-1)
 
 
+def forcing_at_quadrature(N: int, k: int, centers: np.ndarray, delta: float, omega: float,
+                          beta: float = 10.0, chunk: int = 4096) -> np.ndarray:
+    """Body force f(x) = (0, 0, beta (chi_n(x) - 1)), beta = 10 (the
+    right-hand side of eq:discrete-stokes), sampled at every element's Gauss points:
+    component-major [c][e][q] (the layout of mu_q per component)."""
+    n1 = k + 1
+    h = 1.0 / N
+    xi = gauss_points_1d(k)
+    qz, qy, qx = np.meshgrid(np.arange(n1), np.arange(n1), np.arange(n1), indexing="ij")
+    loc = np.stack([(xi[qx.ravel()] + 1) / 2, (xi[qy.ravel()] + 1) / 2, (xi[qz.ravel()] + 1) / 2], -1)
+    n_el = N ** 3
+    out = np.zeros((3, n_el, n1 ** 3), dtype=np.float64)
+    for e0 in range(0, n_el, chunk):
+        e = np.arange(e0, min(e0 + chunk, n_el))
+        ex, ey, ez = e % N, (e // N) % N, e // (N * N)
+        base = np.stack([ex, ey, ez], -1).astype(np.float64)
+        x = h * (base[:, None, :] + loc[None, :, :])
+        out[2, e0:e0 + len(e)] = beta * (chi(x, centers, delta, omega) - 1.0)
+    return out.reshape(-1)
+
+
 def make_inputs(cfg: Config | str, seed: int = 0, *, N: int | None = None) -> dict:
     """All seeded inputs of one config: centres, mu_q, u, p (numpy fp64).
 
