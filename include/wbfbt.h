@@ -141,6 +141,31 @@ wb_status wb_poisson_eigmax(wb_ctx* ctx, int side, const double* v0, int iters, 
  * "inner" reads the choice. */
 wb_status wb_set_inner_cheb(wb_ctx* ctx, double lmin_l, double lmax_l, double lmin_r, double lmax_r);
 
+/* ---- Schur-complement variants beside wBFBT, on the same kernels.
+ * wb_set_schur selects the S~^-1 of the Stokes preconditioner (wb_stokes_fgmres):
+ * 0 = wBFBT (default, eq:wbfbt); 1 = diag(A)-BFBT (C = D = diag(A));
+ * 2 = M_p(1/mu)^-1, applied exactly per element (reading R21: the
+ * eq:lumping diagonal degenerates in the orthonormal modal basis R2).  Kind 2 builds its
+ * element blocks in wb_set_viscosity, so select it before that call.  WB_EINVAL otherwise. */
+wb_status wb_set_schur(wb_ctx* ctx, int kind);
+/* z = (B X B^T)^-1 (B X A X B^T) (B X B^T)^-1 r with X = mask / diag(A) (per DOF), both
+ * Poisson inverses by Jacobi-PCG (O9, `iters` iterations, pseudo-inverse diagonal R11), input
+ * and output projected (R10).  r, z: device, element-major n_p.  Asynchronous.  WB_ESTATE
+ * before wb_set_viscosity; WB_EINVAL; WB_EALIAS. */
+wb_status wb_apply_dabfbt(wb_ctx* ctx, const double* r, double* z, int iters);
+/* z = M_p(1/mu)^-1 r, M_p[i][j] = int q_i q_j / mu per element (Gauss quadrature of R3; the
+ * blocks are inverted by Cholesky in wb_set_viscosity).  WB_ESTATE unless kind 2 was selected
+ * before wb_set_viscosity. */
+wb_status wb_apply_mpinv(wb_ctx* ctx, const double* r, double* z);
+
+/* Load vector of a body force (the multi-sinker forcing
+ * f = (0, 0, beta (chi_n - 1)), beta = 10, the right-hand side of
+ * eq:discrete-stokes): F[(c, g)] = sum_e sum_q w_q detJ f_c(x_q) phi_a(xi_q), Dirichlet rows
+ * 0 (R6).  fq: device, 3 x n_el x n_q, component-major, per element its Gauss points
+ * (q x fastest, the layout of mu_q); F: device, n_v (SoA).  Asynchronous; does not need
+ * wb_set_viscosity.  WB_EINVAL (null), WB_EALIAS. */
+wb_status wb_load_vector(wb_ctx* ctx, const double* fq, double* F);
+
 /* ---- Geometric pressure multigrid for K_w (second half; PAPER.md:2468-2546,
  * Sec. "Parallel hybrid spectral-geometric-algebraic multigrid (HMG) for wBFBT"; reading R20
  * of DESIGN.md).  k = 2 only.  Levels N, N/2, ... while N is even and > 1 (uniform element

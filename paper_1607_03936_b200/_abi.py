@@ -45,6 +45,10 @@ SYMBOLS = [
     ("wb_poisson_eigmax", _i, [_vp, _i, _vp, _i, C.POINTER(_d)]),
     ("wb_get_diagA", _i, [_vp, _vp]),
     ("wb_set_inner_cheb", _i, [_vp, _d, _d, _d, _d]),
+    ("wb_set_schur", _i, [_vp, _i]),
+    ("wb_apply_dabfbt", _i, [_vp, _vp, _vp, _i]),
+    ("wb_apply_mpinv", _i, [_vp, _vp, _vp]),
+    ("wb_load_vector", _i, [_vp, _vp, _vp]),
     ("wb_setup_mg", _i, [_vp, _i]),
     ("wb_mg_vcycle", _i, [_vp, _i, _vp, _vp]),
     ("wb_poisson_mgcg", _i, [_vp, _i, _vp, _vp, _i]),
@@ -238,6 +242,23 @@ class Context:
 
     def set_inner_cheb(self, lmin_l=0.0, lmax_l=0.0, lmin_r=0.0, lmax_r=0.0):
         self._check(self._L.wb_set_inner_cheb(self._h, float(lmin_l), float(lmax_l), float(lmin_r), float(lmax_r)))
+
+    # -- Schur-complement variants
+    def set_schur(self, kind: int):
+        self._check(self._L.wb_set_schur(self._h, int(kind)))
+
+    def apply_dabfbt(self, r, z, iters: int):
+        self._check(self._L.wb_apply_dabfbt(self._h, _ptr(r, self.n_p), _ptr(z, self.n_p), int(iters)))
+        return z
+
+    def apply_mpinv(self, r, z):
+        self._check(self._L.wb_apply_mpinv(self._h, _ptr(r, self.n_p), _ptr(z, self.n_p)))
+        return z
+
+    # -- load vector of a body force sampled at the Gauss points
+    def load_vector(self, fq, F):
+        self._check(self._L.wb_load_vector(self._h, _ptr(fq, 3 * self.n_el * self.n_q), _ptr(F, self.n_v)))
+        return F
 
     # -- geometric pressure multigrid (R20)
     def setup_mg(self, nu: int = 3):

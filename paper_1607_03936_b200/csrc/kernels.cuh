@@ -874,6 +874,51 @@ __global__ void k_lump_node(const double* __restrict__ L, double a_l, double a_r
   if (!b && cr <= 0.0) atomicAdd(nonpos + 1, 1ull);
 }
 
+// Load vector of a body force sampled at the Gauss points (the multi-sinker
+// forcing f = (0, 0, beta (chi - 1))):
+//   F[(c, g)] = sum_{e ni g} sum_q w_q detJ f_c(e, q) phi_a(xi_q),  elements ascending,
+// Dirichlet rows 0 (elimination, R6).  fq: component-major [c][e][q] (q x fastest).
+template <int K>
+__global__ void k_load_node(const double* __restrict__ fq, double* __restrict__ F, Geo G, double detJ) {
+  constexpr int n1 = K + 1, NQ = Ord<K>::NQ;
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G.n_nodes) return;
+  const int nn1 = G.nn1;
+  int gg[3] = {(int)(g % nn1), (int)((g / nn1) % nn1), (int)(g / ((int64_t)nn1 * nn1))};
+  if (node_bnd(gg[0], gg[1], gg[2], nn1)) {
+    F[g] = 0.0; F[G.n_nodes + g] = 0.0; F[2 * G.n_nodes + g] = 0.0;
+    return;
+  }
+  int pe[3][2], pa[3][2], pc[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    int q = gg[d] / K, r = gg[d] % K;
+    pc[d] = 0;
+    if (r != 0) { pe[d][0] = q; pa[d][0] = r; pc[d] = 1; }
+    else {
+      if (q - 1 >= 0) { pe[d][pc[d]] = q - 1; pa[d][pc[d]] = K; pc[d]++; }
+      if (q < G.N) { pe[d][pc[d]] = q; pa[d][pc[d]] = 0; pc[d]++; }
+    }
+  }
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int iz = 0; iz < pc[2]; ++iz)
+    for (int iy = 0; iy < pc[1]; ++iy)
+      for (int ix = 0; ix < pc[0]; ++ix) {
+        const int64_t e = pe[0][ix] + (int64_t)G.N * (pe[1][iy] + (int64_t)G.N * pe[2][iz]);
+        const int ax = pa[0][ix], ay = pa[1][iy], az = pa[2][iz];
+        for (int c = 0; c < 3; ++c) {
+          const double* f = fq + ((int64_t)c * G.n_el + e) * NQ;
+          double s = 0.0;
+          for (int q = 0; q < NQ; ++q) {
+            const int qx = q % n1, qy = (q / n1) % n1, qz = q / (n1 * n1);
+            s = fma(f[q], TB(K).W1[ax][qx] * TB(K).W1[ay][qy] * TB(K).W1[az][qz], s);
+          }
+          acc[c] += detJ * s;
+        }
+      }
+  F[g] = acc[0]; F[G.n_nodes + g] = acc[1]; F[2 * G.n_nodes + g] = acc[2];
+}
+
 // ------------------------------------------------------------------ row a4: Jacobi diagonals
 // diag(K)_{e,m} = sum_{c,a} B_e[m,(c,a)]^2 X^-1[g(e,a)]; stores Minv = 1/diag too.
 template <int K>

@@ -109,5 +109,6 @@ __global__ void __launch_bounds__(256) k_BT_node2(const double* __restrict__ p, 
 #include "k2_tma.cuh"
 #include "k2_zm.cuh"
 #include "k2_mg.cuh"
+#include "k_schur.cuh"
 #include "k2_bbt.cuh"
 #include "k2_setup.cuh"

@@ -22,6 +22,7 @@ struct Tab {
   double BI[MAXN1][MAXN1];  // BI[m][a] = sum_i w_i Lhat_m(xg_i) phi_a(xg_i)
   double BD[MAXN1][MAXN1];  // BD[m][a] = sum_i w_i Lhat_m(xg_i) phi_a'(xg_i)
   double W1[MAXN1][MAXN1];  // W1[a][i] = phi_a(xg_i) w_i   (lumped mass, 1-D factor)
+  double LG[MAXN1][MAXN1];  // LG[m][i] = Lhat_m(xg_i)      (pressure modes at the Gauss points)
 };
 
 // Closed-form node sets.
@@ -117,6 +118,8 @@ inline Tab make_tab(int k) {
     }
   for (int a = 0; a < n1; ++a)
     for (int i = 0; i < n1; ++i) T.W1[a][i] = (double)(I[i][a] * wg[i]);
+  for (int m = 0; m < k; ++m)
+    for (int i = 0; i < n1; ++i) T.LG[m][i] = (double)lhat(m, xg[i]);
   return T;
 }
 

@@ -118,6 +118,15 @@ struct wb_ctx {
   std::vector<cudaGraphExec_t> prof_execs;  // the profiled loops' graphs
   long long launches = 0;
   struct MGH* mg = nullptr;  // pressure multigrid hierarchy (R20), built by wb_setup_mg
+  // Schur-complement variant of the Stokes preconditioner: 0 = wBFBT,
+  // 1 = diag(A)-BFBT, 2 = M_p(1/mu)^-1 element blocks (R21, built in
+  // wb_set_viscosity when selected)
+  int schur = 0;
+  bool dab_valid = false, mp_valid = false;
+  double *dKd = nullptr, *mKd = nullptr, *dv = nullptr;                       // diag(A)-BFBT Poisson
+  double *gp_r = nullptr, *gp_z = nullptr, *gp_p = nullptr, *gp_q = nullptr, *gp_x = nullptr,
+         *gp_y = nullptr, *gp_s = nullptr;                                    // its PCG (element-major)
+  double* mpinv = nullptr;                                                   // n_el x n_m^2
   char err[512] = {0};
 };
 
@@ -924,6 +933,105 @@ wb_status run_wbfbt(wb_ctx* c, const double* r, double* z, int iters) {
   return run_inner(c, 0, c->s2, z, iters);
 }
 
+wb_status dev_dot(wb_ctx* c, const double* a, const double* b, int64_t n, double* out_dev) {
+  k_dot_dev<<<c->red_blocks, VBS, 0, c->stream>>>(a, b, n, c->partial, c->counter, out_dev);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+// ---- diag(A)-BFBT: C = D = diag(A), a per-DOF weight
+// X = mask / diag(A); its Poisson operator K_d = B X B^T runs through the generic B^T / B
+// kernels (element-major vectors) and its inverse is the O9 Jacobi-PCG with device scalars.
+wb_status ensure_dab(wb_ctx* c) {
+  if (c->dab_valid) return WB_OK;
+  wb_status s = ensure_dAinv(c);
+  if (s) return s;
+  for (double** b : {&c->dKd, &c->mKd, &c->gp_r, &c->gp_z, &c->gp_p, &c->gp_q, &c->gp_x, &c->gp_y})
+    if (!lazy_alloc(b, c->n_p)) return set_err(c, WB_ENOMEM, "diag(A)-BFBT allocation failed");
+  if (!lazy_alloc(&c->dv, c->n_v) || !lazy_alloc(&c->gp_s, 4)) return set_err(c, WB_ENOMEM, "allocation failed");
+  const unsigned nb = nblk(c->n_el, 128);
+  switch (c->k) {
+    case 2: k_jacobi_dof<2><<<nb, 128, 0, c->stream>>>(c->dAinv, c->dKd, c->G, c->sB); break;
+    case 3: k_jacobi_dof<3><<<nb, 128, 0, c->stream>>>(c->dAinv, c->dKd, c->G, c->sB); break;
+    default: k_jacobi_dof<4><<<nb, 128, 0, c->stream>>>(c->dAinv, c->dKd, c->G, c->sB); break;
+  }
+  LAUNCH_CHECK(c);
+  double* dmax = c->scal + S_SCR + 2;
+  k_absmax<VBS><<<c->red_blocks, VBS, 0, c->stream>>>(c->dKd, c->n_p, c->partial, c->counter, dmax);
+  LAUNCH_CHECK(c);
+  k_pinv_diag<<<stream_blocks(c->n_p), VBS, 0, c->stream>>>(c->dKd, c->mKd, c->n_p, dmax);
+  LAUNCH_CHECK(c);
+  c->dab_valid = true;
+  return WB_OK;
+}
+// q = B (X o B^T p), element-major, X = mask / diag(A) per DOF
+wb_status run_Kd(wb_ctx* c, const double* p, double* q) {
+  wb_status s = run_BT(c, p, nullptr, c->dv, 0, nullptr, c->nm, 1);
+  if (s) return s;
+  k_mul<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->dv, c->dv, c->dAinv, c->n_v);
+  LAUNCH_CHECK(c);
+  return run_B(c, c->dv, nullptr, q, 0, nullptr, nullptr, nullptr, c->nm, 1);
+}
+static wb_status em_project(wb_ctx* c, double* v) {  // R10 on an element-major vector
+  k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(v, c->n_el, c->nm, c->partial, c->counter, c->scal + S_SCR + 3);
+  LAUNCH_CHECK(c);
+  k_sub_mode0_mean<<<stream_blocks(c->n_el), VBS, 0, c->stream>>>(v, c->n_el, c->nm, c->scal + S_SCR + 3);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+// x = P PCG(K_d, P b), O9 with Minv = pinv(diag K_d), exactly iters iterations
+wb_status run_dpcg(wb_ctx* c, const double* b, double* x, int iters) {
+  const int64_t n = c->n_p;
+  const unsigned nb = stream_blocks(n);
+  CUDA_TRY(c, cudaMemcpyAsync(c->gp_r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  wb_status s = em_project(c, c->gp_r);
+  if (s) return s;
+  CUDA_TRY(c, cudaMemsetAsync(c->gp_x, 0, sizeof(double) * n, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->gp_s, 0, sizeof(double) * 4, c->stream));
+  k_mul<<<nb, VBS, 0, c->stream>>>(c->gp_z, c->gp_r, c->mKd, n);
+  LAUNCH_CHECK(c);
+  CUDA_TRY(c, cudaMemcpyAsync(c->gp_p, c->gp_z, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  if ((s = dev_dot(c, c->gp_r, c->gp_z, n, c->gp_s))) return s;
+  for (int it = 0; it < iters; ++it) {
+    if ((s = run_Kd(c, c->gp_p, c->gp_q))) return s;
+    if ((s = dev_dot(c, c->gp_p, c->gp_q, n, c->gp_s + 1))) return s;
+    k_mgcg_xr<<<nb, VBS, 0, c->stream>>>(c->gp_x, c->gp_r, c->gp_p, c->gp_q, n, c->gp_s);
+    LAUNCH_CHECK(c);
+    k_mul<<<nb, VBS, 0, c->stream>>>(c->gp_z, c->gp_r, c->mKd, n);
+    LAUNCH_CHECK(c);
+    if ((s = dev_dot(c, c->gp_r, c->gp_z, n, c->gp_s + 2))) return s;
+    k_mgcg_p<<<nb, VBS, 0, c->stream>>>(c->gp_p, c->gp_z, n, c->gp_s, c->counter + 3);
+    LAUNCH_CHECK(c);
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(x, c->gp_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  return em_project(c, x);
+}
+// z = (B X B^T)^-1 (B X A X B^T) (B X B^T)^-1 r, X = mask / diag(A), O10 order
+wb_status run_dabfbt(wb_ctx* c, const double* r, double* z, int iters) {
+  wb_status s = ensure_dab(c);
+  if (s) return s;
+  if ((s = run_dpcg(c, r, c->gp_y, iters))) return s;
+  if ((s = run_BT(c, c->gp_y, nullptr, c->tw, 0, nullptr, c->nm, 1))) return s;
+  k_mul<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->tw, c->tw, c->dAinv, c->n_v);
+  LAUNCH_CHECK(c);
+  if ((s = run_A(c, c->tw, c->tv, 0))) return s;
+  k_mul<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->tv, c->tv, c->dAinv, c->n_v);
+  LAUNCH_CHECK(c);
+  if ((s = run_B(c, c->tv, nullptr, c->gp_y, 0, nullptr, nullptr, nullptr, c->nm, 1))) return s;
+  return run_dpcg(c, c->gp_y, z, iters);  // (run_dpcg projects its input)
+}
+// z = scale M_p(1/mu)^-1 r, element blocks (R21)
+wb_status run_mpinv(wb_ctx* c, const double* r, double* z, double scale) {
+  if (!c->mp_valid) return set_err(c, WB_ESTATE, "M_p(1/mu) blocks not built: wb_set_schur(ctx, 2) before wb_set_viscosity");
+  const unsigned nb = nblk(c->n_el, 128);
+  switch (c->nm) {
+    case 4: k_mp_apply<4><<<nb, 128, 0, c->stream>>>(c->mpinv, r, z, c->n_el, scale); break;
+    case 10: k_mp_apply<10><<<nb, 128, 0, c->stream>>>(c->mpinv, r, z, c->n_el, scale); break;
+    default: k_mp_apply<20><<<nb, 128, 0, c->stream>>>(c->mpinv, r, z, c->n_el, scale); break;
+  }
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+
 // ---- Stokes solve (R19): flexible GMRES on [A B^T; B 0] with P^-1 (a; b) =
 // (At^-1 (a - B^T y); y), y = -wBFBT(b), At^-1 = the smoother on A.  Vectors are [u | p],
 // p element-major.  The Gram-Schmidt scalars stay on the device (k_dot_dev / k_axpy_dev);
@@ -940,18 +1048,18 @@ wb_status stokes_K(wb_ctx* c, const double* x, double* y) {
 wb_status stokes_P(wb_ctx* c, const double* v, double* z, const StokesPar& P) {
   wb_status s;
   double* y = z + c->n_v;
-  if ((s = run_wbfbt(c, v + c->n_v, y, P.pcg))) return s;
-  k_axpby<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(y, y, c->n_p, 0.0, -1.0);  // y = -wBFBT(b)
-  LAUNCH_CHECK(c);
+  // y = -S~^-1 b: wBFBT (default), diag(A)-BFBT or M_p(1/mu)^-1
+  if (c->schur == 2) {
+    if ((s = run_mpinv(c, v + c->n_v, y, -1.0))) return s;
+  } else {
+    if ((s = c->schur == 1 ? run_dabfbt(c, v + c->n_v, y, P.pcg) : run_wbfbt(c, v + c->n_v, y, P.pcg))) return s;
+    k_axpby<<<stream_blocks(c->n_p), VBS, 0, c->stream>>>(y, y, c->n_p, 0.0, -1.0);
+    LAUNCH_CHECK(c);
+  }
   if ((s = run_BT(c, y, nullptr, c->gsa, 0, nullptr, c->nm, 1))) return s;
   k_axpby<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->gsa, v, c->n_v, 1.0, -1.0);  // a - B^T y
   LAUNCH_CHECK(c);
   return run_vcheb(c, c->gsa, z, P.sm, P.lo, P.hi);
-}
-wb_status dev_dot(wb_ctx* c, const double* a, const double* b, int64_t n, double* out_dev) {
-  k_dot_dev<<<c->red_blocks, VBS, 0, c->stream>>>(a, b, n, c->partial, c->counter, out_dev);
-  LAUNCH_CHECK(c);
-  return WB_OK;
 }
 wb_status host_scalar(wb_ctx* c, const double* dev, double* h) {
   CUDA_TRY(c, cudaMemcpyAsync(h, dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -1062,7 +1170,8 @@ wb_status check_ctx(wb_ctx* c, bool need_visc) {
 
 void free_all(wb_ctx* c) {
   mg_free(c);
-  double** bufs[] = {&c->mut, &c->Cw, &c->Dw, &c->Cinv, &c->Dinv, &c->dKl, &c->dKr, &c->MinvL, &c->MinvR,
+  double** bufs[] = {&c->dKd, &c->mKd, &c->dv, &c->gp_r, &c->gp_z, &c->gp_p, &c->gp_q, &c->gp_x, &c->gp_y,
+                     &c->gp_s, &c->mpinv, &c->mut, &c->Cw, &c->Dw, &c->Cinv, &c->Dinv, &c->dKl, &c->dKr, &c->MinvL, &c->MinvR,
                      &c->E, &c->tv, &c->tw, &c->px, &c->pr, &c->pp, &c->pp1, &c->pq, &c->pz, &c->s0, &c->s1, &c->s2,
                      &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->Fu, &c->mueff,
                      &c->E3, &c->dAinv, &c->tq, &c->gV, &c->gZ, &c->gw, &c->gb, &c->gx, &c->gsa, &c->gh};
@@ -1317,6 +1426,8 @@ static wb_status finish_lumped(wb_ctx* c);
 template <int K>
 static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
   mg_free(c);  // a multigrid hierarchy belongs to the previous viscosity
+  c->dab_valid = false;
+  c->mp_valid = false;
   const int64_t nmu = c->n_el * c->nq;
   CUDA_TRY(c, cudaMemsetAsync(c->icount, 0, sizeof(unsigned long long) * 4, c->stream));
   c->dA_valid = false;
@@ -1343,6 +1454,12 @@ static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
   if (bad) {
     c->have_visc = false;
     return set_err(c, WB_ENONPOS_MU, "%llu viscosity samples are <= 0 or non-finite", bad);
+  }
+  if (c->schur == 2) {  // M_p(1/mu)^-1 element blocks (R21)
+    if (!lazy_alloc(&c->mpinv, c->n_el * c->nm * c->nm)) return set_err(c, WB_ENOMEM, "M_p allocation failed");
+    k_mp_setup<K><<<nblk(c->n_el, 64), 64, 0, c->stream>>>(mu, c->mpinv, c->n_el, c->detJ);
+    LAUNCH_CHECK(c);
+    c->mp_valid = true;
   }
   // lumped masses: element part into E (1 component; k = 2: by k_setup_mu2), node gather
   if constexpr (K == 2) {
@@ -1664,6 +1781,45 @@ wb_status wb_set_inner_cheb(wb_ctx* c, double lmin_l, double lmax_l, double lmin
       return set_err(c, WB_EINVAL, "each interval must satisfy 0 < lmin < lmax < inf (or all four 0)");
   for (int i = 0; i < 2; ++i) { c->cheb_lo[i] = lo[i]; c->cheb_hi[i] = hi[i]; }
   c->inner = 1;
+  return WB_OK;
+}
+
+wb_status wb_set_schur(wb_ctx* c, int kind) {
+  if (!c) return WB_EINVAL;
+  if (kind < 0 || kind > 2) return set_err(c, WB_EINVAL, "kind must be 0 (wBFBT), 1 (diag(A)-BFBT) or 2 (M_p)");
+  c->schur = kind;
+  return WB_OK;
+}
+
+wb_status wb_apply_dabfbt(wb_ctx* c, const double* r, double* z, int iters) {
+  wb_status s = check_ctx(c, true);
+  if (s) return s;
+  if (!r || !z || iters < 0) return set_err(c, WB_EINVAL, "bad argument");
+  const size_t bp = sizeof(double) * c->n_p;
+  if (overlaps(r, bp, z, bp)) return set_err(c, WB_EALIAS, "r and z overlap");
+  return run_dabfbt(c, r, z, iters);
+}
+
+wb_status wb_apply_mpinv(wb_ctx* c, const double* r, double* z) {
+  wb_status s = check_ctx(c, true);
+  if (s) return s;
+  if (!r || !z) return set_err(c, WB_EINVAL, "bad argument");
+  const size_t bp = sizeof(double) * c->n_p;
+  if (overlaps(r, bp, z, bp)) return set_err(c, WB_EALIAS, "r and z overlap");
+  return run_mpinv(c, r, z, 1.0);
+}
+
+wb_status wb_load_vector(wb_ctx* c, const double* fq, double* F) {
+  if (!c || !fq || !F) return c ? set_err(c, WB_EINVAL, "null pointer") : WB_EINVAL;
+  if (overlaps(fq, sizeof(double) * 3 * c->n_el * c->nq, F, sizeof(double) * c->n_v))
+    return set_err(c, WB_EALIAS, "fq and F overlap");
+  const unsigned nb = nblk(c->n_nodes, 128);
+  switch (c->k) {
+    case 2: k_load_node<2><<<nb, 128, 0, c->stream>>>(fq, F, c->G, c->detJ); break;
+    case 3: k_load_node<3><<<nb, 128, 0, c->stream>>>(fq, F, c->G, c->detJ); break;
+    default: k_load_node<4><<<nb, 128, 0, c->stream>>>(fq, F, c->G, c->detJ); break;
+  }
+  LAUNCH_CHECK(c);
   return WB_OK;
 }
 
