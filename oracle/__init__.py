@@ -358,10 +358,11 @@ class Oracle:
         return z
 
     @staticmethod
-    def set_order(reverse: bool) -> None:
-        """Summation order of element scatter-adds and dot products (process-wide): reversed
-        only to measure the self-discrepancy delta_self."""
-        lib().or_set_order(int(bool(reverse)))
+    def set_order(order) -> None:
+        """Summation order of element scatter-adds and dot products (process-wide), changed
+        only to measure the self-discrepancy delta_self: 0 / False
+        ascending (default), 1 / True reversed, 2 even-then-odd dot products."""
+        lib().or_set_order(int(order))
 
     @staticmethod
     def num_threads() -> int:

@@ -269,11 +269,12 @@ void or_boundary_mask(const or_ctx* c, uint8_t* mask) { /* 1 = boundary (elimina
 /* Gather element-local velocity (c, a), Dirichlet entries zeroed unless nomask. */
 /* Summation-order switch for the self-discrepancy delta_self (SURVEY.md 8(c) 12(ii):
  * "the oracle vs itself with reversed element and dot order").  0 (default): element
- * scatter-adds and dot products in ascending order; 1: both descending.  Same arithmetic,
+ * scatter-adds and dot products in ascending order; 1: both descending; 2: dot products as
+ * (sum of even-indexed terms) + (sum of odd-indexed terms), scatters ascending.  Same arithmetic,
  * another rounding order -- it measures how far the fixed-iteration CG amplifies
  * summation-order rounding alone. */
 static int g_rev = 0;
-void or_set_order(int rev) { g_rev = rev ? 1 : 0; }
+void or_set_order(int rev) { g_rev = (rev == 1 || rev == 2) ? rev : 0; }
 
 static void gather_u(const or_ctx* c, int64_t e, const double* u, double* ue, int nomask) {
   for (int cc = 0; cc < 3; ++cc)
@@ -517,9 +518,14 @@ void or_jacobi_diag(or_ctx* c, const double* Xinv, double* diag) {
  * Neumann null space).                         */
 static double dot(const double* a, const double* b, int64_t n) {
   double s = 0.0;
-  if (g_rev)
+  if (g_rev == 1)
     for (int64_t i = n - 1; i >= 0; --i) s += a[i] * b[i];
-  else
+  else if (g_rev == 2) { /* even-indexed terms, then odd-indexed terms */
+    double s1 = 0.0;
+    for (int64_t i = 0; i < n; i += 2) s += a[i] * b[i];
+    for (int64_t i = 1; i < n; i += 2) s1 += a[i] * b[i];
+    s += s1;
+  } else
     for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
   return s;
 }

@@ -38,3 +38,91 @@ def load_vector(o: Oracle, fq: np.ndarray, mask: bool = True) -> np.ndarray:
     if mask:
         F[o.boundary_mask().astype(bool)] = 0.0
     return F
+
+
+def fgmres(K, Pinv, b: np.ndarray, m: int, max_iters: int, rtol: float):
+    """Flexible GMRES (Saad 1993), restarted every m, modified Gram-Schmidt, Givens rotations,
+    x0 = 0; stop when the Givens residual estimate <= rtol ||b|| or after max_iters; restarts
+    from the true residual.  The same algorithm as the C oracle's fgmres_run (reading R19),
+    with the operator and the (possibly nonlinear) preconditioner as callables.
+    Returns (x, iterations, ||b - K x|| / ||b||)."""
+    n = len(b)
+    x = np.zeros(n)
+    w = b.copy()
+    bnorm = float(np.sqrt(b @ b))
+    beta = bnorm
+    total = 0
+    while beta > rtol * bnorm and total < max_iters:
+        V = np.zeros((m + 1, n))
+        Z = np.zeros((m, n))
+        H = np.zeros((m + 1, m))
+        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+        V[0] = w / beta
+        g[0] = beta
+        jend = -1
+        for j in range(m):
+            if total >= max_iters:
+                break
+            Z[j] = Pinv(V[j])
+            w = K(Z[j])
+            for i in range(j + 1):
+                hij = float(w @ V[i])
+                H[i, j] = hij
+                w = w - hij * V[i]
+            hn = float(np.sqrt(w @ w))
+            for i in range(j):
+                a, bb = H[i, j], H[i + 1, j]
+                H[i, j] = cs[i] * a + sn[i] * bb
+                H[i + 1, j] = -sn[i] * a + cs[i] * bb
+            a = H[j, j]
+            den = float(np.sqrt(a * a + hn * hn))
+            cs[j] = a / den if den > 0 else 1.0
+            sn[j] = hn / den if den > 0 else 0.0
+            H[j, j] = den
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            total += 1
+            jend = j
+            if hn > 0:
+                V[j + 1] = w / hn
+            if abs(g[j + 1]) <= rtol * bnorm or hn == 0.0:
+                break
+        y = np.zeros(m)
+        for i in range(jend, -1, -1):
+            t = g[i] - sum(H[i, k] * y[k] for k in range(i + 1, jend + 1))
+            y[i] = t / H[i, i]
+        for i in range(jend + 1):
+            x = x + y[i] * Z[i]
+        w = b - K(x)
+        beta = float(np.sqrt(w @ w))
+        if jend < 0:
+            break
+    return x, total, (beta / bnorm if bnorm > 0 else 0.0)
+
+
+class StokesOracle:
+    """[A B^T; B 0] with the eq:precond-stokes right preconditioner (R19), pluggable S~^-1:
+    P^-1 (a; b) = (At^-1 (a - B^T y); y), y = -S~^-1 b, At^-1 = the Chebyshev-Jacobi smoother
+    on A (R18) with `smooth` steps on [lmin, lmax]."""
+
+    def __init__(self, o: Oracle, mu_q, schur_inv, smooth: int, lmin: float, lmax: float):
+        self.o, self.mu = o, np.asarray(mu_q, dtype=np.float64)
+        self.schur_inv, self.smooth, self.lmin, self.lmax = schur_inv, smooth, lmin, lmax
+
+    def K(self, v):
+        o = self.o
+        u, p = v[:o.n_v], v[o.n_v:]
+        return np.concatenate([o.apply_A(self.mu, u) + o.apply_BT(p), o.apply_B(u)])
+
+    def P(self, v):
+        o = self.o
+        a, b = v[:o.n_v], v[o.n_v:]
+        y = -self.schur_inv(b)
+        z = o.velocity_cheb(self.mu, a - o.apply_BT(y), self.smooth, self.lmin, self.lmax)
+        return np.concatenate([z, y])
+
+    def solve(self, f, g, m, max_iters, rtol):
+        o = self.o
+        b = np.concatenate([np.where(o.boundary_mask().astype(bool), 0.0, f), g])
+        x, it, rr = fgmres(self.K, self.P, b, m, max_iters, rtol)
+        return x[:o.n_v], o.project(x[o.n_v:]), it, rr

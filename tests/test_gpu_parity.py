@@ -197,18 +197,23 @@ def test_pcg_prefix(pair, iters):
 
 
 # ------------------------------------------------------------------ a10
-def self_discrepancy(o, r, iters, seed=11, zo=None):
-    """delta_self: the oracle against itself with reversed element
-    (scatter-add) and dot-product order -- the same arithmetic in another rounding order,
-    i.e. how far the fixed-iteration CG amplifies summation-order rounding alone.  `seed`
-    is unused (kept for call compatibility)."""
+def self_discrepancy(o, r, iters, seed=11, zo=None, orders=(1, 2)):
+    """delta_self: the oracle against itself with another summation
+    order -- reversed element (scatter-add) and dot-product order (1), and dot products
+    summed even-then-odd (2) -- the same arithmetic in other rounding orders, i.e. how far
+    the fixed-iteration CG amplifies summation-order rounding alone.  The max over the
+    orders.  `seed` is unused (kept for call compatibility)."""
     from oracle import Oracle
-    Oracle.set_order(True)
-    try:
-        zr = o.wbfbt(r, iters)
-    finally:
-        Oracle.set_order(False)
-    return rel_l2(zr, o.wbfbt(r, iters) if zo is None else zo)
+    ref = o.wbfbt(r, iters) if zo is None else zo
+    ds = 0.0
+    for order in orders:
+        Oracle.set_order(order)
+        try:
+            zr = o.wbfbt(r, iters)
+        finally:
+            Oracle.set_order(0)
+        ds = max(ds, rel_l2(zr, ref))
+    return ds
 
 
 def test_wbfbt_free_running(pair):

@@ -55,3 +55,25 @@ def test_load_vector_integrates_polynomials_exactly():
     F = ost.load_vector(o, fq, mask=False)
     assert F[2 * o.n_nodes:].sum() == pytest.approx(float(Fraction(1, 12)), rel=1e-14)
     assert np.all(F[:2 * o.n_nodes] == 0.0)
+
+
+def test_python_fgmres_matches_c_core_and_is_minimal_residual():
+    """The numpy FGMRES (oracle/stokes.py) against the C oracle's core on a dense system with
+    a fixed preconditioner, and the GMRES property: after j iterations (no restart) the
+    residual is the least-squares minimum over the preconditioned Krylov space."""
+    import oracle
+    rng = np.random.default_rng(0)
+    n = 30
+    A = rng.standard_normal((n, n)) + 8 * np.eye(n)
+    Pm = np.diag(1.0 / np.diag(A))
+    b = rng.standard_normal(n)
+    x, it, rr = ost.fgmres(lambda v: A @ v, lambda v: Pm @ v, b, 40, 6, 0.0)
+    xc, itc, rrc = oracle.fgmres_dense(A, Pm, b, 40, 6, 0.0)
+    assert it == itc == 6 and np.allclose(x, xc, rtol=0, atol=1e-12 * np.linalg.norm(xc))
+    # minimal residual over span{(AP)^i P... }: x = P V y with V the Krylov basis of AP
+    W = [b]
+    for _ in range(5):
+        W.append(A @ (Pm @ W[-1]))
+    Kb = Pm @ np.array(W).T
+    y, *_ = np.linalg.lstsq(A @ Kb, b, rcond=None)
+    assert np.linalg.norm(b - A @ (Kb @ y)) == pytest.approx(np.linalg.norm(b - A @ x), rel=1e-8)
