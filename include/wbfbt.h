@@ -177,10 +177,21 @@ wb_status wb_load_vector(wb_ctx* ctx, const double* fq, double* F);
  * [0.1, 1.1] x a 20-step power-iteration estimate (splitmix64 start vector); coarsest level:
  * Jacobi-PCG with min(n_p, 256) iterations. */
 /* Builds the hierarchy of both sides from the current C_w, D_w (after wb_set_viscosity; a
- * later wb_set_viscosity discards it).  nu in [1, 16] (the paper: 3).  Allocates one internal
- * context per coarse level and synchronises the stream.  WB_EINVAL for k != 2 or nu out of
- * range, WB_ESTATE before wb_set_viscosity, WB_ENOMEM. */
-wb_status wb_setup_mg(wb_ctx* ctx, int nu);
+ * later wb_set_viscosity discards it).  nu in [1, 16] (the paper: 3).  mu_q (device, the
+ * n_el x n_q viscosity given to wb_set_viscosity, or NULL): when given, the velocity
+ * hierarchy of A is built too (R22: mu coarsened level by level; A
+ * re-discretised; Q2 nodal interpolation and its transpose as transfers; the same smoother
+ * on A, R18).  Allocates one internal context per coarse level and synchronises the stream.
+ * WB_EINVAL for k != 2 or nu out of range, WB_ESTATE before wb_set_viscosity, WB_ENOMEM. */
+wb_status wb_setup_mg(wb_ctx* ctx, int nu, const double* mu_q);
+/* x = V(b), one velocity V-cycle on M A M (b, x: device SoA n_v; boundary entries of b are
+ * ignored, of x written 0).  WB_ESTATE without a velocity hierarchy. */
+wb_status wb_velocity_vcycle(wb_ctx* ctx, const double* b, double* x);
+/* From now on the Stokes preconditioner's At^-1 (eq:precond-stokes) is `cycles` stationary
+ * velocity V-cycles from x0 = 0 (the paper's choice: an HMG V-cycle)
+ * instead of the Chebyshev smoother; 0: back to the smoother.  WB_ESTATE without a
+ * velocity hierarchy. */
+wb_status wb_set_velocity_mg(wb_ctx* ctx, int cycles);
 /* x = V(b), one V-cycle on K_side (side 0 = l, 1 = r).  b, x: device, element-major n_p,
  * caller-owned; b should be projected (R10).  Asynchronous.  WB_ESTATE without a hierarchy,
  * WB_EINVAL, WB_EALIAS. */

@@ -223,3 +223,101 @@ def wbfbt_mg(o: Oracle, mu_q, state: dict, mg_l: MG, mg_r: MG, r: np.ndarray, it
     v = v * np.tile(state["Cinv"], 3)
     s = o.project(o.apply_B(v))
     return mg_l.pcg(s, iters)
+
+
+# ---------------------------------------------------------------- velocity multigrid (R22)
+def coarsen_mu(mu_f: np.ndarray, Nc: int, wg: np.ndarray) -> np.ndarray:
+    """mu at the coarse Gauss points: the mean, over the fine children whose closure contains
+    the point, of each child's Gauss-weighted mean sum_q w_q mu_q / sum_q w_q (k = 2; the
+    coarse abscissae -sqrt(3/5), 0, +sqrt(3/5) lie in child 0, on the face, in child 1)."""
+    Nf = 2 * Nc
+    w3 = np.array([wg[q % 3] * wg[(q // 3) % 3] * wg[q // 9] for q in range(27)])
+    m = (np.asarray(mu_f).reshape(Nf ** 3, 27) @ w3 / 8.0).reshape(Nc, 2, Nc, 2, Nc, 2)  # [cz][sz][cy][sy][cx][sx]
+    sets = [[0], [0, 1], [1]]
+    out = np.zeros((Nc, Nc, Nc, 27))
+    for q in range(27):
+        qx, qy, qz = q % 3, (q // 3) % 3, q // 9
+        vals = [m[:, sz, :, sy, :, sx] for sz in sets[qz] for sy in sets[qy] for sx in sets[qx]]
+        acc = vals[0].copy()
+        for v in vals[1:]:
+            acc = acc + v
+        out[..., q] = acc / len(vals)
+    return out.reshape(-1)
+
+
+def q2_prolongation_1d(Nc: int, xn: np.ndarray) -> np.ndarray:
+    """P[i_f, I]: coarse Q2 nodal basis (GLL nodes xn of the oracle) evaluated at the fine
+    nodes; fine element nodes sit at coarse-element coordinates -1, -1/2, 0, 1/2, 1."""
+    nc, nf = 2 * Nc + 1, 4 * Nc + 1
+    P = np.zeros((nf, nc))
+    for e in range(Nc):
+        for j, t in enumerate((-1.0, -0.5, 0.0, 0.5, 1.0)):
+            for a in range(3):
+                v = 1.0
+                for b in range(3):
+                    if b != a:
+                        v *= (t - xn[b]) / (xn[a] - xn[b])
+                P[4 * e + j, 2 * e + a] = v
+    return P
+
+
+def vprolong(P1: np.ndarray, xc: np.ndarray) -> np.ndarray:
+    nf, nc = P1.shape
+    out = [np.einsum("ai,bj,ck,ijk->abc", P1, P1, P1, xc[c * nc ** 3:(c + 1) * nc ** 3].reshape(nc, nc, nc)).ravel()
+           for c in range(3)]
+    return np.concatenate(out)
+
+
+def vrestrict(P1: np.ndarray, xf: np.ndarray) -> np.ndarray:
+    nf, nc = P1.shape
+    out = [np.einsum("ai,bj,ck,abc->ijk", P1, P1, P1, xf[c * nf ** 3:(c + 1) * nf ** 3].reshape(nf, nf, nf)).ravel()
+           for c in range(3)]
+    return np.concatenate(out)
+
+
+class VMG:
+    """V-cycle hierarchy of the masked viscous block M A M (R22): levels as the pressure
+    multigrid, A_l re-discretised with the coarsened mu, Q2 nodal transfers, nu Chebyshev-
+    Jacobi steps (R18) on [0.1, 1.1] x a 20-step power estimate (splitmix64 start), 30 on the
+    coarsest level."""
+
+    def __init__(self, N: int, mu_q: np.ndarray, nu: int = NU):
+        self.nu = nu
+        self.Ns = levels_of(N)
+        self.lev = []
+        mu = np.asarray(mu_q, dtype=np.float64)
+        for li, Nl in enumerate(self.Ns):
+            o = Oracle(Nl, 2)
+            if li > 0:
+                mu = coarsen_mu(mu, Nl, o.tables()["wg"])
+            lam = o.velocity_eigmax(mu, splitmix_vector(o.n_v), EIG_ITERS)
+            self.lev.append(dict(N=Nl, o=o, mu=mu, lam=lam, mask=o.boundary_mask().astype(bool)))
+        xn = self.lev[0]["o"].tables()["xn"]
+        self.P = [q2_prolongation_1d(self.Ns[l + 1], xn) for l in range(len(self.Ns) - 1)]
+
+    def A(self, l, v):
+        L = self.lev[l]
+        return L["o"].apply_A(L["mu"], v)
+
+    def smooth(self, l, b, its):
+        L = self.lev[l]
+        return L["o"].velocity_cheb(L["mu"], b, its, CHEB_LO * L["lam"], CHEB_HI * L["lam"])
+
+    def vcycle(self, b, l=0):
+        if l == len(self.lev) - 1:
+            return self.smooth(l, b, 30)
+        L = self.lev[l]
+        x = self.smooth(l, b, self.nu)
+        r = b - self.A(l, x)
+        rc = vrestrict(self.P[l], np.where(L["mask"], 0.0, r))  # Dirichlet rows carry no residual (R6)
+        rc[self.lev[l + 1]["mask"]] = 0.0
+        xc = self.vcycle(rc, l + 1)
+        x = x + np.where(L["mask"], 0.0, vprolong(self.P[l], xc))
+        r = b - self.A(l, x)
+        return x + self.smooth(l, r, self.nu)
+
+    def cycles(self, b, k):
+        x = self.vcycle(b)
+        for _ in range(1, k):
+            x = x + self.vcycle(b - self.A(0, x))
+        return x

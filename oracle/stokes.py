@@ -105,9 +105,10 @@ class StokesOracle:
     P^-1 (a; b) = (At^-1 (a - B^T y); y), y = -S~^-1 b, At^-1 = the Chebyshev-Jacobi smoother
     on A (R18) with `smooth` steps on [lmin, lmax]."""
 
-    def __init__(self, o: Oracle, mu_q, schur_inv, smooth: int, lmin: float, lmax: float):
+    def __init__(self, o: Oracle, mu_q, schur_inv, smooth: int, lmin: float, lmax: float, ainv=None):
         self.o, self.mu = o, np.asarray(mu_q, dtype=np.float64)
         self.schur_inv, self.smooth, self.lmin, self.lmax = schur_inv, smooth, lmin, lmax
+        self.ainv = ainv  # At^-1 callable (e.g. velocity V-cycles, R22); default the smoother (R18)
 
     def K(self, v):
         o = self.o
@@ -118,7 +119,10 @@ class StokesOracle:
         o = self.o
         a, b = v[:o.n_v], v[o.n_v:]
         y = -self.schur_inv(b)
-        z = o.velocity_cheb(self.mu, a - o.apply_BT(y), self.smooth, self.lmin, self.lmax)
+        if self.ainv is not None:
+            z = self.ainv(np.where(o.boundary_mask().astype(bool), 0.0, a - o.apply_BT(y)))
+        else:
+            z = o.velocity_cheb(self.mu, a - o.apply_BT(y), self.smooth, self.lmin, self.lmax)
         return np.concatenate([z, y])
 
     def solve(self, f, g, m, max_iters, rtol):

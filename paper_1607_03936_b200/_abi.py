@@ -49,7 +49,9 @@ SYMBOLS = [
     ("wb_apply_dabfbt", _i, [_vp, _vp, _vp, _i]),
     ("wb_apply_mpinv", _i, [_vp, _vp, _vp]),
     ("wb_load_vector", _i, [_vp, _vp, _vp]),
-    ("wb_setup_mg", _i, [_vp, _i]),
+    ("wb_setup_mg", _i, [_vp, _i, _vp]),
+    ("wb_velocity_vcycle", _i, [_vp, _vp, _vp]),
+    ("wb_set_velocity_mg", _i, [_vp, _i]),
     ("wb_mg_vcycle", _i, [_vp, _i, _vp, _vp]),
     ("wb_poisson_mgcg", _i, [_vp, _i, _vp, _vp, _i]),
     ("wb_set_inner_mg", _i, [_vp, _i]),
@@ -261,8 +263,16 @@ class Context:
         return F
 
     # -- geometric pressure multigrid (R20)
-    def setup_mg(self, nu: int = 3):
-        self._check(self._L.wb_setup_mg(self._h, int(nu)))
+    def setup_mg(self, nu: int = 3, mu=None):
+        self._check(self._L.wb_setup_mg(self._h, int(nu),
+                                        _ptr(mu, self.n_el * self.n_q) if mu is not None else None))
+
+    def velocity_vcycle(self, b, x):
+        self._check(self._L.wb_velocity_vcycle(self._h, _ptr(b, self.n_v), _ptr(x, self.n_v)))
+        return x
+
+    def set_velocity_mg(self, cycles: int = 0):
+        self._check(self._L.wb_set_velocity_mg(self._h, int(cycles)))
 
     def mg_vcycle(self, side: int, b, x):
         self._check(self._L.wb_mg_vcycle(self._h, int(side), _ptr(b, self.n_p), _ptr(x, self.n_p)))

@@ -150,3 +150,114 @@ __global__ void k_mgcg_p(double* __restrict__ p, const double* __restrict__ z, i
 }
 
 }  // namespace wb
+
+namespace wb {
+
+// ---- velocity multigrid (R22): viscosity coarsening and Q2 nodal transfers (k = 2)
+// mu_c at coarse Gauss point q of coarse element E: the mean, over the fine children of E
+// whose closure contains the point, of each child's Gauss-weighted mean sum_q w_q mu_q / 8
+// (coarse Gauss abscissae -sqrt(3/5), 0, +sqrt(3/5) lie in child 0, on the face, in child 1
+// per axis).  Children in ascending (z, y, x) order.
+__global__ void k_mu_coarsen(const double* __restrict__ muf, double* __restrict__ muc, int Nc) {
+  const int Nf = 2 * Nc;
+  const int64_t n = (int64_t)Nc * Nc * Nc * 27;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(i % 27);
+    const int64_t E = i / 27;
+    const int cx = (int)(E % Nc), cy = (int)((E / Nc) % Nc), cz = (int)(E / ((int64_t)Nc * Nc));
+    const int qq[3] = {q % 3, (q / 3) % 3, q / 9};
+    int lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) { lo[d] = qq[d] == 2 ? 1 : 0; hi[d] = qq[d] == 0 ? 0 : 1; }
+    double acc = 0.0;
+    int cnt = 0;
+    for (int sz = lo[2]; sz <= hi[2]; ++sz)
+      for (int sy = lo[1]; sy <= hi[1]; ++sy)
+        for (int sx = lo[0]; sx <= hi[0]; ++sx) {
+          const int64_t ef = (int64_t)(2 * cx + sx) + (int64_t)Nf * ((int64_t)(2 * cy + sy) + (int64_t)Nf * (2 * cz + sz));
+          const double* m = muf + ef * 27;
+          double s = 0.0;
+          for (int k = 0; k < 27; ++k)
+            s = fma(TB(2).w[k % 3] * TB(2).w[(k / 3) % 3] * TB(2).w[k / 9], m[k], s);
+          acc += s / 8.0;
+          ++cnt;
+        }
+    muc[i] = acc / (double)cnt;
+  }
+}
+
+// 1-D weight of fine node i_f on coarse node I (Q2 nodal interpolation on the bisected
+// mesh), d = i_f - 2 I: coarse vertex (I even) 1, 3/8, 0, -1/8 at |d| = 0..3; coarse
+// mid-node (I odd) 1, 3/4 at |d| = 0, 1.
+__device__ __forceinline__ double vmg_w(int I, int d) {
+  const int a = d < 0 ? -d : d;
+  if (I & 1) return a == 0 ? 1.0 : (a == 1 ? 0.75 : 0.0);
+  return a == 0 ? 1.0 : (a == 1 ? 0.375 : (a == 3 ? -0.125 : 0.0));
+}
+
+// r_c = P^T (M r_f) on the coarse (2Nc+1)^3 grid, 3 SoA components, coarse boundary rows 0
+__global__ void k_vmg_restrict(const double* __restrict__ rf, double* __restrict__ rc, int Nc) {
+  const int nc = 2 * Nc + 1, nf = 4 * Nc + 1;
+  const int64_t nnc = (int64_t)nc * nc * nc, nnf = (int64_t)nf * nf * nf;
+  for (int64_t G = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; G < nnc; G += (int64_t)gridDim.x * blockDim.x) {
+    const int I[3] = {(int)(G % nc), (int)((G / nc) % nc), (int)(G / ((int64_t)nc * nc))};
+    if (node_bnd(I[0], I[1], I[2], nc)) { rc[G] = 0.0; rc[nnc + G] = 0.0; rc[2 * nnc + G] = 0.0; continue; }
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int dz = -3; dz <= 3; ++dz) {
+      const double wz = vmg_w(I[2], dz);
+      const int fz = 2 * I[2] + dz;
+      if (wz == 0.0 || fz < 0 || fz >= nf) continue;
+      for (int dy = -3; dy <= 3; ++dy) {
+        const double wy = vmg_w(I[1], dy);
+        const int fy = 2 * I[1] + dy;
+        if (wy == 0.0 || fy < 0 || fy >= nf) continue;
+        for (int dx = -3; dx <= 3; ++dx) {
+          const double wx = vmg_w(I[0], dx);
+          const int fx = 2 * I[0] + dx;
+          if (wx == 0.0 || fx < 0 || fx >= nf) continue;
+          if (node_bnd(fx, fy, fz, nf)) continue;  // Dirichlet rows carry no residual (R6)
+          const double w = wx * wy * wz;
+          const int64_t f = (int64_t)fx + (int64_t)nf * ((int64_t)fy + (int64_t)nf * fz);
+          a0 = fma(w, rf[f], a0);
+          a1 = fma(w, rf[nnf + f], a1);
+          a2 = fma(w, rf[2 * nnf + f], a2);
+        }
+      }
+    }
+    rc[G] = a0; rc[nnc + G] = a1; rc[2 * nnc + G] = a2;
+  }
+}
+
+// x_f += P x_c at the fine interior nodes (fine boundary rows untouched: they stay 0)
+__global__ void k_vmg_prolong_add(const double* __restrict__ xc, double* __restrict__ xf, int Nc) {
+  const int nc = 2 * Nc + 1, nf = 4 * Nc + 1;
+  const int64_t nnc = (int64_t)nc * nc * nc, nnf = (int64_t)nf * nf * nf;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < nnf; g += (int64_t)gridDim.x * blockDim.x) {
+    const int f[3] = {(int)(g % nf), (int)((g / nf) % nf), (int)(g / ((int64_t)nf * nf))};
+    if (node_bnd(f[0], f[1], f[2], nf)) continue;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    // coarse nodes with |f - 2 I| <= 3 per axis
+    for (int Iz = (f[2] - 3 + 1) / 2; Iz <= (f[2] + 3) / 2; ++Iz) {
+      if (Iz < 0 || Iz >= nc) continue;
+      const double wz = vmg_w(Iz, f[2] - 2 * Iz);
+      if (wz == 0.0) continue;
+      for (int Iy = (f[1] - 3 + 1) / 2; Iy <= (f[1] + 3) / 2; ++Iy) {
+        if (Iy < 0 || Iy >= nc) continue;
+        const double wy = vmg_w(Iy, f[1] - 2 * Iy);
+        if (wy == 0.0) continue;
+        for (int Ix = (f[0] - 3 + 1) / 2; Ix <= (f[0] + 3) / 2; ++Ix) {
+          if (Ix < 0 || Ix >= nc) continue;
+          const double wx = vmg_w(Ix, f[0] - 2 * Ix);
+          if (wx == 0.0) continue;
+          const double w = wx * wy * wz;
+          const int64_t G = (int64_t)Ix + (int64_t)nc * ((int64_t)Iy + (int64_t)nc * Iz);
+          a0 = fma(w, xc[G], a0);
+          a1 = fma(w, xc[nnc + G], a1);
+          a2 = fma(w, xc[2 * nnc + G], a2);
+        }
+      }
+    }
+    xf[g] += a0; xf[nnf + g] += a1; xf[2 * nnf + g] += a2;
+  }
+}
+
+}  // namespace wb

@@ -141,9 +141,17 @@ struct MGH {
   double *rk = nullptr, *zk = nullptr, *pk = nullptr, *qk = nullptr, *xk = nullptr;  // MG-PCG on level 0
   double* s = nullptr;  // device scalars: rz, pq, rz', stop
   int inner_iters = 0;  // wBFBT inner solves by MG-PCG with this many iterations (0: off)
+  // velocity multigrid (R22), built when wb_setup_mg gets mu: coarsened viscosities (levels
+  // >= 1, owned), SoA n_v work vectors per level, Chebyshev scales of A_l
+  bool vel = false;
+  double* mu[16] = {};
+  double *vb[16] = {}, *vx[16] = {}, *vr[16] = {}, *vt[16] = {};
+  double vlam[16] = {};
+  int vcycles = 0;  // Stokes At^-1 by this many V-cycles (0: the Chebyshev smoother, R18)
 };
 void mg_free(wb_ctx* c);
 wb_status run_mgcg(wb_ctx* c, int side, const double* b, double* x, int iters);
+wb_status run_vmg(wb_ctx* c, const double* b, double* x);
 
 namespace {
 
@@ -1059,6 +1067,7 @@ wb_status stokes_P(wb_ctx* c, const double* v, double* z, const StokesPar& P) {
   if ((s = run_BT(c, y, nullptr, c->gsa, 0, nullptr, c->nm, 1))) return s;
   k_axpby<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->gsa, v, c->n_v, 1.0, -1.0);  // a - B^T y
   LAUNCH_CHECK(c);
+  if (c->mg && c->mg->vel && c->mg->vcycles > 0) return run_vmg(c, c->gsa, z);  // At^-1: velocity V-cycles (R22)
   return run_vcheb(c, c->gsa, z, P.sm, P.lo, P.hi);
 }
 wb_status host_scalar(wb_ctx* c, const double* dev, double* h) {
@@ -1534,6 +1543,9 @@ void mg_free(wb_ctx* c) {
       if (*b) cudaFree(*b);
     if (l > 0 && M->lev[l]) wb_destroy(M->lev[l]);
   }
+  for (int l = 0; l < M->nl; ++l)
+    for (double** b : {&M->mu[l], &M->vb[l], &M->vx[l], &M->vr[l], &M->vt[l]})
+      if (*b) cudaFree(*b);
   for (double** b : {&M->rk, &M->zk, &M->pk, &M->qk, &M->xk, &M->s})
     if (*b) cudaFree(*b);
   delete M;
@@ -1605,7 +1617,54 @@ wb_status run_mgcg(wb_ctx* c, int side, const double* b, double* x, int iters) {
   return mg_project(c, x);
 }
 
-static wb_status mg_setup(wb_ctx* c, int nu) {
+// x = V_l(b) for M A M (velocity, SoA n_v, R22): x = S(b); x += P V_{l+1}(P^T (b - A x));
+// x += S(b - A x); S = nu Chebyshev-Jacobi steps on [0.1, 1.1] lambda_l; coarsest level: 30 steps
+static wb_status vmg_vcycle(wb_ctx* c, int l, const double* b, double* x) {
+  MGH& M = *c->mg;
+  wb_ctx* L = M.lev[l];
+  L->stream = c->stream;
+  const int64_t n = L->n_v;
+  const double lam = M.vlam[l];
+  if (l == M.nl - 1) return run_vcheb(L, b, x, 30, 0.1 * lam, 1.1 * lam);
+  wb_status s = run_vcheb(L, b, x, M.nu, 0.1 * lam, 1.1 * lam);
+  if (s) return s;
+  if ((s = run_A(L, x, M.vt[l], 0))) return s;
+  k_mg_resid<<<stream_blocks(n), VBS, 0, c->stream>>>(M.vr[l], b, M.vt[l], n);
+  LAUNCH_CHECK(c);
+  const int Nc = M.Ns[l + 1];
+  k_vmg_restrict<<<stream_blocks(M.lev[l + 1]->n_nodes), VBS, 0, c->stream>>>(M.vr[l], M.vb[l + 1], Nc);
+  LAUNCH_CHECK(c);
+  if ((s = vmg_vcycle(c, l + 1, M.vb[l + 1], M.vx[l + 1]))) return s;
+  k_vmg_prolong_add<<<stream_blocks(L->n_nodes), VBS, 0, c->stream>>>(M.vx[l + 1], x, Nc);
+  LAUNCH_CHECK(c);
+  if ((s = run_A(L, x, M.vt[l], 0))) return s;
+  k_mg_resid<<<stream_blocks(n), VBS, 0, c->stream>>>(M.vr[l], b, M.vt[l], n);
+  LAUNCH_CHECK(c);
+  if ((s = run_vcheb(L, M.vr[l], M.vt[l], M.nu, 0.1 * lam, 1.1 * lam))) return s;
+  k_axpy<<<stream_blocks(n), VBS, 0, c->stream>>>(x, M.vt[l], n, 1.0);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+// x = M.vcycles stationary V-cycles on A x = b from x0 = 0 (level 0 vectors reused)
+wb_status run_vmg(wb_ctx* c, const double* b, double* x) {
+  MGH& M = *c->mg;
+  wb_status s = vmg_vcycle(c, 0, b, x);
+  const int64_t n = c->n_v;
+  for (int k = 1; k < M.vcycles && !s; ++k) {
+    if ((s = run_A(c, x, M.vb[0], 0))) return s;
+    k_mg_resid<<<stream_blocks(n), VBS, 0, c->stream>>>(M.vb[0], b, M.vb[0], n);
+    LAUNCH_CHECK(c);
+    if ((s = vmg_vcycle(c, 0, M.vb[0], M.vx[0]))) return s;
+    k_axpy<<<stream_blocks(n), VBS, 0, c->stream>>>(x, M.vx[0], n, 1.0);
+    LAUNCH_CHECK(c);
+  }
+  return s;
+}
+
+template <int K>
+static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r);
+
+static wb_status mg_setup(wb_ctx* c, int nu, const double* mu0) {
   mg_free(c);
   MGH* M = new (std::nothrow) MGH();
   if (!M) return set_err(c, WB_ENOMEM, "multigrid allocation failed");
@@ -1621,10 +1680,17 @@ static wb_status mg_setup(wb_ctx* c, int nu) {
   };
   for (int l = 1; l < M->nl; ++l) {
     wb_ctx* L = nullptr;
-    wb_status st = wb_create(&L, M->Ns[l], 2, c->flags & WB_STRICT_LUMP, (void*)c->stream);
+    wb_status st = wb_create(&L, M->Ns[l], 2, 0, (void*)c->stream);
     if (st) return fail(st, "level context");
     M->lev[l] = L;
     wb_ctx* F = M->lev[l - 1];
+    if (mu0) {  // velocity hierarchy: coarsened viscosity, the level's A (and, overwritten below, its lumping)
+      if (!lazy_alloc(&M->mu[l], L->n_el * 27)) return fail(WB_ENOMEM, "coarse viscosity");
+      const double* muf = l == 1 ? mu0 : M->mu[l - 1];
+      k_mu_coarsen<<<stream_blocks(L->n_el * 27), VBS, 0, c->stream>>>(muf, M->mu[l], M->Ns[l]);
+      LAUNCH_CHECK(c);
+      if ((st = setup_t<2>(L, M->mu[l], 1.0, 1.0))) return fail(st, wb_last_error(L));
+    }
     CUDA_TRY(c, cudaMemsetAsync(L->icount, 0, sizeof(unsigned long long) * 4, c->stream));
     k_mg_inject<<<stream_blocks(L->n_nodes), VBS, 0, c->stream>>>(F->Cw, F->Dw, L->Cw, L->Dw, M->Ns[l]);
     LAUNCH_CHECK(c);
@@ -1645,6 +1711,19 @@ static wb_status mg_setup(wb_ctx* c, int nu) {
   if (!dalloc(&M->rk, n0) || !dalloc(&M->zk, n0) || !dalloc(&M->pk, n0) || !dalloc(&M->qk, n0) ||
       !dalloc(&M->xk, n0) || !dalloc(&M->s, 4))
     return fail(WB_ENOMEM, "MG-PCG vectors");
+  if (mu0) {
+    M->vel = true;
+    for (int l = 0; l < M->nl; ++l) {
+      wb_ctx* L = M->lev[l];
+      const int64_t nv = L->n_v;
+      if (!dalloc(&M->vb[l], nv) || !dalloc(&M->vx[l], nv) || !dalloc(&M->vr[l], nv) || !dalloc(&M->vt[l], nv))
+        return fail(WB_ENOMEM, "velocity level vectors");
+      k_splitmix<<<stream_blocks(nv), VBS, 0, c->stream>>>(M->vb[l], nv, 0x5EEDull);
+      LAUNCH_CHECK(c);
+      wb_status st = run_veigmax(L, M->vb[l], 20, &M->vlam[l]);
+      if (st) return fail(st, "velocity eigenvalue estimate");
+    }
+  }
   // Chebyshev intervals: power iteration (20 steps) from the splitmix64 start vector
   for (int l = 0; l < M->nl - 1; ++l) {
     wb_ctx* L = M->lev[l];
@@ -1823,12 +1902,30 @@ wb_status wb_load_vector(wb_ctx* c, const double* fq, double* F) {
   return WB_OK;
 }
 
-wb_status wb_setup_mg(wb_ctx* c, int nu) {
+wb_status wb_setup_mg(wb_ctx* c, int nu, const double* mu_q) {
   wb_status s = check_ctx(c, true);
   if (s) return s;
-  if (c->k != 2) return set_err(c, WB_EINVAL, "the pressure multigrid is built for k = 2 (R20)");
+  if (c->k != 2) return set_err(c, WB_EINVAL, "the multigrid is built for k = 2 (R20, R22)");
   if (nu < 1 || nu > 16) return set_err(c, WB_EINVAL, "nu must be in [1, 16]");
-  return mg_setup(c, nu);
+  return mg_setup(c, nu, mu_q);
+}
+
+wb_status wb_velocity_vcycle(wb_ctx* c, const double* b, double* x) {
+  wb_status s = check_ctx(c, true);
+  if (s) return s;
+  if (!c->mg || !c->mg->vel) return set_err(c, WB_ESTATE, "no velocity multigrid (wb_setup_mg with mu)");
+  if (!b || !x) return set_err(c, WB_EINVAL, "bad argument");
+  const size_t bv = sizeof(double) * c->n_v;
+  if (overlaps(b, bv, x, bv)) return set_err(c, WB_EALIAS, "b and x overlap");
+  return vmg_vcycle(c, 0, b, x);
+}
+
+wb_status wb_set_velocity_mg(wb_ctx* c, int cycles) {
+  if (!c) return WB_EINVAL;
+  if (cycles < 0) return set_err(c, WB_EINVAL, "cycles must be >= 0");
+  if (cycles > 0 && !(c->mg && c->mg->vel)) return set_err(c, WB_ESTATE, "no velocity multigrid (wb_setup_mg with mu)");
+  if (c->mg) c->mg->vcycles = cycles;
+  return WB_OK;
 }
 
 wb_status wb_mg_vcycle(wb_ctx* c, int side, const double* b, double* x) {
@@ -2108,6 +2205,10 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
     *value = c->inner;
   } else if (!strcmp(key, "mg_levels")) {  // levels of the pressure multigrid (0: none built)
     *value = c->mg ? c->mg->nl : 0;
+  } else if (!strncmp(key, "mg_vlambda_", 11)) {  // Chebyshev scale of the level-l velocity smoother
+    const int l = atoi(key + 11);
+    if (!c->mg || !c->mg->vel || l < 0 || l >= c->mg->nl) return set_err(c, WB_EINVAL, "bad key '%s'", key);
+    *value = c->mg->vlam[l];
   } else if (!strncmp(key, "mg_N_", 5) || !strncmp(key, "mg_lambda_", 10) || !strncmp(key, "mg_nonpos_", 10)) {
     // mg_N_<l>; mg_lambda_<side>_<l> (Chebyshev interval scale); mg_nonpos_<side>_<l>
     if (!c->mg) return set_err(c, WB_ESTATE, "no multigrid hierarchy (wb_setup_mg)");

@@ -167,3 +167,85 @@ def test_mesh_independent_iterations():
         its_j.append(_iters_to(o, L0.K, lambda r: minv * r, b))
     assert max(its) - min(its) <= 2, its
     assert its_j[-1] > 2 * its[-1] and its_j[-1] > its_j[0], (its, its_j)
+
+
+# ---------------------------------------------------------------- velocity multigrid (R22)
+def test_q2_prolongation_interpolates_quadratics_exactly():
+    """Coarse nodal values of u = x^2 y (1 - z), a Q2 function on every coarse element,
+    prolongate to its exact values at the fine nodes; restriction is the transpose."""
+    Nc = 2
+    o = Oracle(Nc, 2)
+    xn = o.tables()["xn"]
+    P1 = omg.q2_prolongation_1d(Nc, xn)
+
+    def nodes(N):
+        line = np.concatenate([[(e + (xn[a] + 1) / 2) / N for a in range(2)] for e in range(N)] + [[1.0]])
+        Z, Y, X = np.meshgrid(line, line, line, indexing="ij")
+        return X.ravel(), Y.ravel(), Z.ravel()
+
+    u = lambda x, y, z: x * x * y * (1 - z)  # noqa: E731
+    xc = np.concatenate([u(*nodes(Nc)), np.zeros((2 * Nc + 1) ** 3), -u(*nodes(Nc))])
+    xf = omg.vprolong(P1, xc)
+    ref = np.concatenate([u(*nodes(2 * Nc)), np.zeros((4 * Nc + 1) ** 3), -u(*nodes(2 * Nc))])
+    assert np.allclose(xf, ref, atol=1e-15)
+    rng = np.random.default_rng(0)
+    a, b = rng.standard_normal(xc.size), rng.standard_normal(xf.size)
+    assert omg.vprolong(P1, a) @ b == pytest.approx(a @ omg.vrestrict(P1, b), rel=1e-13)
+
+
+def test_mu_coarsening_constants_and_positivity():
+    o = Oracle(4, 2)
+    wg = o.tables()["wg"]
+    assert np.allclose(omg.coarsen_mu(np.full(4 ** 3 * 27, 2.5), 2, wg), 2.5, rtol=1e-15)
+    mu = np.random.default_rng(1).uniform(1e-3, 1e3, 4 ** 3 * 27)
+    mc = omg.coarsen_mu(mu, 2, wg)
+    assert np.all(mc > 0) and mc.max() <= mu.max() and mc.min() >= mu.min()
+
+
+def test_velocity_vcycle_symmetric_and_mesh_independent():
+    """The velocity V-cycle is a symmetric linear map (Chebyshev smoothing and coarse solve
+    are fixed polynomials); MG-PCG on A needs about the same iterations at N = 4, 8, 16 for a
+    smooth viscosity while Jacobi-PCG's grow."""
+    cen = np.array([[0.3, 0.4, 0.5], [0.7, 0.6, 0.4]])
+    o = Oracle(4, 2)
+    mu = synth.viscosity_at_quadrature(4, 2, cen, 20.0, 0.3, 1.0, 10.0)
+    V = omg.VMG(4, mu)
+    mask = o.boundary_mask().astype(bool)
+    rng = np.random.default_rng(2)
+    a, b = (np.where(mask, 0.0, rng.standard_normal(o.n_v)) for _ in range(2))
+    assert V.vcycle(a) @ b == pytest.approx(a @ V.vcycle(b), rel=1e-10)
+    its, its_j = [], []
+    for N in (4, 8, 16):
+        o = Oracle(N, 2)
+        mu = synth.viscosity_at_quadrature(N, 2, cen, 20.0, 0.3, 1.0, 10.0)
+        V = omg.VMG(N, mu)
+        mask = o.boundary_mask().astype(bool)
+        rhs = np.where(mask, 0.0, np.random.default_rng(3).uniform(-1, 1, o.n_v))
+        A = lambda v: o.apply_A(mu, v)  # noqa: E731
+        dA = o.diag_A(mu)
+        dinv = np.where(mask, 0.0, 1.0 / np.where(dA != 0, dA, 1.0))
+        its.append(_cg_its(A, V.vcycle, rhs))
+        its_j.append(_cg_its(A, lambda r: dinv * r, rhs))
+    assert max(its) - min(its) <= 3, its
+    assert its_j[-1] > 2 * its[-1] and its_j[-1] > its_j[0], (its, its_j)
+
+
+def _cg_its(A, prec, b, tol=1e-6, cap=400):
+    x = np.zeros_like(b)
+    r = b.copy()
+    z = prec(r)
+    p = z.copy()
+    rz = r @ z
+    r0 = np.linalg.norm(r)
+    for it in range(1, cap + 1):
+        q = A(p)
+        a = rz / (p @ q)
+        x += a * p
+        r -= a * q
+        if np.linalg.norm(r) < tol * r0:
+            return it
+        z = prec(r)
+        rz1 = r @ z
+        p = z + rz1 / rz * p
+        rz = rz1
+    return cap
