@@ -346,6 +346,47 @@ def run_ours(args):
         b_ev.synchronize()
         t_st[it_o] = a_ev.elapsed_time(b_ev)
     stokes_iter_ms = (t_st[6] - t_st[2]) / 4
+    # ---- SURVEY 8(f) #2b / R20, R22: the multigrids, and the full Stokes solve with the
+    # multi-sinker forcing to the paper's 1e-6 reduction
+    # for the three Schur approximations (Sec. 3.2, Tables 1-2)
+    mg = {}
+    if cfg.k == 2:
+        def ev_ms(fn):
+            a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_ev.record(stream); fn(); b_ev.record(stream)
+            b_ev.synchronize()
+            return a_ev.elapsed_time(b_ev)
+        t_setup_mg = ev_ms(lambda: ctx.setup_mg(3, mu))
+        pb = torch.as_tensor(inp["p"], **f64)
+        ev_ms(lambda: ctx.mg_vcycle(1, pb, qv))
+        t_vc = statistics.median(ev_ms(lambda: ctx.mg_vcycle(1, pb, qv)) for _ in range(5))
+        t_mg = {it: statistics.median(ev_ms(lambda: ctx.poisson_mgcg(1, pb, qv, it)) for _ in range(3)) for it in (2, 10)}
+        ub = torch.as_tensor(inp["u"], **f64)
+        ev_ms(lambda: ctx.velocity_vcycle(ub, yd))
+        t_vvc = statistics.median(ev_ms(lambda: ctx.velocity_vcycle(ub, yd)) for _ in range(5))
+        fq = torch.as_tensor(synth.forcing_at_quadrature(cfg.N, cfg.k, inp["centers"], cfg.delta, cfg.omega), **f64)
+        fl = ctx.load_vector(fq, torch.empty(ctx.n_v, **f64))
+        solves = {}
+        for name, kind in (("wBFBT", 0), ("M_p(1/mu)", 2), ("diag(A)-BFBT", 1)):
+            ctx.set_schur(kind)
+            ctx.set_viscosity(mu)
+            ctx.setup_mg(3, mu)
+            ctx.set_velocity_mg(2)
+            ctx.set_inner_mg(8 if kind == 0 else 0)
+            max_it = 300
+            ms = ev_ms(lambda: solves.__setitem__(name, ctx.stokes_fgmres(fl, gz, us, ps, 200, max_it, 1e-6, 20, 6, 1.0,
+                                                                          2.0)[2:]))
+            it_s, rr_s = solves[name]
+            solves[name] = {"fgmres_iterations": it_s, "relres": rr_s, "solve_ms": ms,
+                            "converged_1e-6": rr_s <= 1e-6}
+        ctx.set_schur(0)
+        ctx.set_viscosity(mu)
+        mg = {"setup_mg_ms": t_setup_mg, "levels": int(ctx.query("mg_levels")), "pressure_vcycle_ms": t_vc,
+              "mgcg_iter_ms": (t_mg[10] - t_mg[2]) / 8, "velocity_vcycle_ms": t_vvc,
+              "stokes_solve": solves,
+              "note": "SURVEY 8(f) #2b (R20, R22) and #1, #3 (not in the step): FGMRES(200) on [A B^T; B 0] with "
+                      "f = the multi-sinker load vector, g = 0, rtol 1e-6, max 300 iterations; At^-1 = 2 velocity "
+                      "V-cycles; wBFBT inner solves MG-PCG(8); diag(A)-BFBT inner PCG(20)"}
     # ---- dominant kernel: the fused Poisson operator inside the PCG loops (2 x iters
     # launches per step).  Profiled pass: the same hot-path step with a CUDA-event
     # pair around every such launch (library option "profile": plain launches on
@@ -433,6 +474,7 @@ def run_ours(args):
                              "note": "SURVEY 8(f) #2 (not in the step): x = P Cheb(K_r, P b), R16"},
                     "velocity_smoother": {"diagA_ms": t_diagA, "iter_us": vsmooth_iter_us,
                                           "note": "R18 (not in the step): x = Cheb(M A M, M b), Jacobi mask/diag(A)"},
+                    "multigrid": mg,
                     "stokes_fgmres": {"iter_ms": stokes_iter_ms, "relres_after": {str(k): v for k, v in rr_st.items()},
                                       "note": "R19 (not in the step): FGMRES on [A B^T; B 0], f = u, g = 0; per "
                                               "iteration wBFBT (2 x iters PCG) + 6 smoother steps"}},
