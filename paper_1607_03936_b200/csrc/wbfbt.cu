@@ -1078,9 +1078,10 @@ wb_status host_scalar(wb_ctx* c, const double* dev, double* h) {
 wb_status run_stokes(wb_ctx* c, const double* f, const double* g, double* u, double* p, int m, int max_iters,
                      double rtol, const StokesPar& P, int* iters_out, double* relres_out) {
   const int64_t n = c->n_v + c->n_p;
-  if (m > c->g_m) {
-    for (double** b : {&c->gV, &c->gZ}) { if (*b) cudaFree(*b); *b = nullptr; }
-    if (!lazy_alloc(&c->gV, n * (m + 1)) || !lazy_alloc(&c->gZ, n * m)) {
+  if (m > c->g_m) {  // the basis and the Hessenberg column grow with the restart length
+    cudaStreamSynchronize(c->stream);
+    for (double** b : {&c->gV, &c->gZ, &c->gh}) { if (*b) cudaFree(*b); *b = nullptr; }
+    if (!lazy_alloc(&c->gV, n * (m + 1)) || !lazy_alloc(&c->gZ, n * m) || !lazy_alloc(&c->gh, (int64_t)m + 2)) {
       c->g_m = 0;
       return set_err(c, WB_ENOMEM, "FGMRES basis allocation failed (restart %d)", m);
     }

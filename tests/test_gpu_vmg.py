@@ -98,3 +98,15 @@ def test_stokes_c5_converges_and_wbfbt_beats_mp():
     it_mp, rr_mp = _solve("C5", 2, max_iters=it)
     print("C5 M_p(1/mu) after", it_mp, "iterations: relres", rr_mp)
     assert rr_mp > 10 * rr
+
+
+def test_stokes_restart_growth():
+    """A later solve with a longer restart than an earlier one (the FGMRES work arrays grow)."""
+    P = Pair("C2", N=6)
+    c = P.ctx
+    f = dev(np.where(P.o.boundary_mask().astype(bool), 0.0, P.inp["u"]))
+    g = empty(c.n_p).zero_()
+    u, p = empty(c.n_v), empty(c.n_p)
+    for m in (3, 40):
+        _, _, it, rr = c.stokes_fgmres(f, g, u, p, m, 45, 0.0, 5, 2, 1.0, 2.0)
+        assert it == 45 and np.isfinite(rr)
