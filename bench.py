@@ -357,6 +357,7 @@ def run_ours(args):
             b_ev.synchronize()
             return a_ev.elapsed_time(b_ev)
         t_setup_mg = ev_ms(lambda: ctx.setup_mg(3, mu))
+        n_levels = int(ctx.query("mg_levels"))
         pb = torch.as_tensor(inp["p"], **f64)
         ev_ms(lambda: ctx.mg_vcycle(1, pb, qv))
         t_vc = statistics.median(ev_ms(lambda: ctx.mg_vcycle(1, pb, qv)) for _ in range(5))
@@ -381,7 +382,7 @@ def run_ours(args):
                             "converged_1e-6": rr_s <= 1e-6}
         ctx.set_schur(0)
         ctx.set_viscosity(mu)
-        mg = {"setup_mg_ms": t_setup_mg, "levels": int(ctx.query("mg_levels")), "pressure_vcycle_ms": t_vc,
+        mg = {"setup_mg_ms": t_setup_mg, "levels": n_levels, "pressure_vcycle_ms": t_vc,
               "mgcg_iter_ms": (t_mg[10] - t_mg[2]) / 8, "velocity_vcycle_ms": t_vvc,
               "stokes_solve": solves,
               "note": "SURVEY 8(f) #2b (R20, R22) and #1, #3 (not in the step): FGMRES(200) on [A B^T; B 0] with "

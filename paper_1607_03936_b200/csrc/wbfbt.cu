@@ -51,7 +51,8 @@ struct wb_ctx {
     long long n_launch = 0;
     cudaGraphExec_t exec = nullptr;
   };
-  static constexpr int MAX_GRAPHS = 8;
+  static constexpr int MAX_GRAPHS = 16;
+  bool in_capture = false;  // a caller is capturing a graph on this context's stream: launch directly
   GraphEntry graphs[MAX_GRAPHS];
   int n_graphs = 0;
   cudaStream_t cap_stream = nullptr;
@@ -147,6 +148,7 @@ struct MGH {
   double* mu[16] = {};
   double *vb[16] = {}, *vx[16] = {}, *vr[16] = {}, *vt[16] = {};
   double vlam[16] = {};
+  double *vin = nullptr, *vout = nullptr;  // fixed in/out of the captured velocity cycles
   int vcycles = 0;  // Stokes At^-1 by this many V-cycles (0: the Chebyshev smoother, R18)
 };
 void mg_free(wb_ctx* c);
@@ -671,7 +673,7 @@ wb_status graph_loop(wb_ctx* c, int kind, int side, int iters, double lo, double
     (void)l0;
     return WB_OK;
   }
-  if (!c->use_graph || c->profile || iters == 0 || !c->cap_stream) return direct();
+  if (c->in_capture || !c->use_graph || c->profile || iters == 0 || !c->cap_stream) return direct();
   wb_ctx::GraphEntry* g = nullptr;
   for (int i = 0; i < c->n_graphs; ++i) {
     const wb_ctx::GraphEntry& e = c->graphs[i];
@@ -684,7 +686,9 @@ wb_status graph_loop(wb_ctx* c, int kind, int side, int iters, double lo, double
     const long long l0 = c->launches;
     CUDA_TRY(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
     c->stream = c->cap_stream;
+    c->in_capture = true;
     wb_status s = direct();
+    c->in_capture = false;
     c->stream = saved;
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(c->cap_stream, &graph);
@@ -1547,8 +1551,9 @@ void mg_free(wb_ctx* c) {
   for (int l = 0; l < M->nl; ++l)
     for (double** b : {&M->mu[l], &M->vb[l], &M->vx[l], &M->vr[l], &M->vt[l]})
       if (*b) cudaFree(*b);
-  for (double** b : {&M->rk, &M->zk, &M->pk, &M->qk, &M->xk, &M->s})
+  for (double** b : {&M->rk, &M->zk, &M->pk, &M->qk, &M->xk, &M->s, &M->vin, &M->vout})
     if (*b) cudaFree(*b);
+  clear_graphs(c);  // graphs that captured the hierarchy's buffers
   delete M;
   c->mg = nullptr;
   cudaGetLastError();
@@ -1567,6 +1572,7 @@ static wb_status mg_vcycle(wb_ctx* c, int side, int l, const double* b, double* 
   MGH& M = *c->mg;
   wb_ctx* L = M.lev[l];
   L->stream = c->stream;
+  if (l > 0) L->in_capture = c->in_capture;
   const int64_t n = L->n_p;
   if (l == M.nl - 1) return run_poisson(L, side, b, x, (int)std::min<int64_t>(n, 256));
   const double lam = M.lam[side][l];
@@ -1601,7 +1607,9 @@ wb_status run_mgcg(wb_ctx* c, int side, const double* b, double* x, int iters) {
   if (s) return s;
   CUDA_TRY(c, cudaMemsetAsync(M.xk, 0, sizeof(double) * n, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(M.s, 0, sizeof(double) * 4, c->stream));
-  if ((s = mg_vcycle(c, side, 0, M.rk, M.zk))) return s;
+  // the V-cycle on the fixed buffers rk -> zk is replayed as one CUDA graph (kind 10 + side)
+  auto vc = [&] { return graph_loop(c, 10 + side, side, 1, 0.0, 0.0, [&] { return mg_vcycle(c, side, 0, M.rk, M.zk); }); };
+  if ((s = vc())) return s;
   CUDA_TRY(c, cudaMemcpyAsync(M.pk, M.zk, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
   if ((s = dev_dot(c, M.rk, M.zk, n, M.s))) return s;
   for (int it = 0; it < iters; ++it) {
@@ -1609,7 +1617,7 @@ wb_status run_mgcg(wb_ctx* c, int side, const double* b, double* x, int iters) {
     if ((s = dev_dot(c, M.pk, M.qk, n, M.s + 1))) return s;
     k_mgcg_xr<<<nb, VBS, 0, c->stream>>>(M.xk, M.rk, M.pk, M.qk, n, M.s);
     LAUNCH_CHECK(c);
-    if ((s = mg_vcycle(c, side, 0, M.rk, M.zk))) return s;
+    if ((s = vc())) return s;
     if ((s = dev_dot(c, M.rk, M.zk, n, M.s + 2))) return s;
     k_mgcg_p<<<nb, VBS, 0, c->stream>>>(M.pk, M.zk, n, M.s, c->counter + 3);
     LAUNCH_CHECK(c);
@@ -1624,6 +1632,7 @@ static wb_status vmg_vcycle(wb_ctx* c, int l, const double* b, double* x) {
   MGH& M = *c->mg;
   wb_ctx* L = M.lev[l];
   L->stream = c->stream;
+  if (l > 0) L->in_capture = c->in_capture;
   const int64_t n = L->n_v;
   const double lam = M.vlam[l];
   if (l == M.nl - 1) return run_vcheb(L, b, x, 30, 0.1 * lam, 1.1 * lam);
@@ -1649,17 +1658,24 @@ static wb_status vmg_vcycle(wb_ctx* c, int l, const double* b, double* x) {
 // x = M.vcycles stationary V-cycles on A x = b from x0 = 0 (level 0 vectors reused)
 wb_status run_vmg(wb_ctx* c, const double* b, double* x) {
   MGH& M = *c->mg;
-  wb_status s = vmg_vcycle(c, 0, b, x);
   const int64_t n = c->n_v;
-  for (int k = 1; k < M.vcycles && !s; ++k) {
-    if ((s = run_A(c, x, M.vb[0], 0))) return s;
-    k_mg_resid<<<stream_blocks(n), VBS, 0, c->stream>>>(M.vb[0], b, M.vb[0], n);
-    LAUNCH_CHECK(c);
-    if ((s = vmg_vcycle(c, 0, M.vb[0], M.vx[0]))) return s;
-    k_axpy<<<stream_blocks(n), VBS, 0, c->stream>>>(x, M.vx[0], n, 1.0);
-    LAUNCH_CHECK(c);
-  }
-  return s;
+  CUDA_TRY(c, cudaMemcpyAsync(M.vin, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  // the cycles on the fixed buffers vin -> vout, replayed as one CUDA graph (kind 12)
+  wb_status s = graph_loop(c, 12, 0, M.vcycles, 0.0, 0.0, [&] {
+    wb_status st = vmg_vcycle(c, 0, M.vin, M.vout);
+    for (int k = 1; k < M.vcycles && !st; ++k) {
+      if ((st = run_A(c, M.vout, M.vb[0], 0))) return st;
+      k_mg_resid<<<stream_blocks(n), VBS, 0, c->stream>>>(M.vb[0], M.vin, M.vb[0], n);
+      LAUNCH_CHECK(c);
+      if ((st = vmg_vcycle(c, 0, M.vb[0], M.vx[0]))) return st;
+      k_axpy<<<stream_blocks(n), VBS, 0, c->stream>>>(M.vout, M.vx[0], n, 1.0);
+      LAUNCH_CHECK(c);
+    }
+    return st;
+  });
+  if (s) return s;
+  CUDA_TRY(c, cudaMemcpyAsync(x, M.vout, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  return WB_OK;
 }
 
 template <int K>
@@ -1714,6 +1730,7 @@ static wb_status mg_setup(wb_ctx* c, int nu, const double* mu0) {
     return fail(WB_ENOMEM, "MG-PCG vectors");
   if (mu0) {
     M->vel = true;
+    if (!dalloc(&M->vin, c->n_v) || !dalloc(&M->vout, c->n_v)) return fail(WB_ENOMEM, "velocity cycle vectors");
     for (int l = 0; l < M->nl; ++l) {
       wb_ctx* L = M->lev[l];
       const int64_t nv = L->n_v;
@@ -1724,6 +1741,11 @@ static wb_status mg_setup(wb_ctx* c, int nu, const double* mu0) {
       wb_status st = run_veigmax(L, M->vb[l], 20, &M->vlam[l]);
       if (st) return fail(st, "velocity eigenvalue estimate");
     }
+  }
+  {  // the coarsest solve's PCG histories, allocated now: the V-cycle is replayed as a captured graph
+    wb_ctx* Lc = M->lev[M->nl - 1];
+    wb_status st = ensure_iters(Lc, (int)std::min<int64_t>(Lc->n_p, 256));
+    if (st) return fail(st, "coarse PCG histories");
   }
   // Chebyshev intervals: power iteration (20 steps) from the splitmix64 start vector
   for (int l = 0; l < M->nl - 1; ++l) {
