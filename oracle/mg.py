@@ -261,18 +261,21 @@ def q2_prolongation_1d(Nc: int, xn: np.ndarray) -> np.ndarray:
     return P
 
 
+def _tp3(P: np.ndarray, X: np.ndarray) -> np.ndarray:
+    """(P x P x P) X for a [z][y][x] array X: the 1-D map P applied along each axis."""
+    X = np.tensordot(P, X, axes=(1, 0))                     # z
+    X = np.tensordot(P, X, axes=(1, 1)).transpose(1, 0, 2)  # y
+    return np.tensordot(X, P, axes=(2, 1))                  # x
+
+
 def vprolong(P1: np.ndarray, xc: np.ndarray) -> np.ndarray:
     nf, nc = P1.shape
-    out = [np.einsum("ai,bj,ck,ijk->abc", P1, P1, P1, xc[c * nc ** 3:(c + 1) * nc ** 3].reshape(nc, nc, nc)).ravel()
-           for c in range(3)]
-    return np.concatenate(out)
+    return np.concatenate([_tp3(P1, xc[c * nc ** 3:(c + 1) * nc ** 3].reshape(nc, nc, nc)).ravel() for c in range(3)])
 
 
 def vrestrict(P1: np.ndarray, xf: np.ndarray) -> np.ndarray:
     nf, nc = P1.shape
-    out = [np.einsum("ai,bj,ck,abc->ijk", P1, P1, P1, xf[c * nf ** 3:(c + 1) * nf ** 3].reshape(nf, nf, nf)).ravel()
-           for c in range(3)]
-    return np.concatenate(out)
+    return np.concatenate([_tp3(P1.T, xf[c * nf ** 3:(c + 1) * nf ** 3].reshape(nf, nf, nf)).ravel() for c in range(3)])
 
 
 class VMG:

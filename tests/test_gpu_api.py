@@ -223,7 +223,7 @@ def test_full_size_wbfbt(full):
     rec = dict(cfg=full.cfg.name, N=full.N, k=full.k, iters=it, err=err)
     if err > 1e-8:
         from tests.test_gpu_parity import self_discrepancy
-        ds = self_discrepancy(full.o, r, it, zo=zo)
+        ds = self_discrepancy(full.o, r, it, zo=zo, orders=(1,))  # one other order decides > 1e-9
         rec["delta_self"] = ds
         st = full.ost
         b = full.o.project(r)
