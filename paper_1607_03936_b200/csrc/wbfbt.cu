@@ -103,7 +103,7 @@ struct wb_ctx {
   CUtensorMap tm_pp, tm_pp1, tm_pz, tm_pr, tm_mL, tm_mR;
   // node-owner z-march Poisson kernel (k2_zm.cuh): tensor maps with its per-layer box,
   // X prescaled on the padded nodal grid, option "k_zm" (default on), z-chunk length
-  bool zm_ok = false;
+  bool zm_ok = false, xz_valid = false;
   int use_zm = 0, zm_zc = 4, zm_var = 0;
   double *XzL = nullptr, *XzR = nullptr;
   static constexpr int ZM_NV = 5;  // kernel variants (tile shape, CTAs per SM): zm_variants below
@@ -344,6 +344,16 @@ const CUtensorMap* tmap_of(wb_ctx* c, const double* p) {
 bool tma_active(const wb_ctx* c) { return c->k == 2 && c->tma_ok && c->use_tma && c->n_el >= 148 * 256 * 2; }
 // the node-owner z-march kernel (k2_zm.cuh) replaces it where set up; it always reads z
 bool zm_active(const wb_ctx* c) { return tma_active(c) && c->zm_ok && c->use_zm; }
+// X = sB^2 C_w^-1, sB^2 D_w^-1 on the padded nodal grid of the z-march kernel: built eagerly
+// (setup with the option on, or when the option is switched on), never inside a captured loop
+wb_status build_xz(wb_ctx* c) {
+  const double s2 = c->sB * c->sB;
+  k_xz_build<<<4 * c->nsm, 256, 0, c->stream>>>(c->Cinv, c->XzL, c->N, s2);
+  k_xz_build<<<4 * c->nsm, 256, 0, c->stream>>>(c->Dinv, c->XzR, c->N, s2);
+  if (cudaGetLastError() != cudaSuccess) return WB_ECUDA;
+  c->xz_valid = true;
+  return WB_OK;
+}
 double* z_out(const wb_ctx* c) { return tma_active(c) && (c->kz || zm_active(c)) ? c->pz : nullptr; }
 const CUtensorMap* zmap_of(wb_ctx* c, const double* p) {
   if (p == c->pp) return &c->tz[c->zm_var][0];
@@ -376,7 +386,7 @@ wb_status run_k2f(wb_ctx* c, const double* pold, double* pnew, const double* r, 
   if (zm_active(c)) {
     const CUtensorMap *tp = zmap_of(c, pold), *tz = zmap_of(c, c->pz);
     const double* xz = X == c->Cinv ? c->XzL : (X == c->Dinv ? c->XzR : nullptr);
-    if (tp && tz && xz && (mode == 2 || r == c->pr)) {
+    if (tp && tz && xz && c->xz_valid && (mode == 2 || r == c->pr)) {
       switch (c->zm_var) {
         case 0: launch_zm_t<16, 8, 2>(c, tp, tz, xz, pnew, q, mode, a, npq); break;
         case 1: launch_zm_t<16, 8, 3>(c, tp, tz, xz, pnew, q, mode, a, npq); break;
@@ -1500,12 +1510,10 @@ static wb_status finish_lumped(wb_ctx* c) {
     k_x_tiles<TMA_TX, TMA_TY, TMA_TZ><<<nt, F::MY * F::MZ, 0, c->stream>>>(c->Cinv, c->Dinv, c->XpL, c->XpR, c->N);
     LAUNCH_CHECK(c);
   }
-  if (c->zm_ok) {  // X = sB^2 C_w^-1, sB^2 D_w^-1 on the padded nodal grid of the z-march kernel
-    const double s2 = c->sB * c->sB;
-    k_xz_build<<<4 * c->nsm, 256, 0, c->stream>>>(c->Cinv, c->XzL, c->N, s2);
-    LAUNCH_CHECK(c);
-    k_xz_build<<<4 * c->nsm, 256, 0, c->stream>>>(c->Dinv, c->XzR, c->N, s2);
-    LAUNCH_CHECK(c);
+  c->xz_valid = false;  // the z-march kernel's X copy (opt-in)
+  if (c->zm_ok && c->use_zm) {
+    wb_status sx = build_xz(c);
+    if (sx) return set_err(c, sx, "z-march X build failed");
   }
   if constexpr (K == 2)
     k_jacobi2<<<nblk(c->n_el, 128), 128, 0, c->stream>>>(c->Cinv, c->Dinv, c->dKl, c->dKr, c->G, c->sB * c->sB);
@@ -2342,6 +2350,7 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k_zm must be 0 or 1");
     c->use_zm = (int)value;
     clear_graphs(c);
+    if (c->use_zm && c->zm_ok && c->have_visc && !c->xz_valid && build_xz(c)) return set_err(c, WB_ECUDA, "X build");
   } else if (!strcmp(key, "zm_var")) {  // z-march kernel variant (tile shape, CTAs per SM)
     if (!(value >= 0.0 && value < wb_ctx::ZM_NV) || value != (double)(int)value)
       return set_err(c, WB_EINVAL, "zm_var must be an integer in [0, %d)", wb_ctx::ZM_NV);
