@@ -1689,7 +1689,7 @@ wb_status run_vmg(wb_ctx* c, const double* b, double* x) {
 template <int K>
 static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r);
 
-static wb_status mg_setup(wb_ctx* c, int nu, const double* mu0) {
+static wb_status mg_setup_body(wb_ctx* c, int nu, const double* mu0) {
   mg_free(c);
   MGH* M = new (std::nothrow) MGH();
   if (!M) return set_err(c, WB_ENOMEM, "multigrid allocation failed");
@@ -1767,6 +1767,16 @@ static wb_status mg_setup(wb_ctx* c, int nu, const double* mu0) {
   }
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return WB_OK;
+}
+static wb_status mg_setup(wb_ctx* c, int nu, const double* mu0) {
+  const wb_status s = mg_setup_body(c, nu, mu0);
+  if (s && c->mg) {
+    char msg[sizeof(c->err)];
+    std::memcpy(msg, c->err, sizeof(msg));
+    mg_free(c);  // never leave a partial hierarchy behind
+    std::memcpy(c->err, msg, sizeof(msg));
+  }
+  return s;
 }
 
 extern "C" {
