@@ -305,6 +305,19 @@ def test_large_poisson_paths_ragged_tiles(N):
     for x in xs[1:]:
         assert np.array_equal(xs[0], x)
     assert rel_l2(xs[0], p.o.poisson(st["Dinv"], st["diagKr"], b, 5)) <= 1e-12
+    if tma:  # the opt-in node-owner z-march kernel (k_zm), every tile variant
+        p.ctx.set_option("k_ws", 0)
+        p.ctx.set_option("k_zm", 1)
+        assert p.ctx.query("k_zm") == 1
+        try:
+            for var in range(5):
+                p.ctx.set_option("zm_var", var)
+                q = host(p.ctx.apply_K(1, dev(b), empty(p.ctx.n_p)))
+                assert rel_l2(q, p.o.apply_K(st["Dinv"], b)) <= 1e-11
+                x = host(p.ctx.poisson_pcg(1, dev(b), empty(p.ctx.n_p), 5))
+                assert rel_l2(x, p.o.poisson(st["Dinv"], st["diagKr"], b, 5)) <= 1e-12
+        finally:
+            p.ctx.set_option("k_zm", 0)
 
 
 def test_nonpos_counts_per_side():
