@@ -275,7 +275,11 @@ wb_status wb_get_jacobi(wb_ctx* ctx, double* diagKl, double* diagKr);
  * flag or before a solve, WB_EINVAL for i outside [0, n)), "kz" (1 if the PCG
  * update stores z = Minv r for the TMA Poisson kernel), "k_tma" (1 if
  * the k = 2 Poisson operator runs as the TMA kernel for this mesh), "k_ws" (1 if
- * it runs as the warp-specialised TMA kernel), "weights" (the option below). */
+ * it runs as the warp-specialised TMA kernel), "weights" (the option below),
+ * "pcg_nonfinite" (failure detection: the number of non-finite rz_i / pq_i control scalars of
+ * the last PCG solve, 0 when healthy; WB_ESTATE before a solve), "k_zm" / "zm_zc" (the opt-in
+ * z-march Poisson kernel), "mg_levels", "mg_N_<l>", "mg_lambda_<side>_<l>",
+ * "mg_nonpos_<side>_<l>", "mg_vlambda_<l>" (the multigrid hierarchy of wb_setup_mg). */
 wb_status wb_query(wb_ctx* ctx, const char* key, double* value);
 /* Method option (changes the results): "weights", the wBFBT weights the next
  * wb_set_viscosity lumps: 0 = w_l = w_r = sqrt(mu), eq:wbfbt, the default; 1 = the

@@ -2322,6 +2322,27 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
     const bool is_alpha = key[0] == 'a' || !strcmp(key, "last_alpha_beta");
     *value = !ran ? 0.0 : (is_alpha ? rz[0] / pq : rz[1] / rz[0]);
   }
+  else if (!strcmp(key, "pcg_nonfinite")) {
+    // failure detection: the number of non-finite control scalars (rz_i, pq_i) of
+    // the last PCG solve, from the device histories (0 for a healthy solve); available in every
+    // context, read on demand (one small copy, synchronises)
+    const int n = c->last_pcg_iters;
+    if (n < 0) return set_err(c, WB_ESTATE, "no PCG solve yet");
+    std::vector<double> rz(n + 1, 0.0), pq(n + 1, 0.0);
+    std::vector<int> st(n + 1, 0);
+    if (n > 0) {
+      CUDA_TRY(c, cudaMemcpyAsync(rz.data(), rz_hist(c), sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(c, cudaMemcpyAsync(pq.data(), pq_hist(c), sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(c, cudaMemcpyAsync(st.data(), c->stop, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    int bad = 0;
+    for (int i = 0; i < n; ++i) {
+      if (!std::isfinite(rz[i])) ++bad;
+      if (!st[i] && !std::isfinite(pq[i])) ++bad;
+    }
+    *value = bad;
+  }
   else if (!strcmp(key, "last_pcg_stop_iter")) {
     int st[1024];
     int n = c->it_cap + 1 < 1024 ? c->it_cap + 1 : 1024;

@@ -332,3 +332,20 @@ def test_nonpos_counts_per_side():
     assert nc != nd
     assert p.ctx.query("n_nonpos_Cw") == nc
     assert p.ctx.query("n_nonpos_Dw") == nd
+
+
+def test_pcg_failure_detection():
+    """a healthy solve reports no non-finite PCG scalars; a right-hand side with a
+    NaN entry does (the status of an asynchronous apply cannot carry it)."""
+    import torch
+    from paper_1607_03936_b200 import WBError
+    p = Pair("C2", N=6)
+    with pytest.raises(WBError, match="WB_ESTATE"):
+        p.ctx.query("pcg_nonfinite")
+    b = p.inp["p"].copy()
+    p.ctx.poisson_pcg(1, dev(b), empty(p.ctx.n_p), 10)
+    assert p.ctx.query("pcg_nonfinite") == 0
+    b[17] = float("nan")
+    x = p.ctx.poisson_pcg(1, dev(b), empty(p.ctx.n_p), 10)
+    assert p.ctx.query("pcg_nonfinite") > 0
+    assert not bool(torch.isfinite(x).all())
