@@ -466,6 +466,9 @@ def run_ours(args):
                     "A_fp64_frac": A_DFMA_PER_ELEMENT * n_el / (tA * 1e-3) / DFMA_PEAK_INSTR_PER_S,
                     "A_ms_warm": tAw, "A_gdofs_warm": n_v / (tAw * 1e-3) / 1e9,
                     "B_gdofs": n_v / (tB * 1e-3) / 1e9, "BT_gdofs": n_v / (tBT * 1e-3) / 1e9,
+                    "B_ms": tB, "BT_ms": tBT,
+                    "B_hbm_frac": 8 * (n_v + n_p) / (tB * 1e-3) / 1e9 / hbm,
+                    "BT_hbm_frac": 8 * (n_v + n_p) / (tBT * 1e-3) / 1e9 / hbm,
                     "K_ms_cold": tK, "K_ms_warm": tKw, "wbfbt_ms": tW, "wbfbt_applies_per_s": 1e3 / tW,
                     "setup_ms": tS, "setup_grad_weights_ms": tSg,
                     "cheb": {"iter_us": cheb_iter_us, "solve_ms": t_cheb[iters], "iters": iters,
