@@ -153,24 +153,80 @@ class MGLevel:
         return self.o.poisson_cheb(self.X, self.diagK, b, NU, CHEB_LO * self.lam, CHEB_HI * self.lam)
 
 
+def p_transfer_table(of: Oracle, oc: Oracle) -> np.ndarray:
+    """T[mf][mc]: fine-order (P_{kf-1}) coefficient of mode mf from coarse-order (P_{kc-1}) mode
+    mc on the SAME element, by L2 projection with the fine order's Gauss rule (the spectral
+    level of the paper's HMG): int q_mc^c q_mf^f over the reference cube."""
+    tf, tc = of.tables(), oc.tables()
+    xg, wg = tf["xg"], tf["wg"]
+
+    def lhat(m, x):
+        cc = np.zeros(m + 1)
+        cc[m] = 1.0
+        return np.sqrt((2 * m + 1) / 2.0) * npleg.legval(x, cc)
+
+    T = np.zeros((of.n_m, oc.n_m))
+    for mf in range(of.n_m):
+        for mc in range(oc.n_m):
+            acc = 0.0
+            for iz in range(len(xg)):
+                for iy in range(len(xg)):
+                    for ix in range(len(xg)):
+                        xi = (xg[ix], xg[iy], xg[iz])
+                        qc = np.prod([lhat(tc["modes"][mc][d], xi[d]) for d in range(3)])
+                        qf = np.prod([lhat(tf["modes"][mf][d], xi[d]) for d in range(3)])
+                        acc += wg[ix] * wg[iy] * wg[iz] * qc * qf
+            T[mf, mc] = acc
+    return T
+
+
 class MG:
-    """The V-cycle hierarchy of one side's K_w, built from that side's lumped mass C_w."""
+    """The V-cycle hierarchy of one side's K_w, built from that side's lumped mass C_w.
+    k = 2: h-levels N, N/2, ... (R20).  k = 4: the paper's HMG order --
+    first a spectral level (Q4 x P3disc -> Q2 x P1disc on the same mesh), then the k = 2
+    h-levels.  Every level re-discretised, weights by density injection at coincident nodes
+    (the Q2 GLL nodes are Q4 GLL nodes: index 2i per axis, as on the bisected mesh)."""
 
     def __init__(self, N: int, Cw: np.ndarray, k: int = 2):
-        assert k == 2, "pressure multigrid is built for Q2 x P1disc (R20)"
-        self.Ns = levels_of(N)
+        assert k in (2, 4), "pressure multigrid for k = 2 (h) and k = 4 (p then h) (R20)"
+        self.spec = [(N, k)] + ([(N, 2)] if k == 4 else [])
+        while self.spec[-1][0] % 2 == 0 and self.spec[-1][0] > 1:
+            self.spec.append((self.spec[-1][0] // 2, 2))
+        self.Ns = [n for n, _ in self.spec]
         self.levels = []
         C = np.asarray(Cw, dtype=np.float64)
         M_prev = None
-        for li, Nl in enumerate(self.Ns):
-            o = Oracle(Nl, k)
+        for li, (Nl, kl) in enumerate(self.spec):
+            o = Oracle(Nl, kl)
             M = o.lumped(np.ones(o.n_el * o.n_q))["Cw"]  # unweighted lumped velocity mass
             if li > 0:
-                C = inject_weights(C, M_prev, M, Nl, k)
-            self.levels.append(MGLevel(Nl, k, C))
+                C = inject_weights(C, M_prev, M, Nl, kl)
+            self.levels.append(MGLevel(Nl, kl, C))
             M_prev = M
-        self.T = prolongation_tables(self.levels[0].o)
-        self.nm = self.levels[0].o.n_m
+        # transfers per level pair: ("h", T[8][4][4]) on k = 2, ("p", T[nm_f][nm_c]) spectral
+        self.trans = []
+        for li in range(len(self.spec) - 1):
+            (Nf, kf), (Nc, kc) = self.spec[li], self.spec[li + 1]
+            if Nf == Nc:
+                self.trans.append(("p", p_transfer_table(self.levels[li].o, self.levels[li + 1].o)))
+            else:
+                self.trans.append(("h", prolongation_tables(self.levels[li + 1].o)))
+        self.T = prolongation_tables(Oracle(2, 2))
+        self.nm = 4
+
+    def _restrict(self, l, r):
+        kind, T = self.trans[l]
+        if kind == "p":
+            ne = self.levels[l].o.n_el
+            return (r.reshape(ne, -1) @ T).reshape(-1)
+        return restrict(T, r, self.Ns[l + 1], 4)
+
+    def _prolong(self, l, xc):
+        kind, T = self.trans[l]
+        if kind == "p":
+            ne = self.levels[l].o.n_el
+            return (xc.reshape(ne, -1) @ T.T).reshape(-1)
+        return prolong(T, xc, self.Ns[l + 1], 4)
 
     def coarse_iters(self) -> int:
         return min(self.levels[-1].o.n_p, COARSE_CAP)
@@ -181,9 +237,8 @@ class MG:
             return L.o.poisson(L.X, L.diagK, b, self.coarse_iters())
         x = L.smooth(b)
         r = b - L.K(x)
-        Nc = self.Ns[l + 1]
-        xc = self.vcycle(restrict(self.T, r, Nc, self.nm), l + 1)
-        x = x + prolong(self.T, xc, Nc, self.nm)
+        xc = self.vcycle(self._restrict(l, r), l + 1)
+        x = x + self._prolong(l, xc)
         r = b - L.K(x)
         return x + L.smooth(r)
 

@@ -249,3 +249,47 @@ def _cg_its(A, prec, b, tol=1e-6, cap=400):
         p = z + rz1 / rz * p
         rz = rz1
     return cap
+
+
+# ---------------------------------------------------------------- spectral (p) level, k = 4
+def test_p_transfer_is_mode_embedding():
+    """P1disc modes are the first four P3disc modes (R2 ordering, orthonormal on the same
+    element): the spectral transfer is [I_4; 0] (closed form)."""
+    T = omg.p_transfer_table(Oracle(1, 4), Oracle(1, 2))
+    ref = np.zeros((20, 4))
+    ref[:4, :4] = np.eye(4)
+    assert np.allclose(T, ref, atol=1e-14)
+
+
+def test_k4_hierarchy_weights_and_converged_mgpcg():
+    N = 2
+    o = Oracle(N, 4)
+    M = o.lumped(np.ones(o.n_el * o.n_q))["Cw"]
+    m = omg.MG(N, 2.5 * M, k=4)
+    assert [(L.N, L.o.k) for L in m.levels] == [(2, 4), (2, 2), (1, 2)]
+    for L in m.levels:
+        Ml = L.o.lumped(np.ones(L.o.n_el * L.o.n_q))["Cw"]
+        assert np.allclose(L.C, 2.5 * Ml, rtol=1e-13)
+    st = o.setup(_mild(o, 5))
+    m = omg.MG(N, st["Dw"], k=4)
+    B = _dense_B(o)
+    K = B @ (np.tile(m.levels[0].X, 3)[:, None] * B.T)
+    b = o.project(np.random.default_rng(6).uniform(-1, 1, o.n_p))
+    xe = _pinv_deflated(K, nm=o.n_m) @ b
+    x = m.pcg(b, 30)
+    assert np.linalg.norm(x - xe) <= 1e-8 * np.linalg.norm(xe)
+
+
+def test_k4_mg_beats_jacobi():
+    """C4's recipe (Q4 x P3disc, 8 sinkers, DR 1e6) on 8^3: p/h-MG-PCG reaches a 1e-6 reduction
+    in far fewer iterations than Jacobi-PCG (52 vs 317)."""
+    inp = synth.make_inputs("C4", 0, N=8)
+    o = Oracle(8, 4)
+    st = o.setup(inp["mu_q"])
+    m = omg.MG(8, st["Dw"], k=4)
+    L0 = m.levels[0]
+    b = o.project(inp["p"])
+    its = _iters_to(o, L0.K, m.vcycle, b)
+    minv = np.where(np.abs(L0.diagK) > 1e-13 * np.abs(L0.diagK).max(), 1 / L0.diagK, 0.0)
+    its_j = _iters_to(o, L0.K, lambda r: minv * r, b)
+    assert its < 60 and its_j > 4 * its, (its, its_j)  # measured 52 vs 317
