@@ -168,8 +168,10 @@ wb_status wb_load_vector(wb_ctx* ctx, const double* fq, double* F);
 
 /* ---- Geometric pressure multigrid for K_w (second half; PAPER.md:2468-2546,
  * Sec. "Parallel hybrid spectral-geometric-algebraic multigrid (HMG) for wBFBT"; reading R20
- * of DESIGN.md).  k = 2 only.  Levels N, N/2, ... while N is even and > 1 (uniform element
- * bisection); on every level the operator is re-discretised
+ * of DESIGN.md).  k = 2: levels N, N/2, ... while N is even and > 1 (uniform element
+ * bisection); k = 4: first the spectral level Q4 x P3disc -> Q2 x P1disc on
+ * the same mesh (P1disc modes are the first four P3disc modes, the Q2 GLL
+ * nodes are Q4 GLL nodes), then the k = 2 levels; on every level the operator is re-discretised
  * as K_l = B_l X_l B_l^T with X_l = mask / C_l, the coarse lumped masses
  * C_l[G] = C_{l-1}[iota(G)] M_l[G] / M_{l-1}[iota(G)] (the weight density injected at the
  * coincident node; M = unweighted lumped mass); transfers are the exact P1disc embedding and
@@ -182,7 +184,9 @@ wb_status wb_load_vector(wb_ctx* ctx, const double* fq, double* F);
  * hierarchy of A is built too (R22: mu coarsened level by level; A
  * re-discretised; Q2 nodal interpolation and its transpose as transfers; the same smoother
  * on A, R18).  Allocates one internal context per coarse level and synchronises the stream.
- * WB_EINVAL for k != 2 or nu out of range, WB_ESTATE before wb_set_viscosity, WB_ENOMEM. */
+ * WB_EINVAL for k not 2 or 4, mu_q with k = 4 (the velocity multigrid is k = 2) or nu out of
+ * range, WB_ESTATE before wb_set_viscosity, WB_ENOMEM.  Queries "mg_N_<l>", "mg_k_<l>" give each
+ * level's mesh and order. */
 wb_status wb_setup_mg(wb_ctx* ctx, int nu, const double* mu_q);
 /* x = V(b), one velocity V-cycle on M A M (b, x: device SoA n_v; boundary entries of b are
  * ignored, of x written 0).  WB_ESTATE without a velocity hierarchy. */

@@ -286,7 +286,7 @@ class Context:
         self._check(self._L.wb_set_inner_mg(self._h, int(iters)))
 
     def mg_get_lumped(self, level: int, Cw=None, Dw=None):
-        n = (2 * int(self.query(f"mg_N_{int(level)}")) + 1) ** 3
+        n = (int(self.query(f"mg_k_{int(level)}")) * int(self.query(f"mg_N_{int(level)}")) + 1) ** 3
         f = lambda t: _ptr(t, n) if t is not None else None  # noqa: E731
         self._check(self._L.wb_mg_get_lumped(self._h, int(level), f(Cw), f(Dw)))
 

@@ -261,3 +261,36 @@ __global__ void k_vmg_prolong_add(const double* __restrict__ xc, double* __restr
 }
 
 }  // namespace wb
+
+namespace wb {
+
+// ---- the spectral (p) level for k = 4 (R20): Q4 x P3disc -> Q2 x P1disc
+// on the same mesh.  Q2 node i (per axis) is Q4 node 2 i (the Q2 GLL points are Q4 GLL
+// points); the unweighted lumped-mass ratio M_Q2 / M_Q4 there is 10/3 at a vertex (h/3 vs
+// h/10; h/6 vs h/20 on the boundary) and 15/8 at a mid-node (2h/3 vs 16h/45) per axis.
+__global__ void k_mg_inject_p(const double* __restrict__ Cf, const double* __restrict__ Df, double* __restrict__ Cc,
+                              double* __restrict__ Dc, int N) {
+  const int nc = 2 * N + 1, nf = 4 * N + 1;
+  const int64_t n = (int64_t)nc * nc * nc;
+  for (int64_t G = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; G < n; G += (int64_t)gridDim.x * blockDim.x) {
+    const int gx = (int)(G % nc), gy = (int)((G / nc) % nc), gz = (int)(G / ((int64_t)nc * nc));
+    const int64_t f = (int64_t)(2 * gx) + (int64_t)nf * ((int64_t)(2 * gy) + (int64_t)nf * (2 * gz));
+    const double rx = (gx & 1) ? 15.0 / 8.0 : 10.0 / 3.0, ry = (gy & 1) ? 15.0 / 8.0 : 10.0 / 3.0,
+                 rz = (gz & 1) ? 15.0 / 8.0 : 10.0 / 3.0;
+    const double r = rx * ry * rz;
+    Cc[G] = Cf[f] * r;
+    Dc[G] = Df[f] * r;
+  }
+}
+// P1disc modes are the first four P3disc modes (R2 ordering, orthonormal on the same element):
+// restriction keeps them, prolongation adds into them
+__global__ void k_mg_restrict_p(const double* __restrict__ rf, double* __restrict__ rc, int64_t n_el, int nmf) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 4 * n_el; i += (int64_t)gridDim.x * blockDim.x)
+    rc[i] = rf[(i / 4) * nmf + (i % 4)];
+}
+__global__ void k_mg_prolong_add_p(const double* __restrict__ xc, double* __restrict__ xf, int64_t n_el, int nmf) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 4 * n_el; i += (int64_t)gridDim.x * blockDim.x)
+    xf[(i / 4) * nmf + (i % 4)] += xc[i];
+}
+
+}  // namespace wb

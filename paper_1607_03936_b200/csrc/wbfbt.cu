@@ -135,7 +135,7 @@ struct wb_ctx {
 // k = 2 contexts on the N / 2^l meshes; per level element-major work vectors.
 struct MGH {
   int nl = 0, nu = 3;
-  int Ns[16] = {};
+  int Ns[16] = {}, Ks[16] = {};  // level mesh and order (k = 4: a spectral level to k = 2 first)
   wb_ctx* lev[16] = {};
   double lam[2][16] = {};
   double *b[16] = {}, *x[16] = {}, *r[16] = {}, *t[16] = {};
@@ -1590,10 +1590,17 @@ static wb_status mg_vcycle(wb_ctx* c, int side, int l, const double* b, double* 
   k_mg_resid<<<stream_blocks(n), VBS, 0, c->stream>>>(M.r[l], b, M.t[l], n);
   LAUNCH_CHECK(c);
   const int Nc = M.Ns[l + 1];
-  k_mg_restrict<<<stream_blocks((int64_t)Nc * Nc * Nc), VBS, 0, c->stream>>>(M.r[l], M.b[l + 1], Nc);
+  const bool pl = Nc == M.Ns[l];  // spectral level (same mesh, lower order)
+  if (pl)
+    k_mg_restrict_p<<<stream_blocks(4 * L->n_el), VBS, 0, c->stream>>>(M.r[l], M.b[l + 1], L->n_el, L->nm);
+  else
+    k_mg_restrict<<<stream_blocks((int64_t)Nc * Nc * Nc), VBS, 0, c->stream>>>(M.r[l], M.b[l + 1], Nc);
   LAUNCH_CHECK(c);
   if ((s = mg_vcycle(c, side, l + 1, M.b[l + 1], M.x[l + 1]))) return s;
-  k_mg_prolong_add<<<stream_blocks(L->n_el), VBS, 0, c->stream>>>(M.x[l + 1], x, Nc);
+  if (pl)
+    k_mg_prolong_add_p<<<stream_blocks(4 * L->n_el), VBS, 0, c->stream>>>(M.x[l + 1], x, L->n_el, L->nm);
+  else
+    k_mg_prolong_add<<<stream_blocks(L->n_el), VBS, 0, c->stream>>>(M.x[l + 1], x, Nc);
   LAUNCH_CHECK(c);
   if ((s = run_K(L, side, x, M.t[l]))) return s;
   k_mg_resid<<<stream_blocks(n), VBS, 0, c->stream>>>(M.r[l], b, M.t[l], n);
@@ -1696,8 +1703,9 @@ static wb_status mg_setup_body(wb_ctx* c, int nu, const double* mu0) {
   c->mg = M;
   M->nu = nu;
   int N = c->N;
-  M->Ns[M->nl++] = N;
-  while (N % 2 == 0 && N > 1 && M->nl < 16) { N /= 2; M->Ns[M->nl++] = N; }
+  M->Ns[M->nl] = N; M->Ks[M->nl++] = c->k;
+  if (c->k == 4) { M->Ns[M->nl] = N; M->Ks[M->nl++] = 2; }  // spectral level first
+  while (N % 2 == 0 && N > 1 && M->nl < 16) { N /= 2; M->Ns[M->nl] = N; M->Ks[M->nl++] = 2; }
   M->lev[0] = c;
   auto fail = [&](wb_status st, const char* what) {
     mg_free(c);
@@ -1705,7 +1713,7 @@ static wb_status mg_setup_body(wb_ctx* c, int nu, const double* mu0) {
   };
   for (int l = 1; l < M->nl; ++l) {
     wb_ctx* L = nullptr;
-    wb_status st = wb_create(&L, M->Ns[l], 2, 0, (void*)c->stream);
+    wb_status st = wb_create(&L, M->Ns[l], M->Ks[l], 0, (void*)c->stream);
     if (st) return fail(st, "level context");
     M->lev[l] = L;
     wb_ctx* F = M->lev[l - 1];
@@ -1717,7 +1725,10 @@ static wb_status mg_setup_body(wb_ctx* c, int nu, const double* mu0) {
       if ((st = setup_t<2>(L, M->mu[l], 1.0, 1.0))) return fail(st, wb_last_error(L));
     }
     CUDA_TRY(c, cudaMemsetAsync(L->icount, 0, sizeof(unsigned long long) * 4, c->stream));
-    k_mg_inject<<<stream_blocks(L->n_nodes), VBS, 0, c->stream>>>(F->Cw, F->Dw, L->Cw, L->Dw, M->Ns[l]);
+    if (M->Ns[l] == M->Ns[l - 1])
+      k_mg_inject_p<<<stream_blocks(L->n_nodes), VBS, 0, c->stream>>>(F->Cw, F->Dw, L->Cw, L->Dw, M->Ns[l]);
+    else
+      k_mg_inject<<<stream_blocks(L->n_nodes), VBS, 0, c->stream>>>(F->Cw, F->Dw, L->Cw, L->Dw, M->Ns[l]);
     LAUNCH_CHECK(c);
     k_inv_lumped<<<stream_blocks(L->n_nodes), VBS, 0, c->stream>>>(L->Cw, L->Dw, L->Cinv, L->Dinv, L->icount + 1,
                                                                    L->G);
@@ -1946,7 +1957,8 @@ wb_status wb_load_vector(wb_ctx* c, const double* fq, double* F) {
 wb_status wb_setup_mg(wb_ctx* c, int nu, const double* mu_q) {
   wb_status s = check_ctx(c, true);
   if (s) return s;
-  if (c->k != 2) return set_err(c, WB_EINVAL, "the multigrid is built for k = 2 (R20, R22)");
+  if (c->k != 2 && c->k != 4) return set_err(c, WB_EINVAL, "the multigrid is built for k = 2 and 4 (R20)");
+  if (c->k != 2 && mu_q) return set_err(c, WB_EINVAL, "the velocity multigrid is built for k = 2 (R22)");
   if (nu < 1 || nu > 16) return set_err(c, WB_EINVAL, "nu must be in [1, 16]");
   return mg_setup(c, nu, mu_q);
 }
@@ -2250,14 +2262,16 @@ wb_status wb_query(wb_ctx* c, const char* key, double* value) {
     const int l = atoi(key + 11);
     if (!c->mg || !c->mg->vel || l < 0 || l >= c->mg->nl) return set_err(c, WB_EINVAL, "bad key '%s'", key);
     *value = c->mg->vlam[l];
-  } else if (!strncmp(key, "mg_N_", 5) || !strncmp(key, "mg_lambda_", 10) || !strncmp(key, "mg_nonpos_", 10)) {
+  } else if (!strncmp(key, "mg_N_", 5) || !strncmp(key, "mg_k_", 5) || !strncmp(key, "mg_lambda_", 10) ||
+             !strncmp(key, "mg_nonpos_", 10)) {
     // mg_N_<l>; mg_lambda_<side>_<l> (Chebyshev interval scale); mg_nonpos_<side>_<l>
     if (!c->mg) return set_err(c, WB_ESTATE, "no multigrid hierarchy (wb_setup_mg)");
     int side = 0, l = -1;
-    if (key[3] == 'N') l = atoi(key + 5);
+    if (key[3] == 'N' || key[3] == 'k') l = atoi(key + 5);
     else if (sscanf(key + (key[3] == 'l' ? 10 : 10), "%d_%d", &side, &l) != 2) l = -1;
     if (l < 0 || l >= c->mg->nl || side < 0 || side > 1) return set_err(c, WB_EINVAL, "bad multigrid key '%s'", key);
     if (key[3] == 'N') *value = c->mg->Ns[l];
+    else if (key[3] == 'k') *value = c->mg->Ks[l];
     else if (key[3] == 'l') *value = c->mg->lam[side][l];
     else {
       wb_status st = read_nonpos(c->mg->lev[l]);

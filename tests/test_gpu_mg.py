@@ -8,7 +8,7 @@ from tests.gpu_common import Pair, dev, empty, host, rel_l2
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("C2", None), ("C3", None), ("C1", None), ("C2", 8)]
+CASES = [("C2", None), ("C3", None), ("C1", None), ("C2", 8), ("C4", 8), ("C4", None)]
 
 
 @pytest.fixture(scope="module", params=CASES, ids=lambda c: f"{c[0]}-N{c[1]}")
@@ -17,8 +17,8 @@ def mgpair(request):
     cfg, N = request.param
     P = Pair(cfg, N)
     P.ctx.setup_mg(3)
-    P.mg_l = omg.MG(P.N, P.ost["Cw"])
-    P.mg_r = omg.MG(P.N, P.ost["Dw"])
+    P.mg_l = omg.MG(P.N, P.ost["Cw"], k=P.k)
+    P.mg_r = omg.MG(P.N, P.ost["Dw"], k=P.k)
     return P
 
 
@@ -27,8 +27,8 @@ def test_levels_weights_and_intervals(mgpair):
     c = P.ctx
     assert int(c.query("mg_levels")) == len(P.mg_r.levels)
     for l, (Ll, Lr) in enumerate(zip(P.mg_l.levels, P.mg_r.levels)):
-        assert int(c.query(f"mg_N_{l}")) == Lr.N
-        n = (2 * Lr.N + 1) ** 3
+        assert int(c.query(f"mg_N_{l}")) == Lr.N and int(c.query(f"mg_k_{l}")) == Lr.o.k
+        n = (Lr.o.k * Lr.N + 1) ** 3
         Cg, Dg = empty(n), empty(n)
         c.mg_get_lumped(l, Cg, Dg)
         for g, o in ((Cg, Ll.C), (Dg, Lr.C)):
@@ -113,3 +113,24 @@ def test_full_size_c5_mgcg():
     bp = P.o.project(b)
     x = host(P.ctx.poisson_mgcg(1, dev(bp), empty(P.ctx.n_p), 30))
     assert P.o.poisson_relres(P.ost["Dinv"], bp, x) < 1e-6
+
+
+def test_k4_pmg_convergence():
+    """C4 (24^3, Q4 x P3disc, DR 1e6): the p/h multigrid (spectral level, then h-levels) as
+    PCG preconditioner reaches a 1e-6 reduction in far fewer iterations than Jacobi-PCG."""
+    P = Pair("C4")
+    P.ctx.setup_mg(3)
+    assert [int(P.ctx.query(f"mg_k_{l}")) for l in range(int(P.ctx.query("mg_levels")))] == [4, 2, 2, 2, 2]
+    st = P.ost
+    b = P.o.project(P.inp["p"])
+    bd = dev(b)
+    got = None
+    for it in range(10, 80, 5):
+        x = host(P.ctx.poisson_mgcg(1, bd, empty(P.ctx.n_p), it))
+        if P.o.poisson_relres(st["Dinv"], b, x) < 1e-6:
+            got = it
+            break
+    x = host(P.ctx.poisson_pcg(1, bd, empty(P.ctx.n_p), 4 * (got or 80)))
+    rr_j = P.o.poisson_relres(st["Dinv"], b, x)
+    print("C4 p/h-MG-PCG iterations to 1e-6:", got, "; Jacobi-PCG relres after 4x as many:", rr_j)
+    assert got is not None and rr_j > 1e-6
