@@ -333,25 +333,74 @@ def vrestrict(P1: np.ndarray, xf: np.ndarray) -> np.ndarray:
     return np.concatenate([_tp3(P1.T, xf[c * nf ** 3:(c + 1) * nf ** 3].reshape(nf, nf, nf)).ravel() for c in range(3)])
 
 
+def coarsen_mu_p(mu_f: np.ndarray, n_el: int, wg4: np.ndarray) -> np.ndarray:
+    """The spectral velocity level (k = 4 -> 2 on the same element): mu at the 3 Gauss points
+    per axis as the Gauss-weighted mean of the 5-point samples grouped by position (per axis
+    {0, 1} -> the point at -sqrt(3/5), {2} -> 0, {3, 4} -> +sqrt(3/5)), tensor product."""
+    groups = [[0, 1], [2], [3, 4]]
+    m = np.asarray(mu_f).reshape(n_el, 5, 5, 5)  # [e][qz][qy][qx]
+    out = np.zeros((n_el, 3, 3, 3))
+    for cz in range(3):
+        for cy in range(3):
+            for cx in range(3):
+                num, den = 0.0, 0.0
+                for iz in groups[cz]:
+                    for iy in groups[cy]:
+                        for ix in groups[cx]:
+                            w = wg4[ix] * wg4[iy] * wg4[iz]
+                            num = num + w * m[:, iz, iy, ix]
+                            den += w
+                out[:, cz, cy, cx] = num / den
+    return out.reshape(-1)
+
+
+def p_prolongation_1d(N: int, xn2: np.ndarray, xn4: np.ndarray) -> np.ndarray:
+    """P[i_f, I]: the Q2 nodal basis of each element evaluated at its Q4 GLL nodes (same mesh)."""
+    nf, nc = 4 * N + 1, 2 * N + 1
+    P = np.zeros((nf, nc))
+    for e in range(N):
+        for j in range(5):
+            t = xn4[j]
+            for a in range(3):
+                v = 1.0
+                for b in range(3):
+                    if b != a:
+                        v *= (t - xn2[b]) / (xn2[a] - xn2[b])
+                P[4 * e + j, 2 * e + a] = v
+    return P
+
+
 class VMG:
     """V-cycle hierarchy of the masked viscous block M A M (R22): levels as the pressure
-    multigrid, A_l re-discretised with the coarsened mu, Q2 nodal transfers, nu Chebyshev-
-    Jacobi steps (R18) on [0.1, 1.1] x a 20-step power estimate (splitmix64 start), 30 on the
-    coarsest level."""
+    multigrid (k = 4: first the spectral level to Q2 on the same mesh), A_l re-discretised with
+    the coarsened mu, Q2 (or Q2-in-Q4) nodal transfers, nu Chebyshev-Jacobi steps (R18) on
+    [0.1, 1.1] x a 20-step power estimate (splitmix64 start), 30 on the coarsest level."""
 
-    def __init__(self, N: int, mu_q: np.ndarray, nu: int = NU):
+    def __init__(self, N: int, mu_q: np.ndarray, nu: int = NU, k: int = 2):
+        assert k in (2, 4)
         self.nu = nu
-        self.Ns = levels_of(N)
+        self.spec = [(N, k)] + ([(N, 2)] if k == 4 else [])
+        while self.spec[-1][0] % 2 == 0 and self.spec[-1][0] > 1:
+            self.spec.append((self.spec[-1][0] // 2, 2))
+        self.Ns = [n for n, _ in self.spec]
         self.lev = []
         mu = np.asarray(mu_q, dtype=np.float64)
-        for li, Nl in enumerate(self.Ns):
-            o = Oracle(Nl, 2)
+        for li, (Nl, kl) in enumerate(self.spec):
+            o = Oracle(Nl, kl)
             if li > 0:
-                mu = coarsen_mu(mu, Nl, o.tables()["wg"])
+                if Nl == self.spec[li - 1][0]:
+                    mu = coarsen_mu_p(mu, o.n_el, self.lev[-1]["o"].tables()["wg"])
+                else:
+                    mu = coarsen_mu(mu, Nl, o.tables()["wg"])
             lam = o.velocity_eigmax(mu, splitmix_vector(o.n_v), EIG_ITERS)
             self.lev.append(dict(N=Nl, o=o, mu=mu, lam=lam, mask=o.boundary_mask().astype(bool)))
-        xn = self.lev[0]["o"].tables()["xn"]
-        self.P = [q2_prolongation_1d(self.Ns[l + 1], xn) for l in range(len(self.Ns) - 1)]
+        xn2 = Oracle(1, 2).tables()["xn"]
+        self.P = []
+        for l in range(len(self.spec) - 1):
+            if self.spec[l][0] == self.spec[l + 1][0]:
+                self.P.append(p_prolongation_1d(self.Ns[l], xn2, self.lev[l]["o"].tables()["xn"]))
+            else:
+                self.P.append(q2_prolongation_1d(self.Ns[l + 1], xn2))
 
     def A(self, l, v):
         L = self.lev[l]

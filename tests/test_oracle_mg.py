@@ -293,3 +293,31 @@ def test_k4_mg_beats_jacobi():
     minv = np.where(np.abs(L0.diagK) > 1e-13 * np.abs(L0.diagK).max(), 1 / L0.diagK, 0.0)
     its_j = _iters_to(o, L0.K, lambda r: minv * r, b)
     assert its < 60 and its_j > 4 * its, (its, its_j)  # measured 52 vs 317
+
+
+def test_velocity_p_level():
+    """k = 4 velocity hierarchy: the Q2-in-Q4 prolongation reproduces a Q2 field exactly at the
+    Q4 nodes; the spectral mu coarsening is exact on constants; the V-cycle stays symmetric."""
+    N = 2
+    o4, o2 = Oracle(N, 4), Oracle(N, 2)
+    P1 = omg.p_prolongation_1d(N, o2.tables()["xn"], o4.tables()["xn"])
+
+    def nodes(o):
+        xn = o.tables()["xn"]
+        k = o.k
+        line = np.concatenate([[(e + (xn[a] + 1) / 2) / N for a in range(k)] for e in range(N)] + [[1.0]])
+        Z, Y, X = np.meshgrid(line, line, line, indexing="ij")
+        return X.ravel(), Y.ravel(), Z.ravel()
+
+    u = lambda x, y, z: (x * x - y) * z * (1 - z)  # noqa: E731
+    zc = np.zeros((2 * N + 1) ** 3)
+    xf = omg.vprolong(P1, np.concatenate([u(*nodes(o2)), zc, zc]))
+    assert np.allclose(xf[:(4 * N + 1) ** 3], u(*nodes(o4)), atol=1e-14)
+    assert np.allclose(omg.coarsen_mu_p(np.full(o4.n_el * 125, 3.0), o4.n_el, o4.tables()["wg"]), 3.0, rtol=1e-15)
+    mu = np.random.default_rng(0).uniform(0.5, 2.0, o4.n_el * 125)
+    V = omg.VMG(N, mu, k=4)
+    assert [(L["N"], L["o"].k) for L in V.lev] == [(2, 4), (2, 2), (1, 2)]
+    mask = o4.boundary_mask().astype(bool)
+    rng = np.random.default_rng(1)
+    a, b = (np.where(mask, 0.0, rng.standard_normal(o4.n_v)) for _ in range(2))
+    assert V.vcycle(a) @ b == pytest.approx(a @ V.vcycle(b), rel=1e-10)
