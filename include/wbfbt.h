@@ -184,8 +184,9 @@ wb_status wb_load_vector(wb_ctx* ctx, const double* fq, double* F);
  * hierarchy of A is built too (R22: mu coarsened level by level; A
  * re-discretised; Q2 nodal interpolation and its transpose as transfers; the same smoother
  * on A, R18).  Allocates one internal context per coarse level and synchronises the stream.
- * WB_EINVAL for k not 2 or 4, mu_q with k = 4 (the velocity multigrid is k = 2) or nu out of
- * range, WB_ESTATE before wb_set_viscosity, WB_ENOMEM.  Queries "mg_N_<l>", "mg_k_<l>" give each
+ * For k = 4 the velocity hierarchy starts with the spectral level too (Q2-in-Q4 nodal transfers,
+ * mu grouped onto the Q2 Gauss points).  WB_EINVAL for k not 2 or 4 or nu out of range,
+ * WB_ESTATE before wb_set_viscosity, WB_ENOMEM.  Queries "mg_N_<l>", "mg_k_<l>" give each
  * level's mesh and order. */
 wb_status wb_setup_mg(wb_ctx* ctx, int nu, const double* mu_q);
 /* x = V(b), one velocity V-cycle on M A M (b, x: device SoA n_v; boundary entries of b are

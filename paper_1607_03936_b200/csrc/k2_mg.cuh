@@ -294,3 +294,115 @@ __global__ void k_mg_prolong_add_p(const double* __restrict__ xc, double* __rest
 }
 
 }  // namespace wb
+
+namespace wb {
+
+// ---- velocity spectral level for k = 4 (R22): Q4 -> Q2 on the same mesh
+// mu at the 27 Q2 Gauss points from the 125 Q4 ones: per axis the 5-point samples grouped
+// {0, 1}, {2}, {3, 4} (by position), Gauss-weighted mean of the tensor-product group
+__global__ void k_mu_coarsen_p(const double* __restrict__ mu4, double* __restrict__ mu2, int64_t n_el) {
+  const int64_t n = n_el * 27;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(i % 27);
+    const int64_t e = i / 27;
+    const int cq[3] = {q % 3, (q / 3) % 3, q / 9};
+    int lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) { lo[d] = cq[d] == 0 ? 0 : (cq[d] == 1 ? 2 : 3); hi[d] = cq[d] == 0 ? 1 : (cq[d] == 1 ? 2 : 4); }
+    const double* m = mu4 + e * 125;
+    double num = 0.0, den = 0.0;
+    for (int iz = lo[2]; iz <= hi[2]; ++iz)
+      for (int iy = lo[1]; iy <= hi[1]; ++iy)
+        for (int ix = lo[0]; ix <= hi[0]; ++ix) {
+          const double w = TB(4).w[ix] * TB(4).w[iy] * TB(4).w[iz];
+          num = fma(w, m[ix + 5 * (iy + 5 * iz)], num);
+          den += w;
+        }
+    mu2[i] = num / den;
+  }
+}
+
+// Q2 basis at the Q4 GLL abscissae -1, -s, 0, s, 1 (s = sqrt(3/7)): W[a2][a4]
+__device__ __forceinline__ double vmgp_w(int a2, int a4) {
+  const double s = 0.65465367070797714380, s2 = 3.0 / 7.0;  // sqrt(3/7)
+  const double t = a4 == 0 ? -1.0 : (a4 == 1 ? -s : (a4 == 2 ? 0.0 : (a4 == 3 ? s : 1.0)));
+  const double t2 = a4 == 1 || a4 == 3 ? s2 : t * t;
+  if (a2 == 0) return 0.5 * (t2 - t);
+  if (a2 == 1) return 1.0 - t2;
+  return 0.5 * (t2 + t);
+}
+// per-axis coupling list of coarse (Q2) node I with fine (Q4) nodes j and weights (<= 7)
+__device__ __forceinline__ int vmgp_list(int I, int N, int* j, double* w) {
+  int n = 0;
+  if (I & 1) {  // mid-node of element e: its interior Q4 nodes
+    const int e = I >> 1;
+    for (int a4 = 1; a4 <= 3; ++a4) { j[n] = 4 * e + a4; w[n] = vmgp_w(1, a4); ++n; }
+  } else {
+    const int e = I >> 1;
+    if (e >= 1)
+      for (int a4 = 1; a4 <= 3; ++a4) { j[n] = 4 * (e - 1) + a4; w[n] = vmgp_w(2, a4); ++n; }
+    j[n] = 4 * e; w[n] = 1.0; ++n;
+    if (e < N)
+      for (int a4 = 1; a4 <= 3; ++a4) { j[n] = 4 * e + a4; w[n] = vmgp_w(0, a4); ++n; }
+  }
+  return n;
+}
+// r_c = P^T (M r_f) (Q4 grid -> Q2 grid, same mesh), coarse boundary rows 0
+__global__ void k_vmg_restrict_p(const double* __restrict__ rf, double* __restrict__ rc, int N) {
+  const int nc = 2 * N + 1, nf = 4 * N + 1;
+  const int64_t nnc = (int64_t)nc * nc * nc, nnf = (int64_t)nf * nf * nf;
+  for (int64_t G = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; G < nnc; G += (int64_t)gridDim.x * blockDim.x) {
+    const int I[3] = {(int)(G % nc), (int)((G / nc) % nc), (int)(G / ((int64_t)nc * nc))};
+    if (node_bnd(I[0], I[1], I[2], nc)) { rc[G] = 0.0; rc[nnc + G] = 0.0; rc[2 * nnc + G] = 0.0; continue; }
+    int jx[7], jy[7], jz[7];
+    double wx[7], wy[7], wz[7];
+    const int nx = vmgp_list(I[0], N, jx, wx), ny = vmgp_list(I[1], N, jy, wy), nz = vmgp_list(I[2], N, jz, wz);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int kz = 0; kz < nz; ++kz)
+      for (int ky = 0; ky < ny; ++ky)
+        for (int kx = 0; kx < nx; ++kx) {
+          if (node_bnd(jx[kx], jy[ky], jz[kz], nf)) continue;
+          const double w = wx[kx] * wy[ky] * wz[kz];
+          const int64_t f = (int64_t)jx[kx] + (int64_t)nf * ((int64_t)jy[ky] + (int64_t)nf * jz[kz]);
+          a0 = fma(w, rf[f], a0);
+          a1 = fma(w, rf[nnf + f], a1);
+          a2 = fma(w, rf[2 * nnf + f], a2);
+        }
+    rc[G] = a0; rc[nnc + G] = a1; rc[2 * nnc + G] = a2;
+  }
+}
+// x_f += P x_c at the interior Q4 nodes
+__global__ void k_vmg_prolong_add_p(const double* __restrict__ xc, double* __restrict__ xf, int N) {
+  const int nc = 2 * N + 1, nf = 4 * N + 1;
+  const int64_t nnc = (int64_t)nc * nc * nc, nnf = (int64_t)nf * nf * nf;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < nnf; g += (int64_t)gridDim.x * blockDim.x) {
+    const int f[3] = {(int)(g % nf), (int)((g / nf) % nf), (int)(g / ((int64_t)nf * nf))};
+    if (node_bnd(f[0], f[1], f[2], nf)) continue;
+    int I[3][3], n[3];
+    double w[3][3];
+    for (int d = 0; d < 3; ++d) {
+      const int j = f[d];
+      if ((j & 3) == 0) { I[d][0] = j >> 1; w[d][0] = 1.0; n[d] = 1; }
+      else {
+        const int e = j >> 2, a4 = j & 3;
+        n[d] = 0;
+        for (int a2 = 0; a2 < 3; ++a2) {
+          const double ww = vmgp_w(a2, a4);
+          if (ww != 0.0) { I[d][n[d]] = 2 * e + a2; w[d][n[d]] = ww; ++n[d]; }
+        }
+      }
+    }
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int kz = 0; kz < n[2]; ++kz)
+      for (int ky = 0; ky < n[1]; ++ky)
+        for (int kx = 0; kx < n[0]; ++kx) {
+          const double ww = w[0][kx] * w[1][ky] * w[2][kz];
+          const int64_t G = (int64_t)I[0][kx] + (int64_t)nc * ((int64_t)I[1][ky] + (int64_t)nc * I[2][kz]);
+          a0 = fma(ww, xc[G], a0);
+          a1 = fma(ww, xc[nnc + G], a1);
+          a2 = fma(ww, xc[2 * nnc + G], a2);
+        }
+    xf[g] += a0; xf[nnf + g] += a1; xf[2 * nnf + g] += a2;
+  }
+}
+
+}  // namespace wb

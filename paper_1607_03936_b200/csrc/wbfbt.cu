@@ -1657,10 +1657,17 @@ static wb_status vmg_vcycle(wb_ctx* c, int l, const double* b, double* x) {
   k_mg_resid<<<stream_blocks(n), VBS, 0, c->stream>>>(M.vr[l], b, M.vt[l], n);
   LAUNCH_CHECK(c);
   const int Nc = M.Ns[l + 1];
-  k_vmg_restrict<<<stream_blocks(M.lev[l + 1]->n_nodes), VBS, 0, c->stream>>>(M.vr[l], M.vb[l + 1], Nc);
+  const bool pl = Nc == M.Ns[l];  // spectral level (Q4 -> Q2 on the same mesh)
+  if (pl)
+    k_vmg_restrict_p<<<stream_blocks(M.lev[l + 1]->n_nodes), VBS, 0, c->stream>>>(M.vr[l], M.vb[l + 1], Nc);
+  else
+    k_vmg_restrict<<<stream_blocks(M.lev[l + 1]->n_nodes), VBS, 0, c->stream>>>(M.vr[l], M.vb[l + 1], Nc);
   LAUNCH_CHECK(c);
   if ((s = vmg_vcycle(c, l + 1, M.vb[l + 1], M.vx[l + 1]))) return s;
-  k_vmg_prolong_add<<<stream_blocks(L->n_nodes), VBS, 0, c->stream>>>(M.vx[l + 1], x, Nc);
+  if (pl)
+    k_vmg_prolong_add_p<<<stream_blocks(L->n_nodes), VBS, 0, c->stream>>>(M.vx[l + 1], x, Nc);
+  else
+    k_vmg_prolong_add<<<stream_blocks(L->n_nodes), VBS, 0, c->stream>>>(M.vx[l + 1], x, Nc);
   LAUNCH_CHECK(c);
   if ((s = run_A(L, x, M.vt[l], 0))) return s;
   k_mg_resid<<<stream_blocks(n), VBS, 0, c->stream>>>(M.vr[l], b, M.vt[l], n);
@@ -1720,7 +1727,10 @@ static wb_status mg_setup_body(wb_ctx* c, int nu, const double* mu0) {
     if (mu0) {  // velocity hierarchy: coarsened viscosity, the level's A (and, overwritten below, its lumping)
       if (!lazy_alloc(&M->mu[l], L->n_el * 27)) return fail(WB_ENOMEM, "coarse viscosity");
       const double* muf = l == 1 ? mu0 : M->mu[l - 1];
-      k_mu_coarsen<<<stream_blocks(L->n_el * 27), VBS, 0, c->stream>>>(muf, M->mu[l], M->Ns[l]);
+      if (M->Ns[l] == M->Ns[l - 1])  // spectral level: 125 -> 27 Gauss points per element
+        k_mu_coarsen_p<<<stream_blocks(L->n_el * 27), VBS, 0, c->stream>>>(muf, M->mu[l], L->n_el);
+      else
+        k_mu_coarsen<<<stream_blocks(L->n_el * 27), VBS, 0, c->stream>>>(muf, M->mu[l], M->Ns[l]);
       LAUNCH_CHECK(c);
       if ((st = setup_t<2>(L, M->mu[l], 1.0, 1.0))) return fail(st, wb_last_error(L));
     }
@@ -1958,7 +1968,6 @@ wb_status wb_setup_mg(wb_ctx* c, int nu, const double* mu_q) {
   wb_status s = check_ctx(c, true);
   if (s) return s;
   if (c->k != 2 && c->k != 4) return set_err(c, WB_EINVAL, "the multigrid is built for k = 2 and 4 (R20)");
-  if (c->k != 2 && mu_q) return set_err(c, WB_EINVAL, "the velocity multigrid is built for k = 2 (R22)");
   if (nu < 1 || nu > 16) return set_err(c, WB_EINVAL, "nu must be in [1, 16]");
   return mg_setup(c, nu, mu_q);
 }

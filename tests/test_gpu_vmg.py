@@ -10,13 +10,14 @@ from tests.gpu_common import Pair, dev, empty, host, rel_l2
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module", params=[("C2", None), ("C3", None)], ids=lambda c: c[0])
+@pytest.fixture(scope="module", params=[("C2", None), ("C3", None), ("C4", 4)], ids=lambda c: c[0])
 def vpair(request):
     from oracle import mg as omg
     cfg, N = request.param
     P = Pair(cfg, N)
     P.ctx.setup_mg(3, P.mu)
-    P.vmg = omg.VMG(P.N, P.inp["mu_q"])
+    P.vmg = omg.VMG(P.N, P.inp["mu_q"], k=P.k)
+    assert P.ctx.query("mg_levels") == len(P.vmg.lev)
     return P
 
 
@@ -36,12 +37,13 @@ def _forcing(P):
     return synth.forcing_at_quadrature(P.N, P.k, P.inp["centers"], c.delta, c.omega)
 
 
-def test_stokes_full_mg_matches_oracle():
+@pytest.mark.parametrize("cfg,N", [("C2", None), ("C4", 4)])
+def test_stokes_full_mg_matches_oracle(cfg, N):
     """FGMRES, 4 iterations, At^-1 = one velocity V-cycle, wBFBT with MG-PCG(3) inner solves:
-    GPU vs oracle <= 1e-8."""
+    GPU vs oracle <= 1e-8 (C4: both hierarchies start with the spectral level)."""
     from oracle import mg as omg
     from oracle import stokes as ost
-    P = Pair("C2")
+    P = Pair(cfg, N)
     c = P.ctx
     c.setup_mg(3, P.mu)
     c.set_inner_mg(3)
@@ -51,8 +53,8 @@ def test_stokes_full_mg_matches_oracle():
     u, p = empty(c.n_v), empty(c.n_p)
     _, _, it, rr = c.stokes_fgmres(dev(f), dev(g), u, p, 10, 4, 0.0, 10, 6, 1.0, 2.0)
     mu = P.inp["mu_q"]
-    ml, mr = omg.MG(P.N, P.ost["Cw"]), omg.MG(P.N, P.ost["Dw"])
-    V = omg.VMG(P.N, mu)
+    ml, mr = omg.MG(P.N, P.ost["Cw"], k=P.k), omg.MG(P.N, P.ost["Dw"], k=P.k)
+    V = omg.VMG(P.N, mu, k=P.k)
     so = ost.StokesOracle(P.o, mu, lambda b: omg.wbfbt_mg(P.o, mu, P.ost, ml, mr, b, 3), 6, 1.0, 2.0,
                           ainv=lambda a: V.cycles(a, 1))
     uo, po, ito, rro = so.solve(f, g, 10, 4, 0.0)
@@ -98,6 +100,14 @@ def test_stokes_c5_converges_and_wbfbt_beats_mp():
     it_mp, rr_mp = _solve("C5", 2, max_iters=it)
     print("C5 M_p(1/mu) after", it_mp, "iterations: relres", rr_mp)
     assert rr_mp > 10 * rr
+
+
+def test_stokes_c4_converges_with_spectral_levels():
+    """C4 (24^3, Q4 x P3disc, DR 1e6): with the spectral level in both multigrids the solve
+    reaches the 1e-6 reduction."""
+    it, rr = _solve("C4", 0, max_iters=300)
+    print("C4 FGMRES iterations to 1e-6 (wBFBT, MG inner, 2 velocity V-cycles):", it, rr)
+    assert rr <= 1e-6
 
 
 def test_stokes_restart_growth():
