@@ -1,0 +1,517 @@
+// k4_fused.cuh -- fused high-order Poisson operator q = K_w p = B X B^T p (rows a8, a9 for
+// k = 3, 4; C4 is Q4 x P3disc), with the PCG direction update folded in, in one kernel.
+//
+// K_w = B X^-1 B^T on P_{k-1}^disc (eq:wbfbt PAPER.md:439-445), X = C_w^-1
+// or D_w^-1 per node (0 on the Dirichlet boundary: the mask).  The element divergence matrix is
+// a product of 1-D integrals:
+//   B_e[(m1,m2,m3),(c,a)] = sB prod_d M_cd[m_d][a_d],  M_cd = BD if d == c else BI,
+// so on the structured mesh B^T is, per component c, a tensor product of three ASSEMBLED 1-D
+// operators (element modes -> nodes, the shared element-end node receiving from both sides):
+//   (B^T p)_c = sB sum_m (T^c_x,m1 (x) T^c_y,m2 (x) T^c_z,m3) p_m.
+// A CTA takes a TX x TY x TZ element tile.  It loads p (after the update p = z + beta p_old,
+// z = Minv r stored by the PCG update kernel) on the tile plus one halo element layer, and
+// contracts one axis at a time into the tile's (kT+1)^3 nodes, so the tile-face nodes get
+// their neighbours' contributions without any exchange:
+//   Z : Wz[pair(m1,m2)][ly][lx][nz] = sum_{lz, m3} T_z  p        (halo columns included)
+//   Y : Wy[m1][lx][ny][nz]          = sum_{ly, m2} T_y  Wz
+//   X : y_c(nx,ny,nz) = sB X(n) sum_{lx, m1} T_x Wy              (the node line in registers)
+// then B restricted to the tile's own elements, the same 1-D factors transposed:
+//   X': V[m1][lx'][ny][nz] = sum_nx T_x y_c   (same thread, no shared-memory round trip)
+//   Y': U[pair][ly'][lx'][nz] = sum_ny T_y V
+//   Z': q[e][m] += sum_nz T_z U          (accumulated over c in registers; q = sB acc)
+// Each 1-D contraction walks its line element by element with a two-element sliding window
+// (the shared end node takes the lower element's node K and the upper one's node 0), so the
+// loops stay rolled: the kernel is compact (instruction-cache resident).  Stages with a
+// triangular mode index give every warp ONE group (m1 + m2 for Z / Z', m1 for Y / Y'), padded
+// to whole warps, so their mode loops are compile-time.  The component loop is a runtime loop;
+// each stage loads its 1-D table (BI or BD by axis and component) into registers.
+// Every node value is a sum over its elements in a fixed order: bitwise reproducible.
+// mode (as k_K2_fused): 0 -> p = z; 1 -> p = z + beta p_old; 2 -> p = p_old.
+// ctl: PCG control of iteration it (pcg_control); <p, q> block partials -> pqp (one per CTA).
+#pragma once
+#include "kernels.cuh"
+#include "mbar.cuh"
+
+namespace wb {
+
+template <int K, int TX, int TY, int TZ, bool TMA = false>
+struct FK4 {
+  static constexpr int NM = K * (K + 1) * (K + 2) / 6, NP = K * (K + 1) / 2;
+  static constexpr int EX = TX + 2, EY = TY + 2, EZ = TZ + 2;             // extended (halo) elements
+  static constexpr int NX = K * TX + 1, NY = K * TY + 1, NZ = K * TZ + 1;  // tile nodes per axis
+  static constexpr int NEH = EX * EY * EZ;
+  static constexpr int PE = NM * NEH;           // Pe[m][lz][ly][lx]
+  // X at the tile nodes, rows of XR (TMA: even, the box's 16-byte inner extent)
+  static constexpr int XR = TMA ? (NX + 1) / 2 * 2 : NX;
+  static constexpr int XS = XR * NY * NZ;       // Xs[nz][ny][XR]
+  static constexpr int WZ = NP * EY * EX * NZ;  // Wz[p][ly][lx][nz]
+  static constexpr int WY = K * EX * NY * NZ;   // Wy[m1][lx][ny][nz]
+  static constexpr int VV = K * TX * NY * NZ;   // V[m1][lx'][ny][nz]   (in the Wz space)
+  static constexpr int UU = NP * TY * TX * NZ;  // U[p][ly'][lx'][nz]   (in the Wy space)
+  static_assert(VV <= WZ && UU <= WY, "V / U must fit the Wz / Wy spaces");
+  // TMA staging of the z and p_old halo boxes (in the Wz / Wy spaces): x from ex0 - 2 (the
+  // start must be 16-byte aligned: TX even), 8 wide, [m][lz][ly][8]
+  static constexpr int BX = 8, BOX = BX * EY * EZ * NM;
+  static_assert(!TMA || (TX % 2 == 0 && EX + 1 <= BX), "TMA boxes need an even TX <= 6");
+  static constexpr int al16(int n) { return (n + 15) / 16 * 16; }  // 128-byte multiples of doubles
+  static constexpr int mxx(int a, int b) { return a > b ? a : b; }
+  static constexpr int SZ = al16(TMA ? mxx(WZ, BOX) : WZ), SY = al16(TMA ? mxx(WY, BOX) : WY);
+  static constexpr int OFF_XS = al16(PE), OFF_WZ = OFF_XS + al16(XS), OFF_WY = OFF_WZ + SZ, OFF_T = OFF_WY + SY;
+  static constexpr int TABS = 2 * K * (K + 1);  // BI, BD copies
+  static constexpr int OFF_B = OFF_T + al16(TABS);
+  static constexpr int SMEM = OFF_B * 8 + 16;   // + the mbarrier
+  static constexpr unsigned BOXB = BOX * 8u, XB = XS * 8u;
+  static constexpr int w32(int n) { return (n + 31) / 32 * 32; }
+  static constexpr int GWZ = w32(EX * EY), GWY = w32(EX * NZ), GWY2 = w32(TX * NZ), GWZ2 = w32(TX * TY);
+  static constexpr int IX = NY * NZ;
+  static constexpr int mx(int a, int b) { return a > b ? a : b; }
+  static constexpr int NTH = mx(mx(K * GWZ, K * GWY), mx(mx(w32(IX), K * GWY2), K * GWZ2));
+};
+
+// X = C_w^-1 or D_w^-1 with rows padded to nn1 + 1 (an even, 16-byte row stride for the
+// TMA tensor map of the k = 4 kernel); the pad column is 0
+__global__ void k_xpad4(const double* __restrict__ XL, const double* __restrict__ XR, double* __restrict__ PL,
+                        double* __restrict__ PR, int nn1) {
+  const int64_t rp = nn1 + 1, n = rp * nn1 * nn1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int gx = (int)(i % rp);
+    const int64_t row = i / rp;
+    const bool in = gx < nn1;
+    PL[i] = in ? XL[row * nn1 + gx] : 0.0;
+    PR[i] = in ? XR[row * nn1 + gx] : 0.0;
+  }
+}
+
+// pair index of (m1, m2), m1 + m2 <= K-1: for m1: for m2 (m1 outer)
+template <int K>
+__host__ __device__ constexpr int k4_pair(int m1, int m2) { return m1 * K - m1 * (m1 - 1) / 2 + m2; }
+// mode index of (m1, m2, m3) in the R2 order: for d: for m3 <= d: for m2 <= d - m3: m1 = d - m2 - m3
+__host__ __device__ constexpr int k4_mode(int m1, int m2, int m3) {
+  return (m1 + m2 + m3) * (m1 + m2 + m3 + 1) * (m1 + m2 + m3 + 2) / 6 + m3 * (m1 + m2 + m3 + 1) -
+         m3 * (m3 - 1) / 2 + m2;
+}
+// rows m < NR of a 1-D table ([K][K+1] in shared memory) into registers.  (Measured: the
+// table as compile-time constant-bank operands, one code copy per BI / BD, is slower: 33.9
+// vs 30.3 us per C4 PCG iteration -- the doubled code misses the instruction cache.)
+template <int K, int NR>
+__device__ __forceinline__ void k4_tab(const double* __restrict__ T, double (&M)[NR][K + 1]) {
+#pragma unroll
+  for (int m = 0; m < NR; ++m)
+#pragma unroll
+    for (int a = 0; a <= K; ++a) M[m][a] = T[m * (K + 1) + a];
+}
+
+// stage Z: thread (column lx + EX ly, degree group G = m1 + m2): pairs (G - j, j), m3 < K - G
+template <int K, int TX, int TY, int TZ, int G>
+__device__ __forceinline__ void k4_z_grp(const double* __restrict__ Pe, double* __restrict__ Wz, int col,
+                                         const double* __restrict__ Tz) {
+  using F = FK4<K, TX, TY, TZ>;
+  constexpr int NM3 = K - G;
+  double M[NM3][K + 1];
+  k4_tab<K, NM3>(Tz, M);
+#pragma unroll
+  for (int j = 0; j <= G; ++j) {
+    const int m1 = G - j, m2 = j;
+    double P[F::EZ][NM3];
+#pragma unroll
+    for (int lz = 0; lz < F::EZ; ++lz)
+#pragma unroll
+      for (int m3 = 0; m3 < NM3; ++m3) P[lz][m3] = Pe[col + k4_mode(m1, m2, m3) * F::NEH + lz * F::EX * F::EY];
+    double* out = Wz + k4_pair<K>(m1, m2) * (F::EY * F::EX * F::NZ) + col * F::NZ;
+#pragma unroll
+    for (int n = 0; n < F::NZ; ++n) {
+      const int l = n / K + 1, a = n % K;
+      double s = 0.0;
+#pragma unroll
+      for (int m3 = 0; m3 < NM3; ++m3) s = fma(M[m3][a], P[l][m3], s);
+      if (a == 0) {
+#pragma unroll
+        for (int m3 = 0; m3 < NM3; ++m3) s = fma(M[m3][K], P[l - 1][m3], s);
+      }
+      out[n] = s;
+    }
+  }
+}
+template <int K, int TX, int TY, int TZ>
+__device__ __forceinline__ void k4_stage_z(const double* __restrict__ Pe, double* __restrict__ Wz, int t,
+                                           const double* Tz) {
+  using F = FK4<K, TX, TY, TZ>;
+  const int g = t / F::GWZ, col = t % F::GWZ;
+  if (g >= K || col >= F::EX * F::EY) return;
+  switch (g) {
+    case 0: k4_z_grp<K, TX, TY, TZ, 0>(Pe, Wz, col, Tz); break;
+    case 1: k4_z_grp<K, TX, TY, TZ, 1>(Pe, Wz, col, Tz); break;
+    case 2: if constexpr (K > 2) k4_z_grp<K, TX, TY, TZ, (K > 2 ? 2 : 0)>(Pe, Wz, col, Tz); break;
+    default: if constexpr (K > 3) k4_z_grp<K, TX, TY, TZ, (K > 3 ? 3 : 0)>(Pe, Wz, col, Tz); break;
+  }
+}
+
+// stage Y: thread (nz, lx) of group m1 = M1 contracts (ly, m2 < K - M1)
+template <int K, int TX, int TY, int TZ, int M1>
+__device__ __forceinline__ void k4_y_grp(const double* __restrict__ Wz, double* __restrict__ Wy, int it,
+                                         const double* __restrict__ Ty) {
+  using F = FK4<K, TX, TY, TZ>;
+  constexpr int NM2 = K - M1;
+  double M[NM2][K + 1];
+  k4_tab<K, NM2>(Ty, M);
+  const int nz = it % F::NZ, lx = it / F::NZ;
+  const double* ib = Wz + lx * F::NZ + nz;
+  double R[F::EY][NM2];
+#pragma unroll
+  for (int ly = 0; ly < F::EY; ++ly)
+#pragma unroll
+    for (int m2 = 0; m2 < NM2; ++m2) R[ly][m2] = ib[(k4_pair<K>(M1, m2) * F::EY + ly) * F::EX * F::NZ];
+  double* out = Wy + ((M1 * F::EX + lx) * F::NY) * F::NZ + nz;
+#pragma unroll
+  for (int n = 0; n < F::NY; ++n) {
+    const int l = n / K + 1, a = n % K;
+    double s = 0.0;
+#pragma unroll
+    for (int m2 = 0; m2 < NM2; ++m2) s = fma(M[m2][a], R[l][m2], s);
+    if (a == 0) {
+#pragma unroll
+      for (int m2 = 0; m2 < NM2; ++m2) s = fma(M[m2][K], R[l - 1][m2], s);
+    }
+    out[n * F::NZ] = s;
+  }
+}
+template <int K, int TX, int TY, int TZ>
+__device__ __forceinline__ void k4_stage_y(const double* __restrict__ Wz, double* __restrict__ Wy, int t,
+                                           const double* Ty) {
+  using F = FK4<K, TX, TY, TZ>;
+  const int g = t / F::GWY, it = t % F::GWY;
+  if (g >= K || it >= F::EX * F::NZ) return;
+  switch (g) {
+    case 0: k4_y_grp<K, TX, TY, TZ, 0>(Wz, Wy, it, Ty); break;
+    case 1: k4_y_grp<K, TX, TY, TZ, 1>(Wz, Wy, it, Ty); break;
+    case 2: if constexpr (K > 2) k4_y_grp<K, TX, TY, TZ, (K > 2 ? 2 : 0)>(Wz, Wy, it, Ty); break;
+    default: if constexpr (K > 3) k4_y_grp<K, TX, TY, TZ, (K > 3 ? 3 : 0)>(Wz, Wy, it, Ty); break;
+  }
+}
+
+// stages X and X' on the node line (ny, nz): y = sB X B^T along x, then its x-contraction
+// onto the own elements' modes m1
+template <int K, int TX, int TY, int TZ, int XR>
+__device__ __forceinline__ void k4_stage_x(const double* __restrict__ Wy, const double* __restrict__ Xs,
+                                           double* __restrict__ V, int item, double sB,
+                                           const double* __restrict__ Tx) {
+  using F = FK4<K, TX, TY, TZ>;
+  if (item >= F::IX) return;
+  double M[K][K + 1];
+  k4_tab<K, K>(Tx, M);
+  const int nz = item % F::NZ, ny = item / F::NZ;
+  const double* ib = Wy + ny * F::NZ + nz;
+  double R[F::EX][K];
+#pragma unroll
+  for (int lx = 0; lx < F::EX; ++lx)
+#pragma unroll
+    for (int m1 = 0; m1 < K; ++m1) R[lx][m1] = ib[(m1 * F::EX + lx) * F::NY * F::NZ];
+  double acc[TX][K];
+#pragma unroll
+  for (int l = 0; l < TX; ++l)
+#pragma unroll
+    for (int m1 = 0; m1 < K; ++m1) acc[l][m1] = 0.0;
+  const double* xr = Xs + (nz * F::NY + ny) * XR;
+#pragma unroll
+  for (int n = 0; n < F::NX; ++n) {
+    const int l = n / K + 1, a = n % K;
+    double s = 0.0;
+#pragma unroll
+    for (int m1 = 0; m1 < K; ++m1) s = fma(M[m1][a], R[l][m1], s);
+    if (a == 0) {
+#pragma unroll
+      for (int m1 = 0; m1 < K; ++m1) s = fma(M[m1][K], R[l - 1][m1], s);
+    }
+    const double y = sB * xr[n] * s;  // X = 0 on the boundary and outside the mesh
+    if (l - 1 < TX) {
+#pragma unroll
+      for (int m1 = 0; m1 < K; ++m1) acc[l - 1][m1] = fma(M[m1][a], y, acc[l - 1][m1]);
+    }
+    if (a == 0 && l >= 2) {
+#pragma unroll
+      for (int m1 = 0; m1 < K; ++m1) acc[l - 2][m1] = fma(M[m1][K], y, acc[l - 2][m1]);
+    }
+  }
+  double* ob = V + ny * F::NZ + nz;
+#pragma unroll
+  for (int l = 0; l < TX; ++l)
+#pragma unroll
+    for (int m1 = 0; m1 < K; ++m1) ob[(m1 * TX + l) * F::NY * F::NZ] = acc[l][m1];
+}
+
+// stage Y': thread (nz, lx') of group m1 = M1: V line along y -> U rows (M1, m2)
+template <int K, int TX, int TY, int TZ, int M1>
+__device__ __forceinline__ void k4_y2_grp(const double* __restrict__ V, double* __restrict__ U, int it,
+                                          const double* __restrict__ Ty) {
+  using F = FK4<K, TX, TY, TZ>;
+  constexpr int NM2 = K - M1;
+  double M[NM2][K + 1];
+  k4_tab<K, NM2>(Ty, M);
+  const int nz = it % F::NZ, lx = it / F::NZ;
+  double acc[TY][NM2];
+#pragma unroll
+  for (int l = 0; l < TY; ++l)
+#pragma unroll
+    for (int m2 = 0; m2 < NM2; ++m2) acc[l][m2] = 0.0;
+  const double* in = V + ((M1 * TX + lx) * F::NY) * F::NZ + nz;
+#pragma unroll
+  for (int n = 0; n < F::NY; ++n) {
+    const int l = n / K + 1, a = n % K;
+    const double y = in[n * F::NZ];
+    if (l - 1 < TY) {
+#pragma unroll
+      for (int m2 = 0; m2 < NM2; ++m2) acc[l - 1][m2] = fma(M[m2][a], y, acc[l - 1][m2]);
+    }
+    if (a == 0 && l >= 2) {
+#pragma unroll
+      for (int m2 = 0; m2 < NM2; ++m2) acc[l - 2][m2] = fma(M[m2][K], y, acc[l - 2][m2]);
+    }
+  }
+  double* ob = U + lx * F::NZ + nz;
+#pragma unroll
+  for (int l = 0; l < TY; ++l)
+#pragma unroll
+    for (int m2 = 0; m2 < NM2; ++m2) ob[(k4_pair<K>(M1, m2) * TY + l) * TX * F::NZ] = acc[l][m2];
+}
+template <int K, int TX, int TY, int TZ>
+__device__ __forceinline__ void k4_stage_y2(const double* __restrict__ V, double* __restrict__ U, int t,
+                                            const double* Ty) {
+  using F = FK4<K, TX, TY, TZ>;
+  const int g = t / F::GWY2, it = t % F::GWY2;
+  if (g >= K || it >= TX * F::NZ) return;
+  switch (g) {
+    case 0: k4_y2_grp<K, TX, TY, TZ, 0>(V, U, it, Ty); break;
+    case 1: k4_y2_grp<K, TX, TY, TZ, 1>(V, U, it, Ty); break;
+    case 2: if constexpr (K > 2) k4_y2_grp<K, TX, TY, TZ, (K > 2 ? 2 : 0)>(V, U, it, Ty); break;
+    default: if constexpr (K > 3) k4_y2_grp<K, TX, TY, TZ, (K > 3 ? 3 : 0)>(V, U, it, Ty); break;
+  }
+}
+
+// stage Z': thread (lx', ly') of degree group G accumulates A[j][lz'][m3] over the components
+// (TZ is small: this loop is unrolled so the accumulators stay in registers)
+template <int K, int TZ>
+struct K4Acc {
+  double v[K][TZ][K];  // [pair j in the group][lz'][m3]  (only j <= G, m3 < K - G used)
+};
+template <int K, int TX, int TY, int TZ, int G>
+__device__ __forceinline__ void k4_z2_grp(const double* __restrict__ U, K4Acc<K, TZ>& A, int col,
+                                          const double* __restrict__ Tz) {
+  using F = FK4<K, TX, TY, TZ>;
+  constexpr int NM3 = K - G;
+  double M[NM3][K + 1];
+  k4_tab<K, NM3>(Tz, M);
+#pragma unroll
+  for (int j = 0; j <= G; ++j) {
+    const double* in = U + (k4_pair<K>(G - j, j) * TY * TX + col) * F::NZ;
+#pragma unroll
+    for (int n = 0; n < F::NZ; ++n) {
+      const int l = n / K + 1, a = n % K;
+      const double y = in[n];
+      if (l - 1 < TZ) {
+#pragma unroll
+        for (int m3 = 0; m3 < NM3; ++m3) A.v[j][l - 1][m3] = fma(M[m3][a], y, A.v[j][l - 1][m3]);
+      }
+      if (a == 0 && l >= 2) {
+#pragma unroll
+        for (int m3 = 0; m3 < NM3; ++m3) A.v[j][l - 2][m3] = fma(M[m3][K], y, A.v[j][l - 2][m3]);
+      }
+    }
+  }
+}
+template <int K, int TX, int TY, int TZ>
+__device__ __forceinline__ void k4_stage_z2(const double* __restrict__ U, K4Acc<K, TZ>& A, int t, const double* Tz) {
+  using F = FK4<K, TX, TY, TZ>;
+  const int g = t / F::GWZ2, col = t % F::GWZ2;
+  if (g >= K || col >= TX * TY) return;
+  switch (g) {
+    case 0: k4_z2_grp<K, TX, TY, TZ, 0>(U, A, col, Tz); break;
+    case 1: k4_z2_grp<K, TX, TY, TZ, 1>(U, A, col, Tz); break;
+    case 2: if constexpr (K > 2) k4_z2_grp<K, TX, TY, TZ, (K > 2 ? 2 : 0)>(U, A, col, Tz); break;
+    default: if constexpr (K > 3) k4_z2_grp<K, TX, TY, TZ, (K > 3 ? 3 : 0)>(U, A, col, Tz); break;
+  }
+}
+
+// q = sB acc for the group's modes of own element column (lx', ly'), <p, q> partial
+template <int K, int TX, int TY, int TZ, int G>
+__device__ __forceinline__ double k4_q_grp(const K4Acc<K, TZ>& A, const double* __restrict__ Pe, double* q, int col,
+                                           int ex0, int ey0, int ez0, int N, int64_t ne, double sB) {
+  using F = FK4<K, TX, TY, TZ>;
+  constexpr int NM3 = K - G;
+  const int lx = col % TX, ly = col / TX;
+  const int ex = ex0 + lx, ey = ey0 + ly;
+  double dot = 0.0;
+  if (ex >= N || ey >= N) return 0.0;
+#pragma unroll
+  for (int lz = 0; lz < TZ; ++lz) {
+    const int ez = ez0 + lz;
+    if (ez < N) {
+      const int64_t e = ex + (int64_t)N * (ey + (int64_t)N * ez);
+      const double* pe = Pe + ((lz + 1) * F::EY + ly + 1) * F::EX + lx + 1;
+#pragma unroll
+      for (int j = 0; j <= G; ++j)
+#pragma unroll
+        for (int m3 = 0; m3 < NM3; ++m3) {
+          const int m = k4_mode(G - j, j, m3);
+          const double o = sB * A.v[j][lz][m3];
+          q[(int64_t)m * ne + e] = o;
+          dot = fma(pe[m * F::NEH], o, dot);
+        }
+    }
+  }
+  return dot;
+}
+
+template <int K, int TX, int TY, int TZ, int MINB, bool TMA>
+__global__ void __launch_bounds__(FK4<K, TX, TY, TZ, TMA>::NTH, MINB)
+    k_K4_fused(const double* __restrict__ pold, double* __restrict__ pnew, const double* __restrict__ z,
+               const double* __restrict__ X, double* __restrict__ q, Geo G, double sB, int mode, int it, int ctl,
+               const double* __restrict__ rzp, int nrz, double* rz_hist, const double* pq_hist, int* stop,
+               double* pqp, const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_z,
+               const __grid_constant__ CUtensorMap tm_x) {
+  using F = FK4<K, TX, TY, TZ, TMA>;
+  extern __shared__ __align__(1024) double sm[];
+  double* Pe = sm;
+  double* Xs = sm + F::OFF_XS;
+  double* Wz = sm + F::OFF_WZ;
+  double* Wy = sm + F::OFF_WY;
+  double* Tb = sm + F::OFF_T;  // [0] BI, [1] BD, each [K][K+1]
+  uint64_t* bar = (uint64_t*)(sm + F::OFF_B);
+  const int N = G.N;
+  const int64_t ne = G.n_el;
+  const int t = threadIdx.x;
+  const int NTX = (N + TX - 1) / TX, NTY = (N + TY - 1) / TY;
+  const int tile = blockIdx.x;
+  const int tx = tile % NTX, ty = (tile / NTX) % NTY, tz = tile / (NTX * NTY);
+  const int ex0 = TX * tx, ey0 = TY * ty, ez0 = TZ * tz;
+  if constexpr (TMA) {
+    // one thread issues the tile's boxes (zero fill outside the mesh); they land while the
+    // PCG control reduction below runs
+    if (t == 0) {
+      mbar_init(&bar[0], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&bar[0], F::XB + (mode != 2 ? F::BOXB : 0u) + (mode != 0 ? F::BOXB : 0u));
+      tma_load_3d(Xs, &tm_x, K * ex0, K * ey0, K * ez0, &bar[0]);
+      if (mode != 2) tma_load_4d(Wz, &tm_z, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
+      if (mode != 0) tma_load_4d(Wy, &tm_p, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
+    }
+  } else {
+    // X at the tile nodes (asynchronous copies; 0 outside the mesh)
+    for (int i = t; i < F::XS; i += F::NTH) {
+      const int nx = i % F::NX, ny = (i / F::NX) % F::NY, nz = i / (F::NX * F::NY);
+      const int gx = K * ex0 + nx, gy = K * ey0 + ny, gz = K * ez0 + nz;
+      if (gx < G.nn1 && gy < G.nn1 && gz < G.nn1) cp_async8(Xs + i, X + node_id(gx, gy, gz, G.nn1));
+      else Xs[i] = 0.0;
+    }
+  }
+  for (int i = t; i < F::TABS; i += F::NTH) {
+    const int w = i / (K * (K + 1)), m = (i / (K + 1)) % K, a = i % (K + 1);
+    Tb[i] = w ? TB(K).BD[m][a] : TB(K).BI[m][a];
+  }
+  // p on the tile + halo (0 outside the mesh): the thread's loads are issued before the
+  // PCG control reduction, which only the update needs
+  constexpr int HPER = TMA ? 1 : (F::PE + F::NTH - 1) / F::NTH;
+  double po[HPER], zz[HPER];
+  int64_t gi[HPER];
+  if constexpr (!TMA) {
+#pragma unroll
+    for (int k = 0; k < HPER; ++k) {
+      const int i = t + k * F::NTH;
+      const int lx = i % F::EX, ly = (i / F::EX) % F::EY, lz = (i / (F::EX * F::EY)) % F::EZ, m = i / F::NEH;
+      const int ex = ex0 + lx - 1, ey = ey0 + ly - 1, ez = ez0 + lz - 1;
+      const bool ok =
+          i < F::PE && (unsigned)ex < (unsigned)N && (unsigned)ey < (unsigned)N && (unsigned)ez < (unsigned)N;
+      gi[k] = ok ? (int64_t)m * ne + ex + (int64_t)N * (ey + (int64_t)N * ez) : -1;
+      po[k] = (ok && mode != 0) ? __ldg(pold + gi[k]) : 0.0;
+      zz[k] = (ok && mode != 2) ? __ldg(z + gi[k]) : 0.0;
+    }
+  }
+  double beta = 0.0;
+  if (ctl) {
+    if (pcg_control<F::NTH>(it, rzp, nrz, rz_hist, pq_hist, stop, &beta)) {
+      if (TMA && t == 0) mbar_wait(&bar[0], 0);  // drain the copies in flight before exiting
+      return;
+    }
+  } else if (mode == 1) {
+    beta = rz_hist[it] / rz_hist[it - 1];
+  }
+  if constexpr (TMA) {
+    __syncthreads();  // barrier init visible
+    mbar_wait(&bar[0], 0);
+    // p = z + beta p_old from the boxes ([m][lz][ly][8], column lx + 1)
+    for (int i = t; i < F::PE; i += F::NTH) {
+      const int row = i / F::EX, lx = i - row * F::EX, b = row * F::BX + lx + 1;
+      Pe[i] = mode == 2 ? Wy[b] : (mode == 1 ? fma(beta, Wy[b], Wz[b]) : Wz[b]);
+    }
+    __syncthreads();
+    if (mode != 2) {  // own elements' p_new
+      for (int i = t; i < TX * TY * TZ * F::NM; i += F::NTH) {
+        const int lx = i % TX, ly = (i / TX) % TY, lz = (i / (TX * TY)) % TZ, m = i / (TX * TY * TZ);
+        const int ex = ex0 + lx, ey = ey0 + ly, ez = ez0 + lz;
+        if (ex < N && ey < N && ez < N)
+          pnew[(int64_t)m * ne + ex + (int64_t)N * (ey + (int64_t)N * ez)] =
+              Pe[((m * F::EZ + lz + 1) * F::EY + ly + 1) * F::EX + lx + 1];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < HPER; ++k) {
+      const int i = t + k * F::NTH;
+      if (i >= F::PE) continue;
+      double v = 0.0;
+      if (gi[k] >= 0) {
+        v = mode == 2 ? po[k] : (mode == 1 ? fma(beta, po[k], zz[k]) : zz[k]);
+        const int lx = i % F::EX, ly = (i / F::EX) % F::EY, lz = (i / (F::EX * F::EY)) % F::EZ;
+        const bool own = lx >= 1 && ly >= 1 && lz >= 1 && lx <= TX && ly <= TY && lz <= TZ;
+        if (own && mode != 2) pnew[gi[k]] = v;
+      }
+      Pe[i] = v;
+    }
+    cp_async_wait_all();
+  }
+  K4Acc<K, TZ> qa;
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+#pragma unroll
+    for (int l = 0; l < TZ; ++l)
+#pragma unroll
+      for (int m = 0; m < K; ++m) qa.v[j][l][m] = 0.0;
+  __syncthreads();
+  const int TS = K * (K + 1);
+#pragma unroll 1
+  for (int c = 0; c < 3; ++c) {
+    // M_cd = BD on the component's own axis d == c
+    const double* Tx = Tb + (c == 0 ? TS : 0);
+    const double* Ty = Tb + (c == 1 ? TS : 0);
+    const double* Tz = Tb + (c == 2 ? TS : 0);
+    k4_stage_z<K, TX, TY, TZ>(Pe, Wz, t, Tz);
+    __syncthreads();
+    k4_stage_y<K, TX, TY, TZ>(Wz, Wy, t, Ty);
+    __syncthreads();
+    k4_stage_x<K, TX, TY, TZ, F::XR>(Wy, Xs, Wz /* V */, t, sB, Tx);
+    __syncthreads();
+    k4_stage_y2<K, TX, TY, TZ>(Wz /* V */, Wy /* U */, t, Ty);
+    __syncthreads();
+    k4_stage_z2<K, TX, TY, TZ>(Wy /* U */, qa, t, Tz);
+    __syncthreads();
+  }
+  // q = sB acc on the own elements, <p, q> partial
+  double dot = 0.0;
+  {
+    const int g = t / F::GWZ2, col = t % F::GWZ2;
+    if (g < K && col < TX * TY) {
+      switch (g) {
+        case 0: dot = k4_q_grp<K, TX, TY, TZ, 0>(qa, Pe, q, col, ex0, ey0, ez0, N, ne, sB); break;
+        case 1: dot = k4_q_grp<K, TX, TY, TZ, 1>(qa, Pe, q, col, ex0, ey0, ez0, N, ne, sB); break;
+        case 2:
+          if constexpr (K > 2) dot = k4_q_grp<K, TX, TY, TZ, (K > 2 ? 2 : 0)>(qa, Pe, q, col, ex0, ey0, ez0, N, ne, sB);
+          break;
+        default:
+          if constexpr (K > 3) dot = k4_q_grp<K, TX, TY, TZ, (K > 3 ? 3 : 0)>(qa, Pe, q, col, ex0, ey0, ez0, N, ne, sB);
+          break;
+      }
+    }
+  }
+  store_partial<F::NTH>(dot, pqp);
+}
+
+}  // namespace wb

@@ -112,3 +112,4 @@ __global__ void __launch_bounds__(256) k_BT_node2(const double* __restrict__ p, 
 #include "k_schur.cuh"
 #include "k2_bbt.cuh"
 #include "k2_setup.cuh"
+#include "k4_fused.cuh"

@@ -108,6 +108,13 @@ struct wb_ctx {
   double *XzL = nullptr, *XzR = nullptr;
   static constexpr int ZM_NV = 5;  // kernel variants (tile shape, CTAs per SM): zm_variants below
   CUtensorMap tz[ZM_NV][3];        // per variant: maps of pp, pp1, pz
+  int k4f = 1, k4_var = 1;  // k = 3, 4: fused Poisson kernel (k4_fused.cuh) on, its tile variant
+  // k = 4, even N: TMA tensor maps of the fused kernel's tile variant 1 (z, p boxes; X with
+  // padded rows X4L / X4R)
+  bool tma4_ok = false;
+  double *X4L = nullptr, *X4R = nullptr;
+  struct K4Maps { CUtensorMap pp, pp1, pz, xL, xR; };
+  K4Maps tm4[2];  // per TMA tile variant (k4_var 1: 4 x 4 x 2, 5: 4 x 2 x 2)
   int kz = 0;  // TMA Poisson kernel: 1 = z = Minv r stored by the PCG update and loaded as one box; 0 = r + Minv boxes (default: faster with the y-fastest storage)
   int k_dbg = 0;  // timing probe bits for the fused K kernel (results invalid when nonzero)
   // profiling: CUDA-event pairs around every Poisson-operator launch (direct launches)
@@ -304,6 +311,55 @@ wb_status launch_k2f_t(wb_ctx* c, const double* pold, double* pnew, const double
   *npq = grid;
   return WB_OK;
 }
+// fused k = 3, 4 Poisson operator (+ PCG direction update), one CTA per element tile
+template <int K, int TX, int TY, int TZ, int MINB, bool TMA = false>
+wb_status launch_k4f_t(wb_ctx* c, const double* pold, double* pnew, const double* X, double* q, int mode, PcgArgs a,
+                       int* npq, const CUtensorMap* tp = nullptr, const CUtensorMap* tz = nullptr,
+                       const CUtensorMap* tx = nullptr) {
+  using F = FK4<K, TX, TY, TZ, TMA>;
+  const int N = c->N;
+  const int nt = ((N + TX - 1) / TX) * ((N + TY - 1) / TY) * ((N + TZ - 1) / TZ);
+  static const CUtensorMap none{};
+  k_K4_fused<K, TX, TY, TZ, MINB, TMA><<<nt, F::NTH, F::SMEM, c->stream>>>(
+      pold, pnew, c->pz, X, q, c->G, c->sB, mode, a.it, a.ctl, c->rzp, c->red_blocks, rz_hist(c), pq_hist(c),
+      c->stop, c->pqp, tp ? *tp : none, tz ? *tz : none, tx ? *tx : none);
+  LAUNCH_CHECK(c);
+  *npq = nt;
+  return WB_OK;
+}
+#define K4_VARIANTS(X_)                                                                                         \
+  X_(4, 3, 3, 3, 1, false) X_(4, 4, 4, 2, 2, false) X_(4, 4, 4, 2, 2, true) X_(4, 2, 2, 2, 2, false)             \
+  X_(4, 4, 4, 4, 1, false) X_(3, 3, 3, 3, 2, false) X_(3, 4, 4, 4, 2, false) X_(4, 4, 2, 2, 3, false)           \
+  X_(4, 4, 2, 2, 3, true)
+constexpr int K4_NV = 6;  // variants per order: k4_var indexes them (k = 3 has 2)
+wb_status run_k4f(wb_ctx* c, const double* pold, double* pnew, const double* X, double* q, int mode, PcgArgs a,
+                  int* npq) {
+  if (c->k == 4) {
+    switch (c->k4_var) {
+      case 1:    // 4 x 4 x 2 tiles, TMA staging where the maps exist (else the same kernel with loads)
+      case 5: {  // 4 x 2 x 2 tiles, TMA, three CTAs per SM
+        const wb_ctx::K4Maps& m = c->tm4[c->k4_var == 1 ? 0 : 1];
+        const CUtensorMap* tp = pold == c->pp ? &m.pp : (pold == c->pp1 ? &m.pp1 : nullptr);
+        const CUtensorMap* tx = X == c->Cinv ? &m.xL : (X == c->Dinv ? &m.xR : nullptr);
+        if (c->k4_var == 5) {
+          if (c->tma4_ok && tp && tx)
+            return launch_k4f_t<4, 4, 2, 2, 3, true>(c, pold, pnew, X, q, mode, a, npq, tp, &m.pz, tx);
+          return launch_k4f_t<4, 4, 2, 2, 3>(c, pold, pnew, X, q, mode, a, npq);
+        }
+        if (c->tma4_ok && tp && tx)
+          return launch_k4f_t<4, 4, 4, 2, 2, true>(c, pold, pnew, X, q, mode, a, npq, tp, &m.pz, tx);
+        return launch_k4f_t<4, 4, 4, 2, 2>(c, pold, pnew, X, q, mode, a, npq);
+      }
+      case 2: return launch_k4f_t<4, 2, 2, 2, 2>(c, pold, pnew, X, q, mode, a, npq);
+      case 3: return launch_k4f_t<4, 4, 4, 4, 1>(c, pold, pnew, X, q, mode, a, npq);
+      case 4: return launch_k4f_t<4, 4, 4, 2, 2>(c, pold, pnew, X, q, mode, a, npq);
+      default: return launch_k4f_t<4, 3, 3, 3, 1>(c, pold, pnew, X, q, mode, a, npq);
+    }
+  }
+  if (c->k4_var == 1) return launch_k4f_t<3, 4, 4, 4, 2>(c, pold, pnew, X, q, mode, a, npq);
+  return launch_k4f_t<3, 3, 3, 3, 2>(c, pold, pnew, X, q, mode, a, npq);
+}
+
 // element tile of the k = 2 A kernels and its CTAs per SM
 #ifndef A_TX
 #define A_TX 4
@@ -354,7 +410,11 @@ wb_status build_xz(wb_ctx* c) {
   c->xz_valid = true;
   return WB_OK;
 }
-double* z_out(const wb_ctx* c) { return tma_active(c) && (c->kz || zm_active(c)) ? c->pz : nullptr; }
+// k = 3, 4: the fused Poisson kernel (k4_fused.cuh); it reads z = Minv r from the PCG kernels
+bool k4f_active(const wb_ctx* c) { return c->k >= 3 && c->k4f; }
+double* z_out(const wb_ctx* c) {
+  return (tma_active(c) && (c->kz || zm_active(c))) || k4f_active(c) ? c->pz : nullptr;
+}
 const CUtensorMap* zmap_of(wb_ctx* c, const double* p) {
   if (p == c->pp) return &c->tz[c->zm_var][0];
   if (p == c->pp1) return &c->tz[c->zm_var][1];
@@ -505,6 +565,47 @@ bool setup_tma(wb_ctx* c) {
          make_tm_vec(&c->tm_mL, c->MinvL, c->N, c->nm) && make_tm_vec(&c->tm_mR, c->MinvR, c->N, c->nm);
 }
 
+// k = 4 fused Poisson kernel, TMA tile variants: 4-D maps of the mode-major PCG vectors
+// [m][ez][ey][ex] (row stride N: N even), box = x from ex0 - 2, 8 wide, the tile's y / z
+// halo, all modes; 3-D maps of X with rows padded to nn1 + 1, box = the tile's nodes
+template <class F>
+bool make_tm4_vec(CUtensorMap* tm, const double* base, int N) {
+  const cuuint64_t n = (cuuint64_t)N;
+  const cuuint64_t dims[4] = {n, n, n, (cuuint64_t)F::NM};
+  const cuuint64_t strides[3] = {n * 8, n * n * 8, n * n * n * 8};
+  const cuuint32_t box[4] = {(cuuint32_t)F::BX, (cuuint32_t)F::EY, (cuuint32_t)F::EZ, (cuuint32_t)F::NM};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+template <class F>
+bool make_tm4_x(CUtensorMap* tm, const double* base, int nn1) {
+  const cuuint64_t r = (cuuint64_t)nn1 + 1, n = (cuuint64_t)nn1;
+  const cuuint64_t dims[3] = {r, n, n};
+  const cuuint64_t strides[2] = {r * 8, r * n * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)F::XR, (cuuint32_t)F::NY, (cuuint32_t)F::NZ};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+template <class F>
+bool make_tm4(wb_ctx* c, wb_ctx::K4Maps& m) {
+  return make_tm4_vec<F>(&m.pp, c->pp, c->N) && make_tm4_vec<F>(&m.pp1, c->pp1, c->N) &&
+         make_tm4_vec<F>(&m.pz, c->pz, c->N) && make_tm4_x<F>(&m.xL, c->X4L, c->G.nn1) &&
+         make_tm4_x<F>(&m.xR, c->X4R, c->G.nn1);
+}
+bool setup_tma4(wb_ctx* c) {
+  if (c->k != 4 || (c->N & 1) || c->pl.off != 0 || c->pl.sm != c->n_el || !get_encode()) return false;
+  const size_t bx = sizeof(double) * (size_t)(c->G.nn1 + 1) * c->G.nn1 * c->G.nn1;
+  if (cudaMalloc(&c->X4L, bx) != cudaSuccess || cudaMalloc(&c->X4R, bx) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return make_tm4<FK4<4, 4, 4, 2, true>>(c, c->tm4[0]) && make_tm4<FK4<4, 4, 2, 2, true>>(c, c->tm4[1]);
+}
+
 wb_status configure_kernels(wb_ctx* c) {
   CUDA_TRY(c, cudaFuncSetAttribute(k_A_tile<A_TX, A_TY, A_TZ, A_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)Tile2<A_TX, A_TY, A_TZ>::SMEM));
@@ -514,6 +615,11 @@ wb_status configure_kernels(wb_ctx* c) {
                                    (int)FK2<4, 8, 8>::SMEM));
   CUDA_TRY(c, cudaFuncSetAttribute(k_K2_fused<4, 4, 4, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)FK2<4, 4, 4>::SMEM));
+#define K4_ATTR(K_, TX_, TY_, TZ_, MB_, T_)                                                  \
+  CUDA_TRY(c, cudaFuncSetAttribute(k_K4_fused<K_, TX_, TY_, TZ_, MB_, T_>,                       \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FK4<K_, TX_, TY_, TZ_, T_>::SMEM));
+  K4_VARIANTS(K4_ATTR)
+#undef K4_ATTR
   CUDA_TRY(c, cudaFuncSetAttribute(k_A_slice<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(8 * 12 * Ord<3>::NQ * sizeof(double))));
   CUDA_TRY(c, cudaFuncSetAttribute(k_A_slice<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -584,6 +690,10 @@ wb_status run_K_pcg(wb_ctx* c, int side, int mode, const double* pold, double* p
   if (c->k == 2) {
     *pcur = mode == 2 ? pold : pnew;  // (mode 2 leaves p as is; the TMA kernel then skips the copy)
     return run_k2f(c, pold, pnew, r, Minv, X, q, mode, a, npq);
+  }
+  if (k4f_active(c) && (mode == 2 || r == c->pr)) {  // k = 3, 4: the fused tile kernel (k4_fused.cuh)
+    *pcur = mode == 2 ? pold : pnew;
+    return run_k4f(c, pold, pnew, X, q, mode, a, npq);
   }
   // generic k: direction update pold -> pnew (+ control), then B^T (element + gather) and B (+ dot)
   const double* p = pold;
@@ -1222,6 +1332,9 @@ void free_all(wb_ctx* c) {
   if (c->XpL) cudaFree(c->XpL);
   if (c->XpR) cudaFree(c->XpR);
   c->XpL = c->XpR = nullptr;
+  if (c->X4L) cudaFree(c->X4L);
+  if (c->X4R) cudaFree(c->X4R);
+  c->X4L = c->X4R = nullptr;
   c->counter = nullptr; c->stop = nullptr; c->icount = nullptr;
   cudaGetLastError();  // teardown must not leave an error for the next context's launch checks
 }
@@ -1377,6 +1490,7 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
     return WB_ECUDA;
   }
   c->tma_ok = setup_tma(c);  // the pointer kernel serves contexts without the y-fastest storage
+  c->tma4_ok = setup_tma4(c);  // k = 4, even N: the fused kernel's TMA variant (else its LDG form)
   c->zm_ok = c->tma_ok && setup_zm(c);
   if (c->ylay && !c->tma_ok) {
     free_all(c);
@@ -1508,6 +1622,10 @@ static wb_status finish_lumped(wb_ctx* c) {
     using F = FK2<TMA_TX, TMA_TY, TMA_TZ>;
     const int nt = ((c->N + TMA_TX - 1) / TMA_TX) * ((c->N + TMA_TY - 1) / TMA_TY) * ((c->N + TMA_TZ - 1) / TMA_TZ);
     k_x_tiles<TMA_TX, TMA_TY, TMA_TZ><<<nt, F::MY * F::MZ, 0, c->stream>>>(c->Cinv, c->Dinv, c->XpL, c->XpR, c->N);
+    LAUNCH_CHECK(c);
+  }
+  if (c->tma4_ok) {  // X with padded rows for the k = 4 fused kernel's TMA variant
+    k_xpad4<<<stream_blocks(c->n_nodes), VBS, 0, c->stream>>>(c->Cinv, c->Dinv, c->X4L, c->X4R, c->G.nn1);
     LAUNCH_CHECK(c);
   }
   c->xz_valid = false;  // the z-march kernel's X copy (opt-in)
@@ -2396,6 +2514,15 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
   } else if (!strcmp(key, "weights")) {  // wBFBT weights of the next wb_set_viscosity (R17)
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "weights must be 0 or 1");
     c->weights = (int)value;
+  } else if (!strcmp(key, "k4f")) {  // k = 3, 4: 1 = fused tile Poisson kernel, 0 = B^T / gather / B kernels
+    if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k4f must be 0 or 1");
+    c->k4f = (int)value;
+    clear_graphs(c);
+  } else if (!strcmp(key, "k4_var")) {  // tile variant of the fused k = 3, 4 Poisson kernel
+    if (!(value >= 0.0 && value < K4_NV) || value != (double)(int)value)
+      return set_err(c, WB_EINVAL, "k4_var must be an integer in [0, %d)", K4_NV);
+    c->k4_var = (int)value;
+    clear_graphs(c);
   } else if (!strcmp(key, "k_ws")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k_ws must be 0 or 1");
     c->k_ws = (int)value;
