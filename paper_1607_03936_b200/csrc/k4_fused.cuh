@@ -332,7 +332,7 @@ __device__ __forceinline__ void k4_stage_z2(const double* __restrict__ U, K4Acc<
 }
 
 // q = sB acc for the group's modes of own element column (lx', ly'), <p, q> partial
-template <int K, int TX, int TY, int TZ, int G>
+template <int K, int TX, int TY, int TZ, int G, bool OWN = false>
 __device__ __forceinline__ double k4_q_grp(const K4Acc<K, TZ>& A, const double* __restrict__ Pe, double* q, int col,
                                            int ex0, int ey0, int ez0, int N, int64_t ne, double sB) {
   using F = FK4<K, TX, TY, TZ>;
@@ -346,7 +346,8 @@ __device__ __forceinline__ double k4_q_grp(const K4Acc<K, TZ>& A, const double* 
     const int ez = ez0 + lz;
     if (ez < N) {
       const int64_t e = ex + (int64_t)N * (ey + (int64_t)N * ez);
-      const double* pe = Pe + ((lz + 1) * F::EY + ly + 1) * F::EX + lx + 1;
+      // own p: Pe (the halo layout) or, OWN, a [m][lz][ly][lx] copy of the own elements
+      const double* pe = OWN ? Pe + (lz * TY + ly) * TX + lx : Pe + ((lz + 1) * F::EY + ly + 1) * F::EX + lx + 1;
 #pragma unroll
       for (int j = 0; j <= G; ++j)
 #pragma unroll
@@ -354,7 +355,7 @@ __device__ __forceinline__ double k4_q_grp(const K4Acc<K, TZ>& A, const double* 
           const int m = k4_mode(G - j, j, m3);
           const double o = sB * A.v[j][lz][m3];
           q[(int64_t)m * ne + e] = o;
-          dot = fma(pe[m * F::NEH], o, dot);
+          dot = fma(pe[m * (OWN ? TX * TY * TZ : F::NEH)], o, dot);
         }
     }
   }
@@ -512,6 +513,142 @@ __global__ void __launch_bounds__(FK4<K, TX, TY, TZ, TMA>::NTH, MINB)
     }
   }
   store_partial<F::NTH>(dot, pqp);
+}
+
+// The same operator with all three components in flight at once (one CTA per SM, 5 barrier
+// intervals per tile instead of 15): stage Z for the two z tables (BI feeds c = 0, 1; BD
+// feeds c = 2), then Y, X/X', Y' per component on separate buffers, then Z' summing the
+// components in order.  TMA staging only (k = 4, even TX, N even).  Shared memory:
+//   Xs | A = [Pe | Wz_I | Wz_D] (later V_0..2) | B = Wy_0..2 (the p boxes first, later U_0..2) | Po | tables
+template <int K, int TX, int TY, int TZ>
+struct FK43 {
+  using F = FK4<K, TX, TY, TZ, true>;
+  static constexpr int al16(int n) { return (n + 15) / 16 * 16; }
+  static constexpr int WZ = al16(F::WZ), WY = al16(F::WY), VV = al16(F::VV), UU = al16(F::UU);
+  static constexpr int NOWN = TX * TY * TZ * F::NM;
+  static constexpr int A_ = al16(F::PE) + 2 * WZ, B_ = 3 * WY;
+  static_assert(3 * VV <= A_ && 3 * UU <= B_ && 2 * F::BOX <= B_, "3C buffers");
+  static constexpr int OFF_XS = 0, OFF_A = al16(F::XS), OFF_WZ = OFF_A + al16(F::PE), OFF_B = OFF_A + A_,
+                       OFF_PO = OFF_B + B_, OFF_T = OFF_PO + al16(NOWN), OFF_BAR = OFF_T + al16(F::TABS);
+  static constexpr int SMEM = OFF_BAR * 8 + 16;
+  static constexpr int NZT = 2 * K * F::GWZ, NYT = K * F::GWY, NXT = F::w32(F::IX), NY2T = K * F::GWY2;
+  static constexpr int mx(int a, int b) { return a > b ? a : b; }
+  static constexpr int NTH = mx(mx(NZT, 3 * NYT), mx(3 * NXT, 3 * NY2T));
+};
+
+template <int K, int TX, int TY, int TZ>
+__global__ void __launch_bounds__(FK43<K, TX, TY, TZ>::NTH, 1)
+    k_K4_3c(double* __restrict__ pnew, double* __restrict__ q, Geo G, double sB, int mode, int it, int ctl,
+            const double* __restrict__ rzp, int nrz, double* rz_hist, const double* pq_hist, int* stop, double* pqp,
+            const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_z,
+            const __grid_constant__ CUtensorMap tm_x) {
+  using F = FK4<K, TX, TY, TZ, true>;
+  using H = FK43<K, TX, TY, TZ>;
+  extern __shared__ __align__(1024) double sm[];
+  double* Xs = sm + H::OFF_XS;
+  double* Pe = sm + H::OFF_A;
+  double* Wz = sm + H::OFF_WZ;  // [v][WZ]
+  double* Vb = sm + H::OFF_A;   // [c][VV]
+  double* Wy = sm + H::OFF_B;   // [c][WY]
+  double* Ub = sm + H::OFF_B;   // [c][UU]
+  double* Po = sm + H::OFF_PO;
+  double* Tb = sm + H::OFF_T;
+  uint64_t* bar = (uint64_t*)(sm + H::OFF_BAR);
+  const int N = G.N;
+  const int64_t ne = G.n_el;
+  const int t = threadIdx.x;
+  const int NTX = (N + TX - 1) / TX, NTY = (N + TY - 1) / TY;
+  const int tile = blockIdx.x;
+  const int tx = tile % NTX, ty = (tile / NTX) % NTY, tz = tile / (NTX * NTY);
+  const int ex0 = TX * tx, ey0 = TY * ty, ez0 = TZ * tz;
+  double* Zbox = Wy;
+  double* Pbox = Wy + F::BOX;
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&bar[0], F::XB + (mode != 2 ? F::BOXB : 0u) + (mode != 0 ? F::BOXB : 0u));
+    tma_load_3d(Xs, &tm_x, K * ex0, K * ey0, K * ez0, &bar[0]);
+    if (mode != 2) tma_load_4d(Zbox, &tm_z, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
+    if (mode != 0) tma_load_4d(Pbox, &tm_p, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
+  }
+  for (int i = t; i < F::TABS; i += H::NTH) {
+    const int w = i / (K * (K + 1)), m = (i / (K + 1)) % K, a = i % (K + 1);
+    Tb[i] = w ? TB(K).BD[m][a] : TB(K).BI[m][a];
+  }
+  double beta = 0.0;
+  if (ctl) {
+    if (pcg_control<H::NTH>(it, rzp, nrz, rz_hist, pq_hist, stop, &beta)) {
+      if (t == 0) mbar_wait(&bar[0], 0);
+      return;
+    }
+  } else if (mode == 1) {
+    beta = rz_hist[it] / rz_hist[it - 1];
+  }
+  __syncthreads();
+  mbar_wait(&bar[0], 0);
+  for (int i = t; i < F::PE; i += H::NTH) {
+    const int row = i / F::EX, lx = i - row * F::EX, b = row * F::BX + lx + 1;
+    Pe[i] = mode == 2 ? Pbox[b] : (mode == 1 ? fma(beta, Pbox[b], Zbox[b]) : Zbox[b]);
+  }
+  __syncthreads();
+  for (int i = t; i < H::NOWN; i += H::NTH) {  // own p: a copy for <p, q>, p_new to global
+    const int lx = i % TX, ly = (i / TX) % TY, lz = (i / (TX * TY)) % TZ, m = i / (TX * TY * TZ);
+    const double v = Pe[((m * F::EZ + lz + 1) * F::EY + ly + 1) * F::EX + lx + 1];
+    Po[i] = v;
+    const int ex = ex0 + lx, ey = ey0 + ly, ez = ez0 + lz;
+    if (mode != 2 && ex < N && ey < N && ez < N) pnew[(int64_t)m * ne + ex + (int64_t)N * (ey + (int64_t)N * ez)] = v;
+  }
+  const int TS = K * (K + 1);
+  // Z: v = 0 (BI) for c = 0, 1; v = 1 (BD) for c = 2
+  if (t < H::NZT) {
+    const int v = t / (K * F::GWZ);
+    k4_stage_z<K, TX, TY, TZ>(Pe, Wz + v * H::WZ, t - v * K * F::GWZ, Tb + v * TS);
+  }
+  __syncthreads();
+  {  // Y per component
+    const int c = t / H::NYT, it2 = t - c * H::NYT;
+    if (c < 3)
+      k4_stage_y<K, TX, TY, TZ>(Wz + (c == 2 ? H::WZ : 0), Wy + c * H::WY, it2, Tb + (c == 1 ? TS : 0));
+  }
+  __syncthreads();
+  {  // X / X' per component (V over Pe and Wz: both dead now)
+    const int c = t / H::NXT, it2 = t - c * H::NXT;
+    if (c < 3)
+      k4_stage_x<K, TX, TY, TZ, F::XR>(Wy + c * H::WY, Xs, Vb + c * H::VV, it2, sB, Tb + (c == 0 ? TS : 0));
+  }
+  __syncthreads();
+  {  // Y' per component (U over Wy)
+    const int c = t / H::NY2T, it2 = t - c * H::NY2T;
+    if (c < 3) k4_stage_y2<K, TX, TY, TZ>(Vb + c * H::VV, Ub + c * H::UU, it2, Tb + (c == 1 ? TS : 0));
+  }
+  __syncthreads();
+  // Z': the components in order into the same accumulators, then q and <p, q>
+  K4Acc<K, TZ> qa;
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+#pragma unroll
+    for (int l = 0; l < TZ; ++l)
+#pragma unroll
+      for (int m = 0; m < K; ++m) qa.v[j][l][m] = 0.0;
+  double dot = 0.0;
+  if (t < K * F::GWZ2) {
+#pragma unroll 1
+    for (int c = 0; c < 3; ++c) k4_stage_z2<K, TX, TY, TZ>(Ub + c * H::UU, qa, t, Tb + (c == 2 ? TS : 0));
+    const int g = t / F::GWZ2, col = t % F::GWZ2;
+    if (g < K && col < TX * TY) {
+      switch (g) {
+        case 0: dot = k4_q_grp<K, TX, TY, TZ, 0, true>(qa, Po, q, col, ex0, ey0, ez0, N, ne, sB); break;
+        case 1: dot = k4_q_grp<K, TX, TY, TZ, 1, true>(qa, Po, q, col, ex0, ey0, ez0, N, ne, sB); break;
+        case 2:
+          if constexpr (K > 2) dot = k4_q_grp<K, TX, TY, TZ, (K > 2 ? 2 : 0), true>(qa, Po, q, col, ex0, ey0, ez0, N, ne, sB);
+          break;
+        default:
+          if constexpr (K > 3) dot = k4_q_grp<K, TX, TY, TZ, (K > 3 ? 3 : 0), true>(qa, Po, q, col, ex0, ey0, ez0, N, ne, sB);
+          break;
+      }
+    }
+  }
+  store_partial<H::NTH>(dot, pqp);
 }
 
 }  // namespace wb

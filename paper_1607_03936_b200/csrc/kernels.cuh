@@ -1310,6 +1310,46 @@ __global__ void __launch_bounds__(VBS) k_unit_dev(double* __restrict__ out, cons
   const double nrm = sqrt(*h2);
   for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS) out[i] = in[i] / nrm;
 }
+// FGMRES least-squares update on the device (R19), one thread: column j of the Hessenberg
+// (h[0..j] Gram-Schmidt scalars, h[j+1] = <w, w>) gets the previous Givens rotations, a new
+// rotation (cs[j], sn[j]) zeroes its subdiagonal, the rotated right-hand side g is updated,
+// and R[i][j] (row stride m) is stored.  res[0] = |g[j+1]| (the residual estimate), res[1]
+// = |h_{j+1,j}|.  The arithmetic is the host loop's, operation for operation (no contraction).
+__global__ void k_givens(int j, int m, const double* __restrict__ h, double* __restrict__ R, double* __restrict__ cs,
+                         double* __restrict__ sn, double* __restrict__ g, double* __restrict__ res) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double hn = sqrt(h[j + 1]);
+  for (int i = 0; i <= j; ++i) R[(size_t)i * m + j] = h[i];
+  for (int i = 0; i < j; ++i) {
+    const double a = R[(size_t)i * m + j], b = R[(size_t)(i + 1) * m + j];
+    R[(size_t)i * m + j] = __dadd_rn(__dmul_rn(cs[i], a), __dmul_rn(sn[i], b));
+    R[(size_t)(i + 1) * m + j] = __dadd_rn(__dmul_rn(-sn[i], a), __dmul_rn(cs[i], b));
+  }
+  const double a = R[(size_t)j * m + j], den = sqrt(__dadd_rn(__dmul_rn(a, a), __dmul_rn(hn, hn)));
+  cs[j] = den > 0.0 ? a / den : 1.0;
+  sn[j] = den > 0.0 ? hn / den : 0.0;
+  R[(size_t)j * m + j] = den;
+  g[j + 1] = __dmul_rn(-sn[j], g[j]);
+  g[j] = __dmul_rn(cs[j], g[j]);
+  res[0] = fabs(g[j + 1]);
+  res[1] = hn;
+}
+// back substitution R y = g on columns 0..jend (one thread), as the host loop did
+__global__ void k_fgmres_y(int jend, int m, const double* __restrict__ R, const double* __restrict__ g,
+                           double* __restrict__ y) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int i = jend; i >= 0; --i) {
+    double t = g[i];
+    for (int k = i + 1; k <= jend; ++k) t = __dsub_rn(t, __dmul_rn(R[(size_t)i * m + k], y[k]));
+    y[i] = t / R[(size_t)i * m + i];
+  }
+}
+// y += (*a) x  (device scalar)
+__global__ void __launch_bounds__(VBS) k_axpy_devp(double* __restrict__ y, const double* __restrict__ x, int64_t n,
+                                                   const double* __restrict__ a) {
+  const double s = *a;
+  for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS) y[i] += s * x[i];
+}
 // y += a x  (host scalar)
 __global__ void __launch_bounds__(VBS) k_axpy(double* __restrict__ y, const double* __restrict__ x, int64_t n, double a) {
   for (int64_t i = (int64_t)blockIdx.x * VBS + threadIdx.x; i < n; i += (int64_t)gridDim.x * VBS) y[i] += a * x[i];

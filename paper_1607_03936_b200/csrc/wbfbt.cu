@@ -81,6 +81,8 @@ struct wb_ctx {
   // n_v scratch, device scalars; sized for the largest restart length used so far
   double *gV = nullptr, *gZ = nullptr, *gw = nullptr, *gb = nullptr, *gx = nullptr, *gsa = nullptr,
          *gh = nullptr;
+  double* gls = nullptr;  // FGMRES least-squares state on the device: R (m x m), cs, sn, g, y, residual
+  double* gres_h = nullptr;  // pinned host copy of the residual estimate (2 doubles)
   int g_m = 0;
   // wBFBT inner Poisson solves: 0 = Jacobi-PCG (a9), 1 = Chebyshev-Jacobi on [cheb_lo, cheb_hi]
   // per side (0 = l, 1 = r), set by wb_set_inner_cheb
@@ -331,7 +333,7 @@ wb_status launch_k4f_t(wb_ctx* c, const double* pold, double* pnew, const double
   X_(4, 3, 3, 3, 1, false) X_(4, 4, 4, 2, 2, false) X_(4, 4, 4, 2, 2, true) X_(4, 2, 2, 2, 2, false)             \
   X_(4, 4, 4, 4, 1, false) X_(3, 3, 3, 3, 2, false) X_(3, 4, 4, 4, 2, false) X_(4, 4, 2, 2, 3, false)           \
   X_(4, 4, 2, 2, 3, true)
-constexpr int K4_NV = 6;  // variants per order: k4_var indexes them (k = 3 has 2)
+constexpr int K4_NV = 7;  // variants per order: k4_var indexes them (k = 3 has 2)
 wb_status run_k4f(wb_ctx* c, const double* pold, double* pnew, const double* X, double* q, int mode, PcgArgs a,
                   int* npq) {
   if (c->k == 4) {
@@ -349,6 +351,20 @@ wb_status run_k4f(wb_ctx* c, const double* pold, double* pnew, const double* X, 
         if (c->tma4_ok && tp && tx)
           return launch_k4f_t<4, 4, 4, 2, 2, true>(c, pold, pnew, X, q, mode, a, npq, tp, &m.pz, tx);
         return launch_k4f_t<4, 4, 4, 2, 2>(c, pold, pnew, X, q, mode, a, npq);
+      }
+      case 6: {  // 4 x 4 x 2 tiles, the three components concurrently (k_K4_3c), TMA only
+        const wb_ctx::K4Maps& m = c->tm4[0];
+        const CUtensorMap* tp = pold == c->pp ? &m.pp : (pold == c->pp1 ? &m.pp1 : nullptr);
+        const CUtensorMap* tx = X == c->Cinv ? &m.xL : (X == c->Dinv ? &m.xR : nullptr);
+        if (!(c->tma4_ok && tp && tx)) return launch_k4f_t<4, 4, 4, 2, 2>(c, pold, pnew, X, q, mode, a, npq);
+        using H = FK43<4, 4, 4, 2>;
+        const int N = c->N, nt = ((N + 3) / 4) * ((N + 3) / 4) * ((N + 1) / 2);
+        k_K4_3c<4, 4, 4, 2><<<nt, H::NTH, H::SMEM, c->stream>>>(pnew, q, c->G, c->sB, mode, a.it, a.ctl, c->rzp,
+                                                                c->red_blocks, rz_hist(c), pq_hist(c), c->stop,
+                                                                c->pqp, *tp, m.pz, *tx);
+        LAUNCH_CHECK(c);
+        *npq = nt;
+        return WB_OK;
       }
       case 2: return launch_k4f_t<4, 2, 2, 2, 2>(c, pold, pnew, X, q, mode, a, npq);
       case 3: return launch_k4f_t<4, 4, 4, 4, 1>(c, pold, pnew, X, q, mode, a, npq);
@@ -620,6 +636,8 @@ wb_status configure_kernels(wb_ctx* c) {
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FK4<K_, TX_, TY_, TZ_, T_>::SMEM));
   K4_VARIANTS(K4_ATTR)
 #undef K4_ATTR
+  CUDA_TRY(c, cudaFuncSetAttribute(k_K4_3c<4, 4, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)FK43<4, 4, 4, 2>::SMEM));
   CUDA_TRY(c, cudaFuncSetAttribute(k_A_slice<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(8 * 12 * Ord<3>::NQ * sizeof(double))));
   CUDA_TRY(c, cudaFuncSetAttribute(k_A_slice<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1167,7 +1185,8 @@ wb_status run_mpinv(wb_ctx* c, const double* r, double* z, double scale) {
 // ---- Stokes solve (R19): flexible GMRES on [A B^T; B 0] with P^-1 (a; b) =
 // (At^-1 (a - B^T y); y), y = -wBFBT(b), At^-1 = the smoother on A.  Vectors are [u | p],
 // p element-major.  The Gram-Schmidt scalars stay on the device (k_dot_dev / k_axpy_dev);
-// the Hessenberg column comes to the host once per iteration for the Givens rotations.
+// the Givens rotations, the Hessenberg (as R) and the back substitution stay on the device;
+// the host reads the 16-byte residual estimate once per iteration for the stop test.
 struct StokesPar { int pcg, sm; double lo, hi; };
 wb_status stokes_K(wb_ctx* c, const double* x, double* y) {
   wb_status s;
@@ -1204,8 +1223,9 @@ wb_status run_stokes(wb_ctx* c, const double* f, const double* g, double* u, dou
   const int64_t n = c->n_v + c->n_p;
   if (m > c->g_m) {  // the basis and the Hessenberg column grow with the restart length
     cudaStreamSynchronize(c->stream);
-    for (double** b : {&c->gV, &c->gZ, &c->gh}) { if (*b) cudaFree(*b); *b = nullptr; }
-    if (!lazy_alloc(&c->gV, n * (m + 1)) || !lazy_alloc(&c->gZ, n * m) || !lazy_alloc(&c->gh, (int64_t)m + 2)) {
+    for (double** b : {&c->gV, &c->gZ, &c->gh, &c->gls}) { if (*b) cudaFree(*b); *b = nullptr; }
+    if (!lazy_alloc(&c->gV, n * (m + 1)) || !lazy_alloc(&c->gZ, n * m) || !lazy_alloc(&c->gh, (int64_t)m + 2) ||
+        !lazy_alloc(&c->gls, (int64_t)m * m + 4 * (int64_t)m + 4)) {
       c->g_m = 0;
       return set_err(c, WB_ENOMEM, "FGMRES basis allocation failed (restart %d)", m);
     }
@@ -1215,6 +1235,16 @@ wb_status run_stokes(wb_ctx* c, const double* f, const double* g, double* u, dou
       !lazy_alloc(&c->gh, (int64_t)m + 2))
     return set_err(c, WB_ENOMEM, "FGMRES work allocation failed");
   if (c->g_m < m) return set_err(c, WB_ENOMEM, "FGMRES basis too small");
+  if (!c->gres_h && cudaMallocHost(&c->gres_h, 2 * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    c->gres_h = nullptr;
+    return set_err(c, WB_ENOMEM, "FGMRES pinned scalar allocation failed");
+  }
+  // device least-squares state (the Hessenberg never leaves the device; the host reads the
+  // 16-byte residual estimate once per iteration for the stop test)
+  const int gm = c->g_m;
+  double *dR = c->gls, *dcs = dR + (int64_t)gm * gm, *dsn = dcs + gm, *dg = dsn + gm, *dy = dg + gm + 1,
+         *dres = dy + gm;
   wb_status s;
   k_mask_v<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(f, c->gb, c->G);  // b = (M f; g)
   LAUNCH_CHECK(c);
@@ -1225,14 +1255,13 @@ wb_status run_stokes(wb_ctx* c, const double* f, const double* g, double* u, dou
   if ((s = dev_dot(c, c->gb, c->gb, n, c->gh)) || (s = host_scalar(c, c->gh, &bn2))) return s;
   const double bnorm = std::sqrt(bn2);
   double beta = bnorm;
-  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), gv(m + 1), y(m), col(m + 2);
   int total = 0;
   while (beta > rtol * bnorm && total < max_iters) {
     // V_0 = w / beta, beta^2 = <w, w> still in gh[0] from the dot that gave beta
     k_unit_dev<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->gV, c->gw, n, c->gh);
     LAUNCH_CHECK(c);
-    std::fill(gv.begin(), gv.end(), 0.0);
-    gv[0] = beta;
+    CUDA_TRY(c, cudaMemsetAsync(dg, 0, sizeof(double) * (gm + 1), c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(dg, &beta, sizeof(double), cudaMemcpyHostToDevice, c->stream));
     int jend = -1;
     for (int j = 0; j < m && total < max_iters; ++j) {
       double* Vj = c->gV + (int64_t)j * n;
@@ -1244,36 +1273,25 @@ wb_status run_stokes(wb_ctx* c, const double* f, const double* g, double* u, dou
         LAUNCH_CHECK(c);
       }
       if ((s = dev_dot(c, c->gw, c->gw, n, c->gh + j + 1))) return s;
-      CUDA_TRY(c, cudaMemcpyAsync(col.data(), c->gh, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, c->stream));
+      k_givens<<<1, 1, 0, c->stream>>>(j, gm, c->gh, dR, dcs, dsn, dg, dres);
+      LAUNCH_CHECK(c);
+      CUDA_TRY(c, cudaMemcpyAsync(c->gres_h, dres, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-      const double hn = std::sqrt(col[j + 1]);
-      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = col[i];
-      for (int i = 0; i < j; ++i) {  // previous rotations
-        const double a = H[(size_t)i * m + j], b = H[(size_t)(i + 1) * m + j];
-        H[(size_t)i * m + j] = cs[i] * a + sn[i] * b;
-        H[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * b;
-      }
-      const double a = H[(size_t)j * m + j], den = std::sqrt(a * a + hn * hn);
-      cs[j] = den > 0.0 ? a / den : 1.0;
-      sn[j] = den > 0.0 ? hn / den : 0.0;
-      H[(size_t)j * m + j] = den;
-      gv[j + 1] = -sn[j] * gv[j];
-      gv[j] = cs[j] * gv[j];
+      const double gres = c->gres_h[0], hn = c->gres_h[1];
       ++total;
       jend = j;
       if (hn > 0.0) {
         k_unit_dev<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->gV + (int64_t)(j + 1) * n, c->gw, n, c->gh + j + 1);
         LAUNCH_CHECK(c);
       }
-      if (std::fabs(gv[j + 1]) <= rtol * bnorm || hn == 0.0) break;
+      if (gres <= rtol * bnorm || hn == 0.0) break;
     }
-    for (int i = jend; i >= 0; --i) {
-      double t = gv[i];
-      for (int k = i + 1; k <= jend; ++k) t -= H[(size_t)i * m + k] * y[k];
-      y[i] = t / H[(size_t)i * m + i];
+    if (jend >= 0) {
+      k_fgmres_y<<<1, 1, 0, c->stream>>>(jend, gm, dR, dg, dy);
+      LAUNCH_CHECK(c);
     }
     for (int i = 0; i <= jend; ++i) {
-      k_axpy<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->gx, c->gZ + (int64_t)i * n, n, y[i]);
+      k_axpy_devp<<<stream_blocks(c->n_v), VBS, 0, c->stream>>>(c->gx, c->gZ + (int64_t)i * n, n, dy + i);
       LAUNCH_CHECK(c);
     }
     if ((s = stokes_K(c, c->gx, c->gw))) return s;  // true residual
@@ -1308,8 +1326,9 @@ void free_all(wb_ctx* c) {
                      &c->gp_s, &c->mpinv, &c->mut, &c->Cw, &c->Dw, &c->Cinv, &c->Dinv, &c->dKl, &c->dKr, &c->MinvL, &c->MinvR,
                      &c->E, &c->tv, &c->tw, &c->px, &c->pr, &c->pp, &c->pp1, &c->pq, &c->pz, &c->s0, &c->s1, &c->s2,
                      &c->partial, &c->pqp, &c->rzp, &c->scal, &c->stage, &c->Fu, &c->mueff,
-                     &c->E3, &c->dAinv, &c->tq, &c->gV, &c->gZ, &c->gw, &c->gb, &c->gx, &c->gsa, &c->gh};
+                     &c->E3, &c->dAinv, &c->tq, &c->gV, &c->gZ, &c->gw, &c->gb, &c->gx, &c->gsa, &c->gh, &c->gls};
   clear_graphs(c);
+  if (c->gres_h) { cudaFreeHost(c->gres_h); c->gres_h = nullptr; }
   if (c->cap_stream) { cudaStreamDestroy(c->cap_stream); c->cap_stream = nullptr; }
   if (c->copy_stream) { cudaStreamDestroy(c->copy_stream); c->copy_stream = nullptr; }
   for (cudaEvent_t* e : {&c->ev_in, &c->ev_ab, &c->ev_bt, &c->ev_done, &c->ev_p})
