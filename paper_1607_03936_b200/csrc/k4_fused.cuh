@@ -34,7 +34,7 @@
 
 namespace wb {
 
-template <int K, int TX, int TY, int TZ, bool TMA = false>
+template <int K, int TX, int TY, int TZ, bool TMA = false, bool XG = false>
 struct FK4 {
   static constexpr int NM = K * (K + 1) * (K + 2) / 6, NP = K * (K + 1) / 2;
   static constexpr int EX = TX + 2, EY = TY + 2, EZ = TZ + 2;             // extended (halo) elements
@@ -42,8 +42,9 @@ struct FK4 {
   static constexpr int NEH = EX * EY * EZ;
   static constexpr int PE = NM * NEH;           // Pe[m][lz][ly][lx]
   // X at the tile nodes, rows of XR (TMA: even, the box's 16-byte inner extent)
+  // (XG: no X in shared memory; stage X reads its node line from the padded global copy)
   static constexpr int XR = TMA ? (NX + 1) / 2 * 2 : NX;
-  static constexpr int XS = XR * NY * NZ;       // Xs[nz][ny][XR]
+  static constexpr int XS = XG ? 0 : XR * NY * NZ;  // Xs[nz][ny][XR]
   static constexpr int WZ = NP * EY * EX * NZ;  // Wz[p][ly][lx][nz]
   static constexpr int WY = K * EX * NY * NZ;   // Wy[m1][lx][ny][nz]
   static constexpr int VV = K * TX * NY * NZ;   // V[m1][lx'][ny][nz]   (in the Wz space)
@@ -191,10 +192,11 @@ __device__ __forceinline__ void k4_stage_y(const double* __restrict__ Wz, double
 
 // stages X and X' on the node line (ny, nz): y = sB X B^T along x, then its x-contraction
 // onto the own elements' modes m1
-template <int K, int TX, int TY, int TZ, int XR>
+template <int K, int TX, int TY, int TZ, int XR, bool XG = false>
 __device__ __forceinline__ void k4_stage_x(const double* __restrict__ Wy, const double* __restrict__ Xs,
                                            double* __restrict__ V, int item, double sB,
-                                           const double* __restrict__ Tx) {
+                                           const double* __restrict__ Tx, const double* __restrict__ xg = nullptr,
+                                           int xlim = 0) {
   using F = FK4<K, TX, TY, TZ>;
   if (item >= F::IX) return;
   double M[K][K + 1];
@@ -212,6 +214,11 @@ __device__ __forceinline__ void k4_stage_x(const double* __restrict__ Wy, const 
 #pragma unroll
     for (int m1 = 0; m1 < K; ++m1) acc[l][m1] = 0.0;
   const double* xr = Xs + (nz * F::NY + ny) * XR;
+  double xv[XG ? F::NX : 1];
+  if constexpr (XG) {  // the line's X (global, 0 past the mesh), all loads in flight first
+#pragma unroll
+    for (int n = 0; n < F::NX; ++n) xv[n] = n < xlim ? __ldg(xg + n) : 0.0;
+  }
 #pragma unroll
   for (int n = 0; n < F::NX; ++n) {
     const int l = n / K + 1, a = n % K;
@@ -222,7 +229,7 @@ __device__ __forceinline__ void k4_stage_x(const double* __restrict__ Wy, const 
 #pragma unroll
       for (int m1 = 0; m1 < K; ++m1) s = fma(M[m1][K], R[l - 1][m1], s);
     }
-    const double y = sB * xr[n] * s;  // X = 0 on the boundary and outside the mesh
+    const double y = sB * (XG ? xv[XG ? n : 0] : xr[n]) * s;  // X = 0 on the boundary and outside the mesh
     if (l - 1 < TX) {
 #pragma unroll
       for (int m1 = 0; m1 < K; ++m1) acc[l - 1][m1] = fma(M[m1][a], y, acc[l - 1][m1]);
@@ -362,14 +369,14 @@ __device__ __forceinline__ double k4_q_grp(const K4Acc<K, TZ>& A, const double* 
   return dot;
 }
 
-template <int K, int TX, int TY, int TZ, int MINB, bool TMA>
-__global__ void __launch_bounds__(FK4<K, TX, TY, TZ, TMA>::NTH, MINB)
+template <int K, int TX, int TY, int TZ, int MINB, bool TMA, bool XG = false>
+__global__ void __launch_bounds__(FK4<K, TX, TY, TZ, TMA, XG>::NTH, MINB)
     k_K4_fused(const double* __restrict__ pold, double* __restrict__ pnew, const double* __restrict__ z,
                const double* __restrict__ X, double* __restrict__ q, Geo G, double sB, int mode, int it, int ctl,
                const double* __restrict__ rzp, int nrz, double* rz_hist, const double* pq_hist, int* stop,
                double* pqp, const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_z,
                const __grid_constant__ CUtensorMap tm_x) {
-  using F = FK4<K, TX, TY, TZ, TMA>;
+  using F = FK4<K, TX, TY, TZ, TMA, XG>;
   extern __shared__ __align__(1024) double sm[];
   double* Pe = sm;
   double* Xs = sm + F::OFF_XS;
@@ -391,11 +398,11 @@ __global__ void __launch_bounds__(FK4<K, TX, TY, TZ, TMA>::NTH, MINB)
       mbar_init(&bar[0], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       mbar_expect_tx(&bar[0], F::XB + (mode != 2 ? F::BOXB : 0u) + (mode != 0 ? F::BOXB : 0u));
-      tma_load_3d(Xs, &tm_x, K * ex0, K * ey0, K * ez0, &bar[0]);
+      if (!XG) tma_load_3d(Xs, &tm_x, K * ex0, K * ey0, K * ez0, &bar[0]);
       if (mode != 2) tma_load_4d(Wz, &tm_z, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
       if (mode != 0) tma_load_4d(Wy, &tm_p, ex0 - 2, ey0 - 1, ez0 - 1, 0, &bar[0]);
     }
-  } else {
+  } else if constexpr (!XG) {
     // X at the tile nodes (asynchronous copies; 0 outside the mesh)
     for (int i = t; i < F::XS; i += F::NTH) {
       const int nx = i % F::NX, ny = (i / F::NX) % F::NY, nz = i / (F::NX * F::NY);
@@ -477,6 +484,16 @@ __global__ void __launch_bounds__(FK4<K, TX, TY, TZ, TMA>::NTH, MINB)
 #pragma unroll
       for (int m = 0; m < K; ++m) qa.v[j][l][m] = 0.0;
   __syncthreads();
+  // XG: the stage-X thread's node line in the padded global X (row stride nn1 + 1)
+  const double* xg = nullptr;
+  int xlim = 0;
+  if constexpr (XG) {
+    const int nz = t % F::NZ, ny = t / F::NZ, gy = K * ey0 + ny, gz = K * ez0 + nz;
+    if (t < F::IX && gy < G.nn1 && gz < G.nn1) {
+      xg = X + ((int64_t)gz * G.nn1 + gy) * (G.nn1 + 1) + K * ex0;
+      xlim = min(F::NX, G.nn1 - K * ex0);
+    }
+  }
   const int TS = K * (K + 1);
 #pragma unroll 1
   for (int c = 0; c < 3; ++c) {
@@ -488,7 +505,7 @@ __global__ void __launch_bounds__(FK4<K, TX, TY, TZ, TMA>::NTH, MINB)
     __syncthreads();
     k4_stage_y<K, TX, TY, TZ>(Wz, Wy, t, Ty);
     __syncthreads();
-    k4_stage_x<K, TX, TY, TZ, F::XR>(Wy, Xs, Wz /* V */, t, sB, Tx);
+    k4_stage_x<K, TX, TY, TZ, F::XR, XG>(Wy, Xs, Wz /* V */, t, sB, Tx, xg, xlim);
     __syncthreads();
     k4_stage_y2<K, TX, TY, TZ>(Wz /* V */, Wy /* U */, t, Ty);
     __syncthreads();

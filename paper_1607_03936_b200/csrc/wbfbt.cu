@@ -116,7 +116,7 @@ struct wb_ctx {
   bool tma4_ok = false;
   double *X4L = nullptr, *X4R = nullptr;
   struct K4Maps { CUtensorMap pp, pp1, pz, xL, xR; };
-  K4Maps tm4[2];  // per TMA tile variant (k4_var 1: 4 x 4 x 2, 5: 4 x 2 x 2)
+  K4Maps tm4[3];  // per TMA tile shape: 4 x 4 x 2 (k4_var 1, 6, 8), 4 x 2 x 2 (5), 4 x 4 x 3 (7)
   int kz = 0;  // TMA Poisson kernel: 1 = z = Minv r stored by the PCG update and loaded as one box; 0 = r + Minv boxes (default: faster with the y-fastest storage)
   int k_dbg = 0;  // timing probe bits for the fused K kernel (results invalid when nonzero)
   // profiling: CUDA-event pairs around every Poisson-operator launch (direct launches)
@@ -314,15 +314,15 @@ wb_status launch_k2f_t(wb_ctx* c, const double* pold, double* pnew, const double
   return WB_OK;
 }
 // fused k = 3, 4 Poisson operator (+ PCG direction update), one CTA per element tile
-template <int K, int TX, int TY, int TZ, int MINB, bool TMA = false>
+template <int K, int TX, int TY, int TZ, int MINB, bool TMA = false, bool XG = false>
 wb_status launch_k4f_t(wb_ctx* c, const double* pold, double* pnew, const double* X, double* q, int mode, PcgArgs a,
                        int* npq, const CUtensorMap* tp = nullptr, const CUtensorMap* tz = nullptr,
                        const CUtensorMap* tx = nullptr) {
-  using F = FK4<K, TX, TY, TZ, TMA>;
+  using F = FK4<K, TX, TY, TZ, TMA, XG>;
   const int N = c->N;
   const int nt = ((N + TX - 1) / TX) * ((N + TY - 1) / TY) * ((N + TZ - 1) / TZ);
   static const CUtensorMap none{};
-  k_K4_fused<K, TX, TY, TZ, MINB, TMA><<<nt, F::NTH, F::SMEM, c->stream>>>(
+  k_K4_fused<K, TX, TY, TZ, MINB, TMA, XG><<<nt, F::NTH, F::SMEM, c->stream>>>(
       pold, pnew, c->pz, X, q, c->G, c->sB, mode, a.it, a.ctl, c->rzp, c->red_blocks, rz_hist(c), pq_hist(c),
       c->stop, c->pqp, tp ? *tp : none, tz ? *tz : none, tx ? *tx : none);
   LAUNCH_CHECK(c);
@@ -333,7 +333,7 @@ wb_status launch_k4f_t(wb_ctx* c, const double* pold, double* pnew, const double
   X_(4, 3, 3, 3, 1, false) X_(4, 4, 4, 2, 2, false) X_(4, 4, 4, 2, 2, true) X_(4, 2, 2, 2, 2, false)             \
   X_(4, 4, 4, 4, 1, false) X_(3, 3, 3, 3, 2, false) X_(3, 4, 4, 4, 2, false) X_(4, 4, 2, 2, 3, false)           \
   X_(4, 4, 2, 2, 3, true)
-constexpr int K4_NV = 7;  // variants per order: k4_var indexes them (k = 3 has 2)
+constexpr int K4_NV = 9;  // variants per order: k4_var indexes them (k = 3 has 2)
 wb_status run_k4f(wb_ctx* c, const double* pold, double* pnew, const double* X, double* q, int mode, PcgArgs a,
                   int* npq) {
   if (c->k == 4) {
@@ -365,6 +365,16 @@ wb_status run_k4f(wb_ctx* c, const double* pold, double* pnew, const double* X, 
         LAUNCH_CHECK(c);
         *npq = nt;
         return WB_OK;
+      }
+      case 7:    // X from the padded global copy (no Xs): 4 x 4 x 3 tiles (one wave at C4), 4 x 4 x 2
+      case 8: {
+        const wb_ctx::K4Maps& m = c->tm4[c->k4_var == 7 ? 2 : 0];
+        const CUtensorMap* tp = pold == c->pp ? &m.pp : (pold == c->pp1 ? &m.pp1 : nullptr);
+        const double* xg = X == c->Cinv ? c->X4L : (X == c->Dinv ? c->X4R : nullptr);
+        if (!(c->tma4_ok && tp && xg)) return launch_k4f_t<4, 4, 4, 2, 2>(c, pold, pnew, X, q, mode, a, npq);
+        if (c->k4_var == 7)
+          return launch_k4f_t<4, 4, 4, 3, 2, true, true>(c, pold, pnew, xg, q, mode, a, npq, tp, &m.pz, &m.xL);
+        return launch_k4f_t<4, 4, 4, 2, 2, true, true>(c, pold, pnew, xg, q, mode, a, npq, tp, &m.pz, &m.xL);
       }
       case 2: return launch_k4f_t<4, 2, 2, 2, 2>(c, pold, pnew, X, q, mode, a, npq);
       case 3: return launch_k4f_t<4, 4, 4, 4, 1>(c, pold, pnew, X, q, mode, a, npq);
@@ -619,7 +629,8 @@ bool setup_tma4(wb_ctx* c) {
     cudaGetLastError();
     return false;
   }
-  return make_tm4<FK4<4, 4, 4, 2, true>>(c, c->tm4[0]) && make_tm4<FK4<4, 4, 2, 2, true>>(c, c->tm4[1]);
+  return make_tm4<FK4<4, 4, 4, 2, true>>(c, c->tm4[0]) && make_tm4<FK4<4, 4, 2, 2, true>>(c, c->tm4[1]) &&
+         make_tm4<FK4<4, 4, 4, 3, true>>(c, c->tm4[2]);
 }
 
 wb_status configure_kernels(wb_ctx* c) {
@@ -636,6 +647,10 @@ wb_status configure_kernels(wb_ctx* c) {
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FK4<K_, TX_, TY_, TZ_, T_>::SMEM));
   K4_VARIANTS(K4_ATTR)
 #undef K4_ATTR
+  CUDA_TRY(c, cudaFuncSetAttribute(k_K4_fused<4, 4, 4, 3, 2, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)FK4<4, 4, 4, 3, true, true>::SMEM));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_K4_fused<4, 4, 4, 2, 2, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)FK4<4, 4, 4, 2, true, true>::SMEM));
   CUDA_TRY(c, cudaFuncSetAttribute(k_K4_3c<4, 4, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)FK43<4, 4, 4, 2>::SMEM));
   CUDA_TRY(c, cudaFuncSetAttribute(k_A_slice<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
