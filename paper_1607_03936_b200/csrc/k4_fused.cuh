@@ -668,4 +668,204 @@ __global__ void __launch_bounds__(FK43<K, TX, TY, TZ>::NTH, 1)
   store_partial<H::NTH>(dot, pqp);
 }
 
+// ---------------------------------------------------------------- standalone B^T and B (k = 3, 4)
+// The same tile stages outside the PCG (rows a6, a7 at high order; wBFBT's B^T and B):
+//   k_BT4_tile: y = s o B^T p on the tile's own nodes (stages Z, Y, then X without X'), s =
+//     xs (the wBFBT X scaling), else the Dirichlet mask (0 on the boundary, R6), or 1 (nomask);
+//     a tile writes its nodes of local index < K T per axis, plus the mesh's last node plane.
+//   k_B4_tile: p = sB B (s o u): X' straight from the global node lines, then Y', Z'.
+// p is read / written at p[e se + m sm] (element-major ABI: se = n_m, sm = 1).
+template <int K, int TX, int TY, int TZ>
+struct FB4 {
+  using F = FK4<K, TX, TY, TZ>;
+  static constexpr int al16(int n) { return (n + 15) / 16 * 16; }
+  static constexpr int OFF_WZ = al16(F::PE), OFF_WY = OFF_WZ + al16(F::WZ), OFF_T = OFF_WY + al16(F::WY);
+  static constexpr int SMEM_BT = (OFF_T + al16(F::TABS)) * 8;
+  static constexpr int OFF_U = al16(F::VV), OFF_TB = OFF_U + al16(F::UU);
+  static constexpr int SMEM_B = (OFF_TB + al16(F::TABS)) * 8;
+  static constexpr int NTH_B = F::mx(F::mx(F::w32(F::IX), K * F::GWY2), K * F::GWZ2);
+};
+
+template <int K, int NTH>
+__device__ __forceinline__ void k4_load_tabs(double* Tb) {
+  for (int i = threadIdx.x; i < 2 * K * (K + 1); i += NTH) {
+    const int w = i / (K * (K + 1)), m = (i / (K + 1)) % K, a = i % (K + 1);
+    Tb[i] = w ? TB(K).BD[m][a] : TB(K).BI[m][a];
+  }
+}
+
+template <int K, int TX, int TY, int TZ>
+__global__ void __launch_bounds__(FK4<K, TX, TY, TZ>::NTH)
+    k_BT4_tile(const double* __restrict__ p, const double* __restrict__ xs, double* __restrict__ y, Geo G, double sB,
+               int nomask, int64_t se, int64_t sm_) {
+  using F = FK4<K, TX, TY, TZ>;
+  using H = FB4<K, TX, TY, TZ>;
+  extern __shared__ __align__(16) double smb[];
+  double* Pe = smb;
+  double* Wz = smb + H::OFF_WZ;
+  double* Wy = smb + H::OFF_WY;
+  double* Tb = smb + H::OFF_T;
+  const int N = G.N, t = threadIdx.x;
+  const int NTX = (N + TX - 1) / TX, NTY = (N + TY - 1) / TY;
+  const int tile = blockIdx.x;
+  const int ex0 = TX * (tile % NTX), ey0 = TY * ((tile / NTX) % NTY), ez0 = TZ * (tile / (NTX * NTY));
+  k4_load_tabs<K, F::NTH>(Tb);
+  for (int i = t; i < F::PE; i += F::NTH) {  // p on the tile + halo, 0 outside the mesh
+    const int ext = i % F::NEH, m = i / F::NEH;
+    const int lx = ext % F::EX, ly = (ext / F::EX) % F::EY, lz = ext / (F::EX * F::EY);
+    const int ex = ex0 + lx - 1, ey = ey0 + ly - 1, ez = ez0 + lz - 1;
+    const bool ok = (unsigned)ex < (unsigned)N && (unsigned)ey < (unsigned)N && (unsigned)ez < (unsigned)N;
+    Pe[i] = ok ? __ldg(p + (ex + (int64_t)N * (ey + (int64_t)N * ez)) * se + m * sm_) : 0.0;
+  }
+  __syncthreads();
+  const int TS = K * (K + 1);
+  const int nz = t % F::NZ, ny = t / F::NZ;
+  const int gy = K * ey0 + ny, gz = K * ez0 + nz;
+  // own node line: local index < K T, or the mesh's last node plane
+  const bool line = t < F::IX && gy < G.nn1 && gz < G.nn1 && (ny < K * TY || gy == G.nn1 - 1) &&
+                    (nz < K * TZ || gz == G.nn1 - 1);
+#pragma unroll 1
+  for (int c = 0; c < 3; ++c) {
+    const double* Tx = Tb + (c == 0 ? TS : 0);
+    const double* Ty = Tb + (c == 1 ? TS : 0);
+    const double* Tz = Tb + (c == 2 ? TS : 0);
+    k4_stage_z<K, TX, TY, TZ>(Pe, Wz, t, Tz);
+    __syncthreads();
+    k4_stage_y<K, TX, TY, TZ>(Wz, Wy, t, Ty);
+    __syncthreads();
+    if (line) {  // stage X: B^T along x on the line, scaled, to the global nodes
+      double M[K][K + 1];
+      k4_tab<K, K>(Tx, M);
+      const double* ib = Wy + ny * F::NZ + nz;
+      double R[F::EX][K];
+#pragma unroll
+      for (int lx = 0; lx < F::EX; ++lx)
+#pragma unroll
+        for (int m1 = 0; m1 < K; ++m1) R[lx][m1] = ib[(m1 * F::EX + lx) * F::NY * F::NZ];
+      const int64_t row = (int64_t)c * G.n_nodes + node_id(K * ex0, gy, gz, G.nn1);
+      const bool ybnd = gy == 0 || gz == 0 || gy == G.nn1 - 1 || gz == G.nn1 - 1;
+#pragma unroll
+      for (int n = 0; n < F::NX; ++n) {
+        const int l = n / K + 1, a = n % K;
+        const int gx = K * ex0 + n;
+        if (gx >= G.nn1 || (n == K * TX && gx != G.nn1 - 1)) continue;
+        double s = 0.0;
+#pragma unroll
+        for (int m1 = 0; m1 < K; ++m1) s = fma(M[m1][a], R[l][m1], s);
+        if (a == 0) {
+#pragma unroll
+          for (int m1 = 0; m1 < K; ++m1) s = fma(M[m1][K], R[l - 1][m1], s);
+        }
+        double o = sB * s;
+        if (xs) o *= xs[row - (int64_t)c * G.n_nodes + n];
+        else if (!nomask && (ybnd || gx == 0 || gx == G.nn1 - 1)) o = 0.0;
+        y[row + n] = o;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int K, int TX, int TY, int TZ>
+__global__ void __launch_bounds__(FB4<K, TX, TY, TZ>::NTH_B)
+    k_B4_tile(const double* __restrict__ u, const double* __restrict__ xs, double* __restrict__ p, Geo G, double sB,
+              int nomask, int64_t se, int64_t sm_) {
+  using F = FK4<K, TX, TY, TZ>;
+  using H = FB4<K, TX, TY, TZ>;
+  extern __shared__ __align__(16) double smb[];
+  double* V = smb;
+  double* U = smb + H::OFF_U;
+  double* Tb = smb + H::OFF_TB;
+  const int N = G.N, t = threadIdx.x;
+  const int NTX = (N + TX - 1) / TX, NTY = (N + TY - 1) / TY;
+  const int tile = blockIdx.x;
+  const int ex0 = TX * (tile % NTX), ey0 = TY * ((tile / NTX) % NTY), ez0 = TZ * (tile / (NTX * NTY));
+  k4_load_tabs<K, H::NTH_B>(Tb);
+  K4Acc<K, TZ> qa;
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+#pragma unroll
+    for (int l = 0; l < TZ; ++l)
+#pragma unroll
+      for (int m = 0; m < K; ++m) qa.v[j][l][m] = 0.0;
+  const int TS = K * (K + 1);
+  const int nz = t % F::NZ, ny = t / F::NZ;
+  const int gy = K * ey0 + ny, gz = K * ez0 + nz;
+  const bool line = t < F::IX && gy < G.nn1 && gz < G.nn1;
+  const int64_t row = line ? node_id(K * ex0, gy, gz, G.nn1) : 0;
+  const int xlim = line ? min(F::NX, G.nn1 - K * ex0) : 0;
+  const bool ybnd = gy == 0 || gz == 0 || gy == G.nn1 - 1 || gz == G.nn1 - 1;
+  __syncthreads();
+#pragma unroll 1
+  for (int c = 0; c < 3; ++c) {
+    const double* Tx = Tb + (c == 0 ? TS : 0);
+    const double* Ty = Tb + (c == 1 ? TS : 0);
+    const double* Tz = Tb + (c == 2 ? TS : 0);
+    if (t < F::IX) {  // stage X': the node line (s o u) along x onto the own elements' m1
+      double yv[F::NX];
+      const double* ur = u + (int64_t)c * G.n_nodes + row;
+#pragma unroll
+      for (int n = 0; n < F::NX; ++n) {
+        double v = n < xlim ? __ldg(ur + n) : 0.0;
+        if (xs) v *= n < xlim ? __ldg(xs + row + n) : 0.0;
+        else if (!nomask && (ybnd || K * ex0 + n == 0 || K * ex0 + n == G.nn1 - 1)) v = 0.0;
+        yv[n] = v;
+      }
+      double M[K][K + 1];
+      k4_tab<K, K>(Tx, M);
+      double acc[TX][K];
+#pragma unroll
+      for (int l = 0; l < TX; ++l)
+#pragma unroll
+        for (int m1 = 0; m1 < K; ++m1) acc[l][m1] = 0.0;
+#pragma unroll
+      for (int n = 0; n < F::NX; ++n) {
+        const int l = n / K + 1, a = n % K;
+        if (l - 1 < TX) {
+#pragma unroll
+          for (int m1 = 0; m1 < K; ++m1) acc[l - 1][m1] = fma(M[m1][a], yv[n], acc[l - 1][m1]);
+        }
+        if (a == 0 && l >= 2) {
+#pragma unroll
+          for (int m1 = 0; m1 < K; ++m1) acc[l - 2][m1] = fma(M[m1][K], yv[n], acc[l - 2][m1]);
+        }
+      }
+      double* ob = V + ny * F::NZ + nz;
+#pragma unroll
+      for (int l = 0; l < TX; ++l)
+#pragma unroll
+        for (int m1 = 0; m1 < K; ++m1) ob[(m1 * TX + l) * F::NY * F::NZ] = acc[l][m1];
+    }
+    __syncthreads();
+    k4_stage_y2<K, TX, TY, TZ>(V, U, t, Ty);
+    __syncthreads();
+    k4_stage_z2<K, TX, TY, TZ>(U, qa, t, Tz);
+    __syncthreads();
+  }
+  const int g = t / F::GWZ2, col = t % F::GWZ2;
+  if (g < K && col < TX * TY) {
+    const int lx = col % TX, ly = col / TX, ex = ex0 + lx, ey = ey0 + ly;
+    if (ex < N && ey < N) {
+#pragma unroll
+      for (int lz = 0; lz < TZ; ++lz) {
+        const int ez = ez0 + lz;
+        if (ez >= N) break;
+        const int64_t e = ex + (int64_t)N * (ey + (int64_t)N * ez);
+        // the group's modes (G - j, j, m3): written through a compile-time switch on g
+        switch (g) {
+#define K4_QW(GG)                                                                                  \
+  case GG:                                                                                         \
+    if constexpr (K > GG) {                                                                        \
+      _Pragma("unroll") for (int j = 0; j <= GG; ++j) _Pragma("unroll") for (int m3 = 0; m3 < K - GG; ++m3) \
+          p[e * se + (int64_t)k4_mode(GG - j, j, m3) * sm_] = sB * qa.v[j][lz][m3];                \
+    }                                                                                              \
+    break;
+          K4_QW(0) K4_QW(1) K4_QW(2) K4_QW(3)
+#undef K4_QW
+        }
+      }
+    }
+  }
+}
+
 }  // namespace wb

@@ -110,6 +110,9 @@ struct wb_ctx {
   double *XzL = nullptr, *XzR = nullptr;
   static constexpr int ZM_NV = 5;  // kernel variants (tile shape, CTAs per SM): zm_variants below
   CUtensorMap tz[ZM_NV][3];        // per variant: maps of pp, pp1, pz
+  // k = 3, 4 standalone B^T / B: 1 = B^T by the tile kernel (k4_fused.cuh), 2 = B^T and B by the tile
+  // kernels, 0 = the element kernels (+ gather).  Measured at C4: B^T 33 vs 43 us, B 54 vs 23 us.
+  int k4bt = 1;
   int k4f = 1, k4_var = 1;  // k = 3, 4: fused Poisson kernel (k4_fused.cuh) on, its tile variant
   // k = 4, even N: TMA tensor maps of the fused kernel's tile variant 1 (z, p boxes; X with
   // padded rows X4L / X4R)
@@ -651,6 +654,10 @@ wb_status configure_kernels(wb_ctx* c) {
                                    (int)FK4<4, 4, 4, 3, true, true>::SMEM));
   CUDA_TRY(c, cudaFuncSetAttribute(k_K4_fused<4, 4, 4, 2, 2, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)FK4<4, 4, 4, 2, true, true>::SMEM));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_BT4_tile<4, 4, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)FB4<4, 4, 4, 2>::SMEM_BT));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_BT4_tile<3, 4, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)FB4<3, 4, 4, 4>::SMEM_BT));
   CUDA_TRY(c, cudaFuncSetAttribute(k_K4_3c<4, 4, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)FK43<4, 4, 4, 2>::SMEM));
   CUDA_TRY(c, cudaFuncSetAttribute(k_A_slice<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -679,8 +686,26 @@ wb_status run_A(wb_ctx* c, const double* u, double* y, int nomask) {
   return DISPATCH_K(c, launch_gather_t, (const double*)nullptr, y, nomask);
 }
 // y = M B^T p (X o ... if xs), p[e*se + m*sm]
+template <int K, int TX, int TY, int TZ>
+void launch_bt4(wb_ctx* c, const double* p, const double* xs, double* y, int nomask, int64_t se, int64_t sm) {
+  const int N = c->N, nt = ((N + TX - 1) / TX) * ((N + TY - 1) / TY) * ((N + TZ - 1) / TZ);
+  k_BT4_tile<K, TX, TY, TZ><<<nt, FK4<K, TX, TY, TZ>::NTH, FB4<K, TX, TY, TZ>::SMEM_BT, c->stream>>>(
+      p, xs, y, c->G, c->sB, nomask, se, sm);
+}
+template <int K, int TX, int TY, int TZ>
+void launch_b4(wb_ctx* c, const double* u, const double* xs, double* p, int nomask, int64_t se, int64_t sm) {
+  const int N = c->N, nt = ((N + TX - 1) / TX) * ((N + TY - 1) / TY) * ((N + TZ - 1) / TZ);
+  k_B4_tile<K, TX, TY, TZ><<<nt, FB4<K, TX, TY, TZ>::NTH_B, FB4<K, TX, TY, TZ>::SMEM_B, c->stream>>>(
+      u, xs, p, c->G, c->sB, nomask, se, sm);
+}
 wb_status run_BT(wb_ctx* c, const double* p, const double* xs, double* y, int nomask, const int* stop,
                  int64_t se, int64_t sm) {
+  if (c->k >= 3 && c->k4bt && !stop) {  // tile kernels (k4_fused.cuh)
+    if (c->k == 4) launch_bt4<4, 4, 4, 2>(c, p, xs, y, nomask, se, sm);
+    else launch_bt4<3, 4, 4, 4>(c, p, xs, y, nomask, se, sm);
+    LAUNCH_CHECK(c);
+    return WB_OK;
+  }
   if (c->k == 2) {
     if (stop) {  // (generic-k PCG only; kept for completeness)
       dim3 grid(nblk(c->N + 1, 64), nblk(c->G.nn1, 4), 2 * c->G.nn1);
@@ -698,6 +723,12 @@ wb_status run_BT(wb_ctx* c, const double* p, const double* xs, double* y, int no
 }
 wb_status run_B(wb_ctx* c, const double* u, const double* xs, double* p, int nomask, const int* stop,
                 const double* dv, double* total, int64_t se, int64_t sm) {
+  if (c->k >= 3 && c->k4bt == 2 && !stop && !dv) {  // tile kernel (k4_fused.cuh)
+    if (c->k == 4) launch_b4<4, 4, 4, 2>(c, u, xs, p, nomask, se, sm);
+    else launch_b4<3, 4, 4, 4>(c, u, xs, p, nomask, se, sm);
+    LAUNCH_CHECK(c);
+    return WB_OK;
+  }
   if (c->k == 2 && !stop && !dv) {
     const int nt = ((c->N + 3) / 4) * ((c->N + 3) / 4) * ((c->N + 3) / 4);
     k_B_tile2<4, 4, 4><<<nt, BTile2<4, 4, 4>::NTH, BTile2<4, 4, 4>::SMEM, c->stream>>>(u, xs, p, c->G, c->sB, nomask,
@@ -2552,6 +2583,9 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k4f must be 0 or 1");
     c->k4f = (int)value;
     clear_graphs(c);
+  } else if (!strcmp(key, "k4bt")) {  // k = 3, 4: 1 = B^T tile kernel, 2 = B^T and B tile kernels, 0 = neither
+    if (value != 0.0 && value != 1.0 && value != 2.0) return set_err(c, WB_EINVAL, "k4bt must be 0, 1 or 2");
+    c->k4bt = (int)value;
   } else if (!strcmp(key, "k4_var")) {  // tile variant of the fused k = 3, 4 Poisson kernel
     if (!(value >= 0.0 && value < K4_NV) || value != (double)(int)value)
       return set_err(c, WB_EINVAL, "k4_var must be an integer in [0, %d)", K4_NV);

@@ -84,3 +84,19 @@ def test_k4_fused_full_c4_prefix():
     z = host(pr.ctx.apply_wbfbt(dev(b), empty(pr.ctx.n_p), 10))
     assert rel_l2(z, pr.o.wbfbt(b, 10)) <= 1e-10
     assert synth.CONFIGS["C4"].N == 24
+
+
+@pytest.mark.parametrize("opt", [0, 1, 2])
+def test_k4_tile_B_BT(pair, opt):
+    """Standalone B and B^T at high order through each path (option k4bt: 0 element kernels
+    + gather, 1 the B^T tile kernel, 2 the B^T and B tile kernels) against the oracle,
+    masked and X-scaled forms (<= 1e-11; boundary rows exactly 0)."""
+    ctx, o = pair.ctx, pair.o
+    ctx.set_option("k4bt", opt)
+    u, p = pair.inp["u"], pair.inp["p"]
+    y = host(ctx.apply_BT(dev(p), empty(ctx.n_v)))
+    assert rel_l2(y, o.apply_BT(p)) <= 1e-11
+    assert np.all(y[o.boundary_mask().astype(bool)] == 0.0)
+    q = host(ctx.apply_B(dev(u), empty(ctx.n_p)))
+    assert rel_l2(q, o.apply_B(u)) <= 1e-11
+    ctx.set_option("k4bt", 1)
