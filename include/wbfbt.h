@@ -296,6 +296,15 @@ wb_status wb_query(wb_ctx* ctx, const char* key, double* value);
  * kernel loads it as one box; 0 = it loads r and Minv, the default),
  * "k_ws" (k = 2 TMA Poisson kernel: 1 = warp-specialised, producer warps build
  * the next tile's direction box while the consumer warps apply B^T X^-1 B),
+ * "k4f" (k = 3, 4: 1 = the fused tile Poisson kernel of k4_fused.cuh, K_w = B X B^T by
+ * assembled 1-D contractions with the PCG direction update folded in, default; 0 = the
+ * B^T element kernel + node gather + B kernel), "k4_var" (its tile variant, 0..8; 1 =
+ * 4 x 4 x 2 tiles with TMA staging, the default; DESIGN.md Sec. 7 lists the others),
+ * "k4bt" (k = 3, 4 standalone B^T / B: 1 = B^T by the tile kernel, default; 2 = B too;
+ * 0 = the element kernels), "k_zm" / "zm_var" / "zm_zc" (k = 2: the opt-in z-march Poisson
+ * kernel, its variant and z-chunk length), "tma" (k = 2: 1 = the TMA Poisson kernel where the
+ * context's storage allows it, default), "k_variant" (k = 2 pointer Poisson kernel: 1 or 2 CTAs
+ * per SM), "k_dbg" (timing probe bits that skip kernel phases: results invalid, tools only),
  * "graph" (1 = replay the PCG iteration loop as a CUDA graph, default; 0 =
  * plain launches), "profile" (1 = plain launches with a CUDA-event pair around
  * every Poisson-operator launch; wb_query "prof_k_ms" / "prof_k_count" read

@@ -578,10 +578,10 @@ __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* 
   const int le = threadIdx.x / P, t = threadIdx.x % P, ta = t % n1, tb = t / n1;
   const int64_t e = (int64_t)blockIdx.x * NE + le;
   const bool valid = e < G.n_el;
-  double* A0 = sm + (size_t)le * 12 * NQ;
-  double* A1 = A0 + 3 * NQ;
-  double* GX = A1 + 3 * NQ;
-  double* GY = GX + 3 * NQ;
+  // three 3 NQ buffers per element, reused by liveness (X1: A0, GX, A1'; X2: A1, A0'; X3: GY)
+  double* X1 = sm + (size_t)le * 9 * NQ;
+  double* X2 = X1 + 3 * NQ;
+  double* X3 = X2 + 3 * NQ;
 #define IX(c, z, y, x) ((c)*NQ + ((z)*n1 + (y)) * n1 + (x))
   int ex = 0, ey = 0, ez = 0;
   if (valid) elem_xyz(e, G.N, ex, ey, ez);
@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* 
       const int gx = K * ex + ta, gy = K * ey + tb, gz = K * ez + z;
       double v = 0.0;
       if (valid && (nomask || !node_bnd(gx, gy, gz, G.nn1))) v = u[c * G.n_nodes + node_id(gx, gy, gz, G.nn1)];
-      A0[IX(c, z, tb, ta)] = v;
+      X1[IX(c, z, tb, ta)] = v;
     }
   __syncthreads();
   // S2 x-interp: thread (y = ta, z = tb)
@@ -601,13 +601,13 @@ __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* 
   for (int c = 0; c < 3; ++c) {
     double v[n1];
 #pragma unroll
-    for (int j = 0; j < n1; ++j) v[j] = A0[IX(c, tb, ta, j)];
+    for (int j = 0; j < n1; ++j) v[j] = X1[IX(c, tb, ta, j)];
 #pragma unroll
     for (int i = 0; i < n1; ++i) {
       double s = 0.0;
 #pragma unroll
       for (int j = 0; j < n1; ++j) s = fma(TB(K).I[i][j], v[j], s);
-      A1[IX(c, tb, ta, i)] = s;
+      X2[IX(c, tb, ta, i)] = s;
     }
   }
   __syncthreads();
@@ -616,13 +616,13 @@ __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* 
   for (int c = 0; c < 3; ++c) {
     double v[n1];
 #pragma unroll
-    for (int j = 0; j < n1; ++j) v[j] = A1[IX(c, tb, j, ta)];
+    for (int j = 0; j < n1; ++j) v[j] = X2[IX(c, tb, j, ta)];
 #pragma unroll
     for (int i = 0; i < n1; ++i) {
       double s = 0.0;
 #pragma unroll
       for (int j = 0; j < n1; ++j) s = fma(TB(K).I[i][j], v[j], s);
-      A0[IX(c, tb, i, ta)] = s;
+      X1[IX(c, tb, i, ta)] = s;
     }
   }
   __syncthreads();
@@ -632,14 +632,14 @@ __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* 
   for (int c = 0; c < 3; ++c) {
     double v[n1], Uz[n1];
 #pragma unroll
-    for (int j = 0; j < n1; ++j) v[j] = A0[IX(c, j, tb, ta)];
+    for (int j = 0; j < n1; ++j) v[j] = X1[IX(c, j, tb, ta)];
 #pragma unroll
     for (int i = 0; i < n1; ++i) {
       double s = 0.0;
 #pragma unroll
       for (int j = 0; j < n1; ++j) s = fma(TB(K).I[i][j], v[j], s);
       Uz[i] = s;
-      A1[IX(c, i, tb, ta)] = s;
+      X2[IX(c, i, tb, ta)] = s;
     }
 #pragma unroll
     for (int i = 0; i < n1; ++i) {
@@ -655,14 +655,14 @@ __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* 
   for (int c = 0; c < 3; ++c) {
     double v[n1], w[n1];
 #pragma unroll
-    for (int j = 0; j < n1; ++j) { v[j] = A1[IX(c, tb, ta, j)]; w[j] = A1[IX(c, tb, j, ta)]; }
+    for (int j = 0; j < n1; ++j) { v[j] = X2[IX(c, tb, ta, j)]; w[j] = X2[IX(c, tb, j, ta)]; }
 #pragma unroll
     for (int i = 0; i < n1; ++i) {
       double s = 0.0, r = 0.0;
 #pragma unroll
       for (int j = 0; j < n1; ++j) { s = fma(TB(K).Dg[i][j], v[j], s); r = fma(TB(K).Dg[i][j], w[j], r); }
-      GX[IX(c, tb, ta, i)] = s;
-      GY[IX(c, tb, i, ta)] = r;
+      X1[IX(c, tb, ta, i)] = s;
+      X3[IX(c, tb, i, ta)] = r;
     }
   }
   __syncthreads();
@@ -673,15 +673,15 @@ __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* 
     double g[3][3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      g[c][0] = GX[IX(c, iz, tb, ta)];
-      g[c][1] = GY[IX(c, iz, tb, ta)];
+      g[c][0] = X1[IX(c, iz, tb, ta)];
+      g[c][1] = X3[IX(c, iz, tb, ta)];
       g[c][2] = Gz[c][iz];
     }
     const double mu = valid ? mut[e * NQ + (iz * n1 + tb) * n1 + ta] : 0.0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      GX[IX(c, iz, tb, ta)] = mu * (g[c][0] + g[0][c]);
-      GY[IX(c, iz, tb, ta)] = mu * (g[c][1] + g[1][c]);
+      X1[IX(c, iz, tb, ta)] = mu * (g[c][0] + g[0][c]);
+      X3[IX(c, iz, tb, ta)] = mu * (g[c][1] + g[1][c]);
       Wz[c][iz] = mu * (g[c][2] + g[2][c]);
     }
   }
@@ -691,13 +691,13 @@ __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* 
   for (int c = 0; c < 3; ++c) {
     double v[n1];
 #pragma unroll
-    for (int i = 0; i < n1; ++i) v[i] = GX[IX(c, tb, ta, i)];
+    for (int i = 0; i < n1; ++i) v[i] = X1[IX(c, tb, ta, i)];
 #pragma unroll
     for (int j = 0; j < n1; ++j) {
       double s = 0.0;
 #pragma unroll
       for (int i = 0; i < n1; ++i) s = fma(TB(K).Dg[i][j], v[i], s);
-      A0[IX(c, tb, ta, j)] = s;
+      X2[IX(c, tb, ta, j)] = s;
     }
   }
   __syncthreads();
@@ -706,13 +706,13 @@ __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* 
   for (int c = 0; c < 3; ++c) {
     double v[n1];
 #pragma unroll
-    for (int i = 0; i < n1; ++i) v[i] = GY[IX(c, tb, i, ta)];
+    for (int i = 0; i < n1; ++i) v[i] = X3[IX(c, tb, i, ta)];
 #pragma unroll
     for (int j = 0; j < n1; ++j) {
-      double s = A0[IX(c, tb, j, ta)];
+      double s = X2[IX(c, tb, j, ta)];
 #pragma unroll
       for (int i = 0; i < n1; ++i) s = fma(TB(K).Dg[i][j], v[i], s);
-      A0[IX(c, tb, j, ta)] = s;
+      X2[IX(c, tb, j, ta)] = s;
     }
   }
   __syncthreads();
@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* 
     double Vz[n1];
 #pragma unroll
     for (int j = 0; j < n1; ++j) {
-      double s = A0[IX(c, j, tb, ta)];
+      double s = X2[IX(c, j, tb, ta)];
 #pragma unroll
       for (int i = 0; i < n1; ++i) s = fma(TB(K).Dg[i][j], Wz[c][i], s);
       Vz[j] = s;
@@ -732,7 +732,7 @@ __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* 
       double s = 0.0;
 #pragma unroll
       for (int j = 0; j < n1; ++j) s = fma(TB(K).I[j][a], Vz[j], s);
-      A1[IX(c, a, tb, ta)] = s;
+      X1[IX(c, a, tb, ta)] = s;
     }
   }
   __syncthreads();
@@ -741,13 +741,13 @@ __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* 
   for (int c = 0; c < 3; ++c) {
     double v[n1];
 #pragma unroll
-    for (int j = 0; j < n1; ++j) v[j] = A1[IX(c, tb, j, ta)];
+    for (int j = 0; j < n1; ++j) v[j] = X1[IX(c, tb, j, ta)];
 #pragma unroll
     for (int a = 0; a < n1; ++a) {
       double s = 0.0;
 #pragma unroll
       for (int j = 0; j < n1; ++j) s = fma(TB(K).I[j][a], v[j], s);
-      A0[IX(c, tb, a, ta)] = s;
+      X2[IX(c, tb, a, ta)] = s;
     }
   }
   __syncthreads();
@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(NE*(K + 1) * (K + 1)) k_A_slice(const double* 
   for (int c = 0; c < 3; ++c) {
     double v[n1];
 #pragma unroll
-    for (int j = 0; j < n1; ++j) v[j] = A0[IX(c, tb, ta, j)];
+    for (int j = 0; j < n1; ++j) v[j] = X2[IX(c, tb, ta, j)];
 #pragma unroll
     for (int a = 0; a < n1; ++a) {
       double s = 0.0;

@@ -238,14 +238,18 @@ wb_status ensure_iters(wb_ctx* c, int iters) {
   return WB_OK;
 }
 
+// elements per block of the k = 4 A slice kernel (9 NQ doubles of shared memory each)
+#ifndef A4_NE
+#define A4_NE 4
+#endif
 // ---------------------------------------------------------------- kernel dispatch helpers
 template <int K>
 wb_status launch_A_t(wb_ctx* c, const double* u, double* out_E, int nomask) {
   if constexpr (K == 2) {  // k = 2 goes through the tile kernels (run_A)
     return set_err(c, WB_ESTATE, "internal: element-local A path is not used for k = 2");
   } else {
-    constexpr int NE = (K == 3) ? 8 : 5;
-    const size_t smem = (size_t)NE * 12 * Ord<K>::NQ * sizeof(double);  // attribute set in configure_kernels
+    constexpr int NE = (K == 3) ? 8 : A4_NE;
+    const size_t smem = (size_t)NE * 9 * Ord<K>::NQ * sizeof(double);  // attribute set in configure_kernels
     k_A_slice<K, NE><<<nblk(c->n_el, NE), NE * (K + 1) * (K + 1), smem, c->stream>>>(c->mut, u, out_E, c->G, nomask);
     LAUNCH_CHECK(c);
     return WB_OK;
@@ -661,9 +665,9 @@ wb_status configure_kernels(wb_ctx* c) {
   CUDA_TRY(c, cudaFuncSetAttribute(k_K4_3c<4, 4, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)FK43<4, 4, 4, 2>::SMEM));
   CUDA_TRY(c, cudaFuncSetAttribute(k_A_slice<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(8 * 12 * Ord<3>::NQ * sizeof(double))));
-  CUDA_TRY(c, cudaFuncSetAttribute(k_A_slice<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(5 * 12 * Ord<4>::NQ * sizeof(double))));
+                                   (int)(8 * 9 * Ord<3>::NQ * sizeof(double))));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_A_slice<4, A4_NE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(A4_NE * 9 * Ord<4>::NQ * sizeof(double))));
   return WB_OK;
 }
 
