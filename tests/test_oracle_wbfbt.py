@@ -49,8 +49,12 @@ def converged_iters(o, Xinv, diagK, b, tol=1e-13, step=5, cap=2000):
     raise AssertionError("PCG did not converge")
 
 
-@pytest.mark.parametrize("N,k", [(2, 2), (3, 2), (2, 4)])
+@pytest.mark.parametrize("N,k", [(2, 2), (3, 2), (2, 4), (1, 2), (1, 4)])
 def test_pcg_converges_to_pseudoinverse(N, k):
+    """N = 1 pins the pseudo-inverse Jacobi threshold of R11 (jacobi_minv): on one element
+    every velocity node but the interior ones is Dirichlet, the constant-mode row of K vanishes
+    (the interior bubbles' derivatives integrate to zero), its diagonal is rounding-level, and
+    only Minv = 0 there (not 1 / diag) lets PCG converge to the deflated K^+ b."""
     o = Oracle(N, k)
     st = o.setup(_mild_mu(o))
     assert st["n_nonpos_Dw"] == 0
@@ -62,6 +66,21 @@ def test_pcg_converges_to_pseudoinverse(N, k):
     x = o.poisson(st["Dinv"], st["diagKr"], b, iters=it)
     ref = _pinv_deflated(K, z) @ b
     assert np.linalg.norm(x - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("N,k", [(2, 2), (2, 4)])
+def test_poisson_relres_closed_forms(N, k):
+    """or_poisson_relres = ||b - K x|| / ||b||: exactly 1 at x = 0, and |1 - t| at
+    x = t K^+ b for b in the range of K (b projected off the constant pressure)."""
+    o = Oracle(N, k)
+    st = o.setup(_mild_mu(o, 3))
+    B = _dense_B(o)
+    K = B @ (np.tile(st["Dinv"], 3)[:, None] * B.T)
+    b = o.project(np.random.default_rng(5).uniform(-1, 1, o.n_p))
+    assert o.poisson_relres(st["Dinv"], b, np.zeros(o.n_p)) == 1.0
+    xs = _pinv_deflated(K, _z0(o)) @ b
+    for t, want in ((1.0, 0.0), (0.5, 0.5), (-1.0, 2.0)):
+        assert abs(o.poisson_relres(st["Dinv"], b, t * xs) - want) <= 1e-11
 
 
 def test_pcg_one_iteration_closed_form():
