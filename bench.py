@@ -427,6 +427,36 @@ def run_ours(args):
                       "(graph launch gaps as in the timed step)"}
     tKw = k_avg
 
+    # ---- the high-order configuration C4 (Q4 x P3disc, BASELINE.json configs[3]), not in the
+    # step: A / B / B^T GDOF/s, wBFBT applies/s at its 2 x 50 PCG iterations, and the fused
+    # k = 4 Poisson kernel (k_K4_fused, k4_fused.cuh) launch time inside the PCG graphs
+    c4 = None
+    if args.config != "C4" and not args.no_c4:
+        cfg4 = synth.CONFIGS["C4"]
+        inp4 = synth.make_inputs(cfg4, seed=replica_seed(rank))
+        ctx4 = Context(cfg4.N, cfg4.k, stream=stream.cuda_stream)
+        mu4, u4, p4 = d(inp4["mu_q"]), d(inp4["u"]), d(inp4["p"])
+        ctx4.set_viscosity(mu4)
+        y4, q4, z4 = torch.empty(ctx4.n_v, **f64), torch.empty(ctx4.n_p, **f64), torch.empty(ctx4.n_p, **f64)
+        tA4 = timed(lambda: ctx4.apply_A(u4, y4))
+        tB4 = timed(lambda: ctx4.apply_B(u4, q4))
+        tBT4 = timed(lambda: ctx4.apply_BT(p4, y4))
+        tW4 = timed(lambda: ctx4.apply_wbfbt(p4, z4, cfg4.iters), reps=max(3, args.comp_reps // 4))
+        ctx4.set_option("profile", 1)
+        ctx4.apply_wbfbt(p4, z4, cfg4.iters)
+        torch.cuda.synchronize()
+        k4_ms, k4_n = ctx4.query("prof_k_ms"), int(ctx4.query("prof_k_count"))
+        ctx4.set_option("profile", 0)
+        n4 = ctx4.n_v
+        c4 = {"workload": workload_of(cfg4), "A_gdofs": n4 / (tA4 * 1e-3) / 1e9, "A_ms": tA4,
+              "B_gdofs": n4 / (tB4 * 1e-3) / 1e9, "BT_gdofs": n4 / (tBT4 * 1e-3) / 1e9,
+              "wbfbt_ms": tW4, "wbfbt_applies_per_s": 1e3 / tW4,
+              "k4_fused_launch_us": 1e3 * k4_ms / max(k4_n, 1), "k4_fused_launches_per_apply": k4_n,
+              "note": "C4 (not in the step): L2 flushed before each rep; k_K4_fused timed by CUDA-event record "
+                      "nodes around every launch of one wBFBT apply's captured PCG loops"}
+        ctx4.close()
+        del mu4, u4, p4, y4, q4, z4
+
     # ---- end to end through the host entry (pinned buffers)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
     hmu, hu, hp = pin(inp["mu_q"]), pin(inp["u"]), pin(inp["p"])
@@ -481,7 +511,8 @@ def run_ours(args):
                     "multigrid": mg,
                     "stokes_fgmres": {"iter_ms": stokes_iter_ms, "relres_after": {str(k): v for k, v in rr_st.items()},
                                       "note": "R19 (not in the step): FGMRES on [A B^T; B 0], f = u, g = 0; per "
-                                              "iteration wBFBT (2 x iters PCG) + 6 smoother steps"}},
+                                              "iteration wBFBT (2 x iters PCG) + 6 smoother steps"},
+                    "C4": c4},
                 "roofline": roof,
                 "e2e": {"value": e2e, "unit": unit_of(cfg), "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h},
@@ -504,6 +535,7 @@ def main():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--comp-reps", type=int, default=30)  # median of >= 30 reps
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")  # skip the high-order C4 component block
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

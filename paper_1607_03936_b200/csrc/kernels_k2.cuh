@@ -113,3 +113,4 @@ __global__ void __launch_bounds__(256) k_BT_node2(const double* __restrict__ p, 
 #include "k2_bbt.cuh"
 #include "k2_setup.cuh"
 #include "k4_fused.cuh"
+#include "k2_zc.cuh"

@@ -112,6 +112,7 @@ struct wb_ctx {
   CUtensorMap tz[ZM_NV][3];        // per variant: maps of pp, pp1, pz
   // k = 3, 4 standalone B^T / B: 1 = B^T by the tile kernel (k4_fused.cuh), 2 = B^T and B by the tile
   // kernels, 0 = the element kernels (+ gather).  Measured at C4: B^T 33 vs 43 us, B 54 vs 23 us.
+  int bbt_zc = 0;  // k = 2 B / B^T: 0 = tile / box kernels, 2 / 4 / 8 = z-marching column kernels (k2_zc.cuh), CZ layers
   int k4bt = 1;
   int k4f = 1, k4_var = 1;  // k = 3, 4: fused Poisson kernel (k4_fused.cuh) on, its tile variant
   // k = 4, even N: TMA tensor maps of the fused kernel's tile variant 1 (z, p boxes; X with
@@ -710,6 +711,17 @@ wb_status run_BT(wb_ctx* c, const double* p, const double* xs, double* y, int no
     LAUNCH_CHECK(c);
     return WB_OK;
   }
+  if (c->k == 2 && !stop && c->bbt_zc) {  // z-marching columns (k2_zc.cuh)
+    const int64_t nc = (int64_t)c->G.nn1 * c->G.nn1;
+    const int cz = c->bbt_zc;
+    const int64_t nt = nc * ((c->N + cz - 1) / cz);
+    const unsigned nb = (unsigned)((nt + 127) / 128);
+    if (cz == 2) k_BT_zc2<2><<<nb, 128, 0, c->stream>>>(p, xs, y, c->G, c->sB, nomask, se, sm);
+    else if (cz == 4) k_BT_zc2<4><<<nb, 128, 0, c->stream>>>(p, xs, y, c->G, c->sB, nomask, se, sm);
+    else k_BT_zc2<8><<<nb, 128, 0, c->stream>>>(p, xs, y, c->G, c->sB, nomask, se, sm);
+    LAUNCH_CHECK(c);
+    return WB_OK;
+  }
   if (c->k == 2) {
     if (stop) {  // (generic-k PCG only; kept for completeness)
       dim3 grid(nblk(c->N + 1, 64), nblk(c->G.nn1, 4), 2 * c->G.nn1);
@@ -730,6 +742,16 @@ wb_status run_B(wb_ctx* c, const double* u, const double* xs, double* p, int nom
   if (c->k >= 3 && c->k4bt == 2 && !stop && !dv) {  // tile kernel (k4_fused.cuh)
     if (c->k == 4) launch_b4<4, 4, 4, 2>(c, u, xs, p, nomask, se, sm);
     else launch_b4<3, 4, 4, 4>(c, u, xs, p, nomask, se, sm);
+    LAUNCH_CHECK(c);
+    return WB_OK;
+  }
+  if (c->k == 2 && !stop && !dv && c->bbt_zc) {  // z-marching columns (k2_zc.cuh)
+    const int cz = c->bbt_zc;
+    const int64_t nt = (int64_t)c->N * c->N * ((c->N + cz - 1) / cz);
+    const unsigned nb = (unsigned)((nt + 127) / 128);
+    if (cz == 2) k_B_zc2<2><<<nb, 128, 0, c->stream>>>(u, xs, p, c->G, c->sB, nomask, se, sm);
+    else if (cz == 4) k_B_zc2<4><<<nb, 128, 0, c->stream>>>(u, xs, p, c->G, c->sB, nomask, se, sm);
+    else k_B_zc2<8><<<nb, 128, 0, c->stream>>>(u, xs, p, c->G, c->sB, nomask, se, sm);
     LAUNCH_CHECK(c);
     return WB_OK;
   }
@@ -2587,6 +2609,10 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k4f must be 0 or 1");
     c->k4f = (int)value;
     clear_graphs(c);
+  } else if (!strcmp(key, "bbt_zc")) {  // k = 2 B / B^T: 0 = tile / box kernels, 2, 4, 8 = z-march, CZ layers
+    if (value != 0.0 && value != 2.0 && value != 4.0 && value != 8.0)
+      return set_err(c, WB_EINVAL, "bbt_zc must be 0, 2, 4 or 8");
+    c->bbt_zc = (int)value;
   } else if (!strcmp(key, "k4bt")) {  // k = 3, 4: 1 = B^T tile kernel, 2 = B^T and B tile kernels, 0 = neither
     if (value != 0.0 && value != 1.0 && value != 2.0) return set_err(c, WB_EINVAL, "k4bt must be 0, 1 or 2");
     c->k4bt = (int)value;
