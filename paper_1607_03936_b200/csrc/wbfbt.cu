@@ -112,7 +112,9 @@ struct wb_ctx {
   CUtensorMap tz[ZM_NV][3];        // per variant: maps of pp, pp1, pz
   // k = 3, 4 standalone B^T / B: 1 = B^T by the tile kernel (k4_fused.cuh), 2 = B^T and B by the tile
   // kernels, 0 = the element kernels (+ gather).  Measured at C4: B^T 33 vs 43 us, B 54 vs 23 us.
-  int bbt_zc = 0;  // k = 2 B / B^T: 0 = tile / box kernels, 2 / 4 / 8 = z-marching column kernels (k2_zc.cuh), CZ layers
+  // k = 2 B / B^T: 0 = tile / box kernels, 2 / 4 / 8 = z-marching column kernels (k2_zc.cuh) with CZ
+  // element layers per chunk, -1 = auto (4 on meshes with N >= 48, else 0)
+  int bbt_zc = -1;
   int k4bt = 1;
   int k4f = 1, k4_var = 1;  // k = 3, 4: fused Poisson kernel (k4_fused.cuh) on, its tile variant
   // k = 4, even N: TMA tensor maps of the fused kernel's tile variant 1 (z, p boxes; X with
@@ -690,6 +692,8 @@ wb_status run_A(wb_ctx* c, const double* u, double* y, int nomask) {
   if (s) return s;
   return DISPATCH_K(c, launch_gather_t, (const double*)nullptr, y, nomask);
 }
+// chunk length of the k = 2 z-march B / B^T kernels, 0 = the tile / box kernels
+int zc_of(const wb_ctx* c) { return c->bbt_zc >= 0 ? c->bbt_zc : (c->N >= 48 ? 4 : 0); }
 // y = M B^T p (X o ... if xs), p[e*se + m*sm]
 template <int K, int TX, int TY, int TZ>
 void launch_bt4(wb_ctx* c, const double* p, const double* xs, double* y, int nomask, int64_t se, int64_t sm) {
@@ -711,9 +715,9 @@ wb_status run_BT(wb_ctx* c, const double* p, const double* xs, double* y, int no
     LAUNCH_CHECK(c);
     return WB_OK;
   }
-  if (c->k == 2 && !stop && c->bbt_zc) {  // z-marching columns (k2_zc.cuh)
+  if (c->k == 2 && !stop && zc_of(c)) {  // z-marching columns (k2_zc.cuh)
     const int64_t nc = (int64_t)c->G.nn1 * c->G.nn1;
-    const int cz = c->bbt_zc;
+    const int cz = zc_of(c);
     const int64_t nt = nc * ((c->N + cz - 1) / cz);
     const unsigned nb = (unsigned)((nt + 127) / 128);
     if (cz == 2) k_BT_zc2<2><<<nb, 128, 0, c->stream>>>(p, xs, y, c->G, c->sB, nomask, se, sm);
@@ -745,8 +749,8 @@ wb_status run_B(wb_ctx* c, const double* u, const double* xs, double* p, int nom
     LAUNCH_CHECK(c);
     return WB_OK;
   }
-  if (c->k == 2 && !stop && !dv && c->bbt_zc) {  // z-marching columns (k2_zc.cuh)
-    const int cz = c->bbt_zc;
+  if (c->k == 2 && !stop && !dv && zc_of(c)) {  // z-marching columns (k2_zc.cuh)
+    const int cz = zc_of(c);
     const int64_t nt = (int64_t)c->N * c->N * ((c->N + cz - 1) / cz);
     const unsigned nb = (unsigned)((nt + 127) / 128);
     if (cz == 2) k_B_zc2<2><<<nb, 128, 0, c->stream>>>(u, xs, p, c->G, c->sB, nomask, se, sm);
@@ -2610,8 +2614,8 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
     c->k4f = (int)value;
     clear_graphs(c);
   } else if (!strcmp(key, "bbt_zc")) {  // k = 2 B / B^T: 0 = tile / box kernels, 2, 4, 8 = z-march, CZ layers
-    if (value != 0.0 && value != 2.0 && value != 4.0 && value != 8.0)
-      return set_err(c, WB_EINVAL, "bbt_zc must be 0, 2, 4 or 8");
+    if (value != -1.0 && value != 0.0 && value != 2.0 && value != 4.0 && value != 8.0)
+      return set_err(c, WB_EINVAL, "bbt_zc must be -1 (auto), 0, 2, 4 or 8");
     c->bbt_zc = (int)value;
   } else if (!strcmp(key, "k4bt")) {  // k = 3, 4: 1 = B^T tile kernel, 2 = B^T and B tile kernels, 0 = neither
     if (value != 0.0 && value != 1.0 && value != 2.0) return set_err(c, WB_EINVAL, "k4bt must be 0, 1 or 2");

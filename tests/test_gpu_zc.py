@@ -1,5 +1,6 @@
 """k = 2 B and B^T by z-marching columns (csrc/k2_zc.cuh, option bbt_zc = 2, 4, 8 element
-layers per chunk) against the oracle (rows a6, a7: <= 1e-11, boundary rows exactly 0), on
+layers per chunk; the default on N >= 48 meshes, so the full-size C5 tests of test_gpu_api /
+test_gpu_parity run it too) against the oracle (rows a6, a7: <= 1e-11, boundary rows exactly 0), on
 ragged and chunk-ragged meshes, and inside wBFBT (the X-scaled forms) against the default
 tile / box kernels."""
 import numpy as np
@@ -28,7 +29,7 @@ def test_zc_B_BT(pair, cz):
         q = host(ctx.apply_B(dev(u), empty(ctx.n_p)))
         assert rel_l2(q, o.apply_B(u)) <= 1e-11
     finally:
-        ctx.set_option("bbt_zc", 0)
+        ctx.set_option("bbt_zc", -1)
 
 
 def test_zc_in_wbfbt(pair):
@@ -36,11 +37,12 @@ def test_zc_in_wbfbt(pair):
     z-march kernels agree with the tile / box kernels to rounding."""
     ctx = pair.ctx
     r = dev(pair.inp["p"])
-    z0 = host(ctx.apply_wbfbt(r, empty(ctx.n_p), 5))
-    ctx.set_option("bbt_zc", 4)
     try:
+        ctx.set_option("bbt_zc", 0)
+        z0 = host(ctx.apply_wbfbt(r, empty(ctx.n_p), 5))
+        ctx.set_option("bbt_zc", 4)
         z1 = host(ctx.apply_wbfbt(r, empty(ctx.n_p), 5))
     finally:
-        ctx.set_option("bbt_zc", 0)
+        ctx.set_option("bbt_zc", -1)
     tol = 1e-9 if (pair.ost["n_nonpos_Cw"] or pair.ost["n_nonpos_Dw"]) else 1e-12
     assert rel_l2(z1, z0) <= tol
