@@ -433,7 +433,20 @@ const CUtensorMap* tmap_of(wb_ctx* c, const double* p) {
 
 // the k = 2 Poisson operator runs as the TMA kernel (k_K2_tma); the PCG init/update
 // kernels then also store z = Minv r, which it reads instead of r and Minv
-bool tma_active(const wb_ctx* c) { return c->k == 2 && c->tma_ok && c->use_tma && c->n_el >= 148 * 256 * 2; }
+// smallest mesh (elements) that gets the TMA Poisson kernel's y-fastest storage (even N only).
+// Every even mesh by default: measured against the pointer kernel (4 x 4 x 4 tiles) on the
+// small configs, wBFBT applies/s C1 2056 -> 2353, C2 797 -> 1012, C3 598 -> 876 (round 1 kept
+// the pointer kernel below two 256-element tiles per SM).  WB_TMA_MIN_EL overrides it at
+// wb_create (measurement only).
+int64_t tma_min_el() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("WB_TMA_MIN_EL");
+    v = e ? atoll(e) : 0;
+  }
+  return v;
+}
+bool tma_active(const wb_ctx* c) { return c->k == 2 && c->tma_ok && c->use_tma && c->ylay; }
 // the node-owner z-march kernel (k2_zm.cuh) replaces it where set up; it always reads z
 bool zm_active(const wb_ctx* c) { return tma_active(c) && c->zm_ok && c->use_zm; }
 // X = sB^2 C_w^-1, sB^2 D_w^-1 on the padded nodal grid of the z-march kernel: built eagerly
@@ -1523,7 +1536,7 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
   alloc(&c->Cw, c->n_nodes); alloc(&c->Dw, c->n_nodes); alloc(&c->Cinv, c->n_nodes); alloc(&c->Dinv, c->n_nodes);
   // PCG vector storage: y fastest with zero pads for the TMA Poisson kernel (k = 2, even N,
   // large meshes, tensor-map encoder available), else mode-major m n_el + e
-  c->ylay = k == 2 && !(N & 1) && c->n_el >= 148 * 256 * 2 && get_encode();
+  c->ylay = k == 2 && !(N & 1) && c->n_el >= tma_min_el() && get_encode();
   if (c->ylay) {
     const int64_t sz = N + 2, sx = (int64_t)N * sz, sm = (int64_t)N * sx;
     c->pl = PLay{sm, sx, 1, sz, c->nm * sm, 1};
@@ -1586,7 +1599,7 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
   }
   c->tma_ok = setup_tma(c);  // the pointer kernel serves contexts without the y-fastest storage
   c->tma4_ok = setup_tma4(c);  // k = 4, even N: the fused kernel's TMA variant (else its LDG form)
-  c->zm_ok = c->tma_ok && setup_zm(c);
+  c->zm_ok = false;  // the opt-in z-march kernel's buffers and maps: set up when option k_zm is first set
   if (c->ylay && !c->tma_ok) {
     free_all(c);
     delete c;
@@ -2633,6 +2646,8 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k_zm must be 0 or 1");
     c->use_zm = (int)value;
     clear_graphs(c);
+    if (c->use_zm && c->tma_ok && !c->zm_ok && !(c->zm_ok = setup_zm(c)))
+      return set_err(c, WB_ECUDA, "z-march kernel setup failed");
     if (c->use_zm && c->zm_ok && c->have_visc && !c->xz_valid && build_xz(c)) return set_err(c, WB_ECUDA, "X build");
   } else if (!strcmp(key, "zm_var")) {  // z-march kernel variant (tile shape, CTAs per SM)
     if (!(value >= 0.0 && value < wb_ctx::ZM_NV) || value != (double)(int)value)
