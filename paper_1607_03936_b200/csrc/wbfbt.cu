@@ -122,7 +122,7 @@ struct wb_ctx {
   bool tma4_ok = false;
   double *X4L = nullptr, *X4R = nullptr;
   struct K4Maps { CUtensorMap pp, pp1, pz, xL, xR; };
-  K4Maps tm4[3];  // per TMA tile shape: 4 x 4 x 2 (k4_var 1, 6, 8), 4 x 2 x 2 (5), 4 x 4 x 3 (7)
+  K4Maps tm4[4];  // per TMA tile shape: 4 x 4 x 2 (k4_var 1, 6, 8), 4 x 2 x 2 (5), 4 x 4 x 3 (7), 4 x 3 x 2 (9)
   int kz = 0;  // TMA Poisson kernel: 1 = z = Minv r stored by the PCG update and loaded as one box; 0 = r + Minv boxes (default: faster with the y-fastest storage)
   int k_dbg = 0;  // timing probe bits for the fused K kernel (results invalid when nonzero)
   // profiling: CUDA-event pairs around every Poisson-operator launch (direct launches)
@@ -342,8 +342,8 @@ wb_status launch_k4f_t(wb_ctx* c, const double* pold, double* pnew, const double
 #define K4_VARIANTS(X_)                                                                                         \
   X_(4, 3, 3, 3, 1, false) X_(4, 4, 4, 2, 2, false) X_(4, 4, 4, 2, 2, true) X_(4, 2, 2, 2, 2, false)             \
   X_(4, 4, 4, 4, 1, false) X_(3, 3, 3, 3, 2, false) X_(3, 4, 4, 4, 2, false) X_(4, 4, 2, 2, 3, false)           \
-  X_(4, 4, 2, 2, 3, true)
-constexpr int K4_NV = 9;  // variants per order: k4_var indexes them (k = 3 has 2)
+  X_(4, 4, 2, 2, 3, true) X_(4, 4, 3, 2, 2, true) X_(4, 4, 3, 2, 2, false)
+constexpr int K4_NV = 10;  // variants per order: k4_var indexes them (k = 3 has 2)
 wb_status run_k4f(wb_ctx* c, const double* pold, double* pnew, const double* X, double* q, int mode, PcgArgs a,
                   int* npq) {
   if (c->k == 4) {
@@ -385,6 +385,14 @@ wb_status run_k4f(wb_ctx* c, const double* pold, double* pnew, const double* X, 
         if (c->k4_var == 7)
           return launch_k4f_t<4, 4, 4, 3, 2, true, true>(c, pold, pnew, xg, q, mode, a, npq, tp, &m.pz, &m.xL);
         return launch_k4f_t<4, 4, 4, 2, 2, true, true>(c, pold, pnew, xg, q, mode, a, npq, tp, &m.pz, &m.xL);
+      }
+      case 9: {  // 4 x 3 x 2 tiles (576 at C4: 1.95 waves of two CTAs per SM), TMA
+        const wb_ctx::K4Maps& m = c->tm4[3];
+        const CUtensorMap* tp = pold == c->pp ? &m.pp : (pold == c->pp1 ? &m.pp1 : nullptr);
+        const CUtensorMap* tx = X == c->Cinv ? &m.xL : (X == c->Dinv ? &m.xR : nullptr);
+        if (c->tma4_ok && tp && tx)
+          return launch_k4f_t<4, 4, 3, 2, 2, true>(c, pold, pnew, X, q, mode, a, npq, tp, &m.pz, tx);
+        return launch_k4f_t<4, 4, 3, 2, 2>(c, pold, pnew, X, q, mode, a, npq);
       }
       case 2: return launch_k4f_t<4, 2, 2, 2, 2>(c, pold, pnew, X, q, mode, a, npq);
       case 3: return launch_k4f_t<4, 4, 4, 4, 1>(c, pold, pnew, X, q, mode, a, npq);
@@ -653,7 +661,7 @@ bool setup_tma4(wb_ctx* c) {
     return false;
   }
   return make_tm4<FK4<4, 4, 4, 2, true>>(c, c->tm4[0]) && make_tm4<FK4<4, 4, 2, 2, true>>(c, c->tm4[1]) &&
-         make_tm4<FK4<4, 4, 4, 3, true>>(c, c->tm4[2]);
+         make_tm4<FK4<4, 4, 4, 3, true>>(c, c->tm4[2]) && make_tm4<FK4<4, 4, 3, 2, true>>(c, c->tm4[3]);
 }
 
 wb_status configure_kernels(wb_ctx* c) {

@@ -22,7 +22,7 @@ def pair(request):
 
 
 def variants(k):
-    return [0, 1, 2, 3, 4, 5, 6, 7, 8] if k == 4 else [0, 1]
+    return [0, 1, 2, 3, 4, 5, 6, 7, 8, 9] if k == 4 else [0, 1]
 
 
 def test_k4_fused_apply_K(pair):

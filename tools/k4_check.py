@@ -24,7 +24,7 @@ for cfg, N in [("C4", 1), ("C4", 2), ("C4", 3), ("C4", 5), ("C4", 8), ("C4", 12)
     c.set_viscosity(d(inp["mu_q"]))
     p = d(inp["p"])
     out = {}
-    for var in ([None, 0, 1, 2, 3, 4, 5, 6, 7, 8] if inp["k"] == 4 else [None, 0, 1]):
+    for var in ([None, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9] if inp["k"] == 4 else [None, 0, 1]):
         if var is None:
             c.set_option("k4f", 0)
         else:
@@ -59,7 +59,7 @@ def t_us(fn, reps=9):
     return statistics.median(ts) * 1e3
 
 
-for var in [None, 0, 1, 2, 3, 4, 5, 6, 7, 8]:
+for var in [None, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9]:
     if var is None:
         c.set_option("k4f", 0)
     else:
