@@ -284,7 +284,10 @@ wb_status wb_get_jacobi(wb_ctx* ctx, double* diagKl, double* diagKr);
  * "pcg_nonfinite" (failure detection: the number of non-finite rz_i / pq_i control scalars of
  * the last PCG solve, 0 when healthy; WB_ESTATE before a solve), "k_zm" / "zm_zc" (the opt-in
  * z-march Poisson kernel), "mg_levels", "mg_N_<l>", "mg_lambda_<side>_<l>",
- * "mg_nonpos_<side>_<l>", "mg_vlambda_<l>" (the multigrid hierarchy of wb_setup_mg). */
+ * "mg_nonpos_<side>_<l>", "mg_vlambda_<l>", "mg_k_<l>" (the multigrid hierarchy of wb_setup_mg),
+ * "inner" (wBFBT's inner solve: 0 PCG, 1 Chebyshev), "prof_k_ms" / "prof_k_count" (option
+ * "profile"), "occ_k2" / "occ_a2" (resident CTAs per SM of the k = 2 Poisson / A kernels), and, in
+ * builds with -DWB_KPROF only, the phase-timer probes "kprof_<i>", "aprof_<i>", "ktl_<cta>_<i>". */
 wb_status wb_query(wb_ctx* ctx, const char* key, double* value);
 /* Method option (changes the results): "weights", the wBFBT weights the next
  * wb_set_viscosity lumps: 0 = w_l = w_r = sqrt(mu), eq:wbfbt, the default; 1 = the
@@ -301,7 +304,9 @@ wb_status wb_query(wb_ctx* ctx, const char* key, double* value);
  * B^T element kernel + node gather + B kernel), "k4_var" (its tile variant, 0..8; 1 =
  * 4 x 4 x 2 tiles with TMA staging, the default; DESIGN.md Sec. 7 lists the others),
  * "k4bt" (k = 3, 4 standalone B^T / B: 1 = B^T by the tile kernel, default; 2 = B too;
- * 0 = the element kernels), "k_zm" / "zm_var" / "zm_zc" (k = 2: the opt-in z-march Poisson
+ * 0 = the element kernels), "bbt_zc" (k = 2 standalone B / B^T: -1 = auto, the z-marching column
+ * kernels with 4 element layers per chunk on meshes with N >= 48, else the tile / box kernels,
+ * default; 0 = always the tile / box kernels; 2, 4, 8 = the column kernels with that chunk), "k_zm" / "zm_var" / "zm_zc" (k = 2: the opt-in z-march Poisson
  * kernel, its variant and z-chunk length), "tma" (k = 2: 1 = the TMA Poisson kernel where the
  * context's storage allows it, default), "k_variant" (k = 2 pointer Poisson kernel: 1 or 2 CTAs
  * per SM), "k_dbg" (timing probe bits that skip kernel phases: results invalid, tools only),

@@ -74,3 +74,22 @@ def test_create_without_gpu_fails_loudly(built):
     h = ctypes.c_void_p()
     st = lib().wb_create(ctypes.byref(h), 4, 2, 0, None)
     assert st != 0 and not h.value
+
+
+def test_every_option_and_query_key_is_documented():
+    """Every key wb_set_option accepts, and every key wb_query answers, is named in the
+    header's documentation (include/wbfbt.h), so the ABI description stays complete."""
+    import re
+    src = open(os.path.join(ROOT, "paper_1607_03936_b200", "csrc", "wbfbt.cu")).read()
+    hdr = open(os.path.join(ROOT, "include", "wbfbt.h")).read()
+    i, j = src.index("wb_status wb_set_option("), src.index("wb_status wb_sync(")
+    opts = re.findall(r'strcmp\(key, "([^"]+)"\)', src[i:j])
+    assert len(opts) >= 10
+    missing = [k for k in opts if f'"{k}"' not in hdr]
+    assert not missing, f"options not documented in include/wbfbt.h: {missing}"
+    i, j = src.index("wb_status wb_query("), src.index("wb_status wb_set_option(")
+    keys = re.findall(r'strcmp\(key, "([^"]+)"\)', src[i:j])
+    prefixes = re.findall(r'strncmp\(key, "([^"]+)"', src[i:j])
+    assert len(keys) >= 10
+    missing = [k for k in keys if f'"{k}"' not in hdr] + [p for p in prefixes if f'"{p}' not in hdr]
+    assert not missing, f"query keys not documented in include/wbfbt.h: {missing}"
