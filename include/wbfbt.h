@@ -297,7 +297,8 @@ wb_status wb_query(wb_ctx* ctx, const char* key, double* value);
  * Tuning knobs (results are identical up to rounding for every setting):
  * "kz" (k = 2 TMA Poisson kernel: 1 = the PCG update stores z = Minv r and the
  * kernel loads it as one box; 0 = it loads r and Minv, the default),
- * "k_ws" (k = 2 TMA Poisson kernel: 1 = warp-specialised, producer warps build
+ * "k2_pair" (k = 2 TMA Poisson kernel: 1 = each class-(0, *) pencil thread also computes the
+ * class-(1, *) pencil of the same (y, z) from its loads), "k_ws" (k = 2 TMA Poisson kernel: 1 = warp-specialised, producer warps build
  * the next tile's direction box while the consumer warps apply B^T X^-1 B),
  * "k4f" (k = 3, 4: 1 = the fused tile Poisson kernel of k4_fused.cuh, K_w = B X B^T by
  * assembled 1-D contractions with the PCG direction update folded in, default; 0 = the

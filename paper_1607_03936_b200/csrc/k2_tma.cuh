@@ -189,6 +189,100 @@ __device__ __forceinline__ void fkt_pencil(const double* __restrict__ Ps, double
       }
 }
 
+// Paired pencils (option "k2_pair"): the class-(0, RZ) pencil at (jy, jz) reads the element
+// rows qy = jy, jy + 1; the class-(1, RZ) pencil at the same (jy, jz) reads qy = jy + 1 only,
+// a subset.  One thread computes both from the same Ps loads (about 30 % fewer step-1 Ps reads
+// per tile), with two accumulator rows.  hasB: jy < TY (the class-(1, RZ) pencil exists).
+template <int TX, int TY, int TZ>
+__device__ __forceinline__ void fkt_row_out(double (&acc)[3][FK2<TX, TY, TZ>::MX], double* __restrict__ T,
+                                            const double* __restrict__ Xs, int ny, int nz, double sB) {
+  using F = FK2<TX, TY, TZ>;
+  using K = FKT<TX, TY, TZ>;
+  const double* Xr = Xs + K::row(ny, nz);
+#pragma unroll
+  for (int nx = 0; nx < F::MX; ++nx) {
+    const double f = sB * Xr[nx * K::NROW];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[c][nx] *= f;
+  }
+  double* Sr = T + K::row(ny, nz);
+#pragma unroll
+  for (int lx = 0; lx < TX; ++lx)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int m1 = 0; m1 < 2; ++m1) {
+        double sv = 0.0;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax)
+          if (x2_nz(c, ax, m1)) sv = fma(c_X2[c][ax][m1], acc[c][2 * lx + ax], sv);
+        Sr[K::sidx(c, m1, lx)] = sv;
+      }
+}
+template <int TX, int TY, int TZ, int RZ>
+__device__ __forceinline__ void fkt_pencil2(const double* __restrict__ Ps, double* __restrict__ T,
+                                            const double* __restrict__ Xs, int jy, int jz, double sB, bool hasB) {
+  using F = FK2<TX, TY, TZ>;
+  using K = FKT<TX, TY, TZ>;
+  const int nz = 2 * jz + RZ;
+  double accA[3][F::MX], accB[3][F::MX];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int nx = 0; nx < F::MX; ++nx) accA[c][nx] = accB[c][nx] = 0.0;
+#pragma unroll
+  for (int qx = 0; qx < K::HX; ++qx) {
+    double WA[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}}, WB[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int iz = 0; iz < (RZ ? 1 : 2); ++iz) {
+      const int qz = RZ ? jz + 1 : jz + iz;
+      const int az = RZ ? 1 : (iz == 0 ? 2 : 0);
+#pragma unroll
+      for (int iy = 0; iy < 2; ++iy) {
+        const int qy = jy + iy;
+        const int ay = iy == 0 ? 2 : 0;
+        const int h = K::pidx(qx, qy, qz);
+        const double p000 = Ps[h], p100 = Ps[K::NHP + h], p010 = Ps[2 * K::NHP + h], p001 = Ps[3 * K::NHP + h];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (w2_nz(c, ay, az, 0)) {
+            WA[c][0] = fma(c_W2[c][ay][az][0], p000, WA[c][0]);
+            WA[c][1] = fma(c_W2[c][ay][az][0], p100, WA[c][1]);
+          }
+          if (w2_nz(c, ay, az, 1)) WA[c][0] = fma(c_W2[c][ay][az][1], p010, WA[c][0]);
+          if (w2_nz(c, ay, az, 2)) WA[c][0] = fma(c_W2[c][ay][az][2], p001, WA[c][0]);
+          if (iy == 1) {  // the class-(1, RZ) pencil: local y node 1 of element qy = jy + 1
+            if (w2_nz(c, 1, az, 0)) {
+              WB[c][0] = fma(c_W2[c][1][az][0], p000, WB[c][0]);
+              WB[c][1] = fma(c_W2[c][1][az][0], p100, WB[c][1]);
+            }
+            if (w2_nz(c, 1, az, 1)) WB[c][0] = fma(c_W2[c][1][az][1], p010, WB[c][0]);
+            if (w2_nz(c, 1, az, 2)) WB[c][0] = fma(c_W2[c][1][az][2], p001, WB[c][0]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const int nx = 2 * qx - 2 + ax;
+      if (nx < 0 || nx >= F::MX) continue;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (x2_nz(c, ax, 0)) {
+          accA[c][nx] = fma(c_X2[c][ax][0], WA[c][0], accA[c][nx]);
+          accB[c][nx] = fma(c_X2[c][ax][0], WB[c][0], accB[c][nx]);
+        }
+        if (x2_nz(c, ax, 1)) {
+          accA[c][nx] = fma(c_X2[c][ax][1], WA[c][1], accA[c][nx]);
+          accB[c][nx] = fma(c_X2[c][ax][1], WB[c][1], accB[c][nx]);
+        }
+      }
+    }
+  }
+  fkt_row_out<TX, TY, TZ>(accA, T, Xs, 2 * jy, nz, sB);
+  if (hasB) fkt_row_out<TX, TY, TZ>(accB, T, Xs, 2 * jy + 1, nz, sB);
+}
+
 // step 1 of the warp-specialised kernel: one pencil per consumer thread.  Not inlined, so
 // the pencils get the registers to themselves (inlined into the tile loop, the loop state
 // of step 2 is kept live across them and they spill under the 15-warp register cap).
@@ -258,7 +352,7 @@ __device__ __noinline__ double fkt_step2(const double* __restrict__ Pc, const do
 // loads: tm_pold / tm_r / tm_minv over [m][ez][ey][ex]; X from its tile-blocked pencil layout XT.
 // ZB: the PCG update kernels store z = Minv r and the kernel loads a z box; else it
 // loads r and Minv boxes and forms Minv r itself (same product either way).
-template <int TX, int TY, int TZ, int MINB, bool ZB>
+template <int TX, int TY, int TZ, int MINB, bool ZB, bool PAIR = false>
 __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     k_K2_tma(const __grid_constant__ CUtensorMap tm_pold, const __grid_constant__ CUtensorMap tm_z,
              const __grid_constant__ CUtensorMap tm_minv, const double* __restrict__ XT,
@@ -369,7 +463,17 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     // 1. t at the tile nodes by x-pencils
     mbar_wait(&bar[2], ph);
     lap(3);
-    if (!(dbg & 0x100)) {
+    if (PAIR && !(dbg & 0x100)) {
+      // paired pencils: threads [0, (TY+1)(TZ+1)) the class-(0,0) + (1,0) pairs, then, from
+      // the next warp boundary, the class-(0,1) + (1,1) pairs
+      const int t = threadIdx.x;
+      constexpr int P0 = (TY + 1) * (TZ + 1), O1 = (P0 + 31) / 32 * 32, P1 = (TY + 1) * TZ;
+      if (t < P0) fkt_pencil2<TX, TY, TZ, 0>(Ps, T, Xs, t % (TY + 1), t / (TY + 1), sB, t % (TY + 1) < TY);
+      else if (t >= O1 && t < O1 + P1) {
+        const int i = t - O1;
+        fkt_pencil2<TX, TY, TZ, 1>(Ps, T, Xs, i % (TY + 1), i / (TY + 1), sB, i % (TY + 1) < TY);
+      }
+    } else if (!(dbg & 0x100)) {
       const int t = threadIdx.x;
       if (t < F::OFF1) {
         if (t < F::cls_n(0, 0)) fkt_pencil<TX, TY, TZ, 0, 0>(Ps, T, Xs, t % (TY + 1), t / (TY + 1), sB);

@@ -97,6 +97,7 @@ struct wb_ctx {
   bool tma_ok = false;
   int use_tma = 1;
   int k_ws = 0;  // 1: the TMA Poisson operator runs warp-specialised (k_K2_ws)
+  int k2_pair = 0;  // 1: the TMA Poisson kernel computes the class-(1, *) pencils with their class-(0, *) partners
   double *XpL = nullptr, *XpR = nullptr;  // C_w^-1, D_w^-1 in the TMA kernel's X-block layout (k_x_tiles)
   // k = 2, even N: MinvL | XpL | x r p p' q z | MinvR | XpR carved from one slab (each
   // side's PCG working set contiguous; a persisting L2 access-policy window over it was
@@ -525,8 +526,10 @@ wb_status run_k2f(wb_ctx* c, const double* pold, double* pnew, const double* r, 
       const int grid = std::max(1, std::min(nt, TMA_MINB * c->nsm));  // persistent, all resident
       using KW = FKW<TMA_TX, TMA_TY, TMA_TZ>;
       auto kern = c->k_ws ? (c->kz ? k_K2_ws<TMA_TX, TMA_TY, TMA_TZ, true> : k_K2_ws<TMA_TX, TMA_TY, TMA_TZ, false>)
-                          : (c->kz ? k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, true>
-                                   : k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, false>);
+                  : c->k2_pair ? (c->kz ? k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, true, true>
+                                        : k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, false, true>)
+                               : (c->kz ? k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, true>
+                                        : k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, false>);
       const int nth = c->k_ws ? KW::NTH : FK2<TMA_TX, TMA_TY, TMA_TZ>::NTH;
       const size_t smem = c->k_ws ? KW::SMEM : KT::SMEM;
       kern<<<grid, nth, smem, c->stream>>>(
@@ -609,6 +612,10 @@ bool setup_tma(wb_ctx* c) {
   if (cudaFuncSetAttribute(k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FKT<TMA_TX, TMA_TY, TMA_TZ>::SMEM) != cudaSuccess ||
       cudaFuncSetAttribute(k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FKT<TMA_TX, TMA_TY, TMA_TZ>::SMEM) != cudaSuccess ||
+      cudaFuncSetAttribute(k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, true, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FKT<TMA_TX, TMA_TY, TMA_TZ>::SMEM) != cudaSuccess ||
+      cudaFuncSetAttribute(k_K2_tma<TMA_TX, TMA_TY, TMA_TZ, TMA_MINB, false, true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FKT<TMA_TX, TMA_TY, TMA_TZ>::SMEM) != cudaSuccess ||
       cudaFuncSetAttribute(k_K2_ws<TMA_TX, TMA_TY, TMA_TZ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)FKW<TMA_TX, TMA_TY, TMA_TZ>::SMEM) != cudaSuccess ||
@@ -2645,6 +2652,10 @@ wb_status wb_set_option(wb_ctx* c, const char* key, double value) {
     if (!(value >= 0.0 && value < K4_NV) || value != (double)(int)value)
       return set_err(c, WB_EINVAL, "k4_var must be an integer in [0, %d)", K4_NV);
     c->k4_var = (int)value;
+    clear_graphs(c);
+  } else if (!strcmp(key, "k2_pair")) {  // TMA Poisson kernel: paired class-(0,*) / (1,*) pencils
+    if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k2_pair must be 0 or 1");
+    c->k2_pair = (int)value;
     clear_graphs(c);
   } else if (!strcmp(key, "k_ws")) {
     if (value != 0.0 && value != 1.0) return set_err(c, WB_EINVAL, "k_ws must be 0 or 1");

@@ -46,3 +46,16 @@ def test_zc_in_wbfbt(pair):
         ctx.set_option("bbt_zc", -1)
     tol = 1e-9 if (pair.ost["n_nonpos_Cw"] or pair.ost["n_nonpos_Dw"]) else 1e-12
     assert rel_l2(z1, z0) <= tol
+
+
+def test_k2_pair_bitwise():
+    """Option k2_pair (the TMA Poisson kernel with paired class-(0,*) / (1,*) pencils, same
+    per-row arithmetic): PCG results bitwise equal to the default kernel, on a ragged mesh."""
+    pr = Pair("C2", 10)
+    b = dev(pr.inp["p"])
+    x0 = host(pr.ctx.poisson_pcg(1, b, empty(pr.ctx.n_p), 12))
+    pr.ctx.set_option("k2_pair", 1)
+    x1 = host(pr.ctx.poisson_pcg(1, b, empty(pr.ctx.n_p), 12))
+    pr.ctx.set_option("k2_pair", 0)
+    assert np.array_equal(x0, x1)
+    assert rel_l2(x1, pr.o.poisson(pr.ost["Dinv"], pr.ost["diagKr"], pr.inp["p"], 12)) <= 1e-12
