@@ -44,6 +44,8 @@ def lib():
             L = C.CDLL(_LIB)
             L.or_create.restype = C.c_void_p
             L.or_create.argtypes = [C.c_int, C.c_int]
+            L.or_create_box.restype = C.c_void_p
+            L.or_create_box.argtypes = [C.c_int, C.c_int, C.c_int]
             L.or_destroy.argtypes = [C.c_void_p]
             L.or_sizes.argtypes = [C.c_void_p, _I64]
             L.or_tables.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, _D, C.POINTER(C.c_int)]
@@ -133,14 +135,16 @@ def sizes_only(N: int, k: int) -> dict:
 
 
 class Oracle:
-    """One structured mesh (N^3 elements, Q_k x P_{k-1}^disc) on the unit cube."""
+    """One structured mesh (N^3 elements, Q_k x P_{k-1}^disc) on the unit cube; with Nz given,
+    the box of N x N x Nz elements of side 1/N (z-stacked cubes: the global mesh of the slab
+    decomposition; reading R24)."""
 
-    def __init__(self, N: int, k: int):
+    def __init__(self, N: int, k: int, Nz: int | None = None):
         self.L = lib()
-        self.h = self.L.or_create(N, k)
+        self.h = self.L.or_create(N, k) if Nz is None else self.L.or_create_box(N, Nz, k)
         if not self.h:
-            raise ValueError(f"oracle: bad N={N} k={k}")
-        self.N, self.k = N, k
+            raise ValueError(f"oracle: bad N={N} k={k} Nz={Nz}")
+        self.N, self.k, self.Nz = N, k, (N if Nz is None else Nz)
         s = np.zeros(6, dtype=np.int64)
         self.L.or_sizes(self.h, s.ctypes.data_as(_I64))
         self.n_el, self.n_nodes, self.n_v, self.n_p, self.n_q, self.n_m = (int(v) for v in s)

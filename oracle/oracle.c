@@ -45,7 +45,7 @@
 #define OR_MAXN1 9 /* up to k = 8 */
 
 typedef struct {
-  int N, k, n1, nq, nm;
+  int N, Nz, k, n1, nq, nm;      /* N x N x Nz elements of side h = 1/N (Nz = N: the unit cube) */
   int64_t n_el, n_nodes, n_v, n_p;
   double h, detJ;                  /* h = 1/N, detJ = (h/2)^3 */
   double xn[OR_MAXN1];             /* GLL nodes (R1) */
@@ -141,13 +141,17 @@ static long double dlagrange(const double* xn, int n1, int a, long double t) {
 /* ---------------------------------------------------------------- context */
 static int or_nmodes(int k) { return k * (k + 1) * (k + 2) / 6; } /* C(k+2,3) = dim P_{k-1} in 3-D */
 
-or_ctx* or_create(int N, int k) {
-  if (N < 1 || k < 1 || k + 1 > OR_MAXN1) return NULL;
+/* Box mesh: N x N x Nz cubic elements of side h = 1/N on [0,1]^2 x [0, Nz/N].  Nz = N is the
+ * paper's unit cube; Nz != N is the union of z-stacked cubes that the
+ * element-partition domain decomposition of PAPER.md:2480-2487 distributes (SURVEY 8(e),
+ * DESIGN.md reading R24).  Every formula below is per element and does not see Nz. */
+or_ctx* or_create_box(int N, int Nz, int k) {
+  if (N < 1 || Nz < 1 || k < 1 || k + 1 > OR_MAXN1) return NULL;
   or_ctx* c = (or_ctx*)calloc(1, sizeof(or_ctx));
-  c->N = N; c->k = k; c->n1 = k + 1; c->nq = c->n1 * c->n1 * c->n1; c->nm = or_nmodes(k);
-  c->n_el = (int64_t)N * N * N;
+  c->N = N; c->Nz = Nz; c->k = k; c->n1 = k + 1; c->nq = c->n1 * c->n1 * c->n1; c->nm = or_nmodes(k);
+  c->n_el = (int64_t)N * N * Nz;
   int64_t nn1 = (int64_t)k * N + 1;
-  c->n_nodes = nn1 * nn1 * nn1; c->n_v = 3 * c->n_nodes; c->n_p = c->nm * c->n_el;
+  c->n_nodes = nn1 * nn1 * ((int64_t)k * Nz + 1); c->n_v = 3 * c->n_nodes; c->n_p = c->nm * c->n_el;
   c->h = 1.0 / N;
   c->detJ = (c->h / 2) * (c->h / 2) * (c->h / 2);
   gll_nodes(k, c->xn);
@@ -207,6 +211,8 @@ or_ctx* or_create(int N, int k) {
   return c;
 }
 
+or_ctx* or_create(int N, int k) { return or_create_box(N, N, k); }
+
 void or_destroy(or_ctx* c) {
   if (!c) return;
   free(c->gphi); free(c->vphi); free(c->wq); free(c->Be); free(c->work); free(c);
@@ -246,12 +252,12 @@ static int64_t or_node(const or_ctx* c, int64_t e, int a) {
 static int or_node_is_boundary(const or_ctx* c, int64_t g) {
   int64_t nn1 = (int64_t)c->k * c->N + 1;
   int64_t gx = g % nn1, gy = (g / nn1) % nn1, gz = g / (nn1 * nn1);
-  return gx == 0 || gy == 0 || gz == 0 || gx == nn1 - 1 || gy == nn1 - 1 || gz == nn1 - 1;
+  return gx == 0 || gy == 0 || gz == 0 || gx == nn1 - 1 || gy == nn1 - 1 || gz == (int64_t)c->k * c->Nz;
 }
 /* element touches the boundary iff any index is 0 or N-1 (eq:bdramp set D) */
 static int or_elem_on_boundary(const or_ctx* c, int64_t e) {
   int64_t N = c->N, ex = e % N, ey = (e / N) % N, ez = e / (N * N);
-  return ex == 0 || ey == 0 || ez == 0 || ex == N - 1 || ey == N - 1 || ez == N - 1;
+  return ex == 0 || ey == 0 || ez == 0 || ex == N - 1 || ey == N - 1 || ez == c->Nz - 1;
 }
 
 void or_boundary_elements(const or_ctx* c, uint8_t* flag) {
@@ -367,7 +373,7 @@ void or_apply_A_sampled(or_ctx* c, const double* mu_q, const double* u, const in
     if (!or_node_is_boundary(c, g)) {
       int64_t gx = g % nn1, gy = (g / nn1) % nn1, gz = g / (nn1 * nn1);
       /* elements containing node g, in increasing element index */
-      for (int64_t ez = 0; ez < N; ++ez) { int64_t az = gz - k * ez; if (az < 0 || az > k) continue;
+      for (int64_t ez = 0; ez < c->Nz; ++ez) { int64_t az = gz - k * ez; if (az < 0 || az > k) continue;
         for (int64_t ey = 0; ey < N; ++ey) { int64_t ay = gy - k * ey; if (ay < 0 || ay > k) continue;
           for (int64_t ex = 0; ex < N; ++ex) { int64_t ax = gx - k * ex; if (ax < 0 || ax > k) continue;
             int64_t e = ex + N * (ey + N * ez);
