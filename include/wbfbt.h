@@ -261,6 +261,57 @@ wb_status wb_hotpath_host(wb_ctx* ctx, const double* mu_q, double a_l, double a_
                           const double* u, const double* p, int iters, double* yA, double* pB,
                           double* yBT, double* z);
 
+/* ---- z-slab domain decomposition (the element-partition domain
+ * decomposition of PAPER.md:2480-2487; reading R24).  One context per rank (one process per
+ * GPU).  Rank r of R owns the r-th of R cubes of N^3 elements stacked along z: the global mesh
+ * has N x N x (R N) elements of side h = 1/N on [0,1]^2 x [0,R] (global element
+ * e = ex + N (ey + N (r N + ez))), and neighbouring ranks share (replicate) the node plane
+ * between them.  Every vector argument of the calls below is the rank's LOCAL part in the cube
+ * layouts of this header: velocity vectors carry both shared planes, and a velocity OUTPUT
+ * holds the full (summed) value on them, identical bit for bit on both owners; pressure vectors
+ * are element-local and never shared.  The Dirichlet boundary is the GLOBAL box boundary: the
+ * shared planes are interior except on their x / y rim, and the boundary amplification a_l, a_r
+ * (eq:bdramp) applies to elements on the global boundary only.
+ *
+ * On a slab context the calls wb_set_viscosity, wb_apply_A, wb_apply_B, wb_apply_BT,
+ * wb_apply_K, wb_poisson_pcg, wb_apply_wbfbt, wb_get_lumped, wb_get_jacobi,
+ * wb_get_boundary_mask (the global mask), wb_sizes, wb_sync and wb_query compute the GLOBAL
+ * operators; each must be entered by all R ranks together (they are collective).  Per
+ * operator apply there is one exchange: the partial nodal sums on the shared planes
+ * (3 (kN+1)^2 doubles per plane; C_w, D_w once per wb_set_viscosity), and every inner product,
+ * the projection mean and max|diag K| is one all-reduce of 1 double.  K_w runs unfused
+ * (B^T, plane sum, B) and the PCG is the O9 recurrence with device scalars; the single-GPU
+ * fused kernels and CUDA graphs are not used.  Every other call returns WB_ESTATE.
+ *
+ * Communication is the caller's (torch.distributed over NCCL in the Python binding): the two
+ * callbacks act on buffers the caller owns and registers here.
+ *   send_lo, recv_lo, send_hi, recv_hi: device, `cap` doubles each, cap >= 3 (kN+1)^2;
+ *   scal: device, >= 8 doubles.
+ *   exchange(user, n): send send_lo[0..n) to rank-1 and send_hi[0..n) to rank+1; receive
+ *     rank-1's send_hi into recv_lo and rank+1's send_lo into recv_hi (rank 0 has no lower,
+ *     rank R-1 no upper neighbour: skip those).  The library has enqueued the packing on the
+ *     context's stream before the call and enqueues the unpacking after it, so the transfer
+ *     must be ordered on that stream (NCCL on the same stream) or be complete on return after
+ *     synchronising it.
+ *   allreduce(user, offset, n, op): reduce scal[offset..offset+n) over all ranks in place, the
+ *     same bits on every rank; op 0 = sum, 1 = max.  Same stream rule.
+ *   Both return 0 on success; anything else aborts the call with WB_ECUDA.
+ * wb_slab_create: rank in [0, nranks), nranks >= 1 (nranks = 1 is the plain cube through the
+ * slab code path), other arguments as wb_create; WB_DEBUG_NOMASK is refused.  Errors as
+ * wb_create. */
+typedef struct wb_slab_comm {
+  void* user;
+  int (*exchange)(void* user, int64_t n);
+  int (*allreduce)(void* user, int offset, int n, int op);
+  double *send_lo, *recv_lo, *send_hi, *recv_hi;
+  int64_t cap;
+  double* scal;
+} wb_slab_comm;
+wb_status wb_slab_create(wb_ctx** out, int N, int k, int rank, int nranks, unsigned flags, void* stream);
+/* Registers the communicator (copied).  WB_EINVAL for a null callback / buffer or cap too small,
+ * WB_ESTATE on a context that is not a slab context. */
+wb_status wb_slab_set_comm(wb_ctx* ctx, const wb_slab_comm* comm);
+
 /* One PCG iteration (DESIGN.md Sec. 4 recurrence) from a supplied state, in
  * place: x, r, p device n_p; *rz host in/out.  Test entry for one-step
  * parity. */

@@ -9,5 +9,7 @@ fallback: importing without the built library raises.
 from ._abi import (WBError, Context, lib, library_path, version, sizes,  # noqa: F401
                    WB_STRICT_LUMP, WB_DEBUG_NOMASK, WB_DEBUG_SCALARS, SYMBOLS)
 
-__all__ = ["WBError", "Context", "lib", "library_path", "version", "sizes", "WB_STRICT_LUMP",
+from .slab import SlabContext, SlabComm, DistComm, ThreadComm  # noqa: F401,E402
+
+__all__ = ["SlabContext", "SlabComm", "DistComm", "ThreadComm", "WBError", "Context", "lib", "library_path", "version", "sizes", "WB_STRICT_LUMP",
            "WB_DEBUG_NOMASK", "WB_DEBUG_SCALARS", "SYMBOLS"]

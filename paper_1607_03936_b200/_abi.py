@@ -62,6 +62,8 @@ SYMBOLS = [
     ("wb_apply_wbfbt", _i, [_vp, _vp, _vp, _i]),
     ("wb_hotpath", _i, [_vp, _vp, _d, _d, _vp, _vp, _i, _vp, _vp, _vp, _vp]),
     ("wb_hotpath_host", _i, [_vp, _vp, _d, _d, _vp, _vp, _i, _vp, _vp, _vp, _vp]),
+    ("wb_slab_create", _i, [C.POINTER(_vp), _i, _i, _i, _i, _u, _vp]),
+    ("wb_slab_set_comm", _i, [_vp, _vp]),
     ("wb_debug_pcg_step", _i, [_vp, _i, _vp, _vp, _vp, C.POINTER(_d)]),
     ("wb_get_lumped", _i, [_vp, _vp, _vp, _vp, _vp]),
     ("wb_get_jacobi", _i, [_vp, _vp, _vp]),

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(128) k_setup_mu2(const double* __restrict__ mu
 // class as k_BT_node2: block (64, 4), grid (ceil((N+1)/64), ceil(nn1/4), 2 nn1).
 template <int RX, int RY, int RZ>
 __device__ __forceinline__ void lump2_node(const double* __restrict__ L, int64_t ne, int N, int gx, int gy, int gz,
-                                           double a_l, double a_r, double& cl, double& cr) {
+                                           double a_l, double a_r, double& cl, double& cr, int zopen) {
 #pragma unroll
   for (int iz = 0; iz < (RZ ? 1 : 2); ++iz) {
     const int ez = RZ ? (gz >> 1) : ((gz >> 1) - 1 + iz), az = RZ ? 1 : (iz == 0 ? 2 : 0);
@@ -87,7 +87,8 @@ __device__ __forceinline__ void lump2_node(const double* __restrict__ L, int64_t
         const int ex = RX ? (gx >> 1) : ((gx >> 1) - 1 + ix), ax = RX ? 1 : (ix == 0 ? 2 : 0);
         if (ex < 0 || ex >= N) continue;
         const int64_t e = ex + (int64_t)N * (ey + (int64_t)N * ez);
-        const bool onb = ex == 0 || ey == 0 || ez == 0 || ex == N - 1 || ey == N - 1 || ez == N - 1;
+        const bool onb = ex == 0 || ey == 0 || (ez == 0 && !(zopen & 1)) || ex == N - 1 || ey == N - 1 ||
+                         (ez == N - 1 && !(zopen & 2));
         const double l = __ldg(L + (int64_t)(ax + 3 * (ay + 3 * az)) * ne + e);
         cl += (onb ? a_l : 1.0) * l;
         cr += (onb ? a_r : 1.0) * l;
@@ -107,14 +108,14 @@ __global__ void __launch_bounds__(256) k_lump_node2(const double* __restrict__ L
   double cl = 0.0, cr = 0.0;
   const int cls = rx | ((gy & 1) << 1) | ((gz & 1) << 2);  // warp-uniform
   switch (cls) {
-    case 0: lump2_node<0, 0, 0>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr); break;
-    case 1: lump2_node<1, 0, 0>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr); break;
-    case 2: lump2_node<0, 1, 0>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr); break;
-    case 3: lump2_node<1, 1, 0>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr); break;
-    case 4: lump2_node<0, 0, 1>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr); break;
-    case 5: lump2_node<1, 0, 1>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr); break;
-    case 6: lump2_node<0, 1, 1>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr); break;
-    default: lump2_node<1, 1, 1>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr); break;
+    case 0: lump2_node<0, 0, 0>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr, G.zopen); break;
+    case 1: lump2_node<1, 0, 0>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr, G.zopen); break;
+    case 2: lump2_node<0, 1, 0>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr, G.zopen); break;
+    case 3: lump2_node<1, 1, 0>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr, G.zopen); break;
+    case 4: lump2_node<0, 0, 1>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr, G.zopen); break;
+    case 5: lump2_node<1, 0, 1>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr, G.zopen); break;
+    case 6: lump2_node<0, 1, 1>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr, G.zopen); break;
+    default: lump2_node<1, 1, 1>(L, G.n_el, G.N, gx, gy, gz, a_l, a_r, cl, cr, G.zopen); break;
   }
   const int64_t g = node_id(gx, gy, gz, nn1);
   const bool b = node_bnd(gx, gy, gz, nn1);

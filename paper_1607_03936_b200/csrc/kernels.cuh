@@ -17,6 +17,9 @@ __constant__ Tab c_tab[3];  // k = 2, 3, 4
 struct Geo {
   int N, k, nn1;     // nn1 = kN + 1 nodes per axis
   int64_t n_el, n_nodes, n_p;
+  // slab contexts (slab_dd.cuh): bit 0 / 1 = the z-lo / z-hi face is shared with a neighbouring
+  // rank, i.e. not part of the global boundary (read by the lumping kernels' a_l / a_r test only)
+  int zopen = 0;
 };
 
 // Storage of the mode-major PCG vectors (x, r, p, q, z, Minv): entry (m, e) of element
@@ -861,7 +864,8 @@ __global__ void k_lump_node(const double* __restrict__ L, double a_l, double a_r
         const int ex = pe[0][ix], ey = pe[1][iy], ez = pe[2][iz];
         const int64_t e = ex + (int64_t)G.N * (ey + (int64_t)G.N * ez);
         const int a = pa[0][ix] + n1 * (pa[1][iy] + n1 * pa[2][iz]);
-        const bool onb = ex == 0 || ey == 0 || ez == 0 || ex == G.N - 1 || ey == G.N - 1 || ez == G.N - 1;
+        const bool onb = ex == 0 || ey == 0 || (ez == 0 && !(G.zopen & 1)) || ex == G.N - 1 || ey == G.N - 1 ||
+                         (ez == G.N - 1 && !(G.zopen & 2));
         const double l = L[(int64_t)a * G.n_el + e];
         cl += (onb ? a_l : 1.0) * l;
         cr += (onb ? a_r : 1.0) * l;

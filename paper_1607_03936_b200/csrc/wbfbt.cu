@@ -16,6 +16,7 @@
 
 #include "../../include/wbfbt.h"
 #include "kernels_k2.cuh"
+#include "slab_dd.cuh"
 
 using namespace wb;
 
@@ -134,6 +135,7 @@ struct wb_ctx {
   bool prof_cap = false;  // profiling inside a stream capture: event-record graph nodes
   std::vector<cudaGraphExec_t> prof_execs;  // the profiled loops' graphs
   long long launches = 0;
+  struct DD* dd = nullptr;  // z-slab domain decomposition state (slab contexts only; wb_slab_create)
   struct MGH* mg = nullptr;  // pressure multigrid hierarchy (R20), built by wb_setup_mg
   // Schur-complement variant of the Stokes preconditioner: 0 = wBFBT,
   // 1 = diag(A)-BFBT, 2 = M_p(1/mu)^-1 element blocks (R21, built in
@@ -166,6 +168,19 @@ struct MGH {
   double vlam[16] = {};
   double *vin = nullptr, *vout = nullptr;  // fixed in/out of the captured velocity cycles
   int vcycles = 0;  // Stokes At^-1 by this many V-cycles (0: the Chebyshev smoother, R18)
+};
+// z-slab domain decomposition: this rank's place in the z-stack, the
+// caller's communicator, the global Dirichlet mask and the element-major PCG vectors
+struct DD {
+  int rank = 0, nranks = 1;
+  bool have_comm = false;
+  wb_slab_comm comm{};
+  double* own_scal = nullptr;  // nranks = 1 without a communicator: local scalar slots
+  double* gm = nullptr;        // n_nodes: 0 on the global boundary, else 1
+  double* vs = nullptr;        // n_v scratch (masked input of A, nodal B^T p of K_w)
+  double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr, *x = nullptr, *y = nullptr;  // n_p
+  double* mK[2] = {nullptr, nullptr};  // pinv(diag K_side), element-major
+  double* scal() const { return have_comm ? comm.scal : own_scal; }
 };
 void mg_free(wb_ctx* c);
 wb_status run_mgcg(wb_ctx* c, int side, const double* b, double* x, int iters);
@@ -1418,14 +1433,188 @@ wb_status run_stokes(wb_ctx* c, const double* f, const double* g, double* u, dou
   return WB_OK;
 }
 
-wb_status check_ctx(wb_ctx* c, bool need_visc) {
+// ================================================================ z-slab domain decomposition
+// (R24).  The global operators from the cube
+// kernels: unmasked local applies, one sum of the shared planes' partials, the global mask.
+enum { DS_RZ = 0, DS_PQ = 1, DS_RZ1 = 2, DS_STOP = 3, DS_MEAN = 4, DS_MAX = 5 };
+
+wb_status dd_allreduce(wb_ctx* c, int offset, int n, int op) {
+  DD* d = c->dd;
+  if (d->nranks == 1) return WB_OK;
+  if (d->comm.allreduce(d->comm.user, offset, n, op) != 0)
+    return set_err(c, WB_ECUDA, "slab communicator: allreduce failed");
+  return WB_OK;
+}
+// sum the shared z planes of nf nodal fields (n_nodes each) with the neighbours' partials
+wb_status dd_plane_sum(wb_ctx* c, double* const* f, int nf) {
+  DD* d = c->dd;
+  if (d->nranks == 1) return WB_OK;
+  const int64_t np = (int64_t)c->G.nn1 * c->G.nn1, n = np * nf;
+  if (n > d->comm.cap) return set_err(c, WB_EINVAL, "slab exchange buffers too small");
+  const int zo = c->G.zopen;
+  for (int i = 0; i < nf; ++i) {
+    if (zo & 1)
+      CUDA_TRY(c, cudaMemcpyAsync(d->comm.send_lo + i * np, f[i], sizeof(double) * np, cudaMemcpyDeviceToDevice,
+                                  c->stream));
+    if (zo & 2)
+      CUDA_TRY(c, cudaMemcpyAsync(d->comm.send_hi + i * np, f[i] + c->n_nodes - np, sizeof(double) * np,
+                                  cudaMemcpyDeviceToDevice, c->stream));
+  }
+  if (d->comm.exchange(d->comm.user, n) != 0) return set_err(c, WB_ECUDA, "slab communicator: exchange failed");
+  for (int i = 0; i < nf; ++i) {
+    if (zo & 1) {
+      k_dd_add<<<stream_blocks(np), VBS, 0, c->stream>>>(f[i], d->comm.recv_lo + i * np, np);
+      LAUNCH_CHECK(c);
+    }
+    if (zo & 2) {
+      k_dd_add<<<stream_blocks(np), VBS, 0, c->stream>>>(f[i] + c->n_nodes - np, d->comm.recv_hi + i * np, np);
+      LAUNCH_CHECK(c);
+    }
+  }
+  return WB_OK;
+}
+wb_status dd_plane_sum3(wb_ctx* c, double* v) {
+  double* f[3] = {v, v + c->n_nodes, v + 2 * c->n_nodes};
+  return dd_plane_sum(c, f, 3);
+}
+// row a3 on a slab: plane-sum C_w, D_w, then the inverses under the global mask
+wb_status dd_finish_lump(wb_ctx* c) {
+  double* f[2] = {c->Cw, c->Dw};
+  wb_status s = dd_plane_sum(c, f, 2);
+  if (s) return s;
+  CUDA_TRY(c, cudaMemsetAsync(c->icount + 1, 0, sizeof(unsigned long long) * 2, c->stream));
+  k_dd_inv<<<stream_blocks(c->n_nodes), VBS, 0, c->stream>>>(c->Cw, c->Dw, c->dd->gm, c->Cinv, c->Dinv,
+                                                              c->icount + 1, c->n_nodes);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+// max|diag K_side| over all ranks (the R11 threshold is global), then this rank's element-major Minv
+wb_status dd_after_dmax(wb_ctx* c, int side, const double* diag, double* dmax) {
+  DD* d = c->dd;
+  double* sc = d->scal();
+  CUDA_TRY(c, cudaMemcpyAsync(sc + DS_MAX, dmax, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  wb_status s = dd_allreduce(c, DS_MAX, 1, 1);
+  if (s) return s;
+  CUDA_TRY(c, cudaMemcpyAsync(dmax, sc + DS_MAX, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  k_pinv_diag<<<stream_blocks(c->n_p), VBS, 0, c->stream>>>(diag, d->mK[side], c->n_p, dmax);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+// y = M A M u (global): mask the input, unmasked cube apply, plane sum, mask
+wb_status dd_A(wb_ctx* c, const double* u, double* y, bool u_masked) {
+  DD* d = c->dd;
+  const double* in = u;
+  if (!u_masked) {
+    k_dd_scale3<<<stream_blocks(c->n_nodes), VBS, 0, c->stream>>>(d->vs, u, d->gm, c->n_nodes);
+    LAUNCH_CHECK(c);
+    in = d->vs;
+  }
+  wb_status s = run_A(c, in, y, 1);
+  if (s) return s;
+  if ((s = dd_plane_sum3(c, y))) return s;
+  k_dd_scale3<<<stream_blocks(c->n_nodes), VBS, 0, c->stream>>>(y, y, d->gm, c->n_nodes);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+// p = B (xs o u), xs a nodal scaling that carries the global mask (default: the mask itself)
+wb_status dd_B(wb_ctx* c, const double* u, const double* xs, double* p) {
+  return run_B(c, u, xs ? xs : c->dd->gm, p, 0, nullptr, nullptr, nullptr, c->nm, 1);
+}
+// y = xs o (B^T p) (global), xs as above
+wb_status dd_BT(wb_ctx* c, const double* p, const double* xs, double* y) {
+  wb_status s = run_BT(c, p, nullptr, y, 1, nullptr, c->nm, 1);
+  if (s) return s;
+  if ((s = dd_plane_sum3(c, y))) return s;
+  k_dd_scale3<<<stream_blocks(c->n_nodes), VBS, 0, c->stream>>>(y, y, xs ? xs : c->dd->gm, c->n_nodes);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+// q = B (X o B^T p) (global, O6), X = C_w^-1 or D_w^-1 with the global mask
+wb_status dd_K(wb_ctx* c, int side, const double* p, double* q) {
+  DD* d = c->dd;
+  wb_status s = run_BT(c, p, nullptr, d->vs, 1, nullptr, c->nm, 1);
+  if (s) return s;
+  if ((s = dd_plane_sum3(c, d->vs))) return s;
+  return run_B(c, d->vs, side == 0 ? c->Cinv : c->Dinv, q, 0, nullptr, nullptr, nullptr, c->nm, 1);
+}
+// global <a, b> into scalar slot `slot`: this rank's fixed-order sum, then one all-reduce
+wb_status dd_dot(wb_ctx* c, const double* a, const double* b, int slot) {
+  wb_status s = dev_dot(c, a, b, c->n_p, c->dd->scal() + slot);
+  if (s) return s;
+  return dd_allreduce(c, slot, 1, 0);
+}
+// R10 on the local part of an element-major vector (global mean)
+wb_status dd_project(wb_ctx* c, double* v) {
+  DD* d = c->dd;
+  k_mode0_sum<<<c->red_blocks, VBS, 0, c->stream>>>(v, c->n_el, c->nm, c->partial, c->counter, d->scal() + DS_MEAN);
+  LAUNCH_CHECK(c);
+  wb_status s = dd_allreduce(c, DS_MEAN, 1, 0);
+  if (s) return s;
+  k_dd_sub_mean<<<stream_blocks(c->n_el), VBS, 0, c->stream>>>(v, c->n_el, c->nm, d->scal() + DS_MEAN,
+                                                               (double)c->n_el * d->nranks);
+  LAUNCH_CHECK(c);
+  return WB_OK;
+}
+// x = P PCG(K_side, P b), the O9 recurrence with the scalars on the device, exactly iters iterations
+wb_status dd_pcg(wb_ctx* c, int side, const double* b, double* x, int iters) {
+  DD* d = c->dd;
+  const int64_t n = c->n_p;
+  const unsigned nb = stream_blocks(n);
+  double* sc = d->scal();
+  CUDA_TRY(c, cudaMemcpyAsync(d->r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  wb_status s = dd_project(c, d->r);
+  if (s) return s;
+  CUDA_TRY(c, cudaMemsetAsync(d->x, 0, sizeof(double) * n, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(sc, 0, sizeof(double) * 4, c->stream));
+  k_mul<<<nb, VBS, 0, c->stream>>>(d->z, d->r, d->mK[side], n);
+  LAUNCH_CHECK(c);
+  CUDA_TRY(c, cudaMemcpyAsync(d->p, d->z, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  if ((s = dd_dot(c, d->r, d->z, DS_RZ))) return s;
+  for (int it = 0; it < iters; ++it) {
+    if ((s = dd_K(c, side, d->p, d->q))) return s;
+    if ((s = dd_dot(c, d->p, d->q, DS_PQ))) return s;
+    k_mgcg_xr<<<nb, VBS, 0, c->stream>>>(d->x, d->r, d->p, d->q, n, sc);
+    LAUNCH_CHECK(c);
+    k_mul<<<nb, VBS, 0, c->stream>>>(d->z, d->r, d->mK[side], n);
+    LAUNCH_CHECK(c);
+    if ((s = dd_dot(c, d->r, d->z, DS_RZ1))) return s;
+    k_mgcg_p<<<nb, VBS, 0, c->stream>>>(d->p, d->z, n, sc, c->counter + 3);
+    LAUNCH_CHECK(c);
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(x, d->x, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  return dd_project(c, x);
+}
+// O10 on the slab: z = P PCG(K_l) P B C_w^-1 A D_w^-1 B^T P PCG(K_r) P r
+wb_status dd_wbfbt(wb_ctx* c, const double* r, double* z, int iters) {
+  DD* d = c->dd;
+  wb_status s = dd_pcg(c, 1, r, d->y, iters);
+  if (s) return s;
+  if ((s = dd_BT(c, d->y, c->Dinv, c->tw))) return s;
+  if ((s = dd_A(c, c->tw, c->tv, true))) return s;
+  if ((s = dd_B(c, c->tv, c->Cinv, d->y))) return s;
+  return dd_pcg(c, 0, d->y, z, iters);
+}
+void dd_free(wb_ctx* c) {
+  DD* d = c->dd;
+  if (!d) return;
+  for (double** b : {&d->own_scal, &d->gm, &d->vs, &d->r, &d->z, &d->p, &d->q, &d->x, &d->y, &d->mK[0], &d->mK[1]})
+    if (*b) cudaFree(*b);
+  delete d;
+  c->dd = nullptr;
+}
+
+wb_status check_ctx(wb_ctx* c, bool need_visc, bool dd_ok = false) {
   if (!c) return WB_EINVAL;
+  if (c->dd && !dd_ok) return set_err(c, WB_ESTATE, "this call is not available on a slab context (wbfbt.h, z-slab)");
+  if (c->dd && c->dd->nranks > 1 && !c->dd->have_comm)
+    return set_err(c, WB_ESTATE, "slab context without a communicator: wb_slab_set_comm first");
   if (need_visc && !c->have_visc) return set_err(c, WB_ESTATE, "wb_set_viscosity has not been called");
   return WB_OK;
 }
 
 void free_all(wb_ctx* c) {
   mg_free(c);
+  dd_free(c);
   double** bufs[] = {&c->dKd, &c->mKd, &c->dv, &c->gp_r, &c->gp_z, &c->gp_p, &c->gp_q, &c->gp_x, &c->gp_y,
                      &c->gp_s, &c->mpinv, &c->mut, &c->Cw, &c->Dw, &c->Cinv, &c->Dinv, &c->dKl, &c->dKr, &c->MinvL, &c->MinvR,
                      &c->E, &c->tv, &c->tw, &c->px, &c->pr, &c->pp, &c->pp1, &c->pq, &c->pz, &c->s0, &c->s1, &c->s2,
@@ -1624,6 +1813,44 @@ wb_status wb_create(wb_ctx** out, int N, int k, unsigned flags, void* stream) {
   return WB_OK;
 }
 
+wb_status wb_slab_create(wb_ctx** out, int N, int k, int rank, int nranks, unsigned flags, void* stream) {
+  if (!out) return WB_EINVAL;
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks || (flags & WB_DEBUG_NOMASK)) return WB_EINVAL;
+  wb_ctx* c = nullptr;
+  wb_status s = wb_create(&c, N, k, flags, stream);
+  if (s) return s;
+  DD* d = new (std::nothrow) DD();
+  if (!d) { wb_destroy(c); return WB_ENOMEM; }
+  c->dd = d;
+  d->rank = rank; d->nranks = nranks;
+  c->G.zopen = (rank > 0 ? 1 : 0) | (rank < nranks - 1 ? 2 : 0);
+  bool ok = lazy_alloc(&d->gm, c->n_nodes) && lazy_alloc(&d->vs, c->n_v) && lazy_alloc(&d->own_scal, 8);
+  for (double** b : {&d->r, &d->z, &d->p, &d->q, &d->x, &d->y, &d->mK[0], &d->mK[1]}) ok = ok && lazy_alloc(b, c->n_p);
+  if (!ok) { wb_destroy(c); return WB_ENOMEM; }
+  k_dd_mask<<<nblk(c->n_nodes, 256), 256, 0, c->stream>>>(d->gm, c->G);
+  if (cudaGetLastError() != cudaSuccess || cudaMemsetAsync(d->own_scal, 0, sizeof(double) * 8, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    wb_destroy(c);
+    return WB_ECUDA;
+  }
+  *out = c;
+  return WB_OK;
+}
+
+wb_status wb_slab_set_comm(wb_ctx* c, const wb_slab_comm* comm) {
+  if (!c || !comm) return WB_EINVAL;
+  if (!c->dd) return set_err(c, WB_ESTATE, "not a slab context (wb_slab_create)");
+  const int64_t np = (int64_t)c->G.nn1 * c->G.nn1;
+  if (!comm->exchange || !comm->allreduce || !comm->send_lo || !comm->recv_lo || !comm->send_hi || !comm->recv_hi ||
+      !comm->scal || comm->cap < 3 * np)
+    return set_err(c, WB_EINVAL, "slab communicator: null callback / buffer, or cap < 3 (kN+1)^2");
+  c->dd->comm = *comm;
+  c->dd->have_comm = true;
+  c->have_visc = false;  // the lumped masses depend on the neighbours: wb_set_viscosity again
+  return WB_OK;
+}
+
 void wb_destroy(wb_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->stream);
@@ -1663,6 +1890,11 @@ wb_status wb_get_dofmap(wb_ctx* c, int64_t* map) {
 
 wb_status wb_get_boundary_mask(wb_ctx* c, uint8_t* mask) {
   if (!c || !mask) return WB_EINVAL;
+  if (c->dd) {
+    k_dd_bmask<<<nblk(c->n_nodes, 256), 256, 0, c->stream>>>(mask, c->dd->gm, c->n_nodes);
+    LAUNCH_CHECK(c);
+    return WB_OK;
+  }
   k_bmask<<<nblk(c->n_nodes, 256), 256, 0, c->stream>>>(mask, c->G);
   LAUNCH_CHECK(c);
   return WB_OK;
@@ -1734,6 +1966,10 @@ static wb_status setup_t(wb_ctx* c, const double* mu, double a_l, double a_r) {
                                                                  c->icount + 1, c->G);
   }
   LAUNCH_CHECK(c);
+  if (c->dd) {  // slab: C_w, D_w summed over the shared planes, inverses under the global mask
+    wb_status sd = dd_finish_lump(c);
+    if (sd) return sd;
+  }
   return finish_lumped<K>(c);
 }
 
@@ -1767,6 +2003,10 @@ static wb_status finish_lumped(wb_ctx* c) {
     double* dmax = c->scal + S_DMAX + side;
     k_absmax<VBS><<<c->red_blocks, VBS, 0, c->stream>>>(d, c->n_p, c->partial, c->counter, dmax);
     LAUNCH_CHECK(c);
+    if (c->dd) {
+      wb_status sd = dd_after_dmax(c, side, d, dmax);
+      if (sd) return sd;
+    }
     if (c->nm == 4)
       k_minv_t<<<stream_blocks(c->n_p / 4), VBS, 0, c->stream>>>(d, side == 0 ? c->MinvL : c->MinvR, dmax, c->pl,
                                                                  c->N);
@@ -2045,6 +2285,8 @@ extern "C" {
 
 wb_status wb_set_viscosity(wb_ctx* c, const double* mu_q, double a_l, double a_r) {
   if (!c || !mu_q) return WB_EINVAL;
+  if (c->dd && c->dd->nranks > 1 && !c->dd->have_comm)
+    return set_err(c, WB_ESTATE, "slab context without a communicator: wb_slab_set_comm first");
   if (!(a_l >= 1.0) || !(a_r >= 1.0) || !std::isfinite(a_l) || !std::isfinite(a_r))
     return set_err(c, WB_EINVAL, "a_l, a_r must be finite and >= 1");
   switch (c->k) {
@@ -2055,42 +2297,47 @@ wb_status wb_set_viscosity(wb_ctx* c, const double* mu_q, double a_l, double a_r
 }
 
 wb_status wb_apply_A(wb_ctx* c, const double* u, double* y) {
-  wb_status s = check_ctx(c, true);
+  wb_status s = check_ctx(c, true, true);
   if (s) return s;
   if (!u || !y) return set_err(c, WB_EINVAL, "null pointer");
   if (overlaps(u, 8 * c->n_v, y, 8 * c->n_v)) return set_err(c, WB_EALIAS, "u and y overlap");
+  if (c->dd) return dd_A(c, u, y, false);
   return run_A(c, u, y, (c->flags & WB_DEBUG_NOMASK) ? 1 : 0);
 }
 
 wb_status wb_apply_B(wb_ctx* c, const double* u, double* p) {
-  wb_status s = check_ctx(c, false);
+  wb_status s = check_ctx(c, false, true);
   if (s) return s;
   if (!u || !p) return set_err(c, WB_EINVAL, "null pointer");
   if (overlaps(u, 8 * c->n_v, p, 8 * c->n_p)) return set_err(c, WB_EALIAS, "u and p overlap");
+  if (c->dd) return dd_B(c, u, nullptr, p);
   return run_B(c, u, nullptr, p, (c->flags & WB_DEBUG_NOMASK) ? 1 : 0, nullptr, nullptr, nullptr, c->nm, 1);
 }
 
 wb_status wb_apply_BT(wb_ctx* c, const double* p, double* y) {
-  wb_status s = check_ctx(c, false);
+  wb_status s = check_ctx(c, false, true);
   if (s) return s;
   if (!p || !y) return set_err(c, WB_EINVAL, "null pointer");
   if (overlaps(p, 8 * c->n_p, y, 8 * c->n_v)) return set_err(c, WB_EALIAS, "p and y overlap");
+  if (c->dd) return dd_BT(c, p, nullptr, y);
   return run_BT(c, p, nullptr, y, (c->flags & WB_DEBUG_NOMASK) ? 1 : 0, nullptr, c->nm, 1);
 }
 
 wb_status wb_apply_K(wb_ctx* c, int side, const double* p, double* q) {
-  wb_status s = check_ctx(c, true);
+  wb_status s = check_ctx(c, true, true);
   if (s) return s;
   if (!p || !q || (side != 0 && side != 1)) return set_err(c, WB_EINVAL, "bad argument");
   if (overlaps(p, 8 * c->n_p, q, 8 * c->n_p)) return set_err(c, WB_EALIAS, "p and q overlap");
+  if (c->dd) return dd_K(c, side, p, q);
   return run_K(c, side, p, q);
 }
 
 wb_status wb_poisson_pcg(wb_ctx* c, int side, const double* b, double* x, int iters) {
-  wb_status s = check_ctx(c, true);
+  wb_status s = check_ctx(c, true, true);
   if (s) return s;
   if (!b || !x || (side != 0 && side != 1) || iters < 0) return set_err(c, WB_EINVAL, "bad argument");
   if (overlaps(b, 8 * c->n_p, x, 8 * c->n_p)) return set_err(c, WB_EALIAS, "b and x overlap");
+  if (c->dd) return dd_pcg(c, side, b, x, iters);
   return run_poisson(c, side, b, x, iters);
 }
 
@@ -2153,6 +2400,7 @@ wb_status wb_stokes_fgmres(wb_ctx* c, const double* f, const double* g, double* 
 
 wb_status wb_set_inner_cheb(wb_ctx* c, double lmin_l, double lmax_l, double lmin_r, double lmax_r) {
   if (!c) return WB_EINVAL;
+  if (c->dd) return check_ctx(c, false);
   if (lmin_l == 0.0 && lmax_l == 0.0 && lmin_r == 0.0 && lmax_r == 0.0) {
     c->inner = 0;
     return WB_OK;
@@ -2168,6 +2416,7 @@ wb_status wb_set_inner_cheb(wb_ctx* c, double lmin_l, double lmax_l, double lmin
 
 wb_status wb_set_schur(wb_ctx* c, int kind) {
   if (!c) return WB_EINVAL;
+  if (c->dd) return check_ctx(c, false);
   if (kind < 0 || kind > 2) return set_err(c, WB_EINVAL, "kind must be 0 (wBFBT), 1 (diag(A)-BFBT) or 2 (M_p)");
   c->schur = kind;
   return WB_OK;
@@ -2193,6 +2442,7 @@ wb_status wb_apply_mpinv(wb_ctx* c, const double* r, double* z) {
 
 wb_status wb_load_vector(wb_ctx* c, const double* fq, double* F) {
   if (!c || !fq || !F) return c ? set_err(c, WB_EINVAL, "null pointer") : WB_EINVAL;
+  if (c->dd) return check_ctx(c, false);
   if (overlaps(fq, sizeof(double) * 3 * c->n_el * c->nq, F, sizeof(double) * c->n_v))
     return set_err(c, WB_EALIAS, "fq and F overlap");
   const unsigned nb = nblk(c->n_nodes, 128);
@@ -2225,6 +2475,7 @@ wb_status wb_velocity_vcycle(wb_ctx* c, const double* b, double* x) {
 
 wb_status wb_set_velocity_mg(wb_ctx* c, int cycles) {
   if (!c) return WB_EINVAL;
+  if (c->dd) return check_ctx(c, false);
   if (cycles < 0) return set_err(c, WB_EINVAL, "cycles must be >= 0");
   if (cycles > 0 && !(c->mg && c->mg->vel)) return set_err(c, WB_ESTATE, "no velocity multigrid (wb_setup_mg with mu)");
   if (c->mg) c->mg->vcycles = cycles;
@@ -2253,6 +2504,7 @@ wb_status wb_poisson_mgcg(wb_ctx* c, int side, const double* b, double* x, int i
 
 wb_status wb_set_inner_mg(wb_ctx* c, int iters) {
   if (!c) return WB_EINVAL;
+  if (c->dd) return check_ctx(c, false);
   if (iters < 0) return set_err(c, WB_EINVAL, "iters must be >= 0");
   if (iters > 0 && !c->mg) return set_err(c, WB_ESTATE, "no multigrid hierarchy (wb_setup_mg)");
   if (c->mg) c->mg->inner_iters = iters;
@@ -2261,6 +2513,7 @@ wb_status wb_set_inner_mg(wb_ctx* c, int iters) {
 
 wb_status wb_mg_get_lumped(wb_ctx* c, int level, double* Cw, double* Dw) {
   if (!c) return WB_EINVAL;
+  if (c->dd) return check_ctx(c, false);
   if (!c->mg) return set_err(c, WB_ESTATE, "no multigrid hierarchy (wb_setup_mg)");
   if (level < 0 || level >= c->mg->nl) return set_err(c, WB_EINVAL, "bad level");
   wb_ctx* L = c->mg->lev[level];
@@ -2272,10 +2525,11 @@ wb_status wb_mg_get_lumped(wb_ctx* c, int level, double* Cw, double* Dw) {
 }
 
 wb_status wb_apply_wbfbt(wb_ctx* c, const double* r, double* z, int iters) {
-  wb_status s = check_ctx(c, true);
+  wb_status s = check_ctx(c, true, true);
   if (s) return s;
   if (!r || !z || iters < 0) return set_err(c, WB_EINVAL, "bad argument");
   if (overlaps(r, 8 * c->n_p, z, 8 * c->n_p)) return set_err(c, WB_EALIAS, "r and z overlap");
+  if (c->dd) return dd_wbfbt(c, r, z, iters);
   return run_wbfbt(c, r, z, iters);
 }
 
@@ -2298,6 +2552,7 @@ static wb_status hotpath_host_body(wb_ctx* c, double* dmu, double a_l, double a_
 wb_status wb_hotpath_host(wb_ctx* c, const double* mu_q, double a_l, double a_r, const double* u, const double* p,
                           int iters, double* yA, double* pB, double* yBT, double* z) {
   if (!c || !mu_q || !u || !p || !yA || !pB || !yBT || !z) return WB_EINVAL;
+  if (c->dd) return check_ctx(c, false);
   // validate everything that can be checked on the host before any copy is issued
   if (iters < 0) return set_err(c, WB_EINVAL, "iters must be >= 0");
   if (!(a_l >= 1.0) || !(a_r >= 1.0) || !std::isfinite(a_l) || !std::isfinite(a_r))
@@ -2421,7 +2676,7 @@ wb_status wb_debug_pcg_step(wb_ctx* c, int side, double* x, double* r, double* p
 }
 
 wb_status wb_get_lumped(wb_ctx* c, double* Cw, double* Dw, double* Cinv, double* Dinv) {
-  wb_status s = check_ctx(c, true);
+  wb_status s = check_ctx(c, true, true);
   if (s) return s;
   const size_t b = sizeof(double) * c->n_nodes;
   if (Cw) CUDA_TRY(c, cudaMemcpyAsync(Cw, c->Cw, b, cudaMemcpyDeviceToDevice, c->stream));
@@ -2432,7 +2687,7 @@ wb_status wb_get_lumped(wb_ctx* c, double* Cw, double* Dw, double* Cinv, double*
 }
 
 wb_status wb_get_jacobi(wb_ctx* c, double* dKl, double* dKr) {
-  wb_status s = check_ctx(c, true);
+  wb_status s = check_ctx(c, true, true);
   if (s) return s;
   const size_t b = sizeof(double) * c->n_p;
   if (dKl) CUDA_TRY(c, cudaMemcpyAsync(dKl, c->dKl, b, cudaMemcpyDeviceToDevice, c->stream));
