@@ -457,6 +457,19 @@ def run_ours(args):
         ctx4.close()
         del mu4, u4, p4, y4, q4, z4
 
+    # ---- the slab code path on this one GPU (one rank, no communication): the
+    # cost of its unfused K_w (B^T, plane sum, B) and launch-by-launch PCG against the fused path
+    from paper_1607_03936_b200 import SlabContext, ThreadComm
+    sctx = SlabContext(cfg.N, cfg.k, ThreadComm.group(1, SlabContext.plane_cap(cfg.N, cfg.k), "cuda")[0],
+                       stream=stream.cuda_stream)
+    sctx.set_viscosity(mu)
+    tWs = timed(lambda: sctx.apply_wbfbt(p, z, iters), reps=3)
+    tKs = timed(lambda: sctx.apply_K(1, p, qv), reps=10)
+    slab = {"wbfbt_ms": tWs, "wbfbt_applies_per_s": 1e3 / tWs, "K_ms_cold": tKs, "ranks": 1,
+            "note": "z-slab decomposition code path with one rank (not in the step): unfused K_w and a "
+                    "launch-by-launch device-scalar PCG; multi-rank runs: bench.py --slab under torchrun"}
+    sctx.close()
+
     # ---- end to end through the host entry (pinned buffers)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
     hmu, hu, hp = pin(inp["mu_q"]), pin(inp["u"]), pin(inp["p"])
@@ -512,13 +525,76 @@ def run_ours(args):
                     "stokes_fgmres": {"iter_ms": stokes_iter_ms, "relres_after": {str(k): v for k, v in rr_st.items()},
                                       "note": "R19 (not in the step): FGMRES on [A B^T; B 0], f = u, g = 0; per "
                                               "iteration wBFBT (2 x iters PCG) + 6 smoother steps"},
-                    "C4": c4},
+                    "C4": c4, "slab": slab},
                 "roofline": roof,
                 "e2e": {"value": e2e, "unit": unit_of(cfg), "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h},
                 "gpu_launches": launches,
                 "clocks": clk.summary(),
                 "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+# ---------------------------------------------------------------------- slab decomposition (opt-in)
+def run_slab(args):
+    """--slab: ONE global problem on the box N x N x (R N), R = world size, rank r owning the
+    r-th cube.  The step is the same hot-path call on a
+    slab context; its shared-plane sums and scalar all-reduces go through torch.distributed
+    (NCCL).  Strong coupling per PCG iteration, so this is the communication-bound mode the
+    survey predicts; the default (replicas) stays the headline."""
+    import torch
+
+    import synth
+    from paper_1607_03936_b200 import DistComm, SlabContext, ThreadComm
+
+    rank, world, local = dist_init(args.gpus)
+    cfg = synth.CONFIGS[args.config]
+    inp = synth.make_inputs(cfg, seed=replica_seed(rank))  # rank r's cube of the global viscosity
+    stream = torch.cuda.current_stream()
+    cap = SlabContext.plane_cap(cfg.N, cfg.k)
+    comm = DistComm(cap, "cuda") if world > 1 else ThreadComm.group(1, cap, "cuda")[0]
+    ctx = SlabContext(cfg.N, cfg.k, comm, stream=stream.cuda_stream)
+    d = lambda a: torch.as_tensor(a, dtype=torch.float64, device="cuda")  # noqa: E731
+    mu, u, p = d(inp["mu_q"]), d(inp["u"]), d(inp["p"])
+    f64 = dict(dtype=torch.float64, device="cuda")
+    yA, pB, yBT, z = (torch.empty(n, **f64) for n in (ctx.n_v, ctx.n_p, ctx.n_v, ctx.n_p))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    iters = cfg.iters
+    for _ in range(args.warmup):
+        ctx.hotpath(mu, u, p, iters, yA, pB, yBT, z)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    l0, x0, a0 = ctx.query("kernel_launches"), comm.n_exchange, comm.n_allreduce
+    barrier(world)
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            ctx.hotpath(mu, u, p, iters, yA, pB, yBT, z)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    t_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev), world)
+    if rank == 0:
+        n_v_glob = 3 * (cfg.k * cfg.N + 1) ** 2 * (cfg.k * cfg.N * world + 1)
+        line = {"metric": METRIC, "value": args.steps / (t_ms * 1e-3),
+                "unit": f"global hot-path steps/s on the {cfg.N}x{cfg.N}x{cfg.N * world} box "
+                        f"(setup + A + B + B^T + wBFBT 2x{iters} PCG), slab-decomposed",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": workload_of(cfg) + f", z-stacked x{world}", "N": cfg.N, "k": cfg.k,
+                           "l2": "flushed (256 MiB memset) before every timed step",
+                           "parallelism": f"slab{world}", "n_v_global": n_v_glob},
+                "gpu_launches": int(ctx.query("kernel_launches") - l0),
+                "comm": {"plane_exchanges_per_step": (comm.n_exchange - x0) / args.steps,
+                         "allreduces_per_step": (comm.n_allreduce - a0) / args.steps,
+                         "plane_bytes": 8 * cap, "backend": "nccl" if world > 1 else "none"},
+                "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -536,9 +612,12 @@ def main():
     ap.add_argument("--comp-reps", type=int, default=30)  # median of >= 30 reps
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c4", action="store_true")  # skip the high-order C4 component block
+    ap.add_argument("--slab", action="store_true")  # one global z-slab-decomposed problem instead of replicas
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.slab:
+        return run_slab(args)
     return run_ours(args)
 
 

@@ -4,7 +4,7 @@
 // A slab context is a cube context whose z-lo / z-hi faces may be shared with a neighbouring
 // rank (Geo::zopen).  The operators run the cube kernels WITHOUT their built-in Dirichlet mask
 // (nomask, or a nodal scaling xs), the shared planes' partial sums are exchanged and added
-// (k_dd_add), and the GLOBAL mask gm is applied here.  Both owners of a shared plane compute
+// (k_dd_unpack_add), and the GLOBAL mask gm is applied here.  Both owners of a shared plane compute
 // own + received: the two-term sum commutes, so their copies agree bit for bit.
 #pragma once
 #include "kernels.cuh"
@@ -30,10 +30,32 @@ __global__ void k_dd_bmask(uint8_t* __restrict__ mask, const double* __restrict_
   mask[g] = b; mask[n_nodes + g] = b; mask[2 * n_nodes + g] = b;
 }
 
-// v[i] += recv[i] on one shared plane (n = fields x plane nodes are handled per field by the host)
-__global__ void k_dd_add(double* __restrict__ v, const double* __restrict__ recv, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    v[i] += recv[i];
+// The shared planes of up to 3 nodal fields (n_nodes each; plane z = 0 is the first np entries,
+// plane z = kN the last np) in one launch: pack into the send buffers, or add the received
+// partials.  zopen bit 0 / 1 selects the lo / hi plane.
+struct DDFields {
+  double* f[3];
+  int nf;
+};
+__global__ void k_dd_pack(DDFields F, double* __restrict__ send_lo, double* __restrict__ send_hi, int64_t np,
+                          int64_t n_nodes, int zopen) {
+  const int64_t n = np * F.nf;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i / np);
+    const int64_t j = i - k * np;
+    if (zopen & 1) send_lo[i] = F.f[k][j];
+    if (zopen & 2) send_hi[i] = F.f[k][n_nodes - np + j];
+  }
+}
+__global__ void k_dd_unpack_add(DDFields F, const double* __restrict__ recv_lo, const double* __restrict__ recv_hi,
+                                int64_t np, int64_t n_nodes, int zopen) {
+  const int64_t n = np * F.nf;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i / np);
+    const int64_t j = i - k * np;
+    if (zopen & 1) F.f[k][j] += recv_lo[i];
+    if (zopen & 2) F.f[k][n_nodes - np + j] += recv_hi[i];
+  }
 }
 
 // Cinv = gm / C_w, Dinv = gm / D_w from the plane-summed lumped masses (row a3 with the global

@@ -1449,28 +1449,18 @@ wb_status dd_allreduce(wb_ctx* c, int offset, int n, int op) {
 wb_status dd_plane_sum(wb_ctx* c, double* const* f, int nf) {
   DD* d = c->dd;
   if (d->nranks == 1) return WB_OK;
+  if (nf > 3) return set_err(c, WB_EINVAL, "at most 3 fields per plane sum");
   const int64_t np = (int64_t)c->G.nn1 * c->G.nn1, n = np * nf;
   if (n > d->comm.cap) return set_err(c, WB_EINVAL, "slab exchange buffers too small");
   const int zo = c->G.zopen;
-  for (int i = 0; i < nf; ++i) {
-    if (zo & 1)
-      CUDA_TRY(c, cudaMemcpyAsync(d->comm.send_lo + i * np, f[i], sizeof(double) * np, cudaMemcpyDeviceToDevice,
-                                  c->stream));
-    if (zo & 2)
-      CUDA_TRY(c, cudaMemcpyAsync(d->comm.send_hi + i * np, f[i] + c->n_nodes - np, sizeof(double) * np,
-                                  cudaMemcpyDeviceToDevice, c->stream));
-  }
+  DDFields F{};
+  F.nf = nf;
+  for (int i = 0; i < nf; ++i) F.f[i] = f[i];
+  k_dd_pack<<<stream_blocks(n), VBS, 0, c->stream>>>(F, d->comm.send_lo, d->comm.send_hi, np, c->n_nodes, zo);
+  LAUNCH_CHECK(c);
   if (d->comm.exchange(d->comm.user, n) != 0) return set_err(c, WB_ECUDA, "slab communicator: exchange failed");
-  for (int i = 0; i < nf; ++i) {
-    if (zo & 1) {
-      k_dd_add<<<stream_blocks(np), VBS, 0, c->stream>>>(f[i], d->comm.recv_lo + i * np, np);
-      LAUNCH_CHECK(c);
-    }
-    if (zo & 2) {
-      k_dd_add<<<stream_blocks(np), VBS, 0, c->stream>>>(f[i] + c->n_nodes - np, d->comm.recv_hi + i * np, np);
-      LAUNCH_CHECK(c);
-    }
-  }
+  k_dd_unpack_add<<<stream_blocks(n), VBS, 0, c->stream>>>(F, d->comm.recv_lo, d->comm.recv_hi, np, c->n_nodes, zo);
+  LAUNCH_CHECK(c);
   return WB_OK;
 }
 wb_status dd_plane_sum3(wb_ctx* c, double* v) {

@@ -20,7 +20,7 @@ from tests.gpu_common import dev, empty, host, rel_l2
 pytestmark = pytest.mark.gpu
 
 # (N, k, R): even (TMA-capable) and odd cubes, k = 2 and 4, 1..3 ranks; (16, 2, 2) spans several
-# kernel tiles per rank, (48, 2, 2) runs the z-marching B / B^T kernels of the large meshes
+# kernel tiles per rank; the C5-size case is test_full_size_C5_per_rank_two_ranks below
 CASES = [(4, 2, 1), (4, 2, 2), (5, 2, 2), (6, 2, 3), (16, 2, 2), (13, 2, 3), (3, 4, 2), (8, 4, 2), (6, 3, 2)]
 
 
@@ -218,9 +218,11 @@ def test_hotpath_and_refusals(case):
         assert case.comms[0].n_exchange > 0 and case.comms[0].n_allreduce > 0
 
 
-def test_large_mesh_kernels_two_ranks():
-    """N = 48 per rank: the z-marching B / B^T kernels and the tile A kernel of the C5-size path."""
-    c = SlabCase(48, 2, 2, cfg="C5")
+def test_full_size_C5_per_rank_two_ranks():
+    """BASELINE.json's C5 size on every rank (64^3 per rank, the 64 x 64 x 128 box; the z-marching
+    B / B^T kernels and the tile A kernel of the large meshes): A, K_w and a 5-iteration PCG prefix
+    against the oracle on the whole box."""
+    c = SlabCase(64, 2, 2, cfg="C5")
     try:
         us = [dev(c.loc_v(c.u, r)) for r in range(2)]
         ps = [dev(c.loc_p(c.p, r)) for r in range(2)]
