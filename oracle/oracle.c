@@ -25,7 +25,9 @@
  *   eq:bdramp          PAPER.md:2219-2251 boundary amplification a_l, a_r on elements touching the boundary
  *   K_w (Neumann)
  *   mu at quad points
- * Readings of silences (R1..R14) are listed in DESIGN.md Sec. 3; the ones used
+ *   element partition  PAPER.md:2480-2487 the box mesh N x N x Nz (or_create_box) is the global
+ *                      mesh of the z-slab decomposition (R24); pinned in tests/test_oracle_box.py
+ * Readings of silences (R1..R24) are listed in DESIGN.md Sec. 3; the ones used
  * here are cited inline.
  *
  * Parity pins: every function below is pinned by tests/test_oracle_*.py
