@@ -436,12 +436,22 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
   if (tl) g_ktl[blockIdx.x][1] = gtimer();
 #endif
   double dot = 0.0;
+  // tile coordinates without divisions in the loop (the runtime div / mod chains ran on every
+  // warp at the top of each tile with nothing to overlap them): the stride gridDim.x is
+  // decomposed once, then each step adds it with carries
+  int sx, sy, sz, nx0, ny0, nz0;
+  coords(gridDim.x, sx, sy, sz);  // = (TX tx, TY ty, TZ tz) of the stride
+  coords(tile, nx0, ny0, nz0);
+  const int LX = TX * NTX, LY = TY * NTY;
   for (int k = 0; tile < n_tiles; ++k, tile += gridDim.x) {
     const unsigned ph = k & 1;
     const int next = tile + gridDim.x;
-    int ex0, ey0, ez0, nx0 = 0, ny0 = 0, nz0 = 0;
-    coords(tile, ex0, ey0, ez0);
-    if (next < n_tiles) coords(next, nx0, ny0, nz0);
+    const int ex0 = nx0, ey0 = ny0, ez0 = nz0;
+    nx0 += sx;
+    if (nx0 >= LX) { nx0 -= LX; ny0 += TY; }
+    ny0 += sy;
+    if (ny0 >= LY) { ny0 -= LY; nz0 += TZ; }
+    nz0 += sz;
     // 0. p = Minv r (+ beta p_old) from the raw boxes into Ps (the element step stores the
     // tile's own p_new)
     mbar_wait(&bar[0], ph);
