@@ -292,6 +292,18 @@ __device__ __forceinline__ A2Tile a2_tile_of(int tile, const Geo& G) {
   t.inner = t.bx > 0 && t.by > 0 && t.bz > 0 && t.bx + 2 * TX < e && t.by + 2 * TY < e && t.bz + 2 * TZ < e;
   return t;
 }
+// the same from a 3-D grid (NTX, NTY, NTZ): no runtime div / mod (tile = tx + NTX (ty + NTY tz), the
+// linear launch order of the 1-D form)
+template <int TX, int TY, int TZ>
+__device__ __forceinline__ A2Tile a2_tile_of_grid(const Geo& G) {
+  A2Tile t;
+  t.tx = blockIdx.x; t.ty = blockIdx.y; t.tz = blockIdx.z;
+  t.tile = t.tx + gridDim.x * (t.ty + gridDim.y * t.tz);
+  t.bx = 2 * TX * t.tx; t.by = 2 * TY * t.ty; t.bz = 2 * TZ * t.tz;
+  const int e = G.nn1 - 1;
+  t.inner = t.bx > 0 && t.by > 0 && t.bz > 0 && t.bx + 2 * TX < e && t.by + 2 * TY < e && t.bz + 2 * TZ < e;
+  return t;
+}
 
 // Stage NC nodal components (component stride cs) of a tile's (2TX+1)(2TY+1)(2TZ+1)
 // node box into Us[cc][nz][ny][col] by cp.async (no wait); nodes outside the mesh,
@@ -375,11 +387,11 @@ __global__ void __launch_bounds__(3 * TX * TY * TZ, MINB)
   double* X = smem_a2;  // [XS]: gradient exchange, then element slots R[c][a][le]
   double* Mu = smem_a2 + T::XS;
   double* Us = Mu + 27 * NE;
-  const int tile = blockIdx.x;
 #ifdef WB_KPROF
   long long a_tc = clock64();
 #endif
-  const A2Tile t = a2_tile_of<TX, TY, TZ>(tile, G);
+  const A2Tile t = a2_tile_of_grid<TX, TY, TZ>(G);  // launched on the (NTX, NTY, NTZ) grid
+  const int tile = t.tile;
   a2_stage<TX, TY, TZ>(mutT, u, Mu, Us, t, G, nomask);
   A_LAP(0);
   const int le = threadIdx.x % NE, c = threadIdx.x / NE;

@@ -723,7 +723,8 @@ wb_status configure_kernels(wb_ctx* c) {
 
 wb_status run_A(wb_ctx* c, const double* u, double* y, int nomask) {
   if (c->k == 2) {
-    k_A_tile<A_TX, A_TY, A_TZ, A_MINB><<<c->n_tiles, 3 * A_TX * A_TY * A_TZ, Tile2<A_TX, A_TY, A_TZ>::SMEM,
+    const dim3 tg((c->N + A_TX - 1) / A_TX, (c->N + A_TY - 1) / A_TY, (c->N + A_TZ - 1) / A_TZ);  // = n_tiles
+    k_A_tile<A_TX, A_TY, A_TZ, A_MINB><<<tg, 3 * A_TX * A_TY * A_TZ, Tile2<A_TX, A_TY, A_TZ>::SMEM,
                                          c->stream>>>(c->mut, u, y, c->Fu, c->G, nomask);
     LAUNCH_CHECK(c);
     k_A_skel<A_TX, A_TY, A_TZ><<<nblk(a2_skel_count<A_TX, A_TY, A_TZ>(c->N), 256), 256, 0, c->stream>>>(
