@@ -89,13 +89,25 @@ struct FKT {
 // two 8-byte stores (25 row + 2 s, + 1) of a half-warp 16 distinct bank pairs, since
 // 5 and 9 = 25 mod 16 are odd.  (A row-major walk makes the stores 2-way conflicted.)
 template <int TX, int TY, int TZ, bool ZB>
+__device__ __forceinline__ void fkt_copy_pair_rs(int r, int sp, const double* __restrict__ Pb,
+                                                 const double* __restrict__ Zb, const double* __restrict__ Mb,
+                                                 double* __restrict__ Pd, int mode, double beta);
+template <int TX, int TY, int TZ, bool ZB>
 __device__ __forceinline__ void fkt_copy_pair(int t, const double* __restrict__ Pb, const double* __restrict__ Zb,
                                               const double* __restrict__ Mb, double* __restrict__ Pd, int mode,
                                               double beta) {
   using K = FKT<TX, TY, TZ>;
   static_assert(K::HY == 10 && K::QS % 16 == 9 && (4 * K::HX * K::HZ) % 16 == 0, "pair walk layout");
   const int h = t >> 4;
-  const int r = 16 * (h / 5) + (t & 15), sp = h % 5;
+  fkt_copy_pair_rs<TX, TY, TZ, ZB>(16 * (h / 5) + (t & 15), h % 5, Pb, Zb, Mb, Pd, mode, beta);
+}
+// the same with the item's (row, pair column) given: the tile loop of k_K2_tma steps them
+// incrementally instead of dividing the item index
+template <int TX, int TY, int TZ, bool ZB>
+__device__ __forceinline__ void fkt_copy_pair_rs(int r, int sp, const double* __restrict__ Pb,
+                                                 const double* __restrict__ Zb, const double* __restrict__ Mb,
+                                                 double* __restrict__ Pd, int mode, double beta) {
+  using K = FKT<TX, TY, TZ>;
   const int j2 = 5 * r + sp;
   const double2 pp = reinterpret_cast<const double2*>(Pb)[j2];
   double2 v;
@@ -439,6 +451,7 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
   // tile coordinates without divisions in the loop (the runtime div / mod chains ran on every
   // warp at the top of each tile with nothing to overlap them): the stride gridDim.x is
   // decomposed once, then each step adds it with carries
+  const int cp_q = (threadIdx.x >> 4) / 5, cp_s = (threadIdx.x >> 4) % 5, cp_l = threadIdx.x & 15;  // step-0 item
   int sx, sy, sz, nx0, ny0, nz0;
   coords(gridDim.x, sx, sy, sz);  // = (TX tx, TY ty, TZ tz) of the stride
   coords(tile, nx0, ny0, nz0);
@@ -458,8 +471,18 @@ __global__ void __launch_bounds__(FK2<TX, TY, TZ>::NTH, MINB)
     lap(1);
     // the raw box is [m][hx][hz][hy] = Ps's order with row length HY instead of QS:
     // a flat, lane-consecutive walk
-    for (int t = threadIdx.x; t < ((dbg & 0x400) ? 0 : 2 * K::NB); t += F::NTH)
-      fkt_copy_pair<TX, TY, TZ, ZB>(t, Pb, Zb, Mb, Ps, mode, beta);
+    {
+      // item t = threadIdx.x + i NTH: half-warp h = t / 16 takes pair column h % 5 of rows
+      // 16 (h / 5) + (t % 16); h advances by NTH / 16 per pass
+      constexpr int DH = F::NTH / 16, DQ = DH / 5, DS = DH % 5;
+      static_assert(F::NTH % 16 == 0, "pass stride in whole half-warps");
+      int rq = cp_q, sp = cp_s;
+      for (int t = threadIdx.x; t < ((dbg & 0x400) ? 0 : 2 * K::NB); t += F::NTH) {
+        fkt_copy_pair_rs<TX, TY, TZ, ZB>(16 * rq + cp_l, sp, Pb, Zb, Mb, Ps, mode, beta);
+        sp += DS; rq += DQ;
+        if (sp >= 5) { sp -= 5; ++rq; }
+      }
+    }
     __syncthreads();
     lap(2);
     if (threadIdx.x == K::TMA_T && next < n_tiles) {  // raw p, r, Minv buffers are free
