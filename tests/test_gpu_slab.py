@@ -257,3 +257,44 @@ def test_one_rank_slab_equals_cube_context():
     p = dev(inp["p"])
     za, zb = host(a.apply_wbfbt(p, empty(a.n_p), 5)), host(b.apply_wbfbt(p, empty(b.n_p), 5))
     assert rel_l2(zb, za) <= 1e-10
+
+
+def test_slab_argument_and_callback_errors():
+    """Boundary behaviour of the slab entry points (wbfbt.h "z-slab")."""
+    import ctypes as C
+    from paper_1607_03936_b200 import Context, SlabContext, ThreadComm, WBError, WB_DEBUG_NOMASK, lib
+    L = lib()
+    h = C.c_void_p()
+    for N, k, rank, R, flags in [(4, 2, 2, 2, 0), (4, 2, -1, 2, 0), (4, 2, 0, 0, 0), (4, 2, 0, 2, WB_DEBUG_NOMASK),
+                                 (0, 2, 0, 2, 0), (4, 5, 0, 2, 0)]:
+        assert L.wb_slab_create(C.byref(h), N, k, rank, R, flags, None) == -1 and not h.value
+    # buffers too small for the planes
+    with pytest.raises(ValueError):
+        SlabContext(8, 2, ThreadComm.group(1, 10, "cuda")[0])
+    # not a slab context / null communicator
+    ctx = Context(4, 2)
+    assert L.wb_slab_set_comm(ctx._h, None) == -1
+    comms = ThreadComm.group(2, SlabContext.plane_cap(4, 2), "cuda")
+    s0 = SlabContext(4, 2, comms[0])
+    assert L.wb_slab_set_comm(ctx._h, C.byref(s0._cs)) == -7
+    # a multi-rank slab context refuses work before its communicator is registered
+    raw = C.c_void_p()
+    assert L.wb_slab_create(C.byref(raw), 4, 2, 0, 2, 0, None) == 0
+    mu = dev(synth.make_inputs("C1", 0)["mu_q"])
+    assert L.wb_set_viscosity(raw, C.c_void_p(mu.data_ptr()), 1.0, 1.0) == -7
+    L.wb_destroy(raw)
+
+    # a failing callback surfaces as an error with the Python exception attached
+    class Bad(ThreadComm):
+        def exchange(self, n):
+            raise RuntimeError("link down")
+
+        def allreduce(self, offset, n, op):
+            raise RuntimeError("link down")
+    shared = {"comms": [None, None], "barrier": None}
+    bad = SlabContext(4, 2, Bad(0, 2, SlabContext.plane_cap(4, 2), "cuda", shared))
+    with pytest.raises(WBError) as ei:
+        bad.set_viscosity(mu)
+    assert "link down" in str(ei.value)
+    for c in (ctx, s0, bad):
+        c.close()
