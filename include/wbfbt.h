@@ -274,9 +274,12 @@ wb_status wb_hotpath_host(wb_ctx* ctx, const double* mu_q, double a_l, double a_
  * (eq:bdramp) applies to elements on the global boundary only.
  *
  * On a slab context the calls wb_set_viscosity, wb_apply_A, wb_apply_B, wb_apply_BT,
- * wb_apply_K, wb_poisson_pcg, wb_apply_wbfbt, wb_get_lumped, wb_get_jacobi,
- * wb_get_boundary_mask (the global mask), wb_sizes, wb_sync and wb_query compute the GLOBAL
- * operators; each must be entered by all R ranks together (they are collective).  Per
+ * wb_apply_K, wb_poisson_pcg, wb_apply_wbfbt, wb_hotpath (device pointers), wb_get_lumped,
+ * wb_get_jacobi, wb_get_boundary_mask (the global mask), wb_sizes (local sizes), wb_sync and
+ * wb_query compute the GLOBAL operators; the setup, apply and solve calls must be entered by all
+ * R ranks together (they are collective; a rank that fails alone, e.g. WB_ENONPOS_MU, leaves its
+ * neighbours waiting in the exchange, so validate inputs collectively).  "n_nonpos_Cw" /
+ * "n_nonpos_Dw" count this rank's nodes, shared-plane nodes on both of their owners.  Per
  * operator apply there is one exchange: the partial nodal sums on the shared planes
  * (3 (kN+1)^2 doubles per plane; C_w, D_w once per wb_set_viscosity), and every inner product,
  * the projection mean and max|diag K| is one all-reduce of 1 double.  K_w runs unfused
